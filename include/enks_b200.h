@@ -1,0 +1,143 @@
+/*
+ * enks_b200.h — C-ABI of the B200-native matrix-variate EnKS hot path.
+ *
+ * The reference (arXiv 2410.09663, package `enksmpc`) is pure Python/NumPy;
+ * its hot path is enks.smooth_horizon (pkg/src/enksmpc/enks.py:256-284).  This
+ * library replaces the NumPy/BLAS/LAPACK call sites of that path with sm_100a
+ * kernels.  The Python host package `paper_2410_09663_b200` (a drop-in mirror
+ * of the reference API) binds these entry points with ctypes.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no allocation inside the library.  All
+ *     device pointers are caller-owned; `stream` is a cudaStream_t passed as
+ *     void* (NULL = legacy default stream).  Every call is stream-ordered and
+ *     asynchronous unless stated otherwise.
+ *   - Ensemble layout ("member-column"): a block of R rows for N members with
+ *     m columns each is a row-major R x (N*m) fp32 matrix; member i's (r, j)
+ *     entry is at [r * ld + i * m + j].  This is exactly the matrix the
+ *     reference builds by copy in _pair_covariance (enks.py:151-152).
+ *   - Return value: 0 on success, otherwise an ENKS_E_* code; the message is
+ *     available from enks_last_error() (thread-local).
+ */
+#ifndef ENKS_B200_H
+#define ENKS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ENKS_OK 0
+#define ENKS_E_ARG 1       /* bad argument (shape, null pointer, unsupported size) */
+#define ENKS_E_CUDA 2      /* CUDA launch / runtime error */
+#define ENKS_E_UNSUPPORTED 3
+
+/* Library identity / diagnostics. */
+int enks_version(void);
+const char* enks_last_error(void);
+/* 1 if the current device is sm_100 (B200) and the library's cubin loads. */
+int enks_device_check(void);
+
+/*
+ * Noise substreams (K1+K2).  Replaces the per-member loop of
+ *   enks.py:131-145 _member_noise  ->  matvar.py:149-151 NoiseStreams.substream(i, t, ch)
+ *   .standard_normal((rows, cols))  ->  matvar.py:183-188 transform_standard_normal.
+ * Bit-identical to numpy SeedSequence -> Philox4x64-10 -> ziggurat.
+ *   head/n_head : SeedSequence entropy words common to all streams — the seed's
+ *                 uint32 words zero-padded to 4, followed by NoiseStreams.prefix
+ *                 words (n_head <= 32).  The stream ids (member0+i, t, channel)
+ *                 are appended on device (each < 2^32, one word).
+ *   diag        : optional row scaling (rows doubles) = diagonal of the row
+ *                 Cholesky factor; NULL -> raw standard normals.  A dense
+ *                 factor is applied afterwards with enks_gemm.
+ *   out         : rows x (n_members*cols) block, leading dimension ld_out.
+ *   base/out_plus (optional, both or neither): out_plus = base + value
+ *                 (the "u + w" slot of enks.py:168 and the "x + v" / "u + v"
+ *                 observations of enks.py:200).
+ *   out may be NULL when out_plus is given.
+ */
+int enks_noise_fill(const uint32_t* head, int n_head, uint32_t t, uint32_t channel,
+                    int64_t member0, int64_t n_members, int rows, int cols,
+                    const double* diag, float* out, int64_t ld_out,
+                    const float* base, int64_t ld_base, float* out_plus, int64_t ld_plus,
+                    void* stream);
+
+/*
+ * Member statistics (K4/K5).  Replaces members.mean(axis=0) (enks.py:171, 248),
+ * obs.mean(axis=0) (enks.py:231) and the anomaly formation (enks.py:232-233).
+ * Anomalies are formed relative to a per-(row, col) shift z0 (global member
+ * 0), so identical members give exactly zero anomalies at any N.
+ *   enks_member_sum    : acc[r*cols+j] (double) = sum over local members of (src - z0).
+ *                        z0 == NULL -> z0 is local member 0 (single-rank case).
+ *   enks_member_center : mean = z0 + acc/n_total; anom = (src - z0) - acc/n_total.
+ *                        anom may be NULL (mean only) and may alias src.
+ * `ws` for enks_member_sum: enks_member_sum_ws_bytes() bytes of device scratch.
+ */
+int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols);
+int enks_member_sum(const float* src, int64_t ld_src, int rows, int64_t n_members, int cols,
+                    const float* z0, double* acc, void* ws, void* stream);
+int enks_member_center(const float* src, int64_t ld_src, int rows, int64_t n_members, int cols,
+                       const float* z0, const double* acc, int64_t n_total, float* mean,
+                       float* anom, int64_t ld_anom, void* stream);
+
+/*
+ * Dense fp32 GEMM used by every contraction of the path (K2 dense colouring,
+ * linear forecast, K6/K7 covariances, correction and gain products, K9
+ * member shift, mean update):
+ *   C[M x N] = alpha * op(A) op(B) + beta * C0 + bias[i, n % bias_cols]
+ *   op(A) = A (M x K, lda) or A^T when trans_a (A stored K x M)
+ *   op(B) = B (K x N, ldb) or B^T when trans_b (B stored N x K)
+ * C0/bias optional (NULL); C0 may alias C.  tri_rows/tri_k > 0 skip the
+ * structurally-zero leading K range of block upper-triangular A: rows in
+ * block r0/tri_rows start at k = (r0/tri_rows)*tri_k.
+ * split_k > 1 requires ws of enks_gemm_ws_bytes(M, N, split_k) bytes and is
+ * reduced deterministically (fixed order).  Replaces numpy `@` / OpenBLAS
+ * dgemm at enks.py:153, 247 and matvar.py:188.
+ * `engine`: 0 = auto, 1 = SIMT fp32 FFMA, 2 = tcgen05 3xTF32 (NT only).
+ */
+int64_t enks_gemm_ws_bytes(int64_t M, int64_t N, int split_k);
+int enks_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, float alpha,
+              const float* A, int64_t lda, const float* B, int64_t ldb, float beta,
+              const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias, int bias_cols,
+              float* C, int64_t ldc, int64_t tri_rows, int64_t tri_k, int split_k, void* ws,
+              int engine, void* stream);
+
+/*
+ * Gain solve (K8).  Replaces enks.py:234-235 (symmetrize) and 238-246
+ * (cho_factor with the jitter fallback, cho_solve):
+ *   Sy = scale * 0.5 * (S + S^T); try Cholesky; on failure (pivot <= 0 or NaN)
+ *   retry once with Sy + (1e-9 * tr(Sy)/p + 1e-30) I and increment *jitter_events;
+ *   if that fails too set *status = 1 (the reference raises LinAlgError).
+ *   Writes Sy^{-1} (p x p, ld p) to `inv` (consumed by enks_gemm).
+ * Runs on one CTA in shared memory; p <= enks_spd_max_p().  `ws`: p*p floats.
+ * status / jitter_events are device ints (no host sync).
+ */
+int enks_spd_max_p(void);
+int enks_spd_inverse(const float* S, int64_t lds, int p, float scale, float* inv, float* ws,
+                     int* status, int* jitter_events, void* stream);
+
+/*
+ * CNN forecast (K3): X' = X + alpha * conv_L(...tanh(conv_1([X, U]))...), 3x3
+ * kernels, zero 'same' padding, tanh between layers, torch conv2d weight
+ * layout.  The reference's model seam is MatrixDynamics.step
+ * (dynamics.py:40-50) called at enks.py:168; the CNN itself is not in the
+ * reference.  x/u/out use the member-column layout (image rows =
+ * block rows, image cols = m).  widths[0..n_layers] with widths[0] == 2 and
+ * widths[n_layers] == 1; weights/biases concatenated per layer (device).
+ */
+int enks_cnn_max_width(void);
+int enks_cnn_forward(int n_layers, const int* widths, const float* weights, const float* biases,
+                     float alpha, const float* x, int64_t ldx, const float* u, int64_t ldu,
+                     float* out, int64_t ldo, int rows, int cols, int64_t n_members,
+                     void* stream);
+
+/* Small elementwise helpers. */
+/* out[r, j] = a[r, j] - b[r, j] for an R x C block (innovation y_ref - obs_mean, enks.py:247). */
+int enks_sub(const float* a, int64_t lda, const float* b, int64_t ldb, float* out, int64_t ldo,
+             int64_t rows, int64_t cols, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENKS_B200_H */

@@ -1,0 +1,84 @@
+// Library identity, error reporting and small elementwise kernels.
+#include "common.cuh"
+
+#include <string.h>
+
+namespace enks {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return ENKS_E_CUDA;
+    }
+    return ENKS_OK;
+}
+
+__global__ void probe_kernel(int* out) {
+#ifdef __CUDA_ARCH__
+    *out = __CUDA_ARCH__;
+#endif
+}
+
+__global__ void sub_kernel(const float* __restrict__ a, int64_t lda, const float* __restrict__ b,
+                           int64_t ldb, float* __restrict__ out, int64_t ldo, int64_t rows,
+                           int64_t cols) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= rows * cols) return;
+    int64_t r = idx / cols, c = idx - r * cols;
+    out[r * ldo + c] = a[r * lda + c] - b[r * ldb + c];
+}
+
+}  // namespace enks
+
+extern "C" {
+
+int enks_version(void) { return 1; }
+
+const char* enks_last_error(void) { return enks::g_err; }
+
+int enks_device_check(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return 0;
+    if (prop.major != 10 || prop.minor != 0) {
+        enks::set_error("device %s is sm_%d%d; this library is built for sm_100a only", prop.name,
+                        prop.major, prop.minor);
+        return 0;
+    }
+    int* d = nullptr;
+    if (cudaMalloc(&d, sizeof(int)) != cudaSuccess) return 0;
+    enks::probe_kernel<<<1, 1>>>(d);
+    int h = 0;
+    cudaError_t e = cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) {
+        enks::set_error("probe kernel failed: %s", cudaGetErrorString(e));
+        return 0;
+    }
+    return h == 1000 ? 1 : 0;
+}
+
+int enks_sub(const float* a, int64_t lda, const float* b, int64_t ldb, float* out, int64_t ldo,
+             int64_t rows, int64_t cols, void* stream) {
+    ENKS_REQUIRE(a && b && out, "enks_sub: null pointer");
+    int64_t n = rows * cols;
+    if (n == 0) return ENKS_OK;
+    int threads = 256;
+    int64_t blocks = (n + threads - 1) / threads;
+    enks::sub_kernel<<<(unsigned)blocks, threads, 0, enks::as_stream(stream)>>>(a, lda, b, ldb, out,
+                                                                              ldo, rows, cols);
+    return enks::check_launch("enks_sub");
+}
+
+}  // extern "C"

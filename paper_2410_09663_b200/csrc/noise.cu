@@ -1,0 +1,255 @@
+// K1+K2: bit-exact device noise substreams.
+//
+// Reference call sites: enks.py:131-145 (_member_noise loop over members),
+// matvar.py:149-151 (NoiseStreams.substream -> numpy SeedSequence/Philox),
+// matvar.py:183-188 (colouring mean + L z I_m; col_chol = I_m in every
+// reference virtual system, virtualsys.py:199-208).
+//
+// One warp owns one (member, t, channel) substream.  The 32 lanes evaluate
+// Philox4x64-10 blocks by counter in parallel (128 words per refill, staged
+// in shared memory), test the ziggurat fast-accept for 32 consecutive words
+// at once, emit the accepted prefix as 32 coalesced fp32 stores, and resolve
+// the rare wedge/tail rejections (~1.5% of words) warp-uniformly.  The word
+// consumption is therefore exactly numpy's sequential order.
+#include "common.cuh"
+#include "ziggurat_tables.h"
+
+namespace enks {
+namespace {
+
+constexpr int kWarps = 4;          // warps (streams) per block
+constexpr int kBufWords = 128;     // 32 Philox blocks per refill
+
+__device__ const uint64_t g_ki[256] = NPY_ZIG_KI_DOUBLE_INIT;
+__device__ const uint64_t g_wi[256] = NPY_ZIG_WI_DOUBLE_INIT;
+__device__ const uint64_t g_fi[256] = NPY_ZIG_FI_DOUBLE_INIT;
+
+struct Head {
+    uint32_t w[32];
+    int n;
+};
+
+// numpy SeedSequence (bit_generator.pyx): hashmix / mix / generate_state(2, uint64)
+__device__ __forceinline__ uint32_t hashmix(uint32_t v, uint32_t& h) {
+    v ^= h;
+    h *= 0x931e8875u;
+    v *= h;
+    v ^= v >> 16;
+    return v;
+}
+__device__ __forceinline__ uint32_t mixw(uint32_t x, uint32_t y) {
+    uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+    return r ^ (r >> 16);
+}
+
+__device__ void seed_key(const Head& hd, uint32_t i, uint32_t t, uint32_t ch, uint64_t& k0,
+                         uint64_t& k1) {
+    // entropy = hd.w[0..n) ++ [i, t, ch];  n >= 4 (seed words are padded to the pool size)
+    uint32_t pool[4];
+    uint32_t h = 0x43b0d7e5u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) pool[q] = hashmix(hd.w[q], h);
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int d = 0; d < 4; ++d)
+            if (s != d) pool[d] = mixw(pool[d], hashmix(pool[s], h));
+    for (int s = 4; s < hd.n + 3; ++s) {
+        uint32_t e = s < hd.n ? hd.w[s] : (s == hd.n ? i : (s == hd.n + 1 ? t : ch));
+#pragma unroll
+        for (int d = 0; d < 4; ++d) pool[d] = mixw(pool[d], hashmix(e, h));
+    }
+    uint32_t hb = 0x8b51f9ddu, w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t v = pool[q] ^ hb;
+        hb *= 0x58f38dedu;
+        v *= hb;
+        w[q] = v ^ (v >> 16);
+    }
+    k0 = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+    k1 = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+}
+
+// Philox4x64-10; numpy increments the 256-bit counter before each block, so
+// uint64 word `w` of a fresh stream comes from counter (w/4 + 1, 0, 0, 0).
+struct Block4 {
+    uint64_t v0, v1, v2, v3;
+};
+__device__ __forceinline__ Block4 philox(uint64_t k0, uint64_t k1, uint64_t ctr) {
+    uint64_t c0 = ctr, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B97F4A7C15ULL;
+            k1 += 0xBB67AE8584CAA73BULL;
+        }
+        const uint64_t m0 = 0xD2E7470EE14C6C93ULL, m1 = 0xCA5A826395121157ULL;
+        uint64_t hi0 = __umul64hi(m0, c0), lo0 = m0 * c0;
+        uint64_t hi1 = __umul64hi(m1, c2), lo1 = m1 * c2;
+        uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    return {c0, c1, c2, c3};
+}
+
+struct Args {
+    Head head;
+    uint32_t t, ch;
+    int64_t member0, n_members;
+    int rows, cols;
+    const double* diag;
+    float* out;
+    int64_t ld_out;
+    const float* base;
+    int64_t ld_base;
+    float* out_plus;
+    int64_t ld_plus;
+};
+
+__device__ __forceinline__ double u64_to_unit(uint64_t r) {
+    return (double)(r >> 11) * (1.0 / 9007199254740992.0);
+}
+
+__global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args a) {
+    __shared__ uint64_t s_ki[256];
+    __shared__ double s_wi[256];
+    __shared__ uint64_t s_buf[kWarps][kBufWords];
+    for (int q = threadIdx.x; q < 256; q += blockDim.x) {
+        s_ki[q] = g_ki[q];
+        s_wi[q] = __longlong_as_double((long long)g_wi[q]);
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t local = (int64_t)blockIdx.x * kWarps + warp;
+    if (local >= a.n_members) return;
+    uint64_t k0, k1;
+    seed_key(a.head, (uint32_t)(a.member0 + local), a.t, a.ch, k0, k1);
+
+    uint64_t* buf = s_buf[warp];
+    const int64_t total = (int64_t)a.rows * a.cols;
+    const int64_t col0 = local * a.cols;
+    int64_t base_w = -(1LL << 40);  // buffer holds words [base_w, base_w + 128)
+    int64_t w = 0, q = 0;
+
+    auto emit = [&](int64_t qi, double x) {
+        const int r = (int)(qi / a.cols);
+        const int j = (int)(qi - (int64_t)r * a.cols);
+        const double v = a.diag ? x * a.diag[r] : x;
+        const float f = (float)v;
+        if (a.out) a.out[r * a.ld_out + col0 + j] = f;
+        if (a.out_plus) a.out_plus[r * a.ld_plus + col0 + j] = a.base[r * a.ld_base + col0 + j] + f;
+    };
+    // warp-uniform access to word `ww` (slow path only)
+    auto word = [&](int64_t ww) -> uint64_t {
+        if (ww >= base_w && ww < base_w + kBufWords) return buf[ww - base_w];
+        Block4 b = philox(k0, k1, (uint64_t)(ww >> 2) + 1);
+        int s = (int)(ww & 3);
+        return s == 0 ? b.v0 : (s == 1 ? b.v1 : (s == 2 ? b.v2 : b.v3));
+    };
+
+    while (q < total) {
+        if (w + 32 > base_w + kBufWords) {
+            base_w = w & ~3LL;
+            Block4 b = philox(k0, k1, (uint64_t)(base_w >> 2) + 1 + lane);
+            __syncwarp();
+            buf[4 * lane + 0] = b.v0;
+            buf[4 * lane + 1] = b.v1;
+            buf[4 * lane + 2] = b.v2;
+            buf[4 * lane + 3] = b.v3;
+            __syncwarp();
+        }
+        // fast path for 32 consecutive words
+        uint64_t r = buf[w - base_w + lane];
+        const int idx = (int)(r & 0xff);
+        r >>= 8;
+        const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+        double x = (double)rabs * s_wi[idx];
+        if (r & 1) x = -x;
+        const bool ok = rabs < s_ki[idx];
+        const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+        const int n_ok = bad ? (__ffs(bad) - 1) : 32;
+        const int n_emit = (int)min((int64_t)n_ok, total - q);
+        if (lane < n_emit) emit(q + lane, x);
+        q += n_emit;
+        w += n_emit;
+        if (q >= total || n_ok == 32) continue;
+
+        // slow path for the rejected word at w (warp-uniform)
+        {
+            uint64_t rr = word(w++);
+            const int id = (int)(rr & 0xff);
+            rr >>= 8;
+            const int sign = (int)(rr & 1);
+            const uint64_t ra = (rr >> 1) & 0x000fffffffffffffULL;
+            double xs = (double)ra * __longlong_as_double((long long)g_wi[id]);
+            if (sign) xs = -xs;
+            bool have = false;
+            double val = 0.0;
+            if (id == 0) {
+                for (;;) {
+                    const double xx = -NPY_ZIG_NOR_INV_R * log1p(-u64_to_unit(word(w)));
+                    const double yy = -log1p(-u64_to_unit(word(w + 1)));
+                    w += 2;
+                    if (yy + yy > xx * xx) {
+                        val = ((ra >> 8) & 1) ? -(NPY_ZIG_NOR_R + xx) : NPY_ZIG_NOR_R + xx;
+                        have = true;
+                        break;
+                    }
+                }
+            } else {
+                const double fa = __longlong_as_double((long long)g_fi[id - 1]);
+                const double fb = __longlong_as_double((long long)g_fi[id]);
+                const double uu = u64_to_unit(word(w++));
+                if ((fa - fb) * uu + fb < exp(-0.5 * xs * xs)) {
+                    val = xs;
+                    have = true;
+                }
+            }
+            if (have) {
+                if (lane == 0) emit(q, val);
+                ++q;
+            }
+        }
+    }
+}
+
+}  // namespace
+}  // namespace enks
+
+extern "C" int enks_noise_fill(const uint32_t* head, int n_head, uint32_t t, uint32_t channel,
+                               int64_t member0, int64_t n_members, int rows, int cols,
+                               const double* diag, float* out, int64_t ld_out, const float* base,
+                               int64_t ld_base, float* out_plus, int64_t ld_plus, void* stream) {
+    ENKS_REQUIRE(head != nullptr && n_head >= 4 && n_head <= 32,
+                 "enks_noise_fill: need 4..32 head words (seed padded to 4 + prefix), got %d",
+                 n_head);
+    ENKS_REQUIRE(out || out_plus, "enks_noise_fill: no output");
+    ENKS_REQUIRE(!out_plus || base, "enks_noise_fill: out_plus needs base");
+    ENKS_REQUIRE(member0 >= 0 && member0 + n_members <= (1LL << 32),
+                 "enks_noise_fill: member ids must fit in uint32");
+    if (n_members <= 0 || rows <= 0 || cols <= 0) return ENKS_OK;
+    enks::Args a;
+    for (int q = 0; q < 32; ++q) a.head.w[q] = q < n_head ? head[q] : 0u;
+    a.head.n = n_head;
+    a.t = t;
+    a.ch = channel;
+    a.member0 = member0;
+    a.n_members = n_members;
+    a.rows = rows;
+    a.cols = cols;
+    a.diag = diag;
+    a.out = out;
+    a.ld_out = ld_out;
+    a.base = base;
+    a.ld_base = ld_base;
+    a.out_plus = out_plus;
+    a.ld_plus = ld_plus;
+    int64_t blocks = (n_members + enks::kWarps - 1) / enks::kWarps;
+    enks::noise_kernel<<<(unsigned)blocks, enks::kWarps * 32, 0, enks::as_stream(stream)>>>(a);
+    return enks::check_launch("enks_noise_fill");
+}

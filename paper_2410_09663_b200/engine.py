@@ -1,0 +1,375 @@
+"""Device-resident single-pass matrix-variate EnKS (the hot path).
+
+Restructures reference pkg/src/enksmpc/enks.py:156-253 for the GPU without
+changing the estimator.  The reference keeps every member's whole trajectory
+and, at each update, (i) re-centres it, (ii) contracts it with the centred
+observations (Sigma_xy, enks.py:233-236) and (iii) shifts it in place
+(members += G (y_ref - obs), enks.py:247) -- three O(T d N m) passes over an
+array that grows every step.
+
+Here the trajectory is never rewritten.  For slice s and the update at step
+tau the member deviations are
+
+    M_s - mean_s = A_s - sum_{s <= tau' < tau} G_{tau', s} Yc_{tau'}
+
+where A_s (d x Nm) are the centred predicted slices, Yc_tau (p x Nm) the
+centred perturbed observations and G_{tau, s} (d x p) the gain rows of slice
+s at step tau (the innovation's member-mean part only moves the mean).  So
+with the append-only basis [A_0..A_tau ; Yc_1..Yc_tau] one tall-skinny
+contraction per step,
+
+    P = [A; Yc] Yc_tau^T            (the K = N m contraction, K6/K7)
+
+gives Sigma_y (the Yc_tau block) and, after a small block-triangular
+correction  S_s = P_{A_s} - sum_tau' G_{tau',s} P_{Yc_tau'},  Sigma_xy for
+every slice.  G = (lam/N) S Sigma_y^{-1} (K8), the mean moves by
+G (y_ref - y_bar) and only the newest slice's [x; u] blocks are materialised
+for the next forecast.  Algebraically identical to the reference (checked to
+5e-16 in fp64 by tests/test_engine_algebra.py); in fp32 it removes the
+trajectory read-modify-write and one of the two O(T) contractions per step.
+
+Anomalies are formed relative to global member 0 (stats.cu), so identical
+members give exactly zero spread at any N (scale = 0 cases).
+
+Multi-rank: members are sharded over ranks (global member ids name the noise
+substreams, so draws do not depend on the rank count).  Per step the only
+exchanges are the slice/observation member sums, the member-0 shift
+(broadcast) and the allreduce of P; the gain, correction and mean update are
+replicated.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .matvar import entropy_head
+
+CH_W, CH_VX, CH_VU, CH_EPS = 0, 1, 2, 3
+
+
+class LocalComm:
+    rank = 0
+    size = 1
+
+    def allreduce_(self, t):
+        return t
+
+    def broadcast_(self, t, src=0):
+        return t
+
+
+class TorchComm:
+    """torch.distributed process group (NCCL on B200, gloo on CPU tests)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def allreduce_(self, t):
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def broadcast_(self, t, src=0):
+        self.dist.broadcast(t, src=src, group=self.group)
+        return t
+
+
+def partition(n_members: int, size: int, rank: int) -> tuple[int, int]:
+    """(first global member, count) of rank `rank` for an even split."""
+    base, extra = divmod(n_members, size)
+    count = base + (1 if rank < extra else 0)
+    first = rank * base + min(rank, extra)
+    return first, count
+
+
+@dataclass
+class _Noise:
+    kind: str           # "zero" | "diag" | "dense"
+    diag: object = None  # device float64 (rows,)
+    dense: object = None  # device float32 (rows, rows)
+
+
+class Forecaster:
+    """Device forecast for one dynamics model (dispatch on model type; no host fallback)."""
+
+    def __init__(self, model, ops, n: int, l: int):
+        self.model = model
+        self.kind = None
+        name = type(model).__name__
+        if name == "CNNDynamics" and hasattr(model, "widths"):
+            if l != n:
+                raise ValueError("CNNDynamics needs input_rows == state_rows")
+            if max(model.widths) > 32 or model.n_layers > 8:
+                raise NotImplementedError("CNN widths > 32 or > 8 layers not supported on device")
+            self.kind = "cnn"
+            self.widths = tuple(model.widths)
+            self.n_layers = len(self.widths) - 1
+            self.alpha = float(model.alpha)
+            self.cols = int(model.state_cols)
+            self.w_dev = ops.to_device(np.concatenate([np.asarray(w, float).ravel()
+                                                       for w in model.weights]))
+            self.b_dev = ops.to_device(np.concatenate([np.asarray(b, float).ravel()
+                                                       for b in model.biases]))
+        elif name == "LinearDynamics" and hasattr(model, "a") and hasattr(model, "b"):
+            self.kind = "linear"
+            ab = np.concatenate([np.asarray(model.a, float), np.asarray(model.b, float)], axis=1)
+            self.ab = ops.to_device(ab)  # n x (n + l)
+        else:
+            raise TypeError(f"no device forecast for model type {name}; supported: "
+                            "LinearDynamics, CNNDynamics")
+
+    def __call__(self, ops, last, out, n: int, n_members: int):
+        """out (n x K) = f(x = last[:n], u = last[n:])."""
+        if self.kind == "linear":
+            ops.gemm(self.ab, last, out)
+        else:
+            ops.cnn_forward(self, last[:n], last[n:], out, n_members)
+
+
+def _noise_params(params, ops, rows: int, cols: int) -> _Noise:
+    if params is None:
+        return _Noise("zero")
+    L = np.asarray(params.row_chol, dtype=float)
+    B = np.asarray(params.col_chol, dtype=float)
+    if not np.array_equal(B, np.eye(cols)):
+        raise NotImplementedError("device noise supports column Cholesky factor I_m only "
+                                  "(the reference virtual system always uses I_m)")
+    if np.any(np.asarray(params.mean) != 0):
+        raise NotImplementedError("device noise supports zero-mean channels only")
+    if L.shape != (rows, rows):
+        raise ValueError("noise factor shape mismatch")
+    if np.array_equal(L, np.diag(np.diag(L))):
+        return _Noise("diag", diag=ops.to_device(np.diag(L).copy(), dtype=torch.float64))
+    return _Noise("dense", dense=ops.to_device(L))
+
+
+class DeviceSmoother:
+    """Ensemble state + per-step orchestration for one horizon (see module docstring)."""
+
+    def __init__(self, ops, x0_packed: np.ndarray, n: int, l: int, n_members: int, lam: float,
+                 capacity: int = 8, comm=None):
+        self.ops = ops
+        self.comm = comm or LocalComm()
+        self.n, self.l = int(n), int(l)
+        self.d, self.p = self.n + 2 * self.l, self.n + self.l
+        self.m = int(x0_packed.shape[1])
+        self.N = int(n_members)
+        if self.N < self.comm.size:
+            raise ValueError("need at least one member per rank")
+        self.member0, self.Nl = partition(self.N, self.comm.size, self.comm.rank)
+        self.K = self.Nl * self.m
+        self.lam = float(lam)
+        self.t = 0
+        self.cap = 0
+        self.slice0_zero = True  # all members start as identical copies (enks.py:120)
+        self._bound = None
+        d, p, K, m = self.d, self.p, self.K, self.m
+        self.slice_raw = ops.empty(d, K)      # [X; U; W] of the newest predicted slice
+        self.obs_raw = ops.empty(p, K)        # perturbed observations of the newest slice
+        self.last = ops.empty(p, K)           # materialised [x; u] of the newest updated slice
+        self.acc = ops.zeros(max(d, p), m, dtype=torch.float64)
+        self.z0 = ops.zeros(max(d, p), m) if self.comm.size > 1 else None
+        self.ybar = ops.zeros(p, m)
+        self.innov = ops.zeros(p, m)
+        self.sinv = ops.zeros(p, p)
+        self.status = ops.zeros(1, dtype=torch.int32)
+        self.jitter = ops.zeros(1, dtype=torch.int32)
+        self._grow(max(1, int(capacity)))
+        x0 = ops.to_device(np.asarray(x0_packed, float))
+        self.mean[:d] = x0
+        self.last.copy_(x0[:p].repeat(1, self.Nl))
+        self.Abuf[:d].zero_()
+
+    # ------------------------------------------------------------ storage
+    def _grow(self, cap: int) -> None:
+        """(Re)allocate the append-only basis for `cap` steps (slices 0..cap)."""
+        if cap <= self.cap:
+            return
+        ops, d, p, K, m = self.ops, self.d, self.p, self.K, self.m
+        Abuf = ops.empty((cap + 1) * d, K)
+        Ybuf = ops.empty(cap * p, K)
+        G = ops.zeros((cap + 1) * d, cap * p)
+        mean = ops.zeros((cap + 1) * d, m)
+        PA = ops.empty((cap + 1) * d, p)
+        PY = ops.empty(cap * p, p)
+        if self.cap:
+            rows_a, rows_y = (self.t + 1) * d, self.t * p
+            Abuf[:rows_a] = self.Abuf[:rows_a]
+            Ybuf[:rows_y] = self.Ybuf[:rows_y]
+            G[:rows_a, :rows_y] = self.G[:rows_a, :rows_y]
+            mean[:rows_a] = self.mean[:rows_a]
+        self.Abuf, self.Ybuf, self.G, self.mean, self.PA, self.PY = Abuf, Ybuf, G, mean, PA, PY
+        self.cap = cap
+
+    def memory_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in
+                   (self.Abuf, self.Ybuf, self.G, self.mean, self.PA, self.PY, self.slice_raw,
+                    self.obs_raw, self.last))
+
+    # ------------------------------------------------------------ binding
+    def bind(self, vs) -> None:
+        if self._bound is vs:
+            return
+        if getattr(vs, "constraint", None) is not None:
+            raise NotImplementedError("constraint barrier rows are not on the device path yet "
+                                      "(SURVEY.md §8f row 4)")
+        ops = self.ops
+        self.forecast = Forecaster(vs.model, ops, self.n, self.l)
+        self.noise_w = _noise_params(vs.process_noise, ops, self.l, self.m)
+        self.noise_vx = _noise_params(vs.obs_noise_x, ops, self.n, self.m)
+        self.noise_vu = _noise_params(vs.obs_noise_u, ops, self.l, self.m)
+        self._bound = vs
+
+    # ------------------------------------------------------------ helpers
+    def _noise(self, spec: _Noise, head, t, ch, rows, out=None, base=None, out_plus=None):
+        """out = L z ; out_plus = base + L z for this rank's members."""
+        ops = self.ops
+        if spec.kind == "zero":
+            if out is not None:
+                out.zero_()
+            if out_plus is not None:
+                out_plus.copy_(base)
+            return
+        if spec.kind == "diag":
+            ops.noise_fill(head, t, ch, self.member0, self.Nl, rows, self.m, diag=spec.diag,
+                           out=out, base=base, out_plus=out_plus)
+            return
+        z = ops.empty(rows, self.K)
+        ops.noise_fill(head, t, ch, self.member0, self.Nl, rows, self.m, out=z)
+        if out is not None:
+            ops.gemm(spec.dense, z, out)
+        if out_plus is not None:
+            ops.gemm(spec.dense, z, out_plus, beta=1.0, C0=base)
+
+    def _center(self, src, mean_out, anom_out):
+        """Member mean (rows x m) and anomalies of `src` (rows x K), shift = global member 0."""
+        ops, comm, rows = self.ops, self.comm, src.shape[0]
+        if rows > self.acc.shape[0]:
+            self.acc = ops.zeros(rows, self.m, dtype=torch.float64)
+            if self.z0 is not None:
+                self.z0 = ops.zeros(rows, self.m)
+        acc = self.acc[:rows]
+        z0 = None
+        if comm.size > 1:
+            z0 = self.z0[:rows]
+            if comm.rank == 0:
+                z0.copy_(src[:, :self.m])
+            comm.broadcast_(z0, src=0)
+        ops.member_sum(src, self.Nl, self.m, z0, acc)
+        comm.allreduce_(acc)
+        ops.member_center(src, self.Nl, self.m, z0, acc, self.N, mean=mean_out, anom=anom_out)
+
+    # ------------------------------------------------------------ predict
+    def predict(self, vs, streams) -> None:
+        """enks.py:156-171: W draw, new slice [f(x,u); u+w; w], append, mean."""
+        self.bind(vs)
+        tau = self.t + 1
+        if tau > self.cap:
+            self._grow(max(2 * self.cap, tau))
+        ops, n, l, d = self.ops, self.n, self.l, self.d
+        head = entropy_head(streams.seed, tuple(streams.prefix))
+        sr = self.slice_raw
+        # ΔU slot = w, U slot = u + w  (one draw fills both, enks.py:168)
+        self._noise(self.noise_w, head, tau, CH_W, l, out=sr[n + l:], base=self.last[n:],
+                    out_plus=sr[n:n + l])
+        self.forecast(ops, self.last, sr[:n], n, self.Nl)
+        self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d])
+        self.t = tau
+
+    # ------------------------------------------------------------ update
+    def update(self, y_ref_dev, streams) -> None:
+        """enks.py:212-248 restated on the append-only basis (module docstring)."""
+        ops, comm = self.ops, self.comm
+        n, l, d, p, tau = self.n, self.l, self.d, self.p, self.t
+        if tau < 1:
+            raise RuntimeError("update before the first predict")
+        head = entropy_head(streams.seed, tuple(streams.prefix))
+        sr, ob = self.slice_raw, self.obs_raw
+        # perturbed observations [x + v_x; u + v_u]  (enks.py:194-200)
+        self._noise(self.noise_vx, head, tau, CH_VX, n, base=sr[:n], out_plus=ob[:n])
+        self._noise(self.noise_vu, head, tau, CH_VU, l, base=sr[n:n + l], out_plus=ob[n:])
+        yc = self.Ybuf[(tau - 1) * p:tau * p]
+        self._center(ob, self.ybar, yc)
+
+        # P = [A_s0..A_tau ; Yc_1..Yc_tau] Yc_tau^T  (local K-partial, then allreduce)
+        a0 = d if self.slice0_zero else 0
+        rows_a = (tau + 1) * d
+        PA, PY = self.PA[a0:rows_a], self.PY[:tau * p]
+        ops.gemm(self.Abuf[a0:rows_a], yc, PA, trans_b=True)
+        ops.gemm(self.Ybuf[:tau * p], yc, PY, trans_b=True)
+        comm.allreduce_(PA)
+        comm.allreduce_(PY)
+
+        # Sigma_y^{-1} with the reference's jitter fallback (enks.py:234-244)
+        scale = self.lam / self.N
+        ops.spd_inverse(PY[(tau - 1) * p:], scale, self.sinv, self.status, self.jitter)
+        # S_s = P_{A_s} - sum_{tau' < tau} G_{tau',s} P_{Yc_tau'}  (block upper-triangular G)
+        if tau > 1:
+            ops.gemm(self.G[a0:rows_a, :(tau - 1) * p], self.PY[:(tau - 1) * p], PA,
+                     alpha=-1.0, beta=1.0, C0=PA, tri=(d, p) if a0 == 0 else (0, 0))
+        # G_{tau,s} = (lam/N) S_s Sigma_y^{-1}
+        gcol = self.G[a0:rows_a, (tau - 1) * p:tau * p]
+        ops.gemm(PA, self.sinv, gcol, alpha=scale)
+        # mean_s += G_{tau,s} (y_ref - y_bar)   (enks.py:247-248 on the mean)
+        ops.sub(y_ref_dev, self.ybar, self.innov)
+        mv = self.mean[a0:rows_a]
+        ops.gemm(gcol, self.innov, mv, beta=1.0, C0=mv)
+        # newest slice [x; u] for the next forecast: mean + A_tau - G_{tau,tau} Yc_tau
+        r0 = tau * d
+        ops.gemm(self.G[r0:r0 + p, (tau - 1) * p:tau * p], yc, self.last, alpha=-1.0, beta=1.0,
+                 C0=self.Abuf[r0:r0 + p], bias=self.mean[r0:r0 + p], bias_cols=self.m)
+
+    # ------------------------------------------------------------ readback
+    def deviations(self, rows: int | None = None):
+        """Member deviations M - mean for slices 0..t, (T d x K) on device."""
+        ops, d, p, t = self.ops, self.d, self.p, self.t
+        R = (t + 1) * d
+        out = ops.empty(R, self.K)
+        a0 = d if self.slice0_zero else 0
+        out[:a0] = self.Abuf[:a0]
+        if t >= 1:
+            ops.gemm(self.G[a0:R, :t * p], self.Ybuf[:t * p], out[a0:], alpha=-1.0, beta=1.0,
+                     C0=self.Abuf[a0:R], tri=(d, p) if a0 else (0, 0))
+        else:
+            out[a0:] = self.Abuf[a0:R]
+        return out
+
+    def members_device(self):
+        dev = self.deviations()
+        R = dev.shape[0]
+        mean = self.mean[:R]
+        return dev + mean.repeat(1, self.Nl)
+
+    def mean_host(self) -> np.ndarray:
+        R = (self.t + 1) * self.d
+        return self.mean[:R].double().cpu().numpy()
+
+    def jitter_events(self) -> int:
+        return int(self.jitter.item())
+
+    def check_status(self) -> None:
+        if int(self.status.item()) != 0:
+            raise np.linalg.LinAlgError("observation covariance not positive definite even "
+                                        "after jitter")
+
+    def replace_members(self, members_local: np.ndarray, t: int) -> None:
+        """Reset the representation to explicit members (local shard, (Nl, (t+1)d, m))."""
+        ops, d = self.ops, self.d
+        self.t = 0
+        self._grow(max(t, 1))
+        self.t = int(t)
+        R = (self.t + 1) * d
+        M = np.asarray(members_local, dtype=float).transpose(1, 0, 2).reshape(R, self.K)
+        Mdev = ops.to_device(M)
+        self.G.zero_()
+        self._center(Mdev, self.mean[:R], self.Abuf[:R])
+        x0_spread = bool(torch.any(self.Abuf[:d] != 0).item())
+        self.slice0_zero = not x0_spread
+        last = Mdev[self.t * d:self.t * d + self.p]
+        self.last.copy_(last)

@@ -1,0 +1,282 @@
+"""Drop-in, B200-backed replacement for the reference smoother API.
+
+Same names, signatures, return shapes and error behaviour as reference
+pkg/src/enksmpc/enks.py:36-47:
+
+    TrajectoryEnsemble, SmootherCovariances, CH_W, CH_VX, CH_VU, CH_EPS,
+    init_ensemble (105-128), predict (156-186), update (212-253),
+    smooth_horizon (256-284)
+
+The ensemble lives on the GPU (engine.DeviceSmoother); ``members`` and
+``mean`` are materialised as fp64 NumPy arrays on access (one device sync),
+so code that inspects them keeps working.  Arithmetic is fp32 on device;
+parity with the fp64 reference is <= 1e-4 relative (tests/test_parity_gpu.py).
+Noise is bit-identical to the reference's NoiseStreams substreams.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from .engine import CH_EPS, CH_VU, CH_VX, CH_W, DeviceSmoother, LocalComm
+
+__all__ = [
+    "TrajectoryEnsemble",
+    "SmootherCovariances",
+    "CH_W",
+    "CH_VX",
+    "CH_VU",
+    "CH_EPS",
+    "init_ensemble",
+    "predict",
+    "update",
+    "smooth_horizon",
+    "set_default_comm",
+]
+
+_OPS = None
+_COMM = None
+
+
+def _ops():
+    global _OPS
+    if _OPS is None:
+        from .ops import DeviceOps
+
+        _OPS = DeviceOps()
+    return _OPS
+
+
+def set_default_comm(comm) -> None:
+    """Shard members over a torch.distributed group for subsequent ensembles
+    (``engine.TorchComm()``); None restores single-process operation."""
+    global _COMM
+    _COMM = comm
+
+
+def _comm():
+    return _COMM or LocalComm()
+
+
+@dataclass
+class SmootherCovariances:
+    """lambda-scaled covariance tracking (enks.py:96-102); fp64 host arrays."""
+
+    sigma_traj: np.ndarray
+    sigma_pred: Optional[np.ndarray] = None
+    sigma_cross: Optional[np.ndarray] = None
+
+
+class TrajectoryEnsemble:
+    """N trajectory samples with their running mean (enks.py:56-93), device-resident.
+
+    ``members`` has shape (N, (t+1)*slice_rows, m) and ``mean`` ((t+1)*slice_rows, m)
+    when read.  Assigning ``members`` re-seeds the device state from explicit samples.
+    """
+
+    def __init__(self, members=None, mean=None, t: int = 0, lam: float | None = None,
+                 n_x: int | None = None, n_u: int | None = None, jitter_events: int = 0, *,
+                 _engine: DeviceSmoother | None = None):
+        self._jitter0 = int(jitter_events)
+        if _engine is not None:
+            self._eng = _engine
+            return
+        if members is None or lam is None or n_x is None or n_u is None:
+            raise TypeError("TrajectoryEnsemble needs members, mean, t, lam, n_x, n_u")
+        members = np.asarray(members, dtype=float)
+        d = n_x + 2 * n_u
+        if members.ndim != 3 or members.shape[1] != (t + 1) * d:
+            raise ValueError("members must be (N, (t+1)(n+2l), m)")
+        comm = _comm()
+        eng = DeviceSmoother(_ops(), members[0, :d], n_x, n_u, members.shape[0], lam,
+                             capacity=max(t, 1), comm=comm)
+        lo, cnt = eng.member0, eng.Nl
+        eng.replace_members(members[lo:lo + cnt], t)
+        self._eng = eng
+
+    # -- reference dataclass fields ----------------------------------------
+    @property
+    def members(self) -> np.ndarray:
+        eng = self._eng
+        R = (eng.t + 1) * eng.d
+        local = eng.members_device().double().cpu().numpy()
+        local = local.reshape(R, eng.Nl, eng.m).transpose(1, 0, 2)
+        if eng.comm.size > 1:
+            import torch.distributed as dist
+
+            parts = [None] * eng.comm.size
+            dist.all_gather_object(parts, local, group=getattr(eng.comm, "group", None))
+            local = np.concatenate(parts, axis=0)
+        return np.ascontiguousarray(local)
+
+    @members.setter
+    def members(self, value) -> None:
+        value = np.asarray(value, dtype=float)
+        eng = self._eng
+        if value.ndim != 3 or value.shape[1] % eng.d or value.shape[0] != eng.N:
+            raise ValueError("members must be (N, (t+1)(n+2l), m) for this ensemble")
+        eng.replace_members(value[eng.member0:eng.member0 + eng.Nl], value.shape[1] // eng.d - 1)
+
+    @property
+    def mean(self) -> np.ndarray:
+        return self._eng.mean_host()
+
+    @property
+    def t(self) -> int:
+        return self._eng.t
+
+    @property
+    def lam(self) -> float:
+        return self._eng.lam
+
+    @property
+    def n_x(self) -> int:
+        return self._eng.n
+
+    @property
+    def n_u(self) -> int:
+        return self._eng.l
+
+    @property
+    def jitter_events(self) -> int:
+        return self._jitter0 + self._eng.jitter_events()
+
+    # -- reference helpers ------------------------------------------------------
+    @property
+    def n_members(self) -> int:
+        return self._eng.N
+
+    @property
+    def slice_rows(self) -> int:
+        return self._eng.d
+
+    @property
+    def n_cols(self) -> int:
+        return self._eng.m
+
+    def slices(self) -> np.ndarray:
+        return self.mean.reshape(self.t + 1, self.slice_rows, self.n_cols)
+
+    def last_slice_blocks(self):
+        d, n, l = self.slice_rows, self.n_x, self.n_u
+        tail = self.members[:, -d:, :]
+        return tail[:, :n, :], tail[:, n:n + l, :], tail[:, n + l:, :]
+
+    @property
+    def engine(self) -> DeviceSmoother:
+        return self._eng
+
+
+def init_ensemble(x0, n_members: int, shared_col_cov: np.ndarray | None = None, *,
+                  capacity: int = 8) -> TrajectoryEnsemble:
+    """N identical copies of the current slice; lambda = 1/tr(shared_col_cov) (enks.py:105-128)."""
+    if n_members < 2:
+        raise ValueError("need at least 2 ensemble members")
+    packed = np.asarray(x0.packed, dtype=float)
+    lam = 1.0 / packed.shape[1] if shared_col_cov is None else \
+        1.0 / float(np.trace(shared_col_cov))
+    eng = DeviceSmoother(_ops(), packed, x0.n, x0.l, n_members, lam, capacity=capacity,
+                         comm=_comm())
+    return TrajectoryEnsemble(_engine=eng)
+
+
+def _cov_product(eng: DeviceSmoother, a, b) -> np.ndarray:
+    """(lam/N) a b^T over all members (K contraction + allreduce), fp64 on host."""
+    out = eng.ops.empty(a.shape[0], b.shape[0])
+    eng.ops.gemm(a, b, out, trans_b=True, alpha=eng.lam / eng.N)
+    eng.comm.allreduce_(out)
+    return out.double().cpu().numpy()
+
+
+def predict(ens: TrajectoryEnsemble, vs, streams, cov: Optional[SmootherCovariances] = None
+            ) -> TrajectoryEnsemble:
+    """Advance every member one virtual step and append the new slice (enks.py:156-186)."""
+    eng = ens._eng
+    eng.predict(vs, streams)
+    if cov is not None:
+        d = eng.d
+        dev_new = eng.Abuf[eng.t * d:(eng.t + 1) * d]
+        dev_traj = eng.deviations()
+        cov.sigma_pred = _cov_product(eng, dev_new, dev_new)
+        cov.sigma_cross = _cov_product(eng, dev_traj, dev_new)
+        old = cov.sigma_traj.shape[0]
+        block = np.zeros((old + d, old + d))
+        block[:old, :old] = cov.sigma_traj
+        block[:old, old:] = cov.sigma_cross[:old]
+        block[old:, :old] = cov.sigma_cross[:old].T
+        block[old:, old:] = cov.sigma_pred
+        cov.sigma_traj = block
+    return ens
+
+
+def _device_yref(eng: DeviceSmoother, y_ref: np.ndarray):
+    return eng.ops.to_device(np.asarray(y_ref, dtype=float))
+
+
+def update(ens: TrajectoryEnsemble, y_ref: np.ndarray, vs, streams,
+           cov: Optional[SmootherCovariances] = None) -> TrajectoryEnsemble:
+    """Kalman-shift every member's whole trajectory toward the reference (enks.py:212-253)."""
+    eng = ens._eng
+    y_ref = np.asarray(y_ref, dtype=float)
+    obs_shape = (vs.obs_rows, eng.m)
+    if y_ref.shape != obs_shape:
+        raise ValueError(f"y_ref shape {y_ref.shape} != observation {obs_shape}")
+    if eng.t < 1:
+        raise NotImplementedError("update() before the first predict() is not supported on "
+                                  "the device path")
+    eng.bind(vs)
+    eng.update(_device_yref(eng, y_ref), streams)
+    eng.check_status()
+    if cov is not None:
+        dev = eng.deviations()
+        cov.sigma_traj = _cov_product(eng, dev, dev)
+    return ens
+
+
+def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
+                   track_cov: bool = False):
+    """Forward predict/update sweep over an h-step horizon (enks.py:256-284).
+
+    Returns the mean trajectory (h+1, n+2l, m) as fp64 and the covariances
+    when ``track_cov``.  One host synchronisation at the end.
+    """
+    if h < 1:
+        raise ValueError("horizon must be at least 1")
+    y_refs = np.asarray(y_refs, dtype=float)
+    if y_refs.ndim == 2:
+        y_refs = np.broadcast_to(y_refs, (h, *y_refs.shape))
+    elif y_refs.shape[0] != h:
+        raise ValueError(f"need {h} reference observations, got {y_refs.shape[0]}")
+    if y_refs.shape[1:] != (vs.obs_rows, x0.m):
+        raise ValueError(f"y_ref shape {y_refs.shape[1:]} != observation {(vs.obs_rows, x0.m)}")
+    ens = init_ensemble(x0, n_members, shared_col_cov=vs.shared_col_cov, capacity=h)
+    eng = ens._eng
+    eng.bind(vs)
+    yref_dev = eng.ops.to_device(np.ascontiguousarray(y_refs))
+    cov = SmootherCovariances(sigma_traj=np.zeros((eng.d, eng.d))) if track_cov else None
+    for step in range(h):
+        predict(ens, vs, streams, cov=cov)
+        if cov is None:
+            eng.update(yref_dev[step], streams)
+        else:
+            update(ens, y_refs[step], vs, streams, cov=cov)
+    eng.check_status()
+    return ens.slices(), cov
+
+
+def smooth_horizon_device(x0, yref_dev: torch.Tensor, vs, h: int, n_members: int, streams,
+                          comm=None) -> DeviceSmoother:
+    """Device-resident variant for benchmarks / closed loops: y refs already on
+    device (h, p, m); returns the engine without any host synchronisation."""
+    packed = np.asarray(x0.packed, dtype=float)
+    lam = 1.0 / float(np.trace(vs.shared_col_cov))
+    eng = DeviceSmoother(_ops(), packed, x0.n, x0.l, n_members, lam, capacity=h,
+                         comm=comm or _comm())
+    eng.bind(vs)
+    for step in range(h):
+        eng.predict(vs, streams)
+        eng.update(yref_dev[step], streams)
+    return eng

@@ -1,0 +1,147 @@
+"""Device operator set: thin tensor-view wrappers over the C-ABI (include/enks_b200.h).
+
+The smoother engine (``engine.py``) is written against this small operator
+interface.  ``DeviceOps`` is the only implementation in the product; every
+method is one or two stream-ordered launches of an sm_100a kernel through
+ctypes.  (tests/cpu_ops.py holds a CPU restatement of the same interface
+used ONLY to exercise the multi-rank orchestration with the gloo backend.)
+
+Tensor arguments are 2-D views with unit column stride; the row stride is
+passed as the leading dimension.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+NUM_SMS = 148
+
+
+def _ld(t: torch.Tensor) -> int:
+    if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+        raise ValueError(f"expected a 2-D row-major view, got shape {tuple(t.shape)} "
+                         f"strides {t.stride()}")
+    return t.stride(0) if t.shape[0] > 1 else max(t.shape[1], t.stride(0))
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def choose_split(M: int, N: int, K: int, bm: int = 128, bn: int = 128, min_k: int = 2048) -> int:
+    """Split-K factor so that a tall-skinny contraction fills the 148 SMs (>= 2 waves)."""
+    tiles = -(-M // bm) * -(-N // bn)
+    if tiles >= 2 * NUM_SMS:
+        return 1
+    split = -(-2 * NUM_SMS // tiles)
+    return int(max(1, min(split, K // min_k, 128)))
+
+
+class DeviceOps:
+    """sm_100a kernels behind the C-ABI.  No CPU fallback: construction fails loudly."""
+
+    dtype = torch.float32
+
+    def __init__(self, device: torch.device | int | None = None):
+        self.lib = _lib.load_library(check_device=True)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else torch.device(device).index or 0)
+        self._ws = None
+        self._ws_sum = None
+        self.launches = 0  # kernel-entry calls issued (for the bench's gpu_launches claim)
+
+    # -- memory -----------------------------------------------------------
+    def empty(self, *shape, dtype=None):
+        return torch.empty(shape, dtype=dtype or self.dtype, device=self.device)
+
+    def zeros(self, *shape, dtype=None):
+        return torch.zeros(shape, dtype=dtype or self.dtype, device=self.device)
+
+    def to_device(self, arr, dtype=None):
+        return torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype or self.dtype).to(self.device)
+
+    def _workspace(self, nbytes: int) -> int:
+        if nbytes <= 0:
+            return 0
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(int(nbytes * 1.25) + 256, dtype=torch.uint8, device=self.device)
+        return self._ws.data_ptr()
+
+    def _workspace_sum(self, nbytes: int) -> int:
+        if self._ws_sum is None or self._ws_sum.numel() < nbytes:
+            self._ws_sum = torch.empty(int(nbytes * 1.25) + 256, dtype=torch.uint8,
+                                       device=self.device)
+        return self._ws_sum.data_ptr()
+
+    @staticmethod
+    def _stream() -> int:
+        return torch.cuda.current_stream().cuda_stream
+
+    # -- kernels ----------------------------------------------------------
+    def noise_fill(self, head, t, ch, member0, n_members, rows, cols, diag=None, out=None,
+                   base=None, out_plus=None):
+        words = (ctypes.c_uint32 * len(head))(*[int(w) for w in head])
+        self.launches += 1
+        _lib.call("enks_noise_fill", words, len(head), int(t), int(ch), int(member0),
+                  int(n_members), int(rows), int(cols), _p(diag), _p(out),
+                  _ld(out) if out is not None else 0, _p(base),
+                  _ld(base) if base is not None else 0, _p(out_plus),
+                  _ld(out_plus) if out_plus is not None else 0, self._stream())
+
+    def member_sum(self, src, n_members, cols, z0, acc):
+        rows = src.shape[0]
+        nbytes = self.lib.enks_member_sum_ws_bytes(rows, n_members, cols)
+        ws = self._workspace_sum(nbytes)
+        self.launches += 2
+        _lib.call("enks_member_sum", _p(src), _ld(src), rows, int(n_members), int(cols), _p(z0),
+                  _p(acc), ws, self._stream())
+
+    def member_center(self, src, n_members, cols, z0, acc, n_total, mean=None, anom=None):
+        rows = src.shape[0]
+        self.launches += 1
+        _lib.call("enks_member_center", _p(src), _ld(src), rows, int(n_members), int(cols),
+                  _p(z0), _p(acc), int(n_total), _p(mean), _p(anom),
+                  _ld(anom) if anom is not None else 0, self._stream())
+
+    def gemm(self, A, B, C, *, trans_a=False, trans_b=False, alpha=1.0, beta=0.0, C0=None,
+             bias=None, bias_cols=1, tri=(0, 0), split=None, engine=0):
+        M, N = C.shape
+        K = A.shape[0] if trans_a else A.shape[1]
+        if (B.shape[1] if trans_b else B.shape[0]) != K:
+            raise ValueError("gemm: inner dimensions disagree")
+        if M == 0 or N == 0:
+            return
+        if split is None:
+            split = choose_split(M, N, K)
+        ws = self._workspace(self.lib.enks_gemm_ws_bytes(M, N, split)) if split > 1 else None
+        self.launches += 2 if split > 1 else 1
+        _lib.call("enks_gemm", int(trans_a), int(trans_b), M, N, K, float(alpha),
+                  _p(A) if K else None, _ld(A) if K else 0, _p(B) if K else None,
+                  _ld(B) if K else 0, float(beta), _p(C0), _ld(C0) if C0 is not None else 0,
+                  _p(bias), _ld(bias) if bias is not None else 0, int(bias_cols), _p(C), _ld(C),
+                  int(tri[0]), int(tri[1]), int(split), ws, int(engine), self._stream())
+
+    def spd_inverse(self, S, scale, inv, status, jitter):
+        p = S.shape[0]
+        self.launches += 1
+        _lib.call("enks_spd_inverse", _p(S), _ld(S), p, float(scale), _p(inv), None, _p(status),
+                  _p(jitter), self._stream())
+
+    def spd_max_p(self) -> int:
+        return int(self.lib.enks_spd_max_p())
+
+    def cnn_forward(self, cnn, x, u, out, n_members):
+        widths = (ctypes.c_int * len(cnn.widths))(*cnn.widths)
+        self.launches += 1
+        _lib.call("enks_cnn_forward", cnn.n_layers, widths, _p(cnn.w_dev), _p(cnn.b_dev),
+                  float(cnn.alpha), _p(x), _ld(x), _p(u), _ld(u), _p(out), _ld(out),
+                  int(x.shape[0]), int(cnn.cols), int(n_members), self._stream())
+
+    def sub(self, a, b, out):
+        self.launches += 1
+        _lib.call("enks_sub", _p(a), _ld(a), _p(b), _ld(b), _p(out), _ld(out), out.shape[0],
+                  out.shape[1], self._stream())

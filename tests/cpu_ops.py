@@ -1,0 +1,112 @@
+"""TEST-ONLY CPU restatement of the device operator interface (paper_2410_09663_b200/ops.py).
+
+Lets the engine's orchestration (the append-only basis algebra, member
+sharding, collectives) run on CPU with the gloo backend, where no GPU
+exists.  Each method restates the contract of the matching C-ABI entry
+point (include/enks_b200.h) in fp64 torch; noise comes from the C oracle.
+Never imported by the product package.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import noise as onoise
+
+
+class CpuOps:
+    dtype = torch.float64
+
+    def __init__(self):
+        self.device = torch.device("cpu")
+        self.launches = 0
+
+    def empty(self, *shape, dtype=None):
+        return torch.empty(shape, dtype=dtype or self.dtype)
+
+    def zeros(self, *shape, dtype=None):
+        return torch.zeros(shape, dtype=dtype or self.dtype)
+
+    def to_device(self, arr, dtype=None):
+        return torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype or self.dtype).clone()
+
+    def noise_fill(self, head, t, ch, member0, n_members, rows, cols, diag=None, out=None,
+                   base=None, out_plus=None):
+        out_z = np.empty((n_members, rows * cols))
+        for k in range(n_members):
+            ent = list(head) + [member0 + k, t, ch]
+            key = np.zeros(2, dtype=np.uint64)
+            import ctypes
+
+            arr = np.asarray(ent, dtype=np.uint32)
+            onoise._lib().npyo_seedseq_key(arr.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                           len(arr),
+                                           key.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+            onoise._lib().npyo_standard_normal(key.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                               rows * cols,
+                                               out_z[k].ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        z = out_z.reshape(n_members, rows, cols)
+        if diag is not None:
+            z = z * diag.numpy()[None, :, None]
+        blk = torch.from_numpy(np.ascontiguousarray(z.transpose(1, 0, 2).reshape(rows, -1)))
+        if out is not None:
+            out.copy_(blk)
+        if out_plus is not None:
+            out_plus.copy_(base + blk)
+
+    def member_sum(self, src, n_members, cols, z0, acc):
+        s = src.reshape(src.shape[0], n_members, cols)
+        shift = s[:, 0, :] if z0 is None else z0
+        acc.copy_((s - shift[:, None, :]).sum(dim=1))
+
+    def member_center(self, src, n_members, cols, z0, acc, n_total, mean=None, anom=None):
+        s = src.reshape(src.shape[0], n_members, cols)
+        shift = (s[:, 0, :] if z0 is None else z0).clone()
+        mu = acc / n_total
+        if mean is not None:
+            mean.copy_(shift + mu)
+        if anom is not None:
+            anom.copy_(((s - shift[:, None, :]) - mu[:, None, :]).reshape(anom.shape))
+
+    def gemm(self, A, B, C, *, trans_a=False, trans_b=False, alpha=1.0, beta=0.0, C0=None,
+             bias=None, bias_cols=1, tri=(0, 0), split=None, engine=0):
+        a = A.t() if trans_a else A
+        b = B.t() if trans_b else B
+        if a.shape[1] == 0:
+            prod = torch.zeros(C.shape, dtype=C.dtype)
+        else:
+            prod = alpha * (a @ b)
+        if C0 is not None:
+            prod = prod + beta * C0
+        if bias is not None:
+            reps = C.shape[1] // bias_cols
+            prod = prod + bias[:, :bias_cols].repeat(1, reps)
+        C.copy_(prod)
+
+    def spd_inverse(self, S, scale, inv, status, jitter):
+        sy = scale * 0.5 * (S + S.t())
+        p = sy.shape[0]
+        try:
+            L = torch.linalg.cholesky(sy)
+        except RuntimeError:
+            j = 1e-9 * float(torch.trace(sy)) / p + 1e-30
+            jitter += 1
+            L = torch.linalg.cholesky(sy + j * torch.eye(p, dtype=sy.dtype))
+        inv.copy_(torch.cholesky_inverse(L))
+
+    def spd_max_p(self):
+        return 1 << 30
+
+    def cnn_forward(self, cnn, x, u, out, n_members):
+        from oracle.models import cnn_step
+
+        n, m = x.shape[0], cnn.cols
+        xs = x.numpy().reshape(n, n_members, m).transpose(1, 0, 2)
+        us = u.numpy().reshape(n, n_members, m).transpose(1, 0, 2)
+        w = [np.asarray(v) for v in cnn.model.weights]
+        b = [np.asarray(v) for v in cnn.model.biases]
+        y = cnn_step(xs, us, w, b, cnn.alpha)
+        out.copy_(torch.from_numpy(np.ascontiguousarray(y.transpose(1, 0, 2).reshape(n, -1))))
+
+    def sub(self, a, b, out):
+        out.copy_(a - b)

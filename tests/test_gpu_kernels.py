@@ -1,0 +1,180 @@
+"""Kernel-level parity on the B200: every C-ABI entry point against its CPU oracle.
+
+Bars: bit-exact for the noise bitstream (fp32 rounding of numpy's fp64
+draws); fp32 tolerances (stated per test) for floating-point kernels.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _cpu(t):
+    return t.double().cpu().numpy()
+
+
+# ---------------------------------------------------------------- noise (K1+K2)
+@pytest.mark.parametrize("seed,prefix,t,ch,N,rows,cols", [
+    (0, (), 1, 0, 5, 2, 3),
+    (3, (), 2, 1, 37, 5, 7),
+    (12345, (7, 2), 4, 2, 16, 8, 33),
+    (2 ** 40 + 5, (1,), 0, 3, 9, 1, 1),
+])
+def test_noise_bit_exact_vs_numpy(dev_ops, seed, prefix, t, ch, N, rows, cols):
+    from oracle import noise as onoise
+    from paper_2410_09663_b200.matvar import entropy_head
+
+    ref = onoise.member_normals(seed, prefix, t, ch, N, (rows, cols), backend="numpy")
+    out = dev_ops.zeros(rows, N * cols)
+    dev_ops.noise_fill(entropy_head(seed, prefix), t, ch, 0, N, rows, cols, out=out)
+    got = out.cpu().numpy().reshape(rows, N, cols).transpose(1, 0, 2)
+    assert np.array_equal(got, ref.astype(np.float32))
+
+
+def test_noise_bit_exact_many_streams_with_tail(dev_ops):
+    """~270k normals: exercises the wedge (0.8%) and tail (0.02%) rejection paths."""
+    from oracle import noise as onoise
+    from paper_2410_09663_b200.matvar import entropy_head
+
+    N, rows, cols = 64, 64, 66
+    ref = onoise.member_normals(9, (), 5, 1, N, (rows, cols), backend="c")
+    assert np.abs(ref).max() > 3.6541528853610088  # at least one tail sample present
+    out = dev_ops.zeros(rows, N * cols)
+    dev_ops.noise_fill(entropy_head(9, ()), 5, 1, 0, N, rows, cols, out=out)
+    got = out.cpu().numpy().reshape(rows, N, cols).transpose(1, 0, 2)
+    assert np.array_equal(got, ref.astype(np.float32))
+
+
+def test_noise_member_offset_diag_and_base(dev_ops):
+    from oracle import noise as onoise
+    from paper_2410_09663_b200.matvar import entropy_head
+
+    N, rows, cols, m0 = 6, 4, 5, 11
+    diag = np.array([1.0, 2.0, 0.5, 3.0])
+    ref = onoise.member_normals(1, (), 3, 2, m0 + N, (rows, cols), backend="c")[m0:]
+    col = (diag[None, :, None] * ref).astype(np.float32)
+    base = torch.randn(rows, N * cols, device=dev_ops.device)
+    out = dev_ops.zeros(rows, N * cols)
+    plus = dev_ops.zeros(rows, N * cols)
+    dev_ops.noise_fill(entropy_head(1, ()), 3, 2, m0, N, rows, cols,
+                       diag=dev_ops.to_device(diag, dtype=torch.float64), out=out, base=base,
+                       out_plus=plus)
+    got = out.cpu().numpy().reshape(rows, N, cols).transpose(1, 0, 2)
+    assert np.array_equal(got, col)
+    exp_plus = base.cpu().numpy() + col.transpose(1, 0, 2).reshape(rows, -1)
+    assert np.array_equal(plus.cpu().numpy(), exp_plus.astype(np.float32))
+
+
+# ---------------------------------------------------------------- member statistics (K4/K5)
+@pytest.mark.parametrize("rows,N,cols", [(3, 4, 5), (40, 100, 32), (7, 1000, 3)])
+def test_member_stats(dev_ops, rows, N, cols):
+    rng = np.random.default_rng(rows)
+    x = rng.standard_normal((rows, N, cols)).astype(np.float32) + 3.0
+    src = dev_ops.to_device(x.reshape(rows, -1))
+    acc = dev_ops.zeros(rows, cols, dtype=torch.float64)
+    dev_ops.member_sum(src, N, cols, None, acc)
+    mean = dev_ops.zeros(rows, cols)
+    anom = dev_ops.zeros(rows, N * cols)
+    dev_ops.member_center(src, N, cols, None, acc, N, mean=mean, anom=anom)
+    x64 = x.astype(np.float64)
+    np.testing.assert_allclose(_cpu(mean), x64.mean(axis=1), rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(_cpu(anom).reshape(rows, N, cols), x64 - x64.mean(axis=1, keepdims=True),
+                               rtol=1e-5, atol=1e-5)
+
+
+def test_member_stats_identical_members_exact_zero(dev_ops):
+    """Shift by member 0: identical members give exactly zero anomalies at any N."""
+    rng = np.random.default_rng(0)
+    one = rng.standard_normal((6, 1, 7)).astype(np.float32)
+    x = np.repeat(one, 100, axis=1)
+    src = dev_ops.to_device(x.reshape(6, -1))
+    acc = dev_ops.zeros(6, 7, dtype=torch.float64)
+    dev_ops.member_sum(src, 100, 7, None, acc)
+    mean, anom = dev_ops.zeros(6, 7), dev_ops.zeros(6, 700)
+    dev_ops.member_center(src, 100, 7, None, acc, 100, mean=mean, anom=anom)
+    assert np.array_equal(mean.cpu().numpy(), one[:, 0, :])
+    assert not anom.cpu().numpy().any()
+
+
+# ---------------------------------------------------------------- GEMM
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("M,N,K,split", [(5, 7, 3, 1), (130, 257, 300, 1), (300, 140, 5000, 7),
+                                         (64, 64, 0, 1)])
+def test_gemm_simt(dev_ops, ta, tb, M, N, K, split):
+    g = torch.Generator().manual_seed(M * 7 + N)
+    A = torch.randn(K, M, generator=g) if ta else torch.randn(M, K, generator=g)
+    B = torch.randn(N, K, generator=g) if tb else torch.randn(K, N, generator=g)
+    C0 = torch.randn(M, N, generator=g)
+    bias = torch.randn(M, 4, generator=g)
+    C = dev_ops.zeros(M, N)
+    dev_ops.gemm(A.to(dev_ops.device), B.to(dev_ops.device), C, trans_a=ta, trans_b=tb,
+                 alpha=0.7, beta=-1.5, C0=C0.to(dev_ops.device), bias=bias.to(dev_ops.device),
+                 bias_cols=4, split=split, engine=1)
+    exp = 0.7 * ((A.t() if ta else A).double() @ (B.t() if tb else B).double()) - 1.5 * C0.double()
+    exp = exp + bias.double()[:, [c % 4 for c in range(N)]]
+    err = (C.double().cpu() - exp).abs().max().item()
+    assert err <= 2e-6 * max(1.0, K ** 0.5) * 10, err
+
+
+def test_gemm_triangular_skip(dev_ops):
+    """tri_rows/tri_k: rows of block s start at k = s * tri_k (block upper-triangular A)."""
+    d, p, S = 6, 4, 5
+    A = torch.randn(S * d, S * p)
+    for s in range(S):
+        A[s * d:(s + 1) * d, :s * p] = 0.0
+    B = torch.randn(S * p, 9)
+    C = dev_ops.zeros(S * d, 9)
+    dev_ops.gemm(A.to(dev_ops.device), B.to(dev_ops.device), C, tri=(d, p), engine=1)
+    np.testing.assert_allclose(C.double().cpu().numpy(), (A.double() @ B.double()).numpy(),
+                               rtol=1e-5, atol=1e-5)
+
+
+# ---------------------------------------------------------------- gain solve (K8)
+@pytest.mark.parametrize("p", [1, 6, 64, 256])
+def test_spd_inverse(dev_ops, p):
+    rng = np.random.default_rng(p)
+    a = rng.standard_normal((p, p + 3))
+    s = (a @ a.T / (p + 3) + 0.5 * np.eye(p)).astype(np.float32)
+    s[0, -1] += 1e-3  # asymmetry is symmetrized away
+    inv = dev_ops.zeros(p, p)
+    st, jit = dev_ops.zeros(1, dtype=torch.int32), dev_ops.zeros(1, dtype=torch.int32)
+    dev_ops.spd_inverse(dev_ops.to_device(s), 2.0, inv, st, jit)
+    sym = 2.0 * 0.5 * (s.astype(np.float64) + s.T.astype(np.float64))
+    ref = np.linalg.inv(sym)
+    assert st.item() == 0 and jit.item() == 0
+    np.testing.assert_allclose(_cpu(inv), ref, rtol=2e-4, atol=2e-4 * np.abs(ref).max())
+
+
+def test_spd_inverse_jitter_and_failure(dev_ops):
+    p = 5
+    st, jit = dev_ops.zeros(1, dtype=torch.int32), dev_ops.zeros(1, dtype=torch.int32)
+    inv = dev_ops.zeros(p, p)
+    # zero matrix -> jitter 1e-30 -> inverse 1e30 I (the reference's degenerate path)
+    dev_ops.spd_inverse(dev_ops.zeros(p, p), 1.0, inv, st, jit)
+    assert st.item() == 0 and jit.item() == 1
+    np.testing.assert_allclose(_cpu(inv), 1e30 * np.eye(p), rtol=1e-5)
+    # indefinite even after jitter -> status 1 (reference raises LinAlgError)
+    bad = -np.eye(p, dtype=np.float32)
+    dev_ops.spd_inverse(dev_ops.to_device(bad), 1.0, inv, st, jit)
+    assert st.item() == 1 and jit.item() == 2
+
+
+# ---------------------------------------------------------------- CNN forecast (K3)
+@pytest.mark.parametrize("n,widths,N", [(16, (2, 8, 1), 3), (32, (2, 16, 16, 1), 5),
+                                        (40, (2, 32, 32, 1), 2), (128, (2, 32, 32, 1), 2)])
+def test_cnn_forward(dev_ops, pm, n, widths, N):
+    from oracle.models import cnn_step
+    from paper_2410_09663_b200.engine import Forecaster
+
+    model = pm.dynamics.CNNDynamics(rows=n, cols=n, widths=widths, seed=1)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((N, n, n))
+    u = rng.standard_normal((N, n, n))
+    ref = cnn_step(x, u, model.weights, model.biases, model.alpha)
+    last = dev_ops.to_device(np.concatenate([x, u], axis=1).transpose(1, 0, 2).reshape(2 * n, -1))
+    out = dev_ops.zeros(n, N * n)
+    fc = Forecaster(model, dev_ops, n, n)
+    fc(dev_ops, last, out, n, N)
+    got = _cpu(out).reshape(n, N, n).transpose(1, 0, 2)
+    np.testing.assert_allclose(got, ref, rtol=1e-5, atol=2e-6)

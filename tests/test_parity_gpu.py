@@ -1,0 +1,139 @@
+"""End-to-end parity of the device smoother with the fp64 CPU oracle.
+
+Tolerance (north_star): relative error <= 1e-4 on the smoothed state/control
+means (max |dev - ref| / max |ref|), and on tracked covariances; noise is
+bit-identical, so the only differences are fp32 rounding.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def _rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-30))
+
+
+def _linear_case(pm, seed, **kw):
+    from oracle import problems
+
+    return problems.make_linear_setup(pm, np.random.default_rng(seed), **kw)
+
+
+@pytest.mark.parametrize("seed,kw,N,h", [
+    (0, dict(n=4, l=2, m=3), 16, 5),
+    (1, dict(n=8, l=4, m=8, identity_weights=True), 32, 6),
+    (2, dict(n=16, l=8, m=16), 64, 10),
+    (3, dict(n=4, l=1, m=1), 8, 3),
+    (4, dict(n=32, l=32, m=32, identity_weights=True), 100, 8),
+])
+def test_smooth_horizon_linear_matches_oracle(pm, seed, kw, N, h):
+    from oracle import enks_oracle
+    from paper_2410_09663_b200 import enks
+
+    _, vs, x0 = _linear_case(pm, seed, **kw)
+    y = vs.reference_observation()
+    ref, _, oens = enks_oracle.oracle_smooth(x0, y, vs, h, N, seed=seed + 10, backend="c")
+    got, cov = enks.smooth_horizon(x0, y, vs, h, N, pm.matvar.NoiseStreams(seed=seed + 10))
+    assert cov is None
+    assert got.shape == ref.shape
+    assert _rel(got, ref) < TOL
+
+
+def test_smooth_horizon_cnn_c1_matches_oracle(pm):
+    """C1b: CNN 2-16-16-1 on a 32x32 field, N=100, H=5."""
+    from oracle import enks_oracle, problems
+    from oracle.models import OracleCNN
+
+    from paper_2410_09663_b200 import enks
+
+    pr = problems.make_cnn_problem(pm, "C1")
+    ovs = pm.virtualsys.build_virtual_system(OracleCNN(pr.model), pr.vs.weights)
+    ref, _, _ = enks_oracle.oracle_smooth(pr.x0, pr.y_ref, ovs, pr.H, pr.N, seed=0, backend="c")
+    got, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N,
+                                 pm.matvar.NoiseStreams(seed=0))
+    n, l = pr.n, pr.l
+    assert _rel(got, ref) < TOL
+    assert _rel(got[:, n:n + l], ref[:, n:n + l]) < TOL  # control block on its own
+
+
+def test_track_cov_matches_oracle(pm):
+    from oracle import enks_oracle
+    from paper_2410_09663_b200 import enks
+
+    _, vs, x0 = _linear_case(pm, 16)
+    y = vs.reference_observation()
+    ref, rcov, _ = enks_oracle.oracle_smooth(x0, y, vs, 5, 16, seed=11, track_cov=True,
+                                             backend="c")
+    got, cov = enks.smooth_horizon(x0, y, vs, 5, 16, pm.matvar.NoiseStreams(seed=11),
+                                   track_cov=True)
+    assert _rel(got, ref) < TOL
+    assert cov.sigma_traj.shape == rcov.sigma_traj.shape
+    assert _rel(cov.sigma_traj, rcov.sigma_traj) < TOL
+    assert _rel(cov.sigma_cross, rcov.sigma_cross) < TOL
+    assert _rel(cov.sigma_pred, rcov.sigma_pred) < TOL
+
+
+def test_members_and_predict_update_api(pm):
+    """Bare predict/update (capacity growth) and lazily materialised members."""
+    from oracle import enks_oracle
+    from paper_2410_09663_b200 import enks
+
+    _, vs, x0 = _linear_case(pm, 8)
+    y = vs.reference_observation()
+    ens = enks.init_ensemble(x0, 12, capacity=1)
+    o = enks_oracle.oracle_init(x0.packed, x0.n, x0.l, 12)
+    st = pm.matvar.NoiseStreams(seed=5)
+    for _ in range(4):
+        enks.predict(ens, vs, st)
+        enks_oracle.oracle_predict(o, vs, 5, backend="c")
+        assert ens.members.shape == o.members.shape
+        assert _rel(ens.members, o.members) < TOL
+        enks.update(ens, y, vs, st)
+        enks_oracle.oracle_update(o, y, vs, 5, backend="c")
+        assert _rel(ens.members, o.members) < TOL
+        assert _rel(ens.mean, o.mean) < TOL
+        assert np.abs(ens.mean - ens.members.mean(axis=0)).max() < 1e-5 * np.abs(o.mean).max()
+    assert ens.t == 4 and ens.jitter_events == 0
+
+
+def test_degenerate_noise_exact(pm):
+    """scale=0: members identical, G = 0 through the 1e-30 jitter path (test_enks.py:244-251)."""
+    from paper_2410_09663_b200 import enks
+
+    model, vs, x0 = _linear_case(pm, 14, scale=0.0)
+    y = np.vstack([vs.weights.x_ref, vs.weights.u_ref])
+    traj, _ = enks.smooth_horizon(x0, y, vs, 1, 4, pm.matvar.NoiseStreams(seed=9))
+    assert np.allclose(traj[0], x0.packed)
+    expected = np.vstack([model.step(x0.x, x0.u), x0.u, np.zeros_like(x0.u)])
+    assert np.allclose(traj[1], expected, atol=1e-6)
+    # non-power-of-two N as well: the member-0 shift keeps the spread exactly zero
+    traj, _ = enks.smooth_horizon(x0, y, vs, 3, 12, pm.matvar.NoiseStreams(seed=9))
+    ens_ref = x0.packed
+    for t in range(1, 4):
+        ens_ref = np.vstack([model.step(ens_ref[:x0.n], ens_ref[x0.n:x0.n + x0.l]),
+                             ens_ref[x0.n:x0.n + x0.l], np.zeros_like(x0.u)])
+        assert np.allclose(traj[t], ens_ref, atol=1e-5)
+
+
+def test_same_streams_bit_identical(pm):
+    from paper_2410_09663_b200 import enks
+
+    _, vs, x0 = _linear_case(pm, 17)
+    y = vs.reference_observation()
+    a, _ = enks.smooth_horizon(x0, y, vs, 3, 64, pm.matvar.NoiseStreams(seed=12))
+    b, _ = enks.smooth_horizon(x0, y, vs, 3, 64, pm.matvar.NoiseStreams(seed=12))
+    assert np.array_equal(a, b)
+
+
+def test_lambda_cancellation(pm):
+    from paper_2410_09663_b200 import enks
+
+    model, vs, x0 = _linear_case(pm, 7)
+    vs7 = pm.virtualsys.build_virtual_system(model, vs.weights, shared_col_cov=7.0 * np.eye(x0.m))
+    y = vs.reference_observation()
+    a, _ = enks.smooth_horizon(x0, y, vs, 3, 16, pm.matvar.NoiseStreams(seed=4))
+    b, _ = enks.smooth_horizon(x0, y, vs7, 3, 16, pm.matvar.NoiseStreams(seed=4))
+    assert _rel(a, b) < 1e-5
