@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: OIC horizon solves/sec (and member-CNN-steps/sec) of the B200 EnKS.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+One bench "step" = one complete OIC horizon solve (reference enks.py:256-284
+smooth_horizon: init + H x (predict, update)) of the configured problem
+(default C3: 128x128 field, CNN 2-32-32-1, N=1024 members,
+H=50), synthetic inputs, random-init CNN.
+
+  value : horizons/s with inputs resident in HBM, CUDA-event timed (max over ranks)
+  e2e   : the same metric through the public API enks.smooth_horizon with host
+          (NumPy) inputs and a host result each step
+  roofline : the dominant kernel (the cross-moment contraction P = [A; Yc] Yc^T)
+          algorithmic FLOPs / its CUDA-event-measured launch time vs MEASURED_PEAKS.json
+  cpu_baseline : the fp64 oracle port timed on this host on a bounded sample
+          (rank 0, N=1 only), horizon time extrapolated from per-step times
+
+N > 1 (torchrun): members sharded over ranks, NCCL allreduce of the covariance
+partials; strong scaling of one horizon.  --impl reference times the CPU
+oracle port (the reference is pure Python and cannot travel to the box).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--members", type=int, default=None)
+    ap.add_argument("--horizon", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _problem(config: str, members, horizon):
+    from oracle import problems  # builder of synthetic inputs (shapes per SURVEY.md §8d)
+
+    pm = problems.product_modules()
+    return pm, problems.make_cnn_problem(pm, config, n_members=members, horizon=horizon)
+
+
+def _algorithmic(pr):
+    n, l, m, N, H = pr.n, pr.l, pr.m, pr.N, pr.H
+    d, p, K = n + 2 * l, n + l, N * m
+    cnn_flops = N * H * pr.model.flops_per_member_step()
+    # P = [A_1..A_tau; Yc_1..Yc_tau] Yc_tau^T per step
+    cross = sum(2 * tau * (d + p) * p * K for tau in range(1, H + 1))
+    enks_ref = sum(2 * p * p * K + 4 * (t + 1) * d * p * K + p ** 3 / 3 + 2 * p * p * (t + 1) * d
+                   for t in range(1, H + 1))
+    return dict(cnn_tflop=cnn_flops / 1e12, cross_tflop=cross / 1e12, enks_ref_tflop=enks_ref / 1e12)
+
+
+# ---------------------------------------------------------------------- CPU oracle sampling
+def cpu_sample(pr, t_values, threads=None):
+    """Time oracle predict+update steps at trajectory lengths t_values; fit a + b*T.
+
+    Steps are run on synthetic ensembles of the right shape (members = x0 copies
+    plus noise), so a step at T costs exactly what the reference pays there.
+    Returns (horizon_seconds, samples, cores).
+    """
+    import torch
+
+    from oracle import enks_oracle
+
+    cores = threads or os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    vs, x0, N, H = pr.vs, pr.x0, pr.N, pr.H
+    d = x0.n + 2 * x0.l
+    rng = np.random.default_rng(0)
+    samples = []
+    for T in t_values:
+        ens = enks_oracle.oracle_init(x0.packed, x0.n, x0.l, N, shared_col_cov=vs.shared_col_cov)
+        if T > 1:
+            extra = x0.packed[None, None] + 0.1 * rng.standard_normal((N, T - 1, d, x0.m))
+            ens.members = np.concatenate([ens.members, extra.reshape(N, (T - 1) * d, x0.m)], axis=1)
+            ens.t = T - 1
+            ens.mean = ens.members.mean(axis=0)
+        t0 = time.perf_counter()
+        enks_oracle.oracle_predict(ens, vs, 0)
+        enks_oracle.oracle_update(ens, pr.y_ref, vs, 0)
+        samples.append((T, time.perf_counter() - t0))
+        del ens
+    Ts = np.array([s[0] for s in samples], float)
+    ys = np.array([s[1] for s in samples], float)
+    if len(set(Ts)) >= 2:
+        b, a = np.polyfit(Ts, ys, 1)
+        b = max(b, 0.0)
+        a = max(a, float(ys.min()) - b * Ts[np.argmin(ys)])
+    else:
+        a, b = float(ys.mean()), 0.0
+    horizon = sum(a + b * T for T in range(1, H + 1))
+    return horizon, samples, cores
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle port of the reference path, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    pm, pr = _problem(args.config, args.members, args.horizon)
+    ts = [1, 3, 5, 7]
+    per_step = []
+    all_samples = []
+    for k in range(args.warmup + args.steps):
+        T = ts[k % len(ts)]
+        _, samples, cores = cpu_sample(pr, [T])
+        if k >= args.warmup:
+            all_samples.extend(samples)
+            per_step.append(samples[0][1])
+    Ts = np.array([s[0] for s in all_samples], float)
+    ys = np.array([s[1] for s in all_samples], float)
+    b, a = np.polyfit(Ts, ys, 1) if len(set(Ts)) >= 2 else (0.0, float(ys.mean()))
+    b = max(b, 0.0)
+    horizon = sum(a + b * T for T in range(1, pr.H + 1))
+    value = 1.0 / horizon
+    line = {
+        "impl": "reference", "metric": "OIC horizon solves/sec", "value": value,
+        "unit": "horizons/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": horizon * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config(pr, args),
+        "member_cnn_steps_per_s": pr.N * pr.H * value,
+        "cpu_baseline": {"value": value, "unit": "horizons/s", "cores": os.cpu_count(),
+                         "kind": "port",
+                         "sample": f"fp64 oracle port (oracle/enks_oracle.py, torch-CPU fp64 CNN) "
+                                   f"predict+update steps at T={[int(t) for t in Ts]} of "
+                                   f"{args.config} (N={pr.N}); horizon = sum_T (a + b T), "
+                                   f"a={a:.3f}s b={b:.3f}s"},
+        "e2e": {"value": value, "unit": "horizons/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def _config(pr, args):
+    return {"workload": f"{args.config}: OIC horizon solve, {pr.n}x{pr.m} field, "
+                        f"CNN {'-'.join(map(str, pr.widths))}, N={pr.N} members, H={pr.H}",
+            "n": pr.n, "m": pr.m, "l": pr.l, "members": pr.N, "horizon": pr.H,
+            "cnn_widths": list(pr.widths), "parallelism": f"members sharded x{args.gpus}",
+            "l2": "inputs larger than L2 (append-only basis >> 126 MB at C2/C3)"}
+
+
+# ---------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2410_09663_b200.engine import TorchComm
+
+        comm = TorchComm()
+    from paper_2410_09663_b200 import build, enks
+
+    build.build()
+    pm, pr = _problem(args.config, args.members, args.horizon)
+    ops = enks._ops()
+    if comm is not None:
+        enks.set_default_comm(comm)
+    streams = pm.matvar.NoiseStreams(seed=0)
+    h = pr.H
+    yref_dev = ops.to_device(np.broadcast_to(pr.y_ref, (h,) + pr.y_ref.shape).copy())
+
+    def one_step():
+        return enks.smooth_horizon_device(pr.x0, yref_dev, pr.vs, h, pr.N, streams, comm=comm)
+
+    for _ in range(args.warmup):
+        eng = one_step()
+        del eng
+    torch.cuda.synchronize()
+    if comm is not None:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ops.launches
+    ops.profile = []
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record()
+    for _ in range(args.steps):
+        eng = one_step()
+        del eng
+    stop.record()
+    torch.cuda.synchronize()
+    prof, ops.profile = ops.profile, None
+    clk = clocks.stop()
+    launches = (ops.launches - launches0) // max(args.steps, 1)
+    elapsed = start.elapsed_time(stop) / 1e3
+    cross = [(s, e, f) for tag, s, e, f in prof if tag == "cross"]
+    kern_s = sum(s.elapsed_time(e) for s, e, _ in cross) / 1e3
+    kern_flops = sum(f for _, _, f in cross)
+    n_kern = len(cross)
+    if comm is not None:
+        t = torch.tensor([elapsed, kern_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed, kern_s = float(t[0]), float(t[1])
+    value = args.steps / elapsed
+
+    # e2e through the public API with host inputs and a host result each step
+    e2e = None
+    if not args.no_e2e:
+        ebytes_in = (pr.x0.packed.size + h * pr.y_ref.size) * 8
+        for _ in range(1):
+            enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, h, pr.N, streams)
+        torch.cuda.synchronize()
+        if comm is not None:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = None
+        for _ in range(args.steps):
+            y_host = np.broadcast_to(pr.y_ref, (h,) + pr.y_ref.shape)
+            out, _ = enks.smooth_horizon(pr.x0, y_host, pr.vs, h, pr.N, streams)
+        e.record()
+        torch.cuda.synchronize()
+        e2e_s = s.elapsed_time(e) / 1e3
+        if comm is not None:
+            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        cnn_bytes = sum(np.asarray(w).size for w in pr.model.weights) * 4 + \
+            sum(np.asarray(b).size for b in pr.model.biases) * 4
+        e2e = {"value": args.steps / e2e_s, "unit": "horizons/s",
+               "h2d_bytes_per_step": int(ebytes_in // 2 + cnn_bytes + 3 * pr.n * 8),
+               "d2h_bytes_per_step": int(out.size * 4 + 4)}
+
+    peaks, peak_kind = _peaks()
+    alg = _algorithmic(pr)
+    achieved = (kern_flops / max(kern_s, 1e-12)) / 1e12
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    roofline = {
+        "kernel": "cross-moment contraction P=[A;Yc]Yc^T (enks_gemm NT, split-K + fixed-order reduce)",
+        "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak, "traffic": None,
+        "peak_source": f"{peak_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+        "launches_timed": n_kern, "kernel_share_of_step": kern_s / elapsed,
+        "algorithmic_tflop_per_horizon": alg["cross_tflop"],
+    }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        horizon_s, samples, cores = cpu_sample(pr, [1, 4])
+        cpu = {"value": 1.0 / horizon_s, "unit": "horizons/s", "cores": cores, "kind": "port",
+               "sample": f"fp64 oracle port predict+update at T={[s[0] for s in samples]} "
+                         f"({[round(s[1], 2) for s in samples]} s) of {args.config}, "
+                         f"horizon extrapolated as sum_T (a + b T)"}
+
+    if rank == 0:
+        line = {
+            "metric": "OIC horizon solves/sec", "value": value, "unit": "horizons/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (sine-field x0, random-init CNN, bit-exact numpy noise streams)",
+            "config": _config(pr, args),
+            "member_cnn_steps_per_s": pr.N * h * value,
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
+            "cpu_baseline": cpu, "clocks": clk,
+            "algorithmic": alg,
+        }
+        print(json.dumps(line))
+    if comm is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

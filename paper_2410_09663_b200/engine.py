@@ -301,8 +301,8 @@ class DeviceSmoother:
         a0 = d if self.slice0_zero else 0
         rows_a = (tau + 1) * d
         PA, PY = self.PA[a0:rows_a], self.PY[:tau * p]
-        ops.gemm(self.Abuf[a0:rows_a], yc, PA, trans_b=True)
-        ops.gemm(self.Ybuf[:tau * p], yc, PY, trans_b=True)
+        ops.gemm(self.Abuf[a0:rows_a], yc, PA, trans_b=True, tag="cross")
+        ops.gemm(self.Ybuf[:tau * p], yc, PY, trans_b=True, tag="cross")
         comm.allreduce_(PA)
         comm.allreduce_(PY)
 

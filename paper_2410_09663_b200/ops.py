@@ -52,7 +52,8 @@ class DeviceOps:
                                    else torch.device(device).index or 0)
         self._ws = None
         self._ws_sum = None
-        self.launches = 0  # kernel-entry calls issued (for the bench's gpu_launches claim)
+        self.launches = 0  # kernel launches issued through the C-ABI (bench's gpu_launches)
+        self.profile = None  # list -> (tag, start_event, end_event, algorithmic_flops) per tagged op
 
     # -- memory -----------------------------------------------------------
     def empty(self, *shape, dtype=None):
@@ -108,7 +109,7 @@ class DeviceOps:
                   _ld(anom) if anom is not None else 0, self._stream())
 
     def gemm(self, A, B, C, *, trans_a=False, trans_b=False, alpha=1.0, beta=0.0, C0=None,
-             bias=None, bias_cols=1, tri=(0, 0), split=None, engine=0):
+             bias=None, bias_cols=1, tri=(0, 0), split=None, engine=0, tag=None):
         M, N = C.shape
         K = A.shape[0] if trans_a else A.shape[1]
         if (B.shape[1] if trans_b else B.shape[0]) != K:
@@ -119,11 +120,19 @@ class DeviceOps:
             split = choose_split(M, N, K)
         ws = self._workspace(self.lib.enks_gemm_ws_bytes(M, N, split)) if split > 1 else None
         self.launches += 2 if split > 1 else 1
+        prof = self.profile is not None and tag is not None
+        if prof:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
         _lib.call("enks_gemm", int(trans_a), int(trans_b), M, N, K, float(alpha),
                   _p(A) if K else None, _ld(A) if K else 0, _p(B) if K else None,
                   _ld(B) if K else 0, float(beta), _p(C0), _ld(C0) if C0 is not None else 0,
                   _p(bias), _ld(bias) if bias is not None else 0, int(bias_cols), _p(C), _ld(C),
                   int(tri[0]), int(tri[1]), int(split), ws, int(engine), self._stream())
+        if prof:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record()
+            self.profile.append((tag, ev0, ev1, 2.0 * M * N * K))
 
     def spd_inverse(self, S, scale, inv, status, jitter):
         p = S.shape[0]

@@ -69,7 +69,7 @@ class CpuOps:
             anom.copy_(((s - shift[:, None, :]) - mu[:, None, :]).reshape(anom.shape))
 
     def gemm(self, A, B, C, *, trans_a=False, trans_b=False, alpha=1.0, beta=0.0, C0=None,
-             bias=None, bias_cols=1, tri=(0, 0), split=None, engine=0):
+             bias=None, bias_cols=1, tri=(0, 0), split=None, engine=0, tag=None):
         a = A.t() if trans_a else A
         b = B.t() if trans_b else B
         if a.shape[1] == 0:
