@@ -94,7 +94,8 @@ int enks_member_center(const float* src, int64_t ld_src, int rows, int64_t n_mem
  * split_k > 1 requires ws of enks_gemm_ws_bytes(M, N, split_k) bytes and is
  * reduced deterministically (fixed order).  Replaces numpy `@` / OpenBLAS
  * dgemm at enks.py:153, 247 and matvar.py:188.
- * `engine`: 0 = auto, 1 = SIMT fp32 FFMA, 2 = tcgen05 3xTF32 (NT only).
+ * `engine`: 0/1 = SIMT fp32 FFMA; 2 = tcgen05 3xTF32 (trans_a=0, trans_b=1, N <= 256,
+ * no bias/tri; `ws` must then hold enks_tc_gemm_ws_bytes(M, N, K, split_k) bytes).
  */
 int64_t enks_gemm_ws_bytes(int64_t M, int64_t N, int split_k);
 int enks_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, float alpha,
@@ -102,6 +103,20 @@ int enks_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, float a
               const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias, int bias_cols,
               float* C, int64_t ldc, int64_t tri_rows, int64_t tri_k, int split_k, void* ws,
               int engine, void* stream);
+
+/*
+ * tcgen05 3xTF32 contraction with a pre-split B operand (the cross moments
+ * P = [A; Yc] Yc^T of the append-only basis; enks.py:234-236):
+ *   C[M x N] = alpha * A B^T,  B = Bh + Bl with Bh = rna_tf32(B) (enks_tf32_split).
+ * Splitting B once per step lets both basis segments reuse it.  `ws` holds
+ * split_k * M * N floats of deterministic split-K partials (split_k <= 0: auto).
+ */
+int64_t enks_tc_gemm_ws_bytes(int64_t M, int64_t N, int64_t K, int split_k);
+int enks_tf32_split(const float* src, int64_t ld, int64_t rows, int64_t cols, float* hi, float* lo,
+                    void* stream);
+int enks_gemm_nt_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
+                    const float* Bh, const float* Bl, int64_t ldb, float* C, int64_t ldc,
+                    int split_k, void* ws, void* stream);
 
 /*
  * Gain solve (K8).  Replaces enks.py:234-235 (symmetrize) and 238-246

@@ -230,11 +230,11 @@ int enks_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, float a
     ENKS_REQUIRE(split_k <= 1 || ws, "enks_gemm: split_k > 1 needs workspace");
     ENKS_REQUIRE(split_k <= 1024, "enks_gemm: split_k too large");
     cudaStream_t st = enks::as_stream(stream);
-    if (engine == 2 || (engine == 0 && enks::tc_gemm_applicable(trans_a, trans_b, M, N, K, A, lda, B,
-                                                                 ldb, tri_rows))) {
-        int rc = enks::gemm_tc(M, N, K, alpha, A, lda, B, ldb, beta, C0, ldc0, bias, ld_bias,
-                               bias_cols, C, ldc, split_k, ws, st);
-        if (rc != ENKS_E_UNSUPPORTED || engine == 2) return rc;
+    if (engine == 2) {
+        ENKS_REQUIRE(enks::tc_gemm_applicable(trans_a, trans_b, M, N, K, A, lda, B, ldb, tri_rows),
+                     "enks_gemm: tcgen05 engine needs NT, N<=256, K>=128, 16B-aligned operands");
+        return enks::gemm_tc(M, N, K, alpha, A, lda, B, ldb, beta, C0, ldc0, bias, ld_bias,
+                             bias_cols, C, ldc, split_k, ws, st);
     }
     return enks::gemm_simt(trans_a, trans_b, M, N, K, alpha, A, lda, B, ldb, beta, C0, ldc0, bias,
                            ld_bias, bias_cols, C, ldc, tri_rows, tri_k, split_k, ws, st);

@@ -41,6 +41,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import torch
 
@@ -170,6 +172,12 @@ class DeviceSmoother:
         self.slice0_zero = True  # all members start as identical copies (enks.py:120)
         self._bound = None
         d, p, K, m = self.d, self.p, self.K, self.m
+        # tcgen05 3xTF32 cross moments (ENKS_TC=0 forces the SIMT engine for A/B checks)
+        self.use_tc = (os.environ.get("ENKS_TC", "1") != "0" and hasattr(ops, "gemm_nt_tc")
+                       and p <= 256 and K >= 128)
+        if self.use_tc:
+            self.yc_hi = ops.empty(p, K)
+            self.yc_lo = ops.empty(p, K)
         self.slice_raw = ops.empty(d, K)      # [X; U; W] of the newest predicted slice
         self.obs_raw = ops.empty(p, K)        # perturbed observations of the newest slice
         self.last = ops.empty(p, K)           # materialised [x; u] of the newest updated slice
@@ -301,8 +309,13 @@ class DeviceSmoother:
         a0 = d if self.slice0_zero else 0
         rows_a = (tau + 1) * d
         PA, PY = self.PA[a0:rows_a], self.PY[:tau * p]
-        ops.gemm(self.Abuf[a0:rows_a], yc, PA, trans_b=True, tag="cross")
-        ops.gemm(self.Ybuf[:tau * p], yc, PY, trans_b=True, tag="cross")
+        if self.use_tc:
+            ops.tf32_split(yc, self.yc_hi, self.yc_lo)
+            ops.gemm_nt_tc(self.Abuf[a0:rows_a], self.yc_hi, self.yc_lo, PA, tag="cross")
+            ops.gemm_nt_tc(self.Ybuf[:tau * p], self.yc_hi, self.yc_lo, PY, tag="cross")
+        else:
+            ops.gemm(self.Abuf[a0:rows_a], yc, PA, trans_b=True, tag="cross")
+            ops.gemm(self.Ybuf[:tau * p], yc, PY, trans_b=True, tag="cross")
         comm.allreduce_(PA)
         comm.allreduce_(PY)
 

@@ -134,6 +134,37 @@ class DeviceOps:
             ev1.record()
             self.profile.append((tag, ev0, ev1, 2.0 * M * N * K))
 
+    def tc_applicable(self, A, Bh) -> bool:
+        """tcgen05 3xTF32 path: N <= 256, K >= 128, 16-B aligned rows."""
+        K = A.shape[1]
+        return (Bh.shape[0] <= 256 and K >= 128 and _ld(A) % 4 == 0 and _ld(Bh) % 4 == 0
+                and A.data_ptr() % 16 == 0 and Bh.data_ptr() % 16 == 0)
+
+    def tf32_split(self, src, hi, lo):
+        """hi = rna_tf32(src), lo = src - hi (the B operand of the 3xTF32 contraction)."""
+        self.launches += 1
+        _lib.call("enks_tf32_split", _p(src), _ld(src), src.shape[0], src.shape[1], _p(hi), _p(lo),
+                  self._stream())
+
+    def gemm_nt_tc(self, A, Bh, Bl, C, *, alpha=1.0, split=0, tag=None):
+        """C = alpha * A (Bh + Bl)^T on tcgen05 (3xTF32), deterministic split-K."""
+        M, K = A.shape
+        N = Bh.shape[0]
+        if M == 0 or N == 0:
+            return
+        ws = self._workspace(self.lib.enks_tc_gemm_ws_bytes(M, N, K, int(split)))
+        self.launches += 2
+        prof = self.profile is not None and tag is not None
+        if prof:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+        _lib.call("enks_gemm_nt_tc", M, N, K, float(alpha), _p(A), _ld(A), _p(Bh), _p(Bl), _ld(Bh),
+                  _p(C), _ld(C), int(split), ws, self._stream())
+        if prof:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record()
+            self.profile.append((tag, ev0, ev1, 2.0 * M * N * K))
+
     def spd_inverse(self, S, scale, inv, status, jitter):
         p = S.shape[0]
         self.launches += 1

@@ -178,3 +178,29 @@ def test_cnn_forward(dev_ops, pm, n, widths, N):
     fc(dev_ops, last, out, n, N)
     got = _cpu(out).reshape(n, N, n).transpose(1, 0, 2)
     np.testing.assert_allclose(got, ref, rtol=1e-5, atol=2e-6)
+
+
+# ---------------------------------------------------------------- tcgen05 3xTF32 contraction
+@pytest.mark.parametrize("M,N,K,split", [(128, 256, 4096, 1), (300, 256, 131072, 0), (77, 6, 1000, 0),
+                                         (1000, 100, 20000, 3), (640, 256, 131072, 0),
+                                         (5, 32, 128, 1)])
+def test_gemm_nt_tc_3xtf32(dev_ops, M, N, K, split):
+    """Within fp32-FFMA accuracy of the fp64 product (1xTF32 would be ~1e-3 relative)."""
+    g = torch.Generator().manual_seed(M + N + K)
+    A = torch.randn(M, K, generator=g) + 0.5
+    B = torch.randn(N, K, generator=g)
+    dA, dB = A.to(dev_ops.device), B.to(dev_ops.device)
+    bh, bl = dev_ops.empty(N, K), dev_ops.empty(N, K)
+    dev_ops.tf32_split(dB, bh, bl)
+    assert torch.equal((bh + bl).cpu(), B)
+    C = dev_ops.zeros(M, N)
+    dev_ops.gemm_nt_tc(dA, bh, bl, C, alpha=0.5, split=split)
+    ref = 0.5 * (A.double() @ B.double().t())
+    scale = 0.5 * (A.double().abs() @ B.double().abs().t())
+    err = ((C.double().cpu() - ref).abs() / scale).max().item()
+    # the SIMT FFMA engine on the same inputs: the fp32-accumulation error to match
+    C2 = dev_ops.zeros(M, N)
+    dev_ops.gemm(dA, dB, C2, trans_b=True, alpha=0.5, engine=1)
+    err2 = ((C2.double().cpu() - ref).abs() / scale).max().item()
+    assert err < 1e-5, err
+    assert err < max(3 * err2, 1e-6), (err, err2)
