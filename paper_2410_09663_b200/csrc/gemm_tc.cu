@@ -26,8 +26,9 @@ namespace enks {
 namespace {
 
 constexpr int BM = 128, BK = 32;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;        // 4 control warps + 8 converter/epilogue warps
 constexpr int kSmemBudget = 200 * 1024;
+constexpr int kChainChunks = 4;      // TMEM accumulation chain = 4 x 32 = 128 K-elements
 
 struct TcParams {
     int64_t M, N, K;
@@ -46,8 +47,16 @@ struct Layout {
     static constexpr int kA = BM * BK * 4;     // 16 KB (hi in place)
     static constexpr int kB = BN * BK * 4;     // BN x 128 B
     static constexpr int kStage = 2 * kA + 2 * kB;
+    static constexpr int kSlotCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+    static constexpr int kEpiWG = BN > 128 ? 2 : 1;         // warpgroups holding the fp32 sums
+    static constexpr int kColsPerWG = BN > 128 ? BN / 2 : BN;
 };
 
+// The tensor core accumulates into TMEM with truncation; over long K chains that
+// bias reaches ~1e-6 relative (measured: tools/tc_acc_probe.py).  The MMA warp
+// therefore restarts a fresh TMEM slot every kChainChunks chunks (two slots,
+// ping-pong) and the epilogue warps fold each finished chain into fp32 registers
+// with round-to-nearest adds while the other slot fills.
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
@@ -60,8 +69,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* full = bars;
     uint64_t* conv = bars + S;
     uint64_t* empty = bars + 2 * S;
-    uint64_t* accum = bars + 3 * S;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 1);
+    uint64_t* tfull = bars + 3 * S;       // [2] chain finished in slot
+    uint64_t* tempty = bars + 3 * S + 2;  // [2] slot drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * BM;
@@ -69,7 +79,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int c_lo = split * p.chunks_per_split;
     const int c_hi = min(p.total_chunks, c_lo + p.chunks_per_split);
     const int n_chunks = max(0, c_hi - c_lo);
-    constexpr uint32_t kTmemCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+    const int n_groups = (n_chunks + kChainChunks - 1) / kChainChunks;
+    constexpr uint32_t kTmemCols = 2 * L::kSlotCols;
 
     auto stage_a = [&](int s) { return smem + (size_t)s * L::kStage; };
     auto stage_alo = [&](int s) { return smem + (size_t)s * L::kStage + L::kA; };
@@ -79,10 +90,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&conv[s], 128);
+            ptx::mbar_init(&conv[s], 256);
             ptx::mbar_init(&empty[s], 1);
         }
-        ptx::mbar_init(accum, 1);
+        for (int q = 0; q < 2; ++q) {
+            ptx::mbar_init(&tfull[q], 1);
+            ptx::mbar_init(&tempty[q], 4 * L::kEpiWG);
+        }
         ptx::fence_barrier_init();
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmBh);
@@ -113,33 +127,69 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < n_chunks; ++i) {
                 const int s = i % S;
                 const uint32_t ph = (uint32_t)((i / S) & 1);
+                const int g = i / kChainChunks, slot = g & 1;
+                const bool first = (i % kChainChunks) == 0;
+                const bool last = (i % kChainChunks) == kChainChunks - 1 || i == n_chunks - 1;
+                if (first) {
+                    ptx::mbar_wait(&tempty[slot], (uint32_t)(((g >> 1) & 1) ^ 1));
+                    ptx::tc_fence_after();
+                }
                 ptx::mbar_wait(&conv[s], ph);
                 ptx::tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(slot * L::kSlotCols);
 #pragma unroll
                 for (int k = 0; k < BK / 8; ++k) {
                     const uint64_t ah = ptx::desc_kmajor_sw128(stage_a(s) + 32 * k);
                     const uint64_t al = ptx::desc_kmajor_sw128(stage_alo(s) + 32 * k);
                     const uint64_t bh = ptx::desc_kmajor_sw128(stage_bh(s) + 32 * k);
                     const uint64_t bl = ptx::desc_kmajor_sw128(stage_bl(s) + 32 * k);
-                    uint32_t acc = (i | k) ? 1u : 0u;
-                    if (p.products & 1) { ptx::mma_tf32_ss(tmem, al, bh, idesc, acc); acc = 1u; }
-                    if (p.products & 2) { ptx::mma_tf32_ss(tmem, ah, bl, idesc, acc); acc = 1u; }
-                    if (p.products & 4) { ptx::mma_tf32_ss(tmem, ah, bh, idesc, acc); }
+                    uint32_t acc = (first && k == 0) ? 0u : 1u;
+                    if (p.products & 1) { ptx::mma_tf32_ss(d, al, bh, idesc, acc); acc = 1u; }
+                    if (p.products & 2) { ptx::mma_tf32_ss(d, ah, bl, idesc, acc); acc = 1u; }
+                    if (p.products & 4) { ptx::mma_tf32_ss(d, ah, bh, idesc, acc); }
                 }
                 ptx::mma_commit(&empty[s]);
+                if (last) ptx::mma_commit(&tfull[slot]);
             }
-            if (n_chunks > 0) ptx::mma_commit(accum);
         }
     } else if (warp >= 4) {
-        const int t = threadIdx.x - 128;  // row within the tile == TMEM lane
+        const int t = threadIdx.x - 128;          // 0..255
+        const int crow = t & 127, chalf = t >> 7;  // converter: half a row (64 B) each
+        const int wg = (warp - 4) >> 2;            // epilogue warpgroup
+        const bool epi = wg < L::kEpiWG;
+        const int erow = ((warp & 3) << 5) + lane;  // TMEM lane == tile row
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        float acc[L::kColsPerWG];
+#pragma unroll
+        for (int j = 0; j < L::kColsPerWG; ++j) acc[j] = 0.f;
+
+        auto drain = [&](int g) {
+            const int slot = g & 1;
+            ptx::mbar_wait(&tfull[slot], (uint32_t)((g >> 1) & 1));
+            ptx::tc_fence_after();
+            const uint32_t base = tmem + lane_base + (uint32_t)(slot * L::kSlotCols + wg * L::kColsPerWG);
+#pragma unroll
+            for (int c0 = 0; c0 < L::kColsPerWG; c0 += 32) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(base + c0, v);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(v[j]);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
+        };
+
+        int drained = 0;
         for (int i = 0; i < n_chunks; ++i) {
             const int s = i % S;
             const uint32_t ph = (uint32_t)((i / S) & 1);
             ptx::mbar_wait(&full[s], ph);
-            float4* a = reinterpret_cast<float4*>(stage_a(s) + t * 128);
-            float4* alo = reinterpret_cast<float4*>(stage_alo(s) + t * 128);
+            float4* a = reinterpret_cast<float4*>(stage_a(s) + crow * 128 + chalf * 64);
+            float4* alo = reinterpret_cast<float4*>(stage_alo(s) + crow * 128 + chalf * 64);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < 4; ++q) {
                 float4 v = a[q];
                 float4 h, l;
                 h.x = ptx::tf32_round(v.x); l.x = v.x - h.x;
@@ -151,39 +201,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(&conv[s]);
-        }
-        // epilogue: TMEM -> registers -> HBM (row t of the tile)
-        const int64_t r = row0 + t;
-        float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo;
-        if (n_chunks > 0) {
-            ptx::mbar_wait(accum, 0);
-            ptx::tc_fence_after();
-        }
-        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            uint32_t v[32];
-            if (n_chunks > 0) {
-                ptx::tmem_ld_32x32b_x32(tmem + lane_base + c0, v);
-                ptx::tmem_ld_wait();
-            } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = 0u;
+            // fold chain g-1 once chain g has been fully converted (its slot is reused by g+1)
+            if (epi && (i % kChainChunks) == kChainChunks - 1) {
+                const int g = i / kChainChunks;
+                if (g >= 1) drain(g - 1), drained = g;
             }
+        }
+        if (epi) {
+            for (int g = drained; g < n_groups; ++g) drain(g);
+            const int64_t r = row0 + erow;
             if (r < p.M) {
-                if (c0 + 32 <= p.N && ((p.ldo & 3) == 0)) {
+                float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + wg * L::kColsPerWG;
+                const int ncol = (int)min((int64_t)L::kColsPerWG, p.N - (int64_t)wg * L::kColsPerWG);
+                if (ncol == L::kColsPerWG && (p.ldo & 3) == 0) {
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 o = make_float4(p.alpha * __uint_as_float(v[j]),
-                                               p.alpha * __uint_as_float(v[j + 1]),
-                                               p.alpha * __uint_as_float(v[j + 2]),
-                                               p.alpha * __uint_as_float(v[j + 3]));
-                        *reinterpret_cast<float4*>(orow + c0 + j) = o;
-                    }
+                    for (int j = 0; j < L::kColsPerWG; j += 4)
+                        *reinterpret_cast<float4*>(orow + j) =
+                            make_float4(p.alpha * acc[j], p.alpha * acc[j + 1], p.alpha * acc[j + 2],
+                                        p.alpha * acc[j + 3]);
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (c0 + j < p.N) orow[c0 + j] = p.alpha * __uint_as_float(v[j]);
+                    for (int j = 0; j < L::kColsPerWG; ++j)
+                        if (j < ncol) orow[j] = p.alpha * acc[j];
                 }
             }
         }
@@ -261,7 +300,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& m
         return ENKS_E_UNSUPPORTED;
     }
     p.stages = stages;
-    const size_t smem = (size_t)stages * L::kStage + 1024 + 256;
+    const size_t smem = (size_t)stages * L::kStage + 1024 + 512;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(tc_nt_kernel<BN>,

@@ -28,3 +28,19 @@ for K in (128, 4096):
     print(K, "emul 1xtf32", ((r1 - ref).abs() / scale).max().item())
     r3 = r1 + al.double().cpu() @ bh.double().cpu().t() + ah.double().cpu() @ bl.double().cpu().t()
     print(K, "emul 3xtf32", ((r3 - ref).abs() / scale).max().item())
+
+# short accumulation chains: split-K so each CTA accumulates only `cps` chunks in TMEM
+K = 4096
+g = torch.Generator().manual_seed(1)
+A = torch.randn(128, K, generator=g) + 0.5
+B = torch.randn(256, K, generator=g)
+dA, dB = A.cuda(), B.cuda()
+bh, bl = ops.empty(256, K), ops.empty(256, K)
+ops.tf32_split(dB, bh, bl)
+ref = A.double() @ B.double().t()
+scale = A.double().abs() @ B.double().abs().t()
+os.environ["ENKS_TC_PRODUCTS"] = "7"
+for split in (1, 4, 16, 32, 128):
+    C = ops.zeros(128, 256)
+    ops.gemm_nt_tc(dA, bh, bl, C, split=split)
+    print("split", split, "chain K", K // split, ((C.double().cpu() - ref).abs() / scale).max().item())
