@@ -12,9 +12,17 @@
 // stay in shared memory, so HBM sees X and U once and X' once.  Activations
 // at positions outside the image are forced to zero (that is what 'same'
 // zero padding of the next layer reads).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace enks {
+
+bool cnn3_tc_applicable(int n_layers, const int* widths, int rows, int cols);
+int cnn3_tc_forward(const float* weights, const float* biases, float alpha, const float* x,
+                    int64_t ldx, const float* u, int64_t ldu, float* out, int64_t ldo, int rows,
+                    int64_t n_members, cudaStream_t st);
+
 namespace {
 
 constexpr int kTile = 16;
@@ -160,6 +168,13 @@ int enks_cnn_forward(int n_layers, const int* widths, const float* weights, cons
     ENKS_REQUIRE(widths[0] == 2 && widths[n_layers] == 1,
                  "enks_cnn_forward: widths must start at 2 ([X, U]) and end at 1");
     if (n_members <= 0 || rows <= 0 || cols <= 0) return ENKS_OK;
+    {
+        const char* e = getenv("ENKS_CNN_TC");
+        const bool allow = !(e && e[0] == '0');
+        if (allow && cnn3_tc_applicable(n_layers, widths, rows, cols))
+            return cnn3_tc_forward(weights, biases, alpha, x, ldx, u, ldu, out, ldo, rows, n_members,
+                                   as_stream(stream));
+    }
     CnnArgs a;
     a.n_layers = n_layers;
     int woff = 0, boff = 0, max_act = 0;

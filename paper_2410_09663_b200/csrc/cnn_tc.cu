@@ -1,0 +1,410 @@
+// K3 on tcgen05: the 3-layer CNN forecast (widths 2-32-32-1, 128-pixel-wide fields)
+//     X' = X + alpha * conv3(tanh(conv2(tanh(conv1([X, U])))))
+// with the 32->32 layer (92% of the FLOPs) as 3xTF32 tcgen05 MMAs and the thin
+// first/last layers on the CUDA cores, all fused: HBM sees X, U once and X' once.
+//
+// Model seam: MatrixDynamics.step (reference dynamics.py:40-50) called at
+// enks.py:168; the CNN itself is the paper's surrogate (not shipped by the
+// reference) -- defined in dynamics.py::CNNDynamics, restated in
+// fp64 by oracle/models.py.
+//
+// Formulation (one CTA streams whole member images, one image row = one
+// 128-row MMA tile, TMEM lane = pixel):
+//   for every layer-1 output row r (32 channels, written hi/lo into smem,
+//   K-major SWIZZLE_128B) and each vertical tap dy, one MMA group
+//       D[y = r - dy + 1][x][(dx, co)] += sum_ci h1[r][x][ci] * W2[co][ci][dy][dx]
+//   with N = 96 = (3 horizontal taps) x 32 output channels, so the activation
+//   tile is never shifted; the horizontal taps are folded in the epilogue with
+//   warp shuffles (out[x'] = D[x'-1][dx=0] + D[x'][1] + D[x'+1][2]).  Four
+//   96-column TMEM accumulators form a ring over output rows.  The epilogue
+//   applies bias + tanh, the 32->1 layer (again tap-folded by shuffles), and
+//   the residual.  3xTF32: each MMA triple is lo*hi + hi*lo + hi*hi.
+//
+// Warp roles (384 threads): warp 0 = MMA issuer, warp 2 = TMEM allocator,
+// warps 4-7 = layer-1 producer (thread = pixel), warps 8-11 = epilogue
+// (thread = pixel = TMEM lane).
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace enks {
+namespace {
+
+constexpr int W = 128;     // image width (== MMA M)
+constexpr int C1 = 32;     // layer-1 width
+constexpr int C2 = 32;     // layer-2 width
+constexpr int NB = 3 * C2; // MMA N: (dx, co)
+constexpr int NA = 3;      // layer-1 row slots
+constexpr int NACC = 4;    // TMEM output-row accumulators
+constexpr int kThreads = 384;
+
+constexpr int kBTile = NB * 128;        // one dy, hi or lo: 96 rows x 128 B
+constexpr int kATile = W * 128;         // one layer-1 row, hi or lo: 128 rows x 128 B
+constexpr int kOffB = 0;                            // [dy][hi/lo] B tiles
+constexpr int kOffA = kOffB + 3 * 2 * kBTile;       // [slot][hi/lo] A tiles
+constexpr int kOffIn = kOffA + NA * 2 * kATile;     // input ring [4][2][W + 2] floats
+constexpr int kInRow = W + 2;
+constexpr int kOffW1 = kOffIn + 4 * 2 * kInRow * 4; // w1 [C1][20], b1[C1], b2[C2], w3[9][C2], b3
+constexpr int kW1Stride = 20;
+constexpr int kOffB1 = kOffW1 + C1 * kW1Stride * 4;
+constexpr int kOffB2 = kOffB1 + C1 * 4;
+constexpr int kOffW3 = kOffB2 + C2 * 4;
+constexpr int kOffB3 = kOffW3 + 9 * C2 * 4;
+constexpr int kOffX = kOffB3 + 16;                  // exchange buffers
+constexpr int kXD = 2 * 4 * 32;                     // [parity][warp][32]
+constexpr int kXV = 2 * 4 * 4;                      // [parity][warp][3 (+pad)]
+constexpr int kOffBar = kOffX + (2 * kXD + 2 * kXV) * 4;
+constexpr int kSmem = kOffBar + 32 * 8 + 1024;      // + alignment slack
+
+__device__ __forceinline__ uint32_t sw128(int row, int byte) {
+    return (uint32_t)(row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15)));
+}
+
+__device__ __forceinline__ float tanh_fast(float x) {
+    const float t = __expf(2.f * x);
+    return 1.f - __fdividef(2.f, 1.f + t);
+}
+
+struct Cnn3Args {
+    const float* w1;  // (C1, 2, 3, 3)
+    const float* b1;
+    const float* w2;  // (C2, C1, 3, 3)
+    const float* b2;
+    const float* w3;  // (1, C2, 3, 3)
+    const float* b3;
+    float alpha;
+    const float* x;
+    int64_t ldx;
+    const float* u;
+    int64_t ldu;
+    float* out;
+    int64_t ldo;
+    int rows;
+    int64_t n_members;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+    float* in_ring = reinterpret_cast<float*>(sm + kOffIn);
+    float* w1s = reinterpret_cast<float*>(sm + kOffW1);
+    float* b1s = reinterpret_cast<float*>(sm + kOffB1);
+    float* b2s = reinterpret_cast<float*>(sm + kOffB2);
+    float* w3s = reinterpret_cast<float*>(sm + kOffW3);
+    float* b3s = reinterpret_cast<float*>(sm + kOffB3);
+    float* xd0 = reinterpret_cast<float*>(sm + kOffX);
+    float* xd2 = xd0 + kXD;
+    float* xv0 = xd2 + kXD;
+    float* xv2 = xv0 + kXV;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar);
+    uint64_t* a_full = bars;             // [NA]
+    uint64_t* a_empty = bars + NA;       // [NA]
+    uint64_t* acc_full = bars + 2 * NA;  // [NACC]
+    uint64_t* acc_empty = bars + 2 * NA + NACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NA + 2 * NACC);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = a.rows;
+
+    // ---- stage weights (all threads) -------------------------------------------------
+    for (int e = threadIdx.x; e < 3 * NB * C1; e += kThreads) {
+        // B[dy][row = dx*C2 + co][ci] = W2[co][ci][dy][dx]
+        const int dy = e / (NB * C1), rem = e - dy * NB * C1;
+        const int row = rem / C1, ci = rem - row * C1;
+        const int dx = row / C2, co = row - dx * C2;
+        const float v = a.w2[((co * C1 + ci) * 3 + dy) * 3 + dx];
+        const float h = ptx::tf32_round(v);
+        const uint32_t off = sw128(row, ci * 4);
+        *reinterpret_cast<float*>(sm + kOffB + (dy * 2 + 0) * kBTile + off) = h;
+        *reinterpret_cast<float*>(sm + kOffB + (dy * 2 + 1) * kBTile + off) = v - h;
+    }
+    for (int e = threadIdx.x; e < C1 * 18; e += kThreads) {
+        const int c = e / 18, k = e - c * 18;
+        w1s[c * kW1Stride + k] = a.w1[c * 18 + k];  // k = ci*9 + ky*3 + kx
+    }
+    for (int e = threadIdx.x; e < C1; e += kThreads) b1s[e] = a.b1[e];
+    for (int e = threadIdx.x; e < C2; e += kThreads) b2s[e] = a.b2[e];
+    for (int e = threadIdx.x; e < 9 * C2; e += kThreads) {
+        const int k = e / C2, c = e - k * C2;  // w3s[ky*3+kx][c]
+        w3s[e] = a.w3[c * 9 + k];
+    }
+    if (threadIdx.x == 0) {
+        b3s[0] = a.b3[0];
+        for (int s = 0; s < NA; ++s) {
+            ptx::mbar_init(&a_full[s], 128);
+            ptx::mbar_init(&a_empty[s], 1);
+        }
+        for (int q = 0; q < NACC; ++q) {
+            ptx::mbar_init(&acc_full[q], 1);
+            ptx::mbar_init(&acc_empty[q], 4);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+    ptx::fence_proxy_async_smem();  // staged B tiles -> async proxy
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ================= MMA issuer =================
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_tf32(W, NB);
+            int64_t it = 0;
+            for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
+                for (int r = 0; r < n; ++r) {
+                    const int64_t Rg = it * n + r;
+                    const int slot = (int)(Rg % NA);
+                    ptx::mbar_wait(&a_full[slot], (uint32_t)((Rg / NA) & 1));
+                    ptx::tc_fence_after();
+                    const uint8_t* ah_t = sm + kOffA + (slot * 2 + 0) * kATile;
+                    const uint8_t* al_t = sm + kOffA + (slot * 2 + 1) * kATile;
+                    for (int dy = 0; dy < 3; ++dy) {
+                        const int y = r - dy + 1;
+                        if (y < 0 || y >= n) continue;
+                        const int64_t Yg = it * n + y;
+                        const int q = (int)(Yg % NACC);
+                        const bool first = (dy == 0) || (r == 0 && dy == 1);
+                        if (first) {
+                            ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Yg / NACC) & 1) ^ 1));
+                            ptx::tc_fence_after();
+                        }
+                        const uint32_t d = tmem + (uint32_t)(q * NB);
+                        const uint8_t* bh_t = sm + kOffB + (dy * 2 + 0) * kBTile;
+                        const uint8_t* bl_t = sm + kOffB + (dy * 2 + 1) * kBTile;
+#pragma unroll
+                        for (int k = 0; k < C1 / 8; ++k) {
+                            const uint64_t adh = ptx::desc_kmajor_sw128(ah_t + 32 * k);
+                            const uint64_t adl = ptx::desc_kmajor_sw128(al_t + 32 * k);
+                            const uint64_t bdh = ptx::desc_kmajor_sw128(bh_t + 32 * k);
+                            const uint64_t bdl = ptx::desc_kmajor_sw128(bl_t + 32 * k);
+                            ptx::mma_tf32_ss(d, adl, bdh, idesc, (first && k == 0) ? 0u : 1u);
+                            ptx::mma_tf32_ss(d, adh, bdl, idesc, 1u);
+                            ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                        }
+                        // row y complete: after its dy=2 contribution, or the last row's dy=1
+                        if (dy == 2 || (r == n - 1 && dy == 1)) ptx::mma_commit(&acc_full[q]);
+                    }
+                    ptx::mma_commit(&a_empty[slot]);
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ================= layer-1 producer: thread = pixel =================
+        const int x = threadIdx.x - 128;
+        int64_t it = 0;
+        for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
+            const float* xm = a.x + mem * W;
+            const float* um = a.u + mem * W;
+            auto load_row = [&](int j) {  // input row j (0 <= j < n) into ring slot j & 3
+                float* dst = in_ring + (j & 3) * 2 * kInRow;
+                dst[x + 1] = xm[(int64_t)j * a.ldx + x];
+                dst[kInRow + x + 1] = um[(int64_t)j * a.ldu + x];
+                if (x == 0) {
+                    dst[0] = 0.f; dst[kInRow - 1] = 0.f;
+                    dst[kInRow] = 0.f; dst[2 * kInRow - 1] = 0.f;
+                }
+            };
+            load_row(0);
+            for (int r = 0; r < n; ++r) {
+                if (r + 1 < n) load_row(r + 1);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                float in[18];
+#pragma unroll
+                for (int ci = 0; ci < 2; ++ci)
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky) {
+                        const int j = r + ky - 1;
+                        const bool ok = j >= 0 && j < n;
+                        const float* src = in_ring + (j & 3) * 2 * kInRow + ci * kInRow + x;
+#pragma unroll
+                        for (int kx = 0; kx < 3; ++kx) in[ci * 9 + ky * 3 + kx] = ok ? src[kx] : 0.f;
+                    }
+                const int64_t Rg = it * n + r;
+                const int slot = (int)(Rg % NA);
+                ptx::mbar_wait(&a_empty[slot], (uint32_t)(((Rg / NA) & 1) ^ 1));
+                uint8_t* ah_t = sm + kOffA + (slot * 2 + 0) * kATile;
+                uint8_t* al_t = sm + kOffA + (slot * 2 + 1) * kATile;
+#pragma unroll 2
+                for (int c4 = 0; c4 < C1 / 4; ++c4) {
+                    float hv[4];
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) {
+                        const int c = c4 * 4 + cc;
+                        const float4* wr = reinterpret_cast<const float4*>(w1s + c * kW1Stride);
+                        float acc = b1s[c];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float4 wv = wr[q];
+                            acc = fmaf(wv.x, in[4 * q + 0], acc);
+                            acc = fmaf(wv.y, in[4 * q + 1], acc);
+                            acc = fmaf(wv.z, in[4 * q + 2], acc);
+                            acc = fmaf(wv.w, in[4 * q + 3], acc);
+                        }
+                        const float2 wt = *reinterpret_cast<const float2*>(w1s + c * kW1Stride + 16);
+                        acc = fmaf(wt.x, in[16], acc);
+                        acc = fmaf(wt.y, in[17], acc);
+                        hv[cc] = tanh_fast(acc);
+                    }
+                    float4 h4, l4;
+                    h4.x = ptx::tf32_round(hv[0]); l4.x = hv[0] - h4.x;
+                    h4.y = ptx::tf32_round(hv[1]); l4.y = hv[1] - h4.y;
+                    h4.z = ptx::tf32_round(hv[2]); l4.z = hv[2] - h4.z;
+                    h4.w = ptx::tf32_round(hv[3]); l4.w = hv[3] - h4.w;
+                    const uint32_t off = sw128(x, c4 * 16);
+                    *reinterpret_cast<float4*>(ah_t + off) = h4;
+                    *reinterpret_cast<float4*>(al_t + off) = l4;
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::mbar_arrive(&a_full[slot]);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // ring reuse across members
+        }
+    } else if (warp >= 8) {
+        // ================= epilogue: thread = pixel = TMEM lane =================
+        const int ew = warp - 8;  // == warp & 3 -> TMEM lane quarter
+        const int x = ew * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
+        const float b3 = b3s[0];
+        int64_t it = 0;
+        for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
+            float acc3[3] = {0.f, 0.f, 0.f};  // layer-3 partial sums, ring over output rows
+            const float* xm = a.x + mem * W;
+            float* om = a.out + mem * W;
+            for (int y = 0; y < n; ++y) {
+                const int64_t Yg = it * n + y;
+                const int q = (int)(Yg % NACC);
+                const int par = (int)(Yg & 1);
+                ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / NACC) & 1));
+                ptx::tc_fence_after();
+                const uint32_t base = tmem + lane_base + (uint32_t)(q * NB);
+                float s[32], t[32];
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(base + 0, v);  // dx = 0 block
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
+                if (lane == 31) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) xd0[(par * 4 + ew) * 32 + c] = t[c];
+                }
+#pragma unroll
+                for (int c = 0; c < 32; ++c) s[c] = __shfl_up_sync(0xffffffffu, t[c], 1);
+                ptx::tmem_ld_32x32b_x32(base + 32, v);  // dx = 1 block
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) s[c] = (lane == 0 ? 0.f : s[c]) + __uint_as_float(v[c]);
+                ptx::tmem_ld_32x32b_x32(base + 64, v);  // dx = 2 block
+                ptx::tmem_ld_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&acc_empty[q]);
+#pragma unroll
+                for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
+                if (lane == 0) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) xd2[(par * 4 + ew) * 32 + c] = t[c];
+                }
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const float dn = __shfl_down_sync(0xffffffffu, t[c], 1);
+                    if (lane != 31) s[c] += dn;
+                }
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+                if (lane == 0 && ew > 0) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) s[c] += xd0[(par * 4 + ew - 1) * 32 + c];
+                }
+                if (lane == 31 && ew < 3) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) s[c] += xd2[(par * 4 + ew + 1) * 32 + c];
+                }
+                // layer-2 activation and the layer-3 taps v[ky][kx] = sum_c w3 h
+                float vv[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) vv[k] = 0.f;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const float h = tanh_fast(s[c] + b2s[c]);
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) vv[k] = fmaf(w3s[k * C2 + c], h, vv[k]);
+                }
+                // fold horizontal taps: lane x3 takes v[ky][0] from x3-1, v[ky][2] from x3+1
+                float tk[3];
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky) {
+                    const float up = __shfl_up_sync(0xffffffffu, vv[ky * 3 + 0], 1);
+                    const float dn = __shfl_down_sync(0xffffffffu, vv[ky * 3 + 2], 1);
+                    tk[ky] = vv[ky * 3 + 1] + (lane == 0 ? 0.f : up) + (lane == 31 ? 0.f : dn);
+                    if (lane == 31) xv0[(par * 4 + ew) * 4 + ky] = vv[ky * 3 + 0];
+                    if (lane == 0) xv2[(par * 4 + ew) * 4 + ky] = vv[ky * 3 + 2];
+                }
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+                if (lane == 0 && ew > 0) {
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky) tk[ky] += xv0[(par * 4 + ew - 1) * 4 + ky];
+                }
+                if (lane == 31 && ew < 3) {
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky) tk[ky] += xv2[(par * 4 + ew + 1) * 4 + ky];
+                }
+                // h at row y feeds output rows y+1 (ky=0), y (ky=1), y-1 (ky=2)
+                acc3[(y + 1) % 3] += tk[0];
+                acc3[y % 3] += tk[1];
+                if (y >= 1) {
+                    const int yo = y - 1;
+                    const float o = acc3[yo % 3] + tk[2];
+                    acc3[yo % 3] = 0.f;
+                    om[(int64_t)yo * a.ldo + x] = xm[(int64_t)yo * a.ldx + x] + a.alpha * (b3 + o);
+                }
+                if (y == n - 1) {
+                    const float o = acc3[y % 3];
+                    acc3[y % 3] = 0.f;
+                    om[(int64_t)y * a.ldo + x] = xm[(int64_t)y * a.ldx + x] + a.alpha * (b3 + o);
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc(tmem, 512);
+}
+
+}  // namespace
+
+bool cnn3_tc_applicable(int n_layers, const int* widths, int rows, int cols) {
+    return n_layers == 3 && widths[0] == 2 && widths[1] == C1 && widths[2] == C2 &&
+           widths[3] == 1 && cols == W && rows >= 2;
+}
+
+int cnn3_tc_forward(const float* weights, const float* biases, float alpha, const float* x,
+                    int64_t ldx, const float* u, int64_t ldu, float* out, int64_t ldo, int rows,
+                    int64_t n_members, cudaStream_t st) {
+    Cnn3Args a;
+    a.w1 = weights;
+    a.w2 = weights + C1 * 2 * 9;
+    a.w3 = a.w2 + C2 * C1 * 9;
+    a.b1 = biases;
+    a.b2 = biases + C1;
+    a.b3 = biases + C1 + C2;
+    a.alpha = alpha;
+    a.x = x; a.ldx = ldx; a.u = u; a.ldu = ldu; a.out = out; a.ldo = ldo;
+    a.rows = rows;
+    a.n_members = n_members;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(cnn3_tc_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (e != cudaSuccess) {
+            set_error("cnn3_tc: smem attribute: %s", cudaGetErrorString(e));
+            return ENKS_E_CUDA;
+        }
+        configured = true;
+    }
+    const int grid = (int)(n_members < kNumSMs ? n_members : kNumSMs);
+    cnn3_tc_kernel<<<grid, kThreads, kSmem, st>>>(a);
+    return check_launch("enks_cnn_forward(tcgen05)");
+}
+
+}  // namespace enks

@@ -204,3 +204,41 @@ def test_gemm_nt_tc_3xtf32(dev_ops, M, N, K, split):
     err2 = ((C2.double().cpu() - ref).abs() / scale).max().item()
     assert err < 1e-5, err
     assert err < max(3 * err2, 1e-6), (err, err2)
+
+
+@pytest.mark.parametrize("rows,N", [(128, 3), (40, 5)])
+def test_cnn_forward_tcgen05_vs_oracle(dev_ops, pm, rows, N):
+    """The fused tcgen05 conv (widths 2-32-32-1, 128-wide fields) against the fp64 oracle."""
+    from oracle.models import cnn_step
+    from paper_2410_09663_b200.engine import Forecaster
+
+    model = pm.dynamics.CNNDynamics(rows=rows, cols=128, widths=(2, 32, 32, 1), seed=3)
+    model.state_rows = model.input_rows = rows
+    rng = np.random.default_rng(rows)
+    x = rng.standard_normal((N, rows, 128))
+    u = rng.standard_normal((N, rows, 128))
+    ref = cnn_step(x, u, model.weights, model.biases, model.alpha)
+    last = dev_ops.to_device(np.concatenate([x, u], axis=1).transpose(1, 0, 2).reshape(2 * rows, -1))
+    out = dev_ops.zeros(rows, N * 128)
+    Forecaster(model, dev_ops, rows, rows)(dev_ops, last, out, rows, N)
+    got = _cpu(out).reshape(rows, N, 128).transpose(1, 0, 2)
+    np.testing.assert_allclose(got, ref, rtol=1e-5, atol=2e-6)
+
+
+def test_cnn_forward_tcgen05_matches_simt_many_members(dev_ops, pm, monkeypatch):
+    """Persistent CTAs over > 148 members: tcgen05 path == SIMT path to fp32 rounding."""
+    from paper_2410_09663_b200.engine import Forecaster
+
+    n, N = 128, 300
+    model = pm.dynamics.CNNDynamics(rows=n, cols=n, widths=(2, 32, 32, 1), seed=4)
+    g = torch.Generator().manual_seed(0)
+    last = torch.randn(2 * n, N * n, generator=g).to(dev_ops.device)
+    fc = Forecaster(model, dev_ops, n, n)
+    out_tc = dev_ops.zeros(n, N * n)
+    fc(dev_ops, last, out_tc, n, N)
+    monkeypatch.setenv("ENKS_CNN_TC", "0")
+    out_simt = dev_ops.zeros(n, N * n)
+    fc(dev_ops, last, out_simt, n, N)
+    torch.cuda.synchronize()
+    diff = (out_tc - out_simt).abs().max().item()
+    assert diff < 2e-5, diff
