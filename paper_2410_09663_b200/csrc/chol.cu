@@ -10,6 +10,7 @@
 // leave the SM and no host synchronisation is needed: failure is reported
 // through device-side status / jitter counters.
 #include "common.cuh"
+#include "gemm.cuh"
 
 namespace enks {
 namespace {
@@ -21,7 +22,7 @@ __device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }
 
 __global__ void __launch_bounds__(kThreads)
     spd_inverse_kernel(const float* __restrict__ S, int64_t lds, int p, float scale,
-                       float* __restrict__ inv, int* status, int* jitter_events) {
+                       float* __restrict__ linv, int* status, int* jitter_events) {
     extern __shared__ float L[];
     __shared__ float s_inv_piv;
     __shared__ int s_fail;
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kThreads)
     if (failed) {
         if (tid == 0) *status = 1;
         const float nan = __int_as_float(0x7fc00000);
-        for (int e = tid; e < p * p; e += kThreads) inv[e] = nan;
+        for (int e = tid; e < p * p; e += kThreads) linv[e] = nan;
         return;
     }
 
@@ -106,15 +107,10 @@ __global__ void __launch_bounds__(kThreads)
         }
         __syncthreads();
     }
-
-    // inv = Linv^T Linv  (symmetric; inv[i][j] = sum_{k >= max(i,j)} Linv[k][i] Linv[k][j])
+    // dense L^{-1} (zeros above the diagonal) for the L^{-T} L^{-1} product (enks_gemm)
     for (int e = tid; e < p * p; e += kThreads) {
         const int i = e / p, j = e - i * p;
-        if (j > i) continue;
-        float acc = 0.f;
-        for (int k = i; k < p; ++k) acc += L[pk(k, i)] * L[pk(k, j)];
-        inv[(int64_t)i * p + j] = acc;
-        inv[(int64_t)j * p + i] = acc;
+        linv[e] = j <= i ? L[pk(i, j)] : 0.f;
     }
 }
 
@@ -127,8 +123,7 @@ int enks_spd_max_p(void) { return enks::kMaxP; }
 
 int enks_spd_inverse(const float* S, int64_t lds, int p, float scale, float* inv, float* ws,
                      int* status, int* jitter_events, void* stream) {
-    (void)ws;
-    ENKS_REQUIRE(S && inv && status && jitter_events, "enks_spd_inverse: null pointer");
+    ENKS_REQUIRE(S && inv && ws && status && jitter_events, "enks_spd_inverse: null pointer");
     ENKS_REQUIRE(p >= 1 && p <= enks::kMaxP, "enks_spd_inverse: p=%d outside [1, %d]", p,
                  enks::kMaxP);
     const size_t smem = (size_t)p * (p + 1) / 2 * sizeof(float);
@@ -143,9 +138,14 @@ int enks_spd_inverse(const float* S, int64_t lds, int p, float scale, float* inv
         }
         configured = smem;
     }
-    enks::spd_inverse_kernel<<<1, enks::kThreads, smem, enks::as_stream(stream)>>>(
-        S, lds, p, scale, inv, status, jitter_events);
-    return enks::check_launch("enks_spd_inverse");
+    cudaStream_t st = enks::as_stream(stream);
+    enks::spd_inverse_kernel<<<1, enks::kThreads, smem, st>>>(S, lds, p, scale, ws, status,
+                                                              jitter_events);
+    int rc = enks::check_launch("enks_spd_inverse");
+    if (rc) return rc;
+    // Sy^{-1} = L^{-T} L^{-1}: one small GEMM (A = L^{-1} read transposed)
+    return enks::gemm_simt(1, 0, p, p, p, 1.f, ws, p, ws, p, 0.f, nullptr, 0, nullptr, 0, 1, inv,
+                           p, 0, 0, 1, nullptr, st);
 }
 
 }  // extern "C"

@@ -186,18 +186,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = i % S;
             const uint32_t ph = (uint32_t)((i / S) & 1);
             ptx::mbar_wait(&full[s], ph);
-            float4* a = reinterpret_cast<float4*>(stage_a(s) + crow * 128 + chalf * 64);
-            float4* alo = reinterpret_cast<float4*>(stage_alo(s) + crow * 128 + chalf * 64);
+            // elementwise split: any chunk order works; XOR with the row's swizzle phase
+            // spreads the 8 threads of each shared-memory phase over all 32 banks.
+            float4* a = reinterpret_cast<float4*>(stage_a(s) + crow * 128);
+            float4* alo = reinterpret_cast<float4*>(stage_alo(s) + crow * 128);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                float4 v = a[q];
+                const int qq = (chalf * 4 + q) ^ (crow & 7);
+                const float4 v = a[qq];
                 float4 h, l;
                 h.x = ptx::tf32_round(v.x); l.x = v.x - h.x;
                 h.y = ptx::tf32_round(v.y); l.y = v.y - h.y;
                 h.z = ptx::tf32_round(v.z); l.z = v.z - h.z;
                 h.w = ptx::tf32_round(v.w); l.w = v.w - h.w;
-                a[q] = h;
-                alo[q] = l;
+                a[qq] = h;
+                alo[qq] = l;
             }
             ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(&conv[s]);

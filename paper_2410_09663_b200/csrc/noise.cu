@@ -136,9 +136,21 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args a) {
     int64_t base_w = -(1LL << 40);  // buffer holds words [base_w, base_w + 128)
     int64_t w = 0, q = 0;
 
-    auto emit = [&](int64_t qi, double x) {
-        const int r = (int)(qi / a.cols);
-        const int j = (int)(qi - (int64_t)r * a.cols);
+    // (row, col) of normal q, tracked incrementally: (rb, jb) is the position of q (warp-uniform)
+    int rb = 0, jb = 0;
+    auto advance = [&](int k) {
+        jb += k;
+        while (jb >= a.cols) {
+            jb -= a.cols;
+            ++rb;
+        }
+    };
+    auto emit = [&](int off, double x) {  // normal q + off
+        int r = rb, j = jb + off;
+        while (j >= a.cols) {
+            j -= a.cols;
+            ++r;
+        }
         const double v = a.diag ? x * a.diag[r] : x;
         const float f = (float)v;
         if (a.out) a.out[r * a.ld_out + col0 + j] = f;
@@ -174,9 +186,10 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args a) {
         const unsigned bad = __ballot_sync(0xffffffffu, !ok);
         const int n_ok = bad ? (__ffs(bad) - 1) : 32;
         const int n_emit = (int)min((int64_t)n_ok, total - q);
-        if (lane < n_emit) emit(q + lane, x);
+        if (lane < n_emit) emit(lane, x);
         q += n_emit;
         w += n_emit;
+        advance(n_emit);
         if (q >= total || n_ok == 32) continue;
 
         // slow path for the rejected word at w (warp-uniform)
@@ -211,8 +224,9 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args a) {
                 }
             }
             if (have) {
-                if (lane == 0) emit(q, val);
+                if (lane == 0) emit(0, val);
                 ++q;
+                advance(1);
             }
         }
     }

@@ -167,9 +167,11 @@ class DeviceOps:
 
     def spd_inverse(self, S, scale, inv, status, jitter):
         p = S.shape[0]
-        self.launches += 1
-        _lib.call("enks_spd_inverse", _p(S), _ld(S), p, float(scale), _p(inv), None, _p(status),
-                  _p(jitter), self._stream())
+        if getattr(self, "_spd_ws", None) is None or self._spd_ws.numel() < p * p:
+            self._spd_ws = torch.empty(p * p, dtype=torch.float32, device=self.device)
+        self.launches += 2
+        _lib.call("enks_spd_inverse", _p(S), _ld(S), p, float(scale), _p(inv), _p(self._spd_ws),
+                  _p(status), _p(jitter), self._stream())
 
     def spd_max_p(self) -> int:
         return int(self.lib.enks_spd_max_p())

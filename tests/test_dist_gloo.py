@@ -1,0 +1,81 @@
+"""Member sharding over 2 ranks (gloo, CPU): same result as one rank.
+
+Exercises the engine's multi-rank orchestration -- global member ids for the
+noise substreams, the member-0 shift broadcast, the member-sum and cross-moment
+allreduces, replicated gain -- with the test-only CPU operator set.  On B200
+the same code runs with DeviceOps and NCCL (bench.py --gpus N under torchrun).
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem(kind):
+    from oracle import problems
+
+    pm = problems.product_modules()
+    if kind == "cnn":
+        pr = problems.make_cnn_problem(pm, "C1", size=8, n_members=11, horizon=3)
+        return pm, pr.vs, pr.x0, pr.N, pr.H
+    _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(2), n=5, l=3, m=4)
+    return pm, vs, x0, 13, 4
+
+
+def _run(kind, comm):
+    from cpu_ops import CpuOps
+    from paper_2410_09663_b200.engine import DeviceSmoother
+
+    pm, vs, x0, N, h = _problem(kind)
+    ops = CpuOps()
+    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, N, 1.0 / np.trace(vs.shared_col_cov),
+                         capacity=2, comm=comm)
+    st = pm.matvar.NoiseStreams(seed=21)
+    y = ops.to_device(vs.reference_observation())
+    for _ in range(h):
+        eng.predict(vs, st)
+        eng.update(y, st)
+    return eng
+
+
+def _worker(rank, world, port, kind, out):
+    sys.path[:0] = [os.path.dirname(HERE), HERE]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2410_09663_b200.engine import TorchComm
+
+    eng = _run(kind, TorchComm())
+    local = eng.members_device().numpy()
+    parts = [None] * world
+    dist.all_gather_object(parts, (eng.member0, eng.Nl, local))
+    if rank == 0:
+        np.savez(out, mean=eng.mean_host(), members=np.concatenate([p[2] for p in parts], axis=1),
+                 spans=np.array([(p[0], p[1]) for p in parts]), jitter=eng.jitter.item())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["linear", "cnn"])
+def test_two_rank_sharding_matches_single_rank(kind, tmp_path):
+    out = str(tmp_path / "r.npz")
+    mp.spawn(_worker, args=(2, _free_port(), kind, out), nprocs=2, join=True)
+    got = np.load(out)
+    ref = _run(kind, None)
+    assert [tuple(s) for s in got["spans"]] == [(0, 7), (7, 6)] if kind == "linear" else True
+    scale = np.abs(ref.mean_host()).max()
+    assert np.abs(got["mean"] - ref.mean_host()).max() < 1e-10 * scale
+    assert np.abs(got["members"] - ref.members_device().numpy()).max() < 1e-10 * scale
+    assert int(got["jitter"]) == ref.jitter.item()

@@ -1,0 +1,74 @@
+"""The append-only-basis restatement (engine.py) equals the reference algorithm.
+
+Runs the product engine's orchestration against a CPU fp64 operator set
+(tests/cpu_ops.py, test-only) and compares with the fp64 oracle: any
+difference beyond rounding would be an algebra error in the restructuring.
+"""
+import numpy as np
+import pytest
+
+from cpu_ops import CpuOps
+from oracle import enks_oracle, problems
+from paper_2410_09663_b200.engine import DeviceSmoother
+
+
+def _run(pm, x0, y, vs, h, N, seed, cap=2):
+    ops = CpuOps()
+    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, N, 1.0 / np.trace(vs.shared_col_cov), capacity=cap)
+    st = pm.matvar.NoiseStreams(seed=seed)
+    yd = ops.to_device(np.broadcast_to(y, (h,) + y.shape[-2:]).copy() if y.ndim == 2 else y)
+    for k in range(h):
+        eng.predict(vs, st)
+        eng.update(yd[k], st)
+    return eng
+
+
+@pytest.mark.parametrize("kw,N,h,seed", [
+    (dict(n=4, l=2, m=3), 16, 5, 0),
+    (dict(n=4, l=2, m=3, scale=0.0), 4, 3, 1),
+    (dict(n=8, l=4, m=8, identity_weights=True), 32, 6, 2),
+    (dict(n=4, l=1, m=1), 8, 3, 3),
+    (dict(n=6, l=6, m=5), 13, 7, 4),
+])
+def test_engine_equals_oracle_fp64(pm, kw, N, h, seed):
+    _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(seed), **kw)
+    y = vs.reference_observation()
+    ref, _, oens = enks_oracle.oracle_smooth(x0, y, vs, h, N, seed=seed + 7, backend="c")
+    eng = _run(pm, x0, y, vs, h, N, seed + 7)
+    d, m = x0.n + 2 * x0.l, x0.m
+    mean = eng.mean_host().reshape(h + 1, d, m)
+    members = eng.members_device().numpy().reshape((h + 1) * d, N, m).transpose(1, 0, 2)
+    scale = np.abs(ref).max()
+    assert np.abs(mean - ref).max() < 1e-10 * scale
+    assert np.abs(members - oens.members).max() < 1e-10 * np.abs(oens.members).max()
+    assert eng.jitter.item() == oens.jitter_events
+
+
+def test_engine_cnn_equals_oracle_fp64(pm):
+    pr = problems.make_cnn_problem(pm, "C1", size=8, n_members=10, horizon=3)
+    ref, _, _ = enks_oracle.oracle_smooth(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, seed=0, backend="c")
+    eng = _run(pm, pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, 0)
+    assert np.abs(eng.mean_host().reshape(ref.shape) - ref).max() < 1e-10 * np.abs(ref).max()
+
+
+def test_engine_explicit_members_restart(pm):
+    """replace_members (TrajectoryEnsemble(members=...)) then continue == oracle continuing."""
+    _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(5))
+    y = vs.reference_observation()
+    o = enks_oracle.oracle_init(x0.packed, x0.n, x0.l, 9)
+    for _ in range(2):
+        enks_oracle.oracle_predict(o, vs, 3, backend="c")
+        enks_oracle.oracle_update(o, y, vs, 3, backend="c")
+    o.members = o.members + 0.01 * np.random.default_rng(0).standard_normal(o.members.shape)
+    o.mean = o.members.mean(axis=0)
+    ops = CpuOps()
+    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, 9, o.lam, capacity=1)
+    eng.replace_members(o.members, o.t)
+    st = pm.matvar.NoiseStreams(seed=3)
+    for _ in range(2):
+        enks_oracle.oracle_predict(o, vs, 3, backend="c")
+        enks_oracle.oracle_update(o, y, vs, 3, backend="c")
+        eng.predict(vs, st)
+        eng.update(ops.to_device(y), st)
+    got = eng.members_device().numpy().reshape(o.members.shape[1], 9, x0.m).transpose(1, 0, 2)
+    assert np.abs(got - o.members).max() < 1e-10 * np.abs(o.members).max()

@@ -1,0 +1,68 @@
+"""The oracle restatement reproduces the reference's own outputs (golden fixtures).
+
+Fixtures come from the unmodified reference run in the build container
+(tests/golden/make_golden.py); this check runs anywhere, without /root/reference.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import enks_oracle, noise, problems
+from oracle.models import OracleCNN
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _load(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+def _case(pm, name):
+    from golden.make_golden import LINEAR_CASES
+
+    for cname, kw, seed, N, h, sseed, extra in LINEAR_CASES:
+        if cname == name:
+            model, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(seed), **kw)
+            if "col_cov" in extra:
+                vs = pm.virtualsys.build_virtual_system(
+                    model, vs.weights, shared_col_cov=extra["col_cov"] * np.eye(x0.m))
+            return model, vs, x0, N, h, sseed, extra
+    raise KeyError(name)
+
+
+NAMES = ["lin_spd_4x2x3", "lin_id_8x4x8", "lin_m1", "lin_scale0_N4", "lin_trackcov", "lin_colcov7",
+         "lin_yref_stack"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("backend", ["numpy", "c"])
+def test_oracle_matches_reference_golden(pm, name, backend):
+    gold = _load(name)
+    model, vs, x0, N, h, sseed, extra = _case(pm, name)
+    assert np.array_equal(x0.packed, gold["x0"])  # same problem as the reference run
+    out, cov, _ = enks_oracle.oracle_smooth(x0, gold["y"], vs, h, N, seed=sseed,
+                                            track_cov=bool(extra.get("track_cov")),
+                                            backend=backend)
+    np.testing.assert_allclose(out, gold["mean"], rtol=1e-12, atol=1e-12)
+    if extra.get("track_cov"):
+        for k in ("sigma_traj", "sigma_pred", "sigma_cross"):
+            np.testing.assert_allclose(getattr(cov, k), gold[k], rtol=1e-12, atol=1e-12)
+
+
+def test_oracle_cnn_matches_reference_golden(pm):
+    gold = _load("cnn_c1_16")
+    pr = problems.make_cnn_problem(pm, "C1", size=16, n_members=24, horizon=3)
+    assert np.array_equal(pr.x0.packed, gold["x0"])
+    ovs = pm.virtualsys.build_virtual_system(OracleCNN(pr.model), pr.vs.weights)
+    out, _, _ = enks_oracle.oracle_smooth(pr.x0, pr.y_ref, ovs, pr.H, pr.N, seed=1, backend="c")
+    np.testing.assert_allclose(out, gold["mean"], rtol=1e-12, atol=1e-12)
+
+
+def test_c_noise_matches_reference_golden():
+    from golden.make_golden import NOISE_CASES
+
+    gold = _load("noise")
+    for k, (seed, prefix, ids, shape) in enumerate(NOISE_CASES):
+        z = noise.c_standard_normal(seed, tuple(prefix) + tuple(ids), int(np.prod(shape)))
+        assert np.array_equal(z.reshape(shape), gold[f"z{k}"])
