@@ -64,6 +64,18 @@ int enks_noise_fill(const uint32_t* head, int n_head, uint32_t t, uint32_t chann
                     void* stream);
 
 /*
+ * Several noise channels of one step in a single launch (one warp per
+ * (member, job) substream), e.g. W, V_X, V_U of step t: job q draws channel
+ * channel[q] at time t[q] into rows[q] rows with the same out/base/out_plus
+ * semantics as enks_noise_fill (arrays of n_jobs <= 4 entries; host memory).
+ */
+int enks_noise_fill_multi(const uint32_t* head, int n_head, int64_t member0, int64_t n_members,
+                          int cols, int n_jobs, const uint32_t* t, const uint32_t* channel,
+                          const int* rows, const double* const* diag, float* const* out,
+                          const int64_t* ld_out, const float* const* base, const int64_t* ld_base,
+                          float* const* out_plus, const int64_t* ld_plus, void* stream);
+
+/*
  * Member statistics (K4/K5).  Replaces members.mean(axis=0) (enks.py:171, 248),
  * obs.mean(axis=0) (enks.py:231) and the anomaly formation (enks.py:232-233).
  * Anomalies are formed relative to a per-(row, col) shift z0 (global member
@@ -148,6 +160,9 @@ int enks_cnn_forward(int n_layers, const int* widths, const float* weights, cons
                      void* stream);
 
 /* Small elementwise helpers. */
+/* out[r, j] = a[r, j] + b[r, j] (the "u + w + v" observation of enks.py:168, 200). */
+int enks_add(const float* a, int64_t lda, const float* b, int64_t ldb, float* out, int64_t ldo,
+             int64_t rows, int64_t cols, void* stream);
 /* out[r, j] = a[r, j] - b[r, j] for an R x C block (innovation y_ref - obs_mean, enks.py:247). */
 int enks_sub(const float* a, int64_t lda, const float* b, int64_t ldb, float* out, int64_t ldo,
              int64_t rows, int64_t cols, void* stream);

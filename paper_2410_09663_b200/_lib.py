@@ -38,6 +38,8 @@ _SIGS = {
     "enks_device_check": (_c_int, []),
     "enks_noise_fill": (_c_int, [_u32p, _c_int, ctypes.c_uint32, ctypes.c_uint32, _c_i64, _c_i64,
                                  _c_int, _c_int, _vp, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp]),
+    "enks_noise_fill_multi": (_c_int, [_u32p, _c_int, _c_i64, _c_i64, _c_int, _c_int, _u32p, _u32p,
+                                       _ip, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "enks_member_sum_ws_bytes": (_c_i64, [_c_int, _c_i64, _c_int]),
     "enks_member_sum": (_c_int, [_vp, _c_i64, _c_int, _c_i64, _c_int, _vp, _vp, _vp, _vp]),
     "enks_member_center": (_c_int, [_vp, _c_i64, _c_int, _c_i64, _c_int, _vp, _vp, _c_i64, _vp,
@@ -55,6 +57,7 @@ _SIGS = {
     "enks_cnn_max_width": (_c_int, []),
     "enks_cnn_forward": (_c_int, [_c_int, _ip, _vp, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _vp,
                                   _c_i64, _c_int, _c_int, _c_i64, _vp]),
+    "enks_add": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _c_i64, _c_i64, _vp]),
     "enks_sub": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _c_i64, _c_i64, _vp]),
 }
 

@@ -38,6 +38,14 @@ __global__ void sub_kernel(const float* __restrict__ a, int64_t lda, const float
     out[r * ldo + c] = a[r * lda + c] - b[r * ldb + c];
 }
 
+__global__ void add_kernel(const float* __restrict__ a, int64_t lda, const float* __restrict__ b,
+                           int64_t ldb, float* out, int64_t ldo, int64_t rows, int64_t cols) {
+    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= rows * cols) return;
+    int64_t r = idx / cols, c = idx - r * cols;
+    out[r * ldo + c] = a[r * lda + c] + b[r * ldb + c];
+}
+
 }  // namespace enks
 
 extern "C" {
@@ -67,6 +75,16 @@ int enks_device_check(void) {
         return 0;
     }
     return h == 1000 ? 1 : 0;
+}
+
+int enks_add(const float* a, int64_t lda, const float* b, int64_t ldb, float* out, int64_t ldo,
+             int64_t rows, int64_t cols, void* stream) {
+    ENKS_REQUIRE(a && b && out, "enks_add: null pointer");
+    int64_t n = rows * cols;
+    if (n == 0) return ENKS_OK;
+    enks::add_kernel<<<(unsigned)((n + 255) / 256), 256, 0, enks::as_stream(stream)>>>(
+        a, lda, b, ldb, out, ldo, rows, cols);
+    return enks::check_launch("enks_add");
 }
 
 int enks_sub(const float* a, int64_t lda, const float* b, int64_t ldb, float* out, int64_t ldo,

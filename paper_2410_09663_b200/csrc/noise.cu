@@ -96,11 +96,9 @@ __device__ __forceinline__ Block4 philox(uint64_t k0, uint64_t k1, uint64_t ctr)
     return {c0, c1, c2, c3};
 }
 
-struct Args {
-    Head head;
+struct Job {
     uint32_t t, ch;
-    int64_t member0, n_members;
-    int rows, cols;
+    int rows;
     const double* diag;
     float* out;
     int64_t ld_out;
@@ -110,11 +108,21 @@ struct Args {
     int64_t ld_plus;
 };
 
+constexpr int kMaxJobs = 4;
+
+struct Args {
+    Head head;
+    int64_t member0, n_members;
+    int cols;
+    Job job[kMaxJobs];
+};
+
 __device__ __forceinline__ double u64_to_unit(uint64_t r) {
     return (double)(r >> 11) * (1.0 / 9007199254740992.0);
 }
 
-__global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args a) {
+__global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
+    const Job& a = args.job[blockIdx.y];
     __shared__ uint64_t s_ki[256];
     __shared__ double s_wi[256];
     __shared__ uint64_t s_buf[kWarps][kBufWords];
@@ -126,13 +134,14 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args a) {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t local = (int64_t)blockIdx.x * kWarps + warp;
-    if (local >= a.n_members) return;
+    if (local >= args.n_members) return;
     uint64_t k0, k1;
-    seed_key(a.head, (uint32_t)(a.member0 + local), a.t, a.ch, k0, k1);
+    seed_key(args.head, (uint32_t)(args.member0 + local), a.t, a.ch, k0, k1);
+    const int cols = args.cols;
 
     uint64_t* buf = s_buf[warp];
-    const int64_t total = (int64_t)a.rows * a.cols;
-    const int64_t col0 = local * a.cols;
+    const int64_t total = (int64_t)a.rows * cols;
+    const int64_t col0 = local * cols;
     int64_t base_w = -(1LL << 40);  // buffer holds words [base_w, base_w + 128)
     int64_t w = 0, q = 0;
 
@@ -140,15 +149,15 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args a) {
     int rb = 0, jb = 0;
     auto advance = [&](int k) {
         jb += k;
-        while (jb >= a.cols) {
-            jb -= a.cols;
+        while (jb >= cols) {
+            jb -= cols;
             ++rb;
         }
     };
     auto emit = [&](int off, double x) {  // normal q + off
         int r = rb, j = jb + off;
-        while (j >= a.cols) {
-            j -= a.cols;
+        while (j >= cols) {
+            j -= cols;
             ++r;
         }
         const double v = a.diag ? x * a.diag[r] : x;
@@ -235,35 +244,59 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args a) {
 }  // namespace
 }  // namespace enks
 
+namespace enks {
+namespace {
+int launch_noise(const uint32_t* head, int n_head, int64_t member0, int64_t n_members, int cols,
+                 const Job* jobs, int n_jobs, cudaStream_t st) {
+    ENKS_REQUIRE(head != nullptr && n_head >= 4 && n_head <= 32,
+                 "enks_noise_fill: need 4..32 head words (seed padded to 4 + prefix), got %d",
+                 n_head);
+    ENKS_REQUIRE(n_jobs >= 1 && n_jobs <= kMaxJobs, "enks_noise_fill: 1..%d jobs", kMaxJobs);
+    ENKS_REQUIRE(member0 >= 0 && member0 + n_members <= (1LL << 32),
+                 "enks_noise_fill: member ids must fit in uint32");
+    if (n_members <= 0 || cols <= 0) return ENKS_OK;
+    Args a;
+    for (int q = 0; q < 32; ++q) a.head.w[q] = q < n_head ? head[q] : 0u;
+    a.head.n = n_head;
+    a.member0 = member0;
+    a.n_members = n_members;
+    a.cols = cols;
+    for (int j = 0; j < n_jobs; ++j) {
+        ENKS_REQUIRE(jobs[j].out || jobs[j].out_plus, "enks_noise_fill: job %d has no output", j);
+        ENKS_REQUIRE(!jobs[j].out_plus || jobs[j].base, "enks_noise_fill: out_plus needs base");
+        ENKS_REQUIRE(jobs[j].rows > 0, "enks_noise_fill: job %d has no rows", j);
+        a.job[j] = jobs[j];
+    }
+    int64_t blocks = (n_members + kWarps - 1) / kWarps;
+    noise_kernel<<<dim3((unsigned)blocks, (unsigned)n_jobs), kWarps * 32, 0, st>>>(a);
+    return check_launch("enks_noise_fill");
+}
+}  // namespace
+}  // namespace enks
+
 extern "C" int enks_noise_fill(const uint32_t* head, int n_head, uint32_t t, uint32_t channel,
                                int64_t member0, int64_t n_members, int rows, int cols,
                                const double* diag, float* out, int64_t ld_out, const float* base,
                                int64_t ld_base, float* out_plus, int64_t ld_plus, void* stream) {
-    ENKS_REQUIRE(head != nullptr && n_head >= 4 && n_head <= 32,
-                 "enks_noise_fill: need 4..32 head words (seed padded to 4 + prefix), got %d",
-                 n_head);
-    ENKS_REQUIRE(out || out_plus, "enks_noise_fill: no output");
-    ENKS_REQUIRE(!out_plus || base, "enks_noise_fill: out_plus needs base");
-    ENKS_REQUIRE(member0 >= 0 && member0 + n_members <= (1LL << 32),
-                 "enks_noise_fill: member ids must fit in uint32");
-    if (n_members <= 0 || rows <= 0 || cols <= 0) return ENKS_OK;
-    enks::Args a;
-    for (int q = 0; q < 32; ++q) a.head.w[q] = q < n_head ? head[q] : 0u;
-    a.head.n = n_head;
-    a.t = t;
-    a.ch = channel;
-    a.member0 = member0;
-    a.n_members = n_members;
-    a.rows = rows;
-    a.cols = cols;
-    a.diag = diag;
-    a.out = out;
-    a.ld_out = ld_out;
-    a.base = base;
-    a.ld_base = ld_base;
-    a.out_plus = out_plus;
-    a.ld_plus = ld_plus;
-    int64_t blocks = (n_members + enks::kWarps - 1) / enks::kWarps;
-    enks::noise_kernel<<<(unsigned)blocks, enks::kWarps * 32, 0, enks::as_stream(stream)>>>(a);
-    return enks::check_launch("enks_noise_fill");
+    if (rows <= 0) return ENKS_OK;
+    enks::Job j{t, channel, rows, diag, out, ld_out, base, ld_base, out_plus, ld_plus};
+    return enks::launch_noise(head, n_head, member0, n_members, cols, &j, 1,
+                              enks::as_stream(stream));
+}
+
+extern "C" int enks_noise_fill_multi(const uint32_t* head, int n_head, int64_t member0,
+                                     int64_t n_members, int cols, int n_jobs,
+                                     const uint32_t* t, const uint32_t* channel, const int* rows,
+                                     const double* const* diag, float* const* out,
+                                     const int64_t* ld_out, const float* const* base,
+                                     const int64_t* ld_base, float* const* out_plus,
+                                     const int64_t* ld_plus, void* stream) {
+    ENKS_REQUIRE(n_jobs >= 1 && n_jobs <= enks::kMaxJobs, "enks_noise_fill_multi: 1..%d jobs",
+                 enks::kMaxJobs);
+    enks::Job jobs[enks::kMaxJobs];
+    for (int q = 0; q < n_jobs; ++q)
+        jobs[q] = enks::Job{t[q], channel[q], rows[q], diag[q], out[q], ld_out[q],
+                            base[q], ld_base[q], out_plus[q], ld_plus[q]};
+    return enks::launch_noise(head, n_head, member0, n_members, cols, jobs, n_jobs,
+                              enks::as_stream(stream));
 }

@@ -232,6 +232,11 @@ class DeviceSmoother:
         self.noise_w = _noise_params(vs.process_noise, ops, self.l, self.m)
         self.noise_vx = _noise_params(vs.obs_noise_x, ops, self.n, self.m)
         self.noise_vu = _noise_params(vs.obs_noise_u, ops, self.l, self.m)
+        # all channels diagonal: draw W, V_X, V_U of a step in one launch during predict
+        self.fused_noise = (all(c.kind == "diag" for c in (self.noise_w, self.noise_vx, self.noise_vu))
+                            and hasattr(ops, "noise_fill_multi"))
+        self._obs_t = -1
+        self._obs_key = None
         self._bound = vs
 
     # ------------------------------------------------------------ helpers
@@ -282,11 +287,26 @@ class DeviceSmoother:
             self._grow(max(2 * self.cap, tau))
         ops, n, l, d = self.ops, self.n, self.l, self.d
         head = entropy_head(streams.seed, tuple(streams.prefix))
-        sr = self.slice_raw
-        # ΔU slot = w, U slot = u + w  (one draw fills both, enks.py:168)
-        self._noise(self.noise_w, head, tau, CH_W, l, out=sr[n + l:], base=self.last[n:],
-                    out_plus=sr[n:n + l])
+        sr, ob = self.slice_raw, self.obs_raw
         self.forecast(ops, self.last, sr[:n], n, self.Nl)
+        if self.fused_noise:
+            # W (enks.py:165-168) and this step's observation noise V_X, V_U (enks.py:194-200,
+            # drawn at t = tau with the same substream ids update() would use) in one launch:
+            # dU = w, U = u + w, obs_x = x' + v_x, obs_u <- v_u (u + w added below)
+            ops.noise_fill_multi(head, self.member0, self.Nl, self.m, [
+                dict(t=tau, ch=CH_W, rows=l, diag=self.noise_w.diag, out=sr[n + l:],
+                     base=self.last[n:], out_plus=sr[n:n + l]),
+                dict(t=tau, ch=CH_VX, rows=n, diag=self.noise_vx.diag, base=sr[:n],
+                     out_plus=ob[:n]),
+                dict(t=tau, ch=CH_VU, rows=l, diag=self.noise_vu.diag, out=ob[n:]),
+            ])
+            ops.add(sr[n:n + l], ob[n:], ob[n:])
+            self._obs_t = tau
+            self._obs_key = (streams.seed, tuple(streams.prefix))
+        else:
+            # ΔU slot = w, U slot = u + w  (one draw fills both, enks.py:168)
+            self._noise(self.noise_w, head, tau, CH_W, l, out=sr[n + l:], base=self.last[n:],
+                        out_plus=sr[n:n + l])
         self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d])
         self.t = tau
 
@@ -300,8 +320,9 @@ class DeviceSmoother:
         head = entropy_head(streams.seed, tuple(streams.prefix))
         sr, ob = self.slice_raw, self.obs_raw
         # perturbed observations [x + v_x; u + v_u]  (enks.py:194-200)
-        self._noise(self.noise_vx, head, tau, CH_VX, n, base=sr[:n], out_plus=ob[:n])
-        self._noise(self.noise_vu, head, tau, CH_VU, l, base=sr[n:n + l], out_plus=ob[n:])
+        if self._obs_t != tau or self._obs_key != (streams.seed, tuple(streams.prefix)):
+            self._noise(self.noise_vx, head, tau, CH_VX, n, base=sr[:n], out_plus=ob[:n])
+            self._noise(self.noise_vu, head, tau, CH_VU, l, base=sr[n:n + l], out_plus=ob[n:])
         yc = self.Ybuf[(tau - 1) * p:tau * p]
         self._center(ob, self.ybar, yc)
 
@@ -374,6 +395,7 @@ class DeviceSmoother:
     def replace_members(self, members_local: np.ndarray, t: int) -> None:
         """Reset the representation to explicit members (local shard, (Nl, (t+1)d, m))."""
         ops, d = self.ops, self.d
+        self._obs_t = -1
         self.t = 0
         self._grow(max(t, 1))
         self.t = int(t)

@@ -93,6 +93,26 @@ class DeviceOps:
                   _ld(base) if base is not None else 0, _p(out_plus),
                   _ld(out_plus) if out_plus is not None else 0, self._stream())
 
+    def noise_fill_multi(self, head, member0, n_members, cols, jobs):
+        """jobs: list of dicts (t, ch, rows, diag, out, base, out_plus); one launch."""
+        n = len(jobs)
+        words = (ctypes.c_uint32 * len(head))(*[int(w) for w in head])
+        u32 = ctypes.c_uint32 * n
+        vp = ctypes.c_void_p * n
+        i64 = ctypes.c_int64 * n
+        get = lambda k: [j.get(k) for j in jobs]  # noqa: E731
+        self.launches += 1
+        _lib.call("enks_noise_fill_multi", words, len(head), int(member0), int(n_members), int(cols),
+                  n, u32(*[int(j["t"]) for j in jobs]), u32(*[int(j["ch"]) for j in jobs]),
+                  (ctypes.c_int * n)(*[int(j["rows"]) for j in jobs]),
+                  vp(*[_p(v) for v in get("diag")]), vp(*[_p(v) for v in get("out")]),
+                  i64(*[_ld(v) if v is not None else 0 for v in get("out")]),
+                  vp(*[_p(v) for v in get("base")]),
+                  i64(*[_ld(v) if v is not None else 0 for v in get("base")]),
+                  vp(*[_p(v) for v in get("out_plus")]),
+                  i64(*[_ld(v) if v is not None else 0 for v in get("out_plus")]),
+                  self._stream())
+
     def member_sum(self, src, n_members, cols, z0, acc):
         rows = src.shape[0]
         nbytes = self.lib.enks_member_sum_ws_bytes(rows, n_members, cols)
@@ -182,6 +202,11 @@ class DeviceOps:
         _lib.call("enks_cnn_forward", cnn.n_layers, widths, _p(cnn.w_dev), _p(cnn.b_dev),
                   float(cnn.alpha), _p(x), _ld(x), _p(u), _ld(u), _p(out), _ld(out),
                   int(x.shape[0]), int(cnn.cols), int(n_members), self._stream())
+
+    def add(self, a, b, out):
+        self.launches += 1
+        _lib.call("enks_add", _p(a), _ld(a), _p(b), _ld(b), _p(out), _ld(out), out.shape[0],
+                  out.shape[1], self._stream())
 
     def sub(self, a, b, out):
         self.launches += 1

@@ -54,6 +54,15 @@ class CpuOps:
         if out_plus is not None:
             out_plus.copy_(base + blk)
 
+    def noise_fill_multi(self, head, member0, n_members, cols, jobs):
+        for j in jobs:
+            self.noise_fill(head, j["t"], j["ch"], member0, n_members, j["rows"], cols,
+                            diag=j.get("diag"), out=j.get("out"), base=j.get("base"),
+                            out_plus=j.get("out_plus"))
+
+    def add(self, a, b, out):
+        out.copy_(a + b)
+
     def member_sum(self, src, n_members, cols, z0, acc):
         s = src.reshape(src.shape[0], n_members, cols)
         shift = s[:, 0, :] if z0 is None else z0

@@ -242,3 +242,39 @@ def test_cnn_forward_tcgen05_matches_simt_many_members(dev_ops, pm, monkeypatch)
     torch.cuda.synchronize()
     diff = (out_tc - out_simt).abs().max().item()
     assert diff < 2e-5, diff
+
+
+@pytest.mark.parametrize("p", [33, 100, 288])
+def test_spd_inverse_blocked_sizes(dev_ops, p):
+    """Tile padding (p not a multiple of 32) and the largest supported p."""
+    rng = np.random.default_rng(p + 1)
+    a = rng.standard_normal((p, 2 * p))
+    s = (a @ a.T / (2 * p) + 0.2 * np.eye(p)).astype(np.float32)
+    inv = dev_ops.zeros(p, p)
+    st, jit = dev_ops.zeros(1, dtype=torch.int32), dev_ops.zeros(1, dtype=torch.int32)
+    dev_ops.spd_inverse(dev_ops.to_device(s), 1.0, inv, st, jit)
+    ref = np.linalg.inv(s.astype(np.float64))
+    assert st.item() == 0 and jit.item() == 0
+    np.testing.assert_allclose(_cpu(inv), ref, rtol=2e-4, atol=2e-4 * np.abs(ref).max())
+
+
+def test_fused_noise_multi_matches_single(dev_ops):
+    """One launch for (W, V_X, V_U) == three enks_noise_fill launches, bit for bit."""
+    from paper_2410_09663_b200.matvar import entropy_head
+
+    N, cols, rows = 9, 6, (3, 5, 3)
+    head = entropy_head(4, (1,))
+    diag = [dev_ops.to_device(np.linspace(0.5, 2.0, r), dtype=torch.float64) for r in rows]
+    base = [torch.randn(r, N * cols, device=dev_ops.device) for r in rows]
+    single = [dev_ops.zeros(r, N * cols) for r in rows]
+    plus1 = [dev_ops.zeros(r, N * cols) for r in rows]
+    for k, r in enumerate(rows):
+        dev_ops.noise_fill(head, 7, k, 0, N, r, cols, diag=diag[k], out=single[k], base=base[k],
+                           out_plus=plus1[k])
+    multi = [dev_ops.zeros(r, N * cols) for r in rows]
+    plus2 = [dev_ops.zeros(r, N * cols) for r in rows]
+    dev_ops.noise_fill_multi(head, 0, N, cols, [dict(t=7, ch=k, rows=r, diag=diag[k], out=multi[k],
+                                                     base=base[k], out_plus=plus2[k])
+                                                for k, r in enumerate(rows)])
+    for k in range(3):
+        assert torch.equal(single[k], multi[k]) and torch.equal(plus1[k], plus2[k])
