@@ -125,10 +125,26 @@ int enks_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, float a
  */
 int64_t enks_tc_gemm_ws_bytes(int64_t M, int64_t N, int64_t K, int split_k);
 int enks_tf32_split(const float* src, int64_t ld, int64_t rows, int64_t cols, float* hi, float* lo,
-                    void* stream);
+                    int transpose, void* stream);
 int enks_gemm_nt_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
                     const float* Bh, const float* Bl, int64_t ldb, float* C, int64_t ldc,
                     int split_k, void* ws, void* stream);
+
+/*
+ * General tcgen05 3xTF32 GEMM with a pre-split B (B = Bh + Bl):
+ *   C = alpha * A op(B) + beta * C0 + bias[r, c % bias_cols]
+ * b_mn_major = 0: Bh/Bl are N x K (K-major; op(B) = B^T, any N, N-tiles of 256);
+ * b_mn_major = 1: K x N MN-major operands (experimental, not used by the engine).
+ * enks_tf32_split(..., transpose=1) produces the K-major planes of a K x N matrix.
+ * tri_rows/tri_k as in enks_gemm.  Used for the newest-slice member shift
+ * (enks.py:247 restated), the gain correction and the gain itself.
+ * `ws`: split_k * M * N floats when split_k != 1 (split_k <= 0: auto).
+ */
+int enks_gemm_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
+                 const float* Bh, const float* Bl, int64_t ldb, int b_mn_major, float beta,
+                 const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias, int bias_cols,
+                 float* C, int64_t ldc, int64_t tri_rows, int64_t tri_k, int split_k, void* ws,
+                 void* stream);
 
 /*
  * Gain solve (K8).  Replaces enks.py:234-235 (symmetrize) and 238-246

@@ -49,9 +49,12 @@ _SIGS = {
                            _c_f, _vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_i64, _c_i64,
                            _c_int, _vp, _c_int, _vp]),
     "enks_tc_gemm_ws_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64, _c_int]),
-    "enks_tf32_split": (_c_int, [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp]),
+    "enks_tf32_split": (_c_int, [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_int, _vp]),
     "enks_gemm_nt_tc": (_c_int, [_c_i64, _c_i64, _c_i64, _c_f, _vp, _c_i64, _vp, _vp, _c_i64, _vp,
                                  _c_i64, _c_int, _vp, _vp]),
+    "enks_gemm_tc": (_c_int, [_c_i64, _c_i64, _c_i64, _c_f, _vp, _c_i64, _vp, _vp, _c_i64, _c_int,
+                              _c_f, _vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_i64, _c_i64,
+                              _c_int, _vp, _vp]),
     "enks_spd_max_p": (_c_int, []),
     "enks_spd_inverse": (_c_int, [_vp, _c_i64, _c_int, _c_f, _vp, _vp, _vp, _vp, _vp]),
     "enks_cnn_max_width": (_c_int, []),

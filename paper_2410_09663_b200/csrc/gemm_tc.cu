@@ -1,21 +1,26 @@
-// tcgen05 3xTF32 engine for the cross-moment contraction (K6/K7):
-//     C[M x N] = alpha * A[M x K] B[N x K]^T        (both operands K-major, fp32 in HBM)
-// Reference: enks.py:148-153 (_pair_covariance) and 234-236 (Sigma_y, Sigma_xy), here
-// applied to the append-only basis of engine.py (P = [A; Yc] Yc^T).
+// tcgen05 3xTF32 GEMM engine for the path's contractions:
+//   NT  C[M x N] = alpha * A[M x K] B[N x K]^T           (cross moments K6/K7: P = [A; Yc] Yc^T,
+//                                                         enks.py:148-153, 234-236)
+//   NN  C[M x N] = alpha * A[M x K] B[K x N] + beta C0 + bias[r, c % bias_cols]
+//                                                        (member shift / correction / gain
+//                                                         products, enks.py:246-247)
+// A is fp32 row-major (K-major), split in-kernel; B arrives pre-split as (hi, lo)
+// fp32 planes, K-major (NT) or MN-major (NN).
 //
-// Precision: fp32 operands are split x = hi + lo with hi = rna_tf32(x); the MMA
-// accumulates hi*hi + hi*lo + lo*hi in fp32 (TMEM), which matches fp32 FFMA
-// accuracy (the dropped lo*lo term is ~2^-22 relative).  1xTF32 misses the 1e-4
-// parity bar.
+// Precision: x = hi + lo with hi = rna_tf32(x); the MMAs accumulate lo*hi + hi*lo + hi*hi,
+// matching fp32 FFMA accuracy (the dropped lo*lo term is ~2^-22 relative).  The tensor core
+// accumulates into TMEM with truncation; over long K chains that bias reaches ~1e-6 relative
+// (tools/tc_acc_probe.py), so the MMA warp restarts a fresh TMEM slot every kChainChunks
+// chunks (two slots, ping-pong) and the epilogue warps fold each finished chain into fp32
+// registers with round-to-nearest adds while the other slot fills.
 //
-// Structure (one 128 x BN output tile and one K range per CTA, 1 CTA / SM):
-//   warp 0      TMA producer: A tile (128 x 32 fp32, SWIZZLE_128B) + pre-split B_hi, B_lo
-//   warps 4..7  converters: split their A row into hi (in place) / lo (second buffer),
-//               fence.proxy.async, arrive; later the epilogue (tcgen05.ld -> HBM)
+// Structure (one 128 x BN output tile and one K range per CTA, 1 CTA / SM, 384 threads):
+//   warp 0      TMA producer: A tile (128 x 32 fp32, SWIZZLE_128B) + B_hi, B_lo tiles
 //   warp 1      MMA issuer: 4 K-steps x 3 tcgen05.mma.kind::tf32 (M=128, N=BN, K=8) per stage
 //   warp 2      TMEM allocator
-// mbarrier rings: full (TMA bytes), conv (128 converter arrivals), empty (tcgen05.commit).
-// Split-K partials go to a workspace and are summed in a fixed order (deterministic).
+//   warps 4-11  converters (A -> hi in place / lo, fence.proxy.async), then the epilogue
+// mbarrier rings: full (TMA bytes), conv (256 converter arrivals), empty (tcgen05.commit),
+// tfull/tempty (TMEM chain slots).  Split-K partials are summed in a fixed order.
 #include <cuda.h>
 #include <stdlib.h>
 
@@ -32,35 +37,50 @@ constexpr int kChainChunks = 4;      // TMEM accumulation chain = 4 x 32 = 128 K
 
 struct TcParams {
     int64_t M, N, K;
-    float alpha;
-    float* out;   // split partial base (ws) or C
+    float alpha, beta;
+    float* out;            // split partial base (ws) or C
     int64_t ldo;
     int64_t split_stride;  // elements between split partials (0 if writing C directly)
-    int chunks_per_split;
-    int total_chunks;
+    const float* C0;       // direct mode only
+    int64_t ldc0;
+    const float* bias;     // direct mode only
+    int64_t ld_bias;
+    int bias_cols;
+    int64_t tri_rows, tri_k;  // block-triangular A: row tile r0 starts at k = (r0/tri_rows)*tri_k
+    int splits;
     int stages;
-    int products;  // bitmask: 1 = lo*hi, 2 = hi*lo, 4 = hi*hi (debug knob ENKS_TC_PRODUCTS; default 7)
+    int products;  // bitmask: 1 = lo*hi, 2 = hi*lo, 4 = hi*hi (debug knob ENKS_TC_PRODUCTS)
+    uint32_t mn_lbo, mn_sbo;  // MN-major B descriptor strides (debug knob ENKS_TC_MN)
 };
 
 template <int BN>
 struct Layout {
     static constexpr int kA = BM * BK * 4;     // 16 KB (hi in place)
-    static constexpr int kB = BN * BK * 4;     // BN x 128 B
+    static constexpr int kB = BN * BK * 4;     // BN x 32 fp32
     static constexpr int kStage = 2 * kA + 2 * kB;
     static constexpr int kSlotCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
     static constexpr int kEpiWG = BN > 128 ? 2 : 1;         // warpgroups holding the fp32 sums
     static constexpr int kColsPerWG = BN > 128 ? BN / 2 : BN;
 };
 
-// The tensor core accumulates into TMEM with truncation; over long K chains that
-// bias reaches ~1e-6 relative (measured: tools/tc_acc_probe.py).  The MMA warp
-// therefore restarts a fresh TMEM slot every kChainChunks chunks (two slots,
-// ping-pong) and the epilogue warps fold each finished chain into fp32 registers
-// with round-to-nearest adds while the other slot fills.
-template <int BN>
+// UMMA descriptor, MN-major SWIZZLE_128B: 32-element (128 B) MN atoms LBO bytes apart,
+// 8-row K groups 1024 B apart.
+__device__ __forceinline__ uint64_t desc_mnmajor_sw128(const void* smem, uint32_t lbo,
+                                                       uint32_t sbo = 1024) {
+    const uint64_t addr = ptx::smem_u32(smem);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+template <int BN, bool BMN>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_nt_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
-                 const __grid_constant__ CUtensorMap tmBl, const TcParams p) {
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
+                   const __grid_constant__ CUtensorMap tmBl, const TcParams p) {
     using L = Layout<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -75,10 +95,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * BM;
-    const int split = blockIdx.y;
-    const int c_lo = split * p.chunks_per_split;
-    const int c_hi = min(p.total_chunks, c_lo + p.chunks_per_split);
-    const int n_chunks = max(0, c_hi - c_lo);
+    const int64_t col0 = (int64_t)blockIdx.y * BN;
+    const int split = blockIdx.z;
+    // K range of this CTA: [kbeg, K) split evenly (in BK chunks) over the splits
+    int64_t kbeg = 0;
+    if (p.tri_rows > 0) kbeg = (row0 / p.tri_rows) * p.tri_k;
+    kbeg = (kbeg / BK) * BK;
+    if (kbeg > p.K) kbeg = p.K;
+    const int total_chunks = (int)((p.K - kbeg + BK - 1) / BK);
+    const int cps = (total_chunks + p.splits - 1) / p.splits;
+    const int c_lo = min(total_chunks, split * cps);
+    const int c_hi = min(total_chunks, c_lo + cps);
+    const int n_chunks = c_hi - c_lo;
     const int n_groups = (n_chunks + kChainChunks - 1) / kChainChunks;
     constexpr uint32_t kTmemCols = 2 * L::kSlotCols;
 
@@ -115,15 +143,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t ph = (uint32_t)((i / S) & 1);
                 ptx::mbar_wait(&empty[s], ph ^ 1);
                 ptx::mbar_arrive_expect_tx(&full[s], L::kA + 2 * L::kB);
-                const int kc = (c_lo + i) * BK;
+                const int kc = (int)(kbeg + (int64_t)(c_lo + i) * BK);
                 ptx::tma_load_2d(&tmA, &full[s], stage_a(s), kc, (int32_t)row0);
-                ptx::tma_load_2d(&tmBh, &full[s], stage_bh(s), kc, 0);
-                ptx::tma_load_2d(&tmBl, &full[s], stage_bl(s), kc, 0);
+                if (!BMN) {
+                    ptx::tma_load_2d(&tmBh, &full[s], stage_bh(s), kc, (int32_t)col0);
+                    ptx::tma_load_2d(&tmBl, &full[s], stage_bl(s), kc, (int32_t)col0);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BN / 32; ++j) {
+                        ptx::tma_load_2d(&tmBh, &full[s], stage_bh(s) + j * 4096,
+                                         (int32_t)(col0 + 32 * j), kc);
+                        ptx::tma_load_2d(&tmBl, &full[s], stage_bl(s) + j * 4096,
+                                         (int32_t)(col0 + 32 * j), kc);
+                    }
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_tf32(BM, BN);
+            uint32_t idesc = ptx::idesc_tf32(BM, BN);
+            if (BMN) idesc |= 1u << 16;  // B MN-major
             for (int i = 0; i < n_chunks; ++i) {
                 const int s = i % S;
                 const uint32_t ph = (uint32_t)((i / S) & 1);
@@ -141,8 +180,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < BK / 8; ++k) {
                     const uint64_t ah = ptx::desc_kmajor_sw128(stage_a(s) + 32 * k);
                     const uint64_t al = ptx::desc_kmajor_sw128(stage_alo(s) + 32 * k);
-                    const uint64_t bh = ptx::desc_kmajor_sw128(stage_bh(s) + 32 * k);
-                    const uint64_t bl = ptx::desc_kmajor_sw128(stage_bl(s) + 32 * k);
+                    uint64_t bh, bl;
+                    if (!BMN) {
+                        bh = ptx::desc_kmajor_sw128(stage_bh(s) + 32 * k);
+                        bl = ptx::desc_kmajor_sw128(stage_bl(s) + 32 * k);
+                    } else {
+                        bh = desc_mnmajor_sw128(stage_bh(s) + 1024 * k, p.mn_lbo, p.mn_sbo);
+                        bl = desc_mnmajor_sw128(stage_bl(s) + 1024 * k, p.mn_lbo, p.mn_sbo);
+                    }
                     uint32_t acc = (first && k == 0) ? 0u : 1u;
                     if (p.products & 1) { ptx::mma_tf32_ss(d, al, bh, idesc, acc); acc = 1u; }
                     if (p.products & 2) { ptx::mma_tf32_ss(d, ah, bl, idesc, acc); acc = 1u; }
@@ -213,19 +258,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (epi) {
             for (int g = drained; g < n_groups; ++g) drain(g);
             const int64_t r = row0 + erow;
-            if (r < p.M) {
-                float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + wg * L::kColsPerWG;
-                const int ncol = (int)min((int64_t)L::kColsPerWG, p.N - (int64_t)wg * L::kColsPerWG);
-                if (ncol == L::kColsPerWG && (p.ldo & 3) == 0) {
+            const int64_t c_first = col0 + wg * L::kColsPerWG;
+            if (r < p.M && c_first < p.N) {
+                float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + c_first;
+                const int ncol = (int)min((int64_t)L::kColsPerWG, p.N - c_first);
+                const bool direct = p.split_stride == 0;
+                const float* c0row = (direct && p.C0) ? p.C0 + r * p.ldc0 + c_first : nullptr;
+                const float* brow = (direct && p.bias) ? p.bias + r * p.ld_bias : nullptr;
+                const bool vec = ncol == L::kColsPerWG && ((p.ldo & 3) == 0) &&
+                                 ((reinterpret_cast<uintptr_t>(orow) & 15) == 0) &&
+                                 (!c0row || (reinterpret_cast<uintptr_t>(c0row) & 15) == 0);
+                if (vec) {
 #pragma unroll
-                    for (int j = 0; j < L::kColsPerWG; j += 4)
-                        *reinterpret_cast<float4*>(orow + j) =
-                            make_float4(p.alpha * acc[j], p.alpha * acc[j + 1], p.alpha * acc[j + 2],
-                                        p.alpha * acc[j + 3]);
+                    for (int j = 0; j < L::kColsPerWG; j += 4) {
+                        float4 v = make_float4(p.alpha * acc[j], p.alpha * acc[j + 1],
+                                               p.alpha * acc[j + 2], p.alpha * acc[j + 3]);
+                        if (c0row) {
+                            const float4 c = *reinterpret_cast<const float4*>(c0row + j);
+                            v.x += p.beta * c.x; v.y += p.beta * c.y;
+                            v.z += p.beta * c.z; v.w += p.beta * c.w;
+                        }
+                        if (brow) {
+                            v.x += brow[(c_first + j) % p.bias_cols];
+                            v.y += brow[(c_first + j + 1) % p.bias_cols];
+                            v.z += brow[(c_first + j + 2) % p.bias_cols];
+                            v.w += brow[(c_first + j + 3) % p.bias_cols];
+                        }
+                        *reinterpret_cast<float4*>(orow + j) = v;
+                    }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < L::kColsPerWG; ++j)
-                        if (j < ncol) orow[j] = p.alpha * acc[j];
+                    for (int j = 0; j < L::kColsPerWG; ++j) {
+                        if (j < ncol) {
+                            float v = p.alpha * acc[j];
+                            if (c0row) v += p.beta * c0row[j];
+                            if (brow) v += brow[(c_first + j) % p.bias_cols];
+                            orow[j] = v;
+                        }
+                    }
                 }
             }
         }
@@ -236,25 +306,52 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 __global__ void tf32_split_kernel(const float* __restrict__ src, int64_t ld, int64_t rows,
-                                  int64_t cols, float* __restrict__ hi, float* __restrict__ lo) {
+                                  int64_t cols, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t ldo) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= rows * cols) return;
     const int64_t r = e / cols, c = e - r * cols;
     const float v = src[r * ld + c];
     const float h = ptx::tf32_round(v);
-    hi[e] = h;
-    lo[e] = v - h;
+    hi[r * ldo + c] = h;
+    lo[r * ldo + c] = v - h;
+}
+
+// hi/lo split with transpose: src (rows x cols, ld) -> hi, lo (cols x rows, ldo); 32x32 smem tiles
+__global__ void tf32_split_t_kernel(const float* __restrict__ src, int64_t ld, int64_t rows,
+                                    int64_t cols, float* __restrict__ hi, float* __restrict__ lo,
+                                    int64_t ldo) {
+    __shared__ float tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const int64_t r = r0 + ty + k, c = c0 + tx;
+        tile[ty + k][tx] = (r < rows && c < cols) ? src[r * ld + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const int64_t c = c0 + ty + k, r = r0 + tx;  // output row c, column r
+        if (c < cols && r < rows) {
+            const float v = tile[tx][ty + k];
+            const float h = ptx::tf32_round(v);
+            hi[c * ldo + r] = h;
+            lo[c * ldo + r] = v - h;
+        }
+    }
 }
 
 __global__ void sum_splits_kernel(const float* __restrict__ ws, int split, int64_t M, int64_t N,
-                                  float* __restrict__ C, int64_t ldc, const float* __restrict__ C0,
-                                  int64_t ldc0, float beta) {
+                                  float* C, int64_t ldc, const float* C0, int64_t ldc0, float beta,
+                                  const float* __restrict__ bias, int64_t ld_bias, int bias_cols) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= M * N) return;
     const int64_t r = e / N, c = e - r * N;
     float v = 0.f;
     for (int z = 0; z < split; ++z) v += ws[(int64_t)z * M * N + e];
     if (C0) v += beta * C0[r * ldc0 + c];
+    if (bias) v += bias[r * ld_bias + (c % bias_cols)];
     C[r * ldc + c] = v;
 }
 
@@ -276,13 +373,14 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+// 2-D fp32 tensor map over a row-major (rows x cols, ld) matrix; box = box_cols x box_rows
 bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld,
-              int box_rows) {
+              int box_cols, int box_rows) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -292,9 +390,9 @@ bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, i
 
 int bn_for(int64_t N) { return N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256)); }
 
-template <int BN>
+template <int BN, bool BMN>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& ml, TcParams p,
-              int tiles, int split, cudaStream_t st) {
+              dim3 grid, cudaStream_t st) {
     using L = Layout<BN>;
     int stages = kSmemBudget / L::kStage;
     if (stages > 4) stages = 4;
@@ -306,7 +404,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& m
     const size_t smem = (size_t)stages * L::kStage + 1024 + 512;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tc_nt_kernel<BN>,
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, BMN>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) {
             set_error("tc gemm: smem attribute: %s", cudaGetErrorString(e));
@@ -314,16 +412,22 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& m
         }
         configured = true;
     }
-    dim3 grid((unsigned)tiles, (unsigned)split);
-    tc_nt_kernel<BN><<<grid, kThreads, smem, st>>>(ma, mh, ml, p);
+    tc_gemm_kernel<BN, BMN><<<grid, kThreads, smem, st>>>(ma, mh, ml, p);
     return check_launch("enks_gemm(tcgen05)");
 }
 
-}  // namespace
+template <bool BMN>
+int dispatch_bn(int BN, const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& ml,
+                const TcParams& p, dim3 grid, cudaStream_t st) {
+    switch (BN) {
+        case 32: return launch_tc<32, BMN>(ma, mh, ml, p, grid, st);
+        case 64: return launch_tc<64, BMN>(ma, mh, ml, p, grid, st);
+        case 128: return launch_tc<128, BMN>(ma, mh, ml, p, grid, st);
+        default: return launch_tc<256, BMN>(ma, mh, ml, p, grid, st);
+    }
+}
 
-int tc_choose_split(int64_t M, int64_t K) {
-    const int tiles = (int)((M + BM - 1) / BM);
-    const int chunks = (int)((K + BK - 1) / BK);
+int choose_split(int tiles, int64_t chunks) {
     int best = 1;
     double best_eff = 0.0;
     for (int s = 1; s <= 64; ++s) {
@@ -340,6 +444,12 @@ int tc_choose_split(int64_t M, int64_t K) {
     return best;
 }
 
+}  // namespace
+
+int tc_choose_split(int64_t M, int64_t K) {
+    return choose_split((int)((M + BM - 1) / BM), (K + BK - 1) / BK);
+}
+
 bool tc_gemm_applicable(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A,
                         int64_t lda, const float* B, int64_t ldb, int64_t tri_rows) {
     if (trans_a || !trans_b || tri_rows > 0) return false;
@@ -349,32 +459,41 @@ bool tc_gemm_applicable(int trans_a, int trans_b, int64_t M, int64_t N, int64_t 
     return encode_fn() != nullptr;
 }
 
-// A raw fp32 (M x K, lda); B pre-split (Bh, Bl: N x K, ldb).  Writes C = alpha A B^T (+ beta C0).
-int gemm_tc_presplit(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
-                     const float* Bh, const float* Bl, int64_t ldb, float beta, const float* C0,
-                     int64_t ldc0, float* C, int64_t ldc, int split, float* ws, cudaStream_t st) {
-    const int BN = bn_for(N);
+int gemm_tc_general(bool bmn, int64_t M, int64_t N, int64_t K, float alpha, const float* A,
+                    int64_t lda, const float* Bh, const float* Bl, int64_t ldb, float beta,
+                    const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias,
+                    int bias_cols, float* C, int64_t ldc, int64_t tri_rows, int64_t tri_k,
+                    int split, float* ws, cudaStream_t st) {
+    if (M == 0 || N == 0) return ENKS_OK;
+    const int BN = N >= 256 ? 256 : bn_for(N);
     CUtensorMap ma, mh, ml;
-    if (!make_map(&ma, A, M, K, lda, BM) || !make_map(&mh, Bh, N, K, ldb, BN) ||
-        !make_map(&ml, Bl, N, K, ldb, BN)) {
-        set_error("tc gemm: cuTensorMapEncodeTiled failed");
+    bool ok = make_map(&ma, A, M, K, lda, BK, BM);
+    if (!bmn) {
+        ok = ok && make_map(&mh, Bh, N, K, ldb, BK, BN) && make_map(&ml, Bl, N, K, ldb, BK, BN);
+    } else {
+        ok = ok && make_map(&mh, Bh, K, N, ldb, 32, BK) && make_map(&ml, Bl, K, N, ldb, 32, BK);
+    }
+    if (!ok) {
+        set_error("tc gemm: cuTensorMapEncodeTiled failed (alignment / ld %% 4?)");
         return ENKS_E_UNSUPPORTED;
     }
-    const int tiles = (int)((M + BM - 1) / BM);
-    const int total_chunks = (int)((K + BK - 1) / BK);
-    if (split < 1) split = tc_choose_split(M, K);
-    const int cps = (total_chunks + split - 1) / split;
-    split = (total_chunks + cps - 1) / cps;
+    const int m_tiles = (int)((M + BM - 1) / BM);
+    const int n_tiles = (int)((N + BN - 1) / BN);
+    if (split < 1) split = choose_split(m_tiles * n_tiles, (K + BK - 1) / BK);
     TcParams p;
     p.M = M; p.N = N; p.K = K;
-    p.alpha = alpha;
-    p.chunks_per_split = cps;
+    p.alpha = alpha; p.beta = beta;
+    p.tri_rows = tri_rows; p.tri_k = tri_k;
+    p.splits = split;
     {
         const char* e = getenv("ENKS_TC_PRODUCTS");
         p.products = e ? atoi(e) : 7;
+        const char* m = getenv("ENKS_TC_MN");
+        const int mode = m ? atoi(m) : 0;
+        p.mn_lbo = mode == 1 ? 1024 : (mode == 2 ? 4096 : (mode == 3 ? 1024 : 4096));
+        p.mn_sbo = mode == 1 ? 4096 : (mode == 2 ? 4096 : (mode == 3 ? 1024 : 1024));
     }
-    p.total_chunks = total_chunks;
-    const bool direct = (split == 1 && C0 == nullptr);
+    const bool direct = (split == 1);
     if (!direct && !ws) {
         set_error("tc gemm: split-K needs workspace");
         return ENKS_E_ARG;
@@ -382,30 +501,48 @@ int gemm_tc_presplit(int64_t M, int64_t N, int64_t K, float alpha, const float* 
     p.out = direct ? C : ws;
     p.ldo = direct ? ldc : N;
     p.split_stride = direct ? 0 : M * N;
-    int rc;
-    switch (BN) {
-        case 32: rc = launch_tc<32>(ma, mh, ml, p, tiles, split, st); break;
-        case 64: rc = launch_tc<64>(ma, mh, ml, p, tiles, split, st); break;
-        case 128: rc = launch_tc<128>(ma, mh, ml, p, tiles, split, st); break;
-        default: rc = launch_tc<256>(ma, mh, ml, p, tiles, split, st); break;
-    }
+    p.C0 = direct ? C0 : nullptr;
+    p.ldc0 = ldc0;
+    p.bias = direct ? bias : nullptr;
+    p.ld_bias = ld_bias;
+    p.bias_cols = bias_cols > 0 ? bias_cols : 1;
+    dim3 grid((unsigned)m_tiles, (unsigned)n_tiles, (unsigned)split);
+    int rc = bmn ? dispatch_bn<true>(BN, ma, mh, ml, p, grid, st)
+                 : dispatch_bn<false>(BN, ma, mh, ml, p, grid, st);
     if (rc || direct) return rc;
     const int64_t total = M * N;
-    sum_splits_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(ws, split, M, N, C, ldc, C0,
-                                                                      ldc0, beta);
+    sum_splits_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        ws, split, M, N, C, ldc, C0, ldc0, beta, bias, ld_bias, bias_cols > 0 ? bias_cols : 1);
     return check_launch("enks_gemm(tcgen05 split reduce)");
 }
 
+int gemm_tc_presplit(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
+                     const float* Bh, const float* Bl, int64_t ldb, float beta, const float* C0,
+                     int64_t ldc0, float* C, int64_t ldc, int split, float* ws, cudaStream_t st) {
+    return gemm_tc_general(false, M, N, K, alpha, A, lda, Bh, Bl, ldb, beta, C0, ldc0, nullptr, 0,
+                           1, C, ldc, 0, 0, split, ws, st);
+}
+
 int tf32_split(const float* src, int64_t ld, int64_t rows, int64_t cols, float* hi, float* lo,
-               cudaStream_t st) {
+               int64_t ldo, cudaStream_t st) {
     const int64_t total = rows * cols;
     if (total == 0) return ENKS_OK;
-    tf32_split_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(src, ld, rows, cols, hi, lo);
+    tf32_split_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(src, ld, rows, cols, hi, lo,
+                                                                      ldo);
     return check_launch("enks_tf32_split");
 }
 
+int tf32_split_t(const float* src, int64_t ld, int64_t rows, int64_t cols, float* hi, float* lo,
+                 int64_t ldo, cudaStream_t st) {
+    if (rows == 0 || cols == 0) return ENKS_OK;
+    dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    tf32_split_t_kernel<<<grid, 256, 0, st>>>(src, ld, rows, cols, hi, lo, ldo);
+    return check_launch("enks_tf32_split(transpose)");
+}
+
 int64_t tc_ws_bytes(int64_t M, int64_t N, int64_t K, int split) {
-    if (split < 1) split = tc_choose_split(M, K);
+    if (split < 1) split = choose_split((int)((M + BM - 1) / BM) * (int)((N + 255) / 256),
+                                       (K + BK - 1) / BK);
     return ((int64_t)split * M * N + 2 * N * K) * (int64_t)sizeof(float) + 64;
 }
 
@@ -413,14 +550,8 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_
             const float* B, int64_t ldb, float beta, const float* C0, int64_t ldc0,
             const float* bias, int64_t ld_bias, int bias_cols, float* C, int64_t ldc, int split_k,
             void* ws, cudaStream_t st) {
-    (void)ld_bias;
-    (void)bias_cols;
-    if (bias) {
-        set_error("tc gemm: bias epilogue not supported");
-        return ENKS_E_UNSUPPORTED;
-    }
     if (!ws) {
-        set_error("tc gemm: needs workspace (enks_gemm_ws_bytes with engine 2)");
+        set_error("tc gemm: needs workspace (enks_tc_gemm_ws_bytes with engine 2)");
         return ENKS_E_ARG;
     }
     // workspace: [B_hi | B_lo | split partials]
@@ -428,10 +559,10 @@ int gemm_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_
     float* bl = bh + N * K;
     float* part = bl + N * K;
     part = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(part) + 15) & ~uintptr_t(15));
-    int rc = tf32_split(B, ldb, N, K, bh, bl, st);
+    int rc = tf32_split(B, ldb, N, K, bh, bl, K, st);
     if (rc) return rc;
-    return gemm_tc_presplit(M, N, K, alpha, A, lda, bh, bl, K, beta, C0, ldc0, C, ldc,
-                            split_k > 0 ? split_k : 0, part, st);
+    return gemm_tc_general(false, M, N, K, alpha, A, lda, bh, bl, K, beta, C0, ldc0, bias,
+                           ld_bias, bias_cols, C, ldc, 0, 0, split_k > 0 ? split_k : 0, part, st);
 }
 
 }  // namespace enks
@@ -443,9 +574,10 @@ int64_t enks_tc_gemm_ws_bytes(int64_t M, int64_t N, int64_t K, int split_k) {
 }
 
 int enks_tf32_split(const float* src, int64_t ld, int64_t rows, int64_t cols, float* hi, float* lo,
-                    void* stream) {
+                    int transpose, void* stream) {
     ENKS_REQUIRE(src && hi && lo, "enks_tf32_split: null pointer");
-    return enks::tf32_split(src, ld, rows, cols, hi, lo, enks::as_stream(stream));
+    return transpose ? enks::tf32_split_t(src, ld, rows, cols, hi, lo, rows, enks::as_stream(stream))
+                     : enks::tf32_split(src, ld, rows, cols, hi, lo, cols, enks::as_stream(stream));
 }
 
 int enks_gemm_nt_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
@@ -458,6 +590,24 @@ int enks_gemm_nt_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A
     if (M == 0 || N == 0) return ENKS_OK;
     return enks::gemm_tc_presplit(M, N, K, alpha, A, lda, Bh, Bl, ldb, 0.f, nullptr, 0, C, ldc,
                                   split_k, static_cast<float*>(ws), enks::as_stream(stream));
+}
+
+int enks_gemm_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A, int64_t lda,
+                 const float* Bh, const float* Bl, int64_t ldb, int b_mn_major, float beta,
+                 const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias, int bias_cols,
+                 float* C, int64_t ldc, int64_t tri_rows, int64_t tri_k, int split_k, void* ws,
+                 void* stream) {
+    ENKS_REQUIRE(A && Bh && Bl && C, "enks_gemm_tc: null pointer");
+    ENKS_REQUIRE(K >= 1 && (lda & 3) == 0 && (ldb & 3) == 0 &&
+                     !(reinterpret_cast<uintptr_t>(A) & 15) &&
+                     !(reinterpret_cast<uintptr_t>(Bh) & 15) &&
+                     !(reinterpret_cast<uintptr_t>(Bl) & 15),
+                 "enks_gemm_tc: operands need 16-B aligned rows (ld %% 4 == 0)");
+    ENKS_REQUIRE(b_mn_major || N <= 1 << 30, "enks_gemm_tc: bad N");
+    if (M == 0 || N == 0) return ENKS_OK;
+    return enks::gemm_tc_general(b_mn_major != 0, M, N, K, alpha, A, lda, Bh, Bl, ldb, beta, C0, ldc0, bias,
+                                 ld_bias, bias_cols, C, ldc, tri_rows, tri_k, split_k,
+                                 static_cast<float*>(ws), enks::as_stream(stream));
 }
 
 }  // extern "C"

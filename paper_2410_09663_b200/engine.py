@@ -178,6 +178,14 @@ class DeviceSmoother:
         if self.use_tc:
             self.yc_hi = ops.empty(p, K)
             self.yc_lo = ops.empty(p, K)
+        # the gain-side products (correction, gain, newest-slice shift) on tcgen05 as well
+        self.use_tc2 = self.use_tc and p % 4 == 0 and m % 4 == 0 and hasattr(ops, "gemm_tc")
+        if self.use_tc2:
+            self.ycT_hi = ops.empty(K, p)
+            self.ycT_lo = ops.empty(K, p)
+            self.sinvT_hi = ops.empty(p, p)
+            self.sinvT_lo = ops.empty(p, p)
+            self.pyT_hi = self.pyT_lo = None
         self.slice_raw = ops.empty(d, K)      # [X; U; W] of the newest predicted slice
         self.obs_raw = ops.empty(p, K)        # perturbed observations of the newest slice
         self.last = ops.empty(p, K)           # materialised [x; u] of the newest updated slice
@@ -213,6 +221,9 @@ class DeviceSmoother:
             G[:rows_a, :rows_y] = self.G[:rows_a, :rows_y]
             mean[:rows_a] = self.mean[:rows_a]
         self.Abuf, self.Ybuf, self.G, self.mean, self.PA, self.PY = Abuf, Ybuf, G, mean, PA, PY
+        if getattr(self, "use_tc2", False):
+            self.pyT_hi = ops.empty(p * cap * p)
+            self.pyT_lo = ops.empty(p * cap * p)
         self.cap = cap
 
     def memory_bytes(self) -> int:
@@ -344,20 +355,39 @@ class DeviceSmoother:
         scale = self.lam / self.N
         ops.spd_inverse(PY[(tau - 1) * p:], scale, self.sinv, self.status, self.jitter)
         # S_s = P_{A_s} - sum_{tau' < tau} G_{tau',s} P_{Yc_tau'}  (block upper-triangular G)
-        if tau > 1:
-            ops.gemm(self.G[a0:rows_a, :(tau - 1) * p], self.PY[:(tau - 1) * p], PA,
-                     alpha=-1.0, beta=1.0, C0=PA, tri=(d, p) if a0 == 0 else (0, 0))
-        # G_{tau,s} = (lam/N) S_s Sigma_y^{-1}
+        tri = (d, p) if a0 == d else (0, 0)
         gcol = self.G[a0:rows_a, (tau - 1) * p:tau * p]
-        ops.gemm(PA, self.sinv, gcol, alpha=scale)
+        r0 = tau * d
+        if self.use_tc2:
+            if tau > 1:
+                kk = (tau - 1) * p
+                pth = self.pyT_hi[:p * kk].view(p, kk)
+                ptl = self.pyT_lo[:p * kk].view(p, kk)
+                ops.tf32_split(self.PY[:kk], pth, ptl, transpose=True)
+                ops.gemm_tc(self.G[a0:rows_a, :kk], pth, ptl, PA, alpha=-1.0, beta=1.0, C0=PA,
+                            tri=tri, tag="correction")
+            # G_{tau,s} = (lam/N) S_s Sigma_y^{-1}
+            ops.tf32_split(self.sinv, self.sinvT_hi, self.sinvT_lo, transpose=True)
+            ops.gemm_tc(PA, self.sinvT_hi, self.sinvT_lo, gcol, alpha=scale, tag="gain")
+        else:
+            if tau > 1:
+                ops.gemm(self.G[a0:rows_a, :(tau - 1) * p], self.PY[:(tau - 1) * p], PA,
+                         alpha=-1.0, beta=1.0, C0=PA, tri=tri)
+            ops.gemm(PA, self.sinv, gcol, alpha=scale)
         # mean_s += G_{tau,s} (y_ref - y_bar)   (enks.py:247-248 on the mean)
         ops.sub(y_ref_dev, self.ybar, self.innov)
         mv = self.mean[a0:rows_a]
         ops.gemm(gcol, self.innov, mv, beta=1.0, C0=mv)
         # newest slice [x; u] for the next forecast: mean + A_tau - G_{tau,tau} Yc_tau
-        r0 = tau * d
-        ops.gemm(self.G[r0:r0 + p, (tau - 1) * p:tau * p], yc, self.last, alpha=-1.0, beta=1.0,
-                 C0=self.Abuf[r0:r0 + p], bias=self.mean[r0:r0 + p], bias_cols=self.m)
+        g_tt = self.G[r0:r0 + p, (tau - 1) * p:tau * p]
+        if self.use_tc2:
+            ops.tf32_split(yc, self.ycT_hi, self.ycT_lo, transpose=True)
+            ops.gemm_tc(g_tt, self.ycT_hi, self.ycT_lo, self.last, alpha=-1.0, beta=1.0,
+                        C0=self.Abuf[r0:r0 + p], bias=self.mean[r0:r0 + p], bias_cols=self.m,
+                        tag="shift")
+        else:
+            ops.gemm(g_tt, yc, self.last, alpha=-1.0, beta=1.0, C0=self.Abuf[r0:r0 + p],
+                     bias=self.mean[r0:r0 + p], bias_cols=self.m)
 
     # ------------------------------------------------------------ readback
     def deviations(self, rows: int | None = None):

@@ -160,11 +160,12 @@ class DeviceOps:
         return (Bh.shape[0] <= 256 and K >= 128 and _ld(A) % 4 == 0 and _ld(Bh) % 4 == 0
                 and A.data_ptr() % 16 == 0 and Bh.data_ptr() % 16 == 0)
 
-    def tf32_split(self, src, hi, lo):
-        """hi = rna_tf32(src), lo = src - hi (the B operand of the 3xTF32 contraction)."""
+    def tf32_split(self, src, hi, lo, transpose=False):
+        """hi = rna_tf32(src), lo = src - hi (B operand of the 3xTF32 GEMMs); transpose=True
+        writes the (cols x rows) planes, i.e. the K-major form of a K x N operand."""
         self.launches += 1
         _lib.call("enks_tf32_split", _p(src), _ld(src), src.shape[0], src.shape[1], _p(hi), _p(lo),
-                  self._stream())
+                  int(transpose), self._stream())
 
     def gemm_nt_tc(self, A, Bh, Bl, C, *, alpha=1.0, split=0, tag=None):
         """C = alpha * A (Bh + Bl)^T on tcgen05 (3xTF32), deterministic split-K."""
@@ -180,6 +181,33 @@ class DeviceOps:
             ev0.record()
         _lib.call("enks_gemm_nt_tc", M, N, K, float(alpha), _p(A), _ld(A), _p(Bh), _p(Bl), _ld(Bh),
                   _p(C), _ld(C), int(split), ws, self._stream())
+        if prof:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record()
+            self.profile.append((tag, ev0, ev1, 2.0 * M * N * K))
+
+    def gemm_tc(self, A, Bh, Bl, C, *, alpha=1.0, beta=0.0, C0=None, bias=None, bias_cols=1,
+                tri=(0, 0), split=0, tag=None):
+        """C = alpha * A (Bh + Bl)^T + beta * C0 + bias on tcgen05 (3xTF32).
+
+        Bh/Bl are the K-major (N x K) planes of B (see tf32_split(transpose=True))."""
+        M, K = A.shape
+        N = Bh.shape[0]
+        if M == 0 or N == 0:
+            return
+        if split == 0:
+            tiles = -(-M // 128) * -(-N // 256)
+            split = 1 if tiles >= NUM_SMS or K < 1024 else int(min(-(-NUM_SMS // tiles), K // 512))
+        ws = self._workspace(int(split) * M * N * 4) if split > 1 else None
+        self.launches += 2 if split > 1 else 1
+        prof = self.profile is not None and tag is not None
+        if prof:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+        _lib.call("enks_gemm_tc", M, N, K, float(alpha), _p(A), _ld(A), _p(Bh), _p(Bl), _ld(Bh), 0,
+                  float(beta), _p(C0), _ld(C0) if C0 is not None else 0, _p(bias),
+                  _ld(bias) if bias is not None else 0, int(bias_cols), _p(C), _ld(C),
+                  int(tri[0]), int(tri[1]), int(split), ws, self._stream())
         if prof:
             ev1 = torch.cuda.Event(enable_timing=True)
             ev1.record()

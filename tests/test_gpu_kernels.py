@@ -278,3 +278,30 @@ def test_fused_noise_multi_matches_single(dev_ops):
                                                 for k, r in enumerate(rows)])
     for k in range(3):
         assert torch.equal(single[k], multi[k]) and torch.equal(plus1[k], plus2[k])
+
+
+@pytest.mark.parametrize("M,N,K,tri,split", [(256, 4096, 256, None, 1), (300, 256, 2000, None, 0),
+                                             (77, 6, 40, None, 1), (1000, 100, 700, (200, 100), 1),
+                                             (130, 130, 3000, None, 4), (256, 131072, 256, None, 1)])
+def test_gemm_tc_general(dev_ops, M, N, K, tri, split):
+    """C = alpha A B + beta C0 + bias via transposed split planes; triangular skip; N tiling."""
+    g = torch.Generator().manual_seed(M + 3 * N + K)
+    A = torch.randn(M, K, generator=g)
+    if tri:
+        d, p = tri
+        for s in range(M // d + 1):
+            A[s * d:(s + 1) * d, :min(K, s * p)] = 0.0
+    B = torch.randn(K, N, generator=g)
+    C0 = torch.randn(M, N, generator=g)
+    bias = torch.randn(M, 4, generator=g)
+    dA, dB = A.to(dev_ops.device), B.to(dev_ops.device)
+    bh, bl = dev_ops.empty(N, K), dev_ops.empty(N, K)
+    dev_ops.tf32_split(dB, bh, bl, transpose=True)
+    assert torch.equal((bh + bl).cpu(), B.t())
+    C = dev_ops.zeros(M, N)
+    dev_ops.gemm_tc(dA, bh, bl, C, alpha=-0.5, beta=1.0, C0=C0.to(dev_ops.device),
+                    bias=bias.to(dev_ops.device), bias_cols=4, tri=tri or (0, 0), split=split)
+    ref = -0.5 * (A.double() @ B.double()) + C0.double() + bias.double()[:, [c % 4 for c in range(N)]]
+    scale = 0.5 * (A.double().abs() @ B.double().abs()) + C0.double().abs() + 1.0
+    err = ((C.double().cpu() - ref).abs() / scale).max().item()
+    assert err < 1e-6, err
