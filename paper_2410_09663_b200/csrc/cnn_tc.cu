@@ -84,8 +84,9 @@ struct Cnn3Args {
 
 __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+    // align to 1024 B by offsetting the shared pointer itself, so the compiler keeps the
+    // shared address space (LDS/STS rather than generic LD/ST)
+    uint8_t* sm = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     float* in_ring = reinterpret_cast<float*>(sm + kOffIn);
     float* w1s = reinterpret_cast<float*>(sm + kOffW1);
     float* b1s = reinterpret_cast<float*>(sm + kOffB1);

@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmBl, const TcParams p) {
     using L = Layout<BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align to 1024 B by offsetting the shared pointer itself (keeps LDS/STS addressing)
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int S = p.stages;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * L::kStage);
     uint64_t* full = bars;
