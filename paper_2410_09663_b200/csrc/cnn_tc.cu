@@ -43,12 +43,13 @@ constexpr int kOffB = 0;                            // [dy][hi/lo] B tiles
 constexpr int kOffA = kOffB + 3 * 2 * kBTile;       // [slot][hi/lo] A tiles
 constexpr int kOffIn = kOffA + NA * 2 * kATile;     // input ring [4][2][W + 2] floats
 constexpr int kInRow = W + 2;
-constexpr int kOffW1 = kOffIn + 4 * 2 * kInRow * 4; // w1 [C1][20], b1[C1], b2[C2], w3[9][C2], b3
-constexpr int kW1Stride = 20;
-constexpr int kOffB1 = kOffW1 + C1 * kW1Stride * 4;
+constexpr int kOffW1 = kOffIn + 4 * 2 * kInRow * 4; // w1 pairs [C1/2][20] float2, b1, b2, w3, b3
+constexpr int kW1Stride = 20;                        // float2 per channel pair (18 used)
+constexpr int kOffB1 = kOffW1 + (C1 / 2) * kW1Stride * 8;
 constexpr int kOffB2 = kOffB1 + C1 * 4;
-constexpr int kOffW3 = kOffB2 + C2 * 4;
-constexpr int kOffB3 = kOffW3 + 9 * C2 * 4;
+constexpr int kOffW3 = kOffB2 + C2 * 4;              // w3 [C2][12]: taps 0..8 (+pad), per channel
+constexpr int kW3Stride = 12;
+constexpr int kOffB3 = kOffW3 + C2 * kW3Stride * 4;
 constexpr int kOffX = kOffB3 + 16;                  // exchange buffers
 constexpr int kXD = 2 * 4 * 32;                     // [parity][warp][32]
 constexpr int kXV = 2 * 4 * 4;                      // [parity][warp][3 (+pad)]
@@ -120,14 +121,14 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         *reinterpret_cast<float*>(sm + kOffB + (dy * 2 + 1) * kBTile + off) = v - h;
     }
     for (int e = threadIdx.x; e < C1 * 18; e += kThreads) {
-        const int c = e / 18, k = e - c * 18;
-        w1s[c * kW1Stride + k] = a.w1[c * 18 + k];  // k = ci*9 + ky*3 + kx
+        const int c = e / 18, k = e - c * 18;  // k = ci*9 + ky*3 + kx
+        w1s[((c >> 1) * kW1Stride + k) * 2 + (c & 1)] = a.w1[c * 18 + k];
     }
     for (int e = threadIdx.x; e < C1; e += kThreads) b1s[e] = a.b1[e];
     for (int e = threadIdx.x; e < C2; e += kThreads) b2s[e] = a.b2[e];
-    for (int e = threadIdx.x; e < 9 * C2; e += kThreads) {
-        const int k = e / C2, c = e - k * C2;  // w3s[ky*3+kx][c]
-        w3s[e] = a.w3[c * 9 + k];
+    for (int e = threadIdx.x; e < C2 * kW3Stride; e += kThreads) {
+        const int c = e / kW3Stride, k = e - c * kW3Stride;  // w3s[c][ky*3+kx]
+        w3s[e] = k < 9 ? a.w3[c * 9 + k] : 0.f;
     }
     if (threadIdx.x == 0) {
         b3s[0] = a.b3[0];
@@ -152,11 +153,11 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         // ================= MMA issuer =================
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_tf32(W, NB);
-            int64_t it = 0;
+            int it = 0;
             for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
                 for (int r = 0; r < n; ++r) {
-                    const int64_t Rg = it * n + r;
-                    const int slot = (int)(Rg % NA);
+                    const int Rg = it * n + r;
+                    const int slot = Rg % NA;
                     ptx::mbar_wait(&a_full[slot], (uint32_t)((Rg / NA) & 1));
                     ptx::tc_fence_after();
                     const uint8_t* ah_t = sm + kOffA + (slot * 2 + 0) * kATile;
@@ -164,8 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     for (int dy = 0; dy < 3; ++dy) {
                         const int y = r - dy + 1;
                         if (y < 0 || y >= n) continue;
-                        const int64_t Yg = it * n + y;
-                        const int q = (int)(Yg % NACC);
+                        const int Yg = it * n + y;
+                        const int q = Yg % NACC;
                         const bool first = (dy == 0) || (r == 0 && dy == 1);
                         if (first) {
                             ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Yg / NACC) & 1) ^ 1));
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     } else if (warp >= 4 && warp < 8) {
         // ================= layer-1 producer: thread = pixel =================
         const int x = threadIdx.x - 128;
-        int64_t it = 0;
+        int it = 0;
         for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
             const float* xm = a.x + mem * W;
             const float* um = a.u + mem * W;
@@ -222,8 +223,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
 #pragma unroll
                         for (int kx = 0; kx < 3; ++kx) in[ci * 9 + ky * 3 + kx] = ok ? src[kx] : 0.f;
                     }
-                const int64_t Rg = it * n + r;
-                const int slot = (int)(Rg % NA);
+                const int Rg = it * n + r;
+                const int slot = Rg % NA;
                 ptx::mbar_wait(&a_empty[slot], (uint32_t)(((Rg / NA) & 1) ^ 1));
                 uint8_t* ah_t = sm + kOffA + (slot * 2 + 0) * kATile;
                 uint8_t* al_t = sm + kOffA + (slot * 2 + 1) * kATile;
@@ -231,22 +232,19 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 for (int c4 = 0; c4 < C1 / 4; ++c4) {
                     float hv[4];
 #pragma unroll
-                    for (int cc = 0; cc < 4; ++cc) {
-                        const int c = c4 * 4 + cc;
-                        const float4* wr = reinterpret_cast<const float4*>(w1s + c * kW1Stride);
-                        float acc = b1s[c];
+                    for (int pr = 0; pr < 2; ++pr) {  // channel pair (c, c+1), packed FFMA2
+                        const int cp = c4 * 2 + pr;
+                        const float4* wr = reinterpret_cast<const float4*>(w1s + cp * kW1Stride * 2);
+                        float2 acc = make_float2(b1s[2 * cp], b1s[2 * cp + 1]);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const float4 wv = wr[q];
-                            acc = fmaf(wv.x, in[4 * q + 0], acc);
-                            acc = fmaf(wv.y, in[4 * q + 1], acc);
-                            acc = fmaf(wv.z, in[4 * q + 2], acc);
-                            acc = fmaf(wv.w, in[4 * q + 3], acc);
+                        for (int q = 0; q < 9; ++q) {
+                            const float4 wv = wr[q];  // (k=2q: c, c+1), (k=2q+1: c, c+1)
+                            acc = __ffma2_rn(make_float2(wv.x, wv.y), make_float2(in[2 * q], in[2 * q]), acc);
+                            acc = __ffma2_rn(make_float2(wv.z, wv.w),
+                                             make_float2(in[2 * q + 1], in[2 * q + 1]), acc);
                         }
-                        const float2 wt = *reinterpret_cast<const float2*>(w1s + c * kW1Stride + 16);
-                        acc = fmaf(wt.x, in[16], acc);
-                        acc = fmaf(wt.y, in[17], acc);
-                        hv[cc] = tanh_fast(acc);
+                        hv[2 * pr] = tanh_fast(acc.x);
+                        hv[2 * pr + 1] = tanh_fast(acc.y);
                     }
                     float4 h4, l4;
                     h4.x = ptx::tf32_round(hv[0]); l4.x = hv[0] - h4.x;
@@ -268,15 +266,15 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         const int x = ew * 32 + lane;
         const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
         const float b3 = b3s[0];
-        int64_t it = 0;
+        int it = 0;
         for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
             float acc3[3] = {0.f, 0.f, 0.f};  // layer-3 partial sums, ring over output rows
             const float* xm = a.x + mem * W;
             float* om = a.out + mem * W;
             for (int y = 0; y < n; ++y) {
-                const int64_t Yg = it * n + y;
-                const int q = (int)(Yg % NACC);
-                const int par = (int)(Yg & 1);
+                const int Yg = it * n + y;
+                const int q = Yg % NACC;
+                const int par = Yg & 1;
                 ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / NACC) & 1));
                 ptx::tc_fence_after();
                 const uint32_t base = tmem + lane_base + (uint32_t)(q * NB);
@@ -322,15 +320,21 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     for (int c = 0; c < 32; ++c) s[c] += xd2[(par * 4 + ew + 1) * 32 + c];
                 }
                 // layer-2 activation and the layer-3 taps v[ky][kx] = sum_c w3 h
-                float vv[9];
-#pragma unroll
-                for (int k = 0; k < 9; ++k) vv[k] = 0.f;
+                float2 v01 = make_float2(0.f, 0.f), v23 = v01, v45 = v01, v67 = v01;
+                float v8 = 0.f;
 #pragma unroll
                 for (int c = 0; c < 32; ++c) {
                     const float h = tanh_fast(s[c] + b2s[c]);
-#pragma unroll
-                    for (int k = 0; k < 9; ++k) vv[k] = fmaf(w3s[k * C2 + c], h, vv[k]);
+                    const float2 hh = make_float2(h, h);
+                    const float4 w0 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride);
+                    const float4 w1 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride + 4);
+                    v01 = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01);
+                    v23 = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23);
+                    v45 = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45);
+                    v67 = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67);
+                    v8 = fmaf(w3s[c * kW3Stride + 8], h, v8);
                 }
+                const float vv[9] = {v01.x, v01.y, v23.x, v23.y, v45.x, v45.y, v67.x, v67.y, v8};
                 // fold horizontal taps: lane x3 takes v[ky][0] from x3-1, v[ky][2] from x3+1
                 float tk[3];
 #pragma unroll

@@ -30,7 +30,7 @@
 namespace enks {
 namespace {
 
-constexpr int BM = 128, BK = 32;
+constexpr int BM = 128, BK = 32;  // BK: widest K chunk (128 B rows, SWIZZLE_128B)
 constexpr int kThreads = 384;        // 4 control warps + 8 converter/epilogue warps
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kChainChunks = 4;      // TMEM accumulation chain = 4 x 32 = 128 K-elements
@@ -53,10 +53,11 @@ struct TcParams {
     uint32_t mn_lbo, mn_sbo;  // MN-major B descriptor strides (debug knob ENKS_TC_MN)
 };
 
-template <int BN>
+template <int BN, int KB = BK>
 struct Layout {
-    static constexpr int kA = BM * BK * 4;     // 16 KB (hi in place)
-    static constexpr int kB = BN * BK * 4;     // BN x 32 fp32
+    static constexpr int kRowB = KB * 4;       // bytes per operand row in a stage
+    static constexpr int kA = BM * KB * 4;     // A tile (hi in place)
+    static constexpr int kB = BN * KB * 4;     // B tile
     static constexpr int kStage = 2 * kA + 2 * kB;
     static constexpr int kSlotCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
     static constexpr int kEpiWG = BN > 128 ? 2 : 1;         // warpgroups holding the fp32 sums
@@ -77,11 +78,29 @@ __device__ __forceinline__ uint64_t desc_mnmajor_sw128(const void* smem, uint32_
     return d;
 }
 
-template <int BN, bool BMN>
+// UMMA descriptor, K-major SWIZZLE_64B (8-row x 64 B atoms, SBO = 512 B)
+__device__ __forceinline__ uint64_t desc_kmajor_sw64(const void* smem) {
+    const uint64_t addr = ptx::smem_u32(smem);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+    return d;
+}
+
+template <int KB>
+__device__ __forceinline__ uint64_t desc_k(const void* smem) {
+    if constexpr (KB == 32) return ptx::desc_kmajor_sw128(smem);
+    else return desc_kmajor_sw64(smem);
+}
+
+template <int BN, bool BMN, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
                    const __grid_constant__ CUtensorMap tmBl, const TcParams p) {
-    using L = Layout<BN>;
+    using L = Layout<BN, KB>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // align to 1024 B by offsetting the shared pointer itself (keeps LDS/STS addressing)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -101,9 +120,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // K range of this CTA: [kbeg, K) split evenly (in BK chunks) over the splits
     int64_t kbeg = 0;
     if (p.tri_rows > 0) kbeg = (row0 / p.tri_rows) * p.tri_k;
-    kbeg = (kbeg / BK) * BK;
+    kbeg = (kbeg / KB) * KB;
     if (kbeg > p.K) kbeg = p.K;
-    const int total_chunks = (int)((p.K - kbeg + BK - 1) / BK);
+    const int total_chunks = (int)((p.K - kbeg + KB - 1) / KB);
     const int cps = (total_chunks + p.splits - 1) / p.splits;
     const int c_lo = min(total_chunks, split * cps);
     const int c_hi = min(total_chunks, c_lo + cps);
@@ -144,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t ph = (uint32_t)((i / S) & 1);
                 ptx::mbar_wait(&empty[s], ph ^ 1);
                 ptx::mbar_arrive_expect_tx(&full[s], L::kA + 2 * L::kB);
-                const int kc = (int)(kbeg + (int64_t)(c_lo + i) * BK);
+                const int kc = (int)(kbeg + (int64_t)(c_lo + i) * KB);
                 ptx::tma_load_2d(&tmA, &full[s], stage_a(s), kc, (int32_t)row0);
                 if (!BMN) {
                     ptx::tma_load_2d(&tmBh, &full[s], stage_bh(s), kc, (int32_t)col0);
@@ -178,13 +197,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(slot * L::kSlotCols);
 #pragma unroll
-                for (int k = 0; k < BK / 8; ++k) {
-                    const uint64_t ah = ptx::desc_kmajor_sw128(stage_a(s) + 32 * k);
-                    const uint64_t al = ptx::desc_kmajor_sw128(stage_alo(s) + 32 * k);
+                for (int k = 0; k < KB / 8; ++k) {
+                    const uint64_t ah = desc_k<KB>(stage_a(s) + 32 * k);
+                    const uint64_t al = desc_k<KB>(stage_alo(s) + 32 * k);
                     uint64_t bh, bl;
                     if (!BMN) {
-                        bh = ptx::desc_kmajor_sw128(stage_bh(s) + 32 * k);
-                        bl = ptx::desc_kmajor_sw128(stage_bl(s) + 32 * k);
+                        bh = desc_k<KB>(stage_bh(s) + 32 * k);
+                        bl = desc_k<KB>(stage_bl(s) + 32 * k);
                     } else {
                         bh = desc_mnmajor_sw128(stage_bh(s) + 1024 * k, p.mn_lbo, p.mn_sbo);
                         bl = desc_mnmajor_sw128(stage_bl(s) + 1024 * k, p.mn_lbo, p.mn_sbo);
@@ -233,12 +252,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ph = (uint32_t)((i / S) & 1);
             ptx::mbar_wait(&full[s], ph);
             // elementwise split: any chunk order works; XOR with the row's swizzle phase
-            // spreads the 8 threads of each shared-memory phase over all 32 banks.
-            float4* a = reinterpret_cast<float4*>(stage_a(s) + crow * 128);
-            float4* alo = reinterpret_cast<float4*>(stage_alo(s) + crow * 128);
+            // spreads the threads of each shared-memory phase over all 32 banks.
+            constexpr int kChunks = L::kRowB / 16;       // 16-B chunks per row (8 or 4)
+            constexpr int kPer = kChunks / 2;            // per converter thread (half a row)
+            float4* a = reinterpret_cast<float4*>(stage_a(s) + crow * L::kRowB);
+            float4* alo = reinterpret_cast<float4*>(stage_alo(s) + crow * L::kRowB);
+            const int phase = KB == 32 ? (crow & 7) : ((crow >> 1) & 3);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int qq = (chalf * 4 + q) ^ (crow & 7);
+            for (int q = 0; q < kPer; ++q) {
+                const int qq = (chalf * kPer + q) ^ phase;
                 const float4 v = a[qq];
                 float4 h, l;
                 h.x = ptx::tf32_round(v.x); l.x = v.x - h.x;
@@ -376,7 +398,7 @@ EncodeTiledFn encode_fn() {
 
 // 2-D fp32 tensor map over a row-major (rows x cols, ld) matrix; box = box_cols x box_rows
 bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld,
-              int box_cols, int box_rows) {
+              int box_cols, int box_rows, bool sw64 = false) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -384,17 +406,20 @@ bool make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, i
     cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
+constexpr int kBK256 = 16;  // BN = 256: 16-wide K chunks (SWIZZLE_64B) -> 4 pipeline stages
+
 int bn_for(int64_t N) { return N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256)); }
 
-template <int BN, bool BMN>
+template <int BN, bool BMN, int KB>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& ml, TcParams p,
               dim3 grid, cudaStream_t st) {
-    using L = Layout<BN>;
+    using L = Layout<BN, KB>;
     int stages = kSmemBudget / L::kStage;
     if (stages > 4) stages = 4;
     if (stages < 2) {
@@ -405,7 +430,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& m
     const size_t smem = (size_t)stages * L::kStage + 1024 + 512;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, BMN>,
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, BMN, KB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) {
             set_error("tc gemm: smem attribute: %s", cudaGetErrorString(e));
@@ -413,7 +438,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& m
         }
         configured = true;
     }
-    tc_gemm_kernel<BN, BMN><<<grid, kThreads, smem, st>>>(ma, mh, ml, p);
+    tc_gemm_kernel<BN, BMN, KB><<<grid, kThreads, smem, st>>>(ma, mh, ml, p);
     return check_launch("enks_gemm(tcgen05)");
 }
 
@@ -421,10 +446,10 @@ template <bool BMN>
 int dispatch_bn(int BN, const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& ml,
                 const TcParams& p, dim3 grid, cudaStream_t st) {
     switch (BN) {
-        case 32: return launch_tc<32, BMN>(ma, mh, ml, p, grid, st);
-        case 64: return launch_tc<64, BMN>(ma, mh, ml, p, grid, st);
-        case 128: return launch_tc<128, BMN>(ma, mh, ml, p, grid, st);
-        default: return launch_tc<256, BMN>(ma, mh, ml, p, grid, st);
+        case 32: return launch_tc<32, BMN, 32>(ma, mh, ml, p, grid, st);
+        case 64: return launch_tc<64, BMN, 32>(ma, mh, ml, p, grid, st);
+        case 128: return launch_tc<128, BMN, 32>(ma, mh, ml, p, grid, st);
+        default: return launch_tc<256, BMN, BMN ? BK : kBK256>(ma, mh, ml, p, grid, st);
     }
 }
 
@@ -468,9 +493,12 @@ int gemm_tc_general(bool bmn, int64_t M, int64_t N, int64_t K, float alpha, cons
     if (M == 0 || N == 0) return ENKS_OK;
     const int BN = N >= 256 ? 256 : bn_for(N);
     CUtensorMap ma, mh, ml;
-    bool ok = make_map(&ma, A, M, K, lda, BK, BM);
+    const int kb = (BN == 256 && !bmn) ? kBK256 : BK;
+    const bool sw64 = kb == 16;
+    bool ok = make_map(&ma, A, M, K, lda, kb, BM, sw64);
     if (!bmn) {
-        ok = ok && make_map(&mh, Bh, N, K, ldb, BK, BN) && make_map(&ml, Bl, N, K, ldb, BK, BN);
+        ok = ok && make_map(&mh, Bh, N, K, ldb, kb, BN, sw64) &&
+             make_map(&ml, Bl, N, K, ldb, kb, BN, sw64);
     } else {
         ok = ok && make_map(&mh, Bh, K, N, ldb, 32, BK) && make_map(&ml, Bl, K, N, ldb, 32, BK);
     }
@@ -480,7 +508,7 @@ int gemm_tc_general(bool bmn, int64_t M, int64_t N, int64_t K, float alpha, cons
     }
     const int m_tiles = (int)((M + BM - 1) / BM);
     const int n_tiles = (int)((N + BN - 1) / BN);
-    if (split < 1) split = choose_split(m_tiles * n_tiles, (K + BK - 1) / BK);
+    if (split < 1) split = choose_split(m_tiles * n_tiles, (K + kb - 1) / kb);
     TcParams p;
     p.M = M; p.N = N; p.K = K;
     p.alpha = alpha; p.beta = beta;
