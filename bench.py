@@ -309,10 +309,18 @@ def run_ours(args):
     alg = _algorithmic(pr)
     achieved = (kern_flops / max(kern_s, 1e-12)) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    traffic, traffic_note = None, None
+    tpath = os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes")
+        traffic_note = {"launch": tj.get("launch"), "algorithmic_bytes": tj.get("algorithmic_bytes"),
+                        "source": tj.get("source")}
     roofline = {
-        "kernel": "cross-moment contraction P=[A;Yc]Yc^T (enks_gemm NT, split-K + fixed-order reduce)",
+        "kernel": "cross-moment contraction P=[A;Yc]Yc^T (tcgen05 3xTF32, tc_gemm_kernel)",
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved / peak, "traffic": None,
+        "frac": achieved / peak, "traffic": traffic, "traffic_capture": traffic_note,
         "peak_source": f"{peak_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)",
         "launches_timed": n_kern, "kernel_share_of_step": kern_s / elapsed,
         "algorithmic_tflop_per_horizon": alg["cross_tflop"],

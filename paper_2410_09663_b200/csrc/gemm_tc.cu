@@ -10,7 +10,7 @@
 // Precision: x = hi + lo with hi = rna_tf32(x); the MMAs accumulate lo*hi + hi*lo + hi*hi,
 // matching fp32 FFMA accuracy (the dropped lo*lo term is ~2^-22 relative).  The tensor core
 // accumulates into TMEM with truncation; over long K chains that bias reaches ~1e-6 relative
-// (tools/tc_acc_probe.py), so the MMA warp restarts a fresh TMEM slot every kChainChunks
+// (tools/tc_acc_probe.py), so the MMA warp restarts a fresh TMEM slot every p.chain
 // chunks (two slots, ping-pong) and the epilogue warps fold each finished chain into fp32
 // registers with round-to-nearest adds while the other slot fills.
 //
@@ -32,8 +32,8 @@ namespace {
 
 constexpr int BM = 128, BK = 32;  // BK: widest K chunk (128 B rows, SWIZZLE_128B)
 constexpr int kThreads = 384;        // 4 control warps + 8 converter/epilogue warps
-constexpr int kSmemBudget = 200 * 1024;
-constexpr int kChainChunks = 4;      // TMEM accumulation chain = 4 x 32 = 128 K-elements
+constexpr int kSmemBudget = 210 * 1024;
+constexpr int kChainChunksDefault = 8;  // TMEM accumulation chain (chunks)
 
 struct TcParams {
     int64_t M, N, K;
@@ -51,6 +51,8 @@ struct TcParams {
     int stages;
     int products;  // bitmask: 1 = lo*hi, 2 = hi*lo, 4 = hi*hi (debug knob ENKS_TC_PRODUCTS)
     uint32_t mn_lbo, mn_sbo;  // MN-major B descriptor strides (debug knob ENKS_TC_MN)
+    int debug;                // ENKS_TC_DEBUG: 1 = skip A split math, 2 = skip B loads
+    int chain;                // TMEM accumulation chain length in chunks (ENKS_TC_CHAIN)
 };
 
 template <int BN, int KB = BK>
@@ -96,7 +98,7 @@ __device__ __forceinline__ uint64_t desc_k(const void* smem) {
     else return desc_kmajor_sw64(smem);
 }
 
-template <int BN, bool BMN, int KB>
+template <int BN, bool BMN, int KB, int CL>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
                    const __grid_constant__ CUtensorMap tmBl, const TcParams p) {
@@ -116,6 +118,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * BM;
     const int64_t col0 = (int64_t)blockIdx.y * BN;
+    // CL > 1: the CTAs of a cluster (consecutive row tiles, same K range) share the B tile:
+    // each loads 1/CL of it and multicasts, and every CTA's MMA commit releases the stage in
+    // all of them, so B crosses L2 -> SM once per cluster instead of once per CTA.
+    const uint32_t cta_rank = CL > 1 ? ptx::cluster_ctarank() : 0u;
+    constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
     const int split = blockIdx.z;
     // K range of this CTA: [kbeg, K) split evenly (in BK chunks) over the splits
     int64_t kbeg = 0;
@@ -127,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int c_lo = min(total_chunks, split * cps);
     const int c_hi = min(total_chunks, c_lo + cps);
     const int n_chunks = c_hi - c_lo;
-    const int n_groups = (n_chunks + kChainChunks - 1) / kChainChunks;
+    const int n_groups = (n_chunks + p.chain - 1) / p.chain;
     constexpr uint32_t kTmemCols = 2 * L::kSlotCols;
 
     auto stage_a = [&](int s) { return smem + (size_t)s * L::kStage; };
@@ -139,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&conv[s], 256);
-            ptx::mbar_init(&empty[s], 1);
+            ptx::mbar_init(&empty[s], CL);
         }
         for (int q = 0; q < 2; ++q) {
             ptx::mbar_init(&tfull[q], 1);
@@ -153,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) ptx::tmem_alloc(tmem_slot, kTmemCols);
     ptx::tc_fence_before();
     __syncthreads();
+    if (CL > 1) ptx::cluster_sync();  // peers' barriers initialised before any multicast
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -162,12 +170,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = i % S;
                 const uint32_t ph = (uint32_t)((i / S) & 1);
                 ptx::mbar_wait(&empty[s], ph ^ 1);
-                ptx::mbar_arrive_expect_tx(&full[s], L::kA + 2 * L::kB);
+                ptx::mbar_arrive_expect_tx(&full[s], (p.debug & 2) ? L::kA : L::kA + 2 * L::kB);
                 const int kc = (int)(kbeg + (int64_t)(c_lo + i) * KB);
                 ptx::tma_load_2d(&tmA, &full[s], stage_a(s), kc, (int32_t)row0);
-                if (!BMN) {
+                if (p.debug & 2) {
+                } else if (!BMN && CL == 1) {
                     ptx::tma_load_2d(&tmBh, &full[s], stage_bh(s), kc, (int32_t)col0);
                     ptx::tma_load_2d(&tmBl, &full[s], stage_bl(s), kc, (int32_t)col0);
+                } else if (!BMN) {
+                    constexpr int kPiece = BN / CL;  // B rows loaded (and multicast) by this CTA
+                    const int off = (int)cta_rank * kPiece * L::kRowB;
+                    ptx::tma_load_2d_mc(&tmBh, &full[s], stage_bh(s) + off, kc,
+                                        (int32_t)(col0 + cta_rank * kPiece), kMask);
+                    ptx::tma_load_2d_mc(&tmBl, &full[s], stage_bl(s) + off, kc,
+                                        (int32_t)(col0 + cta_rank * kPiece), kMask);
                 } else {
 #pragma unroll
                     for (int j = 0; j < BN / 32; ++j) {
@@ -186,9 +202,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < n_chunks; ++i) {
                 const int s = i % S;
                 const uint32_t ph = (uint32_t)((i / S) & 1);
-                const int g = i / kChainChunks, slot = g & 1;
-                const bool first = (i % kChainChunks) == 0;
-                const bool last = (i % kChainChunks) == kChainChunks - 1 || i == n_chunks - 1;
+                const int g = i / p.chain, slot = g & 1;
+                const bool first = (i % p.chain) == 0;
+                const bool last = (i % p.chain) == p.chain - 1 || i == n_chunks - 1;
                 if (first) {
                     ptx::mbar_wait(&tempty[slot], (uint32_t)(((g >> 1) & 1) ^ 1));
                     ptx::tc_fence_after();
@@ -213,7 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (p.products & 2) { ptx::mma_tf32_ss(d, ah, bl, idesc, acc); acc = 1u; }
                     if (p.products & 4) { ptx::mma_tf32_ss(d, ah, bh, idesc, acc); }
                 }
-                ptx::mma_commit(&empty[s]);
+                if (CL > 1) ptx::mma_commit_mc(&empty[s], kMask);
+                else ptx::mma_commit(&empty[s]);
                 if (last) ptx::mma_commit(&tfull[slot]);
             }
         }
@@ -259,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float4* alo = reinterpret_cast<float4*>(stage_alo(s) + crow * L::kRowB);
             const int phase = KB == 32 ? (crow & 7) : ((crow >> 1) & 3);
 #pragma unroll
-            for (int q = 0; q < kPer; ++q) {
+            for (int q = 0; q < ((p.debug & 1) ? 0 : kPer); ++q) {
                 const int qq = (chalf * kPer + q) ^ phase;
                 const float4 v = a[qq];
                 float4 h, l;
@@ -273,8 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::fence_proxy_async_smem();
             ptx::mbar_arrive(&conv[s]);
             // fold chain g-1 once chain g has been fully converted (its slot is reused by g+1)
-            if (epi && (i % kChainChunks) == kChainChunks - 1) {
-                const int g = i / kChainChunks;
+            if (epi && (i % p.chain) == p.chain - 1) {
+                const int g = i / p.chain;
                 if (g >= 1) drain(g - 1), drained = g;
             }
         }
@@ -325,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if (CL > 1) ptx::cluster_sync();  // no CTA exits while peers may still signal it
     if (warp == 2) ptx::tmem_dealloc(tmem, kTmemCols);
 }
 
@@ -416,12 +434,12 @@ constexpr int kBK256 = 16;  // BN = 256: 16-wide K chunks (SWIZZLE_64B) -> 4 pip
 
 int bn_for(int64_t N) { return N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256)); }
 
-template <int BN, bool BMN, int KB>
+template <int BN, bool BMN, int KB, int CL>
 int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& ml, TcParams p,
               dim3 grid, cudaStream_t st) {
     using L = Layout<BN, KB>;
     int stages = kSmemBudget / L::kStage;
-    if (stages > 4) stages = 4;
+    if (stages > 8) stages = 8;
     if (stages < 2) {
         set_error("tc gemm: stage does not fit shared memory");
         return ENKS_E_UNSUPPORTED;
@@ -430,7 +448,7 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& m
     const size_t smem = (size_t)stages * L::kStage + 1024 + 512;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, BMN, KB>,
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, BMN, KB, CL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) {
             set_error("tc gemm: smem attribute: %s", cudaGetErrorString(e));
@@ -438,18 +456,38 @@ int launch_tc(const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& m
         }
         configured = true;
     }
-    tc_gemm_kernel<BN, BMN, KB><<<grid, kThreads, smem, st>>>(ma, mh, ml, p);
-    return check_launch("enks_gemm(tcgen05)");
+    if (CL == 1) {
+        tc_gemm_kernel<BN, BMN, KB, 1><<<grid, kThreads, smem, st>>>(ma, mh, ml, p);
+        return check_launch("enks_gemm(tcgen05)");
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, BMN, KB, CL>, ma, mh, ml, p);
+    if (e != cudaSuccess) {
+        set_error("tc gemm: cluster launch: %s", cudaGetErrorString(e));
+        return ENKS_E_CUDA;
+    }
+    return check_launch("enks_gemm(tcgen05 cluster)");
 }
 
-template <bool BMN>
+template <bool BMN, int CL>
 int dispatch_bn(int BN, const CUtensorMap& ma, const CUtensorMap& mh, const CUtensorMap& ml,
                 const TcParams& p, dim3 grid, cudaStream_t st) {
     switch (BN) {
-        case 32: return launch_tc<32, BMN, 32>(ma, mh, ml, p, grid, st);
-        case 64: return launch_tc<64, BMN, 32>(ma, mh, ml, p, grid, st);
-        case 128: return launch_tc<128, BMN, 32>(ma, mh, ml, p, grid, st);
-        default: return launch_tc<256, BMN, BMN ? BK : kBK256>(ma, mh, ml, p, grid, st);
+        case 32: return launch_tc<32, BMN, 32, CL>(ma, mh, ml, p, grid, st);
+        case 64: return launch_tc<64, BMN, 32, CL>(ma, mh, ml, p, grid, st);
+        case 128: return launch_tc<128, BMN, 32, CL>(ma, mh, ml, p, grid, st);
+        default: return launch_tc<256, BMN, BMN ? BK : kBK256, CL>(ma, mh, ml, p, grid, st);
     }
 }
 
@@ -491,14 +529,22 @@ int gemm_tc_general(bool bmn, int64_t M, int64_t N, int64_t K, float alpha, cons
                     int bias_cols, float* C, int64_t ldc, int64_t tri_rows, int64_t tri_k,
                     int split, float* ws, cudaStream_t st) {
     if (M == 0 || N == 0) return ENKS_OK;
-    const int BN = N >= 256 ? 256 : bn_for(N);
+    const char* bne = getenv("ENKS_TC_BN");
+    const int bn_cap = bne ? atoi(bne) : 256;
+    const int BN = bn_for(N < bn_cap ? N : bn_cap);
     CUtensorMap ma, mh, ml;
     const int kb = (BN == 256 && !bmn) ? kBK256 : BK;
     const bool sw64 = kb == 16;
+    const int m_tiles0 = (int)((M + BM - 1) / BM);
+    // cluster the row tiles sharing B (multicast) when there are several and no triangular skip
+    const char* ce = getenv("ENKS_TC_CLUSTER");
+    const int want_cl = ce ? atoi(ce) : 1;
+    const int cl = (!bmn && tri_rows == 0 && want_cl == 4 && m_tiles0 >= 4) ? 4
+                 : ((!bmn && tri_rows == 0 && want_cl >= 2 && m_tiles0 >= 2) ? 2 : 1);
     bool ok = make_map(&ma, A, M, K, lda, kb, BM, sw64);
     if (!bmn) {
-        ok = ok && make_map(&mh, Bh, N, K, ldb, kb, BN, sw64) &&
-             make_map(&ml, Bl, N, K, ldb, kb, BN, sw64);
+        ok = ok && make_map(&mh, Bh, N, K, ldb, kb, BN / cl, sw64) &&
+             make_map(&ml, Bl, N, K, ldb, kb, BN / cl, sw64);
     } else {
         ok = ok && make_map(&mh, Bh, K, N, ldb, 32, BK) && make_map(&ml, Bl, K, N, ldb, 32, BK);
     }
@@ -506,7 +552,7 @@ int gemm_tc_general(bool bmn, int64_t M, int64_t N, int64_t K, float alpha, cons
         set_error("tc gemm: cuTensorMapEncodeTiled failed (alignment / ld %% 4?)");
         return ENKS_E_UNSUPPORTED;
     }
-    const int m_tiles = (int)((M + BM - 1) / BM);
+    const int m_tiles = (m_tiles0 + cl - 1) / cl * cl;  // whole clusters (extra tiles idle)
     const int n_tiles = (int)((N + BN - 1) / BN);
     if (split < 1) split = choose_split(m_tiles * n_tiles, (K + kb - 1) / kb);
     TcParams p;
@@ -521,6 +567,11 @@ int gemm_tc_general(bool bmn, int64_t M, int64_t N, int64_t K, float alpha, cons
         const int mode = m ? atoi(m) : 0;
         p.mn_lbo = mode == 1 ? 1024 : (mode == 2 ? 4096 : (mode == 3 ? 1024 : 4096));
         p.mn_sbo = mode == 1 ? 4096 : (mode == 2 ? 4096 : (mode == 3 ? 1024 : 1024));
+        const char* dbg = getenv("ENKS_TC_DEBUG");
+        p.debug = dbg ? atoi(dbg) : 0;
+        const char* ch = getenv("ENKS_TC_CHAIN");
+        p.chain = ch ? atoi(ch) : kChainChunksDefault;
+        if (p.chain < 1) p.chain = 1;
     }
     const bool direct = (split == 1);
     if (!direct && !ws) {
@@ -536,8 +587,10 @@ int gemm_tc_general(bool bmn, int64_t M, int64_t N, int64_t K, float alpha, cons
     p.ld_bias = ld_bias;
     p.bias_cols = bias_cols > 0 ? bias_cols : 1;
     dim3 grid((unsigned)m_tiles, (unsigned)n_tiles, (unsigned)split);
-    int rc = bmn ? dispatch_bn<true>(BN, ma, mh, ml, p, grid, st)
-                 : dispatch_bn<false>(BN, ma, mh, ml, p, grid, st);
+    int rc = bmn ? dispatch_bn<true, 1>(BN, ma, mh, ml, p, grid, st)
+         : (cl == 4 ? dispatch_bn<false, 4>(BN, ma, mh, ml, p, grid, st)
+                    : (cl == 2 ? dispatch_bn<false, 2>(BN, ma, mh, ml, p, grid, st)
+                               : dispatch_bn<false, 1>(BN, ma, mh, ml, p, grid, st)));
     if (rc || direct) return rc;
     const int64_t total = M * N;
     sum_splits_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
