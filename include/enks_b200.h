@@ -147,6 +147,26 @@ int enks_gemm_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A, i
                  void* stream);
 
 /*
+ * fp16-pair storage and contraction of the append-only basis (the dominant
+ * cross moments P = [A; Yc] Yc^T, enks.py:148-153, 234-236):
+ *   enks_f16pair_split : per row r, s_r = 2^e with max|x_r| s_r in [2^13, 2^14);
+ *                        h = fp16(x s), l = fp16(x s - h) (fp16 planes, ld ldo),
+ *                        inv_scale[r] = 1 / s_r.  x = (h + l) / s to ~2^-22.
+ *   enks_f16pair_recon : fp32 reconstruction (members read-back).
+ *   enks_gemm_f16pair  : C[M x N] = alpha * diag(inv_sa) (Ah+Al)(Bh+Bl)^T diag(inv_sb)
+ *                        on tcgen05 kind::f16 (three MMAs per K=16 step, dropped l*l
+ *                        term ~2^-22), N <= 256; `ws` of enks_gemm_f16pair_ws_bytes bytes.
+ */
+int enks_f16pair_split(const float* src, int64_t ld, int64_t rows, int64_t K, void* h, void* l,
+                       int64_t ldo, float* inv_scale, void* stream);
+int enks_f16pair_recon(const void* h, const void* l, int64_t ldi, const float* inv_scale,
+                       int64_t rows, int64_t K, float* out, int64_t ldo, void* stream);
+int64_t enks_gemm_f16pair_ws_bytes(int64_t M, int64_t N, int64_t K);
+int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah, const void* Al,
+                      int64_t lda, const float* inv_sa, const void* Bh, const void* Bl, int64_t ldb,
+                      const float* inv_sb, float* C, int64_t ldc, void* ws, void* stream);
+
+/*
  * Gain solve (K8).  Replaces enks.py:234-235 (symmetrize) and 238-246
  * (cho_factor with the jitter fallback, cho_solve):
  *   Sy = scale * 0.5 * (S + S^T); try Cholesky; on failure (pivot <= 0 or NaN)

@@ -1,0 +1,426 @@
+// Cross moments (K6/K7) on tcgen05 kind::f16 with fp16-pair operands.
+//
+// Reference: enks.py:148-153 (_pair_covariance), 234-236 (Sigma_y, Sigma_xy), applied to
+// the append-only basis of engine.py: P = [A; Yc] Yc_tau^T over K = N*m.
+//
+// Storage: every basis row x (fp32, K long) is kept as two fp16 planes with a per-row
+// power-of-two scale s = 2^e chosen so max|x| s lies in [2^13, 2^14):
+//     h = fp16(x s),  l = fp16(x s - h)          (x s = h + l to ~2^-22 relative)
+// so a basis element costs 4 B (like fp32) and feeds the tensor core directly: no
+// in-kernel split.  The product uses three kind::f16 MMAs per K=16 step,
+//     (h_a + l_a)(h_b + l_b) ~ l_a h_b + h_a l_b + h_a h_b     (dropped l_a l_b ~ 2^-22),
+// products of 11-bit significands are exact in the fp32 accumulator; the result is
+// unscaled in the epilogue by 1/(s_a s_b) (exact, powers of two).  Accuracy therefore
+// matches 3xTF32 while moving half the bytes per K element and running at the f16 rate.
+// As in gemm_tc.cu, TMEM accumulation chains are restarted every `chain` chunks and
+// folded into fp32 registers with round-to-nearest adds (the tensor core truncates).
+//
+// Structure (one 128 x BN tile and one K range per CTA, 384 threads):
+//   warp 0: TMA producer (A_h, A_l, B_h, B_l tiles, SWIZZLE_64B, 32 fp16 = 64 B rows)
+//   warp 1: MMA issuer (2 K-steps x 3 MMAs per stage), warp 2: TMEM allocator,
+//   warps 4-11: epilogue (two warpgroups x 128 columns of fp32 running sums).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace enks {
+namespace {
+
+constexpr int BM = 128;
+constexpr int KC = 32;               // fp16 elements per chunk row (64 B, SWIZZLE_64B)
+constexpr int kThreads = 384;
+constexpr int kSmemBudget = 210 * 1024;
+
+template <int BN>
+struct L16 {
+    static constexpr int kA = BM * KC * 2;   // 8 KB per plane
+    static constexpr int kB = BN * KC * 2;   // BN x 64 B per plane
+    static constexpr int kStage = 2 * kA + 2 * kB;
+    static constexpr int kSlotCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+    static constexpr int kEpiWG = BN > 128 ? 2 : 1;
+    static constexpr int kColsPerWG = BN > 128 ? BN / 2 : BN;
+};
+
+struct P16 {
+    int64_t M, N, K;
+    float alpha;
+    const float* inv_sa;  // per A row
+    const float* inv_sb;  // per B row
+    float* out;
+    int64_t ldo;
+    int64_t split_stride;
+    int splits;
+    int stages;
+    int chain;
+};
+
+__device__ __forceinline__ uint64_t desc_sw64(const void* smem) {
+    const uint64_t addr = ptx::smem_u32(smem);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+    return d;
+}
+
+__device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+constexpr uint32_t idesc_f16(int M, int N) {
+    // D f32 (bits 4-5 = 1), A/B fp16 (format 0), both K-major, N>>3 @17, M>>4 @24
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    f16p_gemm_kernel(const __grid_constant__ CUtensorMap tAh, const __grid_constant__ CUtensorMap tAl,
+                     const __grid_constant__ CUtensorMap tBh, const __grid_constant__ CUtensorMap tBl,
+                     const P16 p) {
+    using L = L16<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int S = p.stages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * L::kStage);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* tfull = bars + 2 * S;
+    uint64_t* tempty = bars + 2 * S + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = (int64_t)blockIdx.x * BM;
+    const int64_t col0 = (int64_t)blockIdx.y * BN;
+    const int split = blockIdx.z;
+    const int total_chunks = (int)((p.K + KC - 1) / KC);
+    const int cps = (total_chunks + p.splits - 1) / p.splits;
+    const int c_lo = min(total_chunks, split * cps);
+    const int n_chunks = min(total_chunks, c_lo + cps) - c_lo;
+    const int chain = p.chain;
+    const int n_groups = (n_chunks + chain - 1) / chain;
+    constexpr uint32_t kTmemCols = 2 * L::kSlotCols;
+
+    auto ah = [&](int s) { return smem + (size_t)s * L::kStage; };
+    auto al = [&](int s) { return smem + (size_t)s * L::kStage + L::kA; };
+    auto bh = [&](int s) { return smem + (size_t)s * L::kStage + 2 * L::kA; };
+    auto bl = [&](int s) { return smem + (size_t)s * L::kStage + 2 * L::kA + L::kB; };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int q = 0; q < 2; ++q) {
+            ptx::mbar_init(&tfull[q], 1);
+            ptx::mbar_init(&tempty[q], 4 * L::kEpiWG);
+        }
+        ptx::fence_barrier_init();
+        ptx::tma_prefetch_desc(&tAh);
+        ptx::tma_prefetch_desc(&tAl);
+        ptx::tma_prefetch_desc(&tBh);
+        ptx::tma_prefetch_desc(&tBl);
+    }
+    if (warp == 2) ptx::tmem_alloc(tmem_slot, kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int i = 0; i < n_chunks; ++i) {
+                const int s = i % S;
+                ptx::mbar_wait(&empty[s], (uint32_t)(((i / S) & 1) ^ 1));
+                ptx::mbar_arrive_expect_tx(&full[s], 2 * L::kA + 2 * L::kB);
+                const int kc = (c_lo + i) * KC;
+                ptx::tma_load_2d(&tAh, &full[s], ah(s), kc, (int32_t)row0);
+                ptx::tma_load_2d(&tAl, &full[s], al(s), kc, (int32_t)row0);
+                ptx::tma_load_2d(&tBh, &full[s], bh(s), kc, (int32_t)col0);
+                ptx::tma_load_2d(&tBl, &full[s], bl(s), kc, (int32_t)col0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16(BM, BN);
+            for (int i = 0; i < n_chunks; ++i) {
+                const int s = i % S;
+                const int g = i / chain, slot = g & 1;
+                const bool first = (i % chain) == 0;
+                const bool last = (i % chain) == chain - 1 || i == n_chunks - 1;
+                if (first) {
+                    ptx::mbar_wait(&tempty[slot], (uint32_t)(((g >> 1) & 1) ^ 1));
+                    ptx::tc_fence_after();
+                }
+                ptx::mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(slot * L::kSlotCols);
+#pragma unroll
+                for (int k = 0; k < KC / 16; ++k) {
+                    const uint64_t dah = desc_sw64(ah(s) + 32 * k), dal = desc_sw64(al(s) + 32 * k);
+                    const uint64_t dbh = desc_sw64(bh(s) + 32 * k), dbl = desc_sw64(bl(s) + 32 * k);
+                    mma_f16_ss(d, dal, dbh, idesc, (first && k == 0) ? 0u : 1u);
+                    mma_f16_ss(d, dah, dbl, idesc, 1u);
+                    mma_f16_ss(d, dah, dbh, idesc, 1u);
+                }
+                ptx::mma_commit(&empty[s]);
+                if (last) ptx::mma_commit(&tfull[slot]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int wg = (warp - 4) >> 2;
+        if (wg < L::kEpiWG) {
+            const int erow = ((warp & 3) << 5) + lane;
+            const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+            float acc[L::kColsPerWG];
+#pragma unroll
+            for (int j = 0; j < L::kColsPerWG; ++j) acc[j] = 0.f;
+            for (int g = 0; g < n_groups; ++g) {
+                const int slot = g & 1;
+                ptx::mbar_wait(&tfull[slot], (uint32_t)((g >> 1) & 1));
+                ptx::tc_fence_after();
+                const uint32_t base =
+                    tmem + lane_base + (uint32_t)(slot * L::kSlotCols + wg * L::kColsPerWG);
+#pragma unroll
+                for (int c0 = 0; c0 < L::kColsPerWG; c0 += 32) {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(base + c0, v);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(v[j]);
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[slot]);
+            }
+            const int64_t r = row0 + erow;
+            const int64_t c_first = col0 + wg * L::kColsPerWG;
+            if (r < p.M && c_first < p.N) {
+                const float sa = p.alpha * p.inv_sa[r];
+                float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + c_first;
+                const int ncol = (int)min((int64_t)L::kColsPerWG, p.N - c_first);
+#pragma unroll
+                for (int j = 0; j < L::kColsPerWG; ++j)
+                    if (j < ncol) orow[j] = acc[j] * sa * p.inv_sb[c_first + j];
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc(tmem, kTmemCols);
+}
+
+// one block per row: scale = 2^e with max|x| * scale in [2^13, 2^14); h = fp16(xs), l = fp16(xs - h)
+__global__ void __launch_bounds__(256) f16pair_split_kernel(const float* __restrict__ src, int64_t ld,
+                                                            int64_t K, __half* __restrict__ h,
+                                                            __half* __restrict__ l, int64_t ldo,
+                                                            float* __restrict__ inv_scale) {
+    const int64_t r = blockIdx.x;
+    const float* row = src + r * ld;
+    float mx = 0.f;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(row[k]));
+    __shared__ float red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+    int e = 0;
+    if (mx > 0.f && isfinite(mx)) {
+        int ex;
+        frexpf(mx, &ex);  // mx = f * 2^ex, f in [0.5, 1)  ->  mx * 2^(14 - ex) in [2^13, 2^14)
+        e = 14 - ex;
+        e = max(-120, min(120, e));
+    }
+    const float s = ldexpf(1.f, e);
+    if (threadIdx.x == 0) inv_scale[r] = ldexpf(1.f, -e);
+    __half* hr = h + r * ldo;
+    __half* lr = l + r * ldo;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+        const float v = row[k] * s;
+        const __half hv = __float2half_rn(v);
+        hr[k] = hv;
+        lr[k] = __float2half_rn(v - __half2float(hv));
+    }
+}
+
+// fp32 reconstruction x = (h + l) / scale (members read-back, covariance tracking)
+__global__ void f16pair_recon_kernel(const __half* __restrict__ h, const __half* __restrict__ l,
+                                     int64_t ldi, const float* __restrict__ inv_scale, int64_t rows,
+                                     int64_t K, float* __restrict__ out, int64_t ldo) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= rows * K) return;
+    const int64_t r = e / K, k = e - r * K;
+    out[r * ldo + k] = (__half2float(h[r * ldi + k]) + __half2float(l[r * ldi + k])) * inv_scale[r];
+}
+
+__global__ void f16p_sum_splits(const float* __restrict__ ws, int split, int64_t M, int64_t N,
+                                float* __restrict__ C, int64_t ldc) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= M * N) return;
+    const int64_t r = e / N, c = e - r * N;
+    float v = 0.f;
+    for (int z = 0; z < split; ++z) v += ws[(int64_t)z * M * N + e];
+    C[r * ldc + c] = v;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode16() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* q = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &qr) ==
+                cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(q);
+    }
+    return fn;
+}
+
+bool map16(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+    EncodeTiledFn fn = encode16();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+int launch16(const CUtensorMap* maps, P16 p, dim3 grid, cudaStream_t st) {
+    using L = L16<BN>;
+    int stages = kSmemBudget / L::kStage;
+    if (stages > 8) stages = 8;
+    p.stages = stages;
+    const size_t smem = (size_t)stages * L::kStage + 1024 + 512;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(f16p_gemm_kernel<BN>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) {
+            set_error("f16p gemm: smem attribute: %s", cudaGetErrorString(e));
+            return ENKS_E_CUDA;
+        }
+        configured = true;
+    }
+    f16p_gemm_kernel<BN><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+    return check_launch("enks_gemm_f16pair");
+}
+
+int choose_split16(int tiles, int64_t chunks) {
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 64; ++s) {
+        if (chunks / s < 8 && s > 1) break;
+        const int units = tiles * s;
+        const int waves = (units + kNumSMs - 1) / kNumSMs;
+        const double eff = (double)units / (double)(waves * kNumSMs);
+        if (eff > best_eff + 0.03) {
+            best_eff = eff;
+            best = s;
+        }
+        if (eff > 0.95) break;
+    }
+    return best;
+}
+
+}  // namespace
+}  // namespace enks
+
+extern "C" {
+
+int enks_f16pair_split(const float* src, int64_t ld, int64_t rows, int64_t K, void* h, void* l,
+                       int64_t ldo, float* inv_scale, void* stream) {
+    ENKS_REQUIRE(src && h && l && inv_scale, "enks_f16pair_split: null pointer");
+    if (rows <= 0 || K <= 0) return ENKS_OK;
+    enks::f16pair_split_kernel<<<(unsigned)rows, 256, 0, enks::as_stream(stream)>>>(
+        src, ld, K, static_cast<__half*>(h), static_cast<__half*>(l), ldo, inv_scale);
+    return enks::check_launch("enks_f16pair_split");
+}
+
+int enks_f16pair_recon(const void* h, const void* l, int64_t ldi, const float* inv_scale,
+                       int64_t rows, int64_t K, float* out, int64_t ldo, void* stream) {
+    ENKS_REQUIRE(h && l && inv_scale && out, "enks_f16pair_recon: null pointer");
+    const int64_t total = rows * K;
+    if (total <= 0) return ENKS_OK;
+    enks::f16pair_recon_kernel<<<(unsigned)((total + 255) / 256), 256, 0, enks::as_stream(stream)>>>(
+        static_cast<const __half*>(h), static_cast<const __half*>(l), ldi, inv_scale, rows, K, out,
+        ldo);
+    return enks::check_launch("enks_f16pair_recon");
+}
+
+int64_t enks_gemm_f16pair_ws_bytes(int64_t M, int64_t N, int64_t K) {
+    const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+    const int tiles = (int)((M + enks::BM - 1) / enks::BM) * (int)((N + BN - 1) / BN);
+    const int split = enks::choose_split16(tiles, (K + enks::KC - 1) / enks::KC);
+    return split > 1 ? (int64_t)split * M * N * (int64_t)sizeof(float) : 0;
+}
+
+int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah, const void* Al,
+                      int64_t lda, const float* inv_sa, const void* Bh, const void* Bl, int64_t ldb,
+                      const float* inv_sb, float* C, int64_t ldc, void* ws, void* stream) {
+    using namespace enks;
+    ENKS_REQUIRE(Ah && Al && Bh && Bl && inv_sa && inv_sb && C, "enks_gemm_f16pair: null pointer");
+    ENKS_REQUIRE(N >= 1 && N <= 256 && K >= 1 && (lda % 8) == 0 && (ldb % 8) == 0,
+                 "enks_gemm_f16pair: need N <= 256 and 16-B aligned fp16 rows (ld %% 8 == 0)");
+    if (M == 0) return ENKS_OK;
+    const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+    CUtensorMap maps[4];
+    if (!map16(&maps[0], Ah, M, K, lda, BM) || !map16(&maps[1], Al, M, K, lda, BM) ||
+        !map16(&maps[2], Bh, N, K, ldb, BN) || !map16(&maps[3], Bl, N, K, ldb, BN)) {
+        set_error("enks_gemm_f16pair: cuTensorMapEncodeTiled failed (alignment?)");
+        return ENKS_E_UNSUPPORTED;
+    }
+    const int m_tiles = (int)((M + BM - 1) / BM);
+    const int split = choose_split16(m_tiles, (K + KC - 1) / KC);
+    ENKS_REQUIRE(split == 1 || ws, "enks_gemm_f16pair: split-K needs workspace");
+    P16 p;
+    p.M = M; p.N = N; p.K = K;
+    p.alpha = alpha;
+    p.inv_sa = inv_sa;
+    p.inv_sb = inv_sb;
+    p.splits = split;
+    const char* ch = getenv("ENKS_TC_CHAIN");
+    p.chain = ch ? atoi(ch) : 8;
+    if (p.chain < 1) p.chain = 1;
+    const bool direct = split == 1;
+    p.out = direct ? C : static_cast<float*>(ws);
+    p.ldo = direct ? ldc : N;
+    p.split_stride = direct ? 0 : M * N;
+    dim3 grid((unsigned)m_tiles, 1, (unsigned)split);
+    cudaStream_t st = as_stream(stream);
+    int rc;
+    switch (BN) {
+        case 32: rc = launch16<32>(maps, p, grid, st); break;
+        case 64: rc = launch16<64>(maps, p, grid, st); break;
+        case 128: rc = launch16<128>(maps, p, grid, st); break;
+        default: rc = launch16<256>(maps, p, grid, st); break;
+    }
+    if (rc || direct) return rc;
+    f16p_sum_splits<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(static_cast<float*>(ws), split,
+                                                                     M, N, C, ldc);
+    return check_launch("enks_gemm_f16pair(split reduce)");
+}
+
+}  // extern "C"

@@ -175,9 +175,15 @@ class DeviceSmoother:
         # tcgen05 3xTF32 cross moments (ENKS_TC=0 forces the SIMT engine for A/B checks)
         self.use_tc = (os.environ.get("ENKS_TC", "1") != "0" and hasattr(ops, "gemm_nt_tc")
                        and p <= 256 and K >= 128)
-        if self.use_tc:
+        # basis storage: fp16 pairs (tcgen05 kind::f16 contraction, gemm_f16p.cu) or fp32
+        self.pair = (self.use_tc and K % 8 == 0 and hasattr(ops, "gemm_f16pair")
+                     and os.environ.get("ENKS_BASIS", "f16pair") == "f16pair")
+        if self.use_tc and not self.pair:
             self.yc_hi = ops.empty(p, K)
             self.yc_lo = ops.empty(p, K)
+        if self.pair:
+            self.A_new = ops.empty(d, K)   # fp32 anomalies of the newest slice
+            self.Yc_new = ops.empty(p, K)  # fp32 centred observations of the newest slice
         # the gain-side products (correction, gain, newest-slice shift) on tcgen05 as well
         self.use_tc2 = self.use_tc and p % 4 == 0 and m % 4 == 0 and hasattr(ops, "gemm_tc")
         if self.use_tc2:
@@ -200,7 +206,7 @@ class DeviceSmoother:
         x0 = ops.to_device(np.asarray(x0_packed, float))
         self.mean[:d] = x0
         self.last.copy_(x0[:p].repeat(1, self.Nl))
-        self.Abuf[:d].zero_()
+        self._store_rows("A", 0, ops.zeros(d, K))
 
     # ------------------------------------------------------------ storage
     def _grow(self, cap: int) -> None:
@@ -208,28 +214,70 @@ class DeviceSmoother:
         if cap <= self.cap:
             return
         ops, d, p, K, m = self.ops, self.d, self.p, self.K, self.m
-        Abuf = ops.empty((cap + 1) * d, K)
-        Ybuf = ops.empty(cap * p, K)
-        G = ops.zeros((cap + 1) * d, cap * p)
-        mean = ops.zeros((cap + 1) * d, m)
-        PA = ops.empty((cap + 1) * d, p)
-        PY = ops.empty(cap * p, p)
+        ra, ry = (cap + 1) * d, cap * p
+        if self.pair:
+            f16 = torch.float16
+            new = dict(Ah=ops.empty(ra, K, dtype=f16), Al=ops.empty(ra, K, dtype=f16),
+                       a_inv=ops.empty(ra), Yh=ops.empty(ry, K, dtype=f16),
+                       Yl=ops.empty(ry, K, dtype=f16), y_inv=ops.empty(ry))
+            a_keys, y_keys = ("Ah", "Al", "a_inv"), ("Yh", "Yl", "y_inv")
+        else:
+            new = dict(Abuf=ops.empty(ra, K), Ybuf=ops.empty(ry, K))
+            a_keys, y_keys = ("Abuf",), ("Ybuf",)
+        G = ops.zeros(ra, ry)
+        mean = ops.zeros(ra, m)
+        PA = ops.empty(ra, p)
+        PY = ops.empty(ry, p)
         if self.cap:
             rows_a, rows_y = (self.t + 1) * d, self.t * p
-            Abuf[:rows_a] = self.Abuf[:rows_a]
-            Ybuf[:rows_y] = self.Ybuf[:rows_y]
+            for k in a_keys:
+                new[k][:rows_a] = getattr(self, k)[:rows_a]
+            for k in y_keys:
+                new[k][:rows_y] = getattr(self, k)[:rows_y]
             G[:rows_a, :rows_y] = self.G[:rows_a, :rows_y]
             mean[:rows_a] = self.mean[:rows_a]
-        self.Abuf, self.Ybuf, self.G, self.mean, self.PA, self.PY = Abuf, Ybuf, G, mean, PA, PY
+        for k, v in new.items():
+            setattr(self, k, v)
+        self.G, self.mean, self.PA, self.PY = G, mean, PA, PY
         if getattr(self, "use_tc2", False):
             self.pyT_hi = ops.empty(p * cap * p)
             self.pyT_lo = ops.empty(p * cap * p)
         self.cap = cap
 
     def memory_bytes(self) -> int:
+        keys = ("Ah", "Al", "a_inv", "Yh", "Yl", "y_inv", "A_new", "Yc_new") if self.pair \
+            else ("Abuf", "Ybuf")
         return sum(t.numel() * t.element_size() for t in
-                   (self.Abuf, self.Ybuf, self.G, self.mean, self.PA, self.PY, self.slice_raw,
-                    self.obs_raw, self.last))
+                   [getattr(self, k) for k in keys] + [self.G, self.mean, self.PA, self.PY,
+                                                       self.slice_raw, self.obs_raw, self.last])
+
+    def _store_rows(self, which: str, r0: int, src) -> None:
+        """Write fp32 rows (anomalies / centred observations) into the basis at row r0."""
+        R = src.shape[0]
+        if self.pair:
+            h, l, inv = (self.Ah, self.Al, self.a_inv) if which == "A" else (self.Yh, self.Yl,
+                                                                            self.y_inv)
+            self.ops.f16pair_split(src, h[r0:r0 + R], l[r0:r0 + R], inv[r0:r0 + R])
+        else:
+            buf = self.Abuf if which == "A" else self.Ybuf
+            if buf[r0:r0 + R].data_ptr() != src.data_ptr():
+                buf[r0:r0 + R].copy_(src)
+
+    def _rows_fp32(self, which: str, r0: int, r1: int):
+        """fp32 view (fp32 basis) or reconstruction (fp16 pairs) of basis rows [r0, r1)."""
+        if not self.pair:
+            return (self.Abuf if which == "A" else self.Ybuf)[r0:r1]
+        h, l, inv = (self.Ah, self.Al, self.a_inv) if which == "A" else (self.Yh, self.Yl,
+                                                                        self.y_inv)
+        out = self.ops.empty(r1 - r0, self.K)
+        if r1 > r0:
+            self.ops.f16pair_recon(h[r0:r1], l[r0:r1], inv[r0:r1], out)
+        return out
+
+    def newest_anomalies(self):
+        """fp32 anomalies of the newest predicted slice (d x K)."""
+        d, t = self.d, self.t
+        return self.A_new if self.pair else self.Abuf[t * d:(t + 1) * d]
 
     # ------------------------------------------------------------ binding
     def bind(self, vs) -> None:
@@ -318,7 +366,11 @@ class DeviceSmoother:
             # ΔU slot = w, U slot = u + w  (one draw fills both, enks.py:168)
             self._noise(self.noise_w, head, tau, CH_W, l, out=sr[n + l:], base=self.last[n:],
                         out_plus=sr[n:n + l])
-        self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d])
+        if self.pair:
+            self._center(sr, self.mean[tau * d:(tau + 1) * d], self.A_new)
+            self._store_rows("A", tau * d, self.A_new)
+        else:
+            self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d])
         self.t = tau
 
     # ------------------------------------------------------------ update
@@ -334,14 +386,22 @@ class DeviceSmoother:
         if self._obs_t != tau or self._obs_key != (streams.seed, tuple(streams.prefix)):
             self._noise(self.noise_vx, head, tau, CH_VX, n, base=sr[:n], out_plus=ob[:n])
             self._noise(self.noise_vu, head, tau, CH_VU, l, base=sr[n:n + l], out_plus=ob[n:])
-        yc = self.Ybuf[(tau - 1) * p:tau * p]
+        yc = self.Yc_new if self.pair else self.Ybuf[(tau - 1) * p:tau * p]
         self._center(ob, self.ybar, yc)
+        if self.pair:
+            self._store_rows("Y", (tau - 1) * p, yc)
 
         # P = [A_s0..A_tau ; Yc_1..Yc_tau] Yc_tau^T  (local K-partial, then allreduce)
         a0 = d if self.slice0_zero else 0
         rows_a = (tau + 1) * d
         PA, PY = self.PA[a0:rows_a], self.PY[:tau * p]
-        if self.use_tc:
+        if self.pair:
+            yb = slice((tau - 1) * p, tau * p)
+            ops.gemm_f16pair(self.Ah[a0:rows_a], self.Al[a0:rows_a], self.a_inv[a0:rows_a],
+                             self.Yh[yb], self.Yl[yb], self.y_inv[yb], PA, tag="cross")
+            ops.gemm_f16pair(self.Yh[:tau * p], self.Yl[:tau * p], self.y_inv[:tau * p],
+                             self.Yh[yb], self.Yl[yb], self.y_inv[yb], PY, tag="cross")
+        elif self.use_tc:
             ops.tf32_split(yc, self.yc_hi, self.yc_lo)
             ops.gemm_nt_tc(self.Abuf[a0:rows_a], self.yc_hi, self.yc_lo, PA, tag="cross")
             ops.gemm_nt_tc(self.Ybuf[:tau * p], self.yc_hi, self.yc_lo, PY, tag="cross")
@@ -380,13 +440,13 @@ class DeviceSmoother:
         ops.gemm(gcol, self.innov, mv, beta=1.0, C0=mv)
         # newest slice [x; u] for the next forecast: mean + A_tau - G_{tau,tau} Yc_tau
         g_tt = self.G[r0:r0 + p, (tau - 1) * p:tau * p]
+        a_new = self.newest_anomalies()
         if self.use_tc2:
             ops.tf32_split(yc, self.ycT_hi, self.ycT_lo, transpose=True)
             ops.gemm_tc(g_tt, self.ycT_hi, self.ycT_lo, self.last, alpha=-1.0, beta=1.0,
-                        C0=self.Abuf[r0:r0 + p], bias=self.mean[r0:r0 + p], bias_cols=self.m,
-                        tag="shift")
+                        C0=a_new[:p], bias=self.mean[r0:r0 + p], bias_cols=self.m, tag="shift")
         else:
-            ops.gemm(g_tt, yc, self.last, alpha=-1.0, beta=1.0, C0=self.Abuf[r0:r0 + p],
+            ops.gemm(g_tt, yc, self.last, alpha=-1.0, beta=1.0, C0=a_new[:p],
                      bias=self.mean[r0:r0 + p], bias_cols=self.m)
 
     # ------------------------------------------------------------ readback
@@ -396,12 +456,13 @@ class DeviceSmoother:
         R = (t + 1) * d
         out = ops.empty(R, self.K)
         a0 = d if self.slice0_zero else 0
-        out[:a0] = self.Abuf[:a0]
+        A = self._rows_fp32("A", 0, R)
+        out[:a0] = A[:a0]
         if t >= 1:
-            ops.gemm(self.G[a0:R, :t * p], self.Ybuf[:t * p], out[a0:], alpha=-1.0, beta=1.0,
-                     C0=self.Abuf[a0:R], tri=(d, p) if a0 else (0, 0))
+            ops.gemm(self.G[a0:R, :t * p], self._rows_fp32("Y", 0, t * p), out[a0:], alpha=-1.0,
+                     beta=1.0, C0=A[a0:R], tri=(d, p) if a0 else (0, 0))
         else:
-            out[a0:] = self.Abuf[a0:R]
+            out[a0:] = A[a0:R]
         return out
 
     def members_device(self):
@@ -433,8 +494,14 @@ class DeviceSmoother:
         M = np.asarray(members_local, dtype=float).transpose(1, 0, 2).reshape(R, self.K)
         Mdev = ops.to_device(M)
         self.G.zero_()
-        self._center(Mdev, self.mean[:R], self.Abuf[:R])
-        x0_spread = bool(torch.any(self.Abuf[:d] != 0).item())
+        anom = ops.empty(R, self.K)
+        self._center(Mdev, self.mean[:R], anom)
+        self._store_rows("A", 0, anom)
+        if self.t:  # no observation history: zero basis rows (their gains are zero)
+            self._store_rows("Y", 0, ops.zeros(self.t * self.p, self.K))
+        if self.pair:
+            self.A_new.copy_(anom[self.t * d:(self.t + 1) * d])
+        x0_spread = bool(torch.any(anom[:d] != 0).item())
         self.slice0_zero = not x0_spread
         last = Mdev[self.t * d:self.t * d + self.p]
         self.last.copy_(last)

@@ -198,7 +198,7 @@ def predict(ens: TrajectoryEnsemble, vs, streams, cov: Optional[SmootherCovarian
     eng.predict(vs, streams)
     if cov is not None:
         d = eng.d
-        dev_new = eng.Abuf[eng.t * d:(eng.t + 1) * d]
+        dev_new = eng.newest_anomalies()
         dev_traj = eng.deviations()
         cov.sigma_pred = _cov_product(eng, dev_new, dev_new)
         cov.sigma_cross = _cov_product(eng, dev_traj, dev_new)

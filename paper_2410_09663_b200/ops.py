@@ -213,6 +213,38 @@ class DeviceOps:
             ev1.record()
             self.profile.append((tag, ev0, ev1, 2.0 * M * N * K))
 
+    # -- fp16-pair basis (gemm_f16p.cu) -------------------------------------
+    def f16pair_split(self, src, h, l, inv_scale):
+        """Per-row power-of-two scaled (hi, lo) fp16 planes of src (rows x K)."""
+        self.launches += 1
+        _lib.call("enks_f16pair_split", _p(src), _ld(src), src.shape[0], src.shape[1], _p(h), _p(l),
+                  _ld(h), _p(inv_scale), self._stream())
+
+    def f16pair_recon(self, h, l, inv_scale, out):
+        self.launches += 1
+        _lib.call("enks_f16pair_recon", _p(h), _p(l), _ld(h), _p(inv_scale), out.shape[0],
+                  out.shape[1], _p(out), _ld(out), self._stream())
+
+    def gemm_f16pair(self, Ah, Al, inv_sa, Bh, Bl, inv_sb, C, *, alpha=1.0, tag=None):
+        """C = alpha * diag(inv_sa) (Ah + Al)(Bh + Bl)^T diag(inv_sb), tcgen05 kind::f16."""
+        M, K = Ah.shape
+        N = Bh.shape[0]
+        if M == 0:
+            return
+        nbytes = self.lib.enks_gemm_f16pair_ws_bytes(M, N, K)
+        ws = self._workspace(nbytes) if nbytes > 0 else None
+        self.launches += 2 if nbytes > 0 else 1
+        prof = self.profile is not None and tag is not None
+        if prof:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+        _lib.call("enks_gemm_f16pair", M, N, K, float(alpha), _p(Ah), _p(Al), _ld(Ah), _p(inv_sa),
+                  _p(Bh), _p(Bl), _ld(Bh), _p(inv_sb), _p(C), _ld(C), ws, self._stream())
+        if prof:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record()
+            self.profile.append((tag, ev0, ev1, 2.0 * M * N * K))
+
     def spd_inverse(self, S, scale, inv, status, jitter):
         p = S.shape[0]
         if getattr(self, "_spd_ws", None) is None or self._spd_ws.numel() < p * p:

@@ -305,3 +305,29 @@ def test_gemm_tc_general(dev_ops, M, N, K, tri, split):
     scale = 0.5 * (A.double().abs() @ B.double().abs()) + C0.double().abs() + 1.0
     err = ((C.double().cpu() - ref).abs() / scale).max().item()
     assert err < 1e-6, err
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 4096), (300, 256, 131072), (77, 6, 1000), (640, 256, 8192),
+                                   (5, 32, 64)])
+def test_gemm_f16pair(dev_ops, M, N, K):
+    """fp16-pair storage + kind::f16 contraction: fp32-FFMA-level accuracy (~2^-22 per product)."""
+    g = torch.Generator().manual_seed(M + N + K)
+    A = (torch.randn(M, K, generator=g) + 0.5) * torch.logspace(-3, 3, M).unsqueeze(1)
+    B = torch.randn(N, K, generator=g)
+    dA, dB = A.to(dev_ops.device), B.to(dev_ops.device)
+    ah = torch.empty(M, K, dtype=torch.float16, device=dev_ops.device)
+    al = torch.empty_like(ah)
+    bh = torch.empty(N, K, dtype=torch.float16, device=dev_ops.device)
+    bl = torch.empty_like(bh)
+    sa, sb = dev_ops.empty(M), dev_ops.empty(N)
+    dev_ops.f16pair_split(dA, ah, al, sa)
+    dev_ops.f16pair_split(dB, bh, bl, sb)
+    rec = dev_ops.empty(M, K)
+    dev_ops.f16pair_recon(ah, al, sa, rec)
+    assert ((rec.double().cpu() - A.double()).abs() / A.double().abs().amax(1, keepdim=True)).max() < 2e-7
+    C = dev_ops.zeros(M, N)
+    dev_ops.gemm_f16pair(ah, al, sa, bh, bl, sb, C, alpha=0.5)
+    ref = 0.5 * (A.double() @ B.double().t())
+    scale = 0.5 * (A.double().abs() @ B.double().abs().t())
+    err = ((C.double().cpu() - ref).abs() / scale).max().item()
+    assert err < 1e-6, err
