@@ -23,6 +23,8 @@
 // Warp roles (384 threads): warp 0 = MMA issuer, warp 2 = TMEM allocator,
 // warps 4-7 = layer-1 producer (thread = pixel), warps 8-11 = epilogue
 // (thread = pixel = TMEM lane).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -56,13 +58,27 @@ constexpr int kXV = 2 * 4 * 4;                      // [parity][warp][3 (+pad)]
 constexpr int kOffBar = kOffX + (2 * kXD + 2 * kXV) * 4;
 constexpr int kSmem = kOffBar + 32 * 8 + 1024;      // + alignment slack
 
+__device__ __forceinline__ float exp2f_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ uint32_t sw128(int row, int byte) {
     return (uint32_t)(row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15)));
 }
 
+// tanh(x) = 1 - 2 / (1 + e^{2x}) with one SFU op (ex2) and a Newton reciprocal on the FMA
+// pipe (the SFU is the scarce unit: 64 tanh per pixel-row across layers 1 and 2).
 __device__ __forceinline__ float tanh_fast(float x) {
-    const float t = __expf(2.f * x);
-    return 1.f - __fdividef(2.f, 1.f + t);
+    x = fminf(fmaxf(x, -15.f), 15.f);
+    const float t = exp2f_approx(x * 2.8853900817779268f);  // e^{2x}
+    const float d = 1.f + t;
+    float r = __int_as_float(0x7EF311C3 - __float_as_int(d));
+    r = r * fmaf(-d, r, 2.f);
+    r = r * fmaf(-d, r, 2.f);
+    r = r * fmaf(-d, r, 2.f);
+    return fmaf(-2.f, r, 1.f);
 }
 
 struct Cnn3Args {
@@ -81,6 +97,7 @@ struct Cnn3Args {
     int64_t ldo;
     int rows;
     int64_t n_members;
+    int debug;  // ENKS_CNN_DEBUG: 1 = no MMAs, 2 = no layer-1 math, 4 = no epilogue math
 };
 
 __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) {
@@ -176,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                         const uint8_t* bh_t = sm + kOffB + (dy * 2 + 0) * kBTile;
                         const uint8_t* bl_t = sm + kOffB + (dy * 2 + 1) * kBTile;
 #pragma unroll
-                        for (int k = 0; k < C1 / 8; ++k) {
+                        for (int k = 0; k < ((a.debug & 1) ? 0 : C1 / 8); ++k) {
                             const uint64_t adh = ptx::desc_kmajor_sw128(ah_t + 32 * k);
                             const uint64_t adl = ptx::desc_kmajor_sw128(al_t + 32 * k);
                             const uint64_t bdh = ptx::desc_kmajor_sw128(bh_t + 32 * k);
@@ -199,18 +216,30 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
             const float* xm = a.x + mem * W;
             const float* um = a.u + mem * W;
-            auto load_row = [&](int j) {  // input row j (0 <= j < n) into ring slot j & 3
+            // input rows are prefetched into registers two rows ahead and written into the
+            // 4-slot ring one iteration later, so the global-load latency overlaps a row of work
+            auto fetch = [&](int j, float& vx, float& vu) {
+                vx = j < n ? xm[(int64_t)j * a.ldx + x] : 0.f;
+                vu = j < n ? um[(int64_t)j * a.ldu + x] : 0.f;
+            };
+            auto put = [&](int j, float vx, float vu) {  // row j into ring slot j & 3
                 float* dst = in_ring + (j & 3) * 2 * kInRow;
-                dst[x + 1] = xm[(int64_t)j * a.ldx + x];
-                dst[kInRow + x + 1] = um[(int64_t)j * a.ldu + x];
+                dst[x + 1] = vx;
+                dst[kInRow + x + 1] = vu;
                 if (x == 0) {
                     dst[0] = 0.f; dst[kInRow - 1] = 0.f;
                     dst[kInRow] = 0.f; dst[2 * kInRow - 1] = 0.f;
                 }
             };
-            load_row(0);
+            float px, pu, qx, qu;
+            fetch(0, px, pu);
+            put(0, px, pu);
+            fetch(1, px, pu);  // row r+1 pending in (px, pu)
             for (int r = 0; r < n; ++r) {
-                if (r + 1 < n) load_row(r + 1);
+                if (r + 1 < n) put(r + 1, px, pu);
+                fetch(r + 2, qx, qu);
+                px = qx;
+                pu = qu;
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 float in[18];
 #pragma unroll
@@ -226,10 +255,14 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 const int Rg = it * n + r;
                 const int slot = Rg % NA;
                 ptx::mbar_wait(&a_empty[slot], (uint32_t)(((Rg / NA) & 1) ^ 1));
+                if (a.debug & 16) {
+                    ptx::mbar_arrive(&a_full[slot]);
+                    continue;
+                }
                 uint8_t* ah_t = sm + kOffA + (slot * 2 + 0) * kATile;
                 uint8_t* al_t = sm + kOffA + (slot * 2 + 1) * kATile;
 #pragma unroll 2
-                for (int c4 = 0; c4 < C1 / 4; ++c4) {
+                for (int c4 = 0; c4 < ((a.debug & 2) ? 0 : C1 / 4); ++c4) {
                     float hv[4];
 #pragma unroll
                     for (int pr = 0; pr < 2; ++pr) {  // channel pair (c, c+1), packed FFMA2
@@ -275,8 +308,16 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 const int Yg = it * n + y;
                 const int q = Yg % NACC;
                 const int par = Yg & 1;
+                // residual inputs of the rows completed below, loaded before the waits
+                const float xres_m = y >= 1 ? xm[(int64_t)(y - 1) * a.ldx + x] : 0.f;
+                const float xres_0 = y == n - 1 ? xm[(int64_t)y * a.ldx + x] : 0.f;
                 ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / NACC) & 1));
                 ptx::tc_fence_after();
+                if (a.debug & 8) {
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&acc_empty[q]);
+                    continue;
+                }
                 const uint32_t base = tmem + lane_base + (uint32_t)(q * NB);
                 float s[32], t[32];
                 uint32_t v[32];
@@ -286,7 +327,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
                 if (lane == 31) {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) xd0[(par * 4 + ew) * 32 + c] = t[c];
+                    for (int c = 0; c < 32; c += 4)
+                        *reinterpret_cast<float4*>(xd0 + (par * 4 + ew) * 32 + c) =
+                            make_float4(t[c], t[c + 1], t[c + 2], t[c + 3]);
                 }
 #pragma unroll
                 for (int c = 0; c < 32; ++c) s[c] = __shfl_up_sync(0xffffffffu, t[c], 1);
@@ -303,7 +346,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
                 if (lane == 0) {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) xd2[(par * 4 + ew) * 32 + c] = t[c];
+                    for (int c = 0; c < 32; c += 4)
+                        *reinterpret_cast<float4*>(xd2 + (par * 4 + ew) * 32 + c) =
+                            make_float4(t[c], t[c + 1], t[c + 2], t[c + 3]);
                 }
 #pragma unroll
                 for (int c = 0; c < 32; ++c) {
@@ -313,28 +358,50 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 asm volatile("bar.sync 2, 128;" ::: "memory");
                 if (lane == 0 && ew > 0) {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) s[c] += xd0[(par * 4 + ew - 1) * 32 + c];
+                    for (int c = 0; c < 32; c += 4) {
+                        const float4 e4 = *reinterpret_cast<const float4*>(xd0 + (par * 4 + ew - 1) * 32 + c);
+                        s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
+                    }
                 }
                 if (lane == 31 && ew < 3) {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) s[c] += xd2[(par * 4 + ew + 1) * 32 + c];
+                    for (int c = 0; c < 32; c += 4) {
+                        const float4 e4 = *reinterpret_cast<const float4*>(xd2 + (par * 4 + ew + 1) * 32 + c);
+                        s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
+                    }
                 }
                 // layer-2 activation and the layer-3 taps v[ky][kx] = sum_c w3 h
-                float2 v01 = make_float2(0.f, 0.f), v23 = v01, v45 = v01, v67 = v01;
-                float v8 = 0.f;
+                // four independent partial sums (8 channels each) for ILP
+                float2 v01[4], v23[4], v45[4], v67[4];
+                float v8[4];
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
+                for (int g = 0; g < 4; ++g) {
+                    v01[g] = v23[g] = v45[g] = v67[g] = make_float2(0.f, 0.f);
+                    v8[g] = 0.f;
+                }
+#pragma unroll
+                for (int c = 0; c < ((a.debug & 4) ? 0 : 32); ++c) {
+                    const int g = c & 3;
                     const float h = tanh_fast(s[c] + b2s[c]);
                     const float2 hh = make_float2(h, h);
                     const float4 w0 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride);
                     const float4 w1 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride + 4);
-                    v01 = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01);
-                    v23 = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23);
-                    v45 = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45);
-                    v67 = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67);
-                    v8 = fmaf(w3s[c * kW3Stride + 8], h, v8);
+                    v01[g] = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01[g]);
+                    v23[g] = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23[g]);
+                    v45[g] = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45[g]);
+                    v67[g] = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67[g]);
+                    v8[g] = fmaf(w3s[c * kW3Stride + 8], h, v8[g]);
                 }
-                const float vv[9] = {v01.x, v01.y, v23.x, v23.y, v45.x, v45.y, v67.x, v67.y, v8};
+#pragma unroll
+                for (int g = 1; g < 4; ++g) {
+                    v01[0].x += v01[g].x; v01[0].y += v01[g].y;
+                    v23[0].x += v23[g].x; v23[0].y += v23[g].y;
+                    v45[0].x += v45[g].x; v45[0].y += v45[g].y;
+                    v67[0].x += v67[g].x; v67[0].y += v67[g].y;
+                    v8[0] += v8[g];
+                }
+                const float vv[9] = {v01[0].x, v01[0].y, v23[0].x, v23[0].y, v45[0].x,
+                                     v45[0].y, v67[0].x, v67[0].y, v8[0]};
                 // fold horizontal taps: lane x3 takes v[ky][0] from x3-1, v[ky][2] from x3+1
                 float tk[3];
 #pragma unroll
@@ -361,12 +428,12 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     const int yo = y - 1;
                     const float o = acc3[yo % 3] + tk[2];
                     acc3[yo % 3] = 0.f;
-                    om[(int64_t)yo * a.ldo + x] = xm[(int64_t)yo * a.ldx + x] + a.alpha * (b3 + o);
+                    om[(int64_t)yo * a.ldo + x] = xres_m + a.alpha * (b3 + o);
                 }
                 if (y == n - 1) {
                     const float o = acc3[y % 3];
                     acc3[y % 3] = 0.f;
-                    om[(int64_t)y * a.ldo + x] = xm[(int64_t)y * a.ldx + x] + a.alpha * (b3 + o);
+                    om[(int64_t)y * a.ldo + x] = xres_0 + a.alpha * (b3 + o);
                 }
             }
         }
@@ -397,6 +464,10 @@ int cnn3_tc_forward(const float* weights, const float* biases, float alpha, cons
     a.x = x; a.ldx = ldx; a.u = u; a.ldu = ldu; a.out = out; a.ldo = ldo;
     a.rows = rows;
     a.n_members = n_members;
+    {
+        const char* e = getenv("ENKS_CNN_DEBUG");
+        a.debug = e ? atoi(e) : 0;
+    }
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(cnn3_tc_kernel,

@@ -29,4 +29,5 @@ e.record()
 torch.cuda.synchronize()
 ms = s.elapsed_time(e) / reps
 flops = N * model.flops_per_member_step()
-print(f"cnn N={N}: {ms:.3f} ms/step, {flops / ms / 1e9:.1f} TFLOP/s algorithmic")
+print(f"cnn N={N} debug={os.environ.get('ENKS_CNN_DEBUG', '0')}: {ms:.3f} ms/step, "
+      f"{flops / ms / 1e9:.1f} TFLOP/s algorithmic")
