@@ -80,7 +80,8 @@ int enks_noise_fill_multi(const uint32_t* head, int n_head, int64_t member0, int
  * obs.mean(axis=0) (enks.py:231) and the anomaly formation (enks.py:232-233).
  * Anomalies are formed relative to a per-(row, col) shift z0 (global member
  * 0), so identical members give exactly zero anomalies at any N.
- *   enks_member_sum    : acc[r*cols+j] (double) = sum over local members of (src - z0).
+ *   enks_member_sum    : acc[r*cols+j] (double) = sum over local members of (src - z0);
+ *                        amax (optional) = max over local members of |src - z0|.
  *                        z0 == NULL -> z0 is local member 0 (single-rank case).
  *   enks_member_center : mean = z0 + acc/n_total; anom = (src - z0) - acc/n_total.
  *                        anom may be NULL (mean only) and may alias src.
@@ -88,10 +89,22 @@ int enks_noise_fill_multi(const uint32_t* head, int n_head, int64_t member0, int
  */
 int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols);
 int enks_member_sum(const float* src, int64_t ld_src, int rows, int64_t n_members, int cols,
-                    const float* z0, double* acc, void* ws, void* stream);
+                    const float* z0, double* acc, float* amax, void* ws, void* stream);
 int enks_member_center(const float* src, int64_t ld_src, int rows, int64_t n_members, int cols,
                        const float* z0, const double* acc, int64_t n_total, float* mean,
                        float* anom, int64_t ld_anom, void* stream);
+
+/*
+ * Centring straight into the fp16-pair basis (see enks_f16pair_split): per-row scale
+ * from the bound max|src - z0| + |mean shift| (amax from enks_member_sum), then
+ * h/l planes (ld ldh) + inv_scale, the member mean, and optionally an fp32 copy of
+ * the first rows_f32 rows (f32, ld_f32).  scale_ws: `rows` floats of scratch.
+ */
+int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64_t n_members,
+                               int cols, const float* z0, const double* acc, const float* amax,
+                               int64_t n_total, float* mean, void* h, void* l, int64_t ldh,
+                               float* inv_scale, float* scale_ws, float* f32, int64_t ld_f32,
+                               int rows_f32, void* stream);
 
 /*
  * Dense fp32 GEMM used by every contraction of the path (K2 dense colouring,

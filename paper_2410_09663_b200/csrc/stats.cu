@@ -9,6 +9,8 @@
 // enks_member_sum is a two-stage deterministic reduction: stage 1 splits the
 // member axis into chunks (fp64 partials, fixed order), stage 2 adds the
 // chunks in order.  enks_member_center is a flat, float4-vectorised pass.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace enks {
@@ -18,7 +20,8 @@ constexpr int kSumThreads = 128;
 
 __global__ void __launch_bounds__(kSumThreads)
     member_partial_kernel(const float* __restrict__ src, int64_t ld, int rows, int64_t n, int cols,
-                          const float* __restrict__ z0, double* __restrict__ part, int64_t chunk) {
+                          const float* __restrict__ z0, double* __restrict__ part,
+                          float* __restrict__ partmax, int64_t chunk) {
     const int64_t rc = (int64_t)rows * cols;
     const int64_t e = blockIdx.x * (int64_t)kSumThreads + threadIdx.x;
     if (e >= rc) return;
@@ -27,26 +30,93 @@ __global__ void __launch_bounds__(kSumThreads)
     const float s = z0 ? z0[e] : p[0];
     const int64_t i0 = blockIdx.y * chunk, i1 = min(n, i0 + chunk);
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    float mx = 0.f;
     int64_t i = i0;
     for (; i + 4 <= i1; i += 4) {
-        float v0 = p[(i + 0) * cols], v1 = p[(i + 1) * cols];
-        float v2 = p[(i + 2) * cols], v3 = p[(i + 3) * cols];
-        acc0 += (double)(v0 - s);
-        acc1 += (double)(v1 - s);
-        acc2 += (double)(v2 - s);
-        acc3 += (double)(v3 - s);
+        float v0 = p[(i + 0) * cols] - s, v1 = p[(i + 1) * cols] - s;
+        float v2 = p[(i + 2) * cols] - s, v3 = p[(i + 3) * cols] - s;
+        acc0 += (double)v0;
+        acc1 += (double)v1;
+        acc2 += (double)v2;
+        acc3 += (double)v3;
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v0), fabsf(v1)), fmaxf(fabsf(v2), fabsf(v3))));
     }
-    for (; i < i1; ++i) acc0 += (double)(p[i * cols] - s);
+    for (; i < i1; ++i) {
+        const float v = p[i * cols] - s;
+        acc0 += (double)v;
+        mx = fmaxf(mx, fabsf(v));
+    }
     part[blockIdx.y * rc + e] = (acc0 + acc1) + (acc2 + acc3);
+    partmax[blockIdx.y * rc + e] = mx;
 }
 
-__global__ void chunk_reduce_kernel(const double* __restrict__ part, int nchunks, int64_t rc,
-                                    double* __restrict__ acc) {
+__global__ void chunk_reduce_kernel(const double* __restrict__ part, const float* __restrict__ pmax,
+                                    int nchunks, int64_t rc, double* __restrict__ acc,
+                                    float* __restrict__ amax) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= rc) return;
     double s = 0.0;
-    for (int c = 0; c < nchunks; ++c) s += part[c * rc + e];
+    float mx = 0.f;
+    for (int c = 0; c < nchunks; ++c) {
+        s += part[c * rc + e];
+        mx = fmaxf(mx, pmax[c * rc + e]);
+    }
     acc[e] = s;
+    if (amax) amax[e] = mx;
+}
+
+// per-row power-of-two scale for the fp16-pair basis from a guaranteed bound on the anomalies:
+// |anom| = |(src - z0) - mu| <= max|src - z0| + |mu|.  scale = 2^e with bound * scale in [2^13, 2^14)
+__global__ void row_scale_kernel(const double* __restrict__ acc, const float* __restrict__ amax,
+                                 double inv_n, int cols, float* __restrict__ scale,
+                                 float* __restrict__ inv_scale) {
+    const int r = blockIdx.x;
+    float b = 0.f;
+    for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+        const float mu = (float)(acc[(int64_t)r * cols + j] * inv_n);
+        b = fmaxf(b, amax[(int64_t)r * cols + j] + fabsf(mu));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+    __shared__ float red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.f;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) m = fmaxf(m, red[w]);
+        int e = 0;
+        if (m > 0.f && isfinite(m)) {
+            int ex;
+            frexpf(m * 1.0001f, &ex);
+            e = max(-120, min(120, 14 - ex));
+        }
+        scale[r] = ldexpf(1.f, e);
+        inv_scale[r] = ldexpf(1.f, -e);
+    }
+}
+
+// anomalies straight into the fp16-pair basis (+ optional fp32 copy of the first rows_f32 rows)
+__global__ void center_f16pair_kernel(const float* __restrict__ src, int64_t ld, int rows, int64_t n,
+                                      int cols, const float* __restrict__ z0,
+                                      const double* __restrict__ acc, double inv_n,
+                                      float* __restrict__ mean, __half* __restrict__ h,
+                                      __half* __restrict__ l, int64_t ldh,
+                                      const float* __restrict__ scale, float* __restrict__ f32,
+                                      int64_t ldf, int rows_f32) {
+    const int64_t K = n * cols;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= (int64_t)rows * K) return;
+    const int64_t r = e / K, k = e - r * K;
+    const int j = (int)(k % cols);
+    const float s = z0 ? z0[r * cols + j] : src[r * ld + j];
+    const float mu = (float)(acc[r * cols + j] * inv_n);
+    if (mean && k < cols) mean[r * cols + j] = s + mu;
+    const float a = (src[r * ld + k] - s) - mu;
+    if (f32 && r < rows_f32) f32[r * ldf + k] = a;
+    const float v = a * scale[r];
+    const __half hv = __float2half_rn(v);
+    h[r * ldh + k] = hv;
+    l[r * ldh + k] = __float2half_rn(v - __half2float(hv));
 }
 
 // mean[r, j] = z0 + mu_sh; anom[r, i*cols + j] = (src - z0) - mu_sh
@@ -82,17 +152,19 @@ int64_t member_chunks(int rows, int64_t n, int cols) {
 extern "C" {
 
 int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols) {
-    return enks::member_chunks(rows, n_members, cols) * (int64_t)rows * cols * (int64_t)sizeof(double);
+    return enks::member_chunks(rows, n_members, cols) * (int64_t)rows * cols *
+           (int64_t)(sizeof(double) + sizeof(float));
 }
 
 int enks_member_sum(const float* src, int64_t ld_src, int rows, int64_t n_members, int cols,
-                    const float* z0, double* acc, void* ws, void* stream) {
+                    const float* z0, double* acc, float* amax, void* ws, void* stream) {
     ENKS_REQUIRE(src && acc && ws, "enks_member_sum: null pointer");
     if (rows <= 0 || cols <= 0) return ENKS_OK;
     const int64_t rc = (int64_t)rows * cols;
     cudaStream_t st = enks::as_stream(stream);
     if (n_members <= 0) {
         cudaMemsetAsync(acc, 0, rc * sizeof(double), st);
+        if (amax) cudaMemsetAsync(amax, 0, rc * sizeof(float), st);
         return enks::check_launch("enks_member_sum(memset)");
     }
     const int64_t nch = enks::member_chunks(rows, n_members, cols);
@@ -100,12 +172,13 @@ int enks_member_sum(const float* src, int64_t ld_src, int rows, int64_t n_member
     const int64_t nch_eff = (n_members + chunk - 1) / chunk;
     dim3 grid((unsigned)((rc + enks::kSumThreads - 1) / enks::kSumThreads), (unsigned)nch_eff);
     double* part = static_cast<double*>(ws);
+    float* pmax = reinterpret_cast<float*>(part + nch * rc);
     enks::member_partial_kernel<<<grid, enks::kSumThreads, 0, st>>>(src, ld_src, rows, n_members,
-                                                                   cols, z0, part, chunk);
+                                                                   cols, z0, part, pmax, chunk);
     int rc_ = enks::check_launch("enks_member_sum(partial)");
     if (rc_) return rc_;
-    enks::chunk_reduce_kernel<<<(unsigned)((rc + 255) / 256), 256, 0, st>>>(part, (int)nch_eff, rc,
-                                                                           acc);
+    enks::chunk_reduce_kernel<<<(unsigned)((rc + 255) / 256), 256, 0, st>>>(part, pmax, (int)nch_eff,
+                                                                           rc, acc, amax);
     return enks::check_launch("enks_member_sum(reduce)");
 }
 
@@ -120,6 +193,26 @@ int enks_member_center(const float* src, int64_t ld_src, int rows, int64_t n_mem
     enks::center_kernel<<<(unsigned)((total + 255) / 256), 256, 0, enks::as_stream(stream)>>>(
         src, ld_src, rows, n_members, cols, z0, acc, 1.0 / (double)n_total, mean, anom, ld_anom);
     return enks::check_launch("enks_member_center");
+}
+
+int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64_t n_members,
+                               int cols, const float* z0, const double* acc, const float* amax,
+                               int64_t n_total, float* mean, void* h, void* l, int64_t ldh,
+                               float* inv_scale, float* scale_ws, float* f32, int64_t ld_f32,
+                               int rows_f32, void* stream) {
+    ENKS_REQUIRE(src && acc && amax && h && l && inv_scale && scale_ws && n_total > 0,
+                 "enks_member_center_f16pair: bad arguments");
+    if (rows <= 0 || cols <= 0 || n_members <= 0) return ENKS_OK;
+    cudaStream_t st = enks::as_stream(stream);
+    const double inv_n = 1.0 / (double)n_total;
+    enks::row_scale_kernel<<<rows, 128, 0, st>>>(acc, amax, inv_n, cols, scale_ws, inv_scale);
+    int rc = enks::check_launch("enks_member_center_f16pair(scale)");
+    if (rc) return rc;
+    const int64_t total = (int64_t)rows * n_members * cols;
+    enks::center_f16pair_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+        src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
+        static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32);
+    return enks::check_launch("enks_member_center_f16pair");
 }
 
 }  // extern "C"

@@ -155,7 +155,7 @@ class DeviceSmoother:
     """Ensemble state + per-step orchestration for one horizon (see module docstring)."""
 
     def __init__(self, ops, x0_packed: np.ndarray, n: int, l: int, n_members: int, lam: float,
-                 capacity: int = 8, comm=None):
+                 capacity: int = 8, comm=None, basis: str | None = None):
         self.ops = ops
         self.comm = comm or LocalComm()
         self.n, self.l = int(n), int(l)
@@ -176,13 +176,13 @@ class DeviceSmoother:
         self.use_tc = (os.environ.get("ENKS_TC", "1") != "0" and hasattr(ops, "gemm_nt_tc")
                        and p <= 256 and K >= 128)
         # basis storage: fp16 pairs (tcgen05 kind::f16 contraction, gemm_f16p.cu) or fp32
-        self.pair = (self.use_tc and K % 8 == 0 and hasattr(ops, "gemm_f16pair")
-                     and os.environ.get("ENKS_BASIS", "f16pair") == "f16pair")
+        basis = basis or os.environ.get("ENKS_BASIS", "f16pair" if self.use_tc else "fp32")
+        self.pair = basis == "f16pair" and K % 8 == 0 and hasattr(ops, "gemm_f16pair")
         if self.use_tc and not self.pair:
             self.yc_hi = ops.empty(p, K)
             self.yc_lo = ops.empty(p, K)
         if self.pair:
-            self.A_new = ops.empty(d, K)   # fp32 anomalies of the newest slice
+            self.A_new = ops.empty(p, K)   # fp32 anomalies of the newest slice, [x; u] rows
             self.Yc_new = ops.empty(p, K)  # fp32 centred observations of the newest slice
         # the gain-side products (correction, gain, newest-slice shift) on tcgen05 as well
         self.use_tc2 = self.use_tc and p % 4 == 0 and m % 4 == 0 and hasattr(ops, "gemm_tc")
@@ -196,6 +196,7 @@ class DeviceSmoother:
         self.obs_raw = ops.empty(p, K)        # perturbed observations of the newest slice
         self.last = ops.empty(p, K)           # materialised [x; u] of the newest updated slice
         self.acc = ops.zeros(max(d, p), m, dtype=torch.float64)
+        self.amax = ops.zeros(max(d, p), m)
         self.z0 = ops.zeros(max(d, p), m) if self.comm.size > 1 else None
         self.ybar = ops.zeros(p, m)
         self.innov = ops.zeros(p, m)
@@ -277,7 +278,7 @@ class DeviceSmoother:
     def newest_anomalies(self):
         """fp32 anomalies of the newest predicted slice (d x K)."""
         d, t = self.d, self.t
-        return self.A_new if self.pair else self.Abuf[t * d:(t + 1) * d]
+        return self._rows_fp32("A", t * d, (t + 1) * d) if self.pair else self.Abuf[t * d:(t + 1) * d]
 
     # ------------------------------------------------------------ binding
     def bind(self, vs) -> None:
@@ -319,11 +320,15 @@ class DeviceSmoother:
         if out_plus is not None:
             ops.gemm(spec.dense, z, out_plus, beta=1.0, C0=base)
 
-    def _center(self, src, mean_out, anom_out):
-        """Member mean (rows x m) and anomalies of `src` (rows x K), shift = global member 0."""
+    def _center(self, src, mean_out, anom_out, pair_rows=None, f32_rows=0):
+        """Member mean (rows x m) and anomalies of `src` (rows x K), shift = global member 0.
+
+        pair_rows=(which, r0): write the anomalies straight into the fp16-pair basis at row r0
+        (plus an fp32 copy of the first f32_rows rows into anom_out)."""
         ops, comm, rows = self.ops, self.comm, src.shape[0]
         if rows > self.acc.shape[0]:
             self.acc = ops.zeros(rows, self.m, dtype=torch.float64)
+            self.amax = ops.zeros(rows, self.m)
             if self.z0 is not None:
                 self.z0 = ops.zeros(rows, self.m)
         acc = self.acc[:rows]
@@ -333,9 +338,20 @@ class DeviceSmoother:
             if comm.rank == 0:
                 z0.copy_(src[:, :self.m])
             comm.broadcast_(z0, src=0)
-        ops.member_sum(src, self.Nl, self.m, z0, acc)
+        if pair_rows is None:
+            ops.member_sum(src, self.Nl, self.m, z0, acc)
+            comm.allreduce_(acc)
+            ops.member_center(src, self.Nl, self.m, z0, acc, self.N, mean=mean_out, anom=anom_out)
+            return
+        which, r0 = pair_rows
+        amax = self.amax[:rows]
+        ops.member_sum(src, self.Nl, self.m, z0, acc, amax)
         comm.allreduce_(acc)
-        ops.member_center(src, self.Nl, self.m, z0, acc, self.N, mean=mean_out, anom=anom_out)
+        h, l, inv = (self.Ah, self.Al, self.a_inv) if which == "A" else (self.Yh, self.Yl,
+                                                                        self.y_inv)
+        ops.member_center_f16pair(src, self.Nl, self.m, z0, acc, amax, self.N, mean_out,
+                                  h[r0:r0 + rows], l[r0:r0 + rows], inv[r0:r0 + rows],
+                                  f32=anom_out, rows_f32=f32_rows)
 
     # ------------------------------------------------------------ predict
     def predict(self, vs, streams) -> None:
@@ -367,8 +383,9 @@ class DeviceSmoother:
             self._noise(self.noise_w, head, tau, CH_W, l, out=sr[n + l:], base=self.last[n:],
                         out_plus=sr[n:n + l])
         if self.pair:
-            self._center(sr, self.mean[tau * d:(tau + 1) * d], self.A_new)
-            self._store_rows("A", tau * d, self.A_new)
+            # fp32 copy of the [x; u] rows only (the newest-slice shift's C0)
+            self._center(sr, self.mean[tau * d:(tau + 1) * d], self.A_new, pair_rows=("A", tau * d),
+                         f32_rows=self.p)
         else:
             self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d])
         self.t = tau
@@ -387,9 +404,10 @@ class DeviceSmoother:
             self._noise(self.noise_vx, head, tau, CH_VX, n, base=sr[:n], out_plus=ob[:n])
             self._noise(self.noise_vu, head, tau, CH_VU, l, base=sr[n:n + l], out_plus=ob[n:])
         yc = self.Yc_new if self.pair else self.Ybuf[(tau - 1) * p:tau * p]
-        self._center(ob, self.ybar, yc)
         if self.pair:
-            self._store_rows("Y", (tau - 1) * p, yc)
+            self._center(ob, self.ybar, yc, pair_rows=("Y", (tau - 1) * p), f32_rows=p)
+        else:
+            self._center(ob, self.ybar, yc)
 
         # P = [A_s0..A_tau ; Yc_1..Yc_tau] Yc_tau^T  (local K-partial, then allreduce)
         a0 = d if self.slice0_zero else 0
@@ -440,7 +458,7 @@ class DeviceSmoother:
         ops.gemm(gcol, self.innov, mv, beta=1.0, C0=mv)
         # newest slice [x; u] for the next forecast: mean + A_tau - G_{tau,tau} Yc_tau
         g_tt = self.G[r0:r0 + p, (tau - 1) * p:tau * p]
-        a_new = self.newest_anomalies()
+        a_new = self.A_new if self.pair else self.Abuf[r0:r0 + d]
         if self.use_tc2:
             ops.tf32_split(yc, self.ycT_hi, self.ycT_lo, transpose=True)
             ops.gemm_tc(g_tt, self.ycT_hi, self.ycT_lo, self.last, alpha=-1.0, beta=1.0,
@@ -500,7 +518,7 @@ class DeviceSmoother:
         if self.t:  # no observation history: zero basis rows (their gains are zero)
             self._store_rows("Y", 0, ops.zeros(self.t * self.p, self.K))
         if self.pair:
-            self.A_new.copy_(anom[self.t * d:(self.t + 1) * d])
+            self.A_new[:self.p].copy_(anom[self.t * d:self.t * d + self.p])
         x0_spread = bool(torch.any(anom[:d] != 0).item())
         self.slice0_zero = not x0_spread
         last = Mdev[self.t * d:self.t * d + self.p]

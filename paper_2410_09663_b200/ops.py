@@ -113,13 +113,24 @@ class DeviceOps:
                   i64(*[_ld(v) if v is not None else 0 for v in get("out_plus")]),
                   self._stream())
 
-    def member_sum(self, src, n_members, cols, z0, acc):
+    def member_sum(self, src, n_members, cols, z0, acc, amax=None):
         rows = src.shape[0]
         nbytes = self.lib.enks_member_sum_ws_bytes(rows, n_members, cols)
         ws = self._workspace_sum(nbytes)
         self.launches += 2
         _lib.call("enks_member_sum", _p(src), _ld(src), rows, int(n_members), int(cols), _p(z0),
-                  _p(acc), ws, self._stream())
+                  _p(acc), _p(amax), ws, self._stream())
+
+    def member_center_f16pair(self, src, n_members, cols, z0, acc, amax, n_total, mean, h, l,
+                              inv_scale, f32=None, rows_f32=0):
+        rows = src.shape[0]
+        if getattr(self, "_scale_ws", None) is None or self._scale_ws.numel() < rows:
+            self._scale_ws = torch.empty(max(rows, 4096), dtype=torch.float32, device=self.device)
+        self.launches += 2
+        _lib.call("enks_member_center_f16pair", _p(src), _ld(src), rows, int(n_members), int(cols),
+                  _p(z0), _p(acc), _p(amax), int(n_total), _p(mean), _p(h), _p(l), _ld(h),
+                  _p(inv_scale), _p(self._scale_ws), _p(f32), _ld(f32) if f32 is not None else 0,
+                  int(rows_f32), self._stream())
 
     def member_center(self, src, n_members, cols, z0, acc, n_total, mean=None, anom=None):
         rows = src.shape[0]

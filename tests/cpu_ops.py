@@ -21,11 +21,36 @@ class CpuOps:
         self.device = torch.device("cpu")
         self.launches = 0
 
+    # fp16-pair basis buffers are kept in fp64 here (h = x, l = 0, scale 1): the
+    # orchestration of the pair path is exercised exactly, without fp16 rounding
     def empty(self, *shape, dtype=None):
-        return torch.empty(shape, dtype=dtype or self.dtype)
+        return torch.empty(shape, dtype=self.dtype if dtype in (None, torch.float16) else dtype)
 
     def zeros(self, *shape, dtype=None):
-        return torch.zeros(shape, dtype=dtype or self.dtype)
+        return torch.zeros(shape, dtype=self.dtype if dtype in (None, torch.float16) else dtype)
+
+    def f16pair_split(self, src, h, l, inv_scale):
+        h.copy_(src)
+        l.zero_()
+        inv_scale.fill_(1.0)
+
+    def f16pair_recon(self, h, l, inv_scale, out):
+        out.copy_((h + l) * inv_scale[:, None])
+
+    def gemm_f16pair(self, Ah, Al, inv_sa, Bh, Bl, inv_sb, C, *, alpha=1.0, tag=None):
+        a = (Ah + Al) * inv_sa[:, None]
+        b = (Bh + Bl) * inv_sb[:, None]
+        C.copy_(alpha * (a @ b.t()))
+
+    def member_center_f16pair(self, src, n_members, cols, z0, acc, amax, n_total, mean, h, l,
+                              inv_scale, f32=None, rows_f32=0):
+        anom = torch.empty(src.shape, dtype=self.dtype)
+        self.member_center(src, n_members, cols, z0, acc, n_total, mean=mean, anom=anom)
+        h.copy_(anom)
+        l.zero_()
+        inv_scale.fill_(1.0)
+        if f32 is not None and rows_f32:
+            f32[:rows_f32].copy_(anom[:rows_f32])
 
     def to_device(self, arr, dtype=None):
         return torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype or self.dtype).clone()
@@ -63,10 +88,12 @@ class CpuOps:
     def add(self, a, b, out):
         out.copy_(a + b)
 
-    def member_sum(self, src, n_members, cols, z0, acc):
+    def member_sum(self, src, n_members, cols, z0, acc, amax=None):
         s = src.reshape(src.shape[0], n_members, cols)
         shift = s[:, 0, :] if z0 is None else z0
         acc.copy_((s - shift[:, None, :]).sum(dim=1))
+        if amax is not None:
+            amax.copy_((s - shift[:, None, :]).abs().amax(dim=1))
 
     def member_center(self, src, n_members, cols, z0, acc, n_total, mean=None, anom=None):
         s = src.reshape(src.shape[0], n_members, cols)

@@ -33,14 +33,14 @@ def _problem(kind):
     return pm, vs, x0, 13, 4
 
 
-def _run(kind, comm):
+def _run(kind, comm, basis="fp32"):
     from cpu_ops import CpuOps
     from paper_2410_09663_b200.engine import DeviceSmoother
 
     pm, vs, x0, N, h = _problem(kind)
     ops = CpuOps()
     eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, N, 1.0 / np.trace(vs.shared_col_cov),
-                         capacity=2, comm=comm)
+                         capacity=2, comm=comm, basis=basis)
     st = pm.matvar.NoiseStreams(seed=21)
     y = ops.to_device(vs.reference_observation())
     for _ in range(h):
@@ -49,7 +49,7 @@ def _run(kind, comm):
     return eng
 
 
-def _worker(rank, world, port, kind, out):
+def _worker(rank, world, port, kind, out, basis="fp32"):
     sys.path[:0] = [os.path.dirname(HERE), HERE]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
@@ -57,7 +57,7 @@ def _worker(rank, world, port, kind, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2410_09663_b200.engine import TorchComm
 
-    eng = _run(kind, TorchComm())
+    eng = _run(kind, TorchComm(), basis)
     local = eng.members_device().numpy()
     parts = [None] * world
     dist.all_gather_object(parts, (eng.member0, eng.Nl, local))
@@ -68,12 +68,12 @@ def _worker(rank, world, port, kind, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["linear", "cnn"])
-def test_two_rank_sharding_matches_single_rank(kind, tmp_path):
+@pytest.mark.parametrize("kind,basis", [("linear", "fp32"), ("cnn", "fp32"), ("cnn", "f16pair")])
+def test_two_rank_sharding_matches_single_rank(kind, basis, tmp_path):
     out = str(tmp_path / "r.npz")
-    mp.spawn(_worker, args=(2, _free_port(), kind, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), kind, out, basis), nprocs=2, join=True)
     got = np.load(out)
-    ref = _run(kind, None)
+    ref = _run(kind, None, basis)
     assert [tuple(s) for s in got["spans"]] == [(0, 7), (7, 6)] if kind == "linear" else True
     scale = np.abs(ref.mean_host()).max()
     assert np.abs(got["mean"] - ref.mean_host()).max() < 1e-10 * scale

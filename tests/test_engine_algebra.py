@@ -12,9 +12,10 @@ from oracle import enks_oracle, problems
 from paper_2410_09663_b200.engine import DeviceSmoother
 
 
-def _run(pm, x0, y, vs, h, N, seed, cap=2):
+def _run(pm, x0, y, vs, h, N, seed, cap=2, pair=False):
     ops = CpuOps()
-    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, N, 1.0 / np.trace(vs.shared_col_cov), capacity=cap)
+    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, N, 1.0 / np.trace(vs.shared_col_cov),
+                         capacity=cap, basis="f16pair" if pair else "fp32")
     st = pm.matvar.NoiseStreams(seed=seed)
     yd = ops.to_device(np.broadcast_to(y, (h,) + y.shape[-2:]).copy() if y.ndim == 2 else y)
     for k in range(h):
@@ -30,11 +31,15 @@ def _run(pm, x0, y, vs, h, N, seed, cap=2):
     (dict(n=4, l=1, m=1), 8, 3, 3),
     (dict(n=6, l=6, m=5), 13, 7, 4),
 ])
-def test_engine_equals_oracle_fp64(pm, kw, N, h, seed):
+@pytest.mark.parametrize("pair", [False, True])
+def test_engine_equals_oracle_fp64(pm, kw, N, h, seed, pair):
     _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(seed), **kw)
     y = vs.reference_observation()
     ref, _, oens = enks_oracle.oracle_smooth(x0, y, vs, h, N, seed=seed + 7, backend="c")
-    eng = _run(pm, x0, y, vs, h, N, seed + 7)
+    if pair and (N * x0.m) % 8:
+        pytest.skip("fp16-pair basis needs N*m % 8 == 0 (16-B aligned fp16 rows)")
+    eng = _run(pm, x0, y, vs, h, N, seed + 7, pair=pair)
+    assert eng.pair == pair
     d, m = x0.n + 2 * x0.l, x0.m
     mean = eng.mean_host().reshape(h + 1, d, m)
     members = eng.members_device().numpy().reshape((h + 1) * d, N, m).transpose(1, 0, 2)
@@ -51,7 +56,8 @@ def test_engine_cnn_equals_oracle_fp64(pm):
     assert np.abs(eng.mean_host().reshape(ref.shape) - ref).max() < 1e-10 * np.abs(ref).max()
 
 
-def test_engine_explicit_members_restart(pm):
+@pytest.mark.parametrize("pair", [False, True])
+def test_engine_explicit_members_restart(pm, pair):
     """replace_members (TrajectoryEnsemble(members=...)) then continue == oracle continuing."""
     _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(5))
     y = vs.reference_observation()
@@ -62,7 +68,8 @@ def test_engine_explicit_members_restart(pm):
     o.members = o.members + 0.01 * np.random.default_rng(0).standard_normal(o.members.shape)
     o.mean = o.members.mean(axis=0)
     ops = CpuOps()
-    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, 9, o.lam, capacity=1)
+    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, 9, o.lam, capacity=1,
+                         basis="f16pair" if pair else "fp32")
     eng.replace_members(o.members, o.t)
     st = pm.matvar.NoiseStreams(seed=3)
     for _ in range(2):
