@@ -168,6 +168,7 @@ class DeviceSmoother:
         self.K = self.Nl * self.m
         self.lam = float(lam)
         self.t = 0
+        self.n_upd = 0  # observation blocks Yc_1..Yc_n_upd in the basis (gains exist for these)
         self.cap = 0
         self.slice0_zero = True  # all members start as identical copies (enks.py:120)
         self._bound = None
@@ -453,6 +454,7 @@ class DeviceSmoother:
                          alpha=-1.0, beta=1.0, C0=PA, tri=tri)
             ops.gemm(PA, self.sinv, gcol, alpha=scale)
         # mean_s += G_{tau,s} (y_ref - y_bar)   (enks.py:247-248 on the mean)
+        self.n_upd = tau
         ops.sub(y_ref_dev, self.ybar, self.innov)
         mv = self.mean[a0:rows_a]
         ops.gemm(gcol, self.innov, mv, beta=1.0, C0=mv)
@@ -476,8 +478,9 @@ class DeviceSmoother:
         a0 = d if self.slice0_zero else 0
         A = self._rows_fp32("A", 0, R)
         out[:a0] = A[:a0]
-        if t >= 1:
-            ops.gemm(self.G[a0:R, :t * p], self._rows_fp32("Y", 0, t * p), out[a0:], alpha=-1.0,
+        ku = min(self.n_upd, t) * p  # only observation blocks that have been drawn
+        if ku:
+            ops.gemm(self.G[a0:R, :ku], self._rows_fp32("Y", 0, ku), out[a0:], alpha=-1.0,
                      beta=1.0, C0=A[a0:R], tri=(d, p) if a0 else (0, 0))
         else:
             out[a0:] = A[a0:R]
@@ -515,7 +518,8 @@ class DeviceSmoother:
         anom = ops.empty(R, self.K)
         self._center(Mdev, self.mean[:R], anom)
         self._store_rows("A", 0, anom)
-        if self.t:  # no observation history: zero basis rows (their gains are zero)
+        self.n_upd = 0  # no observation history: the explicit members carry it
+        if self.t:  # zero observation rows: the cross moments read them (their gains are zero)
             self._store_rows("Y", 0, ops.zeros(self.t * self.p, self.K))
         if self.pair:
             self.A_new[:self.p].copy_(anom[self.t * d:self.t * d + self.p])
