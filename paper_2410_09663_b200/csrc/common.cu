@@ -32,18 +32,18 @@ __global__ void probe_kernel(int* out) {
 __global__ void sub_kernel(const float* __restrict__ a, int64_t lda, const float* __restrict__ b,
                            int64_t ldb, float* __restrict__ out, int64_t ldo, int64_t rows,
                            int64_t cols) {
-    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= rows * cols) return;
-    int64_t r = idx / cols, c = idx - r * cols;
-    out[r * ldo + c] = a[r * lda + c] - b[r * ldb + c];
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+        out[r * ldo + c] = a[r * lda + c] - b[r * ldb + c];
 }
 
 __global__ void add_kernel(const float* __restrict__ a, int64_t lda, const float* __restrict__ b,
                            int64_t ldb, float* out, int64_t ldo, int64_t rows, int64_t cols) {
-    int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= rows * cols) return;
-    int64_t r = idx / cols, c = idx - r * cols;
-    out[r * ldo + c] = a[r * lda + c] + b[r * ldb + c];
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+        out[r * ldo + c] = a[r * lda + c] + b[r * ldb + c];
 }
 
 }  // namespace enks
@@ -82,8 +82,8 @@ int enks_add(const float* a, int64_t lda, const float* b, int64_t ldb, float* ou
     ENKS_REQUIRE(a && b && out, "enks_add: null pointer");
     int64_t n = rows * cols;
     if (n == 0) return ENKS_OK;
-    enks::add_kernel<<<(unsigned)((n + 255) / 256), 256, 0, enks::as_stream(stream)>>>(
-        a, lda, b, ldb, out, ldo, rows, cols);
+    enks::add_kernel<<<dim3((unsigned)((cols + 255) / 256), (unsigned)(rows < 65535 ? rows : 65535)), 256, 0,
+                       enks::as_stream(stream)>>>(a, lda, b, ldb, out, ldo, rows, cols);
     return enks::check_launch("enks_add");
 }
 
@@ -92,10 +92,8 @@ int enks_sub(const float* a, int64_t lda, const float* b, int64_t ldb, float* ou
     ENKS_REQUIRE(a && b && out, "enks_sub: null pointer");
     int64_t n = rows * cols;
     if (n == 0) return ENKS_OK;
-    int threads = 256;
-    int64_t blocks = (n + threads - 1) / threads;
-    enks::sub_kernel<<<(unsigned)blocks, threads, 0, enks::as_stream(stream)>>>(a, lda, b, ldb, out,
-                                                                              ldo, rows, cols);
+    enks::sub_kernel<<<dim3((unsigned)((cols + 255) / 256), (unsigned)(rows < 65535 ? rows : 65535)), 256, 0,
+                       enks::as_stream(stream)>>>(a, lda, b, ldb, out, ldo, rows, cols);
     return enks::check_launch("enks_sub");
 }
 

@@ -261,10 +261,11 @@ __global__ void __launch_bounds__(256) f16pair_split_kernel(const float* __restr
 __global__ void f16pair_recon_kernel(const __half* __restrict__ h, const __half* __restrict__ l,
                                      int64_t ldi, const float* __restrict__ inv_scale, int64_t rows,
                                      int64_t K, float* __restrict__ out, int64_t ldo) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= rows * K) return;
-    const int64_t r = e / K, k = e - r * K;
-    out[r * ldo + k] = (__half2float(h[r * ldi + k]) + __half2float(l[r * ldi + k])) * inv_scale[r];
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+        out[r * ldo + k] =
+            (__half2float(h[r * ldi + k]) + __half2float(l[r * ldi + k])) * inv_scale[r];
 }
 
 __global__ void f16p_sum_splits(const float* __restrict__ ws, int split, int64_t M, int64_t N,
@@ -364,7 +365,8 @@ int enks_f16pair_recon(const void* h, const void* l, int64_t ldi, const float* i
     ENKS_REQUIRE(h && l && inv_scale && out, "enks_f16pair_recon: null pointer");
     const int64_t total = rows * K;
     if (total <= 0) return ENKS_OK;
-    enks::f16pair_recon_kernel<<<(unsigned)((total + 255) / 256), 256, 0, enks::as_stream(stream)>>>(
+    const dim3 grid((unsigned)((K + 255) / 256), (unsigned)(rows < 65535 ? rows : 65535));
+    enks::f16pair_recon_kernel<<<grid, 256, 0, enks::as_stream(stream)>>>(
         static_cast<const __half*>(h), static_cast<const __half*>(l), ldi, inv_scale, rows, K, out,
         ldo);
     return enks::check_launch("enks_f16pair_recon");

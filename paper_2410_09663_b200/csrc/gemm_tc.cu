@@ -349,13 +349,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void tf32_split_kernel(const float* __restrict__ src, int64_t ld, int64_t rows,
                                   int64_t cols, float* __restrict__ hi, float* __restrict__ lo,
                                   int64_t ldo) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= rows * cols) return;
-    const int64_t r = e / cols, c = e - r * cols;
-    const float v = src[r * ld + c];
-    const float h = ptx::tf32_round(v);
-    hi[r * ldo + c] = h;
-    lo[r * ldo + c] = v - h;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const float v = src[r * ld + c];
+        const float h = ptx::tf32_round(v);
+        hi[r * ldo + c] = h;
+        lo[r * ldo + c] = v - h;
+    }
 }
 
 // hi/lo split with transpose: src (rows x cols, ld) -> hi, lo (cols x rows, ldo); 32x32 smem tiles
@@ -609,8 +610,8 @@ int tf32_split(const float* src, int64_t ld, int64_t rows, int64_t cols, float* 
                int64_t ldo, cudaStream_t st) {
     const int64_t total = rows * cols;
     if (total == 0) return ENKS_OK;
-    tf32_split_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(src, ld, rows, cols, hi, lo,
-                                                                      ldo);
+    tf32_split_kernel<<<dim3((unsigned)((cols + 255) / 256), (unsigned)(rows < 65535 ? rows : 65535)), 256, 0, st>>>(
+        src, ld, rows, cols, hi, lo, ldo);
     return check_launch("enks_tf32_split");
 }
 

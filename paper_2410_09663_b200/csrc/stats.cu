@@ -104,10 +104,10 @@ __global__ void center_f16pair_kernel(const float* __restrict__ src, int64_t ld,
                                       const float* __restrict__ scale, float* __restrict__ f32,
                                       int64_t ldf, int rows_f32) {
     const int64_t K = n * cols;
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= (int64_t)rows * K) return;
-    const int64_t r = e / K, k = e - r * K;
-    const int j = (int)(k % cols);
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = blockIdx.y;
+    if (k >= K) return;
+    const int j = (int)((uint32_t)k % (uint32_t)cols);
     const float s = z0 ? z0[r * cols + j] : src[r * ld + j];
     const float mu = (float)(acc[r * cols + j] * inv_n);
     if (mean && k < cols) mean[r * cols + j] = s + mu;
@@ -125,10 +125,10 @@ __global__ void center_kernel(const float* __restrict__ src, int64_t ld, int row
                               const double* __restrict__ acc, double inv_n, float* __restrict__ mean,
                               float* anom, int64_t lda) {
     const int64_t K = n * cols;
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= (int64_t)rows * K) return;
-    const int64_t r = e / K, k = e - r * K;
-    const int j = (int)(k % cols);
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r = blockIdx.y;
+    if (k >= K) return;
+    const int j = (int)((uint32_t)k % (uint32_t)cols);
     const float s = z0 ? z0[r * cols + j] : src[r * ld + j];
     const float mu = (float)(acc[r * cols + j] * inv_n);
     if (mean && k < cols) mean[r * cols + j] = s + mu;
@@ -186,11 +186,13 @@ int enks_member_center(const float* src, int64_t ld_src, int rows, int64_t n_mem
                        const float* z0, const double* acc, int64_t n_total, float* mean,
                        float* anom, int64_t ld_anom, void* stream) {
     ENKS_REQUIRE(src && acc && n_total > 0, "enks_member_center: bad arguments");
+    ENKS_REQUIRE(rows <= 65535, "enks_member_center: rows > 65535");
     ENKS_REQUIRE(!(anom == src && z0 == nullptr),
                  "enks_member_center: in-place centring needs an explicit z0");
     if (rows <= 0 || cols <= 0 || n_members <= 0) return ENKS_OK;
-    const int64_t total = (int64_t)rows * n_members * cols;
-    enks::center_kernel<<<(unsigned)((total + 255) / 256), 256, 0, enks::as_stream(stream)>>>(
+    const int64_t K = n_members * cols;
+    enks::center_kernel<<<dim3((unsigned)((K + 255) / 256), (unsigned)rows), 256, 0,
+                          enks::as_stream(stream)>>>(
         src, ld_src, rows, n_members, cols, z0, acc, 1.0 / (double)n_total, mean, anom, ld_anom);
     return enks::check_launch("enks_member_center");
 }
@@ -202,14 +204,15 @@ int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64
                                int rows_f32, void* stream) {
     ENKS_REQUIRE(src && acc && amax && h && l && inv_scale && scale_ws && n_total > 0,
                  "enks_member_center_f16pair: bad arguments");
+    ENKS_REQUIRE(rows <= 65535, "enks_member_center_f16pair: rows > 65535");
     if (rows <= 0 || cols <= 0 || n_members <= 0) return ENKS_OK;
     cudaStream_t st = enks::as_stream(stream);
     const double inv_n = 1.0 / (double)n_total;
     enks::row_scale_kernel<<<rows, 128, 0, st>>>(acc, amax, inv_n, cols, scale_ws, inv_scale);
     int rc = enks::check_launch("enks_member_center_f16pair(scale)");
     if (rc) return rc;
-    const int64_t total = (int64_t)rows * n_members * cols;
-    enks::center_f16pair_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+    const int64_t K = n_members * cols;
+    enks::center_f16pair_kernel<<<dim3((unsigned)((K + 255) / 256), (unsigned)rows), 256, 0, st>>>(
         src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
         static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32);
     return enks::check_launch("enks_member_center_f16pair");
