@@ -208,6 +208,24 @@ int enks_cnn_forward(int n_layers, const int* widths, const float* weights, cons
                      float* out, int64_t ldo, int rows, int cols, int64_t n_members,
                      void* stream);
 
+/*
+ * Burgers forecast: cfg.substeps forward-Euler steps of the
+ * 2-D viscous Burgers solver for every member, force held constant
+ * (replaces BurgersDynamics.step, dynamics.py:264-270 -> _step_packed 183-216,
+ * called at enks.py:168).  x/out: (2*grid_n x n_members*grid_n) member-column
+ * layout, phi_x rows above phi_y rows; u: u_rows x K with u_rows = 2 (boundary
+ * force on rows grid_n-1 / 2*grid_n-1) or 2*grid_n (pointwise source), 0 = none.
+ * CFL (dynamics.py:168-180): max|phi| over every substep input is folded into
+ * *vmax (device float, caller zeroes it) and a non-finite entry sets bit 0 of
+ * *flags; the caller raises CflError from them.  ws: enks_burgers_ws_bytes bytes
+ * (0 when the member field fits in shared memory).
+ */
+int64_t enks_burgers_ws_bytes(int grid_n, int n_members, int substeps);
+int enks_burgers_forward(const float* x, int64_t ldx, const float* u, int64_t ldu, int u_rows,
+                         float* out, int64_t ldo, int grid_n, int n_members, int substeps,
+                         double nu, double dt, double dx, float* vmax, int* flags, void* ws,
+                         void* stream);
+
 /* Small elementwise helpers. */
 /* out[r, j] = a[r, j] + b[r, j] (the "u + w + v" observation of enks.py:168, 200). */
 int enks_add(const float* a, int64_t lda, const float* b, int64_t ldb, float* out, int64_t ldo,

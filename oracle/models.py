@@ -7,6 +7,11 @@
 * ``OracleCNN``    MatrixDynamics wrapper around ``cnn_step`` (plugs into the
                    oracle smoother and into the reference's own smooth_horizon).
 * ``linear_step``  reference dynamics.py:53-63.
+* ``burgers_step`` reference dynamics.py:156-216 (_neighbor_slices, _cfl_check,
+                   _step_packed), restated with explicit padded-array shifts; one
+                   call = ``substeps`` solver steps (BurgersDynamics.step 264-270).
+                   Pinned bit-for-bit against the reference (tests/golden/burgers_*.npz).
+* ``OracleBurgers`` MatrixDynamics wrapper around ``burgers_step``.
 """
 from __future__ import annotations
 
@@ -59,3 +64,61 @@ class OracleCNN:
 
 def linear_step(x, u, a, b):
     return np.asarray(a, float) @ np.asarray(x, float) + np.asarray(b, float) @ np.asarray(u, float)
+
+
+class OracleCflError(RuntimeError):
+    pass
+
+
+def burgers_step(packed, force, grid_n: int, nu: float, dt: float, mode: str = "boundary",
+                 substeps: int = 1):
+    """fp64 Burgers forecast on (..., 2g, g) packed fields (dynamics.py:183-216, 264-270).
+
+    Edge-copy ghost cells (dynamics.py:156-165): pad by one with the edge value, read the
+    four shifted interior windows.  Returns (out, max|phi| over every substep input)."""
+    g = grid_n
+    dx = 1.0 / (g - 1)
+    out = np.asarray(packed, dtype=float)
+    vmax_all = 0.0
+    for _ in range(substeps):
+        vx, vy = out[..., :g, :], out[..., g:, :]
+        vmax = max(float(np.max(np.abs(vx))), float(np.max(np.abs(vy))))
+        if not np.isfinite(vmax):
+            raise OracleCflError("non-finite field")
+        if nu * dt / dx ** 2 > 0.25 or vmax * dt / dx > 1.0:
+            raise OracleCflError("CFL violated")
+        vmax_all = max(vmax_all, vmax)
+        new = []
+        for q in (vx, vy):
+            pad = [(0, 0)] * (q.ndim - 2) + [(1, 1), (1, 1)]
+            qp = np.pad(q, pad, mode="edge")
+            up, down = qp[..., :-2, 1:-1], qp[..., 2:, 1:-1]
+            left, right = qp[..., 1:-1, :-2], qp[..., 1:-1, 2:]
+            lap = (up + down + left + right - 4.0 * q) / dx ** 2
+            ddx = np.where(vx > 0, q - left, right - q) / dx
+            ddy = np.where(vy > 0, q - up, down - q) / dx
+            new.append(q + dt * (nu * lap - vx * ddx - vy * ddy))
+        out = np.concatenate(new, axis=-2)
+        if force is not None:
+            f = np.asarray(force, dtype=float)
+            if mode == "pointwise":
+                out = out + dt * f
+            else:
+                out[..., g - 1, :] += dt * f[..., 0, :]
+                out[..., 2 * g - 1, :] += dt * f[..., 1, :]
+    return out, vmax_all
+
+
+class OracleBurgers:
+    """fp64 MatrixDynamics for the Burgers model, from a BurgersDynamics-like spec."""
+
+    def __init__(self, spec):
+        cfg = spec.cfg
+        self.g, self.nu, self.dt = int(cfg.grid_n), float(cfg.nu), float(cfg.dt)
+        self.mode, self.substeps = cfg.control_mode, int(cfg.substeps)
+        self.state_rows = spec.state_rows
+        self.state_cols = spec.state_cols
+        self.input_rows = spec.input_rows
+
+    def step(self, x, u):
+        return burgers_step(x, u, self.g, self.nu, self.dt, self.mode, self.substeps)[0]

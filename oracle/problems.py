@@ -82,6 +82,24 @@ def make_cnn_problem(mods, config: str = "C1", seed: int = 0, size=None, n_membe
                            y_ref=vs.reference_observation())
 
 
+def make_burgers_problem(mods, mode: str = "boundary", grid_n: int = 32, n_members: int = 100,
+                         horizon: int = 5, seed: int = 0, substeps: int = 1, model=None):
+    """C1a: reference Burgers FD, grid 32 -> X 64 x 32, boundary (l = 2) or
+    pointwise (l = 64) control, N = 100, H = 5, x0 = make_initial_field(cfg, seed), u0 = dU0 = 0,
+    identity weights, x_ref = 1, u_ref = 0."""
+    cfg = mods.dynamics.BurgersConfig(grid_n=grid_n, control_mode=mode, substeps=substeps)
+    if model is None:
+        model = mods.dynamics.BurgersDynamics(cfg)
+    n, m, l = 2 * grid_n, grid_n, model.input_rows
+    weights = mods.virtualsys.MpcWeights(r=np.eye(n), q_u=np.eye(l), q_du=np.eye(l),
+                                         x_ref=np.ones((n, m)), u_ref=np.zeros((l, m)), scale=1.0)
+    vs = mods.virtualsys.build_virtual_system(model, weights)
+    x = mods.dynamics.make_initial_field(cfg, seed).packed
+    x0 = mods.virtualsys.AugmentedState(x, np.zeros((l, m)), np.zeros((l, m)))
+    return SimpleNamespace(model=model, vs=vs, x0=x0, n=n, l=l, m=m, N=n_members, H=horizon,
+                           cfg=cfg, y_ref=vs.reference_observation())
+
+
 def product_modules():
     import paper_2410_09663_b200 as pkg
 

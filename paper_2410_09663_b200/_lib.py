@@ -27,6 +27,7 @@ class NativeError(RuntimeError):
 _c_i64 = ctypes.c_int64
 _c_int = ctypes.c_int
 _c_f = ctypes.c_float
+_c_d = ctypes.c_double
 _vp = ctypes.c_void_p
 _u32p = ctypes.POINTER(ctypes.c_uint32)
 _ip = ctypes.POINTER(ctypes.c_int)
@@ -68,6 +69,9 @@ _SIGS = {
     "enks_cnn_max_width": (_c_int, []),
     "enks_cnn_forward": (_c_int, [_c_int, _ip, _vp, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _vp,
                                   _c_i64, _c_int, _c_int, _c_i64, _vp]),
+    "enks_burgers_ws_bytes": (_c_i64, [_c_int, _c_int, _c_int]),
+    "enks_burgers_forward": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int,
+                                      _c_int, _c_int, _c_d, _c_d, _c_d, _vp, _vp, _vp, _vp]),
     "enks_add": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _c_i64, _c_i64, _vp]),
     "enks_sub": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _c_i64, _c_i64, _vp]),
 }

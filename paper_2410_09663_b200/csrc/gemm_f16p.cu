@@ -55,6 +55,7 @@ struct P16 {
     int splits;
     int stages;
     int chain;
+    int products;  // 3: lh + hl + hh;  2: hl + hh (A's low plane not read)
 };
 
 __device__ __forceinline__ uint64_t desc_sw64(const void* smem) {
@@ -144,10 +145,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < n_chunks; ++i) {
                 const int s = i % S;
                 ptx::mbar_wait(&empty[s], (uint32_t)(((i / S) & 1) ^ 1));
-                ptx::mbar_arrive_expect_tx(&full[s], 2 * L::kA + 2 * L::kB);
+                ptx::mbar_arrive_expect_tx(&full[s], (p.products == 3 ? 2 : 1) * L::kA + 2 * L::kB);
                 const int kc = (c_lo + i) * KC;
                 ptx::tma_load_2d(&tAh, &full[s], ah(s), kc, (int32_t)row0);
-                ptx::tma_load_2d(&tAl, &full[s], al(s), kc, (int32_t)row0);
+                if (p.products == 3) ptx::tma_load_2d(&tAl, &full[s], al(s), kc, (int32_t)row0);
                 ptx::tma_load_2d(&tBh, &full[s], bh(s), kc, (int32_t)col0);
                 ptx::tma_load_2d(&tBl, &full[s], bl(s), kc, (int32_t)col0);
             }
@@ -171,8 +172,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < KC / 16; ++k) {
                     const uint64_t dah = desc_sw64(ah(s) + 32 * k), dal = desc_sw64(al(s) + 32 * k);
                     const uint64_t dbh = desc_sw64(bh(s) + 32 * k), dbl = desc_sw64(bl(s) + 32 * k);
-                    mma_f16_ss(d, dal, dbh, idesc, (first && k == 0) ? 0u : 1u);
-                    mma_f16_ss(d, dah, dbl, idesc, 1u);
+                    if (p.products == 3) {
+                        mma_f16_ss(d, dal, dbh, idesc, (first && k == 0) ? 0u : 1u);
+                        mma_f16_ss(d, dah, dbl, idesc, 1u);
+                    } else {
+                        mma_f16_ss(d, dah, dbl, idesc, (first && k == 0) ? 0u : 1u);
+                    }
                     mma_f16_ss(d, dah, dbh, idesc, 1u);
                 }
                 ptx::mma_commit(&empty[s]);
@@ -220,6 +225,178 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 2) ptx::tmem_dealloc(tmem, kTmemCols);
+}
+
+
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2) for N in (128, 256]: a cluster of two CTAs computes a
+// 256 x 256 tile with one tcgen05.mma.cta_group::2 per product.  Each CTA stages its own
+// 128 A rows and HALF of the B rows (128), so per unit of MMA work every SM moves and reads
+// 2/3 of the shared-memory bytes of the single-CTA 128 x 256 kernel (whose three products
+// per K step re-read the full B tile from smem and were shared-memory-bandwidth bound).
+// The leader CTA (rank 0) issues the MMAs; its full[] barriers count both CTAs' TMA bytes;
+// MMA completion is multicast to both CTAs' empty[] / tfull[] barriers; each CTA drains
+// its own TMEM (its 128 rows x 256 columns) and arrives on the leader's tempty[].
+struct LP {
+    static constexpr int kA = BM * KC * 2;       // 8 KB per plane (128 rows)
+    static constexpr int kB = 128 * KC * 2;      // 8 KB per plane (this CTA's 128 B rows)
+    static constexpr int kStage = 2 * kA + 2 * kB;
+    static constexpr int kCols = 256;            // accumulator columns per slot
+};
+
+__device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    f16p_gemm_pair_kernel(const __grid_constant__ CUtensorMap tAh,
+                          const __grid_constant__ CUtensorMap tAl,
+                          const __grid_constant__ CUtensorMap tBh,
+                          const __grid_constant__ CUtensorMap tBl, const P16 p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int S = p.stages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * LP::kStage);
+    uint64_t* full = bars;            // leader's are used
+    uint64_t* empty = bars + S;       // both
+    uint64_t* tfull = bars + 2 * S;   // both
+    uint64_t* tempty = bars + 2 * S + 2;  // leader's are used
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+
+    const uint32_t rank = ptx::cluster_ctarank();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = (int64_t)blockIdx.x * BM;
+    const int split = blockIdx.z;
+    const int total_chunks = (int)((p.K + KC - 1) / KC);
+    const int cps = (total_chunks + p.splits - 1) / p.splits;
+    const int c_lo = min(total_chunks, split * cps);
+    const int n_chunks = min(total_chunks, c_lo + cps) - c_lo;
+    const int chain = p.chain;
+    const int n_groups = (n_chunks + chain - 1) / chain;
+    constexpr uint32_t kTmemCols = 2 * LP::kCols;
+
+    auto ah = [&](int s) { return smem + (size_t)s * LP::kStage; };
+    auto al = [&](int s) { return smem + (size_t)s * LP::kStage + LP::kA; };
+    auto bh = [&](int s) { return smem + (size_t)s * LP::kStage + 2 * LP::kA; };
+    auto bl = [&](int s) { return smem + (size_t)s * LP::kStage + 2 * LP::kA + LP::kB; };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int q = 0; q < 2; ++q) {
+            ptx::mbar_init(&tfull[q], 1);
+            ptx::mbar_init(&tempty[q], 2 * 8);  // 8 epilogue warps in each CTA of the pair
+        }
+        ptx::fence_barrier_init();
+        ptx::tma_prefetch_desc(&tAh);
+        ptx::tma_prefetch_desc(&tAl);
+        ptx::tma_prefetch_desc(&tBh);
+        ptx::tma_prefetch_desc(&tBl);
+    }
+    if (warp == 2) ptx::tmem_alloc_pair(tmem_slot, kTmemCols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const int32_t brow = (int32_t)(rank * 128);
+            for (int i = 0; i < n_chunks; ++i) {
+                const int s = i % S;
+                ptx::mbar_wait_bounded(&empty[s], (uint32_t)(((i / S) & 1) ^ 1));
+                if (rank == 0)
+                    ptx::mbar_arrive_expect_tx(&full[s], 2 * (p.products == 3 ? LP::kStage
+                                                                             : LP::kStage - LP::kA));
+                const int kc = (c_lo + i) * KC;
+                ptx::tma_load_2d_pair(&tAh, &full[s], ah(s), kc, (int32_t)row0);
+                if (p.products == 3) ptx::tma_load_2d_pair(&tAl, &full[s], al(s), kc, (int32_t)row0);
+                ptx::tma_load_2d_pair(&tBh, &full[s], bh(s), kc, brow);
+                ptx::tma_load_2d_pair(&tBl, &full[s], bl(s), kc, brow);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = idesc_f16(2 * BM, 256);
+            for (int i = 0; i < n_chunks; ++i) {
+                const int s = i % S;
+                const int g = i / chain, slot = g & 1;
+                const bool first = (i % chain) == 0;
+                const bool last = (i % chain) == chain - 1 || i == n_chunks - 1;
+                if (first) {
+                    ptx::mbar_wait_bounded(&tempty[slot], (uint32_t)(((g >> 1) & 1) ^ 1));
+                    ptx::tc_fence_after();
+                }
+                ptx::mbar_wait_bounded(&full[s], (uint32_t)((i / S) & 1));
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(slot * LP::kCols);
+#pragma unroll
+                for (int k = 0; k < KC / 16; ++k) {
+                    const uint64_t dah = desc_sw64(ah(s) + 32 * k), dal = desc_sw64(al(s) + 32 * k);
+                    const uint64_t dbh = desc_sw64(bh(s) + 32 * k), dbl = desc_sw64(bl(s) + 32 * k);
+                    if (p.products == 3) {
+                        mma_f16_pair(d, dal, dbh, idesc, (first && k == 0) ? 0u : 1u);
+                        mma_f16_pair(d, dah, dbl, idesc, 1u);
+                    } else {
+                        mma_f16_pair(d, dah, dbl, idesc, (first && k == 0) ? 0u : 1u);
+                    }
+                    mma_f16_pair(d, dah, dbh, idesc, 1u);
+                }
+                ptx::mma_commit_pair(&empty[s], 0x3);
+                if (last) ptx::mma_commit_pair(&tfull[slot], 0x3);
+            }
+        }
+    } else if (warp >= 4) {
+        const int wg = (warp - 4) >> 2;
+        constexpr int kCols = 128;  // per warpgroup
+        const int erow = ((warp & 3) << 5) + lane;
+        const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        float acc[kCols];
+#pragma unroll
+        for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
+        for (int g = 0; g < n_groups; ++g) {
+            const int slot = g & 1;
+            ptx::mbar_wait_bounded(&tfull[slot], (uint32_t)((g >> 1) & 1));
+            ptx::tc_fence_after();
+            const uint32_t base = tmem + lane_base + (uint32_t)(slot * LP::kCols + wg * kCols);
+#pragma unroll
+            for (int c0 = 0; c0 < kCols; c0 += 32) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(base + c0, v);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[c0 + j] += __uint_as_float(v[j]);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(&tempty[slot], 0);
+        }
+        const int64_t r = row0 + erow;
+        const int64_t c_first = (int64_t)wg * kCols;
+        if (r < p.M && c_first < p.N) {
+            const float sa = p.alpha * p.inv_sa[r];
+            float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + c_first;
+            const int ncol = (int)min((int64_t)kCols, p.N - c_first);
+#pragma unroll
+            for (int j = 0; j < kCols; ++j)
+                if (j < ncol) orow[j] = acc[j] * sa * p.inv_sb[c_first + j];
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    if (warp == 2) ptx::tmem_dealloc_pair(tmem, kTmemCols);
 }
 
 // one block per row: scale = 2^e with max|x| * scale in [2^13, 2^14); h = fp16(xs), l = fp16(xs - h)
@@ -329,6 +506,53 @@ int launch16(const CUtensorMap* maps, P16 p, dim3 grid, cudaStream_t st) {
     return check_launch("enks_gemm_f16pair");
 }
 
+int launch_pair(const CUtensorMap* maps, P16 p, dim3 grid, cudaStream_t st) {
+    int stages = kSmemBudget / LP::kStage;
+    if (stages > 8) stages = 8;
+    p.stages = stages;
+    const size_t smem = (size_t)stages * LP::kStage + 1024 + 512;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(f16p_gemm_pair_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) {
+            set_error("f16p pair gemm: smem attribute: %s", cudaGetErrorString(e));
+            return ENKS_E_CUDA;
+        }
+        configured = true;
+    }
+    f16p_gemm_pair_kernel<<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+    return check_launch("enks_gemm_f16pair(pair)");
+}
+
+// pairs of CTAs over 74 pair slots
+int choose_split_pairs(int pairs, int64_t chunks) {
+    int best = 1;
+    double best_eff = 0.0;
+    const int slots = kNumSMs / 2;
+    for (int s = 1; s <= 64; ++s) {
+        if (chunks / s < 8 && s > 1) break;
+        const int units = pairs * s;
+        const int waves = (units + slots - 1) / slots;
+        const double eff = (double)units / (double)(waves * slots);
+        if (eff > best_eff + 0.03) {
+            best_eff = eff;
+            best = s;
+        }
+        if (eff > 0.95) break;
+    }
+    return best;
+}
+
+bool use_pair(int64_t N) {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("ENKS_F16P_PAIR");
+        mode = e ? atoi(e) : 1;
+    }
+    return mode != 0 && N > 128;
+}
+
 int choose_split16(int tiles, int64_t chunks) {
     int best = 1;
     double best_eff = 0.0;
@@ -375,7 +599,9 @@ int enks_f16pair_recon(const void* h, const void* l, int64_t ldi, const float* i
 int64_t enks_gemm_f16pair_ws_bytes(int64_t M, int64_t N, int64_t K) {
     const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
     const int tiles = (int)((M + enks::BM - 1) / enks::BM) * (int)((N + BN - 1) / BN);
-    const int split = enks::choose_split16(tiles, (K + enks::KC - 1) / enks::KC);
+    const int64_t chunks = (K + enks::KC - 1) / enks::KC;
+    const int split = enks::use_pair(N) ? enks::choose_split_pairs((tiles + 1) / 2, chunks)
+                                        : enks::choose_split16(tiles, chunks);
     return split > 1 ? (int64_t)split * M * N * (int64_t)sizeof(float) : 0;
 }
 
@@ -390,12 +616,15 @@ int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* 
     const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
     CUtensorMap maps[4];
     if (!map16(&maps[0], Ah, M, K, lda, BM) || !map16(&maps[1], Al, M, K, lda, BM) ||
-        !map16(&maps[2], Bh, N, K, ldb, BN) || !map16(&maps[3], Bl, N, K, ldb, BN)) {
+        !map16(&maps[2], Bh, N, K, ldb, use_pair(N) ? 128 : BN) ||
+        !map16(&maps[3], Bl, N, K, ldb, use_pair(N) ? 128 : BN)) {
         set_error("enks_gemm_f16pair: cuTensorMapEncodeTiled failed (alignment?)");
         return ENKS_E_UNSUPPORTED;
     }
     const int m_tiles = (int)((M + BM - 1) / BM);
-    const int split = choose_split16(m_tiles, (K + KC - 1) / KC);
+    const bool pair = use_pair(N);
+    const int split = pair ? choose_split_pairs((m_tiles + 1) / 2, (K + KC - 1) / KC)
+                           : choose_split16(m_tiles, (K + KC - 1) / KC);
     ENKS_REQUIRE(split == 1 || ws, "enks_gemm_f16pair: split-K needs workspace");
     P16 p;
     p.M = M; p.N = N; p.K = K;
@@ -405,6 +634,8 @@ int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* 
     p.splits = split;
     const char* ch = getenv("ENKS_TC_CHAIN");
     p.chain = ch ? atoi(ch) : 8;
+    const char* pr = getenv("ENKS_F16P_PRODUCTS");
+    p.products = (pr && atoi(pr) == 2) ? 2 : 3;
     if (p.chain < 1) p.chain = 1;
     const bool direct = split == 1;
     p.out = direct ? C : static_cast<float*>(ws);
@@ -413,7 +644,10 @@ int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* 
     dim3 grid((unsigned)m_tiles, 1, (unsigned)split);
     cudaStream_t st = as_stream(stream);
     int rc;
-    switch (BN) {
+    if (pair) {
+        grid.x = (unsigned)((m_tiles + 1) & ~1);
+        rc = launch_pair(maps, p, grid, st);
+    } else switch (BN) {
         case 32: rc = launch16<32>(maps, p, grid, st); break;
         case 64: rc = launch16<64>(maps, p, grid, st); break;
         case 128: rc = launch16<128>(maps, p, grid, st); break;

@@ -19,6 +19,7 @@ namespace {
 
 constexpr int kWarps = 4;          // warps (streams) per block
 constexpr int kBufWords = 128;     // 32 Philox blocks per refill
+constexpr int kMaxRowCols = 512;   // row-staged output path: cols % 4 == 0, 32 <= cols <= 512
 
 __device__ const uint64_t g_ki[256] = NPY_ZIG_KI_DOUBLE_INIT;
 __device__ const uint64_t g_wi[256] = NPY_ZIG_WI_DOUBLE_INIT;
@@ -121,8 +122,14 @@ __device__ __forceinline__ double u64_to_unit(uint64_t r) {
     return (double)(r >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// RB (row-staged): the normals of a row are collected in shared memory (two row slots) and
+// written as float4 once the row is complete, with the row's `base` values and diagonal
+// scale prefetched a row ahead -- the sequential stream never waits on a global load.
+// Otherwise each batch of accepted normals is stored straight away (any cols / alignment).
+template <bool RB>
 __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
     const Job& a = args.job[blockIdx.y];
+    __shared__ __align__(16) float s_row[RB ? kWarps : 1][RB ? 2 * kMaxRowCols : 1];
     __shared__ uint64_t s_ki[256];
     __shared__ double s_wi[256];
     __shared__ uint64_t s_buf[kWarps][kBufWords];
@@ -165,6 +172,67 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
         if (a.out) a.out[r * a.ld_out + col0 + j] = f;
         if (a.out_plus) a.out_plus[r * a.ld_plus + col0 + j] = a.base[r * a.ld_base + col0 + j] + f;
     };
+    // ---- row-staged output (RB)
+    double dcur = 0.0, dnext = 0.0;
+    float4 bpre[kMaxRowCols / 128];
+    auto load_diag = [&](int r) { return (a.diag && r < a.rows) ? a.diag[r] : 1.0; };
+    auto prefetch_base = [&](int r) {
+        if constexpr (RB) {
+            if (!a.out_plus || r >= a.rows) return;
+#pragma unroll
+            for (int i = 0; i < kMaxRowCols / 128; ++i) {
+                const int c = lane * 4 + i * 128;
+                if (c < cols)
+                    bpre[i] = __ldg(reinterpret_cast<const float4*>(a.base + r * a.ld_base + col0 + c));
+            }
+        }
+    };
+    auto flush = [&](int r) {
+        __syncwarp();
+        const float* row = &s_row[RB ? warp : 0][(r & 1) * kMaxRowCols];
+#pragma unroll
+        for (int i = 0; i < kMaxRowCols / 128; ++i) {
+            const int c = lane * 4 + i * 128;
+            if (c < cols) {
+                const float4 v = *reinterpret_cast<const float4*>(row + c);
+                if (a.out) *reinterpret_cast<float4*>(a.out + r * a.ld_out + col0 + c) = v;
+                if (a.out_plus) {
+                    const float4 b = bpre[i];
+                    *reinterpret_cast<float4*>(a.out_plus + r * a.ld_plus + col0 + c) =
+                        make_float4(b.x + v.x, b.y + v.y, b.z + v.z, b.w + v.w);
+                }
+            }
+        }
+        __syncwarp();
+    };
+    auto emit_rb = [&](int off, double x) {
+        int j = jb + off, slot = rb & 1;
+        double dg = dcur;
+        if (j >= cols) {
+            j -= cols;
+            slot ^= 1;
+            dg = dnext;
+        }
+        const double v = a.diag ? x * dg : x;
+        s_row[RB ? warp : 0][slot * kMaxRowCols + j] = (float)v;
+    };
+    auto advance_rb = [&](int k) {
+        jb += k;
+        if (jb >= cols) {  // k <= 32 <= cols: at most one row completes
+            jb -= cols;
+            flush(rb);
+            ++rb;
+            dcur = dnext;
+            dnext = load_diag(rb + 1);
+            prefetch_base(rb);
+        }
+    };
+    if (RB) {
+        dcur = load_diag(0);
+        dnext = load_diag(1);
+        prefetch_base(0);
+    }
+
     // warp-uniform access to word `ww` (slow path only)
     auto word = [&](int64_t ww) -> uint64_t {
         if (ww >= base_w && ww < base_w + kBufWords) return buf[ww - base_w];
@@ -195,10 +263,17 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
         const unsigned bad = __ballot_sync(0xffffffffu, !ok);
         const int n_ok = bad ? (__ffs(bad) - 1) : 32;
         const int n_emit = (int)min((int64_t)n_ok, total - q);
-        if (lane < n_emit) emit(lane, x);
+        if (RB) {
+            if (lane < n_emit) emit_rb(lane, x);
+        } else if (lane < n_emit) {
+            emit(lane, x);
+        }
         q += n_emit;
         w += n_emit;
-        advance(n_emit);
+        if (RB)
+            advance_rb(n_emit);
+        else
+            advance(n_emit);
         if (q >= total || n_ok == 32) continue;
 
         // slow path for the rejected word at w (warp-uniform)
@@ -233,9 +308,15 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
                 }
             }
             if (have) {
-                if (lane == 0) emit(0, val);
-                ++q;
-                advance(1);
+                if (RB) {
+                    if (lane == 0) emit_rb(0, val);
+                    ++q;
+                    advance_rb(1);
+                } else {
+                    if (lane == 0) emit(0, val);
+                    ++q;
+                    advance(1);
+                }
             }
         }
     }
@@ -267,8 +348,20 @@ int launch_noise(const uint32_t* head, int n_head, int64_t member0, int64_t n_me
         ENKS_REQUIRE(jobs[j].rows > 0, "enks_noise_fill: job %d has no rows", j);
         a.job[j] = jobs[j];
     }
+    // row-staged path when every job's rows can be written as aligned float4 rows
+    bool rb = cols % 4 == 0 && cols >= 32 && cols <= kMaxRowCols;
+    auto al16 = [](const void* ptr) { return ((uintptr_t)ptr & 15) == 0; };
+    for (int j = 0; j < n_jobs && rb; ++j) {
+        const Job& q = a.job[j];
+        rb = (!q.out || (al16(q.out) && q.ld_out % 4 == 0)) &&
+             (!q.out_plus || (al16(q.out_plus) && q.ld_plus % 4 == 0 && al16(q.base) &&
+                              q.ld_base % 4 == 0));
+    }
     int64_t blocks = (n_members + kWarps - 1) / kWarps;
-    noise_kernel<<<dim3((unsigned)blocks, (unsigned)n_jobs), kWarps * 32, 0, st>>>(a);
+    if (rb)
+        noise_kernel<true><<<dim3((unsigned)blocks, (unsigned)n_jobs), kWarps * 32, 0, st>>>(a);
+    else
+        noise_kernel<false><<<dim3((unsigned)blocks, (unsigned)n_jobs), kWarps * 32, 0, st>>>(a);
     return check_launch("enks_noise_fill");
 }
 }  // namespace

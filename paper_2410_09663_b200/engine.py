@@ -58,6 +58,9 @@ class LocalComm:
     def allreduce_(self, t):
         return t
 
+    def allreduce_max_(self, t):
+        return t
+
     def broadcast_(self, t, src=0):
         return t
 
@@ -75,6 +78,10 @@ class TorchComm:
 
     def allreduce_(self, t):
         self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def allreduce_max_(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return t
 
     def broadcast_(self, t, src=0):
@@ -122,16 +129,52 @@ class Forecaster:
             self.kind = "linear"
             ab = np.concatenate([np.asarray(model.a, float), np.asarray(model.b, float)], axis=1)
             self.ab = ops.to_device(ab)  # n x (n + l)
+        elif name == "BurgersDynamics" and hasattr(model, "cfg"):
+            cfg = model.cfg
+            g = int(cfg.grid_n)
+            if n != 2 * g or l not in (2, 2 * g):
+                raise ValueError("BurgersDynamics: state must be 2n x n and force 2 x n / 2n x n")
+            self.kind = "burgers"
+            self.grid_n, self.substeps = g, int(cfg.substeps)
+            self.nu, self.dt, self.dx = float(cfg.nu), float(cfg.dt), float(cfg.dx)
+            diff = self.nu * self.dt / self.dx ** 2
+            if diff > 0.25:  # input-independent half of the CFL check (dynamics.py:172-177)
+                from .dynamics import CflError
+                raise CflError(f"CFL violated: nu*dt/dx^2 = {diff:.4g} (limit 0.25)")
+            self.vmax = ops.zeros(1)                       # max |phi| over all substep inputs
+            self.flags = ops.zeros(1, dtype=torch.int32)   # bit 0: non-finite entry
         else:
             raise TypeError(f"no device forecast for model type {name}; supported: "
-                            "LinearDynamics, CNNDynamics")
+                            "LinearDynamics, CNNDynamics, BurgersDynamics")
 
     def __call__(self, ops, last, out, n: int, n_members: int):
         """out (n x K) = f(x = last[:n], u = last[n:])."""
         if self.kind == "linear":
             ops.gemm(self.ab, last, out)
+        elif self.kind == "burgers":
+            ops.burgers_forward(self, last[:n], last[n:], out, n_members)
         else:
             ops.cnn_forward(self, last[:n], last[n:], out, n_members)
+
+
+    def check_cfl(self, comm=None) -> None:
+        """Raise CflError if any forecast so far saw max|phi| dt/dx > 1 or a non-finite
+        entry (dynamics.py:168-180, checked lazily over the whole batch and all ranks)."""
+        from .dynamics import CflError
+
+        st = torch.stack([self.vmax[0], self.flags[0].float()])
+        if comm is not None and comm.size > 1:
+            comm.allreduce_max_(st)
+        vmax, bad = float(st[0].item()), float(st[1].item())
+        adv = vmax * self.dt / self.dx
+        if bad or not np.isfinite(vmax):
+            raise CflError("field contains non-finite entries")
+        if adv > 1.0:
+            raise CflError(f"CFL violated: max|phi|*dt/dx = {adv:.4g} (limit 1)")
+
+    @property
+    def advection_number(self) -> float:
+        return float(self.vmax[0].item()) * self.dt / self.dx
 
 
 def _noise_params(params, ops, rows: int, cols: int) -> _Noise:
@@ -500,6 +543,9 @@ class DeviceSmoother:
         return int(self.jitter.item())
 
     def check_status(self) -> None:
+        fc = getattr(self, "forecast", None)
+        if fc is not None and fc.kind == "burgers":
+            fc.check_cfl(self.comm)
         if int(self.status.item()) != 0:
             raise np.linalg.LinAlgError("observation covariance not positive definite even "
                                         "after jitter")

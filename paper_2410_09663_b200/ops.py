@@ -274,6 +274,22 @@ class DeviceOps:
                   float(cnn.alpha), _p(x), _ld(x), _p(u), _ld(u), _p(out), _ld(out),
                   int(x.shape[0]), int(cnn.cols), int(n_members), self._stream())
 
+    def burgers_forward(self, bur, x, u, out, n_members):
+        """bur: engine.Forecaster of kind 'burgers' (grid, solver constants, vmax/flags)."""
+        g, sub = bur.grid_n, bur.substeps
+        ws = int(self.lib.enks_burgers_ws_bytes(g, int(n_members), sub))
+        wsp = None
+        if ws:
+            if getattr(self, "_bur_ws", None) is None or self._bur_ws.numel() * 4 < ws:
+                self._bur_ws = torch.empty((ws + 3) // 4, dtype=torch.float32, device=self.device)
+            wsp = self._bur_ws
+        self.launches += 1 if not ws else sub
+        _lib.call("enks_burgers_forward", _p(x), _ld(x), _p(u) if u is not None else None,
+                  _ld(u) if u is not None else 0, int(u.shape[0]) if u is not None else 0,
+                  _p(out), _ld(out), g, int(n_members), sub, float(bur.nu), float(bur.dt),
+                  float(bur.dx), _p(bur.vmax), _p(bur.flags), _p(wsp) if wsp is not None else None,
+                  self._stream())
+
     def add(self, a, b, out):
         self.launches += 1
         _lib.call("enks_add", _p(a), _ld(a), _p(b), _ld(b), _p(out), _ld(out), out.shape[0],

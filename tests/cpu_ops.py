@@ -144,5 +144,16 @@ class CpuOps:
         y = cnn_step(xs, us, w, b, cnn.alpha)
         out.copy_(torch.from_numpy(np.ascontiguousarray(y.transpose(1, 0, 2).reshape(n, -1))))
 
+    def burgers_forward(self, bur, x, u, out, n_members):
+        from oracle.models import burgers_step
+
+        g = bur.grid_n
+        xs = x.numpy().reshape(2 * g, n_members, g).transpose(1, 0, 2)
+        us = u.numpy().reshape(u.shape[0], n_members, g).transpose(1, 0, 2)
+        mode = "pointwise" if u.shape[0] == 2 * g else "boundary"
+        y, vmax = burgers_step(xs, us, g, bur.nu, bur.dt, mode, bur.substeps)
+        bur.vmax[0] = max(float(bur.vmax[0]), vmax)
+        out.copy_(torch.from_numpy(np.ascontiguousarray(y.transpose(1, 0, 2).reshape(2 * g, -1))))
+
     def sub(self, a, b, out):
         out.copy_(a - b)

@@ -52,6 +52,32 @@ def _cnn_case(ref):
     return dict(mean=out, x0=x0.packed)
 
 
+BURGERS_STEP_CASES = [(12, "boundary", 1), (12, "pointwise", 3), (32, "boundary", 3),
+                      (32, "pointwise", 1)]
+
+
+def _burgers_steps(ref):
+    """Reference BurgersDynamics.step (dynamics.py:264-270) on seeded member batches."""
+    out = {}
+    for k, (g, mode, sub) in enumerate(BURGERS_STEP_CASES):
+        cfg = ref.dynamics.BurgersConfig(grid_n=g, control_mode=mode, substeps=sub)
+        model = ref.dynamics.BurgersDynamics(cfg)
+        rng = np.random.default_rng(100 + k)
+        x = np.stack([ref.dynamics.make_initial_field(cfg, s).packed for s in range(3)])
+        x = x + 0.05 * rng.standard_normal(x.shape)
+        u = rng.standard_normal((3, model.input_rows, g))
+        out[f"x{k}"], out[f"u{k}"], out[f"y{k}"] = x, u, model.step(x, u)
+    return out
+
+
+def _burgers_horizon(ref, mode):
+    """Reference smooth_horizon (enks.py:256-284) with the reference Burgers model (C1a)."""
+    pr = problems.make_burgers_problem(ref, mode)
+    out, _ = ref.enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N,
+                                     ref.matvar.NoiseStreams(seed=2))
+    return dict(mean=out, x0=pr.x0.packed)
+
+
 def main():
     ref = problems.reference_modules()
     for name, kw, seed, N, h, sseed, extra in LINEAR_CASES:
@@ -77,6 +103,10 @@ def main():
     _, vs, x0 = problems.make_linear_setup(ref, np.random.default_rng(11), n=4, l=1, m=1)
     np.savez_compressed(os.path.join(HERE, "exact_lin_4x1x1.npz"), x0=x0.packed,
                         exact=base.exact_linear_smoother(x0, vs, h=3))
+    np.savez_compressed(os.path.join(HERE, "burgers_steps.npz"), **_burgers_steps(ref))
+    for mode in ("boundary", "pointwise"):
+        np.savez_compressed(os.path.join(HERE, f"burgers_c1a_{mode}.npz"),
+                            **_burgers_horizon(ref, mode))
     noise = {}
     for k, (seed, prefix, ids, shape) in enumerate(NOISE_CASES):
         st = ref.matvar.NoiseStreams(seed=seed, prefix=prefix)

@@ -79,3 +79,15 @@ def test_engine_explicit_members_restart(pm, pair):
         eng.update(ops.to_device(y), st)
     got = eng.members_device().numpy().reshape(o.members.shape[1], 9, x0.m).transpose(1, 0, 2)
     assert np.abs(got - o.members).max() < 1e-10 * np.abs(o.members).max()
+
+
+@pytest.mark.parametrize("mode", ["boundary", "pointwise"])
+def test_engine_burgers_equals_oracle_fp64(pm, mode):
+    from oracle.models import OracleBurgers
+
+    pr = problems.make_burgers_problem(pm, mode, grid_n=8, n_members=12, horizon=3)
+    ovs = pm.virtualsys.build_virtual_system(OracleBurgers(pr.model), pr.vs.weights)
+    ref, _, _ = enks_oracle.oracle_smooth(pr.x0, pr.y_ref, ovs, pr.H, pr.N, seed=2, backend="c")
+    eng = _run(pm, pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, 2)
+    assert eng.forecast.kind == "burgers"
+    assert np.abs(eng.mean_host().reshape(ref.shape) - ref).max() < 1e-10 * np.abs(ref).max()

@@ -32,12 +32,14 @@ def test_noise_bit_exact_vs_numpy(dev_ops, seed, prefix, t, ch, N, rows, cols):
     assert np.array_equal(got, ref.astype(np.float32))
 
 
-def test_noise_bit_exact_many_streams_with_tail(dev_ops):
-    """~270k normals: exercises the wedge (0.8%) and tail (0.02%) rejection paths."""
+@pytest.mark.parametrize("cols", [66, 64])
+def test_noise_bit_exact_many_streams_with_tail(dev_ops, cols):
+    """~270k normals: exercises the wedge (0.8%) and tail (0.02%) rejection paths
+    (cols 66: direct stores; cols 64: row-staged float4 path)."""
     from oracle import noise as onoise
     from paper_2410_09663_b200.matvar import entropy_head
 
-    N, rows, cols = 64, 64, 66
+    N, rows = 64, 64
     ref = onoise.member_normals(9, (), 5, 1, N, (rows, cols), backend="c")
     assert np.abs(ref).max() > 3.6541528853610088  # at least one tail sample present
     out = dev_ops.zeros(rows, N * cols)
@@ -46,12 +48,13 @@ def test_noise_bit_exact_many_streams_with_tail(dev_ops):
     assert np.array_equal(got, ref.astype(np.float32))
 
 
-def test_noise_member_offset_diag_and_base(dev_ops):
+@pytest.mark.parametrize("N,rows,cols,m0", [(6, 4, 5, 11), (6, 4, 32, 11), (5, 9, 128, 3),
+                                            (3, 70, 512, 0)])
+def test_noise_member_offset_diag_and_base(dev_ops, N, rows, cols, m0):
     from oracle import noise as onoise
     from paper_2410_09663_b200.matvar import entropy_head
 
-    N, rows, cols, m0 = 6, 4, 5, 11
-    diag = np.array([1.0, 2.0, 0.5, 3.0])
+    diag = np.linspace(0.5, 3.0, rows)
     ref = onoise.member_normals(1, (), 3, 2, m0 + N, (rows, cols), backend="c")[m0:]
     col = (diag[None, :, None] * ref).astype(np.float32)
     base = torch.randn(rows, N * cols, device=dev_ops.device)
@@ -331,3 +334,57 @@ def test_gemm_f16pair(dev_ops, M, N, K):
     scale = 0.5 * (A.double().abs() @ B.double().abs().t())
     err = ((C.double().cpu() - ref).abs() / scale).max().item()
     assert err < 1e-6, err
+
+
+def _burgers_forecaster(dev_ops, pm, g, mode, substeps, dt=0.001):
+    from paper_2410_09663_b200.engine import Forecaster
+
+    model = pm.dynamics.BurgersDynamics(pm.dynamics.BurgersConfig(grid_n=g, control_mode=mode,
+                                                                  substeps=substeps, dt=dt))
+    return model, Forecaster(model, dev_ops, 2 * g, model.input_rows)
+
+
+@pytest.mark.parametrize("g,mode,substeps,N", [(8, "boundary", 1, 5), (32, "pointwise", 3, 100),
+                                               (32, "boundary", 4, 37), (64, "pointwise", 2, 9),
+                                               (128, "boundary", 3, 3), (128, "pointwise", 1, 2)])
+def test_burgers_forward_vs_oracle(dev_ops, pm, g, mode, substeps, N):
+    """Fused shared-memory kernel (g <= 64) and per-substep global kernel (g = 128)."""
+    from oracle.models import burgers_step
+
+    model, fc = _burgers_forecaster(dev_ops, pm, g, mode, substeps)
+    rng = np.random.default_rng(g + N)
+    base = pm.dynamics.make_initial_field(model.cfg, 0).packed
+    x = base[None] + 0.1 * rng.standard_normal((N, 2 * g, g))
+    u = rng.standard_normal((N, model.input_rows, g))
+    ref, vmax = burgers_step(x, u, g, model.cfg.nu, model.cfg.dt, mode, substeps)
+    last = np.concatenate([x, u], axis=1).transpose(1, 0, 2).reshape(2 * g + u.shape[1], N * g)
+    last_d = dev_ops.to_device(last)
+    out = dev_ops.zeros(2 * g, N * g)
+    fc(dev_ops, last_d, out, 2 * g, N)
+    got = out.double().cpu().numpy().reshape(2 * g, N, g).transpose(1, 0, 2)
+    assert np.abs(got - ref).max() < 1e-5 * np.abs(ref).max()
+    assert abs(float(fc.vmax[0]) - vmax) <= 1e-6 * vmax
+    fc.check_cfl()
+
+
+def test_burgers_cfl_and_nonfinite_flags(dev_ops, pm):
+    from paper_2410_09663_b200.dynamics import CflError
+
+    g, N = 16, 4
+    _, fc = _burgers_forecaster(dev_ops, pm, g, "boundary", 1, dt=0.01)
+    last = np.zeros((2 * g + 2, N * g))
+    last[:2 * g] = 0.5                      # |phi| dt/dx = 0.5 * 0.01 * 15 = 0.075: fine
+    out = dev_ops.zeros(2 * g, N * g)
+    fc(dev_ops, dev_ops.to_device(last), out, 2 * g, N)
+    fc.check_cfl()
+    last[3, 5 * 1 + g] = 10.0               # 10 * 0.01 * 15 = 1.5 > 1 on member 1
+    fc(dev_ops, dev_ops.to_device(last), out, 2 * g, N)
+    with pytest.raises(CflError, match="CFL"):
+        fc.check_cfl()
+    _, fc = _burgers_forecaster(dev_ops, pm, g, "boundary", 1, dt=0.01)
+    last[3, 5 + g] = np.nan
+    fc(dev_ops, dev_ops.to_device(last), out, 2 * g, N)
+    with pytest.raises(CflError, match="non-finite"):
+        fc.check_cfl()
+    with pytest.raises(CflError, match="nu"):
+        _burgers_forecaster(dev_ops, pm, g, "boundary", 1, dt=0.5)

@@ -66,3 +66,35 @@ def test_c_noise_matches_reference_golden():
     for k, (seed, prefix, ids, shape) in enumerate(NOISE_CASES):
         z = noise.c_standard_normal(seed, tuple(prefix) + tuple(ids), int(np.prod(shape)))
         assert np.array_equal(z.reshape(shape), gold[f"z{k}"])
+
+
+def test_oracle_burgers_step_matches_reference_golden():
+    from golden.make_golden import BURGERS_STEP_CASES
+    from oracle.models import burgers_step
+
+    gold = _load("burgers_steps")
+    for k, (g, mode, sub) in enumerate(BURGERS_STEP_CASES):
+        y, _ = burgers_step(gold[f"x{k}"], gold[f"u{k}"], g, 0.005, 0.001, mode, sub)
+        assert np.array_equal(y, gold[f"y{k}"]), (g, mode, sub)
+
+
+def test_product_host_burgers_step_matches_reference_golden(pm):
+    from golden.make_golden import BURGERS_STEP_CASES
+
+    gold = _load("burgers_steps")
+    for k, (g, mode, sub) in enumerate(BURGERS_STEP_CASES):
+        model = pm.dynamics.BurgersDynamics(pm.dynamics.BurgersConfig(grid_n=g, control_mode=mode,
+                                                                      substeps=sub))
+        assert np.array_equal(model.step(gold[f"x{k}"], gold[f"u{k}"]), gold[f"y{k}"])
+
+
+@pytest.mark.parametrize("mode", ["boundary", "pointwise"])
+def test_oracle_burgers_horizon_matches_reference_golden(pm, mode):
+    from oracle.models import OracleBurgers
+
+    gold = _load(f"burgers_c1a_{mode}")
+    pr = problems.make_burgers_problem(pm, mode)
+    assert np.array_equal(pr.x0.packed, gold["x0"])
+    ovs = pm.virtualsys.build_virtual_system(OracleBurgers(pr.model), pr.vs.weights)
+    out, _, _ = enks_oracle.oracle_smooth(pr.x0, pr.y_ref, ovs, pr.H, pr.N, seed=2, backend="c")
+    np.testing.assert_allclose(out, gold["mean"], rtol=1e-12, atol=1e-12)

@@ -137,3 +137,22 @@ def test_lambda_cancellation(pm):
     a, _ = enks.smooth_horizon(x0, y, vs, 3, 16, pm.matvar.NoiseStreams(seed=4))
     b, _ = enks.smooth_horizon(x0, y, vs7, 3, 16, pm.matvar.NoiseStreams(seed=4))
     assert _rel(a, b) < 1e-5
+
+
+@pytest.mark.parametrize("mode", ["boundary", "pointwise"])
+def test_smooth_horizon_burgers_c1a_matches_reference_golden(pm, mode):
+    """C1a: the reference's own Burgers FD problem (grid 32, N=100, H=5), compared with the
+    UNMODIFIED reference smooth_horizon output (tests/golden/burgers_c1a_*.npz)."""
+    import os
+
+    from oracle import problems
+    from paper_2410_09663_b200 import enks
+
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", f"burgers_c1a_{mode}.npz"))
+    pr = problems.make_burgers_problem(pm, mode)
+    assert np.array_equal(pr.x0.packed, gold["x0"])
+    got, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N,
+                                 pm.matvar.NoiseStreams(seed=2))
+    n, l = pr.n, pr.l
+    assert _rel(got, gold["mean"]) < TOL
+    assert _rel(got[:, n:n + l], gold["mean"][:, n:n + l]) < TOL

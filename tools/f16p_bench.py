@@ -8,7 +8,7 @@ sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", os.path.dirname(os.path.dir
 from paper_2410_09663_b200.ops import DeviceOps  # noqa: E402
 
 ops = DeviceOps()
-for M in (2560, 19200):
+for M in (2560, 8064, 19200):
     K, N = 131072, 256
     A = torch.randn(M, K, device="cuda")
     B = torch.randn(N, K, device="cuda")
@@ -18,8 +18,8 @@ for M in (2560, 19200):
     ops.f16pair_split(A, ah, al, sa)
     ops.f16pair_split(B, bh, bl, sb)
     C = torch.empty(M, N, device="cuda")
-    for chain in ("8", "32"):
-        os.environ["ENKS_TC_CHAIN"] = chain
+    for chain in ("3", "2"):
+        os.environ["ENKS_F16P_PRODUCTS"] = chain
         for _ in range(2):
             ops.gemm_f16pair(ah, al, sa, bh, bl, sb, C)
         torch.cuda.synchronize()
@@ -30,6 +30,6 @@ for M in (2560, 19200):
         e.record()
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / 5
-        print(f"f16pair M={M} chain={chain}: {ms:.3f} ms {2 * M * N * K / ms / 1e9:.0f} TF/s "
+        print(f"f16pair pair={os.environ.get('ENKS_F16P_PAIR', '1')} M={M} products={chain}: {ms:.3f} ms {2 * M * N * K / ms / 1e9:.0f} TF/s "
               f"A {M * K * 4 / ms / 1e6:.0f} GB/s", flush=True)
     del A, ah, al

@@ -42,9 +42,10 @@ print(f"oracle {time.time() - t0:.1f}s", flush=True)
 from paper_2410_09663_b200 import enks  # noqa: E402
 
 n, l = pr.n, pr.l
-for tc in ("1", "0"):
+for tc, prod in (("1", "3"), ("1", "2"), ("0", "3")):
     os.environ["ENKS_TC"] = tc
+    os.environ["ENKS_F16P_PRODUCTS"] = prod
     got, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, pm.matvar.NoiseStreams(seed=0))
     sc = np.abs(ref).max()
-    print(f"ENKS_TC={tc} rel all {np.abs(got - ref).max() / sc:.3e}  X {np.abs(got[:, :n] - ref[:, :n]).max() / sc:.3e}"
+    print(f"ENKS_TC={tc} products={prod} rel all {np.abs(got - ref).max() / sc:.3e}  X {np.abs(got[:, :n] - ref[:, :n]).max() / sc:.3e}"
           f"  U {np.abs(got[:, n:n + l] - ref[:, n:n + l]).max() / np.abs(ref[:, n:n + l]).max():.3e}", flush=True)
