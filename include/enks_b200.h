@@ -226,6 +226,27 @@ int enks_burgers_forward(const float* x, int64_t ldx, const float* u, int64_t ld
                          double nu, double dt, double dx, float* vmax, int* flags, void* ws,
                          void* stream);
 
+/*
+ * Constraint barrier observation row (enks.py:201-208,
+ * virtualsys.py:289-302).  S: predicted slices (d x n_members*m, member-column layout).
+ * g_i = <coef, S_i> + c0 (kind 0, coef d x m) or max_{r0<=r<r1}|S_i[r,:]| + c0 (kind 1);
+ * out[i*m + j] = softplus_{alpha,beta}(g_i) + sqrt_var * eps[i] for all j (fp64 math).
+ * eps: the first draw of substream (i, t, CH_EPS) per member (enks_noise_fill, 1 x 1).
+ */
+int enks_barrier_row(const float* S, int64_t lds, int d, int m, int64_t n_members, int kind,
+                     const float* coef, int64_t ldc, double c0, int r0, int r1, double alpha,
+                     double beta, double sqrt_var, const float* eps, float* out, void* stream);
+
+/*
+ * Quadratic trace for the closed-loop metrics:
+ * out[0] = (accumulate ? out[0] : 0) + scale * sum_ij E[i,j] X[i,j] in fp64, one CTA,
+ * fixed reduction order.  stage_cost (virtualsys.py:279-286) is tr[e^T W^-1 e] summed over
+ * the x / u / dU blocks = sum(e * (W^-1 e)); the SPEC controller's rmse is
+ * ||phi - phi_ref||_F^2 / points (SPEC.md controller.rmse).
+ */
+int enks_quad_form(const float* E, int64_t lde, const float* X, int64_t ldx, int64_t rows,
+                   int64_t cols, double scale, double* out, int accumulate, void* stream);
+
 /* Small elementwise helpers. */
 /* out[r, j] = a[r, j] + b[r, j] (the "u + w + v" observation of enks.py:168, 200). */
 int enks_add(const float* a, int64_t lda, const float* b, int64_t ldb, float* out, int64_t ldo,

@@ -8,6 +8,7 @@ own data layout (members (N, (t+1) d, m), fp64, BLAS GEMMs, LAPACK Cholesky):
   _draw               enks.py:131-145 (per-member substream draws, coloured)
   _pair_cov           enks.py:148-153 ((lam/N) A B^T over (member, column) pairs)
   oracle_predict      enks.py:156-186 (W draw, [f(x,u); u+w; w], append, mean, optional cov)
+  _barrier_rows       enks.py:201-208 + virtualsys.py:289-302 (constraint barrier row)
   oracle_update       enks.py:189-253 (perturbed obs, Sigma_y, Sigma_xy, jittered Cholesky gain,
                                        whole-trajectory shift, mean, optional cov)
   oracle_smooth       enks.py:256-284 (h x (predict, update))
@@ -91,6 +92,22 @@ def _draw(params, seed, prefix, t, ch, n_members, shape, backend):
     return params.mean + params.row_chol @ z @ params.col_chol.T
 
 
+def _barrier_rows(spec, x, u, du, seed, prefix, t, backend):
+    """One row per member: softplus(g(slice_i)) + sqrt(var) * (first draw of (i, t, CH_EPS))."""
+    import math
+    from types import SimpleNamespace
+
+    N, m = x.shape[0], x.shape[2]
+    eps = _noise.member_normals(seed, prefix, t, CH_EPS, N, (1, 1), backend=backend)[:, 0, 0]
+    rows = np.empty((N, 1, m))
+    for i in range(N):
+        g = float(spec.g(SimpleNamespace(x=x[i], u=u[i], du=du[i])))
+        z = spec.beta * g
+        clean = z / spec.alpha if z > 30.0 else math.log1p(math.exp(z)) / spec.alpha
+        rows[i, 0, :] = clean + math.sqrt(spec.noise_var) * eps[i]
+    return rows
+
+
 def _pair_cov(a: np.ndarray, b: np.ndarray, lam: float) -> np.ndarray:
     N = a.shape[0]
     am = np.swapaxes(a, 0, 1).reshape(a.shape[1], -1)
@@ -146,7 +163,8 @@ def oracle_update(ens: OracleEnsemble, y_ref: np.ndarray, vs, seed: int, prefix=
     vu = _draw(vs.obs_noise_u, seed, prefix, ens.t, CH_VU, ens.N, (ens.n_u, m), backend)
     obs = np.concatenate([x + vx, u + vu], axis=1)
     if getattr(vs, "constraint", None) is not None:
-        raise NotImplementedError("oracle: constraint rows not restated yet")
+        obs = np.concatenate([obs, _barrier_rows(vs.constraint, x, u, du, seed, prefix, ens.t,
+                                                 backend)], axis=1)
     t1 = time.perf_counter()
     if y_ref.shape != obs.shape[1:]:
         raise ValueError(f"y_ref shape {y_ref.shape} != observation {obs.shape[1:]}")

@@ -100,6 +100,20 @@ def make_burgers_problem(mods, mode: str = "boundary", grid_n: int = 32, n_membe
                            cfg=cfg, y_ref=vs.reference_observation())
 
 
+def make_constraint(mods, kind: str, n: int, l: int, m: int):
+    """ConstraintSpec with a device-expressible g (product virtualsys Linear/BoxConstraint),
+    built from the given module's ConstraintSpec so it plugs into either side."""
+    from paper_2410_09663_b200.virtualsys import BoxConstraint, LinearConstraint
+
+    if kind == "linear":
+        g = LinearConstraint(cu=0.3 * np.ones((l, m)), cx=0.05 * np.ones((n, m)), c0=-0.5)
+    elif kind == "box":
+        g = BoxConstraint(1.0, "u")
+    else:
+        raise ValueError(kind)
+    return mods.virtualsys.ConstraintSpec(g=g, alpha=10.0, beta=5.0, noise_var=1e-2)
+
+
 def product_modules():
     import paper_2410_09663_b200 as pkg
 

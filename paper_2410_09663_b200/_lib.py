@@ -72,6 +72,9 @@ _SIGS = {
     "enks_burgers_ws_bytes": (_c_i64, [_c_int, _c_int, _c_int]),
     "enks_burgers_forward": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int,
                                       _c_int, _c_int, _c_d, _c_d, _c_d, _vp, _vp, _vp, _vp]),
+    "enks_barrier_row": (_c_int, [_vp, _c_i64, _c_int, _c_int, _c_i64, _c_int, _vp, _c_i64, _c_d,
+                                  _c_int, _c_int, _c_d, _c_d, _c_d, _vp, _vp, _vp]),
+    "enks_quad_form": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_i64, _c_i64, _c_d, _vp, _c_int, _vp]),
     "enks_add": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _c_i64, _c_i64, _vp]),
     "enks_sub": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _c_i64, _c_i64, _vp]),
 }

@@ -46,9 +46,41 @@ __global__ void add_kernel(const float* __restrict__ a, int64_t lda, const float
         out[r * ldo + c] = a[r * lda + c] + b[r * ldb + c];
 }
 
+// out[0] (+)= scale * sum_ij E_ij X_ij, fp64, one CTA, fixed reduction order (deterministic)
+__global__ void __launch_bounds__(1024) quad_form_kernel(const float* __restrict__ E, int64_t lde,
+                                                        const float* __restrict__ X, int64_t ldx,
+                                                        int64_t rows, int64_t cols, double scale,
+                                                        double* out, int accumulate) {
+    double acc = 0.0;
+    const int64_t total = rows * cols;
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+        const int64_t r = e / cols, c = e - r * cols;
+        acc += (double)E[r * lde + c] * (double)X[r * ldx + c];
+    }
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        out[0] = (accumulate ? out[0] : 0.0) + scale * t;
+    }
+}
+
 }  // namespace enks
 
 extern "C" {
+
+int enks_quad_form(const float* E, int64_t lde, const float* X, int64_t ldx, int64_t rows,
+                   int64_t cols, double scale, double* out, int accumulate, void* stream) {
+    ENKS_REQUIRE(E && X && out, "enks_quad_form: null pointer");
+    ENKS_REQUIRE(rows >= 0 && cols >= 0, "enks_quad_form: negative shape");
+    enks::quad_form_kernel<<<1, 1024, 0, enks::as_stream(stream)>>>(E, lde, X, ldx, rows, cols,
+                                                                    scale, out, accumulate);
+    return enks::check_launch("enks_quad_form");
+}
 
 int enks_version(void) { return 1; }
 

@@ -177,6 +177,39 @@ class Forecaster:
         return float(self.vmax[0].item()) * self.dt / self.dx
 
 
+@dataclass
+class _Barrier:
+    kind: int            # 0 linear functional, 1 max-abs over a row block
+    coef: object         # device (d x m) fp32 for kind 0
+    c0: float
+    r0: int
+    r1: int
+    alpha: float
+    beta: float
+    sqrt_var: float
+
+
+def _barrier_spec(con, ops, n: int, l: int, m: int) -> _Barrier:
+    """Device form of ConstraintSpec.g: LinearConstraint / BoxConstraint only (no host g)."""
+    from .virtualsys import BoxConstraint, LinearConstraint
+
+    g = con.g
+    common = dict(alpha=float(con.alpha), beta=float(con.beta),
+                  sqrt_var=float(np.sqrt(con.noise_var)))
+    if isinstance(g, LinearConstraint):
+        coef = np.zeros((n + 2 * l, m))
+        for r0, c in ((0, g.cx), (n, g.cu), (n + l, g.cdu)):
+            if c is not None:
+                c = np.asarray(c, float)
+                coef[r0:r0 + c.shape[0]] = c
+        return _Barrier(0, ops.to_device(coef), float(g.c0), 0, n + 2 * l, **common)
+    if isinstance(g, BoxConstraint):
+        r0, r1 = {"x": (0, n), "u": (n, n + l), "du": (n + l, n + 2 * l)}[g.block]
+        return _Barrier(1, None, -float(g.bound), r0, r1, **common)
+    raise TypeError("constraint g must be a LinearConstraint or BoxConstraint on the device "
+                    f"path (got {type(g).__name__}); arbitrary host callables are not evaluated")
+
+
 def _noise_params(params, ops, rows: int, cols: int) -> _Noise:
     if params is None:
         return _Noise("zero")
@@ -202,7 +235,10 @@ class DeviceSmoother:
         self.ops = ops
         self.comm = comm or LocalComm()
         self.n, self.l = int(n), int(l)
-        self.d, self.p = self.n + 2 * self.l, self.n + self.l
+        # d: slice rows [X; U; dU]; q: state rows [X; U] fed to the forecast; p: observation
+        # rows [X; U] (+1 barrier row when a constraint is bound, enks.py:201-208)
+        self.d, self.q = self.n + 2 * self.l, self.n + self.l
+        self.p = self.q
         self.m = int(x0_packed.shape[1])
         self.N = int(n_members)
         if self.N < self.comm.size:
@@ -215,18 +251,34 @@ class DeviceSmoother:
         self.cap = 0
         self.slice0_zero = True  # all members start as identical copies (enks.py:120)
         self._bound = None
-        d, p, K, m = self.d, self.p, self.K, self.m
-        # tcgen05 3xTF32 cross moments (ENKS_TC=0 forces the SIMT engine for A/B checks)
+        self.barrier = None
+        self._basis = basis
+        d, q, K = self.d, self.q, self.K
+        self.slice_raw = ops.empty(d, K)      # [X; U; W] of the newest predicted slice
+        self.last = ops.empty(q, K)           # materialised [x; u] of the newest updated slice
+        self.status = ops.zeros(1, dtype=torch.int32)
+        self.jitter = ops.zeros(1, dtype=torch.int32)
+        self._alloc_obs()
+        self._grow(max(1, int(capacity)))
+        x0 = ops.to_device(np.asarray(x0_packed, float))
+        self.mean[:d] = x0
+        self.last.copy_(x0[:q].repeat(1, self.Nl))
+        self._store_rows("A", 0, ops.zeros(d, K))
+
+    def _alloc_obs(self) -> None:
+        """Buffers whose shape depends on the observation row count p."""
+        ops, d, p, q, K, m = self.ops, self.d, self.p, self.q, self.K, self.m
+        # tcgen05 cross moments (ENKS_TC=0 forces the SIMT engine for A/B checks)
         self.use_tc = (os.environ.get("ENKS_TC", "1") != "0" and hasattr(ops, "gemm_nt_tc")
                        and p <= 256 and K >= 128)
         # basis storage: fp16 pairs (tcgen05 kind::f16 contraction, gemm_f16p.cu) or fp32
-        basis = basis or os.environ.get("ENKS_BASIS", "f16pair" if self.use_tc else "fp32")
+        basis = self._basis or os.environ.get("ENKS_BASIS", "f16pair" if self.use_tc else "fp32")
         self.pair = basis == "f16pair" and K % 8 == 0 and hasattr(ops, "gemm_f16pair")
         if self.use_tc and not self.pair:
             self.yc_hi = ops.empty(p, K)
             self.yc_lo = ops.empty(p, K)
         if self.pair:
-            self.A_new = ops.empty(p, K)   # fp32 anomalies of the newest slice, [x; u] rows
+            self.A_new = ops.empty(q, K)   # fp32 anomalies of the newest slice, [x; u] rows
             self.Yc_new = ops.empty(p, K)  # fp32 centred observations of the newest slice
         # the gain-side products (correction, gain, newest-slice shift) on tcgen05 as well
         self.use_tc2 = self.use_tc and p % 4 == 0 and m % 4 == 0 and hasattr(ops, "gemm_tc")
@@ -236,22 +288,47 @@ class DeviceSmoother:
             self.sinvT_hi = ops.empty(p, p)
             self.sinvT_lo = ops.empty(p, p)
             self.pyT_hi = self.pyT_lo = None
-        self.slice_raw = ops.empty(d, K)      # [X; U; W] of the newest predicted slice
         self.obs_raw = ops.empty(p, K)        # perturbed observations of the newest slice
-        self.last = ops.empty(p, K)           # materialised [x; u] of the newest updated slice
         self.acc = ops.zeros(max(d, p), m, dtype=torch.float64)
         self.amax = ops.zeros(max(d, p), m)
         self.z0 = ops.zeros(max(d, p), m) if self.comm.size > 1 else None
         self.ybar = ops.zeros(p, m)
         self.innov = ops.zeros(p, m)
         self.sinv = ops.zeros(p, p)
-        self.status = ops.zeros(1, dtype=torch.int32)
-        self.jitter = ops.zeros(1, dtype=torch.int32)
-        self._grow(max(1, int(capacity)))
-        x0 = ops.to_device(np.asarray(x0_packed, float))
-        self.mean[:d] = x0
-        self.last.copy_(x0[:p].repeat(1, self.Nl))
-        self._store_rows("A", 0, ops.zeros(d, K))
+        self.eps = ops.empty(1, self.Nl) if p > q else None   # CH_EPS draws (barrier row)
+
+    def _set_obs_rows(self, p: int) -> None:
+        """Re-plan the observation-dependent storage (a constraint adds a barrier row);
+        only before the first predict, when no observation history exists."""
+        if p == self.p:
+            return
+        if self.t != 0:
+            raise ValueError("the observation rows (constraint) cannot change mid-horizon")
+        d, cap = self.d, self.cap
+        x0 = self.mean[:d].clone()
+        self.p = p
+        self._alloc_obs()
+        self.cap = 0
+        self._grow(cap)
+        self.reset(x0)
+
+    def reset(self, x0) -> None:
+        """Start a new horizon from N identical copies of x0 ((d x m), host or device),
+        reusing every buffer (closed-loop driver: one smoother per MPC step, enks.py:105-128)."""
+        d, q = self.d, self.q
+        x0 = x0 if torch.is_tensor(x0) else self.ops.to_device(np.asarray(x0, float))
+        self.t = 0
+        self.n_upd = 0
+        self.slice0_zero = True
+        self._obs_t = -1
+        self.mean[:d].copy_(x0)
+        self.last.copy_(x0[:q].repeat(1, self.Nl))
+        if self.pair:
+            self.Ah[:d].zero_()
+            self.Al[:d].zero_()
+            self.a_inv[:d].fill_(1.0)
+        else:
+            self.Abuf[:d].zero_()
 
     # ------------------------------------------------------------ storage
     def _grow(self, cap: int) -> None:
@@ -328,10 +405,10 @@ class DeviceSmoother:
     def bind(self, vs) -> None:
         if self._bound is vs:
             return
-        if getattr(vs, "constraint", None) is not None:
-            raise NotImplementedError("constraint barrier rows are not on the device path yet "
-                                      "(SURVEY.md §8f row 4)")
         ops = self.ops
+        con = getattr(vs, "constraint", None)
+        self.barrier = None if con is None else _barrier_spec(con, ops, self.n, self.l, self.m)
+        self._set_obs_rows(self.q + (0 if con is None else 1))
         self.forecast = Forecaster(vs.model, ops, self.n, self.l)
         self.noise_w = _noise_params(vs.process_noise, ops, self.l, self.m)
         self.noise_vx = _noise_params(vs.obs_noise_x, ops, self.n, self.m)
@@ -344,6 +421,16 @@ class DeviceSmoother:
         self._bound = vs
 
     # ------------------------------------------------------------ helpers
+    def _barrier_row(self, head, t) -> None:
+        """Observation row q: softplus(g(slice_i)) + sqrt(var) eps_i, eps_i the first draw of
+        substream (i, t, CH_EPS)  (enks.py:201-208, virtualsys.py:289-302)."""
+        if self.barrier is None:
+            return
+        ops = self.ops
+        ops.noise_fill(head, t, CH_EPS, self.member0, self.Nl, 1, 1, out=self.eps)
+        ops.barrier_row(self.barrier, self.slice_raw, self.n, self.l, self.m, self.Nl, self.eps,
+                        self.obs_raw[self.q:self.q + 1])
+
     def _noise(self, spec: _Noise, head, t, ch, rows, out=None, base=None, out_plus=None):
         """out = L z ; out_plus = base + L z for this rank's members."""
         ops = self.ops
@@ -417,9 +504,10 @@ class DeviceSmoother:
                      base=self.last[n:], out_plus=sr[n:n + l]),
                 dict(t=tau, ch=CH_VX, rows=n, diag=self.noise_vx.diag, base=sr[:n],
                      out_plus=ob[:n]),
-                dict(t=tau, ch=CH_VU, rows=l, diag=self.noise_vu.diag, out=ob[n:]),
+                dict(t=tau, ch=CH_VU, rows=l, diag=self.noise_vu.diag, out=ob[n:n + l]),
             ])
-            ops.add(sr[n:n + l], ob[n:], ob[n:])
+            ops.add(sr[n:n + l], ob[n:n + l], ob[n:n + l])
+            self._barrier_row(head, tau)
             self._obs_t = tau
             self._obs_key = (streams.seed, tuple(streams.prefix))
         else:
@@ -429,7 +517,7 @@ class DeviceSmoother:
         if self.pair:
             # fp32 copy of the [x; u] rows only (the newest-slice shift's C0)
             self._center(sr, self.mean[tau * d:(tau + 1) * d], self.A_new, pair_rows=("A", tau * d),
-                         f32_rows=self.p)
+                         f32_rows=self.q)
         else:
             self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d])
         self.t = tau
@@ -446,7 +534,9 @@ class DeviceSmoother:
         # perturbed observations [x + v_x; u + v_u]  (enks.py:194-200)
         if self._obs_t != tau or self._obs_key != (streams.seed, tuple(streams.prefix)):
             self._noise(self.noise_vx, head, tau, CH_VX, n, base=sr[:n], out_plus=ob[:n])
-            self._noise(self.noise_vu, head, tau, CH_VU, l, base=sr[n:n + l], out_plus=ob[n:])
+            self._noise(self.noise_vu, head, tau, CH_VU, l, base=sr[n:n + l],
+                        out_plus=ob[n:n + l])
+            self._barrier_row(head, tau)
         yc = self.Yc_new if self.pair else self.Ybuf[(tau - 1) * p:tau * p]
         if self.pair:
             self._center(ob, self.ybar, yc, pair_rows=("Y", (tau - 1) * p), f32_rows=p)
@@ -502,15 +592,16 @@ class DeviceSmoother:
         mv = self.mean[a0:rows_a]
         ops.gemm(gcol, self.innov, mv, beta=1.0, C0=mv)
         # newest slice [x; u] for the next forecast: mean + A_tau - G_{tau,tau} Yc_tau
-        g_tt = self.G[r0:r0 + p, (tau - 1) * p:tau * p]
+        q = self.q
+        g_tt = self.G[r0:r0 + q, (tau - 1) * p:tau * p]
         a_new = self.A_new if self.pair else self.Abuf[r0:r0 + d]
         if self.use_tc2:
             ops.tf32_split(yc, self.ycT_hi, self.ycT_lo, transpose=True)
             ops.gemm_tc(g_tt, self.ycT_hi, self.ycT_lo, self.last, alpha=-1.0, beta=1.0,
-                        C0=a_new[:p], bias=self.mean[r0:r0 + p], bias_cols=self.m, tag="shift")
+                        C0=a_new[:q], bias=self.mean[r0:r0 + q], bias_cols=self.m, tag="shift")
         else:
-            ops.gemm(g_tt, yc, self.last, alpha=-1.0, beta=1.0, C0=a_new[:p],
-                     bias=self.mean[r0:r0 + p], bias_cols=self.m)
+            ops.gemm(g_tt, yc, self.last, alpha=-1.0, beta=1.0, C0=a_new[:q],
+                     bias=self.mean[r0:r0 + q], bias_cols=self.m)
 
     # ------------------------------------------------------------ readback
     def deviations(self, rows: int | None = None):
@@ -568,8 +659,8 @@ class DeviceSmoother:
         if self.t:  # zero observation rows: the cross moments read them (their gains are zero)
             self._store_rows("Y", 0, ops.zeros(self.t * self.p, self.K))
         if self.pair:
-            self.A_new[:self.p].copy_(anom[self.t * d:self.t * d + self.p])
+            self.A_new[:self.q].copy_(anom[self.t * d:self.t * d + self.q])
         x0_spread = bool(torch.any(anom[:d] != 0).item())
         self.slice0_zero = not x0_spread
-        last = Mdev[self.t * d:self.t * d + self.p]
+        last = Mdev[self.t * d:self.t * d + self.q]
         self.last.copy_(last)

@@ -63,7 +63,8 @@ class DeviceOps:
         return torch.zeros(shape, dtype=dtype or self.dtype, device=self.device)
 
     def to_device(self, arr, dtype=None):
-        return torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype or self.dtype).to(self.device)
+        arr = np.require(arr, requirements=["C", "W"])  # (copies read-only broadcast views)
+        return torch.as_tensor(arr, dtype=dtype or self.dtype).to(self.device)
 
     def _workspace(self, nbytes: int) -> int:
         if nbytes <= 0:
@@ -289,6 +290,21 @@ class DeviceOps:
                   _p(out), _ld(out), g, int(n_members), sub, float(bur.nu), float(bur.dt),
                   float(bur.dx), _p(bur.vmax), _p(bur.flags), _p(wsp) if wsp is not None else None,
                   self._stream())
+
+    def barrier_row(self, bar, S, n, l, m, n_members, eps, out):
+        """out (1 x n_members*m) = softplus(g(S_i)) + sqrt_var * eps_i (engine._Barrier spec)."""
+        self.launches += 1
+        d = n + 2 * l
+        _lib.call("enks_barrier_row", _p(S), _ld(S), d, m, int(n_members), bar.kind,
+                  _p(bar.coef), _ld(bar.coef) if bar.coef is not None else 0, float(bar.c0),
+                  bar.r0, bar.r1, bar.alpha, bar.beta, bar.sqrt_var, _p(eps), _p(out),
+                  self._stream())
+
+    def quad_form(self, E, X, out, scale=1.0, accumulate=False):
+        """out (1-element fp64 device tensor) (+)= scale * sum(E * X)."""
+        self.launches += 1
+        _lib.call("enks_quad_form", _p(E), _ld(E), _p(X), _ld(X), E.shape[0], E.shape[1],
+                  float(scale), _p(out), int(bool(accumulate)), self._stream())
 
     def add(self, a, b, out):
         self.launches += 1

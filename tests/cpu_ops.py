@@ -155,5 +155,24 @@ class CpuOps:
         bur.vmax[0] = max(float(bur.vmax[0]), vmax)
         out.copy_(torch.from_numpy(np.ascontiguousarray(y.transpose(1, 0, 2).reshape(2 * g, -1))))
 
+    def barrier_row(self, bar, S, n, l, m, n_members, eps, out):
+        import math
+
+        d = n + 2 * l
+        Sm = S.numpy().reshape(d, n_members, m)
+        for i in range(n_members):
+            blk = Sm[bar.r0:bar.r1, i, :]
+            if bar.kind == 0:
+                g = float(np.sum(bar.coef.numpy()[bar.r0:bar.r1] * blk)) + bar.c0
+            else:
+                g = float(np.max(np.abs(blk))) + bar.c0
+            z = bar.beta * g
+            clean = z / bar.alpha if z > 30.0 else math.log1p(math.exp(z)) / bar.alpha
+            out[0, i * m:(i + 1) * m] = clean + bar.sqrt_var * float(eps[0, i])
+
+    def quad_form(self, E, X, out, scale=1.0, accumulate=False):
+        v = scale * float((E.double() * X.double()).sum())
+        out[0] = (float(out[0]) if accumulate else 0.0) + v
+
     def sub(self, a, b, out):
         out.copy_(a - b)

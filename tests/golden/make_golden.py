@@ -34,6 +34,8 @@ LINEAR_CASES = [
     ("lin_trackcov", dict(n=4, l=2, m=3), 16, 16, 5, 11, {"track_cov": True}),
     ("lin_colcov7", dict(n=4, l=2, m=3), 7, 16, 3, 4, {"col_cov": 7.0}),
     ("lin_yref_stack", dict(n=5, l=3, m=4), 21, 20, 4, 3, {"yref_stack": True}),
+    ("lin_con_linear", dict(n=4, l=2, m=4), 2, 16, 4, 8, {"constraint": "linear"}),
+    ("lin_con_box", dict(n=4, l=2, m=4), 4, 24, 5, 9, {"constraint": "box"}),
 ]
 NOISE_CASES = [(0, (), (0, 1, 0), (3, 4)), (3, (), (7, 2, 1), (5, 7)), (12345, (7, 2), (1, 4, 2), (8, 33)),
                (2 ** 40 + 5, (1,), (3, 0, 3), (64, 66))]
@@ -85,6 +87,9 @@ def main():
         if "col_cov" in extra:
             vs = ref.virtualsys.build_virtual_system(model, vs.weights,
                                                      shared_col_cov=extra["col_cov"] * np.eye(x0.m))
+        if "constraint" in extra:
+            con = problems.make_constraint(ref, extra["constraint"], x0.n, x0.l, x0.m)
+            vs = ref.virtualsys.build_virtual_system(model, vs.weights, constraint=con)
         y = vs.reference_observation()
         if extra.get("yref_stack"):
             y = np.stack([y + 0.1 * k for k in range(h)])

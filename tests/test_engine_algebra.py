@@ -91,3 +91,29 @@ def test_engine_burgers_equals_oracle_fp64(pm, mode):
     eng = _run(pm, pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, 2)
     assert eng.forecast.kind == "burgers"
     assert np.abs(eng.mean_host().reshape(ref.shape) - ref).max() < 1e-10 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("kind", ["linear", "box"])
+@pytest.mark.parametrize("pair", [False, True])
+def test_engine_constraint_barrier_equals_oracle_fp64(pm, kind, pair):
+    """Barrier observation row (enks.py:201-208): p = n + l + 1 observation rows."""
+    model, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(2), n=4, l=2, m=4)
+    con = problems.make_constraint(pm, kind, x0.n, x0.l, x0.m)
+    vs = pm.virtualsys.build_virtual_system(model, vs.weights, constraint=con)
+    y = vs.reference_observation()
+    ref, _, oens = enks_oracle.oracle_smooth(x0, y, vs, 4, 16, seed=8, backend="c")
+    eng = _run(pm, x0, y, vs, 4, 16, 8, pair=pair)
+    assert eng.p == x0.n + x0.l + 1 and eng.q == x0.n + x0.l
+    mean = eng.mean_host().reshape(ref.shape)
+    assert np.abs(mean - ref).max() < 1e-10 * np.abs(ref).max()
+    members = eng.members_device().numpy().reshape(ref.shape[0] * ref.shape[1], 16, 4)
+    assert np.abs(members.transpose(1, 0, 2) - oens.members).max() < 1e-10 * np.abs(ref).max()
+
+
+def test_engine_rejects_host_only_constraint(pm):
+    model, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(2))
+    con = pm.virtualsys.ConstraintSpec(g=lambda s: float(s.u.sum()))
+    vs = pm.virtualsys.build_virtual_system(model, vs.weights, constraint=con)
+    eng = DeviceSmoother(CpuOps(), x0.packed, x0.n, x0.l, 8, 1.0 / x0.m)
+    with pytest.raises(TypeError, match="LinearConstraint or BoxConstraint"):
+        eng.bind(vs)

@@ -27,12 +27,15 @@ def _case(pm, name):
             if "col_cov" in extra:
                 vs = pm.virtualsys.build_virtual_system(
                     model, vs.weights, shared_col_cov=extra["col_cov"] * np.eye(x0.m))
+            if "constraint" in extra:
+                con = problems.make_constraint(pm, extra["constraint"], x0.n, x0.l, x0.m)
+                vs = pm.virtualsys.build_virtual_system(model, vs.weights, constraint=con)
             return model, vs, x0, N, h, sseed, extra
     raise KeyError(name)
 
 
 NAMES = ["lin_spd_4x2x3", "lin_id_8x4x8", "lin_m1", "lin_scale0_N4", "lin_trackcov", "lin_colcov7",
-         "lin_yref_stack"]
+         "lin_yref_stack", "lin_con_linear", "lin_con_box"]
 
 
 @pytest.mark.parametrize("name", NAMES)

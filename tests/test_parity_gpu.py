@@ -156,3 +156,21 @@ def test_smooth_horizon_burgers_c1a_matches_reference_golden(pm, mode):
     n, l = pr.n, pr.l
     assert _rel(got, gold["mean"]) < TOL
     assert _rel(got[:, n:n + l], gold["mean"][:, n:n + l]) < TOL
+
+
+@pytest.mark.parametrize("name,kind", [("lin_con_linear", "linear"), ("lin_con_box", "box")])
+def test_smooth_horizon_constraint_matches_reference_golden(pm, name, kind):
+    """Barrier row on the device (csrc/barrier.cu) vs the UNMODIFIED reference run."""
+    import os
+
+    from golden.make_golden import LINEAR_CASES
+    from oracle import problems
+    from paper_2410_09663_b200 import enks
+
+    _, kw, seed, N, h, sseed, _ = next(c for c in LINEAR_CASES if c[0] == name)
+    model, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(seed), **kw)
+    con = problems.make_constraint(pm, kind, x0.n, x0.l, x0.m)
+    vs = pm.virtualsys.build_virtual_system(model, vs.weights, constraint=con)
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", name + ".npz"))
+    got, _ = enks.smooth_horizon(x0, gold["y"], vs, h, N, pm.matvar.NoiseStreams(seed=sseed))
+    assert _rel(got, gold["mean"]) < TOL
