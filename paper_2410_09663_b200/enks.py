@@ -184,9 +184,17 @@ def init_ensemble(x0, n_members: int, shared_col_cov: np.ndarray | None = None, 
 
 
 def _cov_product(eng: DeviceSmoother, a, b) -> np.ndarray:
-    """(lam/N) a b^T over all members (K contraction + allreduce), fp64 on host."""
-    out = eng.ops.empty(a.shape[0], b.shape[0])
-    eng.ops.gemm(a, b, out, trans_b=True, alpha=eng.lam / eng.N)
+    """(lam/N) a b^T over all members (K contraction + allreduce), fp64 on host.
+
+    Covariance tracking at scale: for K >= 128 the contraction runs on
+    the tcgen05 fp16-pair kernel (N in 256-column launches), else on the SIMT GEMM."""
+    ops = eng.ops
+    out = ops.empty(a.shape[0], b.shape[0])
+    K = a.shape[1]
+    if hasattr(ops, "gemm_nt_f16pair") and K >= 128 and K % 8 == 0:
+        ops.gemm_nt_f16pair(a, b, out, alpha=eng.lam / eng.N)
+    else:
+        ops.gemm(a, b, out, trans_b=True, alpha=eng.lam / eng.N)
     eng.comm.allreduce_(out)
     return out.double().cpu().numpy()
 

@@ -257,6 +257,24 @@ class DeviceOps:
             ev1.record()
             self.profile.append((tag, ev0, ev1, 2.0 * M * N * K))
 
+    def gemm_nt_f16pair(self, a, b, out, *, alpha=1.0, tag=None):
+        """out (M x N) = alpha a b^T for fp32 a (M x K), b (N x K) on tcgen05: both operands
+        split into fp16-pair planes once, N covered in 256-column launches (any N)."""
+        M, K = a.shape
+        N = b.shape[0]
+        f16 = torch.float16
+        ah, al, sa = self.empty(M, K, dtype=f16), self.empty(M, K, dtype=f16), self.empty(M)
+        self.f16pair_split(a, ah, al, sa)
+        if b is a:
+            bh, bl, sb = ah, al, sa
+        else:
+            bh, bl, sb = self.empty(N, K, dtype=f16), self.empty(N, K, dtype=f16), self.empty(N)
+            self.f16pair_split(b, bh, bl, sb)
+        for j0 in range(0, N, 256):
+            j1 = min(N, j0 + 256)
+            self.gemm_f16pair(ah, al, sa, bh[j0:j1], bl[j0:j1], sb[j0:j1], out[:, j0:j1],
+                              alpha=alpha, tag=tag)
+
     def spd_inverse(self, S, scale, inv, status, jitter):
         p = S.shape[0]
         if getattr(self, "_spd_ws", None) is None or self._spd_ws.numel() < p * p:

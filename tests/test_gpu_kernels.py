@@ -388,3 +388,23 @@ def test_burgers_cfl_and_nonfinite_flags(dev_ops, pm):
         fc.check_cfl()
     with pytest.raises(CflError, match="nu"):
         _burgers_forecaster(dev_ops, pm, g, "boundary", 1, dt=0.5)
+
+
+@pytest.mark.parametrize("M,N,K", [(600, 300, 1024), (77, 513, 4096)])
+def test_gemm_nt_f16pair_blocked_columns(dev_ops, M, N, K):
+    """Covariance-tracking contraction: fp16-pair planes, N > 256 in 256-column launches."""
+    g = torch.Generator().manual_seed(M * N)
+    A = torch.randn(M, K, generator=g)
+    B = torch.randn(N, K, generator=g)
+    C = dev_ops.zeros(M, N)
+    dev_ops.gemm_nt_f16pair(A.to(dev_ops.device), B.to(dev_ops.device), C, alpha=0.25)
+    ref = 0.25 * (A.double() @ B.double().t())
+    scale = 0.25 * (A.double().abs() @ B.double().abs().t())
+    assert ((C.double().cpu() - ref).abs() / scale).max().item() < 1e-6
+    Cs = dev_ops.zeros(M, M)
+    dA = A.to(dev_ops.device)
+    dev_ops.gemm_nt_f16pair(dA, dA, Cs)
+    refs = A.double() @ A.double().t()
+    # Gram diagonals are all-positive sums: the tensor core's truncating TMEM accumulation
+    # within one 256-deep chain biases them by up to ~chain/2 * 2^-24 (see gemm_f16p.cu)
+    assert ((Cs.double().cpu() - refs).abs() / (A.double().abs() @ A.double().abs().t())).max() < 5e-6

@@ -174,3 +174,22 @@ def test_smooth_horizon_constraint_matches_reference_golden(pm, name, kind):
     gold = np.load(os.path.join(os.path.dirname(__file__), "golden", name + ".npz"))
     got, _ = enks.smooth_horizon(x0, gold["y"], vs, h, N, pm.matvar.NoiseStreams(seed=sseed))
     assert _rel(got, gold["mean"]) < TOL
+
+
+def test_track_cov_tensor_core_path_matches_oracle(pm):
+    """C1b-shaped CNN with track_cov: K = N m = 3200 routes the covariance contractions through
+    the fp16-pair tcgen05 kernel in 256-column blocks (T d = 576 > 256)."""
+    from oracle import enks_oracle, problems
+    from oracle.models import OracleCNN
+    from paper_2410_09663_b200 import enks
+
+    pr = problems.make_cnn_problem(pm, "C1", n_members=100, horizon=5)
+    ovs = pm.virtualsys.build_virtual_system(OracleCNN(pr.model), pr.vs.weights)
+    ref, rcov, _ = enks_oracle.oracle_smooth(pr.x0, pr.y_ref, ovs, pr.H, pr.N, seed=4,
+                                             track_cov=True, backend="c")
+    got, cov = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N,
+                                   pm.matvar.NoiseStreams(seed=4), track_cov=True)
+    assert _rel(got, ref) < TOL
+    for k in ("sigma_traj", "sigma_cross", "sigma_pred"):
+        assert getattr(cov, k).shape == getattr(rcov, k).shape
+        assert _rel(getattr(cov, k), getattr(rcov, k)) < TOL, k
