@@ -318,13 +318,41 @@ def run_ours(args):
         traffic_note = {"launch": tj.get("launch"), "algorithmic_bytes": tj.get("algorithmic_bytes"),
                         "source": tj.get("source")}
     roofline = {
-        "kernel": "cross-moment contraction P=[A;Yc]Yc^T (tcgen05 3xTF32, tc_gemm_kernel)",
+        "kernel": "cross-moment contraction P=[A;Yc]Yc^T (tcgen05 kind::f16 on fp16-pair "
+                  "operands, CTA-pair f16p_gemm_pair_kernel)",
         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": achieved / peak, "traffic": traffic, "traffic_capture": traffic_note,
         "peak_source": f"{peak_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)",
         "launches_timed": n_kern, "kernel_share_of_step": kern_s / elapsed,
         "algorithmic_tflop_per_horizon": alg["cross_tflop"],
+        "mma_work_frac": 3.0 * achieved / peak,
+        "note": "achieved counts algorithmic flops (2 M N K); the kernel issues three kind::f16 "
+                "MMAs (lo*hi, hi*lo, hi*hi) per algorithmic product for fp32-level accuracy, so "
+                "the tensor pipe does mma_work_frac of the sustained peak",
     }
+    # per-kernel-family breakdown (CUDA events around every tagged op of the timed region)
+    hbm = float(peaks.get("hbm_gbs", 6536.0))
+    fam = {}
+    for tag, s_, e_, w in prof:
+        t = s_.elapsed_time(e_) / 1e3
+        f = fam.setdefault(tag, [0.0, 0.0, 0])
+        f[0] += t
+        f[1] += w
+        f[2] += 1
+    kinds = {"cross": ("tensor", "TFLOP/s"), "forecast": ("tensor", "TFLOP/s"),
+             "correction": ("tensor", "TFLOP/s"), "gain": ("tensor", "TFLOP/s"),
+             "shift": ("tensor", "TFLOP/s"), "noise": ("hbm", "GB/s"), "stats": ("hbm", "GB/s"),
+             "gain_solve": ("latency", "TFLOP/s")}
+    kernels = {}
+    for tag, (t, w, cnt) in sorted(fam.items(), key=lambda kv: -kv[1][0]):
+        bound, unit = kinds.get(tag, ("?", "?"))
+        rate = w / max(t, 1e-12) / (1e12 if unit == "TFLOP/s" else 1e9)
+        pk = peak if bound == "tensor" else (hbm if bound == "hbm" else None)
+        kernels[tag] = {"ms_per_horizon": t / args.steps * 1e3, "share": t / elapsed,
+                        "launches": cnt // max(args.steps, 1), "achieved": rate, "unit": unit,
+                        "bound": bound, "peak": pk, "frac": (rate / pk) if pk else None}
+    if "forecast" in fam:
+        kernels["forecast"]["member_steps_per_s"] = pr.N * h * args.steps / fam["forecast"][0]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -343,7 +371,7 @@ def run_ours(args):
             "data": "synthetic (sine-field x0, random-init CNN, bit-exact numpy noise streams)",
             "config": _config(pr, args),
             "member_cnn_steps_per_s": pr.N * h * value,
-            "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,
             "cpu_baseline": cpu, "clocks": clk,
             "algorithmic": alg,
         }

@@ -21,7 +21,7 @@ namespace enks {
 bool cnn3_tc_applicable(int n_layers, const int* widths, int rows, int cols);
 int cnn3_tc_forward(const float* weights, const float* biases, float alpha, const float* x,
                     int64_t ldx, const float* u, int64_t ldu, float* out, int64_t ldo, int rows,
-                    int64_t n_members, cudaStream_t st);
+                    int cols, int64_t n_members, cudaStream_t st);
 
 namespace {
 
@@ -172,7 +172,7 @@ int enks_cnn_forward(int n_layers, const int* widths, const float* weights, cons
         const char* e = getenv("ENKS_CNN_TC");
         const bool allow = !(e && e[0] == '0');
         if (allow && cnn3_tc_applicable(n_layers, widths, rows, cols))
-            return cnn3_tc_forward(weights, biases, alpha, x, ldx, u, ldu, out, ldo, rows, n_members,
+            return cnn3_tc_forward(weights, biases, alpha, x, ldx, u, ldu, out, ldo, rows, cols, n_members,
                                    as_stream(stream));
     }
     CnnArgs a;

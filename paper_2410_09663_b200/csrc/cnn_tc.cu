@@ -1,4 +1,4 @@
-// K3 on tcgen05: the 3-layer CNN forecast (widths 2-32-32-1, 128-pixel-wide fields)
+// K3 on tcgen05: the 3-layer CNN forecast (widths 2-32-32-1, fields 32, 64 or 128 pixels wide)
 //     X' = X + alpha * conv3(tanh(conv2(tanh(conv1([X, U])))))
 // with the 32->32 layer (92% of the FLOPs) as 3xTF32 tcgen05 MMAs and the thin
 // first/last layers on the CUDA cores, all fused: HBM sees X, U once and X' once.
@@ -19,6 +19,11 @@
 //   96-column TMEM accumulators form a ring over output rows.  The epilogue
 //   applies bias + tanh, the 32->1 layer (again tap-folded by shuffles), and
 //   the residual.  3xTF32: each MMA triple is lo*hi + hi*lo + hi*hi.
+//
+// Narrow fields: a 128-pixel MMA row carries 128 / seg whole images side by side (seg = image
+// width 32 or 64).  In the member-column layout those are simply the next 128 columns, so the
+// addressing is unchanged; only the horizontal taps are cut at the image boundaries (which
+// fall on warp boundaries), as the zero 'same' padding requires.
 //
 // Warp roles (384 threads): warp 0 = MMA issuer, warp 2 = TMEM allocator,
 // warps 4-7 = layer-1 producer (thread = pixel), warps 8-11 = epilogue
@@ -96,7 +101,9 @@ struct Cnn3Args {
     float* out;
     int64_t ldo;
     int rows;
-    int64_t n_members;
+    int64_t n_members;  // 128-pixel row groups ("virtual members")
+    int64_t cols_total; // n_members_real * seg: columns beyond it are padding
+    int seg;            // image width: 32, 64 or 128
     int debug;  // ENKS_CNN_DEBUG: 1 = no MMAs, 2 = no layer-1 math, 4 = no epilogue math
 };
 
@@ -212,15 +219,17 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     } else if (warp >= 4 && warp < 8) {
         // ================= layer-1 producer: thread = pixel =================
         const int x = threadIdx.x - 128;
+        const int xs = x & (a.seg - 1);  // pixel within its image
         int it = 0;
         for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
             const float* xm = a.x + mem * W;
             const float* um = a.u + mem * W;
+            const bool col_ok = mem * W + x < a.cols_total;
             // input rows are prefetched into registers two rows ahead and written into the
             // 4-slot ring one iteration later, so the global-load latency overlaps a row of work
             auto fetch = [&](int j, float& vx, float& vu) {
-                vx = j < n ? xm[(int64_t)j * a.ldx + x] : 0.f;
-                vu = j < n ? um[(int64_t)j * a.ldu + x] : 0.f;
+                vx = (j < n && col_ok) ? xm[(int64_t)j * a.ldx + x] : 0.f;
+                vu = (j < n && col_ok) ? um[(int64_t)j * a.ldu + x] : 0.f;
             };
             auto put = [&](int j, float vx, float vu) {  // row j into ring slot j & 3
                 float* dst = in_ring + (j & 3) * 2 * kInRow;
@@ -249,8 +258,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                         const int j = r + ky - 1;
                         const bool ok = j >= 0 && j < n;
                         const float* src = in_ring + (j & 3) * 2 * kInRow + ci * kInRow + x;
-#pragma unroll
-                        for (int kx = 0; kx < 3; ++kx) in[ci * 9 + ky * 3 + kx] = ok ? src[kx] : 0.f;
+                        in[ci * 9 + ky * 3 + 0] = (ok && xs != 0) ? src[0] : 0.f;
+                        in[ci * 9 + ky * 3 + 1] = ok ? src[1] : 0.f;
+                        in[ci * 9 + ky * 3 + 2] = (ok && xs != a.seg - 1) ? src[2] : 0.f;
                     }
                 const int Rg = it * n + r;
                 const int slot = Rg % NA;
@@ -299,18 +309,22 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         const int x = ew * 32 + lane;
         const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
         const float b3 = b3s[0];
+        // cross-warp tap exchange only inside an image (seg = 32: never; 64: not across 63|64)
+        const bool xl = ew > 0 && ((ew * 32) & (a.seg - 1)) != 0;
+        const bool xr = ew < 3 && (((ew + 1) * 32) & (a.seg - 1)) != 0;
         int it = 0;
         for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
             float acc3[3] = {0.f, 0.f, 0.f};  // layer-3 partial sums, ring over output rows
             const float* xm = a.x + mem * W;
             float* om = a.out + mem * W;
+            const bool col_ok = mem * W + x < a.cols_total;
             for (int y = 0; y < n; ++y) {
                 const int Yg = it * n + y;
                 const int q = Yg % NACC;
                 const int par = Yg & 1;
                 // residual inputs of the rows completed below, loaded before the waits
-                const float xres_m = y >= 1 ? xm[(int64_t)(y - 1) * a.ldx + x] : 0.f;
-                const float xres_0 = y == n - 1 ? xm[(int64_t)y * a.ldx + x] : 0.f;
+                const float xres_m = (y >= 1 && col_ok) ? xm[(int64_t)(y - 1) * a.ldx + x] : 0.f;
+                const float xres_0 = (y == n - 1 && col_ok) ? xm[(int64_t)y * a.ldx + x] : 0.f;
                 ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / NACC) & 1));
                 ptx::tc_fence_after();
                 if (a.debug & 8) {
@@ -356,14 +370,14 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     if (lane != 31) s[c] += dn;
                 }
                 asm volatile("bar.sync 2, 128;" ::: "memory");
-                if (lane == 0 && ew > 0) {
+                if (lane == 0 && xl) {
 #pragma unroll
                     for (int c = 0; c < 32; c += 4) {
                         const float4 e4 = *reinterpret_cast<const float4*>(xd0 + (par * 4 + ew - 1) * 32 + c);
                         s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
                     }
                 }
-                if (lane == 31 && ew < 3) {
+                if (lane == 31 && xr) {
 #pragma unroll
                     for (int c = 0; c < 32; c += 4) {
                         const float4 e4 = *reinterpret_cast<const float4*>(xd2 + (par * 4 + ew + 1) * 32 + c);
@@ -413,11 +427,11 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     if (lane == 0) xv2[(par * 4 + ew) * 4 + ky] = vv[ky * 3 + 2];
                 }
                 asm volatile("bar.sync 2, 128;" ::: "memory");
-                if (lane == 0 && ew > 0) {
+                if (lane == 0 && xl) {
 #pragma unroll
                     for (int ky = 0; ky < 3; ++ky) tk[ky] += xv0[(par * 4 + ew - 1) * 4 + ky];
                 }
-                if (lane == 31 && ew < 3) {
+                if (lane == 31 && xr) {
 #pragma unroll
                     for (int ky = 0; ky < 3; ++ky) tk[ky] += xv2[(par * 4 + ew + 1) * 4 + ky];
                 }
@@ -428,12 +442,12 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     const int yo = y - 1;
                     const float o = acc3[yo % 3] + tk[2];
                     acc3[yo % 3] = 0.f;
-                    om[(int64_t)yo * a.ldo + x] = xres_m + a.alpha * (b3 + o);
+                    if (col_ok) om[(int64_t)yo * a.ldo + x] = xres_m + a.alpha * (b3 + o);
                 }
                 if (y == n - 1) {
                     const float o = acc3[y % 3];
                     acc3[y % 3] = 0.f;
-                    om[(int64_t)y * a.ldo + x] = xres_0 + a.alpha * (b3 + o);
+                    if (col_ok) om[(int64_t)y * a.ldo + x] = xres_0 + a.alpha * (b3 + o);
                 }
             }
         }
@@ -447,12 +461,12 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
 
 bool cnn3_tc_applicable(int n_layers, const int* widths, int rows, int cols) {
     return n_layers == 3 && widths[0] == 2 && widths[1] == C1 && widths[2] == C2 &&
-           widths[3] == 1 && cols == W && rows >= 2;
+           widths[3] == 1 && (cols == 32 || cols == 64 || cols == W) && rows >= 2;
 }
 
 int cnn3_tc_forward(const float* weights, const float* biases, float alpha, const float* x,
                     int64_t ldx, const float* u, int64_t ldu, float* out, int64_t ldo, int rows,
-                    int64_t n_members, cudaStream_t st) {
+                    int cols, int64_t n_members, cudaStream_t st) {
     Cnn3Args a;
     a.w1 = weights;
     a.w2 = weights + C1 * 2 * 9;
@@ -463,7 +477,10 @@ int cnn3_tc_forward(const float* weights, const float* biases, float alpha, cons
     a.alpha = alpha;
     a.x = x; a.ldx = ldx; a.u = u; a.ldu = ldu; a.out = out; a.ldo = ldo;
     a.rows = rows;
-    a.n_members = n_members;
+    a.seg = cols;
+    a.cols_total = n_members * cols;
+    a.n_members = (a.cols_total + W - 1) / W;
+    n_members = a.n_members;
     {
         const char* e = getenv("ENKS_CNN_DEBUG");
         a.debug = e ? atoi(e) : 0;

@@ -11,6 +11,7 @@ passed as the leading dimension.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import numpy as np
@@ -83,11 +84,31 @@ class DeviceOps:
     def _stream() -> int:
         return torch.cuda.current_stream().cuda_stream
 
+    @contextlib.contextmanager
+    def _prof(self, tag, work):
+        """CUDA-event bracket of one op when profiling (bench): (tag, ev0, ev1, work)."""
+        if self.profile is None:
+            yield
+            return
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        yield
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev1.record()
+        self.profile.append((tag, ev0, ev1, float(work)))
+
     # -- kernels ----------------------------------------------------------
     def noise_fill(self, head, t, ch, member0, n_members, rows, cols, diag=None, out=None,
                    base=None, out_plus=None):
         words = (ctypes.c_uint32 * len(head))(*[int(w) for w in head])
         self.launches += 1
+        nb = 4 * rows * cols * n_members * ((out is not None) + 2 * (out_plus is not None))
+        with self._prof("noise", nb):
+            self._noise_fill(words, head, t, ch, member0, n_members, rows, cols, diag, out, base,
+                             out_plus)
+
+    def _noise_fill(self, words, head, t, ch, member0, n_members, rows, cols, diag, out, base,
+                    out_plus):
         _lib.call("enks_noise_fill", words, len(head), int(t), int(ch), int(member0),
                   int(n_members), int(rows), int(cols), _p(diag), _p(out),
                   _ld(out) if out is not None else 0, _p(base),
@@ -103,6 +124,13 @@ class DeviceOps:
         i64 = ctypes.c_int64 * n
         get = lambda k: [j.get(k) for j in jobs]  # noqa: E731
         self.launches += 1
+        nb = sum(4 * j["rows"] * cols * n_members * ((j.get("out") is not None)
+                                                      + 2 * (j.get("out_plus") is not None))
+                 for j in jobs)
+        with self._prof("noise", nb):
+            self._noise_multi(words, head, member0, n_members, cols, n, u32, vp, i64, get, jobs)
+
+    def _noise_multi(self, words, head, member0, n_members, cols, n, u32, vp, i64, get, jobs):
         _lib.call("enks_noise_fill_multi", words, len(head), int(member0), int(n_members), int(cols),
                   n, u32(*[int(j["t"]) for j in jobs]), u32(*[int(j["ch"]) for j in jobs]),
                   (ctypes.c_int * n)(*[int(j["rows"]) for j in jobs]),
@@ -119,8 +147,9 @@ class DeviceOps:
         nbytes = self.lib.enks_member_sum_ws_bytes(rows, n_members, cols)
         ws = self._workspace_sum(nbytes)
         self.launches += 2
-        _lib.call("enks_member_sum", _p(src), _ld(src), rows, int(n_members), int(cols), _p(z0),
-                  _p(acc), _p(amax), ws, self._stream())
+        with self._prof("stats", 4 * rows * n_members * cols):
+            _lib.call("enks_member_sum", _p(src), _ld(src), rows, int(n_members), int(cols),
+                      _p(z0), _p(acc), _p(amax), ws, self._stream())
 
     def member_center_f16pair(self, src, n_members, cols, z0, acc, amax, n_total, mean, h, l,
                               inv_scale, f32=None, rows_f32=0):
@@ -128,10 +157,12 @@ class DeviceOps:
         if getattr(self, "_scale_ws", None) is None or self._scale_ws.numel() < rows:
             self._scale_ws = torch.empty(max(rows, 4096), dtype=torch.float32, device=self.device)
         self.launches += 2
-        _lib.call("enks_member_center_f16pair", _p(src), _ld(src), rows, int(n_members), int(cols),
-                  _p(z0), _p(acc), _p(amax), int(n_total), _p(mean), _p(h), _p(l), _ld(h),
-                  _p(inv_scale), _p(self._scale_ws), _p(f32), _ld(f32) if f32 is not None else 0,
-                  int(rows_f32), self._stream())
+        K = n_members * cols
+        with self._prof("stats", 8 * rows * K + 4 * rows_f32 * K):
+            _lib.call("enks_member_center_f16pair", _p(src), _ld(src), rows, int(n_members),
+                      int(cols), _p(z0), _p(acc), _p(amax), int(n_total), _p(mean), _p(h), _p(l),
+                      _ld(h), _p(inv_scale), _p(self._scale_ws), _p(f32),
+                      _ld(f32) if f32 is not None else 0, int(rows_f32), self._stream())
 
     def member_center(self, src, n_members, cols, z0, acc, n_total, mean=None, anom=None):
         rows = src.shape[0]
@@ -280,6 +311,10 @@ class DeviceOps:
         if getattr(self, "_spd_ws", None) is None or self._spd_ws.numel() < p * p:
             self._spd_ws = torch.empty(p * p, dtype=torch.float32, device=self.device)
         self.launches += 2
+        with self._prof("gain_solve", p ** 3 * (1.0 / 3 + 1.0 / 3 + 1.0)):
+            self._spd(S, p, scale, inv, status, jitter)
+
+    def _spd(self, S, p, scale, inv, status, jitter):
         _lib.call("enks_spd_inverse", _p(S), _ld(S), p, float(scale), _p(inv), _p(self._spd_ws),
                   _p(status), _p(jitter), self._stream())
 
@@ -289,9 +324,12 @@ class DeviceOps:
     def cnn_forward(self, cnn, x, u, out, n_members):
         widths = (ctypes.c_int * len(cnn.widths))(*cnn.widths)
         self.launches += 1
-        _lib.call("enks_cnn_forward", cnn.n_layers, widths, _p(cnn.w_dev), _p(cnn.b_dev),
-                  float(cnn.alpha), _p(x), _ld(x), _p(u), _ld(u), _p(out), _ld(out),
-                  int(x.shape[0]), int(cnn.cols), int(n_members), self._stream())
+        flops = n_members * x.shape[0] * cnn.cols * sum(
+            18 * a * b for a, b in zip(cnn.widths[:-1], cnn.widths[1:]))
+        with self._prof("forecast", flops):
+            _lib.call("enks_cnn_forward", cnn.n_layers, widths, _p(cnn.w_dev), _p(cnn.b_dev),
+                      float(cnn.alpha), _p(x), _ld(x), _p(u), _ld(u), _p(out), _ld(out),
+                      int(x.shape[0]), int(cnn.cols), int(n_members), self._stream())
 
     def burgers_forward(self, bur, x, u, out, n_members):
         """bur: engine.Forecaster of kind 'burgers' (grid, solver constants, vmax/flags)."""

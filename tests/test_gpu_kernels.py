@@ -209,22 +209,27 @@ def test_gemm_nt_tc_3xtf32(dev_ops, M, N, K, split):
     assert err < max(3 * err2, 1e-6), (err, err2)
 
 
-@pytest.mark.parametrize("rows,N", [(128, 3), (40, 5)])
-def test_cnn_forward_tcgen05_vs_oracle(dev_ops, pm, rows, N):
-    """The fused tcgen05 conv (widths 2-32-32-1, 128-wide fields) against the fp64 oracle."""
+@pytest.mark.parametrize("rows,cols,N", [(128, 128, 3), (40, 128, 5), (64, 64, 3), (64, 64, 8),
+                                         (32, 32, 5), (20, 32, 4), (17, 64, 1)])
+def test_cnn_forward_tcgen05_vs_oracle(dev_ops, pm, rows, cols, N):
+    """The fused tcgen05 conv (widths 2-32-32-1) against the fp64 oracle; 32- and 64-wide
+    fields pack 4 / 2 images per 128-pixel MMA row (odd N leaves padding columns)."""
     from oracle.models import cnn_step
     from paper_2410_09663_b200.engine import Forecaster
 
-    model = pm.dynamics.CNNDynamics(rows=rows, cols=128, widths=(2, 32, 32, 1), seed=3)
+    model = pm.dynamics.CNNDynamics(rows=rows, cols=cols, widths=(2, 32, 32, 1), seed=3)
     model.state_rows = model.input_rows = rows
     rng = np.random.default_rng(rows)
-    x = rng.standard_normal((N, rows, 128))
-    u = rng.standard_normal((N, rows, 128))
+    x = rng.standard_normal((N, rows, cols))
+    u = rng.standard_normal((N, rows, cols))
     ref = cnn_step(x, u, model.weights, model.biases, model.alpha)
     last = dev_ops.to_device(np.concatenate([x, u], axis=1).transpose(1, 0, 2).reshape(2 * rows, -1))
-    out = dev_ops.zeros(rows, N * 128)
+    full = dev_ops.zeros(rows, N * cols + 64)
+    full.fill_(7.0)  # sentinel: the padding columns of a partly filled MMA row are never written
+    out = full[:, :N * cols]
     Forecaster(model, dev_ops, rows, rows)(dev_ops, last, out, rows, N)
-    got = _cpu(out).reshape(rows, N, 128).transpose(1, 0, 2)
+    assert bool((full[:, N * cols:] == 7.0).all())
+    got = _cpu(out).reshape(rows, N, cols).transpose(1, 0, 2)
     np.testing.assert_allclose(got, ref, rtol=1e-5, atol=2e-6)
 
 
