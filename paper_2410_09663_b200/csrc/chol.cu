@@ -14,13 +14,15 @@
 // updates run one warp per tile (lane = column, conflict-free 33-float
 // stride).  L^{-1} is formed tile-row by tile-row the same way and stored
 // densely; L^{-T} L^{-1} is one small GEMM.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "gemm.cuh"
 
 namespace enks {
 namespace {
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTS = 32;              // tile size
 constexpr int kLd = 33;              // padded tile row stride (floats)
@@ -46,9 +48,11 @@ __device__ bool factor_diag(float* T, int lane) {
         if (lane > k) a[k] *= inv;
         // trailing: a[i][j] -= l_ik l_jk for k < j <= i
 #pragma unroll
-        for (int j = k + 1; j < kTS; ++j) {
-            const float ljk = __shfl_sync(0xffffffffu, a[k], j);
-            if (lane >= j) a[j] = fmaf(-a[k], ljk, a[j]);
+        for (int j = 1; j < kTS; ++j) {
+            if (j > k) {  // constant trip count: full unroll keeps a[] in registers
+                const float ljk = __shfl_sync(0xffffffffu, a[k], j);
+                if (lane >= j) a[j] = fmaf(-a[k], ljk, a[j]);
+            }
         }
     }
 #pragma unroll
@@ -104,14 +108,13 @@ __device__ void invert_diag(float* T, int lane) {
 
 __global__ void __launch_bounds__(kThreads)
     spd_inverse_kernel(const float* __restrict__ S, int64_t lds, int p, float scale,
-                       float* __restrict__ linv, int* status, int* jitter_events) {
+                       float* __restrict__ linv, int* status, int* jitter_events, int debug) {
     extern __shared__ float sm[];
     float* Lt = sm;                           // lower tile-triangle of L
     __shared__ int s_fail;
     __shared__ double s_trace_part[kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nb = (p + kTS - 1) / kTS;
-    const int P = nb * kTS;
     const int n_tiles = nb * (nb + 1) / 2;
 
     {   // trace (parallel, fp64)
@@ -128,21 +131,37 @@ __global__ void __launch_bounds__(kThreads)
     int failed = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         const float jitter = attempt == 0 ? 0.f : (float)(1e-9 * trace / (double)p + 1e-30);
-        // load sym(S) (+ jitter I); padding rows/cols = identity
-        for (int e = tid; e < P * P; e += kThreads) {
-            const int i = e / P, j = e - i * P;
-            if (j > i) continue;
-            float v;
-            if (i < p && j < p)
-                v = scale * (0.5f * (S[(int64_t)i * lds + j] + S[(int64_t)j * lds + i])) +
-                    (i == j ? jitter : 0.f);
-            else
-                v = (i == j) ? 1.f : 0.f;
-            Lt[tix(i / kTS, j / kTS) * kTile + (i % kTS) * kLd + (j % kTS)] = v;
+        // load sym(S) (+ jitter I) tile by tile with coalesced rows: tile (I, J) gets
+        // 0.5 scale S[I-block][J-block] row-wise, then += 0.5 scale S[J-block][I-block]^T
+        // (also read row-wise, written transposed: stride 33 keeps it conflict-free);
+        // padding rows/cols = identity
+        for (int q = warp; q < n_tiles; q += kWarps) {
+            int I = 0;
+            while ((I + 1) * (I + 2) / 2 <= q) ++I;
+            const int J = q - I * (I + 1) / 2;
+            float* T = Lt + q * kTile;
+            const float hs = 0.5f * scale;
+            const int cj = J * kTS + lane, ci = I * kTS + lane;
+            for (int r = 0; r < kTS; ++r) {
+                const int ri = I * kTS + r;
+                T[r * kLd + lane] = (ri < p && cj < p) ? hs * S[(int64_t)ri * lds + cj] : 0.f;
+            }
+            __syncwarp();
+            for (int r = 0; r < kTS; ++r) {
+                const int rj = J * kTS + r;
+                const float v = (rj < p && ci < p) ? hs * S[(int64_t)rj * lds + ci] : 0.f;
+                T[lane * kLd + r] += v;  // element (I*32 + lane, J*32 + r)
+            }
+            __syncwarp();
+            if (I == J) {
+                const int gi = I * kTS + lane;
+                T[lane * kLd + lane] = gi < p ? T[lane * kLd + lane] + jitter : 1.f;
+            }
         }
+        __syncthreads();
         if (tid == 0) s_fail = 0;
         __syncthreads();
-        for (int K = 0; K < nb; ++K) {
+        for (int K = 0; K < ((debug & 2) ? 0 : nb); ++K) {
             if (warp == 0) {
                 const bool ok = factor_diag(Lt + tix(K, K) * kTile, lane);
                 if (lane == 0 && !ok) s_fail = 1;
@@ -179,7 +198,7 @@ __global__ void __launch_bounds__(kThreads)
     // L^{-1}, tile row by tile row: Linv_II = L_II^{-1};
     // Linv_IJ = -Linv_II * sum_{K=J}^{I-1} L_IK Linv_KJ   (J < I), written over L_IJ.
     // Row I needs Linv tiles of rows < I (already inverted) and L_IK (K < I, still L).
-    for (int I = 0; I < nb; ++I) {
+    for (int I = 0; I < ((debug & 1) ? 0 : nb); ++I) {
         if (warp == 0) invert_diag(Lt + tix(I, I) * kTile, lane);
         __syncthreads();
         // for each J < I (one warp per J): acc = sum_K L_IK Linv_KJ, then Linv_IJ = -Linv_II acc.
@@ -198,7 +217,7 @@ __global__ void __launch_bounds__(kThreads)
                 float b[kTS];  // column `lane` of B
 #pragma unroll
                 for (int k = 0; k < kTS; ++k) b[k] = B[k * kLd + lane];
-#pragma unroll 4
+#pragma unroll
                 for (int r = 0; r < kTS; ++r) {
                     float acc = 0.f;
 #pragma unroll
@@ -222,12 +241,49 @@ __global__ void __launch_bounds__(kThreads)
         }
         __syncthreads();
     }
-    // dense L^{-1} (zeros above the diagonal, p x p)
-    for (int e = tid; e < p * p; e += kThreads) {
-        const int i = e / p, j = e - i * p;
-        linv[e] = (j <= i) ? Lt[tix(i / kTS, j / kTS) * kTile + (i % kTS) * kLd + (j % kTS)] : 0.f;
+    // dense L^{-1} (zeros above the diagonal, p x p), tile rows written coalesced
+    for (int q = warp; q < nb * nb; q += kWarps) {
+        const int I = q / nb, J = q - (q / nb) * nb;
+        const int c = J * kTS + lane;
+        for (int r = 0; r < kTS; ++r) {
+            const int i = I * kTS + r;
+            if (i >= p || c >= p) continue;
+            linv[(int64_t)i * p + c] = (J < I || (J == I && lane <= r))
+                                           ? Lt[tix(I, J) * kTile + r * kLd + lane] : 0.f;
+        }
     }
     (void)n_tiles;
+}
+
+// inv = L^{-T} L^{-1}: inv[i][j] = sum_{k >= max(i, j)} Linv[k][i] Linv[k][j]; one CTA per
+// 32 x 32 output tile, K staged through shared memory in 32-row slabs (coalesced rows)
+__global__ void __launch_bounds__(256) ltl_kernel(const float* __restrict__ linv, int p,
+                                                  float* __restrict__ inv) {
+    __shared__ float a[kTS][kTS + 1], b[kTS][kTS + 1];
+    const int I = blockIdx.y, J = blockIdx.x;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 4 outputs per thread
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int k0 = max(I, J) * kTS;
+    for (int kb = k0; kb < p; kb += kTS) {
+        for (int r = ty; r < kTS; r += 8) {
+            const int k = kb + r;
+            a[r][tx] = (k < p && I * kTS + tx < p) ? linv[(int64_t)k * p + I * kTS + tx] : 0.f;
+            b[r][tx] = (k < p && J * kTS + tx < p) ? linv[(int64_t)k * p + J * kTS + tx] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < kTS; ++k) {
+            const float bv = b[k][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fmaf(a[k][ty * 4 + q], bv, acc[q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = I * kTS + ty * 4 + q, j = J * kTS + tx;
+        if (i < p && j < p) inv[(int64_t)i * p + j] = acc[q];
+    }
 }
 
 }  // namespace
@@ -256,13 +312,19 @@ int enks_spd_inverse(const float* S, int64_t lds, int p, float scale, float* inv
         configured = smem;
     }
     cudaStream_t st = enks::as_stream(stream);
+    static int debug = -1;
+    if (debug < 0) {
+        const char* e = getenv("ENKS_SPD_DEBUG");
+        debug = e ? atoi(e) : 0;
+    }
     enks::spd_inverse_kernel<<<1, enks::kThreads, smem, st>>>(S, lds, p, scale, ws, status,
-                                                              jitter_events);
+                                                              jitter_events, debug);
     int rc = enks::check_launch("enks_spd_inverse");
-    if (rc) return rc;
-    // Sy^{-1} = L^{-T} L^{-1}: one small GEMM (A = L^{-1} read transposed)
-    return enks::gemm_simt(1, 0, p, p, p, 1.f, ws, p, ws, p, 0.f, nullptr, 0, nullptr, 0, 1, inv,
-                           p, 0, 0, 1, nullptr, st);
+    if (rc || (debug & 4)) return rc;
+    // Sy^{-1} = L^{-T} L^{-1}: one CTA per 32 x 32 output tile
+    const dim3 grid((unsigned)nb, (unsigned)nb);
+    enks::ltl_kernel<<<grid, 256, 0, st>>>(ws, p, inv);
+    return enks::check_launch("enks_spd_inverse(ltl)");
 }
 
 }  // extern "C"

@@ -421,6 +421,28 @@ class DeviceSmoother:
         self._bound = vs
 
     # ------------------------------------------------------------ helpers
+    def _side_stream(self):
+        """Second CUDA stream for the gain solve (None off-GPU)."""
+        if getattr(self.ops, "device", None) is None or self.ops.device.type != "cuda":
+            return None
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.ops.device)
+        return self._side
+
+    def _spd_async(self, side, S, scale) -> None:
+        """Sigma_y^{-1} with the reference's jitter fallback (enks.py:234-244), on `side`
+        after everything queued so far on the main stream."""
+        if side is None:
+            self.ops.spd_inverse(S, scale, self.sinv, self.status, self.jitter)
+            return
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.ops.spd_inverse(S, scale, self.sinv, self.status, self.jitter)
+
+    def _join_side(self, side) -> None:
+        if side is not None:
+            torch.cuda.current_stream().wait_stream(side)
+
     def _barrier_row(self, head, t) -> None:
         """Observation row q: softplus(g(slice_i)) + sqrt(var) eps_i, eps_i the first draw of
         substream (i, t, CH_EPS)  (enks.py:201-208, virtualsys.py:289-302)."""
@@ -547,25 +569,37 @@ class DeviceSmoother:
         a0 = d if self.slice0_zero else 0
         rows_a = (tau + 1) * d
         PA, PY = self.PA[a0:rows_a], self.PY[:tau * p]
+        scale = self.lam / self.N
+        side = self._side_stream()
         if self.pair:
             yb = slice((tau - 1) * p, tau * p)
+            yh, yl, yi = self.Yh[yb], self.Yl[yb], self.y_inv[yb]
+            # Sigma_y block first, so the gain solve (one SM, latency-bound) overlaps the big
+            # contraction on a second stream (enks.py:234-246)
+            ops.gemm_f16pair(yh, yl, yi, yh, yl, yi, PY[(tau - 1) * p:], tag="cross")
+            comm.allreduce_(PY[(tau - 1) * p:])
+            self._spd_async(side, PY[(tau - 1) * p:], scale)
             ops.gemm_f16pair(self.Ah[a0:rows_a], self.Al[a0:rows_a], self.a_inv[a0:rows_a],
-                             self.Yh[yb], self.Yl[yb], self.y_inv[yb], PA, tag="cross")
-            ops.gemm_f16pair(self.Yh[:tau * p], self.Yl[:tau * p], self.y_inv[:tau * p],
-                             self.Yh[yb], self.Yl[yb], self.y_inv[yb], PY, tag="cross")
-        elif self.use_tc:
-            ops.tf32_split(yc, self.yc_hi, self.yc_lo)
-            ops.gemm_nt_tc(self.Abuf[a0:rows_a], self.yc_hi, self.yc_lo, PA, tag="cross")
-            ops.gemm_nt_tc(self.Ybuf[:tau * p], self.yc_hi, self.yc_lo, PY, tag="cross")
+                             yh, yl, yi, PA, tag="cross")
+            if tau > 1:
+                ops.gemm_f16pair(self.Yh[:(tau - 1) * p], self.Yl[:(tau - 1) * p],
+                                 self.y_inv[:(tau - 1) * p], yh, yl, yi, PY[:(tau - 1) * p],
+                                 tag="cross")
+                comm.allreduce_(PY[:(tau - 1) * p])
+            comm.allreduce_(PA)
         else:
-            ops.gemm(self.Abuf[a0:rows_a], yc, PA, trans_b=True, tag="cross")
-            ops.gemm(self.Ybuf[:tau * p], yc, PY, trans_b=True, tag="cross")
-        comm.allreduce_(PA)
-        comm.allreduce_(PY)
+            if self.use_tc:
+                ops.tf32_split(yc, self.yc_hi, self.yc_lo)
+                ops.gemm_nt_tc(self.Abuf[a0:rows_a], self.yc_hi, self.yc_lo, PA, tag="cross")
+                ops.gemm_nt_tc(self.Ybuf[:tau * p], self.yc_hi, self.yc_lo, PY, tag="cross")
+            else:
+                ops.gemm(self.Abuf[a0:rows_a], yc, PA, trans_b=True, tag="cross")
+                ops.gemm(self.Ybuf[:tau * p], yc, PY, trans_b=True, tag="cross")
+            comm.allreduce_(PA)
+            comm.allreduce_(PY)
+            # Sigma_y^{-1} with the reference's jitter fallback (enks.py:234-244)
+            self._spd_async(None, PY[(tau - 1) * p:], scale)
 
-        # Sigma_y^{-1} with the reference's jitter fallback (enks.py:234-244)
-        scale = self.lam / self.N
-        ops.spd_inverse(PY[(tau - 1) * p:], scale, self.sinv, self.status, self.jitter)
         # S_s = P_{A_s} - sum_{tau' < tau} G_{tau',s} P_{Yc_tau'}  (block upper-triangular G)
         tri = (d, p) if a0 == d else (0, 0)
         gcol = self.G[a0:rows_a, (tau - 1) * p:tau * p]
@@ -579,12 +613,14 @@ class DeviceSmoother:
                 ops.gemm_tc(self.G[a0:rows_a, :kk], pth, ptl, PA, alpha=-1.0, beta=1.0, C0=PA,
                             tri=tri, tag="correction")
             # G_{tau,s} = (lam/N) S_s Sigma_y^{-1}
+            self._join_side(side)
             ops.tf32_split(self.sinv, self.sinvT_hi, self.sinvT_lo, transpose=True)
             ops.gemm_tc(PA, self.sinvT_hi, self.sinvT_lo, gcol, alpha=scale, tag="gain")
         else:
             if tau > 1:
                 ops.gemm(self.G[a0:rows_a, :(tau - 1) * p], self.PY[:(tau - 1) * p], PA,
                          alpha=-1.0, beta=1.0, C0=PA, tri=tri)
+            self._join_side(side)
             ops.gemm(PA, self.sinv, gcol, alpha=scale)
         # mean_s += G_{tau,s} (y_ref - y_bar)   (enks.py:247-248 on the mean)
         self.n_upd = tau
