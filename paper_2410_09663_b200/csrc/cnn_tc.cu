@@ -73,18 +73,31 @@ __device__ __forceinline__ uint32_t sw128(int row, int byte) {
     return (uint32_t)(row * 128 + ((((byte >> 4) ^ (row & 7)) << 4) | (byte & 15)));
 }
 
-// tanh(x) = 1 - 2 / (1 + e^{2x}) with one SFU op (ex2) and a Newton reciprocal on the FMA
-// pipe (the SFU is the scarce unit: 64 tanh per pixel-row across layers 1 and 2).
-__device__ __forceinline__ float tanh_fast(float x) {
+// tanh(x) = 1 - 2 / (1 + e^{2x}): ex2.approx and rcp.approx on the SFU (~2^-22 relative
+// each), so |error| ~ 1e-7 absolute; ENKS_CNN_TANH=1 selects the FMA-pipe Newton reciprocal
+// (one SFU op per tanh) instead -- the kernel is issue-bound, so fewer instructions win.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+template <bool NEWTON>
+__device__ __forceinline__ float tanh_fast_t(float x) {
     x = fminf(fmaxf(x, -15.f), 15.f);
     const float t = exp2f_approx(x * 2.8853900817779268f);  // e^{2x}
     const float d = 1.f + t;
-    float r = __int_as_float(0x7EF311C3 - __float_as_int(d));
-    r = r * fmaf(-d, r, 2.f);
-    r = r * fmaf(-d, r, 2.f);
-    r = r * fmaf(-d, r, 2.f);
+    float r;
+    if (NEWTON) {
+        r = __int_as_float(0x7EF311C3 - __float_as_int(d));
+        r = r * fmaf(-d, r, 2.f);
+        r = r * fmaf(-d, r, 2.f);
+        r = r * fmaf(-d, r, 2.f);
+    } else {
+        r = rcp_approx(d);
+    }
     return fmaf(-2.f, r, 1.f);
 }
+#define tanh_fast tanh_fast_t<false>
 
 struct Cnn3Args {
     const float* w1;  // (C1, 2, 3, 3)
