@@ -189,6 +189,22 @@ int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* 
  * Runs on one CTA in shared memory; p <= enks_spd_max_p().  `ws`: p*p floats.
  * status / jitter_events are device ints (no host sync).
  */
+/*
+ * Fused-epilogue variant (no split-K), any N (256-column tiles):
+ * C = alpha diag(inv_sa) (Ah + Al)(Bh + Bl)^T diag(inv_sb) + beta C0 + bias[:, c % bias_cols].
+ * Used for the newest-slice shift last = mean + A_tau - G_tt Yc_tau (enks.py:247 restricted to
+ * the newest slice) with B = Yc_tau^T planes from enks_f16pair_transpose (rows <= 256 source
+ * rows re-split into K-major transposed planes with per-output-row scales).
+ */
+int enks_gemm_f16pair_ex(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah,
+                         const void* Al, int64_t lda, const float* inv_sa, const void* Bh,
+                         const void* Bl, int64_t ldb, const float* inv_sb, float beta,
+                         const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias,
+                         int bias_cols, float* C, int64_t ldc, void* stream);
+int enks_f16pair_transpose(const void* h, const void* l, int64_t ldi, const float* inv_src,
+                           int rows, int64_t cols, void* oh, void* ol, int64_t ldo, float* inv_out,
+                           void* stream);
+
 int enks_spd_max_p(void);
 int enks_spd_inverse(const float* S, int64_t lds, int p, float scale, float* inv, float* ws,
                      int* status, int* jitter_events, void* stream);

@@ -56,7 +56,63 @@ struct P16 {
     int stages;
     int chain;
     int products;  // 3: lh + hl + hh;  2: hl + hh (A's low plane not read)
+    // fused epilogue terms (split == 1 only): + beta * C0[r, c] + bias[r, c % bias_cols]
+    float beta;
+    const float* c0;
+    int64_t ldc0;
+    const float* bias;
+    int64_t ld_bias;
+    int bias_cols;
 };
+
+// epilogue of one thread: row r, columns c_first .. c_first + ncol (ncol <= NC)
+template <int NC>
+__device__ __forceinline__ void f16p_store_row(const P16& p, int split, int64_t r, int64_t c_first,
+                                               int ncol, const float (&acc)[NC]) {
+    const float sa = p.alpha * p.inv_sa[r];
+    float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + c_first;
+    if (!p.c0 && !p.bias) {
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+            if (j < ncol) orow[j] = acc[j] * sa * p.inv_sb[c_first + j];
+        return;
+    }
+    const float* crow = p.c0 ? p.c0 + r * p.ldc0 + c_first : nullptr;
+    const float* brow = p.bias ? p.bias + r * p.ld_bias : nullptr;
+    const bool vec = ncol == NC && (((uintptr_t)orow | (uintptr_t)(crow ? crow : orow)) & 15) == 0 &&
+                     (!brow || ((c_first % p.bias_cols) + NC <= p.bias_cols &&
+                                (((uintptr_t)(brow + c_first % p.bias_cols)) & 15) == 0));
+    if (vec) {  // float4 loads / stores: 128 consecutive columns per thread
+        const float* bb = brow ? brow + c_first % p.bias_cols : nullptr;
+#pragma unroll
+        for (int j = 0; j < NC; j += 4) {
+            float4 o;
+            o.x = acc[j] * sa * p.inv_sb[c_first + j];
+            o.y = acc[j + 1] * sa * p.inv_sb[c_first + j + 1];
+            o.z = acc[j + 2] * sa * p.inv_sb[c_first + j + 2];
+            o.w = acc[j + 3] * sa * p.inv_sb[c_first + j + 3];
+            if (crow) {
+                const float4 c = __ldg(reinterpret_cast<const float4*>(crow + j));
+                o.x += p.beta * c.x; o.y += p.beta * c.y; o.z += p.beta * c.z; o.w += p.beta * c.w;
+            }
+            if (bb) {
+                const float4 b = __ldg(reinterpret_cast<const float4*>(bb + j));
+                o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+            }
+            *reinterpret_cast<float4*>(orow + j) = o;
+        }
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        if (j < ncol) {
+            float v = acc[j] * sa * p.inv_sb[c_first + j];
+            if (crow) v += p.beta * crow[j];
+            if (brow) v += brow[(c_first + j) % p.bias_cols];
+            orow[j] = v;
+        }
+    }
+}
 
 __device__ __forceinline__ uint64_t desc_sw64(const void* smem) {
     const uint64_t addr = ptx::smem_u32(smem);
@@ -212,14 +268,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const int64_t r = row0 + erow;
             const int64_t c_first = col0 + wg * L::kColsPerWG;
-            if (r < p.M && c_first < p.N) {
-                const float sa = p.alpha * p.inv_sa[r];
-                float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + c_first;
-                const int ncol = (int)min((int64_t)L::kColsPerWG, p.N - c_first);
-#pragma unroll
-                for (int j = 0; j < L::kColsPerWG; ++j)
-                    if (j < ncol) orow[j] = acc[j] * sa * p.inv_sb[c_first + j];
-            }
+            if (r < p.M && c_first < p.N)
+                f16p_store_row(p, split, r, c_first, (int)min((int64_t)L::kColsPerWG, p.N - c_first),
+                               acc);
         }
     }
     ptx::tc_fence_before();
@@ -274,6 +325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t rank = ptx::cluster_ctarank();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * BM;
+    const int64_t col0 = (int64_t)blockIdx.y * 256;
     const int split = blockIdx.z;
     const int total_chunks = (int)((p.K + KC - 1) / KC);
     const int cps = (total_chunks + p.splits - 1) / p.splits;
@@ -312,7 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            const int32_t brow = (int32_t)(rank * 128);
+            const int32_t brow = (int32_t)(col0 + rank * 128);
             for (int i = 0; i < n_chunks; ++i) {
                 const int s = i % S;
                 ptx::mbar_wait_bounded(&empty[s], (uint32_t)(((i / S) & 1) ^ 1));
@@ -383,15 +435,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (lane == 0) ptx::mbar_arrive_cluster(&tempty[slot], 0);
         }
         const int64_t r = row0 + erow;
-        const int64_t c_first = (int64_t)wg * kCols;
-        if (r < p.M && c_first < p.N) {
-            const float sa = p.alpha * p.inv_sa[r];
-            float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + c_first;
-            const int ncol = (int)min((int64_t)kCols, p.N - c_first);
-#pragma unroll
-            for (int j = 0; j < kCols; ++j)
-                if (j < ncol) orow[j] = acc[j] * sa * p.inv_sb[c_first + j];
-        }
+        const int64_t c_first = col0 + (int64_t)wg * kCols;
+        if (r < p.M && c_first < p.N)
+            f16p_store_row(p, split, r, c_first, (int)min((int64_t)kCols, p.N - c_first), acc);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -431,6 +477,56 @@ __global__ void __launch_bounds__(256) f16pair_split_kernel(const float* __restr
         const __half hv = __float2half_rn(v);
         hr[k] = hv;
         lr[k] = __float2half_rn(v - __half2float(hv));
+    }
+}
+
+// Transposed re-split of fp16-pair rows: src rows r < rows (<= 256) of (h + l) * inv_src[r],
+// columns c -> out row c (K-major in r) with its own power-of-two scale.  One block per 32
+// source columns: coalesced row reads into shared memory, per-column max, coalesced writes.
+constexpr int kTRows = 256;
+__global__ void __launch_bounds__(256) f16pair_transpose_kernel(
+    const __half* __restrict__ h, const __half* __restrict__ l, int64_t ldi,
+    const float* __restrict__ inv_src, int rows, int64_t cols, __half* __restrict__ oh,
+    __half* __restrict__ ol, int64_t ldo, float* __restrict__ inv_out) {
+    __shared__ float tile[kTRows][33];
+    __shared__ float red[8][33];
+    __shared__ float sc[32];
+    const int64_t c0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t c = c0 + tx;
+    float mx = 0.f;
+    for (int r = ty; r < kTRows; r += 8) {
+        float v = 0.f;
+        if (r < rows && c < cols)
+            v = (__half2float(h[r * ldi + c]) + __half2float(l[r * ldi + c])) * inv_src[r];
+        tile[r][tx] = v;
+        mx = fmaxf(mx, fabsf(v));
+    }
+    red[ty][tx] = mx;
+    __syncthreads();
+    if (ty == 0) {
+        float m = red[0][tx];
+        for (int q = 1; q < 8; ++q) m = fmaxf(m, red[q][tx]);
+        int e = 0;
+        if (m > 0.f && isfinite(m)) {
+            int ex;
+            frexpf(m, &ex);
+            e = max(-120, min(120, 14 - ex));
+        }
+        sc[tx] = ldexpf(1.f, e);
+        if (c < cols) inv_out[c] = ldexpf(1.f, -e);
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {  // output row c0 + j, lanes over r
+        const int64_t oc = c0 + j;
+        if (oc >= cols) continue;
+        const float s = sc[j];
+        for (int r = tx; r < rows; r += 32) {
+            const float v = tile[r][j] * s;
+            const __half hv = __float2half_rn(v);
+            oh[oc * ldo + r] = hv;
+            ol[oc * ldo + r] = __float2half_rn(v - __half2float(hv));
+        }
     }
 }
 
@@ -596,35 +692,51 @@ int enks_f16pair_recon(const void* h, const void* l, int64_t ldi, const float* i
     return enks::check_launch("enks_f16pair_recon");
 }
 
-int64_t enks_gemm_f16pair_ws_bytes(int64_t M, int64_t N, int64_t K) {
+}  // extern "C"
+
+namespace enks {
+namespace {
+struct Epi {
+    float beta;
+    const float* c0;
+    int64_t ldc0;
+    const float* bias;
+    int64_t ld_bias;
+    int bias_cols;
+};
+
+int f16p_split_for(int64_t M, int64_t N, int64_t K, bool fused) {
+    if (fused) return 1;
     const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
-    const int tiles = (int)((M + enks::BM - 1) / enks::BM) * (int)((N + BN - 1) / BN);
-    const int64_t chunks = (K + enks::KC - 1) / enks::KC;
-    const int split = enks::use_pair(N) ? enks::choose_split_pairs((tiles + 1) / 2, chunks)
-                                        : enks::choose_split16(tiles, chunks);
-    return split > 1 ? (int64_t)split * M * N * (int64_t)sizeof(float) : 0;
+    const int m_tiles = (int)((M + BM - 1) / BM);
+    const int n_tiles = (int)((N + BN - 1) / BN);
+    const int64_t chunks = (K + KC - 1) / KC;
+    return use_pair(N) ? choose_split_pairs((m_tiles + 1) / 2 * n_tiles, chunks)
+                       : choose_split16(m_tiles * n_tiles, chunks);
 }
 
-int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah, const void* Al,
+int gemm_f16pair_impl(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah, const void* Al,
                       int64_t lda, const float* inv_sa, const void* Bh, const void* Bl, int64_t ldb,
-                      const float* inv_sb, float* C, int64_t ldc, void* ws, void* stream) {
-    using namespace enks;
+                      const float* inv_sb, float* C, int64_t ldc, void* ws, void* stream,
+                      const Epi* epi) {
     ENKS_REQUIRE(Ah && Al && Bh && Bl && inv_sa && inv_sb && C, "enks_gemm_f16pair: null pointer");
-    ENKS_REQUIRE(N >= 1 && N <= 256 && K >= 1 && (lda % 8) == 0 && (ldb % 8) == 0,
-                 "enks_gemm_f16pair: need N <= 256 and 16-B aligned fp16 rows (ld %% 8 == 0)");
+    ENKS_REQUIRE(N >= 1 && K >= 1 && (lda % 8) == 0 && (ldb % 8) == 0,
+                 "enks_gemm_f16pair: need 16-B aligned fp16 rows (ld %% 8 == 0)");
+    ENKS_REQUIRE(N <= 256 || use_pair(N), "enks_gemm_f16pair: N > 256 needs the CTA-pair kernel");
+    ENKS_REQUIRE(!epi || !epi->bias || epi->bias_cols > 0, "enks_gemm_f16pair: bias_cols <= 0");
     if (M == 0) return ENKS_OK;
     const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
+    const bool pair = use_pair(N);
     CUtensorMap maps[4];
     if (!map16(&maps[0], Ah, M, K, lda, BM) || !map16(&maps[1], Al, M, K, lda, BM) ||
-        !map16(&maps[2], Bh, N, K, ldb, use_pair(N) ? 128 : BN) ||
-        !map16(&maps[3], Bl, N, K, ldb, use_pair(N) ? 128 : BN)) {
+        !map16(&maps[2], Bh, N, K, ldb, pair ? 128 : BN) ||
+        !map16(&maps[3], Bl, N, K, ldb, pair ? 128 : BN)) {
         set_error("enks_gemm_f16pair: cuTensorMapEncodeTiled failed (alignment?)");
         return ENKS_E_UNSUPPORTED;
     }
     const int m_tiles = (int)((M + BM - 1) / BM);
-    const bool pair = use_pair(N);
-    const int split = pair ? choose_split_pairs((m_tiles + 1) / 2, (K + KC - 1) / KC)
-                           : choose_split16(m_tiles, (K + KC - 1) / KC);
+    const int n_tiles = (int)((N + BN - 1) / BN);
+    const int split = f16p_split_for(M, N, K, epi != nullptr);
     ENKS_REQUIRE(split == 1 || ws, "enks_gemm_f16pair: split-K needs workspace");
     P16 p;
     p.M = M; p.N = N; p.K = K;
@@ -641,7 +753,13 @@ int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* 
     p.out = direct ? C : static_cast<float*>(ws);
     p.ldo = direct ? ldc : N;
     p.split_stride = direct ? 0 : M * N;
-    dim3 grid((unsigned)m_tiles, 1, (unsigned)split);
+    p.beta = epi ? epi->beta : 0.f;
+    p.c0 = epi ? epi->c0 : nullptr;
+    p.ldc0 = epi ? epi->ldc0 : 0;
+    p.bias = epi ? epi->bias : nullptr;
+    p.ld_bias = epi ? epi->ld_bias : 0;
+    p.bias_cols = epi && epi->bias_cols > 0 ? epi->bias_cols : 1;
+    dim3 grid((unsigned)m_tiles, (unsigned)n_tiles, (unsigned)split);
     cudaStream_t st = as_stream(stream);
     int rc;
     if (pair) {
@@ -657,6 +775,46 @@ int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* 
     f16p_sum_splits<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(static_cast<float*>(ws), split,
                                                                      M, N, C, ldc);
     return check_launch("enks_gemm_f16pair(split reduce)");
+}
+}  // namespace
+}  // namespace enks
+
+extern "C" {
+
+int64_t enks_gemm_f16pair_ws_bytes(int64_t M, int64_t N, int64_t K) {
+    const int split = enks::f16p_split_for(M, N, K, false);
+    return split > 1 ? (int64_t)split * M * N * (int64_t)sizeof(float) : 0;
+}
+
+int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah, const void* Al,
+                      int64_t lda, const float* inv_sa, const void* Bh, const void* Bl, int64_t ldb,
+                      const float* inv_sb, float* C, int64_t ldc, void* ws, void* stream) {
+    return enks::gemm_f16pair_impl(M, N, K, alpha, Ah, Al, lda, inv_sa, Bh, Bl, ldb, inv_sb, C, ldc,
+                                   ws, stream, nullptr);
+}
+
+int enks_gemm_f16pair_ex(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah,
+                         const void* Al, int64_t lda, const float* inv_sa, const void* Bh,
+                         const void* Bl, int64_t ldb, const float* inv_sb, float beta,
+                         const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias,
+                         int bias_cols, float* C, int64_t ldc, void* stream) {
+    const enks::Epi epi{beta, C0, ldc0, bias, ld_bias, bias_cols};
+    return enks::gemm_f16pair_impl(M, N, K, alpha, Ah, Al, lda, inv_sa, Bh, Bl, ldb, inv_sb, C, ldc,
+                                   nullptr, stream, &epi);
+}
+
+int enks_f16pair_transpose(const void* h, const void* l, int64_t ldi, const float* inv_src,
+                           int rows, int64_t cols, void* oh, void* ol, int64_t ldo, float* inv_out,
+                           void* stream) {
+    ENKS_REQUIRE(h && l && inv_src && oh && ol && inv_out, "enks_f16pair_transpose: null pointer");
+    ENKS_REQUIRE(rows >= 1 && rows <= enks::kTRows, "enks_f16pair_transpose: rows must be 1..%d",
+                 enks::kTRows);
+    if (cols <= 0) return ENKS_OK;
+    enks::f16pair_transpose_kernel<<<(unsigned)((cols + 31) / 32), 256, 0,
+                                     enks::as_stream(stream)>>>(
+        static_cast<const __half*>(h), static_cast<const __half*>(l), ldi, inv_src, rows, cols,
+        static_cast<__half*>(oh), static_cast<__half*>(ol), ldo, inv_out);
+    return enks::check_launch("enks_f16pair_transpose");
 }
 
 }  // extern "C"

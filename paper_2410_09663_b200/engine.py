@@ -277,14 +277,25 @@ class DeviceSmoother:
         if self.use_tc and not self.pair:
             self.yc_hi = ops.empty(p, K)
             self.yc_lo = ops.empty(p, K)
+        # newest-slice shift on the fp16-pair kernel: B = Yc_tau^T planes (K x p), re-split
+        # from the basis rows; no fp32 copy of Yc_tau is kept
+        self.shift_f16 = (self.pair and p <= 256 and p % 8 == 0 and m % 4 == 0
+                          and hasattr(ops, "gemm_f16pair_ex"))
         if self.pair:
             self.A_new = ops.empty(q, K)   # fp32 anomalies of the newest slice, [x; u] rows
-            self.Yc_new = ops.empty(p, K)  # fp32 centred observations of the newest slice
+            self.Yc_new = None if self.shift_f16 else ops.empty(p, K)  # fp32 centred obs
+        if self.shift_f16:
+            f16 = torch.float16
+            self.ycT_h, self.ycT_l, self.ycT_inv = (ops.empty(K, p, dtype=f16),
+                                                    ops.empty(K, p, dtype=f16), ops.empty(K))
+            self.gtt_h, self.gtt_l, self.gtt_inv = (ops.empty(q, p, dtype=f16),
+                                                    ops.empty(q, p, dtype=f16), ops.empty(q))
         # the gain-side products (correction, gain, newest-slice shift) on tcgen05 as well
         self.use_tc2 = self.use_tc and p % 4 == 0 and m % 4 == 0 and hasattr(ops, "gemm_tc")
-        if self.use_tc2:
+        if self.use_tc2 and not self.shift_f16:
             self.ycT_hi = ops.empty(K, p)
             self.ycT_lo = ops.empty(K, p)
+        if self.use_tc2:
             self.sinvT_hi = ops.empty(p, p)
             self.sinvT_lo = ops.empty(p, p)
             self.pyT_hi = self.pyT_lo = None
@@ -367,7 +378,7 @@ class DeviceSmoother:
         self.cap = cap
 
     def memory_bytes(self) -> int:
-        keys = ("Ah", "Al", "a_inv", "Yh", "Yl", "y_inv", "A_new", "Yc_new") if self.pair \
+        keys = ("Ah", "Al", "a_inv", "Yh", "Yl", "y_inv", "A_new") if self.pair \
             else ("Abuf", "Ybuf")
         return sum(t.numel() * t.element_size() for t in
                    [getattr(self, k) for k in keys] + [self.G, self.mean, self.PA, self.PY,
@@ -561,7 +572,8 @@ class DeviceSmoother:
             self._barrier_row(head, tau)
         yc = self.Yc_new if self.pair else self.Ybuf[(tau - 1) * p:tau * p]
         if self.pair:
-            self._center(ob, self.ybar, yc, pair_rows=("Y", (tau - 1) * p), f32_rows=p)
+            self._center(ob, self.ybar, yc, pair_rows=("Y", (tau - 1) * p),
+                         f32_rows=0 if yc is None else p)
         else:
             self._center(ob, self.ybar, yc)
 
@@ -631,7 +643,15 @@ class DeviceSmoother:
         q = self.q
         g_tt = self.G[r0:r0 + q, (tau - 1) * p:tau * p]
         a_new = self.A_new if self.pair else self.Abuf[r0:r0 + d]
-        if self.use_tc2:
+        if self.shift_f16:
+            yb = slice((tau - 1) * p, tau * p)
+            ops.f16pair_split(g_tt, self.gtt_h, self.gtt_l, self.gtt_inv)
+            ops.f16pair_transpose(self.Yh[yb], self.Yl[yb], self.y_inv[yb], self.ycT_h,
+                                  self.ycT_l, self.ycT_inv)
+            ops.gemm_f16pair_ex(self.gtt_h, self.gtt_l, self.gtt_inv, self.ycT_h, self.ycT_l,
+                                self.ycT_inv, self.last, alpha=-1.0, beta=1.0, C0=a_new[:q],
+                                bias=self.mean[r0:r0 + q], bias_cols=self.m, tag="shift")
+        elif self.use_tc2:
             ops.tf32_split(yc, self.ycT_hi, self.ycT_lo, transpose=True)
             ops.gemm_tc(g_tt, self.ycT_hi, self.ycT_lo, self.last, alpha=-1.0, beta=1.0,
                         C0=a_new[:q], bias=self.mean[r0:r0 + q], bias_cols=self.m, tag="shift")

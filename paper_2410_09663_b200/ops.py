@@ -288,6 +288,27 @@ class DeviceOps:
             ev1.record()
             self.profile.append((tag, ev0, ev1, 2.0 * M * N * K))
 
+    def f16pair_transpose(self, h, l, inv_src, oh, ol, inv_out):
+        """(h + l) * inv_src (rows x K fp16 pairs, rows <= 256) -> transposed planes (K x rows)."""
+        self.launches += 1
+        _lib.call("enks_f16pair_transpose", _p(h), _p(l), _ld(h), _p(inv_src), h.shape[0],
+                  h.shape[1], _p(oh), _p(ol), _ld(oh), _p(inv_out), self._stream())
+
+    def gemm_f16pair_ex(self, Ah, Al, inv_sa, Bh, Bl, inv_sb, C, *, alpha=1.0, beta=0.0, C0=None,
+                        bias=None, bias_cols=0, tag=None):
+        """C = alpha A B^T (fp16-pair planes, any N) + beta C0 + bias[:, c % bias_cols]."""
+        M, K = Ah.shape
+        N = Bh.shape[0]
+        if M == 0:
+            return
+        self.launches += 1
+        with self._prof(tag, 2.0 * M * N * K) if tag else contextlib.nullcontext():
+            _lib.call("enks_gemm_f16pair_ex", M, N, K, float(alpha), _p(Ah), _p(Al), _ld(Ah),
+                      _p(inv_sa), _p(Bh), _p(Bl), _ld(Bh), _p(inv_sb), float(beta), _p(C0),
+                      _ld(C0) if C0 is not None else 0, _p(bias),
+                      _ld(bias) if bias is not None else 0, int(bias_cols), _p(C), _ld(C),
+                      self._stream())
+
     def gemm_nt_f16pair(self, a, b, out, *, alpha=1.0, tag=None):
         """out (M x N) = alpha a b^T for fp32 a (M x K), b (N x K) on tcgen05: both operands
         split into fp16-pair planes once, N covered in 256-column launches (any N)."""

@@ -42,6 +42,22 @@ class CpuOps:
         b = (Bh + Bl) * inv_sb[:, None]
         C.copy_(alpha * (a @ b.t()))
 
+    def f16pair_transpose(self, h, l, inv_src, oh, ol, inv_out):
+        oh.copy_(((h + l) * inv_src[:, None]).t())
+        ol.zero_()
+        inv_out.fill_(1.0)
+
+    def gemm_f16pair_ex(self, Ah, Al, inv_sa, Bh, Bl, inv_sb, C, *, alpha=1.0, beta=0.0, C0=None,
+                        bias=None, bias_cols=0, tag=None):
+        a = (Ah + Al) * inv_sa[:, None]
+        b = (Bh + Bl) * inv_sb[:, None]
+        out = alpha * (a @ b.t())
+        if C0 is not None:
+            out = out + beta * C0
+        if bias is not None:
+            out = out + bias[:, torch.arange(out.shape[1]) % bias_cols]
+        C.copy_(out)
+
     def member_center_f16pair(self, src, n_members, cols, z0, acc, amax, n_total, mean, h, l,
                               inv_scale, f32=None, rows_f32=0):
         anom = torch.empty(src.shape, dtype=self.dtype)

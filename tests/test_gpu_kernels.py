@@ -413,3 +413,32 @@ def test_gemm_nt_f16pair_blocked_columns(dev_ops, M, N, K):
     # Gram diagonals are all-positive sums: the tensor core's truncating TMEM accumulation
     # within one 256-deep chain biases them by up to ~chain/2 * 2^-24 (see gemm_f16p.cu)
     assert ((Cs.double().cpu() - refs).abs() / (A.double().abs() @ A.double().abs().t())).max() < 5e-6
+
+
+def test_gemm_f16pair_ex_shift_operands(dev_ops):
+    """Newest-slice shift: transposed re-split of fp16-pair rows, then the fused-epilogue GEMM
+    C = C0 + bias - G Yc with N = K in 256-column tiles."""
+    g = torch.Generator().manual_seed(5)
+    p, q, K, m = 256, 256, 4096 + 128, 128
+    Y = torch.randn(p, K, generator=g) * torch.logspace(-2, 2, p).unsqueeze(1)
+    G = torch.randn(q, p, generator=g) * 0.01
+    C0 = torch.randn(q, K, generator=g)
+    bias = torch.randn(q, m, generator=g)
+    f16 = torch.float16
+    yh, yl = dev_ops.empty(p, K, dtype=f16), dev_ops.empty(p, K, dtype=f16)
+    yi = dev_ops.empty(p)
+    dev_ops.f16pair_split(Y.to(dev_ops.device), yh, yl, yi)
+    th, tl, ti = dev_ops.empty(K, p, dtype=f16), dev_ops.empty(K, p, dtype=f16), dev_ops.empty(K)
+    dev_ops.f16pair_transpose(yh, yl, yi, th, tl, ti)
+    rec = dev_ops.empty(K, p)
+    dev_ops.f16pair_recon(th, tl, ti, rec)
+    assert ((rec.double().cpu() - Y.t().double()).abs() /
+            Y.t().double().abs().amax(1, keepdim=True)).max() < 5e-7
+    gh, gl, gi = dev_ops.empty(q, p, dtype=f16), dev_ops.empty(q, p, dtype=f16), dev_ops.empty(q)
+    dev_ops.f16pair_split(G.to(dev_ops.device), gh, gl, gi)
+    out = dev_ops.zeros(q, K)
+    dev_ops.gemm_f16pair_ex(gh, gl, gi, th, tl, ti, out, alpha=-1.0, beta=1.0,
+                            C0=C0.to(dev_ops.device), bias=bias.to(dev_ops.device), bias_cols=m)
+    ref = C0.double() + bias.double()[:, [k % m for k in range(K)]] - G.double() @ Y.double()
+    scale = (G.double().abs() @ Y.double().abs()) + C0.double().abs() + bias.double().abs().amax()
+    assert ((out.double().cpu() - ref).abs() / scale).max().item() < 1e-6
