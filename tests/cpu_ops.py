@@ -69,7 +69,8 @@ class CpuOps:
             f32[:rows_f32].copy_(anom[:rows_f32])
 
     def to_device(self, arr, dtype=None):
-        return torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype or self.dtype).clone()
+        arr = np.require(arr, requirements=["C", "W"])
+        return torch.as_tensor(arr, dtype=dtype or self.dtype).clone()
 
     def noise_fill(self, head, t, ch, member0, n_members, rows, cols, diag=None, out=None,
                    base=None, out_plus=None):

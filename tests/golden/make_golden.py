@@ -80,6 +80,25 @@ def _burgers_horizon(ref, mode):
     return dict(mean=out, x0=pr.x0.packed)
 
 
+VECTOR_CASES = [("vec_m1", dict(n=4, l=1, m=1), 9, 8, 3, 6), ("vec_m2", dict(n=3, l=2, m=2), 12, 16, 4, 5),
+                ("vec_m4", dict(n=6, l=3, m=4), 13, 40, 3, 7)]
+
+
+def _vector_cases(ref):
+    """Reference vector_enks_smooth (baselines.py:95-197) on seeded linear problems."""
+    import importlib
+
+    base = importlib.import_module("enksmpc.baselines")
+    for name, kw, seed, N, h, sseed in VECTOR_CASES:
+        _, vs, x0 = problems.make_linear_setup(ref, np.random.default_rng(seed), **kw)
+        y = vs.reference_observation()
+        mean, rep = base.vector_enks_smooth(x0, y, vs, h, N, ref.matvar.NoiseStreams(seed=sseed))
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), mean=mean, x0=x0.packed,
+                            obs_cov_entries=rep.obs_cov_entries,
+                            cross_cov_entries=rep.cross_cov_entries,
+                            jitter_events=rep.jitter_events)
+
+
 def main():
     ref = problems.reference_modules()
     for name, kw, seed, N, h, sseed, extra in LINEAR_CASES:
@@ -112,6 +131,7 @@ def main():
     for mode in ("boundary", "pointwise"):
         np.savez_compressed(os.path.join(HERE, f"burgers_c1a_{mode}.npz"),
                             **_burgers_horizon(ref, mode))
+    _vector_cases(ref)
     noise = {}
     for k, (seed, prefix, ids, shape) in enumerate(NOISE_CASES):
         st = ref.matvar.NoiseStreams(seed=seed, prefix=prefix)
