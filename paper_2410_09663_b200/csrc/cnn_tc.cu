@@ -44,24 +44,43 @@ constexpr int NA = 3;      // layer-1 row slots
 constexpr int NACC = 4;    // TMEM output-row accumulators
 constexpr int kThreads = 384;
 
-constexpr int kBTile = NB * 128;        // one dy, hi or lo: 96 rows x 128 B
-constexpr int kATile = W * 128;         // one layer-1 row, hi or lo: 128 rows x 128 B
-constexpr int kOffB = 0;                            // [dy][hi/lo] B tiles
-constexpr int kOffA = kOffB + 3 * 2 * kBTile;       // [slot][hi/lo] A tiles
-constexpr int kOffIn = kOffA + NA * 2 * kATile;     // input ring [4][2][W + 2] floats
 constexpr int kInRow = W + 2;
-constexpr int kOffW1 = kOffIn + 4 * 2 * kInRow * 4; // w1 pairs [C1/2][20] float2, b1, b2, w3, b3
 constexpr int kW1Stride = 20;                        // float2 per channel pair (18 used)
-constexpr int kOffB1 = kOffW1 + (C1 / 2) * kW1Stride * 8;
-constexpr int kOffB2 = kOffB1 + C1 * 4;
-constexpr int kOffW3 = kOffB2 + C2 * 4;              // w3 [C2][12]: taps 0..8 (+pad), per channel
 constexpr int kW3Stride = 12;
-constexpr int kOffB3 = kOffW3 + C2 * kW3Stride * 4;
-constexpr int kOffX = kOffB3 + 16;                  // exchange buffers
 constexpr int kXD = 2 * 4 * 32;                     // [parity][warp][32]
 constexpr int kXV = 2 * 4 * 4;                      // [parity][warp][3 (+pad)]
-constexpr int kOffBar = kOffX + (2 * kXD + 2 * kXV) * 4;
-constexpr int kSmem = kOffBar + 32 * 8 + 1024;      // + alignment slack
+
+// Shared-memory / TMEM layout.  SH = false: the three horizontal taps are stacked in N
+// (N = 96, one accumulator per OUTPUT row, horizontal taps folded in the epilogue with warp
+// shuffles).  SH = true (128-pixel images): the three VERTICAL taps are stacked in N and the
+// horizontal taps are three MMAs whose A operand is the layer-1 tile read from row dx (the tile
+// keeps a zero pad row above and below the 128 pixels; a SWIZZLE_128B operand may start at
+// any 128-B row -- tools/probes/tc_shift_probe.cu).  One accumulator per INPUT row r holds
+// its contributions to output rows r+1, r, r-1, which the epilogue adds in registers: no
+// shuffles, no cross-warp exchange for layer 2.
+template <bool SH>
+struct CL {
+    static constexpr int kBRows = NB;                      // rows of one B tile
+    static constexpr int kBTile = kBRows * 128;
+    static constexpr int kNBT = 3;                         // B tiles: dx (SH) or dy
+    static constexpr int kARows = SH ? 136 : W;            // SH: pixel x at row x + 1
+    static constexpr int kATile = kARows * 128;
+    static constexpr int kOffB = 0;                        // [tap][hi/lo] B tiles
+    static constexpr int kOffA = kOffB + kNBT * 2 * kBTile;  // [slot][hi/lo] A tiles
+    static constexpr int kOffIn = kOffA + NA * 2 * kATile;   // input ring [4][2][W + 2] floats
+    static constexpr int kOffW1 = kOffIn + 4 * 2 * kInRow * 4;
+    static constexpr int kOffB1 = kOffW1 + (C1 / 2) * kW1Stride * 8;
+    static constexpr int kOffB2 = kOffB1 + C1 * 4;
+    static constexpr int kOffW3 = kOffB2 + C2 * 4;
+    static constexpr int kOffB3 = kOffW3 + C2 * kW3Stride * 4;
+    static constexpr int kOffX = kOffB3 + 16;
+    static constexpr int kOffBar = kOffX + (2 * kXD + 2 * kXV) * 4;
+    static constexpr int kSmem = kOffBar + 32 * 8 + 1024;
+    static constexpr int kAccCols = NB;                    // TMEM columns per accumulator
+    static constexpr uint32_t kTmemAlloc = 512;
+    static_assert(kSmem <= 232448, "shared memory budget");
+    static_assert(kOffA % 1024 == 0 && kATile % 1024 == 0, "SW128 tiles need 1 KB alignment");
+};
 
 __device__ __forceinline__ float exp2f_approx(float x) {
     float y;
@@ -120,22 +139,24 @@ struct Cnn3Args {
     int debug;  // ENKS_CNN_DEBUG: 1 = no MMAs, 2 = no layer-1 math, 4 = no epilogue math
 };
 
+template <bool SH>
 __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) {
+    using L = CL<SH>;
     extern __shared__ uint8_t smem_raw[];
     // align to 1024 B by offsetting the shared pointer itself, so the compiler keeps the
     // shared address space (LDS/STS rather than generic LD/ST)
     uint8_t* sm = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    float* in_ring = reinterpret_cast<float*>(sm + kOffIn);
-    float* w1s = reinterpret_cast<float*>(sm + kOffW1);
-    float* b1s = reinterpret_cast<float*>(sm + kOffB1);
-    float* b2s = reinterpret_cast<float*>(sm + kOffB2);
-    float* w3s = reinterpret_cast<float*>(sm + kOffW3);
-    float* b3s = reinterpret_cast<float*>(sm + kOffB3);
-    float* xd0 = reinterpret_cast<float*>(sm + kOffX);
+    float* in_ring = reinterpret_cast<float*>(sm + L::kOffIn);
+    float* w1s = reinterpret_cast<float*>(sm + L::kOffW1);
+    float* b1s = reinterpret_cast<float*>(sm + L::kOffB1);
+    float* b2s = reinterpret_cast<float*>(sm + L::kOffB2);
+    float* w3s = reinterpret_cast<float*>(sm + L::kOffW3);
+    float* b3s = reinterpret_cast<float*>(sm + L::kOffB3);
+    float* xd0 = reinterpret_cast<float*>(sm + L::kOffX);
     float* xd2 = xd0 + kXD;
     float* xv0 = xd2 + kXD;
     float* xv2 = xv0 + kXV;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kOffBar);
     uint64_t* a_full = bars;             // [NA]
     uint64_t* a_empty = bars + NA;       // [NA]
     uint64_t* acc_full = bars + 2 * NA;  // [NACC]
@@ -146,16 +167,37 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     const int n = a.rows;
 
     // ---- stage weights (all threads) -------------------------------------------------
-    for (int e = threadIdx.x; e < 3 * NB * C1; e += kThreads) {
-        // B[dy][row = dx*C2 + co][ci] = W2[co][ci][dy][dx]
-        const int dy = e / (NB * C1), rem = e - dy * NB * C1;
-        const int row = rem / C1, ci = rem - row * C1;
-        const int dx = row / C2, co = row - dx * C2;
-        const float v = a.w2[((co * C1 + ci) * 3 + dy) * 3 + dx];
-        const float h = ptx::tf32_round(v);
-        const uint32_t off = sw128(row, ci * 4);
-        *reinterpret_cast<float*>(sm + kOffB + (dy * 2 + 0) * kBTile + off) = h;
-        *reinterpret_cast<float*>(sm + kOffB + (dy * 2 + 1) * kBTile + off) = v - h;
+    if constexpr (SH) {
+        for (int e = threadIdx.x; e < 3 * NB * C1; e += kThreads) {
+            // B[dx][row = dy*C2 + co][ci] = W2[co][ci][dy][dx]
+            const int dx = e / (NB * C1), rem = e - dx * NB * C1;
+            const int row = rem / C1, ci = rem - row * C1;
+            const int dy = row / C2, co = row - dy * C2;
+            const float v = a.w2[((co * C1 + ci) * 3 + dy) * 3 + dx];
+            const float h = ptx::tf32_round(v);
+            const uint32_t off = sw128(row, ci * 4);
+            *reinterpret_cast<float*>(sm + L::kOffB + (dx * 2 + 0) * L::kBTile + off) = h;
+            *reinterpret_cast<float*>(sm + L::kOffB + (dx * 2 + 1) * L::kBTile + off) = v - h;
+        }
+        // zero pad rows (0 and 129..135) of every A slot; never written afterwards
+        for (int e = threadIdx.x; e < NA * 2 * 8 * 32; e += kThreads) {
+            const int tile = e / (8 * 32), rem = e - tile * 8 * 32;
+            const int pr = rem >> 5, k = rem & 31;
+            const int row = pr == 0 ? 0 : 128 + pr;
+            *reinterpret_cast<float*>(sm + L::kOffA + tile * L::kATile + sw128(row, k * 4)) = 0.f;
+        }
+    } else {
+        for (int e = threadIdx.x; e < 3 * NB * C1; e += kThreads) {
+            // B[dy][row = dx*C2 + co][ci] = W2[co][ci][dy][dx]
+            const int dy = e / (NB * C1), rem = e - dy * NB * C1;
+            const int row = rem / C1, ci = rem - row * C1;
+            const int dx = row / C2, co = row - dx * C2;
+            const float v = a.w2[((co * C1 + ci) * 3 + dy) * 3 + dx];
+            const float h = ptx::tf32_round(v);
+            const uint32_t off = sw128(row, ci * 4);
+            *reinterpret_cast<float*>(sm + L::kOffB + (dy * 2 + 0) * L::kBTile + off) = h;
+            *reinterpret_cast<float*>(sm + L::kOffB + (dy * 2 + 1) * L::kBTile + off) = v - h;
+        }
     }
     for (int e = threadIdx.x; e < C1 * 18; e += kThreads) {
         const int c = e / 18, k = e - c * 18;  // k = ci*9 + ky*3 + kx
@@ -179,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+    if (warp == 2) ptx::tmem_alloc(tmem_slot, L::kTmemAlloc);
     ptx::fence_proxy_async_smem();  // staged B tiles -> async proxy
     ptx::tc_fence_before();
     __syncthreads();
@@ -189,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     if (warp == 0) {
         // ================= MMA issuer =================
         if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_tf32(W, NB);
+            constexpr uint32_t idesc = ptx::idesc_tf32(W, L::kAccCols);
             int it = 0;
             for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
                 for (int r = 0; r < n; ++r) {
@@ -197,33 +239,57 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     const int slot = Rg % NA;
                     ptx::mbar_wait(&a_full[slot], (uint32_t)((Rg / NA) & 1));
                     ptx::tc_fence_after();
-                    const uint8_t* ah_t = sm + kOffA + (slot * 2 + 0) * kATile;
-                    const uint8_t* al_t = sm + kOffA + (slot * 2 + 1) * kATile;
-                    for (int dy = 0; dy < 3; ++dy) {
-                        const int y = r - dy + 1;
-                        if (y < 0 || y >= n) continue;
-                        const int Yg = it * n + y;
-                        const int q = Yg % NACC;
-                        const bool first = (dy == 0) || (r == 0 && dy == 1);
-                        if (first) {
-                            ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Yg / NACC) & 1) ^ 1));
-                            ptx::tc_fence_after();
-                        }
-                        const uint32_t d = tmem + (uint32_t)(q * NB);
-                        const uint8_t* bh_t = sm + kOffB + (dy * 2 + 0) * kBTile;
-                        const uint8_t* bl_t = sm + kOffB + (dy * 2 + 1) * kBTile;
+                    const uint8_t* ah_t = sm + L::kOffA + (slot * 2 + 0) * L::kATile;
+                    const uint8_t* al_t = sm + L::kOffA + (slot * 2 + 1) * L::kATile;
+                    if constexpr (SH) {
+                        // D_r[x][(dy, co)] = sum_dx sum_ci h1[r][x + dx - 1][ci] W2[co][ci][dy][dx]
+                        const int q = Rg % NACC;
+                        ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Rg / NACC) & 1) ^ 1));
+                        ptx::tc_fence_after();
+                        const uint32_t d = tmem + (uint32_t)(q * L::kAccCols);
 #pragma unroll
-                        for (int k = 0; k < ((a.debug & 1) ? 0 : C1 / 8); ++k) {
-                            const uint64_t adh = ptx::desc_kmajor_sw128(ah_t + 32 * k);
-                            const uint64_t adl = ptx::desc_kmajor_sw128(al_t + 32 * k);
-                            const uint64_t bdh = ptx::desc_kmajor_sw128(bh_t + 32 * k);
-                            const uint64_t bdl = ptx::desc_kmajor_sw128(bl_t + 32 * k);
-                            ptx::mma_tf32_ss(d, adl, bdh, idesc, (first && k == 0) ? 0u : 1u);
-                            ptx::mma_tf32_ss(d, adh, bdl, idesc, 1u);
-                            ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                        for (int dx = 0; dx < 3; ++dx) {
+                            const uint8_t* bh_t = sm + L::kOffB + (dx * 2 + 0) * L::kBTile;
+                            const uint8_t* bl_t = sm + L::kOffB + (dx * 2 + 1) * L::kBTile;
+#pragma unroll
+                            for (int k = 0; k < ((a.debug & 1) ? 0 : C1 / 8); ++k) {
+                                const uint64_t adh = ptx::desc_kmajor_sw128(ah_t + dx * 128 + 32 * k);
+                                const uint64_t adl = ptx::desc_kmajor_sw128(al_t + dx * 128 + 32 * k);
+                                const uint64_t bdh = ptx::desc_kmajor_sw128(bh_t + 32 * k);
+                                const uint64_t bdl = ptx::desc_kmajor_sw128(bl_t + 32 * k);
+                                ptx::mma_tf32_ss(d, adl, bdh, idesc, (dx == 0 && k == 0) ? 0u : 1u);
+                                ptx::mma_tf32_ss(d, adh, bdl, idesc, 1u);
+                                ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                            }
                         }
-                        // row y complete: after its dy=2 contribution, or the last row's dy=1
-                        if (dy == 2 || (r == n - 1 && dy == 1)) ptx::mma_commit(&acc_full[q]);
+                        ptx::mma_commit(&acc_full[q]);
+                    } else {
+                        for (int dy = 0; dy < 3; ++dy) {
+                            const int y = r - dy + 1;
+                            if (y < 0 || y >= n) continue;
+                            const int Yg = it * n + y;
+                            const int q = Yg % NACC;
+                            const bool first = (dy == 0) || (r == 0 && dy == 1);
+                            if (first) {
+                                ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Yg / NACC) & 1) ^ 1));
+                                ptx::tc_fence_after();
+                            }
+                            const uint32_t d = tmem + (uint32_t)(q * L::kAccCols);
+                            const uint8_t* bh_t = sm + L::kOffB + (dy * 2 + 0) * L::kBTile;
+                            const uint8_t* bl_t = sm + L::kOffB + (dy * 2 + 1) * L::kBTile;
+#pragma unroll
+                            for (int k = 0; k < ((a.debug & 1) ? 0 : C1 / 8); ++k) {
+                                const uint64_t adh = ptx::desc_kmajor_sw128(ah_t + 32 * k);
+                                const uint64_t adl = ptx::desc_kmajor_sw128(al_t + 32 * k);
+                                const uint64_t bdh = ptx::desc_kmajor_sw128(bh_t + 32 * k);
+                                const uint64_t bdl = ptx::desc_kmajor_sw128(bl_t + 32 * k);
+                                ptx::mma_tf32_ss(d, adl, bdh, idesc, (first && k == 0) ? 0u : 1u);
+                                ptx::mma_tf32_ss(d, adh, bdl, idesc, 1u);
+                                ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                            }
+                            // row y complete: after its dy=2 contribution, or the last row's dy=1
+                            if (dy == 2 || (r == n - 1 && dy == 1)) ptx::mma_commit(&acc_full[q]);
+                        }
                     }
                     ptx::mma_commit(&a_empty[slot]);
                 }
@@ -282,8 +348,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     ptx::mbar_arrive(&a_full[slot]);
                     continue;
                 }
-                uint8_t* ah_t = sm + kOffA + (slot * 2 + 0) * kATile;
-                uint8_t* al_t = sm + kOffA + (slot * 2 + 1) * kATile;
+                uint8_t* ah_t = sm + L::kOffA + (slot * 2 + 0) * L::kATile;
+                uint8_t* al_t = sm + L::kOffA + (slot * 2 + 1) * L::kATile;
 #pragma unroll 2
                 for (int c4 = 0; c4 < ((a.debug & 2) ? 0 : C1 / 4); ++c4) {
                     float hv[4];
@@ -307,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     h4.y = ptx::tf32_round(hv[1]); l4.y = hv[1] - h4.y;
                     h4.z = ptx::tf32_round(hv[2]); l4.z = hv[2] - h4.z;
                     h4.w = ptx::tf32_round(hv[3]); l4.w = hv[3] - h4.w;
-                    const uint32_t off = sw128(x, c4 * 16);
+                    const uint32_t off = sw128(SH ? x + 1 : x, c4 * 16);
                     *reinterpret_cast<float4*>(ah_t + off) = h4;
                     *reinterpret_cast<float4*>(al_t + off) = l4;
                 }
@@ -325,149 +391,187 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         // cross-warp tap exchange only inside an image (seg = 32: never; 64: not across 63|64)
         const bool xl = ew > 0 && ((ew * 32) & (a.seg - 1)) != 0;
         const bool xr = ew < 3 && (((ew + 1) * 32) & (a.seg - 1)) != 0;
+        // bias + tanh, layer 3 (32 -> 1, taps folded by shuffles), residual, for the finished
+        // layer-2 pre-activation row y (s = 32 channels of this pixel)
+        auto layer3 = [&](int y, const float (&s)[32], int par, float (&acc3)[3], const float* xm,
+                          float* om, bool col_ok) {
+            const float xres_m = (y >= 1 && col_ok) ? xm[(int64_t)(y - 1) * a.ldx + x] : 0.f;
+            const float xres_0 = (y == n - 1 && col_ok) ? xm[(int64_t)y * a.ldx + x] : 0.f;
+            // layer-2 activation and the layer-3 taps v[ky][kx] = sum_c w3 h
+            // four independent partial sums (8 channels each) for ILP
+            float2 v01[4], v23[4], v45[4], v67[4];
+            float v8[4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                v01[g] = v23[g] = v45[g] = v67[g] = make_float2(0.f, 0.f);
+                v8[g] = 0.f;
+            }
+#pragma unroll
+            for (int c = 0; c < ((a.debug & 4) ? 0 : 32); ++c) {
+                const int g = c & 3;
+                const float h = tanh_fast(s[c] + b2s[c]);
+                const float2 hh = make_float2(h, h);
+                const float4 w0 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride);
+                const float4 w1 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride + 4);
+                v01[g] = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01[g]);
+                v23[g] = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23[g]);
+                v45[g] = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45[g]);
+                v67[g] = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67[g]);
+                v8[g] = fmaf(w3s[c * kW3Stride + 8], h, v8[g]);
+            }
+#pragma unroll
+            for (int g = 1; g < 4; ++g) {
+                v01[0].x += v01[g].x; v01[0].y += v01[g].y;
+                v23[0].x += v23[g].x; v23[0].y += v23[g].y;
+                v45[0].x += v45[g].x; v45[0].y += v45[g].y;
+                v67[0].x += v67[g].x; v67[0].y += v67[g].y;
+                v8[0] += v8[g];
+            }
+            const float vv[9] = {v01[0].x, v01[0].y, v23[0].x, v23[0].y, v45[0].x,
+                                 v45[0].y, v67[0].x, v67[0].y, v8[0]};
+            // fold horizontal taps: lane x3 takes v[ky][0] from x3-1, v[ky][2] from x3+1
+            float tk[3];
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) {
+                const float up = __shfl_up_sync(0xffffffffu, vv[ky * 3 + 0], 1);
+                const float dn = __shfl_down_sync(0xffffffffu, vv[ky * 3 + 2], 1);
+                tk[ky] = vv[ky * 3 + 1] + (lane == 0 ? 0.f : up) + (lane == 31 ? 0.f : dn);
+                if (lane == 31) xv0[(par * 4 + ew) * 4 + ky] = vv[ky * 3 + 0];
+                if (lane == 0) xv2[(par * 4 + ew) * 4 + ky] = vv[ky * 3 + 2];
+            }
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (lane == 0 && xl) {
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky) tk[ky] += xv0[(par * 4 + ew - 1) * 4 + ky];
+            }
+            if (lane == 31 && xr) {
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky) tk[ky] += xv2[(par * 4 + ew + 1) * 4 + ky];
+            }
+            // h at row y feeds output rows y+1 (ky=0), y (ky=1), y-1 (ky=2)
+            acc3[(y + 1) % 3] += tk[0];
+            acc3[y % 3] += tk[1];
+            if (y >= 1) {
+                const int yo = y - 1;
+                const float o = acc3[yo % 3] + tk[2];
+                acc3[yo % 3] = 0.f;
+                if (col_ok) om[(int64_t)yo * a.ldo + x] = xres_m + a.alpha * (b3 + o);
+            }
+            if (y == n - 1) {
+                const float o = acc3[y % 3];
+                acc3[y % 3] = 0.f;
+                if (col_ok) om[(int64_t)y * a.ldo + x] = xres_0 + a.alpha * (b3 + o);
+            }
+        };
         int it = 0;
+        int nproc = 0;  // rows finished by this thread (exchange-buffer parity)
         for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
             float acc3[3] = {0.f, 0.f, 0.f};  // layer-3 partial sums, ring over output rows
             const float* xm = a.x + mem * W;
             float* om = a.out + mem * W;
             const bool col_ok = mem * W + x < a.cols_total;
-            for (int y = 0; y < n; ++y) {
-                const int Yg = it * n + y;
-                const int q = Yg % NACC;
-                const int par = Yg & 1;
-                // residual inputs of the rows completed below, loaded before the waits
-                const float xres_m = (y >= 1 && col_ok) ? xm[(int64_t)(y - 1) * a.ldx + x] : 0.f;
-                const float xres_0 = (y == n - 1 && col_ok) ? xm[(int64_t)y * a.ldx + x] : 0.f;
-                ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / NACC) & 1));
-                ptx::tc_fence_after();
-                if (a.debug & 8) {
+            if constexpr (SH) {
+                // pp = pre-activation of output row r - 1 (waits for D_r's dy = 2 block),
+                // pc = output row r (has D_{r-1}'s dy = 0 block); D_r's dy = 0 block starts r + 1
+                float pp[32], pc[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) pp[c] = pc[c] = 0.f;
+                for (int r = 0; r < n; ++r) {
+                    const int Rg = it * n + r;
+                    const int q = Rg % NACC;
+                    ptx::mbar_wait(&acc_full[q], (uint32_t)((Rg / NACC) & 1));
+                    ptx::tc_fence_after();
+                    const uint32_t base = tmem + lane_base + (uint32_t)(q * L::kAccCols);
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(base + 2 * C2, v);  // dy = 2 -> output row r - 1
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) pp[c] += __uint_as_float(v[c]);
+                    ptx::tmem_ld_32x32b_x32(base + C2, v);      // dy = 1 -> output row r
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) pc[c] += __uint_as_float(v[c]);
+                    ptx::tmem_ld_32x32b_x32(base, v);           // dy = 0 -> output row r + 1
+                    ptx::tmem_ld_wait();
+                    ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&acc_empty[q]);
-                    continue;
-                }
-                const uint32_t base = tmem + lane_base + (uint32_t)(q * NB);
-                float s[32], t[32];
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(base + 0, v);  // dx = 0 block
-                ptx::tmem_ld_wait();
+                    if (r >= 1) layer3(r - 1, pp, (nproc++) & 1, acc3, xm, om, col_ok);
+                    if (r == n - 1) layer3(r, pc, (nproc++) & 1, acc3, xm, om, col_ok);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
-                if (lane == 31) {
-#pragma unroll
-                    for (int c = 0; c < 32; c += 4)
-                        *reinterpret_cast<float4*>(xd0 + (par * 4 + ew) * 32 + c) =
-                            make_float4(t[c], t[c + 1], t[c + 2], t[c + 3]);
-                }
-#pragma unroll
-                for (int c = 0; c < 32; ++c) s[c] = __shfl_up_sync(0xffffffffu, t[c], 1);
-                ptx::tmem_ld_32x32b_x32(base + 32, v);  // dx = 1 block
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int c = 0; c < 32; ++c) s[c] = (lane == 0 ? 0.f : s[c]) + __uint_as_float(v[c]);
-                ptx::tmem_ld_32x32b_x32(base + 64, v);  // dx = 2 block
-                ptx::tmem_ld_wait();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&acc_empty[q]);
-#pragma unroll
-                for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
-                if (lane == 0) {
-#pragma unroll
-                    for (int c = 0; c < 32; c += 4)
-                        *reinterpret_cast<float4*>(xd2 + (par * 4 + ew) * 32 + c) =
-                            make_float4(t[c], t[c + 1], t[c + 2], t[c + 3]);
-                }
-#pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float dn = __shfl_down_sync(0xffffffffu, t[c], 1);
-                    if (lane != 31) s[c] += dn;
-                }
-                asm volatile("bar.sync 2, 128;" ::: "memory");
-                if (lane == 0 && xl) {
-#pragma unroll
-                    for (int c = 0; c < 32; c += 4) {
-                        const float4 e4 = *reinterpret_cast<const float4*>(xd0 + (par * 4 + ew - 1) * 32 + c);
-                        s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
+                    for (int c = 0; c < 32; ++c) {
+                        pp[c] = pc[c];
+                        pc[c] = __uint_as_float(v[c]);
                     }
                 }
-                if (lane == 31 && xr) {
+            } else {
+                for (int y = 0; y < n; ++y) {
+                    const int Yg = it * n + y;
+                    const int q = Yg % NACC;
+                    const int par = Yg & 1;
+                    ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / NACC) & 1));
+                    ptx::tc_fence_after();
+                    const uint32_t base = tmem + lane_base + (uint32_t)(q * L::kAccCols);
+                    float s[32];
+                    float t[32];
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(base + 0, v);  // dx = 0 block
+                    ptx::tmem_ld_wait();
 #pragma unroll
-                    for (int c = 0; c < 32; c += 4) {
-                        const float4 e4 = *reinterpret_cast<const float4*>(xd2 + (par * 4 + ew + 1) * 32 + c);
-                        s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
+                    for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
+                    if (lane == 31) {
+#pragma unroll
+                        for (int c = 0; c < 32; c += 4)
+                            *reinterpret_cast<float4*>(xd0 + (par * 4 + ew) * 32 + c) =
+                                make_float4(t[c], t[c + 1], t[c + 2], t[c + 3]);
                     }
-                }
-                // layer-2 activation and the layer-3 taps v[ky][kx] = sum_c w3 h
-                // four independent partial sums (8 channels each) for ILP
-                float2 v01[4], v23[4], v45[4], v67[4];
-                float v8[4];
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    v01[g] = v23[g] = v45[g] = v67[g] = make_float2(0.f, 0.f);
-                    v8[g] = 0.f;
-                }
+                    for (int c = 0; c < 32; ++c) s[c] = __shfl_up_sync(0xffffffffu, t[c], 1);
+                    ptx::tmem_ld_32x32b_x32(base + 32, v);  // dx = 1 block
+                    ptx::tmem_ld_wait();
 #pragma unroll
-                for (int c = 0; c < ((a.debug & 4) ? 0 : 32); ++c) {
-                    const int g = c & 3;
-                    const float h = tanh_fast(s[c] + b2s[c]);
-                    const float2 hh = make_float2(h, h);
-                    const float4 w0 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride);
-                    const float4 w1 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride + 4);
-                    v01[g] = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01[g]);
-                    v23[g] = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23[g]);
-                    v45[g] = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45[g]);
-                    v67[g] = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67[g]);
-                    v8[g] = fmaf(w3s[c * kW3Stride + 8], h, v8[g]);
-                }
+                    for (int c = 0; c < 32; ++c) s[c] = (lane == 0 ? 0.f : s[c]) + __uint_as_float(v[c]);
+                    ptx::tmem_ld_32x32b_x32(base + 64, v);  // dx = 2 block
+                    ptx::tmem_ld_wait();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&acc_empty[q]);
 #pragma unroll
-                for (int g = 1; g < 4; ++g) {
-                    v01[0].x += v01[g].x; v01[0].y += v01[g].y;
-                    v23[0].x += v23[g].x; v23[0].y += v23[g].y;
-                    v45[0].x += v45[g].x; v45[0].y += v45[g].y;
-                    v67[0].x += v67[g].x; v67[0].y += v67[g].y;
-                    v8[0] += v8[g];
-                }
-                const float vv[9] = {v01[0].x, v01[0].y, v23[0].x, v23[0].y, v45[0].x,
-                                     v45[0].y, v67[0].x, v67[0].y, v8[0]};
-                // fold horizontal taps: lane x3 takes v[ky][0] from x3-1, v[ky][2] from x3+1
-                float tk[3];
+                    for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
+                    if (lane == 0) {
 #pragma unroll
-                for (int ky = 0; ky < 3; ++ky) {
-                    const float up = __shfl_up_sync(0xffffffffu, vv[ky * 3 + 0], 1);
-                    const float dn = __shfl_down_sync(0xffffffffu, vv[ky * 3 + 2], 1);
-                    tk[ky] = vv[ky * 3 + 1] + (lane == 0 ? 0.f : up) + (lane == 31 ? 0.f : dn);
-                    if (lane == 31) xv0[(par * 4 + ew) * 4 + ky] = vv[ky * 3 + 0];
-                    if (lane == 0) xv2[(par * 4 + ew) * 4 + ky] = vv[ky * 3 + 2];
-                }
-                asm volatile("bar.sync 2, 128;" ::: "memory");
-                if (lane == 0 && xl) {
+                        for (int c = 0; c < 32; c += 4)
+                            *reinterpret_cast<float4*>(xd2 + (par * 4 + ew) * 32 + c) =
+                                make_float4(t[c], t[c + 1], t[c + 2], t[c + 3]);
+                    }
 #pragma unroll
-                    for (int ky = 0; ky < 3; ++ky) tk[ky] += xv0[(par * 4 + ew - 1) * 4 + ky];
-                }
-                if (lane == 31 && xr) {
+                    for (int c = 0; c < 32; ++c) {
+                        const float dn = __shfl_down_sync(0xffffffffu, t[c], 1);
+                        if (lane != 31) s[c] += dn;
+                    }
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    if (lane == 0 && xl) {
 #pragma unroll
-                    for (int ky = 0; ky < 3; ++ky) tk[ky] += xv2[(par * 4 + ew + 1) * 4 + ky];
-                }
-                // h at row y feeds output rows y+1 (ky=0), y (ky=1), y-1 (ky=2)
-                acc3[(y + 1) % 3] += tk[0];
-                acc3[y % 3] += tk[1];
-                if (y >= 1) {
-                    const int yo = y - 1;
-                    const float o = acc3[yo % 3] + tk[2];
-                    acc3[yo % 3] = 0.f;
-                    if (col_ok) om[(int64_t)yo * a.ldo + x] = xres_m + a.alpha * (b3 + o);
-                }
-                if (y == n - 1) {
-                    const float o = acc3[y % 3];
-                    acc3[y % 3] = 0.f;
-                    if (col_ok) om[(int64_t)y * a.ldo + x] = xres_0 + a.alpha * (b3 + o);
+                        for (int c = 0; c < 32; c += 4) {
+                            const float4 e4 = *reinterpret_cast<const float4*>(xd0 + (par * 4 + ew - 1) * 32 + c);
+                            s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
+                        }
+                    }
+                    if (lane == 31 && xr) {
+#pragma unroll
+                        for (int c = 0; c < 32; c += 4) {
+                            const float4 e4 = *reinterpret_cast<const float4*>(xd2 + (par * 4 + ew + 1) * 32 + c);
+                            s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
+                        }
+                    }
+                    layer3(y, s, par, acc3, xm, om, col_ok);
                 }
             }
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 2) ptx::tmem_dealloc(tmem, 512);
+    if (warp == 2) ptx::tmem_dealloc(tmem, L::kTmemAlloc);
 }
 
 }  // namespace
@@ -476,6 +580,9 @@ bool cnn3_tc_applicable(int n_layers, const int* widths, int rows, int cols) {
     return n_layers == 3 && widths[0] == 2 && widths[1] == C1 && widths[2] == C2 &&
            widths[3] == 1 && (cols == 32 || cols == 64 || cols == W) && rows >= 2;
 }
+
+template <bool SH>
+int launch_cnn3(const Cnn3Args& a, int grid, cudaStream_t st);
 
 int cnn3_tc_forward(const float* weights, const float* biases, float alpha, const float* x,
                     int64_t ldx, const float* u, int64_t ldu, float* out, int64_t ldo, int rows,
@@ -498,18 +605,25 @@ int cnn3_tc_forward(const float* weights, const float* biases, float alpha, cons
         const char* e = getenv("ENKS_CNN_DEBUG");
         a.debug = e ? atoi(e) : 0;
     }
+    const int grid = (int)(n_members < kNumSMs ? n_members : kNumSMs);
+    if (cols == W) return launch_cnn3<true>(a, grid, st);
+    return launch_cnn3<false>(a, grid, st);
+}
+
+template <bool SH>
+int launch_cnn3(const Cnn3Args& a, int grid, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(cnn3_tc_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        cudaError_t e = cudaFuncSetAttribute(cnn3_tc_kernel<SH>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             CL<SH>::kSmem);
         if (e != cudaSuccess) {
             set_error("cnn3_tc: smem attribute: %s", cudaGetErrorString(e));
             return ENKS_E_CUDA;
         }
         configured = true;
     }
-    const int grid = (int)(n_members < kNumSMs ? n_members : kNumSMs);
-    cnn3_tc_kernel<<<grid, kThreads, kSmem, st>>>(a);
+    cnn3_tc_kernel<SH><<<grid, kThreads, CL<SH>::kSmem, st>>>(a);
     return check_launch("enks_cnn_forward(tcgen05)");
 }
 
