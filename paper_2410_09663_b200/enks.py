@@ -35,6 +35,7 @@ __all__ = [
     "update",
     "smooth_horizon",
     "set_default_comm",
+    "HorizonGraph",
 ]
 
 _OPS = None
@@ -244,12 +245,74 @@ def update(ens: TrajectoryEnsemble, y_ref: np.ndarray, vs, streams,
     return ens
 
 
+class HorizonGraph:
+    """One whole horizon solve (reset + H x (predict, update)) captured as a CUDA graph.
+
+    Static device inputs ``x0`` ((d x m)) and ``y_refs`` ((h, p, m)) are copied in before each
+    ``replay``; the result is the engine's ``mean``.  The noise substreams (seed, prefix), the
+    model and the virtual system are baked into the graph.  Every kernel of the eager path runs
+    on replay (same launches, same order, side-stream gain solve included) -- the graph only
+    removes the per-launch host cost, which dominates small problems."""
+
+    def __init__(self, x0, vs, h: int, n_members: int, streams, comm=None):
+        packed = np.asarray(x0.packed, dtype=float)
+        lam = 1.0 / float(np.trace(vs.shared_col_cov))
+        ops = _ops()
+        self.h, self.vs, self.streams = int(h), vs, streams
+        self.eng = DeviceSmoother(ops, packed, x0.n, x0.l, n_members, lam, capacity=h,
+                                  comm=comm or _comm())
+        self.eng.bind(vs)
+        self.x0 = ops.to_device(packed)
+        self.y_refs = ops.zeros(h, vs.obs_rows, packed.shape[1])
+        self._run()  # warm-up: kernel attributes, workspaces, tensor maps
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._run()
+
+    def _run(self) -> None:
+        eng = self.eng
+        eng.reset(self.x0)
+        for step in range(self.h):
+            eng.predict(self.vs, self.streams)
+            eng.update(self.y_refs[step], self.streams)
+
+    def replay(self) -> DeviceSmoother:
+        eng = self.eng
+        eng.status.zero_()  # per-solve failure flags, as a fresh eager engine would have
+        fc = getattr(eng, "forecast", None)
+        if fc is not None and fc.kind == "burgers":
+            fc.vmax.zero_()
+            fc.flags.zero_()
+        self.graph.replay()
+        eng.t = self.h
+        eng.n_upd = self.h
+        return eng
+
+
+_GRAPHS: dict = {}
+
+
+def _graph_for(x0, vs, h, n_members, streams) -> HorizonGraph:
+    key = (id(vs), id(vs.model), tuple(np.shape(x0.packed)), x0.n, x0.l, int(h), int(n_members),
+           int(streams.seed), tuple(streams.prefix), id(_COMM))
+    g = _GRAPHS.get(key)
+    if g is None or g.vs is not vs:
+        if len(_GRAPHS) >= 8:
+            _GRAPHS.pop(next(iter(_GRAPHS)))
+        g = _GRAPHS[key] = HorizonGraph(x0, vs, h, n_members, streams)
+    return g
+
+
 def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
-                   track_cov: bool = False):
+                   track_cov: bool = False, *, graph: bool = False):
     """Forward predict/update sweep over an h-step horizon (enks.py:256-284).
 
     Returns the mean trajectory (h+1, n+2l, m) as fp64 and the covariances
-    when ``track_cov``.  One host synchronisation at the end.
+    when ``track_cov``.  One host synchronisation at the end.  ``graph=True`` (keyword-only
+    extension) replays a cached CUDA graph of the whole horizon for this (virtual system,
+    shapes, h, N, noise streams): x0 and y_refs are copied into its static inputs, so the
+    model / weights must not be mutated between calls (rebuild the VirtualSystem instead).
     """
     if h < 1:
         raise ValueError("horizon must be at least 1")
@@ -260,6 +323,13 @@ def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
         raise ValueError(f"need {h} reference observations, got {y_refs.shape[0]}")
     if y_refs.shape[1:] != (vs.obs_rows, x0.m):
         raise ValueError(f"y_ref shape {y_refs.shape[1:]} != observation {(vs.obs_rows, x0.m)}")
+    if graph and not track_cov and n_members >= 2 and torch.cuda.is_available():
+        g = _graph_for(x0, vs, h, n_members, streams)
+        g.x0.copy_(torch.from_numpy(np.asarray(x0.packed, dtype=np.float32)), non_blocking=False)
+        g.y_refs.copy_(torch.from_numpy(np.ascontiguousarray(y_refs, dtype=np.float32)))
+        eng = g.replay()
+        eng.check_status()
+        return eng.mean_host().reshape(h + 1, eng.d, eng.m), None
     ens = init_ensemble(x0, n_members, shared_col_cov=vs.shared_col_cov, capacity=h)
     eng = ens._eng
     eng.bind(vs)

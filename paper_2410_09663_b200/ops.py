@@ -53,6 +53,9 @@ class DeviceOps:
                                    else torch.device(device).index or 0)
         self._ws = None
         self._ws_sum = None
+        # workspaces replaced by larger ones are retained (never freed): a captured CUDA graph
+        # (enks.HorizonGraph) may still hold their addresses
+        self._retired = []
         self.launches = 0  # kernel launches issued through the C-ABI (bench's gpu_launches)
         self.profile = None  # list -> (tag, start_event, end_event, algorithmic_flops) per tagged op
 
@@ -71,11 +74,17 @@ class DeviceOps:
         if nbytes <= 0:
             return 0
         if self._ws is None or self._ws.numel() < nbytes:
+            self._retire(self._ws)
             self._ws = torch.empty(int(nbytes * 1.25) + 256, dtype=torch.uint8, device=self.device)
         return self._ws.data_ptr()
 
+    def _retire(self, buf) -> None:
+        if buf is not None:
+            self._retired.append(buf)
+
     def _workspace_sum(self, nbytes: int) -> int:
         if self._ws_sum is None or self._ws_sum.numel() < nbytes:
+            self._retire(self._ws_sum)
             self._ws_sum = torch.empty(int(nbytes * 1.25) + 256, dtype=torch.uint8,
                                        device=self.device)
         return self._ws_sum.data_ptr()
@@ -155,6 +164,7 @@ class DeviceOps:
                               inv_scale, f32=None, rows_f32=0):
         rows = src.shape[0]
         if getattr(self, "_scale_ws", None) is None or self._scale_ws.numel() < rows:
+            self._retire(getattr(self, "_scale_ws", None))
             self._scale_ws = torch.empty(max(rows, 4096), dtype=torch.float32, device=self.device)
         self.launches += 2
         K = n_members * cols
@@ -330,6 +340,7 @@ class DeviceOps:
     def spd_inverse(self, S, scale, inv, status, jitter):
         p = S.shape[0]
         if getattr(self, "_spd_ws", None) is None or self._spd_ws.numel() < p * p:
+            self._retire(getattr(self, "_spd_ws", None))
             self._spd_ws = torch.empty(p * p, dtype=torch.float32, device=self.device)
         self.launches += 2
         with self._prof("gain_solve", p ** 3 * (1.0 / 3 + 1.0 / 3 + 1.0)):
@@ -359,6 +370,7 @@ class DeviceOps:
         wsp = None
         if ws:
             if getattr(self, "_bur_ws", None) is None or self._bur_ws.numel() * 4 < ws:
+                self._retire(getattr(self, "_bur_ws", None))
                 self._bur_ws = torch.empty((ws + 3) // 4, dtype=torch.float32, device=self.device)
             wsp = self._bur_ws
         self.launches += 1 if not ws else sub

@@ -193,3 +193,22 @@ def test_track_cov_tensor_core_path_matches_oracle(pm):
     for k in ("sigma_traj", "sigma_cross", "sigma_pred"):
         assert getattr(cov, k).shape == getattr(rcov, k).shape
         assert _rel(getattr(cov, k), getattr(rcov, k)) < TOL, k
+
+
+def test_cuda_graph_horizon_bit_identical_to_eager(pm):
+    """smooth_horizon(graph=True) replays a captured horizon: same kernels, same results."""
+    from oracle import problems
+    from paper_2410_09663_b200 import enks
+
+    pr = problems.make_cnn_problem(pm, "C1", size=32, n_members=64, horizon=4,
+                                   widths=(2, 32, 32, 1))
+    st = pm.matvar.NoiseStreams(seed=3)
+    eager, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, st)
+    g1, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, st, graph=True)
+    g2, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, st, graph=True)  # replay
+    assert np.array_equal(g1, eager) and np.array_equal(g2, eager)
+    # new static inputs through the same graph
+    x1 = pm.virtualsys.AugmentedState(pr.x0.x * 0.5, pr.x0.u, pr.x0.du)
+    e1, _ = enks.smooth_horizon(x1, pr.y_ref, pr.vs, pr.H, pr.N, st)
+    g3, _ = enks.smooth_horizon(x1, pr.y_ref, pr.vs, pr.H, pr.N, st, graph=True)
+    assert np.array_equal(g3, e1)
