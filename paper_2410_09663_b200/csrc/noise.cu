@@ -128,7 +128,7 @@ __device__ __forceinline__ double u64_to_unit(uint64_t r) {
 // Otherwise each batch of accepted normals is stored straight away (any cols / alignment).
 template <bool RB>
 __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
-    const Job& a = args.job[blockIdx.y];
+    const Job a = args.job[blockIdx.y];  // by value: fields live in registers, not re-read
     __shared__ __align__(16) float s_row[RB ? kWarps : 1][RB ? 2 * kMaxRowCols : 1];
     __shared__ uint64_t s_ki[256];
     __shared__ double s_wi[256];
@@ -147,10 +147,11 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
     const int cols = args.cols;
 
     uint64_t* buf = s_buf[warp];
-    const int64_t total = (int64_t)a.rows * cols;
+    // 32-bit stream positions: a stream holds rows * cols < 2^31 normals (checked on the host)
+    const int total = a.rows * cols;
     const int64_t col0 = local * cols;
-    int64_t base_w = -(1LL << 40);  // buffer holds words [base_w, base_w + 128)
-    int64_t w = 0, q = 0;
+    int base_w = -(1 << 30);  // buffer holds words [base_w, base_w + 128)
+    int w = 0, q = 0;
 
     // (row, col) of normal q, tracked incrementally: (rb, jb) is the position of q (warp-uniform)
     int rb = 0, jb = 0;
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
     }
 
     // warp-uniform access to word `ww` (slow path only)
-    auto word = [&](int64_t ww) -> uint64_t {
+    auto word = [&](int ww) -> uint64_t {
         if (ww >= base_w && ww < base_w + kBufWords) return buf[ww - base_w];
         Block4 b = philox(k0, k1, (uint64_t)(ww >> 2) + 1);
         int s = (int)(ww & 3);
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
         const bool ok = rabs < s_ki[idx];
         const unsigned bad = __ballot_sync(0xffffffffu, !ok);
         const int n_ok = bad ? (__ffs(bad) - 1) : 32;
-        const int n_emit = (int)min((int64_t)n_ok, total - q);
+        const int n_emit = min(n_ok, total - q);
         if (RB) {
             if (lane < n_emit) emit_rb(lane, x);
         } else if (lane < n_emit) {
@@ -346,6 +347,8 @@ int launch_noise(const uint32_t* head, int n_head, int64_t member0, int64_t n_me
         ENKS_REQUIRE(jobs[j].out || jobs[j].out_plus, "enks_noise_fill: job %d has no output", j);
         ENKS_REQUIRE(!jobs[j].out_plus || jobs[j].base, "enks_noise_fill: out_plus needs base");
         ENKS_REQUIRE(jobs[j].rows > 0, "enks_noise_fill: job %d has no rows", j);
+        ENKS_REQUIRE((int64_t)jobs[j].rows * cols < (1LL << 30),
+                     "enks_noise_fill: rows * cols must be < 2^30 per stream");
         a.job[j] = jobs[j];
     }
     // row-staged path when every job's rows can be written as aligned float4 rows
