@@ -119,6 +119,47 @@ __global__ void center_f16pair_kernel(const float* __restrict__ src, int64_t ld,
     l[r * ldh + k] = __float2half_rn(v - __half2float(hv));
 }
 
+// vectorised variant: 4 consecutive columns per thread (cols % 4 == 0, 16-B aligned rows)
+__global__ void center_f16pair_v4_kernel(const float* __restrict__ src, int64_t ld, int rows,
+                                         int64_t n, int cols, const float* __restrict__ z0,
+                                         const double* __restrict__ acc, double inv_n,
+                                         float* __restrict__ mean, __half* __restrict__ h,
+                                         __half* __restrict__ l, int64_t ldh,
+                                         const float* __restrict__ scale, float* __restrict__ f32,
+                                         int64_t ldf, int rows_f32) {
+    const int64_t K = n * cols;
+    const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
+    const int64_t r = blockIdx.y;
+    if (k >= K) return;
+    const int j = (int)((uint32_t)k % (uint32_t)cols);
+    const float4 x = __ldg(reinterpret_cast<const float4*>(src + r * ld + k));
+    const float4 zz = __ldg(reinterpret_cast<const float4*>(z0 ? z0 + r * cols + j : src + r * ld + j));
+    const double2 a01 = __ldg(reinterpret_cast<const double2*>(acc + r * cols + j));
+    const double2 a23 = __ldg(reinterpret_cast<const double2*>(acc + r * cols + j + 2));
+    const float m0 = (float)(a01.x * inv_n), m1 = (float)(a01.y * inv_n);
+    const float m2 = (float)(a23.x * inv_n), m3 = (float)(a23.y * inv_n);
+    if (mean && k < cols)
+        *reinterpret_cast<float4*>(mean + r * cols + j) =
+            make_float4(zz.x + m0, zz.y + m1, zz.z + m2, zz.w + m3);
+    const float4 an = make_float4((x.x - zz.x) - m0, (x.y - zz.y) - m1, (x.z - zz.z) - m2,
+                                  (x.w - zz.w) - m3);
+    if (f32 && r < rows_f32) *reinterpret_cast<float4*>(f32 + r * ldf + k) = an;
+    const float sc = scale[r];
+    const float v[4] = {an.x * sc, an.y * sc, an.z * sc, an.w * sc};
+    __half hv[4], lv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        hv[q] = __float2half_rn(v[q]);
+        lv[q] = __float2half_rn(v[q] - __half2float(hv[q]));
+    }
+    *reinterpret_cast<uint2*>(h + r * ldh + k) =
+        make_uint2(__half_as_ushort(hv[0]) | ((uint32_t)__half_as_ushort(hv[1]) << 16),
+                   __half_as_ushort(hv[2]) | ((uint32_t)__half_as_ushort(hv[3]) << 16));
+    *reinterpret_cast<uint2*>(l + r * ldh + k) =
+        make_uint2(__half_as_ushort(lv[0]) | ((uint32_t)__half_as_ushort(lv[1]) << 16),
+                   __half_as_ushort(lv[2]) | ((uint32_t)__half_as_ushort(lv[3]) << 16));
+}
+
 // mean[r, j] = z0 + mu_sh; anom[r, i*cols + j] = (src - z0) - mu_sh
 __global__ void center_kernel(const float* __restrict__ src, int64_t ld, int rows, int64_t n,
                               int cols, const float* __restrict__ z0,
@@ -212,9 +253,20 @@ int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64
     int rc = enks::check_launch("enks_member_center_f16pair(scale)");
     if (rc) return rc;
     const int64_t K = n_members * cols;
-    enks::center_f16pair_kernel<<<dim3((unsigned)((K + 255) / 256), (unsigned)rows), 256, 0, st>>>(
-        src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
-        static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32);
+    auto a16 = [](const void* ptr) { return ((uintptr_t)ptr & 15) == 0; };
+    const bool v4 = cols % 4 == 0 && ld_src % 4 == 0 && ldh % 4 == 0 && a16(src) &&
+                    ((uintptr_t)h & 7) == 0 && ((uintptr_t)l & 7) == 0 && (!z0 || a16(z0)) &&
+                    a16(acc) && (!mean || a16(mean)) && (!f32 || (a16(f32) && ld_f32 % 4 == 0));
+    if (v4)
+        enks::center_f16pair_v4_kernel<<<dim3((unsigned)((K / 4 + 255) / 256), (unsigned)rows), 256,
+                                         0, st>>>(
+            src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
+            static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32);
+    else
+        enks::center_f16pair_kernel<<<dim3((unsigned)((K + 255) / 256), (unsigned)rows), 256, 0,
+                                      st>>>(
+            src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
+            static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32);
     return enks::check_launch("enks_member_center_f16pair");
 }
 
