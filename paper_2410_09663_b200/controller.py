@@ -33,7 +33,7 @@ import numpy as np
 import torch
 
 from .engine import DeviceSmoother, Forecaster, LocalComm
-from .matvar import NoiseStreams
+from .matvar import NoiseStreams, entropy_head
 from .virtualsys import AugmentedState, MpcWeights, build_virtual_system
 
 __all__ = ["ControllerConfig", "ClosedLoopTrace", "rmse", "mpc_step", "run_closed_loop",
@@ -160,9 +160,11 @@ class DeviceClosedLoop:
             self.ops.gemm(winv, e, we)
             self.ops.quad_form(e, we, out, accumulate=accumulate)
 
-    def _plan(self, k: int) -> None:
+    def _plan(self, k: int, set_head: bool = True) -> None:
         """Smooth H steps from (plant x, prev u, dU0) with streams child(k); keep the U plan."""
         eng, n, l, d, H = self.eng, self.n, self.l, self.d, self.cfg.horizon_h
+        if set_head and eng.dev_head is not None:
+            eng.dev_head.set(entropy_head(self.cfg.seed, (k,)))
         self.x0[:n + l].copy_(self.plant)
         if self.cfg.warm_start:
             self.x0[n + l:].copy_(self.plan_du)
@@ -192,9 +194,50 @@ class DeviceClosedLoop:
         self._quad(eu, "u", cost_out, True)
         self._quad(self.du, "du", cost_out, True)
 
+    # ------------------------------------------------------------ CUDA graph of one MPC step
+    def _graph_body(self) -> None:
+        """plan (smoother with the device-resident noise head) + plant step + metrics into fixed
+        buffers; captured once, replayed per control step with the head of child(k)."""
+        self._plan(0, set_head=False)
+        u = self.plan[0]
+        self.ctl_cur.copy_(u)
+        self._plant_step(u, self.rm_cur, self.cost_cur)
+
+    def _ensure_graph(self) -> None:
+        if getattr(self, "graph", None) is not None:
+            return
+        from .ops import DeviceHead
+
+        ops = self.ops
+        words = entropy_head(self.cfg.seed, (0,))
+        self.dev_head = DeviceHead(ops.zeros(32, dtype=torch.int32), len(words))
+        self.dev_head.set(words)
+        self.eng.dev_head = self.dev_head
+        self.ctl_cur = ops.zeros(self.l, self.m)
+        self.rm_cur = ops.zeros(1, dtype=torch.float64)
+        self.cost_cur = ops.zeros(1, dtype=torch.float64)
+        saved = (self.plant.clone(), self.plan.clone(), self.plan_du.clone())
+        self._graph_body()  # warm-up (kernel attributes, workspaces); the state is restored
+        torch.cuda.synchronize()
+        self.plant.copy_(saved[0])
+        self.plan.copy_(saved[1])
+        self.plan_du.copy_(saved[2])
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._graph_body()
+
     # ------------------------------------------------------------ run
-    def run(self, steps: int, record_every: int = 0) -> ClosedLoopTrace:
+    def run(self, steps: int, record_every: int = 0, graph: bool | None = None) -> ClosedLoopTrace:
+        """``graph`` (default: on a CUDA device with apply_mode='first_action') replays one
+        captured MPC step per control step; the noise head of child(k) is rewritten in device
+        memory before each replay.  Same kernels and results as the eager loop."""
         ops, n, l, m, H = self.ops, self.n, self.l, self.m, self.cfg.horizon_h
+        if graph is None:
+            graph = ops.device.type == "cuda" and self.cfg.apply_mode == "first_action"
+        if graph:
+            if self.cfg.apply_mode != "first_action":
+                raise ValueError("graph replay supports apply_mode='first_action' only")
+            return self._run_graph(steps, record_every)
         rm = ops.zeros(max(steps, 1), dtype=torch.float64)
         cost = ops.zeros(max(steps, 1), dtype=torch.float64)
         controls = ops.zeros(max(steps, 1), l, m)
@@ -236,6 +279,55 @@ class DeviceClosedLoop:
                                cost=cost[:steps].cpu().numpy(), smoother_time=times,
                                rmse0=float(r0.item()),
                                fields=[f.double().cpu().numpy() for f in fields])
+
+
+def _run_graph_impl(self, steps: int, record_every: int) -> ClosedLoopTrace:
+    ops, n, l, m = self.ops, self.n, self.l, self.m
+    rm = ops.zeros(max(steps, 1), dtype=torch.float64)
+    cost = ops.zeros(max(steps, 1), dtype=torch.float64)
+    controls = ops.zeros(max(steps, 1), l, m)
+    r0 = ops.zeros(1, dtype=torch.float64)
+    ex0 = self.err[:n]
+    ops.sub(self.plant[:n], self.x_ref, ex0)
+    ops.quad_form(ex0, ex0, r0, scale=1.0 / ex0.numel())
+    self._ensure_graph()
+    # the heads of child(0 .. steps-1), uploaded once; per step a device-to-device copy (async)
+    heads = np.zeros((max(steps, 1), 32), dtype=np.uint32)
+    for s in range(steps):
+        w = entropy_head(self.cfg.seed, (s,))
+        if len(w) != self.dev_head.n:
+            raise ValueError("noise head length changed across control steps")
+        heads[s, :len(w)] = w
+    heads_dev = ops.to_device(heads.view(np.int32), dtype=torch.int32)
+    events, fields = [], []
+    for s in range(steps):
+        self.dev_head.words.copy_(heads_dev[s])
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        self.graph.replay()
+        ev1.record()
+        events.append((ev0, ev1))
+        controls[s].copy_(self.ctl_cur)
+        rm[s:s + 1].copy_(self.rm_cur)
+        cost[s:s + 1].copy_(self.cost_cur)
+        if record_every and (s + 1) % record_every == 0:
+            fields.append(self.plant[:n].clone())
+    self.eng.t = self.cfg.horizon_h
+    self.eng.check_status()
+    if self.plant_fc.kind == "burgers":
+        self.plant_fc.check_cfl()
+    ctl = controls[:steps].double().cpu().numpy()
+    if not np.all(np.isfinite(ctl)):
+        raise FloatingPointError("non-finite control in the closed loop")
+    times = np.array([a.elapsed_time(b) * 1e-3 for a, b in events]) if events else np.zeros(0)
+    return ClosedLoopTrace(controls=ctl, rmse=rm[:steps].cpu().numpy(),
+                           cost=cost[:steps].cpu().numpy(), smoother_time=times,
+                           rmse0=float(r0.item()),
+                           fields=[f.double().cpu().numpy() for f in fields])
+
+
+DeviceClosedLoop._run_graph = _run_graph_impl
 
 
 def run_closed_loop(plant, model, cfg: ControllerConfig, steps: int, x_init, u_init=None,

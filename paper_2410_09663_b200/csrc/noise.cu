@@ -113,6 +113,7 @@ constexpr int kMaxJobs = 4;
 
 struct Args {
     Head head;
+    const uint32_t* head_dev;  // non-null: head words read from device memory (graph replays)
     int64_t member0, n_members;
     int cols;
     Job job[kMaxJobs];
@@ -143,7 +144,15 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
     const int64_t local = (int64_t)blockIdx.x * kWarps + warp;
     if (local >= args.n_members) return;
     uint64_t k0, k1;
-    seed_key(args.head, (uint32_t)(args.member0 + local), a.t, a.ch, k0, k1);
+    if (args.head_dev) {
+        Head hd;
+        hd.n = args.head.n;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) hd.w[q] = q < hd.n ? __ldg(args.head_dev + q) : 0u;
+        seed_key(hd, (uint32_t)(args.member0 + local), a.t, a.ch, k0, k1);
+    } else {
+        seed_key(args.head, (uint32_t)(args.member0 + local), a.t, a.ch, k0, k1);
+    }
     const int cols = args.cols;
 
     uint64_t* buf = s_buf[warp];
@@ -329,8 +338,8 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
 namespace enks {
 namespace {
 int launch_noise(const uint32_t* head, int n_head, int64_t member0, int64_t n_members, int cols,
-                 const Job* jobs, int n_jobs, cudaStream_t st) {
-    ENKS_REQUIRE(head != nullptr && n_head >= 4 && n_head <= 32,
+                 const Job* jobs, int n_jobs, cudaStream_t st, const uint32_t* head_dev = nullptr) {
+    ENKS_REQUIRE((head != nullptr || head_dev != nullptr) && n_head >= 4 && n_head <= 32,
                  "enks_noise_fill: need 4..32 head words (seed padded to 4 + prefix), got %d",
                  n_head);
     ENKS_REQUIRE(n_jobs >= 1 && n_jobs <= kMaxJobs, "enks_noise_fill: 1..%d jobs", kMaxJobs);
@@ -338,8 +347,9 @@ int launch_noise(const uint32_t* head, int n_head, int64_t member0, int64_t n_me
                  "enks_noise_fill: member ids must fit in uint32");
     if (n_members <= 0 || cols <= 0) return ENKS_OK;
     Args a;
-    for (int q = 0; q < 32; ++q) a.head.w[q] = q < n_head ? head[q] : 0u;
+    for (int q = 0; q < 32; ++q) a.head.w[q] = (head && q < n_head) ? head[q] : 0u;
     a.head.n = n_head;
+    a.head_dev = head_dev;
     a.member0 = member0;
     a.n_members = n_members;
     a.cols = cols;
@@ -395,4 +405,23 @@ extern "C" int enks_noise_fill_multi(const uint32_t* head, int n_head, int64_t m
                             base[q], ld_base[q], out_plus[q], ld_plus[q]};
     return enks::launch_noise(head, n_head, member0, n_members, cols, jobs, n_jobs,
                               enks::as_stream(stream));
+}
+
+extern "C" int enks_noise_fill_multi_dev(const uint32_t* head_dev, int n_head, int64_t member0,
+                                         int64_t n_members, int cols, int n_jobs,
+                                         const uint32_t* t, const uint32_t* channel,
+                                         const int* rows, const double* const* diag,
+                                         float* const* out, const int64_t* ld_out,
+                                         const float* const* base, const int64_t* ld_base,
+                                         float* const* out_plus, const int64_t* ld_plus,
+                                         void* stream) {
+    ENKS_REQUIRE(head_dev, "enks_noise_fill_multi_dev: null head");
+    ENKS_REQUIRE(n_jobs >= 1 && n_jobs <= enks::kMaxJobs, "enks_noise_fill_multi_dev: 1..%d jobs",
+                 enks::kMaxJobs);
+    enks::Job jobs[enks::kMaxJobs];
+    for (int q = 0; q < n_jobs; ++q)
+        jobs[q] = enks::Job{t[q], channel[q], rows[q], diag[q], out[q], ld_out[q],
+                            base[q], ld_base[q], out_plus[q], ld_plus[q]};
+    return enks::launch_noise(nullptr, n_head, member0, n_members, cols, jobs, n_jobs,
+                              enks::as_stream(stream), head_dev);
 }

@@ -252,6 +252,7 @@ class DeviceSmoother:
         self.slice0_zero = True  # all members start as identical copies (enks.py:120)
         self._bound = None
         self.barrier = None
+        self.dev_head = None  # ops.DeviceHead: noise entropy words read from device memory
         self._basis = basis
         d, q, K = self.d, self.q, self.K
         self.slice_raw = ops.empty(d, K)      # [X; U; W] of the newest predicted slice
@@ -432,6 +433,12 @@ class DeviceSmoother:
         self._bound = vs
 
     # ------------------------------------------------------------ helpers
+    def _head(self, streams):
+        """Entropy words of the streams' (seed, prefix), or the device-resident words."""
+        if self.dev_head is not None:
+            return self.dev_head
+        return entropy_head(streams.seed, tuple(streams.prefix))
+
     def _side_stream(self):
         """Second CUDA stream for the gain solve (None off-GPU)."""
         if getattr(self.ops, "device", None) is None or self.ops.device.type != "cuda":
@@ -525,7 +532,7 @@ class DeviceSmoother:
         if tau > self.cap:
             self._grow(max(2 * self.cap, tau))
         ops, n, l, d = self.ops, self.n, self.l, self.d
-        head = entropy_head(streams.seed, tuple(streams.prefix))
+        head = self._head(streams)
         sr, ob = self.slice_raw, self.obs_raw
         self.forecast(ops, self.last, sr[:n], n, self.Nl)
         if self.fused_noise:
@@ -562,7 +569,7 @@ class DeviceSmoother:
         n, l, d, p, tau = self.n, self.l, self.d, self.p, self.t
         if tau < 1:
             raise RuntimeError("update before the first predict")
-        head = entropy_head(streams.seed, tuple(streams.prefix))
+        head = self._head(streams)
         sr, ob = self.slice_raw, self.obs_raw
         # perturbed observations [x + v_x; u + v_u]  (enks.py:194-200)
         if self._obs_t != tau or self._obs_key != (streams.seed, tuple(streams.prefix)):

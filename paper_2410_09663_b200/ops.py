@@ -33,6 +33,20 @@ def _p(t):
     return None if t is None else t.data_ptr()
 
 
+class DeviceHead:
+    """Noise entropy words kept in device memory (int32 tensor, first n used): a captured CUDA
+    graph reads them at replay, so one capture serves every NoiseStreams.child(k)."""
+
+    def __init__(self, words, n: int):
+        self.words, self.n = words, int(n)
+
+    def set(self, host_words) -> None:
+        w = [int(x) for x in host_words]
+        if len(w) != self.n:
+            raise ValueError(f"head has {len(w)} words, the capture used {self.n}")
+        self.words[:self.n].copy_(torch.tensor(np.array(w, dtype=np.uint32).view(np.int32)))
+
+
 def choose_split(M: int, N: int, K: int, bm: int = 128, bn: int = 128, min_k: int = 2048) -> int:
     """Split-K factor so that a tall-skinny contraction fills the 148 SMs (>= 2 waves)."""
     tiles = -(-M // bm) * -(-N // bn)
@@ -109,6 +123,10 @@ class DeviceOps:
     # -- kernels ----------------------------------------------------------
     def noise_fill(self, head, t, ch, member0, n_members, rows, cols, diag=None, out=None,
                    base=None, out_plus=None):
+        if isinstance(head, DeviceHead):
+            self.noise_fill_multi(head, member0, n_members, cols, [dict(
+                t=t, ch=ch, rows=rows, diag=diag, out=out, base=base, out_plus=out_plus)])
+            return
         words = (ctypes.c_uint32 * len(head))(*[int(w) for w in head])
         self.launches += 1
         nb = 4 * rows * cols * n_members * ((out is not None) + 2 * (out_plus is not None))
@@ -127,7 +145,8 @@ class DeviceOps:
     def noise_fill_multi(self, head, member0, n_members, cols, jobs):
         """jobs: list of dicts (t, ch, rows, diag, out, base, out_plus); one launch."""
         n = len(jobs)
-        words = (ctypes.c_uint32 * len(head))(*[int(w) for w in head])
+        words = None if isinstance(head, DeviceHead) else \
+            (ctypes.c_uint32 * len(head))(*[int(w) for w in head])
         u32 = ctypes.c_uint32 * n
         vp = ctypes.c_void_p * n
         i64 = ctypes.c_int64 * n
@@ -140,7 +159,11 @@ class DeviceOps:
             self._noise_multi(words, head, member0, n_members, cols, n, u32, vp, i64, get, jobs)
 
     def _noise_multi(self, words, head, member0, n_members, cols, n, u32, vp, i64, get, jobs):
-        _lib.call("enks_noise_fill_multi", words, len(head), int(member0), int(n_members), int(cols),
+        if isinstance(head, DeviceHead):
+            fn, words, n_head = "enks_noise_fill_multi_dev", _p(head.words), head.n
+        else:
+            fn, n_head = "enks_noise_fill_multi", len(head)
+        _lib.call(fn, words, n_head, int(member0), int(n_members), int(cols),
                   n, u32(*[int(j["t"]) for j in jobs]), u32(*[int(j["ch"]) for j in jobs]),
                   (ctypes.c_int * n)(*[int(j["rows"]) for j in jobs]),
                   vp(*[_p(v) for v in get("diag")]), vp(*[_p(v) for v in get("out")]),

@@ -118,3 +118,17 @@ def test_mpc_step_host_api_and_determinism(pm):
                               vs, 4, 32, seed=2, prefix=(0,), backend="c")
     assert np.abs(traj - ref).max() < 1e-4 * np.abs(ref).max()
     assert np.abs(u1 - ref[1, 4:6]).max() < 1e-4 * np.abs(ref).max()
+
+
+@pytest.mark.gpu
+def test_closed_loop_graph_replay_equals_eager(pm):
+    """One captured MPC step replayed per control step (device-resident noise head of
+    child(k)) gives exactly the eager loop's trace."""
+    from paper_2410_09663_b200.controller import DeviceClosedLoop
+
+    pr = problems.make_burgers_problem(pm, "boundary")
+    cfg = _cfg(pm, pr.vs, horizon_h=5, ensemble_n=100, seed=4)
+    eager = DeviceClosedLoop(pr.model, pr.model, cfg, pr.x0.x).run(8, graph=False)
+    g = DeviceClosedLoop(pr.model, pr.model, cfg, pr.x0.x).run(8, graph=True)
+    assert np.array_equal(g.controls, eager.controls)
+    assert np.array_equal(g.rmse, eager.rmse) and np.array_equal(g.cost, eager.cost)
