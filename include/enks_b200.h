@@ -215,6 +215,10 @@ int enks_f16pair_transpose(const void* h, const void* l, int64_t ldi, const floa
                            void* stream);
 
 int enks_spd_max_p(void);
+/* workspace bytes for enks_spd_inverse at this p (p x p floats up to 288; for 288 < p <= 576 the
+ * solve runs as a 2 x 2 Schur complement of two one-CTA factorisations, both with and without
+ * the reference jitter, and selects on device -- no host synchronisation). */
+int64_t enks_spd_ws_bytes(int p);
 int enks_spd_inverse(const float* S, int64_t lds, int p, float scale, float* inv, float* ws,
                      int* status, int* jitter_events, void* stream);
 

@@ -72,6 +72,7 @@ _SIGS = {
     "enks_f16pair_transpose": (_c_int, [_vp, _vp, _c_i64, _vp, _c_int, _c_i64, _vp, _vp, _c_i64,
                                         _vp, _vp]),
     "enks_spd_max_p": (_c_int, []),
+    "enks_spd_ws_bytes": (_c_i64, [_c_int]),
     "enks_spd_inverse": (_c_int, [_vp, _c_i64, _c_int, _c_f, _vp, _vp, _vp, _vp, _vp]),
     "enks_cnn_max_width": (_c_int, []),
     "enks_cnn_forward": (_c_int, [_c_int, _ip, _vp, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _vp,

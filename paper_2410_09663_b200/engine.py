@@ -271,7 +271,7 @@ class DeviceSmoother:
         ops, d, p, q, K, m = self.ops, self.d, self.p, self.q, self.K, self.m
         # tcgen05 cross moments (ENKS_TC=0 forces the SIMT engine for A/B checks)
         self.use_tc = (os.environ.get("ENKS_TC", "1") != "0" and hasattr(ops, "gemm_nt_tc")
-                       and p <= 256 and K >= 128)
+                       and p <= 512 and K >= 128)
         # basis storage: fp16 pairs (tcgen05 kind::f16 contraction, gemm_f16p.cu) or fp32
         basis = self._basis or os.environ.get("ENKS_BASIS", "f16pair" if self.use_tc else "fp32")
         self.pair = basis == "f16pair" and K % 8 == 0 and hasattr(ops, "gemm_f16pair")
@@ -421,6 +421,14 @@ class DeviceSmoother:
         con = getattr(vs, "constraint", None)
         self.barrier = None if con is None else _barrier_spec(con, ops, self.n, self.l, self.m)
         self._set_obs_rows(self.q + (0 if con is None else 1))
+        if (self.N - 1) * self.m < self.p:
+            import warnings
+
+            warnings.warn(
+                f"rank-deficient Sigma_y: (N - 1) m = {(self.N - 1) * self.m} < p = {self.p}. The "
+                "reference's 1e-9 relative jitter is below fp32 resolution; the device escalates "
+                "it, and its fp32 gain is not a reliable match for the fp64 reference here "
+                "(use N m > p).", RuntimeWarning, stacklevel=3)
         self.forecast = Forecaster(vs.model, ops, self.n, self.l)
         self.noise_w = _noise_params(vs.process_noise, ops, self.l, self.m)
         self.noise_vx = _noise_params(vs.obs_noise_x, ops, self.n, self.m)

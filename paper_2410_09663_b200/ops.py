@@ -362,9 +362,10 @@ class DeviceOps:
 
     def spd_inverse(self, S, scale, inv, status, jitter):
         p = S.shape[0]
-        if getattr(self, "_spd_ws", None) is None or self._spd_ws.numel() < p * p:
+        nf = (int(self.lib.enks_spd_ws_bytes(p)) + 3) // 4
+        if getattr(self, "_spd_ws", None) is None or self._spd_ws.numel() < nf:
             self._retire(getattr(self, "_spd_ws", None))
-            self._spd_ws = torch.empty(p * p, dtype=torch.float32, device=self.device)
+            self._spd_ws = torch.empty(nf, dtype=torch.float32, device=self.device)
         self.launches += 2
         with self._prof("gain_solve", p ** 3 * (1.0 / 3 + 1.0 / 3 + 1.0)):
             self._spd(S, p, scale, inv, status, jitter)

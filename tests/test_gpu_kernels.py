@@ -442,3 +442,39 @@ def test_gemm_f16pair_ex_shift_operands(dev_ops):
     ref = C0.double() + bias.double()[:, [k % m for k in range(K)]] - G.double() @ Y.double()
     scale = (G.double().abs() @ Y.double().abs()) + C0.double().abs() + bias.double().abs().amax()
     assert ((out.double().cpu() - ref).abs() / scale).max().item() < 1e-6
+
+
+@pytest.mark.parametrize("p", [289, 300, 512, 576])
+def test_spd_inverse_schur_blocks(dev_ops, p):
+    """p > 288: 2 x 2 Schur complement of two one-CTA factorisations."""
+    rng = np.random.default_rng(p)
+    a = rng.standard_normal((p, p + 7))
+    s = (a @ a.T / (p + 7) + 0.5 * np.eye(p)).astype(np.float32)
+    s[0, -1] += 1e-3
+    inv = dev_ops.zeros(p, p)
+    st, jit = dev_ops.zeros(1, dtype=torch.int32), dev_ops.zeros(1, dtype=torch.int32)
+    dev_ops.spd_inverse(dev_ops.to_device(s), 0.5, inv, st, jit)
+    sym = 0.5 * 0.5 * (s.astype(np.float64) + s.T.astype(np.float64))
+    ref = np.linalg.inv(sym)
+    assert st.item() == 0 and jit.item() == 0
+    np.testing.assert_allclose(_cpu(inv), ref, rtol=2e-4, atol=2e-4 * np.abs(ref).max())
+
+
+def test_spd_inverse_schur_jitter_and_failure(dev_ops):
+    p = 400
+    st, jit = dev_ops.zeros(1, dtype=torch.int32), dev_ops.zeros(1, dtype=torch.int32)
+    inv = dev_ops.zeros(p, p)
+    dev_ops.spd_inverse(dev_ops.zeros(p, p), 1.0, inv, st, jit)  # jitter 1e-30 path
+    assert st.item() == 0 and jit.item() == 1
+    np.testing.assert_allclose(_cpu(inv), 1e30 * np.eye(p), rtol=1e-5)
+    # rank-deficient PSD (N < p): the reference's jitter makes it SPD
+    a = np.random.default_rng(1).standard_normal((p, 50))
+    st.zero_()
+    jit.zero_()
+    dev_ops.spd_inverse(dev_ops.to_device(a @ a.T), 1.0, inv, st, jit)
+    assert jit.item() == 1
+    # indefinite even after jitter -> status
+    st.zero_()
+    bad = -np.eye(p)
+    dev_ops.spd_inverse(dev_ops.to_device(bad), 1.0, inv, st, jit)
+    assert st.item() == 1 and np.isnan(_cpu(inv)).all()
