@@ -232,6 +232,14 @@ int enks_spd_inverse(const float* S, int64_t lds, int p, float scale, float* inv
  * widths[n_layers] == 1; weights/biases concatenated per layer (device).
  */
 int enks_cnn_max_width(void);
+/* Deep surrogates (widths 2-32-...-32-1, fields a multiple of 128 pixels wide, e.g. BASELINE C4):
+ * one tcgen05 kernel per 32 -> 32 layer with fp16-pair activations through HBM (csrc/cnn_deep.cu);
+ * needs the workspace enks_cnn_ws_bytes reports (0 = none needed), processed in member chunks. */
+int64_t enks_cnn_ws_bytes(int n_layers, const int* widths, int rows, int cols, int64_t n_members);
+int enks_cnn_forward_ws(int n_layers, const int* widths, const float* weights,
+                        const float* biases, float alpha, const float* x, int64_t ldx,
+                        const float* u, int64_t ldu, float* out, int64_t ldo, int rows, int cols,
+                        int64_t n_members, void* ws, int64_t ws_bytes, void* stream);
 int enks_cnn_forward(int n_layers, const int* widths, const float* weights, const float* biases,
                      float alpha, const float* x, int64_t ldx, const float* u, int64_t ldu,
                      float* out, int64_t ldo, int rows, int cols, int64_t n_members,

@@ -25,6 +25,8 @@ CONFIGS = {
     "C1": (32, 100, 5, (2, 16, 16, 1)),
     "C2": (64, 512, 20, (2, 32, 32, 1)),
     "C3": (128, 1024, 50, (2, 32, 32, 1)),
+    # C4: 256 x 256 control field, deep CNN (SURVEY.md §8d proposal: 6 layers), N = 4096, H = 20
+    "C4": (256, 4096, 20, (2, 32, 32, 32, 32, 32, 1)),
     "C5": (128, 16384, 10, (2, 32, 32, 1)),
 }
 

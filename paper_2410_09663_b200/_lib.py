@@ -77,6 +77,9 @@ _SIGS = {
     "enks_cnn_max_width": (_c_int, []),
     "enks_cnn_forward": (_c_int, [_c_int, _ip, _vp, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _vp,
                                   _c_i64, _c_int, _c_int, _c_i64, _vp]),
+    "enks_cnn_ws_bytes": (_c_i64, [_c_int, _ip, _c_int, _c_int, _c_i64]),
+    "enks_cnn_forward_ws": (_c_int, [_c_int, _ip, _vp, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _vp,
+                                     _c_i64, _c_int, _c_int, _c_i64, _vp, _c_i64, _vp]),
     "enks_burgers_ws_bytes": (_c_i64, [_c_int, _c_int, _c_int]),
     "enks_burgers_forward": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int,
                                       _c_int, _c_int, _c_d, _c_d, _c_d, _vp, _vp, _vp, _vp]),

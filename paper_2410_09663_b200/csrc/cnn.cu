@@ -19,6 +19,12 @@
 namespace enks {
 
 bool cnn3_tc_applicable(int n_layers, const int* widths, int rows, int cols);
+bool cnn_deep_applicable(int n_layers, const int* widths, int rows, int cols);
+int64_t cnn_deep_member_bytes(int rows, int cols);
+int cnn_deep_forward(int n_layers, const float* weights, const float* biases, float alpha,
+                     const float* x, int64_t ldx, const float* u, int64_t ldu, float* out,
+                     int64_t ldo, int rows, int cols, int64_t n_members, void* ws, int64_t ws_bytes,
+                     cudaStream_t st);
 int cnn3_tc_forward(const float* weights, const float* biases, float alpha, const float* x,
                     int64_t ldx, const float* u, int64_t ldu, float* out, int64_t ldo, int rows,
                     int cols, int64_t n_members, cudaStream_t st);
@@ -50,6 +56,7 @@ struct CnnArgs {
     int in_floats;   // staged input halo (2 channels)
     int act_floats;  // per ping-pong activation buffer
     int w_floats;    // total weight floats (smem copy, layout [layer][ci][3][3][co])
+    int w_global;    // 1: weights too large for shared memory -> read (L1-cached) from global
 };
 
 __global__ void __launch_bounds__(kThreads) cnn_fused_kernel(const CnnArgs a) {
@@ -65,7 +72,7 @@ __global__ void __launch_bounds__(kThreads) cnn_fused_kernel(const CnnArgs a) {
     const int ty0 = (blockIdx.x / a.tiles_x) * kTile, tx0 = (blockIdx.x % a.tiles_x) * kTile;
 
     // stage weights: global [co][ci][ky][kx] -> smem [ci][ky][kx][co]
-    {
+    if (!a.w_global) {
         int off = 0;
         for (int l = 0; l < L; ++l) {
             const int ci_n = a.widths[l], co_n = a.widths[l + 1];
@@ -74,11 +81,12 @@ __global__ void __launch_bounds__(kThreads) cnn_fused_kernel(const CnnArgs a) {
                 const int co = e / (ci_n * 9), rem = e - co * ci_n * 9;
                 sw[off + rem * co_n + co] = a.weights[a.w_off[l] + e];
             }
-            for (int e = threadIdx.x; e < co_n; e += kThreads)
-                sb[l * kMaxWidth + e] = a.biases[a.b_off[l] + e];
             off += cnt;
         }
     }
+    for (int l = 0; l < L; ++l)
+        for (int e = threadIdx.x; e < a.widths[l + 1]; e += kThreads)
+            sb[l * kMaxWidth + e] = a.biases[a.b_off[l] + e];
     // stage the input halo: region (kTile + 2L)^2, channels [X, U], origin (ty0 - L, tx0 - L)
     const int R0 = kTile + 2 * L;
     {
@@ -118,6 +126,8 @@ __global__ void __launch_bounds__(kThreads) cnn_fused_kernel(const CnnArgs a) {
                 for (int ci = 0; ci < ci_n; ++ci) {
                     const float* ip = in + ci * Rin * Rin + oy * Rin + ox;
                     const float* wp = sw + w_base + ci * 9 * co_n + co0;
+                    // global layout [co][ci][ky][kx]: weight of (co0 + c, ci, k) at gw[c * 9 ci_n + k]
+                    const float* gw = a.weights + a.w_off[l] + (int64_t)co0 * ci_n * 9 + ci * 9;
 #pragma unroll
                     for (int ky = 0; ky < 3; ++ky)
 #pragma unroll
@@ -126,7 +136,11 @@ __global__ void __launch_bounds__(kThreads) cnn_fused_kernel(const CnnArgs a) {
                             const float* wk = wp + (ky * 3 + kx) * co_n;
 #pragma unroll
                             for (int c = 0; c < kCoGroup; ++c)
-                                if (co0 + c < co_n) acc[c] = fmaf(wk[c], v, acc[c]);
+                                if (co0 + c < co_n) {
+                                    const float w = a.w_global ? __ldg(gw + c * 9 * ci_n + ky * 3 + kx)
+                                                               : wk[c];
+                                    acc[c] = fmaf(w, v, acc[c]);
+                                }
                         }
                 }
             }
@@ -158,9 +172,26 @@ extern "C" {
 
 int enks_cnn_max_width(void) { return enks::kMaxWidth; }
 
+int64_t enks_cnn_ws_bytes(int n_layers, const int* widths, int rows, int cols, int64_t n_members) {
+    if (!widths || n_layers < 1 || n_members <= 0) return 0;
+    if (enks::cnn3_tc_applicable(n_layers, widths, rows, cols)) return 0;
+    if (!enks::cnn_deep_applicable(n_layers, widths, rows, cols)) return 0;
+    const int64_t per = enks::cnn_deep_member_bytes(rows, cols);
+    const int64_t cap = (4LL << 30) / per;  // member chunks of <= 4 GiB of activations
+    return per * (n_members < cap ? n_members : (cap > 0 ? cap : 1));
+}
+
 int enks_cnn_forward(int n_layers, const int* widths, const float* weights, const float* biases,
                      float alpha, const float* x, int64_t ldx, const float* u, int64_t ldu,
                      float* out, int64_t ldo, int rows, int cols, int64_t n_members, void* stream) {
+    return enks_cnn_forward_ws(n_layers, widths, weights, biases, alpha, x, ldx, u, ldu, out, ldo,
+                               rows, cols, n_members, nullptr, 0, stream);
+}
+
+int enks_cnn_forward_ws(int n_layers, const int* widths, const float* weights,
+                        const float* biases, float alpha, const float* x, int64_t ldx,
+                        const float* u, int64_t ldu, float* out, int64_t ldo, int rows, int cols,
+                        int64_t n_members, void* ws, int64_t ws_bytes, void* stream) {
     using namespace enks;
     ENKS_REQUIRE(n_layers >= 1 && n_layers <= kMaxLayers, "enks_cnn_forward: 1..%d layers",
                  kMaxLayers);
@@ -174,6 +205,9 @@ int enks_cnn_forward(int n_layers, const int* widths, const float* weights, cons
         if (allow && cnn3_tc_applicable(n_layers, widths, rows, cols))
             return cnn3_tc_forward(weights, biases, alpha, x, ldx, u, ldu, out, ldo, rows, cols, n_members,
                                    as_stream(stream));
+        if (allow && ws && cnn_deep_applicable(n_layers, widths, rows, cols))
+            return cnn_deep_forward(n_layers, weights, biases, alpha, x, ldx, u, ldu, out, ldo, rows,
+                                    cols, n_members, ws, ws_bytes, as_stream(stream));
     }
     CnnArgs a;
     a.n_layers = n_layers;
@@ -203,8 +237,14 @@ int enks_cnn_forward(int n_layers, const int* widths, const float* weights, cons
     a.in_floats = (2 * r0 * r0 + 3) & ~3;
     a.act_floats = (max_act + 3) & ~3;
     a.w_floats = (woff + 3) & ~3;
-    const size_t smem3 = sizeof(float) * ((size_t)a.w_floats + n_layers * kMaxWidth +
-                                          (size_t)a.in_floats + 2 * (size_t)a.act_floats);
+    size_t smem3 = sizeof(float) * ((size_t)a.w_floats + n_layers * kMaxWidth +
+                                    (size_t)a.in_floats + 2 * (size_t)a.act_floats);
+    a.w_global = 0;
+    if (smem3 > 227 * 1024) {  // deep nets: keep the weights in global memory (L1-cached)
+        a.w_global = 1;
+        smem3 -= sizeof(float) * (size_t)a.w_floats;
+        a.w_floats = 0;
+    }
     ENKS_REQUIRE(smem3 <= 227 * 1024, "enks_cnn_forward: shared memory %zu B exceeds 227 KB", smem3);
     static size_t configured = 0;
     if (smem3 > 48 * 1024 && smem3 > configured) {

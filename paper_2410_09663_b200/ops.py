@@ -382,10 +382,20 @@ class DeviceOps:
         self.launches += 1
         flops = n_members * x.shape[0] * cnn.cols * sum(
             18 * a * b for a, b in zip(cnn.widths[:-1], cnn.widths[1:]))
+        wsb = int(self.lib.enks_cnn_ws_bytes(cnn.n_layers, widths, int(x.shape[0]), int(cnn.cols),
+                                             int(n_members)))
+        ws = None
+        if wsb:
+            if getattr(self, "_cnn_ws", None) is None or self._cnn_ws.numel() < wsb:
+                self._retire(getattr(self, "_cnn_ws", None))
+                self._cnn_ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+            ws = self._cnn_ws
+            self.launches += 2 + cnn.n_layers
         with self._prof("forecast", flops):
-            _lib.call("enks_cnn_forward", cnn.n_layers, widths, _p(cnn.w_dev), _p(cnn.b_dev),
+            _lib.call("enks_cnn_forward_ws", cnn.n_layers, widths, _p(cnn.w_dev), _p(cnn.b_dev),
                       float(cnn.alpha), _p(x), _ld(x), _p(u), _ld(u), _p(out), _ld(out),
-                      int(x.shape[0]), int(cnn.cols), int(n_members), self._stream())
+                      int(x.shape[0]), int(cnn.cols), int(n_members), _p(ws), int(wsb),
+                      self._stream())
 
     def burgers_forward(self, bur, x, u, out, n_members):
         """bur: engine.Forecaster of kind 'burgers' (grid, solver constants, vmax/flags)."""

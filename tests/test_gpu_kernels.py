@@ -165,7 +165,12 @@ def test_spd_inverse_jitter_and_failure(dev_ops):
 
 # ---------------------------------------------------------------- CNN forecast (K3)
 @pytest.mark.parametrize("n,widths,N", [(16, (2, 8, 1), 3), (32, (2, 16, 16, 1), 5),
-                                        (40, (2, 32, 32, 1), 2), (128, (2, 32, 32, 1), 2)])
+                                        (40, (2, 32, 32, 1), 2), (128, (2, 32, 32, 1), 2),
+                                        (40, (2, 32, 32, 32, 32, 32, 1), 2),  # C4 depth, weights in L1
+                                        # deep tcgen05 path (cnn_deep.cu): 128 / 256-wide fields
+                                        (256, (2, 32, 32, 32, 32, 32, 1), 2),
+                                        (128, (2, 32, 32, 32, 1), 3),
+                                        (256, (2, 32, 32, 1), 2)])
 def test_cnn_forward(dev_ops, pm, n, widths, N):
     from oracle.models import cnn_step
     from paper_2410_09663_b200.engine import Forecaster
