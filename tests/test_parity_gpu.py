@@ -256,3 +256,21 @@ def test_rank_deficient_sigma_y_jitter(pm, n, l):
             return
     assert ens.jitter_events == oens.jitter_events == 3
     assert np.all(np.isfinite(ens.mean))
+
+
+def test_smooth_horizon_c4_shape_matches_oracle(pm):
+    """BASELINE C4 shapes (256 x 256 field, l = m = 256, 6-layer CNN 2-32-32-32-32-32-1) at a
+    small ensemble: deep tcgen05 CNN, p = 512 cross moments in 256-column tiles, Schur gain."""
+    from oracle import enks_oracle, problems
+    from oracle.models import OracleCNN
+
+    from paper_2410_09663_b200 import enks
+
+    pr = problems.make_cnn_problem(pm, "C4", n_members=8, horizon=2)
+    ovs = pm.virtualsys.build_virtual_system(OracleCNN(pr.model), pr.vs.weights)
+    ref, _, _ = enks_oracle.oracle_smooth(pr.x0, pr.y_ref, ovs, pr.H, pr.N, seed=1, backend="c")
+    got, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N,
+                                 pm.matvar.NoiseStreams(seed=1))
+    n, l = pr.n, pr.l
+    assert _rel(got, ref) < TOL
+    assert _rel(got[:, n:n + l], ref[:, n:n + l]) < TOL
