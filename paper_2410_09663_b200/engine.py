@@ -39,9 +39,9 @@ replicated.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
-
+import contextlib
 import os
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -436,6 +436,8 @@ class DeviceSmoother:
         # all channels diagonal: draw W, V_X, V_U of a step in one launch during predict
         self.fused_noise = (all(c.kind == "diag" for c in (self.noise_w, self.noise_vx, self.noise_vu))
                             and hasattr(ops, "noise_fill_multi"))
+        if self.fused_noise and getattr(self, "vx_raw", None) is None:
+            self.vx_raw = ops.empty(self.n, self.K)  # raw v_x of the newest step
         self._obs_t = -1
         self._obs_key = None
         self._bound = vs
@@ -446,6 +448,14 @@ class DeviceSmoother:
         if self.dev_head is not None:
             return self.dev_head
         return entropy_head(streams.seed, tuple(streams.prefix))
+
+    def _noise_stream(self):
+        """Stream for the noise draws that overlap the forecast (None off-GPU)."""
+        if getattr(self.ops, "device", None) is None or self.ops.device.type != "cuda":
+            return None
+        if getattr(self, "_nstream", None) is None:
+            self._nstream = torch.cuda.Stream(device=self.ops.device)
+        return self._nstream
 
     def _side_stream(self):
         """Second CUDA stream for the gain solve (None off-GPU)."""
@@ -542,23 +552,32 @@ class DeviceSmoother:
         ops, n, l, d = self.ops, self.n, self.l, self.d
         head = self._head(streams)
         sr, ob = self.slice_raw, self.obs_raw
-        self.forecast(ops, self.last, sr[:n], n, self.Nl)
         if self.fused_noise:
             # W (enks.py:165-168) and this step's observation noise V_X, V_U (enks.py:194-200,
-            # drawn at t = tau with the same substream ids update() would use) in one launch:
-            # dU = w, U = u + w, obs_x = x' + v_x, obs_u <- v_u (u + w added below)
-            ops.noise_fill_multi(head, self.member0, self.Nl, self.m, [
-                dict(t=tau, ch=CH_W, rows=l, diag=self.noise_w.diag, out=sr[n + l:],
-                     base=self.last[n:], out_plus=sr[n:n + l]),
-                dict(t=tau, ch=CH_VX, rows=n, diag=self.noise_vx.diag, base=sr[:n],
-                     out_plus=ob[:n]),
-                dict(t=tau, ch=CH_VU, rows=l, diag=self.noise_vu.diag, out=ob[n:n + l]),
-            ])
+            # drawn at t = tau with the same substream ids update() would use) in one launch on a
+            # second stream, concurrently with the forecast (both are SIMT-issue / latency bound
+            # and share SMs): dU = w, U = u + w, raw v_x, raw v_u; the two sums that need the
+            # forecast (x' + v_x, U + v_u) follow on the main stream.
+            ns = self._noise_stream()
+            if ns is not None:
+                ns.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(ns) if ns is not None else contextlib.nullcontext():
+                ops.noise_fill_multi(head, self.member0, self.Nl, self.m, [
+                    dict(t=tau, ch=CH_W, rows=l, diag=self.noise_w.diag, out=sr[n + l:],
+                         base=self.last[n:], out_plus=sr[n:n + l]),
+                    dict(t=tau, ch=CH_VX, rows=n, diag=self.noise_vx.diag, out=self.vx_raw),
+                    dict(t=tau, ch=CH_VU, rows=l, diag=self.noise_vu.diag, out=ob[n:n + l]),
+                ])
+            self.forecast(ops, self.last, sr[:n], n, self.Nl)
+            if ns is not None:
+                torch.cuda.current_stream().wait_stream(ns)
+            ops.add(sr[:n], self.vx_raw, ob[:n])
             ops.add(sr[n:n + l], ob[n:n + l], ob[n:n + l])
             self._barrier_row(head, tau)
             self._obs_t = tau
             self._obs_key = (streams.seed, tuple(streams.prefix))
         else:
+            self.forecast(ops, self.last, sr[:n], n, self.Nl)
             # ΔU slot = w, U slot = u + w  (one draw fills both, enks.py:168)
             self._noise(self.noise_w, head, tau, CH_W, l, out=sr[n + l:], base=self.last[n:],
                         out_plus=sr[n:n + l])
