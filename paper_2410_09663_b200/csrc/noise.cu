@@ -312,7 +312,19 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
                 const double fa = __longlong_as_double((long long)g_fi[id - 1]);
                 const double fb = __longlong_as_double((long long)g_fi[id]);
                 const double uu = u64_to_unit(word(w++));
-                if ((fa - fb) * uu + fb < exp(-0.5 * xs * xs)) {
+                // numpy: accept iff (fa - fb) uu + fb < exp(-x^2 / 2) in double.  Decide with a
+                // single-precision exp (ex2.approx, ~2^-22 relative) when the margin is wide,
+                // and fall back to the double exp only near the boundary: same decisions.
+                const double lhs = (fa - fb) * uu + fb;
+                const float ef = exp2f(-0.72134752044448170f * (float)(xs * xs));  // e^{-x^2/2}
+                bool acc;
+                if (lhs < (double)ef * (1.0 - 4e-6))
+                    acc = true;
+                else if (lhs > (double)ef * (1.0 + 4e-6))
+                    acc = false;
+                else
+                    acc = lhs < exp(-0.5 * xs * xs);
+                if (acc) {
                     val = xs;
                     have = true;
                 }

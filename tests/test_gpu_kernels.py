@@ -483,3 +483,17 @@ def test_spd_inverse_schur_jitter_and_failure(dev_ops):
     bad = -np.eye(p)
     dev_ops.spd_inverse(dev_ops.to_device(bad), 1.0, inv, st, jit)
     assert st.item() == 1 and np.isnan(_cpu(inv)).all()
+
+
+def test_noise_bit_exact_two_million(dev_ops):
+    """2M normals (~24k wedge tests, a few hundred tails): the single-precision screening of
+    the wedge test must reproduce numpy's double-precision decisions exactly."""
+    from oracle import noise as onoise
+    from paper_2410_09663_b200.matvar import entropy_head
+
+    N, rows, cols = 64, 64, 512
+    ref = onoise.member_normals(21, (3,), 2, 0, N, (rows, cols), backend="c")
+    out = dev_ops.zeros(rows, N * cols)
+    dev_ops.noise_fill(entropy_head(21, (3,)), 2, 0, 0, N, rows, cols, out=out)
+    got = out.cpu().numpy().reshape(rows, N, cols).transpose(1, 0, 2)
+    assert np.array_equal(got, ref.astype(np.float32))
