@@ -174,7 +174,8 @@ int enks_cnn_max_width(void) { return enks::kMaxWidth; }
 
 int64_t enks_cnn_ws_bytes(int n_layers, const int* widths, int rows, int cols, int64_t n_members) {
     if (!widths || n_layers < 1 || n_members <= 0) return 0;
-    if (enks::cnn3_tc_applicable(n_layers, widths, rows, cols)) return 0;
+    const char* fe = getenv("ENKS_CNN_FUSED");
+    if (!(fe && fe[0] == '0') && enks::cnn3_tc_applicable(n_layers, widths, rows, cols)) return 0;
     if (!enks::cnn_deep_applicable(n_layers, widths, rows, cols)) return 0;
     const int64_t per = enks::cnn_deep_member_bytes(rows, cols);
     const int64_t cap = (4LL << 30) / per;  // member chunks of <= 4 GiB of activations
@@ -202,7 +203,9 @@ int enks_cnn_forward_ws(int n_layers, const int* widths, const float* weights,
     {
         const char* e = getenv("ENKS_CNN_TC");
         const bool allow = !(e && e[0] == '0');
-        if (allow && cnn3_tc_applicable(n_layers, widths, rows, cols))
+        const char* fe = getenv("ENKS_CNN_FUSED");
+        const bool fused_ok = !(fe && fe[0] == '0');
+        if (allow && fused_ok && cnn3_tc_applicable(n_layers, widths, rows, cols))
             return cnn3_tc_forward(weights, biases, alpha, x, ldx, u, ldu, out, ldo, rows, cols, n_members,
                                    as_stream(stream));
         if (allow && ws && cnn_deep_applicable(n_layers, widths, rows, cols))

@@ -269,12 +269,16 @@ class DeviceSmoother:
     def _alloc_obs(self) -> None:
         """Buffers whose shape depends on the observation row count p."""
         ops, d, p, q, K, m = self.ops, self.d, self.p, self.q, self.K, self.m
+        # every rank must take the same code path (the collectives follow it): decide on the
+        # smallest local column count and on conditions every rank's K satisfies
+        k_min = (self.N // self.comm.size) * m
+        k_aligned = (m % 8 == 0) if self.comm.size > 1 else (K % 8 == 0)
         # tcgen05 cross moments (ENKS_TC=0 forces the SIMT engine for A/B checks)
         self.use_tc = (os.environ.get("ENKS_TC", "1") != "0" and hasattr(ops, "gemm_nt_tc")
-                       and p <= 512 and K >= 128)
+                       and p <= 512 and k_min >= 128)
         # basis storage: fp16 pairs (tcgen05 kind::f16 contraction, gemm_f16p.cu) or fp32
         basis = self._basis or os.environ.get("ENKS_BASIS", "f16pair" if self.use_tc else "fp32")
-        self.pair = basis == "f16pair" and K % 8 == 0 and hasattr(ops, "gemm_f16pair")
+        self.pair = basis == "f16pair" and k_aligned and hasattr(ops, "gemm_f16pair")
         if self.use_tc and not self.pair:
             self.yc_hi = ops.empty(p, K)
             self.yc_lo = ops.empty(p, K)

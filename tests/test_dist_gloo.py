@@ -29,7 +29,13 @@ def _problem(kind):
     if kind == "cnn":
         pr = problems.make_cnn_problem(pm, "C1", size=8, n_members=11, horizon=3)
         return pm, pr.vs, pr.x0, pr.N, pr.H
-    _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(2), n=5, l=3, m=4)
+    if kind == "burgers":
+        pr = problems.make_burgers_problem(pm, "boundary", grid_n=8, n_members=11, horizon=3)
+        return pm, pr.vs, pr.x0, pr.N, pr.H
+    model, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(2), n=5, l=3, m=4)
+    if kind == "constraint":
+        con = problems.make_constraint(pm, "box", x0.n, x0.l, x0.m)
+        vs = pm.virtualsys.build_virtual_system(model, vs.weights, constraint=con)
     return pm, vs, x0, 13, 4
 
 
@@ -68,13 +74,16 @@ def _worker(rank, world, port, kind, out, basis="fp32"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,basis", [("linear", "fp32"), ("cnn", "fp32"), ("cnn", "f16pair")])
+@pytest.mark.parametrize("kind,basis", [("linear", "fp32"), ("cnn", "fp32"), ("cnn", "f16pair"),
+                                        ("burgers", "f16pair"), ("constraint", "f16pair")])
 def test_two_rank_sharding_matches_single_rank(kind, basis, tmp_path):
     out = str(tmp_path / "r.npz")
     mp.spawn(_worker, args=(2, _free_port(), kind, out, basis), nprocs=2, join=True)
     got = np.load(out)
     ref = _run(kind, None, basis)
     assert [tuple(s) for s in got["spans"]] == [(0, 7), (7, 6)] if kind == "linear" else True
+    if kind == "burgers":
+        ref.check_status()  # batch-wide CFL / finiteness flags (max-reduced across ranks on B200)
     scale = np.abs(ref.mean_host()).max()
     assert np.abs(got["mean"] - ref.mean_host()).max() < 1e-10 * scale
     assert np.abs(got["members"] - ref.members_device().numpy()).max() < 1e-10 * scale
