@@ -323,7 +323,8 @@ def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
         raise ValueError(f"need {h} reference observations, got {y_refs.shape[0]}")
     if y_refs.shape[1:] != (vs.obs_rows, x0.m):
         raise ValueError(f"y_ref shape {y_refs.shape[1:]} != observation {(vs.obs_rows, x0.m)}")
-    if graph and not track_cov and n_members >= 2 and torch.cuda.is_available():
+    if graph and not track_cov and n_members >= 2 and torch.cuda.is_available() and \
+            _comm().size == 1:  # (collectives are not captured: multi-rank runs stay eager)
         g = _graph_for(x0, vs, h, n_members, streams)
         g.x0.copy_(torch.from_numpy(np.asarray(x0.packed, dtype=np.float32)), non_blocking=False)
         g.y_refs.copy_(torch.from_numpy(np.ascontiguousarray(y_refs, dtype=np.float32)))
