@@ -122,8 +122,10 @@ def _algorithmic(pr):
     n, l, m, N, H = pr.n, pr.l, pr.m, pr.N, pr.H
     d, p, K = n + 2 * l, n + l, N * m
     cnn_flops = N * H * pr.model.flops_per_member_step()
-    # P = [A_1..A_tau; Yc_1..Yc_tau] Yc_tau^T per step
-    cross = sum(2 * tau * (d + p) * p * K for tau in range(1, H + 1))
+    # P = [A_1..A_tau; Yc_1..Yc_tau] Yc_tau^T per step; A keeps the [X; dU] rows of each slice
+    # under the derived-U chain (engine.py, U = prefix sums of dU), else all d rows
+    ds = n + l if os.environ.get("ENKS_UCHAIN", "1") != "0" else d
+    cross = sum(2 * tau * (ds + p) * p * K for tau in range(1, H + 1))
     enks_ref = sum(2 * p * p * K + 4 * (t + 1) * d * p * K + p ** 3 / 3 + 2 * p * p * (t + 1) * d
                    for t in range(1, H + 1))
     return dict(cnn_tflop=cnn_flops / 1e12, cross_tflop=cross / 1e12, enks_ref_tflop=enks_ref / 1e12)

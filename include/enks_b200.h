@@ -108,12 +108,25 @@ int enks_member_center(const float* src, int64_t ld_src, int rows, int64_t n_mem
  * from the bound max|src - z0| + |mean shift| (amax from enks_member_sum), then
  * h/l planes (ld ldh) + inv_scale, the member mean, and optionally an fp32 copy of
  * the first rows_f32 rows (f32, ld_f32).  scale_ws: `rows` floats of scratch.
+ * Rows [skip0, skip1) are not stored in the basis (later rows move up); skip1 <= skip0: none.
  */
 int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64_t n_members,
                                int cols, const float* z0, const double* acc, const float* amax,
                                int64_t n_total, float* mean, void* h, void* l, int64_t ldh,
                                float* inv_scale, float* scale_ws, float* f32, int64_t ld_f32,
-                               int rows_f32, void* stream);
+                               int rows_f32, int skip0, int skip1, void* stream);
+
+/*
+ * Derived-U chain (replaces the U rows of enks.py:233-248 for slices 1..n_slices): the slice
+ * rows [X; U; dU] obey U_s = U_{s-1} + dU_s member-wise (enks.py:168), so the basis holds only
+ * [X; dU] (n + l rows per slice).  mean (full (n + 2l)-row slices from slice 1, ld_mean) +=
+ * delta (compact increments G (y_ref - y_bar), ld_delta) with U rows getting the prefix sum of
+ * the dU increments; gtt (n + l x p) = [X rows of the newest slice's compact gain;
+ * sum over slices of its dU rows].  Either pair of pointers may be NULL to skip that part.
+ */
+int enks_uchain_apply(const float* delta, int64_t ld_delta, float* mean, int64_t ld_mean,
+                      const float* gcol, int64_t ld_g, float* gtt, int64_t ld_gtt, int n_slices,
+                      int n, int l, int m, int p, void* stream);
 
 /*
  * Dense fp32 GEMM used by every contraction of the path (K2 dense colouring,

@@ -47,7 +47,9 @@ _SIGS = {
     "enks_member_sum": (_c_int, [_vp, _c_i64, _c_int, _c_i64, _c_int, _vp, _vp, _vp, _vp, _vp]),
     "enks_member_center_f16pair": (_c_int, [_vp, _c_i64, _c_int, _c_i64, _c_int, _vp, _vp, _vp,
                                             _c_i64, _vp, _vp, _vp, _c_i64, _vp, _vp, _vp, _c_i64,
-                                            _c_int, _vp]),
+                                            _c_int, _c_int, _c_int, _vp]),
+    "enks_uchain_apply": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _c_int,
+                                   _c_int, _c_int, _c_int, _c_int, _vp]),
     "enks_member_center": (_c_int, [_vp, _c_i64, _c_int, _c_i64, _c_int, _vp, _vp, _c_i64, _vp,
                                     _vp, _c_i64, _vp]),
     "enks_gemm_ws_bytes": (_c_i64, [_c_i64, _c_i64, _c_int]),

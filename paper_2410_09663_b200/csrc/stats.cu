@@ -65,11 +65,16 @@ __global__ void chunk_reduce_kernel(const double* __restrict__ part, const float
     if (amax) amax[e] = mx;
 }
 
+// basis row of source row r when rows [skip0, skip1) are not stored in the basis (-1: skipped)
+__device__ __forceinline__ int basis_row(int r, int skip0, int skip1) {
+    return r < skip0 ? r : (r >= skip1 ? r - (skip1 - skip0) : -1);
+}
+
 // per-row power-of-two scale for the fp16-pair basis from a guaranteed bound on the anomalies:
 // |anom| = |(src - z0) - mu| <= max|src - z0| + |mu|.  scale = 2^e with bound * scale in [2^13, 2^14)
 __global__ void row_scale_kernel(const double* __restrict__ acc, const float* __restrict__ amax,
                                  double inv_n, int cols, float* __restrict__ scale,
-                                 float* __restrict__ inv_scale) {
+                                 float* __restrict__ inv_scale, int skip0, int skip1) {
     const int r = blockIdx.x;
     float b = 0.f;
     for (int j = threadIdx.x; j < cols; j += blockDim.x) {
@@ -91,7 +96,8 @@ __global__ void row_scale_kernel(const double* __restrict__ acc, const float* __
             e = max(-120, min(120, 14 - ex));
         }
         scale[r] = ldexpf(1.f, e);
-        inv_scale[r] = ldexpf(1.f, -e);
+        const int hr = basis_row(r, skip0, skip1);
+        if (hr >= 0) inv_scale[hr] = ldexpf(1.f, -e);
     }
 }
 
@@ -102,7 +108,7 @@ __global__ void center_f16pair_kernel(const float* __restrict__ src, int64_t ld,
                                       float* __restrict__ mean, __half* __restrict__ h,
                                       __half* __restrict__ l, int64_t ldh,
                                       const float* __restrict__ scale, float* __restrict__ f32,
-                                      int64_t ldf, int rows_f32) {
+                                      int64_t ldf, int rows_f32, int skip0, int skip1) {
     const int64_t K = n * cols;
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t r = blockIdx.y;
@@ -113,10 +119,12 @@ __global__ void center_f16pair_kernel(const float* __restrict__ src, int64_t ld,
     if (mean && k < cols) mean[r * cols + j] = s + mu;
     const float a = (src[r * ld + k] - s) - mu;
     if (f32 && r < rows_f32) f32[r * ldf + k] = a;
+    const int64_t hr = basis_row((int)r, skip0, skip1);
+    if (hr < 0) return;
     const float v = a * scale[r];
     const __half hv = __float2half_rn(v);
-    h[r * ldh + k] = hv;
-    l[r * ldh + k] = __float2half_rn(v - __half2float(hv));
+    h[hr * ldh + k] = hv;
+    l[hr * ldh + k] = __float2half_rn(v - __half2float(hv));
 }
 
 // vectorised variant: 4 consecutive columns per thread (cols % 4 == 0, 16-B aligned rows)
@@ -126,7 +134,7 @@ __global__ void center_f16pair_v4_kernel(const float* __restrict__ src, int64_t 
                                          float* __restrict__ mean, __half* __restrict__ h,
                                          __half* __restrict__ l, int64_t ldh,
                                          const float* __restrict__ scale, float* __restrict__ f32,
-                                         int64_t ldf, int rows_f32) {
+                                         int64_t ldf, int rows_f32, int skip0, int skip1) {
     const int64_t K = n * cols;
     const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
     const int64_t r = blockIdx.y;
@@ -144,6 +152,8 @@ __global__ void center_f16pair_v4_kernel(const float* __restrict__ src, int64_t 
     const float4 an = make_float4((x.x - zz.x) - m0, (x.y - zz.y) - m1, (x.z - zz.z) - m2,
                                   (x.w - zz.w) - m3);
     if (f32 && r < rows_f32) *reinterpret_cast<float4*>(f32 + r * ldf + k) = an;
+    const int64_t hr = basis_row((int)r, skip0, skip1);
+    if (hr < 0) return;
     const float sc = scale[r];
     const float v[4] = {an.x * sc, an.y * sc, an.z * sc, an.w * sc};
     __half hv[4], lv[4];
@@ -152,10 +162,10 @@ __global__ void center_f16pair_v4_kernel(const float* __restrict__ src, int64_t 
         hv[q] = __float2half_rn(v[q]);
         lv[q] = __float2half_rn(v[q] - __half2float(hv[q]));
     }
-    *reinterpret_cast<uint2*>(h + r * ldh + k) =
+    *reinterpret_cast<uint2*>(h + hr * ldh + k) =
         make_uint2(__half_as_ushort(hv[0]) | ((uint32_t)__half_as_ushort(hv[1]) << 16),
                    __half_as_ushort(hv[2]) | ((uint32_t)__half_as_ushort(hv[3]) << 16));
-    *reinterpret_cast<uint2*>(l + r * ldh + k) =
+    *reinterpret_cast<uint2*>(l + hr * ldh + k) =
         make_uint2(__half_as_ushort(lv[0]) | ((uint32_t)__half_as_ushort(lv[1]) << 16),
                    __half_as_ushort(lv[2]) | ((uint32_t)__half_as_ushort(lv[3]) << 16));
 }
@@ -174,6 +184,51 @@ __global__ void center_kernel(const float* __restrict__ src, int64_t ld, int row
     const float mu = (float)(acc[r * cols + j] * inv_n);
     if (mean && k < cols) mean[r * cols + j] = s + mu;
     if (anom) anom[r * lda + k] = (src[r * ld + k] - s) - mu;
+}
+
+// Derived-U chain (engine.py, "u-chain"): the slice rows [X; U; dU] satisfy U_s = U_{s-1} + dU_s
+// member-wise (enks.py:168 appends u + w next to w, and every update is linear), so the basis keeps
+// only [X; dU] (ds = n + l rows per slice) and U follows by prefix sums over slices.
+// delta: compact mean increments G_{tau,.} (y_ref - y_bar), slices 1..ns (ds rows each, ld_delta);
+// mean: full layout from slice 1 (d = n + 2l rows each, ld_mean).  Thread per (compact row, col).
+__global__ void uchain_mean_kernel(const float* __restrict__ delta, int64_t ld_delta,
+                                   float* __restrict__ mean, int64_t ld_mean, int ns, int n, int l,
+                                   int m) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;  // 0 .. n + l - 1
+    if (j >= m) return;
+    const int ds = n + l, d = n + 2 * l;
+    if (r < n) {
+        for (int s = 0; s < ns; ++s) mean[(int64_t)(s * d + r) * ld_mean + j] +=
+            delta[(int64_t)(s * ds + r) * ld_delta + j];
+        return;
+    }
+    const int ru = r - n;
+    float run = 0.f;
+    for (int s = 0; s < ns; ++s) {
+        const float dv = delta[(int64_t)(s * ds + n + ru) * ld_delta + j];
+        run += dv;
+        mean[(int64_t)(s * d + n + l + ru) * ld_mean + j] += dv;   // dU_s
+        mean[(int64_t)(s * d + n + ru) * ld_mean + j] += run;      // U_s = sum_{s' <= s} dU_s'
+    }
+}
+
+// Gain rows of the newest slice [X; U] (q x p): X rows copied from the compact gain column,
+// U rows = sum over slices 1..ns of the dU rows (the gain of a prefix sum is the prefix sum of gains)
+__global__ void uchain_gain_kernel(const float* __restrict__ g, int64_t ld_g, float* __restrict__ gtt,
+                                   int64_t ld_gtt, int ns, int n, int l, int p) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;  // 0 .. n + l - 1
+    if (c >= p) return;
+    const int ds = n + l;
+    float v;
+    if (r < n) {
+        v = g[(int64_t)((ns - 1) * ds + r) * ld_g + c];
+    } else {
+        v = 0.f;
+        for (int s = 0; s < ns; ++s) v += g[(int64_t)(s * ds + r) * ld_g + c];
+    }
+    gtt[(int64_t)r * ld_gtt + c] = v;
 }
 
 int64_t member_chunks(int rows, int64_t n, int cols) {
@@ -242,14 +297,17 @@ int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64
                                int cols, const float* z0, const double* acc, const float* amax,
                                int64_t n_total, float* mean, void* h, void* l, int64_t ldh,
                                float* inv_scale, float* scale_ws, float* f32, int64_t ld_f32,
-                               int rows_f32, void* stream) {
+                               int rows_f32, int skip0, int skip1, void* stream) {
     ENKS_REQUIRE(src && acc && amax && h && l && inv_scale && scale_ws && n_total > 0,
                  "enks_member_center_f16pair: bad arguments");
     ENKS_REQUIRE(rows <= 65535, "enks_member_center_f16pair: rows > 65535");
+    if (skip1 <= skip0) skip0 = skip1 = rows;
+    ENKS_REQUIRE(skip0 >= 0 && skip1 <= rows, "enks_member_center_f16pair: bad skipped rows");
     if (rows <= 0 || cols <= 0 || n_members <= 0) return ENKS_OK;
     cudaStream_t st = enks::as_stream(stream);
     const double inv_n = 1.0 / (double)n_total;
-    enks::row_scale_kernel<<<rows, 128, 0, st>>>(acc, amax, inv_n, cols, scale_ws, inv_scale);
+    enks::row_scale_kernel<<<rows, 128, 0, st>>>(acc, amax, inv_n, cols, scale_ws, inv_scale,
+                                                   skip0, skip1);
     int rc = enks::check_launch("enks_member_center_f16pair(scale)");
     if (rc) return rc;
     const int64_t K = n_members * cols;
@@ -261,13 +319,36 @@ int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64
         enks::center_f16pair_v4_kernel<<<dim3((unsigned)((K / 4 + 255) / 256), (unsigned)rows), 256,
                                          0, st>>>(
             src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
-            static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32);
+            static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32, skip0, skip1);
     else
         enks::center_f16pair_kernel<<<dim3((unsigned)((K + 255) / 256), (unsigned)rows), 256, 0,
                                       st>>>(
             src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
-            static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32);
+            static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32, skip0, skip1);
     return enks::check_launch("enks_member_center_f16pair");
 }
 
+int enks_uchain_apply(const float* delta, int64_t ld_delta, float* mean, int64_t ld_mean,
+                      const float* gcol, int64_t ld_g, float* gtt, int64_t ld_gtt, int n_slices,
+                      int n, int l, int m, int p, void* stream) {
+    ENKS_REQUIRE(n >= 0 && l > 0 && m > 0 && p > 0 && n_slices >= 0,
+                 "enks_uchain_apply: bad sizes");
+    ENKS_REQUIRE(n + l <= 65535, "enks_uchain_apply: rows > 65535");
+    if (n_slices == 0) return ENKS_OK;
+    cudaStream_t st = enks::as_stream(stream);
+    if (delta && mean) {
+        enks::uchain_mean_kernel<<<dim3((unsigned)((m + 127) / 128), (unsigned)(n + l)), 128, 0,
+                                   st>>>(delta, ld_delta, mean, ld_mean, n_slices, n, l, m);
+        int rc = enks::check_launch("enks_uchain_apply(mean)");
+        if (rc) return rc;
+    }
+    if (gcol && gtt) {
+        enks::uchain_gain_kernel<<<dim3((unsigned)((p + 127) / 128), (unsigned)(n + l)), 128, 0,
+                                   st>>>(gcol, ld_g, gtt, ld_gtt, n_slices, n, l, p);
+        return enks::check_launch("enks_uchain_apply(gain)");
+    }
+    return ENKS_OK;
+}
+
 }  // extern "C"
+

@@ -254,6 +254,7 @@ class DeviceSmoother:
         self.barrier = None
         self.dev_head = None  # ops.DeviceHead: noise entropy words read from device memory
         self._basis = basis
+        self._explicit = False  # explicit members (replace_members): no derived-U chain
         d, q, K = self.d, self.q, self.K
         self.slice_raw = ops.empty(d, K)      # [X; U; W] of the newest predicted slice
         self.last = ops.empty(q, K)           # materialised [x; u] of the newest updated slice
@@ -264,7 +265,7 @@ class DeviceSmoother:
         x0 = ops.to_device(np.asarray(x0_packed, float))
         self.mean[:d] = x0
         self.last.copy_(x0[:q].repeat(1, self.Nl))
-        self._store_rows("A", 0, ops.zeros(d, K))
+        self._store_rows("A", 0, ops.zeros(self.ds, K))
 
     def _alloc_obs(self) -> None:
         """Buffers whose shape depends on the observation row count p."""
@@ -279,6 +280,14 @@ class DeviceSmoother:
         # basis storage: fp16 pairs (tcgen05 kind::f16 contraction, gemm_f16p.cu) or fp32
         basis = self._basis or os.environ.get("ENKS_BASIS", "f16pair" if self.use_tc else "fp32")
         self.pair = basis == "f16pair" and k_aligned and hasattr(ops, "gemm_f16pair")
+        # derived-U chain: slices are [X; U; dU] with U_s = U_{s-1} + dU_s member-wise
+        # (enks.py:168, preserved by every linear update), so the basis, the cross moments and the
+        # gains keep only the [X; dU] rows (ds = n + l per slice) and U follows by prefix sums
+        # (enks_uchain_apply) -- l fewer rows per slice in the dominant contraction
+        self.chain = (self.pair and self.l > 0 and not self._explicit and hasattr(ops, "uchain_apply")
+                      and os.environ.get("ENKS_UCHAIN", "1") != "0")
+        self.ds = self.n + self.l if self.chain else self.d
+        self.gtt = ops.empty(self.q, p) if self.chain else None
         if self.use_tc and not self.pair:
             self.yc_hi = ops.empty(p, K)
             self.yc_lo = ops.empty(p, K)
@@ -340,9 +349,9 @@ class DeviceSmoother:
         self.mean[:d].copy_(x0)
         self.last.copy_(x0[:q].repeat(1, self.Nl))
         if self.pair:
-            self.Ah[:d].zero_()
-            self.Al[:d].zero_()
-            self.a_inv[:d].fill_(1.0)
+            self.Ah[:self.ds].zero_()
+            self.Al[:self.ds].zero_()
+            self.a_inv[:self.ds].fill_(1.0)
         else:
             self.Abuf[:d].zero_()
 
@@ -351,8 +360,8 @@ class DeviceSmoother:
         """(Re)allocate the append-only basis for `cap` steps (slices 0..cap)."""
         if cap <= self.cap:
             return
-        ops, d, p, K, m = self.ops, self.d, self.p, self.K, self.m
-        ra, ry = (cap + 1) * d, cap * p
+        ops, d, ds, p, K, m = self.ops, self.d, self.ds, self.p, self.K, self.m
+        ra, ry = (cap + 1) * ds, cap * p
         if self.pair:
             f16 = torch.float16
             new = dict(Ah=ops.empty(ra, K, dtype=f16), Al=ops.empty(ra, K, dtype=f16),
@@ -363,20 +372,21 @@ class DeviceSmoother:
             new = dict(Abuf=ops.empty(ra, K), Ybuf=ops.empty(ry, K))
             a_keys, y_keys = ("Abuf",), ("Ybuf",)
         G = ops.zeros(ra, ry)
-        mean = ops.zeros(ra, m)
+        mean = ops.zeros((cap + 1) * d, m)   # full [X; U; dU] slices
         PA = ops.empty(ra, p)
         PY = ops.empty(ry, p)
         if self.cap:
-            rows_a, rows_y = (self.t + 1) * d, self.t * p
+            rows_a, rows_y = (self.t + 1) * ds, self.t * p
             for k in a_keys:
                 new[k][:rows_a] = getattr(self, k)[:rows_a]
             for k in y_keys:
                 new[k][:rows_y] = getattr(self, k)[:rows_y]
             G[:rows_a, :rows_y] = self.G[:rows_a, :rows_y]
-            mean[:rows_a] = self.mean[:rows_a]
+            mean[:(self.t + 1) * d] = self.mean[:(self.t + 1) * d]
         for k, v in new.items():
             setattr(self, k, v)
         self.G, self.mean, self.PA, self.PY = G, mean, PA, PY
+        self.delta = ops.empty(ra, m) if self.chain else None
         if getattr(self, "use_tc2", False):
             self.pyT_hi = ops.empty(p * cap * p)
             self.pyT_lo = ops.empty(p * cap * p)
@@ -414,7 +424,12 @@ class DeviceSmoother:
 
     def newest_anomalies(self):
         """fp32 anomalies of the newest predicted slice (d x K)."""
-        d, t = self.d, self.t
+        d, ds, t, q = self.d, self.ds, self.t, self.q
+        if self.chain:  # [X; U] from the fp32 copy, dU from the basis
+            out = self.ops.empty(d, self.K)
+            out[:q] = self.A_new[:q]
+            out[q:] = self._rows_fp32("A", t * ds + self.n, (t + 1) * ds)
+            return out
         return self._rows_fp32("A", t * d, (t + 1) * d) if self.pair else self.Abuf[t * d:(t + 1) * d]
 
     # ------------------------------------------------------------ binding
@@ -513,7 +528,7 @@ class DeviceSmoother:
         if out_plus is not None:
             ops.gemm(spec.dense, z, out_plus, beta=1.0, C0=base)
 
-    def _center(self, src, mean_out, anom_out, pair_rows=None, f32_rows=0):
+    def _center(self, src, mean_out, anom_out, pair_rows=None, f32_rows=0, skip=(0, 0)):
         """Member mean (rows x m) and anomalies of `src` (rows x K), shift = global member 0.
 
         pair_rows=(which, r0): write the anomalies straight into the fp16-pair basis at row r0
@@ -542,9 +557,10 @@ class DeviceSmoother:
         comm.allreduce_(acc)
         h, l, inv = (self.Ah, self.Al, self.a_inv) if which == "A" else (self.Yh, self.Yl,
                                                                         self.y_inv)
+        hr = rows - (skip[1] - skip[0])  # basis rows written
         ops.member_center_f16pair(src, self.Nl, self.m, z0, acc, amax, self.N, mean_out,
-                                  h[r0:r0 + rows], l[r0:r0 + rows], inv[r0:r0 + rows],
-                                  f32=anom_out, rows_f32=f32_rows)
+                                  h[r0:r0 + hr], l[r0:r0 + hr], inv[r0:r0 + hr],
+                                  f32=anom_out, rows_f32=f32_rows, skip=skip)
 
     # ------------------------------------------------------------ predict
     def predict(self, vs, streams) -> None:
@@ -587,8 +603,10 @@ class DeviceSmoother:
                         out_plus=sr[n:n + l])
         if self.pair:
             # fp32 copy of the [x; u] rows only (the newest-slice shift's C0)
-            self._center(sr, self.mean[tau * d:(tau + 1) * d], self.A_new, pair_rows=("A", tau * d),
-                         f32_rows=self.q)
+            # (derived-U chain: the U rows stay out of the basis; A_new keeps them in fp32)
+            self._center(sr, self.mean[tau * d:(tau + 1) * d], self.A_new,
+                         pair_rows=("A", tau * self.ds), f32_rows=self.q,
+                         skip=(n, n + l) if self.chain else (0, 0))
         else:
             self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d])
         self.t = tau
@@ -616,8 +634,9 @@ class DeviceSmoother:
             self._center(ob, self.ybar, yc)
 
         # P = [A_s0..A_tau ; Yc_1..Yc_tau] Yc_tau^T  (local K-partial, then allreduce)
-        a0 = d if self.slice0_zero else 0
-        rows_a = (tau + 1) * d
+        ds = self.ds  # basis rows per slice (n + l under the derived-U chain, else d)
+        a0 = ds if self.slice0_zero else 0
+        rows_a = (tau + 1) * ds
         PA, PY = self.PA[a0:rows_a], self.PY[:tau * p]
         scale = self.lam / self.N
         side = self._side_stream()
@@ -651,7 +670,7 @@ class DeviceSmoother:
             self._spd_async(None, PY[(tau - 1) * p:], scale)
 
         # S_s = P_{A_s} - sum_{tau' < tau} G_{tau',s} P_{Yc_tau'}  (block upper-triangular G)
-        tri = (d, p) if a0 == d else (0, 0)
+        tri = (ds, p) if a0 == ds else (0, 0)
         gcol = self.G[a0:rows_a, (tau - 1) * p:tau * p]
         r0 = tau * d
         if self.use_tc2:
@@ -675,12 +694,19 @@ class DeviceSmoother:
         # mean_s += G_{tau,s} (y_ref - y_bar)   (enks.py:247-248 on the mean)
         self.n_upd = tau
         ops.sub(y_ref_dev, self.ybar, self.innov)
-        mv = self.mean[a0:rows_a]
-        ops.gemm(gcol, self.innov, mv, beta=1.0, C0=mv)
-        # newest slice [x; u] for the next forecast: mean + A_tau - G_{tau,tau} Yc_tau
         q = self.q
-        g_tt = self.G[r0:r0 + q, (tau - 1) * p:tau * p]
-        a_new = self.A_new if self.pair else self.Abuf[r0:r0 + d]
+        if self.chain:
+            # compact increments, then U rows by prefix sums; newest-slice [X; U] gain rows
+            dl = self.delta[:rows_a - a0]
+            ops.gemm(gcol, self.innov, dl)
+            ops.uchain_apply(dl, self.mean[d:], gcol, self.gtt, tau, n, l, self.m, p)
+            g_tt = self.gtt
+        else:
+            mv = self.mean[a0 // ds * d:(tau + 1) * d]
+            ops.gemm(gcol, self.innov, mv, beta=1.0, C0=mv)
+            g_tt = self.G[tau * ds:tau * ds + q, (tau - 1) * p:tau * p]
+        # newest slice [x; u] for the next forecast: mean + A_tau - G_{tau,tau} Yc_tau
+        a_new = self.A_new if self.pair else self.Abuf[r0:r0 + d]  # (fp32 basis: ds == d)
         if self.shift_f16:
             yb = slice((tau - 1) * p, tau * p)
             ops.f16pair_split(g_tt, self.gtt_h, self.gtt_l, self.gtt_inv)
@@ -700,19 +726,28 @@ class DeviceSmoother:
     # ------------------------------------------------------------ readback
     def deviations(self, rows: int | None = None):
         """Member deviations M - mean for slices 0..t, (T d x K) on device."""
-        ops, d, p, t = self.ops, self.d, self.p, self.t
-        R = (t + 1) * d
-        out = ops.empty(R, self.K)
-        a0 = d if self.slice0_zero else 0
-        A = self._rows_fp32("A", 0, R)
+        ops, d, ds, p, t = self.ops, self.d, self.ds, self.p, self.t
+        R, Rc = (t + 1) * d, (t + 1) * ds
+        out = ops.empty(Rc, self.K)
+        a0 = ds if self.slice0_zero else 0
+        A = self._rows_fp32("A", 0, Rc)
         out[:a0] = A[:a0]
         ku = min(self.n_upd, t) * p  # only observation blocks that have been drawn
         if ku:
-            ops.gemm(self.G[a0:R, :ku], self._rows_fp32("Y", 0, ku), out[a0:], alpha=-1.0,
-                     beta=1.0, C0=A[a0:R], tri=(d, p) if a0 else (0, 0))
+            ops.gemm(self.G[a0:Rc, :ku], self._rows_fp32("Y", 0, ku), out[a0:], alpha=-1.0,
+                     beta=1.0, C0=A[a0:Rc], tri=(ds, p) if a0 else (0, 0))
         else:
-            out[a0:] = A[a0:R]
-        return out
+            out[a0:] = A[a0:Rc]
+        if not self.chain:
+            return out
+        # expand [X; dU] slices to [X; U; dU] with U_s = sum_{s' <= s} dU_s' (slice 0 is zero)
+        n, l, K = self.n, self.l, self.K
+        full = ops.zeros(R, K)
+        fv, cv = full.view(t + 1, d, K), out.view(t + 1, ds, K)
+        fv[:, :n] = cv[:, :n]
+        fv[:, n + l:] = cv[:, n:]
+        fv[:, n:n + l] = torch.cumsum(cv[:, n:], dim=0)
+        return full
 
     def members_device(self):
         dev = self.deviations()
@@ -740,6 +775,10 @@ class DeviceSmoother:
         ops, d = self.ops, self.d
         self._obs_t = -1
         self.t = 0
+        if self.chain:  # explicit members need not obey U_s = U_{s-1} + dU_s: full rows
+            self._explicit = True
+            self._alloc_obs()
+            self.cap = 0
         self._grow(max(t, 1))
         self.t = int(t)
         R = (self.t + 1) * d

@@ -184,7 +184,7 @@ class DeviceOps:
                       _p(z0), _p(acc), _p(amax), ws, self._stream())
 
     def member_center_f16pair(self, src, n_members, cols, z0, acc, amax, n_total, mean, h, l,
-                              inv_scale, f32=None, rows_f32=0):
+                              inv_scale, f32=None, rows_f32=0, skip=(0, 0)):
         rows = src.shape[0]
         if getattr(self, "_scale_ws", None) is None or self._scale_ws.numel() < rows:
             self._retire(getattr(self, "_scale_ws", None))
@@ -195,7 +195,16 @@ class DeviceOps:
             _lib.call("enks_member_center_f16pair", _p(src), _ld(src), rows, int(n_members),
                       int(cols), _p(z0), _p(acc), _p(amax), int(n_total), _p(mean), _p(h), _p(l),
                       _ld(h), _p(inv_scale), _p(self._scale_ws), _p(f32),
-                      _ld(f32) if f32 is not None else 0, int(rows_f32), self._stream())
+                      _ld(f32) if f32 is not None else 0, int(rows_f32), int(skip[0]),
+                      int(skip[1]), self._stream())
+
+    def uchain_apply(self, delta, mean, gcol, gtt, n_slices, n, l, m, p):
+        """Derived-U chain (stats.cu): mean += delta with prefix-summed U rows; gtt = newest
+        slice's [X; U] gain rows from the compact gain column."""
+        self.launches += 2
+        _lib.call("enks_uchain_apply", _p(delta), _ld(delta), _p(mean), _ld(mean), _p(gcol),
+                  _ld(gcol), _p(gtt), _ld(gtt), int(n_slices), int(n), int(l), int(m), int(p),
+                  self._stream())
 
     def member_center(self, src, n_members, cols, z0, acc, n_total, mean=None, anom=None):
         rows = src.shape[0]

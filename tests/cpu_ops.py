@@ -59,14 +59,27 @@ class CpuOps:
         C.copy_(out)
 
     def member_center_f16pair(self, src, n_members, cols, z0, acc, amax, n_total, mean, h, l,
-                              inv_scale, f32=None, rows_f32=0):
+                              inv_scale, f32=None, rows_f32=0, skip=(0, 0)):
         anom = torch.empty(src.shape, dtype=self.dtype)
         self.member_center(src, n_members, cols, z0, acc, n_total, mean=mean, anom=anom)
+        if f32 is not None and rows_f32:
+            f32[:rows_f32].copy_(anom[:rows_f32])
+        if skip[1] > skip[0]:
+            anom = torch.cat([anom[:skip[0]], anom[skip[1]:]])
         h.copy_(anom)
         l.zero_()
         inv_scale.fill_(1.0)
-        if f32 is not None and rows_f32:
-            f32[:rows_f32].copy_(anom[:rows_f32])
+
+    def uchain_apply(self, delta, mean, gcol, gtt, n_slices, n, l, m, p):
+        ds, d = n + l, n + 2 * l
+        dc = delta[:n_slices * ds].reshape(n_slices, ds, m)
+        mv = mean[:n_slices * d].view(n_slices, d, m)
+        mv[:, :n] += dc[:, :n]
+        mv[:, n + l:] += dc[:, n:]
+        mv[:, n:n + l] += torch.cumsum(dc[:, n:], dim=0)
+        gc = gcol[:n_slices * ds].reshape(n_slices, ds, p)
+        gtt[:n].copy_(gc[-1, :n])
+        gtt[n:n + l].copy_(gc[:, n:].sum(dim=0))
 
     def to_device(self, arr, dtype=None):
         arr = np.require(arr, requirements=["C", "W"])

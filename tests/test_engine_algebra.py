@@ -40,6 +40,7 @@ def test_engine_equals_oracle_fp64(pm, kw, N, h, seed, pair):
         pytest.skip("fp16-pair basis needs N*m % 8 == 0 (16-B aligned fp16 rows)")
     eng = _run(pm, x0, y, vs, h, N, seed + 7, pair=pair)
     assert eng.pair == pair
+    assert eng.chain == pair  # the fp16-pair basis keeps [X; dU] only (derived-U chain)
     d, m = x0.n + 2 * x0.l, x0.m
     mean = eng.mean_host().reshape(h + 1, d, m)
     members = eng.members_device().numpy().reshape((h + 1) * d, N, m).transpose(1, 0, 2)
@@ -47,6 +48,20 @@ def test_engine_equals_oracle_fp64(pm, kw, N, h, seed, pair):
     assert np.abs(mean - ref).max() < 1e-10 * scale
     assert np.abs(members - oens.members).max() < 1e-10 * np.abs(oens.members).max()
     assert eng.jitter.item() == oens.jitter_events
+
+
+def test_engine_pair_without_uchain(pm, monkeypatch):
+    """ENKS_UCHAIN=0: the fp16-pair basis with the full [X; U; dU] rows per slice."""
+    monkeypatch.setenv("ENKS_UCHAIN", "0")
+    _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(4), n=6, l=6, m=4)
+    y = vs.reference_observation()
+    ref, _, oens = enks_oracle.oracle_smooth(x0, y, vs, 5, 12, seed=3, backend="c")
+    eng = _run(pm, x0, y, vs, 5, 12, 3, pair=True)
+    assert eng.pair and not eng.chain and eng.ds == eng.d
+    mean = eng.mean_host().reshape(ref.shape)
+    assert np.abs(mean - ref).max() < 1e-10 * np.abs(ref).max()
+    members = eng.members_device().numpy().reshape(ref.shape[0] * ref.shape[1], 12, 4)
+    assert np.abs(members.transpose(1, 0, 2) - oens.members).max() < 1e-10 * np.abs(ref).max()
 
 
 def test_engine_cnn_equals_oracle_fp64(pm):
