@@ -365,6 +365,7 @@ def run_ours(args):
         f[2] += 1
     kinds = {"cross": ("tensor", "TFLOP/s"), "forecast": ("tensor", "TFLOP/s"),
              "correction": ("tensor", "TFLOP/s"), "gain": ("tensor", "TFLOP/s"),
+             "mean": ("tensor", "TFLOP/s"),
              "shift": ("tensor", "TFLOP/s"), "noise": ("hbm", "GB/s"), "stats": ("hbm", "GB/s"),
              "gain_solve": ("latency", "TFLOP/s")}
     kernels = {}

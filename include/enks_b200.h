@@ -97,8 +97,9 @@ int enks_noise_fill_multi_dev(const uint32_t* head_dev, int n_head, int64_t memb
  * `ws` for enks_member_sum: enks_member_sum_ws_bytes() bytes of device scratch.
  */
 int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols);
-int enks_member_sum(const float* src, int64_t ld_src, int rows, int64_t n_members, int cols,
-                    const float* z0, double* acc, float* amax, void* ws, void* stream);
+int enks_member_sum(const float* src, int64_t ld_src, const float* src2, int64_t ld_src2, int rows,
+                    int64_t n_members, int cols, const float* z0, double* acc, float* amax, void* ws,
+                    void* stream);
 int enks_member_center(const float* src, int64_t ld_src, int rows, int64_t n_members, int cols,
                        const float* z0, const double* acc, int64_t n_total, float* mean,
                        float* anom, int64_t ld_anom, void* stream);
@@ -124,6 +125,20 @@ int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64
  * the dU increments; gtt (n + l x p) = [X rows of the newest slice's compact gain;
  * sum over slices of its dU rows].  Either pair of pointers may be NULL to skip that part.
  */
+/*
+ * Observation centring (enks.py:194-200, 231-233) with the perturbed observation formed on the
+ * fly as src + src2 ([x; u] + [v_x; v_u]; enks_member_sum takes the same src2): writes the
+ * fp16-pair basis rows (h, l, inv_scale, as enks_member_center_f16pair), the member mean, and
+ * the transposed pair planes th / tl (K x rows, ld ldt) with one scale per K row (t_inv) --
+ * the K-major B operand of the newest-slice shift (enks.py:247).  rows <= 256.
+ */
+int enks_member_center_f16pair_t(const float* src, int64_t ld_src, const float* src2,
+                                 int64_t ld_src2, int rows, int64_t n_members, int cols,
+                                 const float* z0, const double* acc, const float* amax,
+                                 int64_t n_total, float* mean, void* h, void* l, int64_t ldh,
+                                 float* inv_scale, float* scale_ws, void* th, void* tl, int64_t ldt,
+                                 float* t_inv, void* stream);
+
 int enks_uchain_apply(const float* delta, int64_t ld_delta, float* mean, int64_t ld_mean,
                       const float* gcol, int64_t ld_g, float* gtt, int64_t ld_gtt, int n_slices,
                       int n, int l, int m, int p, void* stream);

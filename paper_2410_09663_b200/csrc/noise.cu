@@ -18,8 +18,8 @@ namespace enks {
 namespace {
 
 constexpr int kWarps = 4;          // warps (streams) per block
-constexpr int kBufWords = 128;     // 32 Philox blocks per refill
-constexpr int kMaxRowCols = 512;   // row-staged output path: cols % 4 == 0, 32 <= cols <= 512
+constexpr int kBufWords = 256;     // 64 Philox blocks per refill (two per lane: ILP)
+constexpr int kMaxRowCols = 256;   // row-staged output path: cols % 4 == 0, 32 <= cols <= 256
 
 __device__ const uint64_t g_ki[256] = NPY_ZIG_KI_DOUBLE_INIT;
 __device__ const uint64_t g_wi[256] = NPY_ZIG_WI_DOUBLE_INIT;
@@ -128,7 +128,7 @@ __device__ __forceinline__ double u64_to_unit(uint64_t r) {
 // scale prefetched a row ahead -- the sequential stream never waits on a global load.
 // Otherwise each batch of accepted normals is stored straight away (any cols / alignment).
 template <bool RB>
-__global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
+__global__ void __launch_bounds__(kWarps * 32, 6) noise_kernel(const Args args) {
     const Job a = args.job[blockIdx.y];  // by value: fields live in registers, not re-read
     __shared__ __align__(16) float s_row[RB ? kWarps : 1][RB ? 2 * kMaxRowCols : 1];
     __shared__ uint64_t s_ki[256];
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
     // 32-bit stream positions: a stream holds rows * cols < 2^31 normals (checked on the host)
     const int total = a.rows * cols;
     const int64_t col0 = local * cols;
-    int base_w = -(1 << 30);  // buffer holds words [base_w, base_w + 128)
+    int base_w = -(1 << 30);  // buffer holds words [base_w, base_w + kBufWords)
     int w = 0, q = 0;
 
     // (row, col) of normal q, tracked incrementally: (rb, jb) is the position of q (warp-uniform)
@@ -251,96 +251,117 @@ __global__ void __launch_bounds__(kWarps * 32) noise_kernel(const Args args) {
         return s == 0 ? b.v0 : (s == 1 ? b.v1 : (s == 2 ? b.v2 : b.v3));
     };
 
+    // Each iteration consumes a group of 32 consecutive words (w .. w+31) completely: every lane
+    // classifies its word as if it started a normal (ziggurat fast accept), and the sequential
+    // structure of numpy's parse is resolved on bitmasks.  A word that fails the fast test and
+    // really starts a normal (bit set in S) either takes the next word as its wedge uniform (wedge:
+    // that word is no start) or starts a tail loop that consumes 2k further words; `carry` counts
+    // consumed words that spill into the next group.  All wedge tests are evaluated speculatively
+    // in parallel (one lane per failing word); only tails (~1 in 10^4 words) run warp-uniformly.
+    const unsigned lt_mask = (1u << lane) - 1u;
+    int carry = 0;
     while (q < total) {
-        if (w + 32 > base_w + kBufWords) {
-            base_w = w & ~3LL;
-            Block4 b = philox(k0, k1, (uint64_t)(base_w >> 2) + 1 + lane);
+        if (w >= base_w + kBufWords) {  // w is a multiple of 32; windows of kBufWords words
+            base_w = w;
             __syncwarp();
-            buf[4 * lane + 0] = b.v0;
-            buf[4 * lane + 1] = b.v1;
-            buf[4 * lane + 2] = b.v2;
-            buf[4 * lane + 3] = b.v3;
+#pragma unroll
+            for (int bq = 0; bq < kBufWords / 128; ++bq) {
+                const Block4 b = philox(k0, k1, (uint64_t)((base_w >> 2) + bq * 32 + lane) + 1);
+                buf[bq * 128 + 4 * lane + 0] = b.v0;
+                buf[bq * 128 + 4 * lane + 1] = b.v1;
+                buf[bq * 128 + 4 * lane + 2] = b.v2;
+                buf[bq * 128 + 4 * lane + 3] = b.v3;
+            }
             __syncwarp();
         }
-        // fast path for 32 consecutive words
-        uint64_t r = buf[w - base_w + lane];
-        const int idx = (int)(r & 0xff);
-        r >>= 8;
+        const uint64_t raw = buf[w - base_w + lane];
+        const int idx = (int)(raw & 0xff);
+        const uint64_t r = raw >> 8;
         const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
         double x = (double)rabs * s_wi[idx];
         if (r & 1) x = -x;
         const bool ok = rabs < s_ki[idx];
         const unsigned bad = __ballot_sync(0xffffffffu, !ok);
-        const int n_ok = bad ? (__ffs(bad) - 1) : 32;
-        const int n_emit = min(n_ok, total - q);
-        if (RB) {
-            if (lane < n_emit) emit_rb(lane, x);
-        } else if (lane < n_emit) {
-            emit(lane, x);
-        }
-        q += n_emit;
-        w += n_emit;
-        if (RB)
-            advance_rb(n_emit);
-        else
-            advance(n_emit);
-        if (q >= total || n_ok == 32) continue;
-
-        // slow path for the rejected word at w (warp-uniform)
-        {
-            uint64_t rr = word(w++);
-            const int id = (int)(rr & 0xff);
-            rr >>= 8;
-            const int sign = (int)(rr & 1);
-            const uint64_t ra = (rr >> 1) & 0x000fffffffffffffULL;
-            double xs = (double)ra * __longlong_as_double((long long)g_wi[id]);
-            if (sign) xs = -xs;
-            bool have = false;
-            double val = 0.0;
-            if (id == 0) {
-                for (;;) {
-                    const double xx = -NPY_ZIG_NOR_INV_R * log1p(-u64_to_unit(word(w)));
-                    const double yy = -log1p(-u64_to_unit(word(w + 1)));
-                    w += 2;
-                    if (yy + yy > xx * xx) {
-                        val = ((ra >> 8) & 1) ? -(NPY_ZIG_NOR_R + xx) : NPY_ZIG_NOR_R + xx;
-                        have = true;
-                        break;
-                    }
-                }
-            } else {
-                const double fa = __longlong_as_double((long long)g_fi[id - 1]);
-                const double fb = __longlong_as_double((long long)g_fi[id]);
-                const double uu = u64_to_unit(word(w++));
+        unsigned S = carry >= 32 ? 0u : (0xffffffffu << carry);  // words that start a normal
+        int next_carry = carry >= 32 ? carry - 32 : 0;
+        unsigned O = S;  // words that emit a normal
+        if (bad & S) {
+            // speculative wedge test of every failing word with the following word as uniform
+            uint64_t nxt = __shfl_down_sync(0xffffffffu, raw, 1);
+            if (bad >> 31) {
+                const uint64_t n31 = word(w + 32);
+                if (lane == 31) nxt = n31;
+            }
+            bool acc = false;
+            if (!ok && idx != 0) {
+                const double fa = __longlong_as_double((long long)g_fi[idx - 1]);
+                const double fb = __longlong_as_double((long long)g_fi[idx]);
+                const double uu = u64_to_unit(nxt);
                 // numpy: accept iff (fa - fb) uu + fb < exp(-x^2 / 2) in double.  Decide with a
                 // single-precision exp (ex2.approx, ~2^-22 relative) when the margin is wide,
                 // and fall back to the double exp only near the boundary: same decisions.
                 const double lhs = (fa - fb) * uu + fb;
-                const float ef = exp2f(-0.72134752044448170f * (float)(xs * xs));  // e^{-x^2/2}
-                bool acc;
+                const float ef = exp2f(-0.72134752044448170f * (float)(x * x));  // e^{-x^2/2}
                 if (lhs < (double)ef * (1.0 - 4e-6))
                     acc = true;
                 else if (lhs > (double)ef * (1.0 + 4e-6))
                     acc = false;
                 else
-                    acc = lhs < exp(-0.5 * xs * xs);
-                if (acc) {
-                    val = xs;
-                    have = true;
-                }
+                    acc = lhs < exp(-0.5 * x * x);
             }
-            if (have) {
-                if (RB) {
-                    if (lane == 0) emit_rb(0, val);
-                    ++q;
-                    advance_rb(1);
-                } else {
-                    if (lane == 0) emit(0, val);
-                    ++q;
-                    advance(1);
+            unsigned accm = __ballot_sync(0xffffffffu, acc);
+            unsigned todo = bad & S;
+            while (todo) {  // warp-uniform walk over the failing starts, in word order
+                const int b = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int idb = __shfl_sync(0xffffffffu, idx, b);
+                int used;  // words consumed after word b
+                if (idb != 0) {
+                    used = 1;
+                } else {  // tail: pairs of uniforms until accepted (numpy's loop, uniform)
+                    const uint64_t rb_raw = __shfl_sync(0xffffffffu, raw, b);
+                    const uint64_t ra = ((rb_raw >> 8) >> 1) & 0x000fffffffffffffULL;
+                    int ww = w + b + 1;
+                    double val;
+                    for (;;) {
+                        const double xx = -NPY_ZIG_NOR_INV_R * log1p(-u64_to_unit(word(ww)));
+                        const double yy = -log1p(-u64_to_unit(word(ww + 1)));
+                        ww += 2;
+                        if (yy + yy > xx * xx) {
+                            val = ((ra >> 8) & 1) ? -(NPY_ZIG_NOR_R + xx) : NPY_ZIG_NOR_R + xx;
+                            break;
+                        }
+                    }
+                    used = ww - (w + b + 1);
+                    if (lane == b) x = val;
+                    accm |= 1u << b;
                 }
+                // the consumed words start no normal
+                const int e = b + 1 + used;  // first word after this normal (group-relative)
+                const unsigned span = (e >= 32 ? 0xffffffffu : ((1u << e) - 1u)) & ~((2u << b) - 1u);
+                S &= ~span;
+                todo &= ~span;
+                if (e > 32) next_carry = e - 32;
+            }
+            O = S & (~bad | accm);
+        }
+        carry = next_carry;
+        const int n_emit = min(__popc(O), total - q);
+        const int pos = __popc(O & lt_mask);
+        if ((O >> lane) & 1u) {
+            if (pos < n_emit) {
+                if (RB)
+                    emit_rb(pos, x);
+                else
+                    emit(pos, x);
             }
         }
+        q += n_emit;
+        w += 32;
+        if (RB)
+            advance_rb(n_emit);
+        else
+            advance(n_emit);
     }
 }
 

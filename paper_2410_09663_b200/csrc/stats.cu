@@ -19,7 +19,8 @@ namespace {
 constexpr int kSumThreads = 128;
 
 __global__ void __launch_bounds__(kSumThreads)
-    member_partial_kernel(const float* __restrict__ src, int64_t ld, int rows, int64_t n, int cols,
+    member_partial_kernel(const float* __restrict__ src, int64_t ld, const float* __restrict__ src2,
+                          int64_t ld2, int rows, int64_t n, int cols,
                           const float* __restrict__ z0, double* __restrict__ part,
                           float* __restrict__ partmax, int64_t chunk) {
     const int64_t rc = (int64_t)rows * cols;
@@ -27,14 +28,17 @@ __global__ void __launch_bounds__(kSumThreads)
     if (e >= rc) return;
     const int r = (int)(e / cols), j = (int)(e - (int64_t)r * cols);
     const float* p = src + r * ld + j;
-    const float s = z0 ? z0[e] : p[0];
+    const float* p2 = src2 ? src2 + r * ld2 + j : nullptr;
+    // element value: src (+ src2, the perturbed observation x + v formed on the fly)
+    auto val = [&](int64_t i) { return p2 ? p[i * cols] + p2[i * cols] : p[i * cols]; };
+    const float s = z0 ? z0[e] : val(0);
     const int64_t i0 = blockIdx.y * chunk, i1 = min(n, i0 + chunk);
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     float mx = 0.f;
     int64_t i = i0;
     for (; i + 4 <= i1; i += 4) {
-        float v0 = p[(i + 0) * cols] - s, v1 = p[(i + 1) * cols] - s;
-        float v2 = p[(i + 2) * cols] - s, v3 = p[(i + 3) * cols] - s;
+        float v0 = val(i + 0) - s, v1 = val(i + 1) - s;
+        float v2 = val(i + 2) - s, v3 = val(i + 3) - s;
         acc0 += (double)v0;
         acc1 += (double)v1;
         acc2 += (double)v2;
@@ -42,7 +46,7 @@ __global__ void __launch_bounds__(kSumThreads)
         mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v0), fabsf(v1)), fmaxf(fabsf(v2), fabsf(v3))));
     }
     for (; i < i1; ++i) {
-        const float v = p[i * cols] - s;
+        const float v = val(i) - s;
         acc0 += (double)v;
         mx = fmaxf(mx, fabsf(v));
     }
@@ -186,6 +190,80 @@ __global__ void center_kernel(const float* __restrict__ src, int64_t ld, int row
     if (anom) anom[r * lda + k] = (src[r * ld + k] - s) - mu;
 }
 
+// Observation centring with the sum x + v formed on the fly (src + src2) that also writes the
+// transposed fp16-pair planes of Yc_tau (K x rows, per-K-row scale) that the newest-slice shift
+// consumes as its K-major B operand -- no materialised observation, no separate transpose pass.
+// One CTA per 32 consecutive K columns: anomalies of all `rows` rows are kept in shared memory.
+constexpr int kTMaxRows = 256;
+__global__ void __launch_bounds__(256) center_f16pair_t_kernel(
+    const float* __restrict__ src, int64_t ld, const float* __restrict__ src2, int64_t ld2, int rows,
+    int64_t n, int cols, const float* __restrict__ z0, const double* __restrict__ acc, double inv_n,
+    float* __restrict__ mean, __half* __restrict__ h, __half* __restrict__ l, int64_t ldh,
+    const float* __restrict__ scale, __half* __restrict__ th, __half* __restrict__ tl, int64_t ldt,
+    float* __restrict__ t_inv) {
+    __shared__ float tile[kTMaxRows][33];
+    __shared__ float red[8][33];
+    __shared__ float sc[32];
+    const int64_t K = n * cols;
+    const int64_t c0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t c = c0 + tx;
+    const bool in = c < K;
+    const int j = in ? (int)((uint64_t)c % (uint64_t)cols) : 0;
+    float mx = 0.f;
+    for (int r = ty; r < rows; r += 8) {
+        float a = 0.f;
+        if (in) {
+            const float x = src[r * ld + c] + (src2 ? src2[r * ld2 + c] : 0.f);
+            const float s = z0 ? z0[(int64_t)r * cols + j]
+                               : src[r * ld + j] + (src2 ? src2[r * ld2 + j] : 0.f);
+            const float mu = (float)(acc[(int64_t)r * cols + j] * inv_n);
+            if (mean && c < cols) mean[(int64_t)r * cols + j] = s + mu;
+            a = (x - s) - mu;
+            const float v = a * scale[r];
+            const __half hv = __float2half_rn(v);
+            h[r * ldh + c] = hv;
+            l[r * ldh + c] = __float2half_rn(v - __half2float(hv));
+        }
+        tile[r][tx] = a;
+        mx = fmaxf(mx, fabsf(a));
+    }
+    red[ty][tx] = mx;
+    __syncthreads();
+    if (ty == 0) {
+        float m = red[0][tx];
+        for (int q = 1; q < 8; ++q) m = fmaxf(m, red[q][tx]);
+        int e = 0;
+        if (m > 0.f && isfinite(m)) {
+            int ex;
+            frexpf(m, &ex);
+            e = max(-120, min(120, 14 - ex));
+        }
+        sc[tx] = ldexpf(1.f, e);
+        if (in) t_inv[c] = ldexpf(1.f, -e);
+    }
+    __syncthreads();
+    for (int jj = ty; jj < 32; jj += 8) {  // transposed row c0 + jj, lanes over pairs of rows
+        const int64_t oc = c0 + jj;
+        if (oc >= K) break;
+        const float s = sc[jj];
+        for (int r = 2 * tx; r < rows; r += 64) {
+            const float v0 = tile[r][jj] * s;
+            const float v1 = r + 1 < rows ? tile[r + 1][jj] * s : 0.f;
+            const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+            const __half l0 = __float2half_rn(v0 - __half2float(h0));
+            const __half l1 = __float2half_rn(v1 - __half2float(h1));
+            if (r + 1 < rows) {
+                *reinterpret_cast<__half2*>(th + oc * ldt + r) = __halves2half2(h0, h1);
+                *reinterpret_cast<__half2*>(tl + oc * ldt + r) = __halves2half2(l0, l1);
+            } else {
+                th[oc * ldt + r] = h0;
+                tl[oc * ldt + r] = l0;
+            }
+        }
+    }
+}
+
 // Derived-U chain (engine.py, "u-chain"): the slice rows [X; U; dU] satisfy U_s = U_{s-1} + dU_s
 // member-wise (enks.py:168 appends u + w next to w, and every update is linear), so the basis keeps
 // only [X; dU] (ds = n + l rows per slice) and U follows by prefix sums over slices.
@@ -252,8 +330,9 @@ int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols) {
            (int64_t)(sizeof(double) + sizeof(float));
 }
 
-int enks_member_sum(const float* src, int64_t ld_src, int rows, int64_t n_members, int cols,
-                    const float* z0, double* acc, float* amax, void* ws, void* stream) {
+int enks_member_sum(const float* src, int64_t ld_src, const float* src2, int64_t ld_src2, int rows,
+                    int64_t n_members, int cols, const float* z0, double* acc, float* amax, void* ws,
+                    void* stream) {
     ENKS_REQUIRE(src && acc && ws, "enks_member_sum: null pointer");
     if (rows <= 0 || cols <= 0) return ENKS_OK;
     const int64_t rc = (int64_t)rows * cols;
@@ -269,8 +348,8 @@ int enks_member_sum(const float* src, int64_t ld_src, int rows, int64_t n_member
     dim3 grid((unsigned)((rc + enks::kSumThreads - 1) / enks::kSumThreads), (unsigned)nch_eff);
     double* part = static_cast<double*>(ws);
     float* pmax = reinterpret_cast<float*>(part + nch * rc);
-    enks::member_partial_kernel<<<grid, enks::kSumThreads, 0, st>>>(src, ld_src, rows, n_members,
-                                                                   cols, z0, part, pmax, chunk);
+    enks::member_partial_kernel<<<grid, enks::kSumThreads, 0, st>>>(
+        src, ld_src, src2, ld_src2, rows, n_members, cols, z0, part, pmax, chunk);
     int rc_ = enks::check_launch("enks_member_sum(partial)");
     if (rc_) return rc_;
     enks::chunk_reduce_kernel<<<(unsigned)((rc + 255) / 256), 256, 0, st>>>(part, pmax, (int)nch_eff,
@@ -326,6 +405,32 @@ int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64
             src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
             static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32, skip0, skip1);
     return enks::check_launch("enks_member_center_f16pair");
+}
+
+int enks_member_center_f16pair_t(const float* src, int64_t ld_src, const float* src2,
+                                 int64_t ld_src2, int rows, int64_t n_members, int cols,
+                                 const float* z0, const double* acc, const float* amax,
+                                 int64_t n_total, float* mean, void* h, void* l, int64_t ldh,
+                                 float* inv_scale, float* scale_ws, void* th, void* tl, int64_t ldt,
+                                 float* t_inv, void* stream) {
+    ENKS_REQUIRE(src && acc && amax && h && l && inv_scale && scale_ws && th && tl && t_inv &&
+                     n_total > 0,
+                 "enks_member_center_f16pair_t: bad arguments");
+    ENKS_REQUIRE(rows <= enks::kTMaxRows && ldt >= rows && ldt % 2 == 0,
+                 "enks_member_center_f16pair_t: rows > %d or bad ldt", enks::kTMaxRows);
+    if (rows <= 0 || cols <= 0 || n_members <= 0) return ENKS_OK;
+    cudaStream_t st = enks::as_stream(stream);
+    const double inv_n = 1.0 / (double)n_total;
+    enks::row_scale_kernel<<<rows, 128, 0, st>>>(acc, amax, inv_n, cols, scale_ws, inv_scale, rows,
+                                                 rows);
+    int rc = enks::check_launch("enks_member_center_f16pair_t(scale)");
+    if (rc) return rc;
+    const int64_t K = n_members * cols;
+    enks::center_f16pair_t_kernel<<<(unsigned)((K + 31) / 32), 256, 0, st>>>(
+        src, ld_src, src2, ld_src2, rows, n_members, cols, z0, acc, inv_n, mean,
+        static_cast<__half*>(h), static_cast<__half*>(l), ldh, scale_ws, static_cast<__half*>(th),
+        static_cast<__half*>(tl), ldt, t_inv);
+    return enks::check_launch("enks_member_center_f16pair_t");
 }
 
 int enks_uchain_apply(const float* delta, int64_t ld_delta, float* mean, int64_t ld_mean,

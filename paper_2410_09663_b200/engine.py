@@ -310,6 +310,7 @@ class DeviceSmoother:
             self.ycT_hi = ops.empty(K, p)
             self.ycT_lo = ops.empty(K, p)
         if self.use_tc2:
+            self.innT_hi, self.innT_lo = ops.empty(m, p), ops.empty(m, p)  # (y_ref - y_bar)^T
             self.sinvT_hi = ops.empty(p, p)
             self.sinvT_lo = ops.empty(p, p)
             self.pyT_hi = self.pyT_lo = None
@@ -455,8 +456,13 @@ class DeviceSmoother:
         # all channels diagonal: draw W, V_X, V_U of a step in one launch during predict
         self.fused_noise = (all(c.kind == "diag" for c in (self.noise_w, self.noise_vx, self.noise_vu))
                             and hasattr(ops, "noise_fill_multi"))
-        if self.fused_noise and getattr(self, "vx_raw", None) is None:
-            self.vx_raw = ops.empty(self.n, self.K)  # raw v_x of the newest step
+        if self.fused_noise and getattr(self, "v_raw", None) is None:
+            self.v_raw = ops.empty(self.q, self.K)  # raw [v_x; v_u] of the newest step
+        # observation never materialised: its centring forms [x; u] + [v_x; v_u] on the fly and
+        # also writes the transposed Yc_tau planes the newest-slice shift reads
+        self.obs_fused = (self.fused_noise and self.shift_f16 and self.barrier is None
+                          and self.p == self.q and hasattr(ops, "member_center_f16pair_t")
+                          and os.environ.get("ENKS_OBS_FUSED", "1") != "0")
         self._obs_t = -1
         self._obs_key = None
         self._bound = vs
@@ -562,6 +568,25 @@ class DeviceSmoother:
                                   h[r0:r0 + hr], l[r0:r0 + hr], inv[r0:r0 + hr],
                                   f32=anom_out, rows_f32=f32_rows, skip=skip)
 
+    def _center_obs_fused(self, tau) -> None:
+        """Centre y = [x; u] + [v_x; v_u] (never materialised) into the basis rows of Yc_tau and
+        the transposed planes of the newest-slice shift; y_bar = member mean (enks.py:231-232)."""
+        ops, comm, p, m = self.ops, self.comm, self.p, self.m
+        src, src2 = self.slice_raw[:p], self.v_raw
+        z0 = None
+        if comm.size > 1:
+            z0 = self.z0[:p]
+            if comm.rank == 0:
+                torch.add(src[:, :m], src2[:, :m], out=z0)
+            comm.broadcast_(z0, src=0)
+        acc, amax = self.acc[:p], self.amax[:p]
+        ops.member_sum(src, self.Nl, m, z0, acc, amax, src2=src2)
+        comm.allreduce_(acc)
+        r0 = (tau - 1) * p
+        ops.member_center_f16pair_t(src, src2, self.Nl, m, z0, acc, amax, self.N, self.ybar,
+                                    self.Yh[r0:r0 + p], self.Yl[r0:r0 + p], self.y_inv[r0:r0 + p],
+                                    self.ycT_h, self.ycT_l, self.ycT_inv)
+
     # ------------------------------------------------------------ predict
     def predict(self, vs, streams) -> None:
         """enks.py:156-171: W draw, new slice [f(x,u); u+w; w], append, mean."""
@@ -585,14 +610,15 @@ class DeviceSmoother:
                 ops.noise_fill_multi(head, self.member0, self.Nl, self.m, [
                     dict(t=tau, ch=CH_W, rows=l, diag=self.noise_w.diag, out=sr[n + l:],
                          base=self.last[n:], out_plus=sr[n:n + l]),
-                    dict(t=tau, ch=CH_VX, rows=n, diag=self.noise_vx.diag, out=self.vx_raw),
-                    dict(t=tau, ch=CH_VU, rows=l, diag=self.noise_vu.diag, out=ob[n:n + l]),
+                    dict(t=tau, ch=CH_VX, rows=n, diag=self.noise_vx.diag, out=self.v_raw[:n]),
+                    dict(t=tau, ch=CH_VU, rows=l, diag=self.noise_vu.diag,
+                         out=self.v_raw[n:n + l]),
                 ])
             self.forecast(ops, self.last, sr[:n], n, self.Nl)
             if ns is not None:
                 torch.cuda.current_stream().wait_stream(ns)
-            ops.add(sr[:n], self.vx_raw, ob[:n])
-            ops.add(sr[n:n + l], ob[n:n + l], ob[n:n + l])
+            if not self.obs_fused:
+                ops.add(sr[:n + l], self.v_raw, ob[:n + l])
             self._barrier_row(head, tau)
             self._obs_t = tau
             self._obs_key = (streams.seed, tuple(streams.prefix))
@@ -621,13 +647,17 @@ class DeviceSmoother:
         head = self._head(streams)
         sr, ob = self.slice_raw, self.obs_raw
         # perturbed observations [x + v_x; u + v_u]  (enks.py:194-200)
-        if self._obs_t != tau or self._obs_key != (streams.seed, tuple(streams.prefix)):
+        redraw = self._obs_t != tau or self._obs_key != (streams.seed, tuple(streams.prefix))
+        if redraw:
             self._noise(self.noise_vx, head, tau, CH_VX, n, base=sr[:n], out_plus=ob[:n])
             self._noise(self.noise_vu, head, tau, CH_VU, l, base=sr[n:n + l],
                         out_plus=ob[n:n + l])
             self._barrier_row(head, tau)
         yc = self.Yc_new if self.pair else self.Ybuf[(tau - 1) * p:tau * p]
-        if self.pair:
+        fused_obs = self.obs_fused and not redraw
+        if fused_obs:
+            self._center_obs_fused(tau)
+        elif self.pair:
             self._center(ob, self.ybar, yc, pair_rows=("Y", (tau - 1) * p),
                          f32_rows=0 if yc is None else p)
         else:
@@ -698,7 +728,11 @@ class DeviceSmoother:
         if self.chain:
             # compact increments, then U rows by prefix sums; newest-slice [X; U] gain rows
             dl = self.delta[:rows_a - a0]
-            ops.gemm(gcol, self.innov, dl)
+            if self.use_tc2 and ops.tc_applicable(gcol, self.innT_hi):
+                ops.tf32_split(self.innov, self.innT_hi, self.innT_lo, transpose=True)
+                ops.gemm_tc(gcol, self.innT_hi, self.innT_lo, dl, tag="mean")
+            else:
+                ops.gemm(gcol, self.innov, dl)
             ops.uchain_apply(dl, self.mean[d:], gcol, self.gtt, tau, n, l, self.m, p)
             g_tt = self.gtt
         else:
@@ -710,8 +744,9 @@ class DeviceSmoother:
         if self.shift_f16:
             yb = slice((tau - 1) * p, tau * p)
             ops.f16pair_split(g_tt, self.gtt_h, self.gtt_l, self.gtt_inv)
-            ops.f16pair_transpose(self.Yh[yb], self.Yl[yb], self.y_inv[yb], self.ycT_h,
-                                  self.ycT_l, self.ycT_inv)
+            if not fused_obs:  # (the fused centring wrote the transposed planes)
+                ops.f16pair_transpose(self.Yh[yb], self.Yl[yb], self.y_inv[yb], self.ycT_h,
+                                      self.ycT_l, self.ycT_inv)
             ops.gemm_f16pair_ex(self.gtt_h, self.gtt_l, self.gtt_inv, self.ycT_h, self.ycT_l,
                                 self.ycT_inv, self.last, alpha=-1.0, beta=1.0, C0=a_new[:q],
                                 bias=self.mean[r0:r0 + q], bias_cols=self.m, tag="shift")

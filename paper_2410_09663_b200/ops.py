@@ -174,14 +174,32 @@ class DeviceOps:
                   i64(*[_ld(v) if v is not None else 0 for v in get("out_plus")]),
                   self._stream())
 
-    def member_sum(self, src, n_members, cols, z0, acc, amax=None):
+    def member_sum(self, src, n_members, cols, z0, acc, amax=None, src2=None):
+        """Member sums of src (+ src2, formed on the fly) relative to z0 (or member 0)."""
         rows = src.shape[0]
         nbytes = self.lib.enks_member_sum_ws_bytes(rows, n_members, cols)
         ws = self._workspace_sum(nbytes)
         self.launches += 2
-        with self._prof("stats", 4 * rows * n_members * cols):
-            _lib.call("enks_member_sum", _p(src), _ld(src), rows, int(n_members), int(cols),
+        nsrc = 1 if src2 is None else 2
+        with self._prof("stats", 4 * nsrc * rows * n_members * cols):
+            _lib.call("enks_member_sum", _p(src), _ld(src), _p(src2),
+                      _ld(src2) if src2 is not None else 0, rows, int(n_members), int(cols),
                       _p(z0), _p(acc), _p(amax), ws, self._stream())
+
+    def member_center_f16pair_t(self, src, src2, n_members, cols, z0, acc, amax, n_total, mean, h,
+                                l, inv_scale, th, tl, t_inv):
+        """Centring of src + src2 into the pair basis rows and transposed pair planes."""
+        rows = src.shape[0]
+        if getattr(self, "_scale_ws", None) is None or self._scale_ws.numel() < rows:
+            self._retire(getattr(self, "_scale_ws", None))
+            self._scale_ws = torch.empty(max(rows, 4096), dtype=torch.float32, device=self.device)
+        self.launches += 2
+        K = n_members * cols
+        with self._prof("stats", 8 * rows * K + 8 * rows * K):
+            _lib.call("enks_member_center_f16pair_t", _p(src), _ld(src), _p(src2), _ld(src2), rows,
+                      int(n_members), int(cols), _p(z0), _p(acc), _p(amax), int(n_total), _p(mean),
+                      _p(h), _p(l), _ld(h), _p(inv_scale), _p(self._scale_ws), _p(th), _p(tl),
+                      _ld(th), _p(t_inv), self._stream())
 
     def member_center_f16pair(self, src, n_members, cols, z0, acc, amax, n_total, mean, h, l,
                               inv_scale, f32=None, rows_f32=0, skip=(0, 0)):

@@ -70,6 +70,17 @@ class CpuOps:
         l.zero_()
         inv_scale.fill_(1.0)
 
+    def member_center_f16pair_t(self, src, src2, n_members, cols, z0, acc, amax, n_total, mean, h,
+                                l, inv_scale, th, tl, t_inv):
+        anom = torch.empty(src.shape, dtype=self.dtype)
+        self.member_center(src + src2, n_members, cols, z0, acc, n_total, mean=mean, anom=anom)
+        h.copy_(anom)
+        l.zero_()
+        inv_scale.fill_(1.0)
+        th.copy_(anom.t())
+        tl.zero_()
+        t_inv.fill_(1.0)
+
     def uchain_apply(self, delta, mean, gcol, gtt, n_slices, n, l, m, p):
         ds, d = n + l, n + 2 * l
         dc = delta[:n_slices * ds].reshape(n_slices, ds, m)
@@ -118,7 +129,9 @@ class CpuOps:
     def add(self, a, b, out):
         out.copy_(a + b)
 
-    def member_sum(self, src, n_members, cols, z0, acc, amax=None):
+    def member_sum(self, src, n_members, cols, z0, acc, amax=None, src2=None):
+        if src2 is not None:
+            src = src + src2
         s = src.reshape(src.shape[0], n_members, cols)
         shift = s[:, 0, :] if z0 is None else z0
         acc.copy_((s - shift[:, None, :]).sum(dim=1))
