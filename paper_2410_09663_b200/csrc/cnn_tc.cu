@@ -25,9 +25,10 @@
 // addressing is unchanged; only the horizontal taps are cut at the image boundaries (which
 // fall on warp boundaries), as the zero 'same' padding requires.
 //
-// Warp roles (384 threads): warp 0 = MMA issuer, warp 2 = TMEM allocator,
-// warps 4-7 = layer-1 producer (thread = pixel), warps 8-11 = epilogue
-// (thread = pixel = TMEM lane).
+// Warp roles (512 threads): warp 0 = MMA issuer, warp 2 = TMEM allocator,
+// warps 4-7 / 8-11 = layer-1 producers of the even / odd image rows (thread = pixel; two
+// groups so that two rows of the latency-bound CUDA-core layer are in flight per SM),
+// warps 12-15 = epilogue (thread = pixel = TMEM lane).
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -41,8 +42,9 @@ constexpr int C1 = 32;     // layer-1 width
 constexpr int C2 = 32;     // layer-2 width
 constexpr int NB = 3 * C2; // MMA N: (dx, co)
 constexpr int NA = 3;      // layer-1 row slots
-constexpr int NACC = 4;    // TMEM output-row accumulators
-constexpr int kThreads = 384;
+constexpr int NACC = 5;    // TMEM accumulators (ring over rows; 5 x 96 <= 512 columns)
+constexpr int kThreads = 512;
+constexpr int kRing = 8;   // input-row ring slots per producer group
 
 constexpr int kInRow = W + 2;
 constexpr int kW1Stride = 20;                        // float2 per channel pair (18 used)
@@ -67,8 +69,8 @@ struct CL {
     static constexpr int kATile = kARows * 128;
     static constexpr int kOffB = 0;                        // [tap][hi/lo] B tiles
     static constexpr int kOffA = kOffB + kNBT * 2 * kBTile;  // [slot][hi/lo] A tiles
-    static constexpr int kOffIn = kOffA + NA * 2 * kATile;   // input ring [4][2][W + 2] floats
-    static constexpr int kOffW1 = kOffIn + 4 * 2 * kInRow * 4;
+    static constexpr int kOffIn = kOffA + NA * 2 * kATile;   // input rings [2][kRing][2][W + 2]
+    static constexpr int kOffW1 = kOffIn + 2 * kRing * 2 * kInRow * 4;
     static constexpr int kOffB1 = kOffW1 + (C1 / 2) * kW1Stride * 8;
     static constexpr int kOffB2 = kOffB1 + C1 * 4;
     static constexpr int kOffW3 = kOffB2 + C2 * 4;
@@ -102,7 +104,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 template <bool NEWTON>
 __device__ __forceinline__ float tanh_fast_t(float x) {
-    x = fminf(fmaxf(x, -15.f), 15.f);
+    // no clamp: e^{2x} -> +inf gives rcp 0 (tanh 1), -> 0 gives tanh -1
     const float t = exp2f_approx(x * 2.8853900817779268f);  // e^{2x}
     const float d = 1.f + t;
     float r;
@@ -227,7 +229,6 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-
     if (warp == 0) {
         // ================= MMA issuer =================
         if (lane == 0) {
@@ -295,23 +296,26 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 }
             }
         }
-    } else if (warp >= 4 && warp < 8) {
-        // ================= layer-1 producer: thread = pixel =================
-        const int x = threadIdx.x - 128;
+    } else if (warp >= 4 && warp < 12) {
+        // ================= layer-1 producers: thread = pixel, group g = row parity ============
+        const int g = (warp - 4) >> 2;
+        const int x = threadIdx.x - 128 - 128 * g;
         const int xs = x & (a.seg - 1);  // pixel within its image
+        float* ring = in_ring + g * kRing * 2 * kInRow;
         int it = 0;
         for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
             const float* xm = a.x + mem * W;
             const float* um = a.u + mem * W;
             const bool col_ok = mem * W + x < a.cols_total;
-            // input rows are prefetched into registers two rows ahead and written into the
-            // 4-slot ring one iteration later, so the global-load latency overlaps a row of work
+            // each group keeps its own ring of input rows; output row r (r = g, g + 2, ...)
+            // reads rows r - 1 .. r + 1 and brings in rows r, r + 1, which were prefetched into
+            // registers one iteration earlier (the global-load latency overlaps a row of work)
             auto fetch = [&](int j, float& vx, float& vu) {
                 vx = (j < n && col_ok) ? xm[(int64_t)j * a.ldx + x] : 0.f;
                 vu = (j < n && col_ok) ? um[(int64_t)j * a.ldu + x] : 0.f;
             };
-            auto put = [&](int j, float vx, float vu) {  // row j into ring slot j & 3
-                float* dst = in_ring + (j & 3) * 2 * kInRow;
+            auto put = [&](int j, float vx, float vu) {  // row j into ring slot j % kRing
+                float* dst = ring + (j & (kRing - 1)) * 2 * kInRow;
                 dst[x + 1] = vx;
                 dst[kInRow + x + 1] = vu;
                 if (x == 0) {
@@ -319,16 +323,19 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     dst[kInRow] = 0.f; dst[2 * kInRow - 1] = 0.f;
                 }
             };
-            float px, pu, qx, qu;
-            fetch(0, px, pu);
-            put(0, px, pu);
-            fetch(1, px, pu);  // row r+1 pending in (px, pu)
-            for (int r = 0; r < n; ++r) {
-                if (r + 1 < n) put(r + 1, px, pu);
-                fetch(r + 2, qx, qu);
-                px = qx;
-                pu = qu;
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+            float p0x, p0u, p1x, p1u;
+            if (g == 1) {  // row 0 (the first odd output row's upper neighbour)
+                fetch(0, p0x, p0u);
+                put(0, p0x, p0u);
+            }
+            fetch(g, p0x, p0u);
+            fetch(g + 1, p1x, p1u);
+            for (int r = g; r < n; r += 2) {
+                put(r, p0x, p0u);
+                if (r + 1 < n) put(r + 1, p1x, p1u);
+                fetch(r + 2, p0x, p0u);
+                fetch(r + 3, p1x, p1u);
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + 2 * g) : "memory");
                 float in[18];
 #pragma unroll
                 for (int ci = 0; ci < 2; ++ci)
@@ -336,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     for (int ky = 0; ky < 3; ++ky) {
                         const int j = r + ky - 1;
                         const bool ok = j >= 0 && j < n;
-                        const float* src = in_ring + (j & 3) * 2 * kInRow + ci * kInRow + x;
+                        const float* src = ring + (j & (kRing - 1)) * 2 * kInRow + ci * kInRow + x;
                         in[ci * 9 + ky * 3 + 0] = (ok && xs != 0) ? src[0] : 0.f;
                         in[ci * 9 + ky * 3 + 1] = ok ? src[1] : 0.f;
                         in[ci * 9 + ky * 3 + 2] = (ok && xs != a.seg - 1) ? src[2] : 0.f;
@@ -380,11 +387,11 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 ptx::fence_proxy_async_smem();
                 ptx::mbar_arrive(&a_full[slot]);
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // ring reuse across members
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + 2 * g) : "memory");  // ring reuse across members
         }
-    } else if (warp >= 8) {
+    } else if (warp >= 12) {
         // ================= epilogue: thread = pixel = TMEM lane =================
-        const int ew = warp - 8;  // == warp & 3 -> TMEM lane quarter
+        const int ew = warp - 12;  // == warp & 3 -> TMEM lane quarter
         const int x = ew * 32 + lane;
         const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
         const float b3 = b3s[0];
@@ -471,38 +478,47 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
             float* om = a.out + mem * W;
             const bool col_ok = mem * W + x < a.cols_total;
             if constexpr (SH) {
-                // pp = pre-activation of output row r - 1 (waits for D_r's dy = 2 block),
-                // pc = output row r (has D_{r-1}'s dy = 0 block); D_r's dy = 0 block starts r + 1
-                float pp[32], pc[32];
-#pragma unroll
-                for (int c = 0; c < 32; ++c) pp[c] = pc[c] = 0.f;
-                for (int r = 0; r < n; ++r) {
-                    const int Rg = it * n + r;
-                    const int q = Rg % NACC;
-                    ptx::mbar_wait(&acc_full[q], (uint32_t)((Rg / NACC) & 1));
+                // accumulator D_j (input row j) holds contributions to output rows j + 1 (dy = 0
+                // block), j (dy = 1) and j - 1 (dy = 2): output row y = D_{y-1}[0] + D_y[1] +
+                // D_{y+1}[2], read straight from TMEM (three live accumulators of the ring), so no
+                // running sums are carried in registers; D_{y-1} is released after row y
+                auto acc_base = [&](int j) {
+                    return tmem + lane_base + (uint32_t)(((it * n + j) % NACC) * L::kAccCols);
+                };
+                auto wait_acc = [&](int j) {
+                    const int Jg = it * n + j;
+                    ptx::mbar_wait(&acc_full[Jg % NACC], (uint32_t)((Jg / NACC) & 1));
                     ptx::tc_fence_after();
-                    const uint32_t base = tmem + lane_base + (uint32_t)(q * L::kAccCols);
-                    uint32_t v[32];
-                    ptx::tmem_ld_32x32b_x32(base + 2 * C2, v);  // dy = 2 -> output row r - 1
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int c = 0; c < 32; ++c) pp[c] += __uint_as_float(v[c]);
-                    ptx::tmem_ld_32x32b_x32(base + C2, v);      // dy = 1 -> output row r
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int c = 0; c < 32; ++c) pc[c] += __uint_as_float(v[c]);
-                    ptx::tmem_ld_32x32b_x32(base, v);           // dy = 0 -> output row r + 1
-                    ptx::tmem_ld_wait();
+                };
+                auto release = [&](int j) {
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&acc_empty[q]);
-                    if (r >= 1) layer3(r - 1, pp, (nproc++) & 1, acc3, xm, om, col_ok);
-                    if (r == n - 1) layer3(r, pc, (nproc++) & 1, acc3, xm, om, col_ok);
+                    if (lane == 0) ptx::mbar_arrive(&acc_empty[(it * n + j) % NACC]);
+                };
+                wait_acc(0);
+                for (int y = 0; y < n; ++y) {
+                    if (y + 1 < n) wait_acc(y + 1);
+                    float s[32];
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(acc_base(y) + C2, v);  // D_y[dy = 1]
+                    ptx::tmem_ld_wait();
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        pp[c] = pc[c];
-                        pc[c] = __uint_as_float(v[c]);
+                    for (int c = 0; c < 32; ++c) s[c] = __uint_as_float(v[c]);
+                    if (y >= 1) {
+                        ptx::tmem_ld_32x32b_x32(acc_base(y - 1), v);  // D_{y-1}[dy = 0]
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) s[c] += __uint_as_float(v[c]);
                     }
+                    if (y + 1 < n) {
+                        ptx::tmem_ld_32x32b_x32(acc_base(y + 1) + 2 * C2, v);  // D_{y+1}[dy = 2]
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) s[c] += __uint_as_float(v[c]);
+                    }
+                    if (y >= 1) release(y - 1);
+                    if (y == n - 1) release(y);
+                    layer3(y, s, (nproc++) & 1, acc3, xm, om, col_ok);
                 }
             } else {
                 for (int y = 0; y < n; ++y) {
