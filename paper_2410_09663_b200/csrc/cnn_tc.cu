@@ -400,10 +400,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         const bool xr = ew < 3 && (((ew + 1) * 32) & (a.seg - 1)) != 0;
         // bias + tanh, layer 3 (32 -> 1, taps folded by shuffles), residual, for the finished
         // layer-2 pre-activation row y (s = 32 channels of this pixel)
-        auto layer3 = [&](int y, const float (&s)[32], int par, float (&acc3)[3], const float* xm,
-                          float* om, bool col_ok) {
-            const float xres_m = (y >= 1 && col_ok) ? xm[(int64_t)(y - 1) * a.ldx + x] : 0.f;
-            const float xres_0 = (y == n - 1 && col_ok) ? xm[(int64_t)y * a.ldx + x] : 0.f;
+        // xres_m = X[y - 1] (prefetched a row ahead by the caller), xres_0 = X[y] (last row only)
+        auto layer3 = [&](int y, const float (&s)[32], int par, float (&acc3)[3], float xres_m,
+                          float xres_0, float* om, bool col_ok) {
             // layer-2 activation and the layer-3 taps v[ky][kx] = sum_c w3 h
             // four independent partial sums (8 channels each) for ILP
             float2 v01[4], v23[4], v45[4], v67[4];
@@ -495,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&acc_empty[(it * n + j) % NACC]);
                 };
+                float xpre = 0.f;
                 wait_acc(0);
                 for (int y = 0; y < n; ++y) {
                     if (y + 1 < n) wait_acc(y + 1);
@@ -518,9 +518,12 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     }
                     if (y >= 1) release(y - 1);
                     if (y == n - 1) release(y);
-                    layer3(y, s, (nproc++) & 1, acc3, xm, om, col_ok);
+                    const float xr_m = xpre;  // X[y - 1]
+                    xpre = col_ok ? xm[(int64_t)y * a.ldx + x] : 0.f;  // X[y]: next row's X[y' - 1]
+                    layer3(y, s, (nproc++) & 1, acc3, xr_m, y == n - 1 ? xpre : 0.f, om, col_ok);
                 }
             } else {
+                float xpre = 0.f;
                 for (int y = 0; y < n; ++y) {
                     const int Yg = it * n + y;
                     const int q = Yg % NACC;
@@ -580,7 +583,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                             s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
                         }
                     }
-                    layer3(y, s, par, acc3, xm, om, col_ok);
+                    const float xr_m = xpre;
+                    xpre = col_ok ? xm[(int64_t)y * a.ldx + x] : 0.f;
+                    layer3(y, s, par, acc3, xr_m, y == n - 1 ? xpre : 0.f, om, col_ok);
                 }
             }
         }
