@@ -139,6 +139,7 @@ struct Cnn3Args {
     int64_t cols_total; // n_members_real * seg: columns beyond it are padding
     int seg;            // image width: 32, 64 or 128
     int debug;  // ENKS_CNN_DEBUG: 1 = no MMAs, 2 = no layer-1 math, 4 = no epilogue math
+    int products;  // 3 (default): lo*hi + hi*lo + hi*hi; 2 (ENKS_CNN_PRODUCTS=2): hi*lo + hi*hi
 };
 
 template <bool SH>
@@ -258,8 +259,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                                 const uint64_t adl = ptx::desc_kmajor_sw128(al_t + dx * 128 + 32 * k);
                                 const uint64_t bdh = ptx::desc_kmajor_sw128(bh_t + 32 * k);
                                 const uint64_t bdl = ptx::desc_kmajor_sw128(bl_t + 32 * k);
-                                ptx::mma_tf32_ss(d, adl, bdh, idesc, (dx == 0 && k == 0) ? 0u : 1u);
-                                ptx::mma_tf32_ss(d, adh, bdl, idesc, 1u);
+                                const uint32_t acc0 = (dx == 0 && k == 0) ? 0u : 1u;
+                                if (a.products == 3) ptx::mma_tf32_ss(d, adl, bdh, idesc, acc0);
+                                ptx::mma_tf32_ss(d, adh, bdl, idesc, a.products == 3 ? 1u : acc0);
                                 ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
                             }
                         }
@@ -284,8 +286,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                                 const uint64_t adl = ptx::desc_kmajor_sw128(al_t + 32 * k);
                                 const uint64_t bdh = ptx::desc_kmajor_sw128(bh_t + 32 * k);
                                 const uint64_t bdl = ptx::desc_kmajor_sw128(bl_t + 32 * k);
-                                ptx::mma_tf32_ss(d, adl, bdh, idesc, (first && k == 0) ? 0u : 1u);
-                                ptx::mma_tf32_ss(d, adh, bdl, idesc, 1u);
+                                const uint32_t acc0 = (first && k == 0) ? 0u : 1u;
+                                if (a.products == 3) ptx::mma_tf32_ss(d, adl, bdh, idesc, acc0);
+                                ptx::mma_tf32_ss(d, adh, bdl, idesc, a.products == 3 ? 1u : acc0);
                                 ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
                             }
                             // row y complete: after its dy=2 contribution, or the last row's dy=1
@@ -625,6 +628,8 @@ int cnn3_tc_forward(const float* weights, const float* biases, float alpha, cons
     {
         const char* e = getenv("ENKS_CNN_DEBUG");
         a.debug = e ? atoi(e) : 0;
+        const char* pe = getenv("ENKS_CNN_PRODUCTS");
+        a.products = (pe && atoi(pe) == 2) ? 2 : 3;
     }
     const int grid = (int)(n_members < kNumSMs ? n_members : kNumSMs);
     if (cols == W) return launch_cnn3<true>(a, grid, st);
