@@ -59,6 +59,9 @@ struct CnnArgs {
     int w_global;    // 1: weights too large for shared memory -> read (L1-cached) from global
 };
 
+// WG: weights read from global memory (deep nets whose weights exceed shared memory); a template
+// parameter, not a runtime flag, so the common shared-memory path keeps a branch-free FMA loop
+template <bool WG>
 __global__ void __launch_bounds__(kThreads) cnn_fused_kernel(const CnnArgs a) {
     extern __shared__ __align__(16) float sm[];
     float* sw = sm;                        // weights, transposed to [ci][ky][kx][co]
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) cnn_fused_kernel(const CnnArgs a) {
     const int ty0 = (blockIdx.x / a.tiles_x) * kTile, tx0 = (blockIdx.x % a.tiles_x) * kTile;
 
     // stage weights: global [co][ci][ky][kx] -> smem [ci][ky][kx][co]
-    if (!a.w_global) {
+    if (!WG) {
         int off = 0;
         for (int l = 0; l < L; ++l) {
             const int ci_n = a.widths[l], co_n = a.widths[l + 1];
@@ -137,8 +140,8 @@ __global__ void __launch_bounds__(kThreads) cnn_fused_kernel(const CnnArgs a) {
 #pragma unroll
                             for (int c = 0; c < kCoGroup; ++c)
                                 if (co0 + c < co_n) {
-                                    const float w = a.w_global ? __ldg(gw + c * 9 * ci_n + ky * 3 + kx)
-                                                               : wk[c];
+                                    const float w = WG ? __ldg(gw + c * 9 * ci_n + ky * 3 + kx)
+                                                       : wk[c];
                                     acc[c] = fmaf(w, v, acc[c]);
                                 }
                         }
@@ -249,19 +252,23 @@ int enks_cnn_forward_ws(int n_layers, const int* widths, const float* weights,
         a.w_floats = 0;
     }
     ENKS_REQUIRE(smem3 <= 227 * 1024, "enks_cnn_forward: shared memory %zu B exceeds 227 KB", smem3);
-    static size_t configured = 0;
-    if (smem3 > 48 * 1024 && smem3 > configured) {
-        cudaError_t e = cudaFuncSetAttribute(cnn_fused_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
+    static size_t configured[2] = {0, 0};
+    if (smem3 > 48 * 1024 && smem3 > configured[a.w_global]) {
+        cudaError_t e = cudaFuncSetAttribute(
+            a.w_global ? cnn_fused_kernel<true> : cnn_fused_kernel<false>,
+            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
         if (e != cudaSuccess) {
             set_error("enks_cnn_forward: smem attribute: %s", cudaGetErrorString(e));
             return ENKS_E_CUDA;
         }
-        configured = smem3;
+        configured[a.w_global] = smem3;
     }
     dim3 grid((unsigned)(a.tiles_x * tiles_y), (unsigned)n_members);
     ENKS_REQUIRE(n_members < 65536, "enks_cnn_forward: n_members must be < 65536 per launch");
-    cnn_fused_kernel<<<grid, kThreads, smem3, as_stream(stream)>>>(a);
+    if (a.w_global)
+        cnn_fused_kernel<true><<<grid, kThreads, smem3, as_stream(stream)>>>(a);
+    else
+        cnn_fused_kernel<false><<<grid, kThreads, smem3, as_stream(stream)>>>(a);
     return check_launch("enks_cnn_forward");
 }
 

@@ -475,8 +475,11 @@ class DeviceSmoother:
         return entropy_head(streams.seed, tuple(streams.prefix))
 
     def _noise_stream(self):
-        """Stream for the noise draws that overlap the forecast (None off-GPU)."""
+        """Stream for the noise draws that overlap the forecast (None off-GPU, or when
+        ENKS_NOISE_CONCURRENT=0: drawn on the main stream before the forecast)."""
         if getattr(self.ops, "device", None) is None or self.ops.device.type != "cuda":
+            return None
+        if os.environ.get("ENKS_NOISE_CONCURRENT", "1") == "0":
             return None
         if getattr(self, "_nstream", None) is None:
             self._nstream = torch.cuda.Stream(device=self.ops.device)
