@@ -497,3 +497,87 @@ def test_noise_bit_exact_two_million(dev_ops):
     dev_ops.noise_fill(entropy_head(21, (3,)), 2, 0, 0, N, rows, cols, out=out)
     got = out.cpu().numpy().reshape(rows, N, cols).transpose(1, 0, 2)
     assert np.array_equal(got, ref.astype(np.float32))
+
+
+# ------------------------------------------------ derived-U chain and fused observation centring
+@pytest.mark.parametrize("ns,n,l,m,p", [(1, 4, 3, 5, 6), (7, 16, 8, 32, 24), (50, 128, 128, 128, 256)])
+def test_uchain_apply(dev_ops, ns, n, l, m, p):
+    """enks_uchain_apply: X / dU mean increments, U rows by prefix sums over slices; newest-slice
+    gain rows [X of the last slice; sum of the dU rows] (fp32, tolerance 1e-5 relative)."""
+    g = torch.Generator(device="cuda").manual_seed(ns)
+    ds, d = n + l, n + 2 * l
+    delta = torch.randn(ns * ds, m, device="cuda", generator=g)
+    mean = torch.randn(ns * d, m, device="cuda", generator=g)
+    gcol = torch.randn(ns * ds, p, device="cuda", generator=g)
+    gtt = torch.empty(n + l, p, device="cuda")
+    ref_mean = mean.double().clone().view(ns, d, m)
+    dc = delta.double().view(ns, ds, m)
+    ref_mean[:, :n] += dc[:, :n]
+    ref_mean[:, n + l:] += dc[:, n:]
+    ref_mean[:, n:n + l] += torch.cumsum(dc[:, n:], dim=0)
+    gc = gcol.double().view(ns, ds, p)
+    ref_g = torch.cat([gc[-1, :n], gc[:, n:].sum(dim=0)])
+    dev_ops.uchain_apply(delta, mean, gcol, gtt, ns, n, l, m, p)
+    torch.cuda.synchronize()
+    assert (mean.double().view(ns, d, m) - ref_mean).abs().max() <= 1e-5 * ref_mean.abs().max()
+    assert (gtt.double() - ref_g).abs().max() <= 1e-5 * ref_g.abs().max()
+
+
+@pytest.mark.parametrize("rows,N,cols", [(6, 8, 4), (256, 64, 128), (100, 33, 32)])
+def test_member_center_f16pair_t_two_sources(dev_ops, rows, N, cols):
+    """Two-source member sum + centring into pair rows and transposed pair planes: equals the
+    centred (src + src2) of the fp32 path to the pair precision (2^-20 relative)."""
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    K = N * cols
+    src = torch.randn(rows, K, device="cuda", generator=g) + 3.0
+    src2 = 0.1 * torch.randn(rows, K, device="cuda", generator=g)
+    acc = torch.zeros(rows, cols, dtype=torch.float64, device="cuda")
+    amax = torch.zeros(rows, cols, device="cuda")
+    dev_ops.member_sum(src, N, cols, None, acc, amax, src2=src2)
+    f16 = torch.float16
+    h, lo, inv = (torch.empty(rows, K, dtype=f16, device="cuda"),
+                  torch.empty(rows, K, dtype=f16, device="cuda"), torch.empty(rows, device="cuda"))
+    ldt = rows + (rows & 1)
+    th, tl, tinv = (torch.empty(K, ldt, dtype=f16, device="cuda"),
+                    torch.empty(K, ldt, dtype=f16, device="cuda"), torch.empty(K, device="cuda"))
+    mean = torch.empty(rows, cols, device="cuda")
+    dev_ops.member_center_f16pair_t(src, src2, N, cols, None, acc, amax, N, mean, h, lo, inv,
+                                    th[:, :rows], tl[:, :rows], tinv)
+    torch.cuda.synchronize()
+    y = (src + src2).double().view(rows, N, cols)
+    mu = y.mean(dim=1)
+    anom = (y - mu[:, None, :]).reshape(rows, K)
+    scale = anom.abs().max()
+    assert (mean.double() - mu).abs().max() <= 1e-6 * mu.abs().max()
+    rec = (h.double() + lo.double()) * inv.double()[:, None]
+    assert (rec - anom).abs().max() <= 2 ** -20 * scale
+    rect = (th[:, :rows].double() + tl[:, :rows].double()) * tinv.double()[:, None]
+    assert (rect - anom.t()).abs().max() <= 2 ** -20 * scale
+
+
+def test_member_center_f16pair_skipped_rows(dev_ops):
+    """Rows [skip0, skip1) (the U block under the derived-U chain) stay out of the basis; the
+    other rows move up; the fp32 copy of the first rows_f32 rows keeps every row."""
+    rows, N, cols, s0, s1 = 12, 16, 8, 4, 8
+    g = torch.Generator(device="cuda").manual_seed(3)
+    src = torch.randn(rows, N * cols, device="cuda", generator=g)
+    acc = torch.zeros(rows, cols, dtype=torch.float64, device="cuda")
+    amax = torch.zeros(rows, cols, device="cuda")
+    dev_ops.member_sum(src, N, cols, None, acc, amax)
+    f16 = torch.float16
+    outs = {}
+    for skip in ((0, 0), (s0, s1)):
+        hr = rows - (skip[1] - skip[0])
+        h, lo, inv = (torch.empty(hr, N * cols, dtype=f16, device="cuda"),
+                      torch.empty(hr, N * cols, dtype=f16, device="cuda"),
+                      torch.empty(hr, device="cuda"))
+        f32 = torch.empty(rows, N * cols, device="cuda")
+        mean = torch.empty(rows, cols, device="cuda")
+        dev_ops.member_center_f16pair(src, N, cols, None, acc, amax, N, mean, h, lo, inv,
+                                      f32=f32, rows_f32=rows, skip=skip)
+        outs[skip] = (h, lo, inv, f32, mean)
+    full, part = outs[(0, 0)], outs[(s0, s1)]
+    keep = list(range(s0)) + list(range(s1, rows))
+    for a, b in zip(full[:3], part[:3]):
+        assert torch.equal(a[keep], b)
+    assert torch.equal(full[3], part[3]) and torch.equal(full[4], part[4])
