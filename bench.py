@@ -8,9 +8,12 @@ smooth_horizon: init + H x (predict, update)) of the configured problem
 (default C3: 128x128 field, CNN 2-32-32-1, N=1024 members,
 H=50), synthetic inputs, random-init CNN.
 
-  value : horizons/s with inputs resident in HBM, CUDA-event timed (max over ranks)
+  value : horizons/s with inputs resident in HBM, CUDA-event timed (max over ranks); on one
+          GPU the horizon is replayed as one CUDA graph (smooth_horizon(graph=True): the same
+          kernels as the eager path, without per-launch host cost; --no-graph times eager)
   e2e   : the same metric through the public API enks.smooth_horizon with host
           (NumPy) inputs and a host result each step
+  kernels : per-kernel-family CUDA-event brackets of one extra eager horizon (untimed)
   roofline : the dominant kernel (the cross-moment contraction P = [A; Yc] Yc^T)
           algorithmic FLOPs / its CUDA-event-measured launch time vs MEASURED_PEAKS.json
   cpu_baseline : the fp64 oracle port timed on this host on a bounded sample
@@ -47,9 +50,11 @@ def _args():
     ap.add_argument("--horizon", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--graph", action="store_true",
-                    help="time replays of a CUDA graph of the horizon (1 GPU); the per-kernel "
-                         "profile then comes from one extra eager horizon")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
+                    help="(default on 1 GPU) time replays of a CUDA graph of the horizon -- "
+                         "smooth_horizon(graph=True), the same kernels as the eager path")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time the eager path (one host launch per kernel)")
     return ap.parse_args()
 
 
@@ -267,7 +272,7 @@ def run_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = ops.launches
-    ops.profile = [] if graph is None else None
+    ops.profile = None  # no event brackets inside the timed region
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     start.record()
@@ -279,16 +284,16 @@ def run_ours(args):
     prof, ops.profile = ops.profile, None
     clk = clocks.stop()
     launches = (ops.launches - launches0) // max(args.steps, 1)
-    prof_steps = args.steps
+    # one extra eager horizon, outside the timed region, for the per-kernel breakdown (CUDA-event
+    # brackets on the launching streams)
+    l0 = ops.launches
+    ops.profile = []
+    enks.smooth_horizon_device(pr.x0, yref_dev, pr.vs, h, pr.N, streams, comm=comm)
+    torch.cuda.synchronize()
+    prof, ops.profile = ops.profile, None
     if graph is not None:
-        # one extra eager horizon, outside the timed region, for the per-kernel breakdown
-        l0 = ops.launches
-        ops.profile = []
-        enks.smooth_horizon_device(pr.x0, yref_dev, pr.vs, h, pr.N, streams)
-        torch.cuda.synchronize()
-        prof, ops.profile = ops.profile, None
         launches = ops.launches - l0
-        prof_steps = 1
+    prof_steps = 1
     elapsed = start.elapsed_time(stop) / 1e3
     cross = [(s, e, f) for tag, s, e, f in prof if tag == "cross"]
     kern_s = sum(s.elapsed_time(e) for s, e, _ in cross) / 1e3
