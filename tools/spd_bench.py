@@ -9,7 +9,7 @@ sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", os.path.dirname(os.path.dir
 from paper_2410_09663_b200.ops import DeviceOps  # noqa: E402
 
 ops = DeviceOps()
-for p in (64, 128, 256, 288):
+for p in [int(v) for v in (sys.argv[1].split(",") if len(sys.argv) > 1 else ("64", "128", "256", "288", "512"))]:
     rng = np.random.default_rng(p)
     a = rng.standard_normal((p, 2 * p))
     s = ops.to_device(a @ a.T / (2 * p) + 0.1 * np.eye(p))
