@@ -118,6 +118,24 @@ int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64
                                int rows_f32, int skip0, int skip1, void* stream);
 
 /*
+ * Forecast + noise in one launch (enks.py:165-168 and 194-200 at step t): the fused 2-32-32-1
+ * CNN forecast (as enks_cnn_forward) whose otherwise idle warps draw the noise jobs of
+ * enks_noise_fill_multi (head words on the host, or head_dev in device memory for graph
+ * replays).  enks_cnn_noise_fusable tells whether the model/shape takes this path (else
+ * ENKS_E_UNSUPPORTED: use enks_noise_fill_multi + enks_cnn_forward).
+ */
+int enks_cnn_noise_fusable(int n_layers, const int* widths, int rows, int cols);
+int enks_cnn_forward_noise(int n_layers, const int* widths, const float* weights,
+                           const float* biases, float alpha, const float* x, int64_t ldx,
+                           const float* u, int64_t ldu, float* out, int64_t ldo, int rows, int cols,
+                           int64_t n_members, const uint32_t* head, const uint32_t* head_dev,
+                           int n_head, int64_t member0, int n_jobs, const uint32_t* t,
+                           const uint32_t* channel, const int* job_rows, const double* const* diag,
+                           float* const* nout, const int64_t* ld_nout, const float* const* base,
+                           const int64_t* ld_base, float* const* out_plus,
+                           const int64_t* ld_plus, void* stream);
+
+/*
  * Derived-U chain (replaces the U rows of enks.py:233-248 for slices 1..n_slices): the slice
  * rows [X; U; dU] obey U_s = U_{s-1} + dU_s member-wise (enks.py:168), so the basis holds only
  * [X; dU] (n + l rows per slice).  mean (full (n + 2l)-row slices from slice 1, ld_mean) +=

@@ -44,6 +44,11 @@ _SIGS = {
     "enks_noise_fill_multi_dev": (_c_int, [_vp, _c_int, _c_i64, _c_i64, _c_int, _c_int, _u32p,
                                            _u32p, _ip, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "enks_member_sum_ws_bytes": (_c_i64, [_c_int, _c_i64, _c_int]),
+    "enks_cnn_noise_fusable": (_c_int, [_c_int, _ip, _c_int, _c_int]),
+    "enks_cnn_forward_noise": (_c_int, [_c_int, _ip, _vp, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _vp,
+                                        _c_i64, _c_int, _c_int, _c_i64, _u32p, _vp, _c_int, _c_i64,
+                                        _c_int, _u32p, _u32p, _ip, _vp, _vp, _vp, _vp, _vp, _vp,
+                                        _vp, _vp]),
     "enks_member_sum": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _c_i64, _c_int, _vp, _vp, _vp,
                                  _vp, _vp]),
     "enks_member_center_f16pair_t": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _c_i64, _c_int,

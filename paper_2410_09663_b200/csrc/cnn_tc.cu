@@ -25,13 +25,17 @@
 // addressing is unchanged; only the horizontal taps are cut at the image boundaries (which
 // fall on warp boundaries), as the zero 'same' padding requires.
 //
-// Warp roles (512 threads): warp 0 = MMA issuer, warp 2 = TMEM allocator,
+// Warp roles (512 threads): warp 0 = MMA issuer, warp 2 = TMEM allocator, warps 1-3 = the step's
+// noise substreams (optional: otherwise idle warps draw W, V_X, V_U with noise_dev.cuh's
+// run_stream in the issue slots the convolution leaves free, instead of a separate launch that
+// would have to share the SMs by time -- neither kernel leaves registers for the other),
 // warps 4-7 / 8-11 = layer-1 producers of the even / odd image rows (thread = pixel; two
 // groups so that two rows of the latency-bound CUDA-core layer are in flight per SM),
 // warps 12-15 = epilogue (thread = pixel = TMEM lane).
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "noise_dev.cuh"
 #include "tc_ptx.cuh"
 
 namespace enks {
@@ -77,7 +81,10 @@ struct CL {
     static constexpr int kOffB3 = kOffW3 + C2 * kW3Stride * 4;
     static constexpr int kOffX = kOffB3 + 16;
     static constexpr int kOffBar = kOffX + (2 * kXD + 2 * kXV) * 4;
-    static constexpr int kSmem = kOffBar + 32 * 8 + 1024;
+    static constexpr int kOffNz = kOffBar + 32 * 8;                       // noise: ki, wi tables
+    static constexpr int kNzWarp = 2 * kMaxRowCols * 4 + kBufWords * 8;     // row slots + words
+    static constexpr int kOffNzW = kOffNz + 256 * 16;                       // [3] per noise warp
+    static constexpr int kSmem = kOffNzW + 3 * kNzWarp + 1024;
     static constexpr int kAccCols = NB;                    // TMEM columns per accumulator
     static constexpr uint32_t kTmemAlloc = 512;
     static_assert(kSmem <= 232448, "shared memory budget");
@@ -140,6 +147,7 @@ struct Cnn3Args {
     int seg;            // image width: 32, 64 or 128
     int debug;  // ENKS_CNN_DEBUG: 1 = no MMAs, 2 = no layer-1 math, 4 = no epilogue math
     int products;  // 3 (default): lo*hi + hi*lo + hi*hi; 2 (ENKS_CNN_PRODUCTS=2): hi*lo + hi*hi
+    NoiseLaunch nz;  // nz.n_jobs > 0: warps 1-3 draw these noise jobs (member-column layout)
 };
 
 template <bool SH>
@@ -592,6 +600,29 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 }
             }
         }
+    } else if (warp >= 1 && warp <= 3 && a.nz.n_jobs > 0) {
+        // ================= noise workers: one substream per warp at a time =================
+        uint64_t* s_ki = reinterpret_cast<uint64_t*>(sm + L::kOffNz);
+        double* s_wi = reinterpret_cast<double*>(sm + L::kOffNz + 256 * 8);
+        load_tables(s_ki, s_wi, threadIdx.x - 32, 96);
+        asm volatile("bar.sync 4, 96;" ::: "memory");
+        uint8_t* mine = sm + L::kOffNzW + (warp - 1) * L::kNzWarp;
+        float* s_row = reinterpret_cast<float*>(mine);
+        uint64_t* buf = reinterpret_cast<uint64_t*>(mine + 2 * kMaxRowCols * 4);
+        const int64_t nm = a.nz.args.n_members;
+        const int64_t total = nm * a.nz.n_jobs;
+        for (int64_t sidx = (int64_t)blockIdx.x * 3 + (warp - 1); sidx < total;
+             sidx += (int64_t)gridDim.x * 3) {
+            const int j = (int)(sidx / nm);
+            const int64_t local = sidx - (int64_t)j * nm;
+            const Job jb = j == 0 ? a.nz.args.job[0]
+                                  : (j == 1 ? a.nz.args.job[1]
+                                            : (j == 2 ? a.nz.args.job[2] : a.nz.args.job[3]));
+            if (a.nz.rb)
+                run_stream<true>(a.nz.args, jb, local, lane, s_row, buf, s_ki, s_wi);
+            else
+                run_stream<false>(a.nz.args, jb, local, lane, s_row, buf, s_ki, s_wi);
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -608,10 +639,12 @@ bool cnn3_tc_applicable(int n_layers, const int* widths, int rows, int cols) {
 template <bool SH>
 int launch_cnn3(const Cnn3Args& a, int grid, cudaStream_t st);
 
-int cnn3_tc_forward(const float* weights, const float* biases, float alpha, const float* x,
-                    int64_t ldx, const float* u, int64_t ldu, float* out, int64_t ldo, int rows,
-                    int cols, int64_t n_members, cudaStream_t st) {
+namespace {
+int cnn3_tc_forward_nz(const float* weights, const float* biases, float alpha, const float* x,
+                       int64_t ldx, const float* u, int64_t ldu, float* out, int64_t ldo, int rows,
+                       int cols, int64_t n_members, cudaStream_t st, const NoiseLaunch* nz) {
     Cnn3Args a;
+    if (nz) a.nz = *nz; else a.nz.n_jobs = 0;
     a.w1 = weights;
     a.w2 = weights + C1 * 2 * 9;
     a.w3 = a.w2 + C2 * C1 * 9;
@@ -635,6 +668,14 @@ int cnn3_tc_forward(const float* weights, const float* biases, float alpha, cons
     if (cols == W) return launch_cnn3<true>(a, grid, st);
     return launch_cnn3<false>(a, grid, st);
 }
+}  // namespace
+
+int cnn3_tc_forward(const float* weights, const float* biases, float alpha, const float* x,
+                    int64_t ldx, const float* u, int64_t ldu, float* out, int64_t ldo, int rows,
+                    int cols, int64_t n_members, cudaStream_t st) {
+    return cnn3_tc_forward_nz(weights, biases, alpha, x, ldx, u, ldu, out, ldo, rows, cols,
+                              n_members, st, nullptr);
+}
 
 template <bool SH>
 int launch_cnn3(const Cnn3Args& a, int grid, cudaStream_t st) {
@@ -654,3 +695,41 @@ int launch_cnn3(const Cnn3Args& a, int grid, cudaStream_t st) {
 }
 
 }  // namespace enks
+
+extern "C" {
+
+int enks_cnn_noise_fusable(int n_layers, const int* widths, int rows, int cols) {
+    return widths && enks::cnn3_tc_applicable(n_layers, widths, rows, cols) ? 1 : 0;
+}
+
+int enks_cnn_forward_noise(int n_layers, const int* widths, const float* weights,
+                           const float* biases, float alpha, const float* x, int64_t ldx,
+                           const float* u, int64_t ldu, float* out, int64_t ldo, int rows, int cols,
+                           int64_t n_members, const uint32_t* head, const uint32_t* head_dev,
+                           int n_head, int64_t member0, int n_jobs, const uint32_t* t,
+                           const uint32_t* channel, const int* job_rows, const double* const* diag,
+                           float* const* nout, const int64_t* ld_nout, const float* const* base,
+                           const int64_t* ld_base, float* const* out_plus,
+                           const int64_t* ld_plus, void* stream) {
+    ENKS_REQUIRE(widths && weights && biases && x && u && out, "enks_cnn_forward_noise: null pointer");
+    if (!enks::cnn3_tc_applicable(n_layers, widths, rows, cols)) {
+        enks::set_error("enks_cnn_forward_noise: only the fused 2-32-32-1 forecast draws noise "
+                        "(check enks_cnn_noise_fusable)");
+        return ENKS_E_UNSUPPORTED;
+    }
+    ENKS_REQUIRE(n_jobs >= 1 && n_jobs <= enks::kMaxJobs, "enks_cnn_forward_noise: 1..%d jobs",
+                 enks::kMaxJobs);
+    if (n_members <= 0) return ENKS_OK;
+    enks::Job jobs[enks::kMaxJobs];
+    for (int q = 0; q < n_jobs; ++q)
+        jobs[q] = enks::Job{t[q], channel[q], job_rows[q], diag[q], nout[q], ld_nout[q],
+                            base[q], ld_base[q], out_plus[q], ld_plus[q]};
+    enks::NoiseLaunch L;
+    int rc = enks::make_noise_launch(head, n_head, head_dev, member0, n_members, cols, jobs,
+                                     n_jobs, L);
+    if (rc) return rc;
+    return enks::cnn3_tc_forward_nz(weights, biases, alpha, x, ldx, u, ldu, out, ldo, rows, cols,
+                                     n_members, enks::as_stream(stream), &L);
+}
+
+}  // extern "C"

@@ -456,6 +456,13 @@ class DeviceSmoother:
         # all channels diagonal: draw W, V_X, V_U of a step in one launch during predict
         self.fused_noise = (all(c.kind == "diag" for c in (self.noise_w, self.noise_vx, self.noise_vu))
                             and hasattr(ops, "noise_fill_multi"))
+        # the fused 2-32-32-1 forecast kernel can draw some of the step's noise jobs (W first) in
+        # its three idle warps; ENKS_NOISE_IN_CNN = how many (0..3; default 0: measured slower --
+        # three warps per SM cannot keep up with the stand-alone launch)
+        fusable = (self.fused_noise and self.forecast.kind == "cnn"
+                   and hasattr(ops, "cnn_forward_noise") and ops.cnn_noise_fusable(self.forecast, self.n))
+        self.noise_in_forecast = (max(0, min(3, int(os.environ.get("ENKS_NOISE_IN_CNN", "0"))))
+                                  if fusable else 0)
         if self.fused_noise and getattr(self, "v_raw", None) is None:
             self.v_raw = ops.empty(self.q, self.K)  # raw [v_x; v_u] of the newest step
         # observation never materialised: its centring forms [x; u] + [v_x; v_u] on the fly and
@@ -606,19 +613,26 @@ class DeviceSmoother:
             # second stream, concurrently with the forecast (both are SIMT-issue / latency bound
             # and share SMs): dU = w, U = u + w, raw v_x, raw v_u; the two sums that need the
             # forecast (x' + v_x, U + v_u) follow on the main stream.
-            ns = self._noise_stream()
-            if ns is not None:
-                ns.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(ns) if ns is not None else contextlib.nullcontext():
-                ops.noise_fill_multi(head, self.member0, self.Nl, self.m, [
-                    dict(t=tau, ch=CH_W, rows=l, diag=self.noise_w.diag, out=sr[n + l:],
+            jobs = [dict(t=tau, ch=CH_W, rows=l, diag=self.noise_w.diag, out=sr[n + l:],
                          base=self.last[n:], out_plus=sr[n:n + l]),
                     dict(t=tau, ch=CH_VX, rows=n, diag=self.noise_vx.diag, out=self.v_raw[:n]),
                     dict(t=tau, ch=CH_VU, rows=l, diag=self.noise_vu.diag,
-                         out=self.v_raw[n:n + l]),
-                ])
-            self.forecast(ops, self.last, sr[:n], n, self.Nl)
-            if ns is not None:
+                         out=self.v_raw[n:n + l])]
+            # the first `noise_in_forecast` jobs are drawn by the fused CNN's idle warps (cnn_tc.cu),
+            # the rest by the noise kernel on a second stream
+            k = self.noise_in_forecast
+            ns = self._noise_stream()
+            if k < len(jobs):
+                if ns is not None:
+                    ns.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(ns) if ns is not None else contextlib.nullcontext():
+                    ops.noise_fill_multi(head, self.member0, self.Nl, self.m, jobs[k:])
+            if k:
+                ops.cnn_forward_noise(self.forecast, self.last[:n], self.last[n:], sr[:n], self.Nl,
+                                      head, self.member0, jobs[:k])
+            else:
+                self.forecast(ops, self.last, sr[:n], n, self.Nl)
+            if ns is not None and k < len(jobs):
                 torch.cuda.current_stream().wait_stream(ns)
             if not self.obs_fused:
                 ops.add(sr[:n + l], self.v_raw, ob[:n + l])

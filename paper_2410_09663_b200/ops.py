@@ -424,6 +424,43 @@ class DeviceOps:
                       int(x.shape[0]), int(cnn.cols), int(n_members), _p(ws), int(wsb),
                       self._stream())
 
+    def cnn_noise_fusable(self, cnn, rows) -> bool:
+        """True when the fused 2-32-32-1 forecast can also draw the step's noise (cnn_tc.cu)."""
+        widths = (ctypes.c_int * len(cnn.widths))(*cnn.widths)
+        return bool(self.lib.enks_cnn_noise_fusable(cnn.n_layers, widths, int(rows), int(cnn.cols)))
+
+    def cnn_forward_noise(self, cnn, x, u, out, n_members, head, member0, jobs):
+        """Forecast out = f(x, u) with the noise jobs (as noise_fill_multi) drawn by the same
+        launch's otherwise idle warps: one kernel instead of two that share SMs by time."""
+        widths = (ctypes.c_int * len(cnn.widths))(*cnn.widths)
+        n = len(jobs)
+        u32 = ctypes.c_uint32 * n
+        vp = ctypes.c_void_p * n
+        i64 = ctypes.c_int64 * n
+        get = lambda k: [j.get(k) for j in jobs]  # noqa: E731
+        if isinstance(head, DeviceHead):
+            words, head_dev, n_head = None, _p(head.words), head.n
+        else:
+            words = (ctypes.c_uint32 * len(head))(*[int(w) for w in head])
+            head_dev, n_head = None, len(head)
+        self.launches += 1
+        flops = n_members * x.shape[0] * cnn.cols * sum(
+            18 * a * b for a, b in zip(cnn.widths[:-1], cnn.widths[1:]))
+        with self._prof("forecast", flops):
+            _lib.call("enks_cnn_forward_noise", cnn.n_layers, widths, _p(cnn.w_dev), _p(cnn.b_dev),
+                      float(cnn.alpha), _p(x), _ld(x), _p(u), _ld(u), _p(out), _ld(out),
+                      int(x.shape[0]), int(cnn.cols), int(n_members), words, head_dev, n_head,
+                      int(member0), n, u32(*[int(j["t"]) for j in jobs]),
+                      u32(*[int(j["ch"]) for j in jobs]),
+                      (ctypes.c_int * n)(*[int(j["rows"]) for j in jobs]),
+                      vp(*[_p(v) for v in get("diag")]), vp(*[_p(v) for v in get("out")]),
+                      i64(*[_ld(v) if v is not None else 0 for v in get("out")]),
+                      vp(*[_p(v) for v in get("base")]),
+                      i64(*[_ld(v) if v is not None else 0 for v in get("base")]),
+                      vp(*[_p(v) for v in get("out_plus")]),
+                      i64(*[_ld(v) if v is not None else 0 for v in get("out_plus")]),
+                      self._stream())
+
     def burgers_forward(self, bur, x, u, out, n_members):
         """bur: engine.Forecaster of kind 'burgers' (grid, solver constants, vmax/flags)."""
         g, sub = bur.grid_n, bur.substeps

@@ -581,3 +581,38 @@ def test_member_center_f16pair_skipped_rows(dev_ops):
     for a, b in zip(full[:3], part[:3]):
         assert torch.equal(a[keep], b)
     assert torch.equal(full[3], part[3]) and torch.equal(full[4], part[4])
+
+
+@pytest.mark.parametrize("cols,N", [(128, 37), (64, 20), (32, 9)])
+def test_cnn_forward_noise_matches_separate_launches(dev_ops, pm, cols, N):
+    """enks_cnn_forward_noise (noise drawn by the fused forecast's idle warps) == the forecast
+    and enks_noise_fill_multi launched separately, bit for bit."""
+    from paper_2410_09663_b200.engine import Forecaster
+    from paper_2410_09663_b200.matvar import entropy_head
+
+    n = cols
+    model = pm.dynamics.CNNDynamics(rows=n, cols=cols, widths=(2, 32, 32, 1), seed=1)
+    fc = Forecaster(model, dev_ops, n, n)
+    assert dev_ops.cnn_noise_fusable(fc, n)
+    K = N * cols
+    g = torch.Generator(device="cuda").manual_seed(cols)
+    last = torch.randn(2 * n, K, device="cuda", generator=g)
+    diag = [torch.rand(n, dtype=torch.float64, device="cuda", generator=g) + 0.5 for _ in range(3)]
+    head = entropy_head(4, (2,))
+    outs = {}
+    for fused in (False, True):
+        o = dict(x=torch.empty(n, K, device="cuda"), w=torch.empty(n, K, device="cuda"),
+                 u=torch.empty(n, K, device="cuda"), vx=torch.empty(n, K, device="cuda"),
+                 vu=torch.empty(n, K, device="cuda"))
+        jobs = [dict(t=3, ch=0, rows=n, diag=diag[0], out=o["w"], base=last[n:], out_plus=o["u"]),
+                dict(t=3, ch=1, rows=n, diag=diag[1], out=o["vx"]),
+                dict(t=3, ch=2, rows=n, diag=diag[2], out=o["vu"])]
+        if fused:
+            dev_ops.cnn_forward_noise(fc, last[:n], last[n:], o["x"], N, head, 5, jobs)
+        else:
+            dev_ops.noise_fill_multi(head, 5, N, cols, jobs)
+            fc(dev_ops, last, o["x"], n, N)
+        torch.cuda.synchronize()
+        outs[fused] = o
+    for k in outs[False]:
+        assert torch.equal(outs[False][k], outs[True][k]), k
