@@ -242,6 +242,12 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         // ================= MMA issuer =================
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_tf32(W, L::kAccCols);
+            // descriptors are built once: the start-address field (addr >> 4, 14 bits) of a tile
+            // at a byte offset o from a base is the base descriptor + (o >> 4)
+            const uint64_t dA0 = ptx::desc_kmajor_sw128(sm + L::kOffA);
+            const uint64_t dB0 = ptx::desc_kmajor_sw128(sm + L::kOffB);
+            constexpr uint64_t kAT = L::kATile >> 4, kBT = L::kBTile >> 4;
+            const bool do_mma = !(a.debug & 1), p3 = a.products == 3;
             int it = 0;
             for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
                 for (int r = 0; r < n; ++r) {
@@ -249,28 +255,27 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     const int slot = Rg % NA;
                     ptx::mbar_wait(&a_full[slot], (uint32_t)((Rg / NA) & 1));
                     ptx::tc_fence_after();
-                    const uint8_t* ah_t = sm + L::kOffA + (slot * 2 + 0) * L::kATile;
-                    const uint8_t* al_t = sm + L::kOffA + (slot * 2 + 1) * L::kATile;
+                    const uint64_t dah0 = dA0 + (uint64_t)(slot * 2) * kAT, dal0 = dah0 + kAT;
                     if constexpr (SH) {
                         // D_r[x][(dy, co)] = sum_dx sum_ci h1[r][x + dx - 1][ci] W2[co][ci][dy][dx]
                         const int q = Rg % NACC;
                         ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Rg / NACC) & 1) ^ 1));
                         ptx::tc_fence_after();
                         const uint32_t d = tmem + (uint32_t)(q * L::kAccCols);
+                        if (do_mma) {
 #pragma unroll
-                        for (int dx = 0; dx < 3; ++dx) {
-                            const uint8_t* bh_t = sm + L::kOffB + (dx * 2 + 0) * L::kBTile;
-                            const uint8_t* bl_t = sm + L::kOffB + (dx * 2 + 1) * L::kBTile;
+                            for (int dx = 0; dx < 3; ++dx) {
+                                const uint64_t bh0 = dB0 + (uint64_t)(dx * 2) * kBT;
 #pragma unroll
-                            for (int k = 0; k < ((a.debug & 1) ? 0 : C1 / 8); ++k) {
-                                const uint64_t adh = ptx::desc_kmajor_sw128(ah_t + dx * 128 + 32 * k);
-                                const uint64_t adl = ptx::desc_kmajor_sw128(al_t + dx * 128 + 32 * k);
-                                const uint64_t bdh = ptx::desc_kmajor_sw128(bh_t + 32 * k);
-                                const uint64_t bdl = ptx::desc_kmajor_sw128(bl_t + 32 * k);
-                                const uint32_t acc0 = (dx == 0 && k == 0) ? 0u : 1u;
-                                if (a.products == 3) ptx::mma_tf32_ss(d, adl, bdh, idesc, acc0);
-                                ptx::mma_tf32_ss(d, adh, bdl, idesc, a.products == 3 ? 1u : acc0);
-                                ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                                for (int k = 0; k < C1 / 8; ++k) {  // A starts dx 128-B rows down
+                                    const uint64_t adh = dah0 + (uint64_t)(dx * 8 + 2 * k);
+                                    const uint64_t adl = dal0 + (uint64_t)(dx * 8 + 2 * k);
+                                    const uint64_t bdh = bh0 + (uint64_t)(2 * k), bdl = bdh + kBT;
+                                    const uint32_t acc0 = (dx == 0 && k == 0) ? 0u : 1u;
+                                    if (p3) ptx::mma_tf32_ss(d, adl, bdh, idesc, acc0);
+                                    ptx::mma_tf32_ss(d, adh, bdl, idesc, p3 ? 1u : acc0);
+                                    ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                                }
                             }
                         }
                         ptx::mma_commit(&acc_full[q]);
@@ -286,18 +291,18 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                                 ptx::tc_fence_after();
                             }
                             const uint32_t d = tmem + (uint32_t)(q * L::kAccCols);
-                            const uint8_t* bh_t = sm + L::kOffB + (dy * 2 + 0) * L::kBTile;
-                            const uint8_t* bl_t = sm + L::kOffB + (dy * 2 + 1) * L::kBTile;
+                            const uint64_t bh0 = dB0 + (uint64_t)(dy * 2) * kBT;
+                            if (do_mma) {
 #pragma unroll
-                            for (int k = 0; k < ((a.debug & 1) ? 0 : C1 / 8); ++k) {
-                                const uint64_t adh = ptx::desc_kmajor_sw128(ah_t + 32 * k);
-                                const uint64_t adl = ptx::desc_kmajor_sw128(al_t + 32 * k);
-                                const uint64_t bdh = ptx::desc_kmajor_sw128(bh_t + 32 * k);
-                                const uint64_t bdl = ptx::desc_kmajor_sw128(bl_t + 32 * k);
-                                const uint32_t acc0 = (first && k == 0) ? 0u : 1u;
-                                if (a.products == 3) ptx::mma_tf32_ss(d, adl, bdh, idesc, acc0);
-                                ptx::mma_tf32_ss(d, adh, bdl, idesc, a.products == 3 ? 1u : acc0);
-                                ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                                for (int k = 0; k < C1 / 8; ++k) {
+                                    const uint64_t adh = dah0 + (uint64_t)(2 * k);
+                                    const uint64_t adl = dal0 + (uint64_t)(2 * k);
+                                    const uint64_t bdh = bh0 + (uint64_t)(2 * k), bdl = bdh + kBT;
+                                    const uint32_t acc0 = (first && k == 0) ? 0u : 1u;
+                                    if (p3) ptx::mma_tf32_ss(d, adl, bdh, idesc, acc0);
+                                    ptx::mma_tf32_ss(d, adh, bdl, idesc, p3 ? 1u : acc0);
+                                    ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                                }
                             }
                             // row y complete: after its dy=2 contribution, or the last row's dy=1
                             if (dy == 2 || (r == n - 1 && dy == 1)) ptx::mma_commit(&acc_full[q]);
