@@ -23,6 +23,8 @@
 #include <cuda_fp16.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -72,6 +74,16 @@ __device__ __forceinline__ void f16p_store_row(const P16& p, int split, int64_t 
     const float sa = p.alpha * p.inv_sa[r];
     float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + c_first;
     if (!p.c0 && !p.bias) {
+        if (ncol == NC && (((uintptr_t)orow) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < NC; j += 4)
+                *reinterpret_cast<float4*>(orow + j) =
+                    make_float4(acc[j] * sa * p.inv_sb[c_first + j],
+                                acc[j + 1] * sa * p.inv_sb[c_first + j + 1],
+                                acc[j + 2] * sa * p.inv_sb[c_first + j + 2],
+                                acc[j + 3] * sa * p.inv_sb[c_first + j + 3]);
+            return;
+        }
 #pragma unroll
         for (int j = 0; j < NC; ++j)
             if (j < ncol) orow[j] = acc[j] * sa * p.inv_sb[c_first + j];
@@ -325,7 +337,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t rank = ptx::cluster_ctarank();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * BM;
-    const int64_t col0 = (int64_t)blockIdx.y * 256;
+    // persistent over 256-column tiles (blockIdx.y, + gridDim.y, ...): the next tile's loads and
+    // MMAs overlap this tile's epilogue (double-buffered TMEM slots continue across tiles)
+    const int64_t n_tiles = (p.N + 255) / 256;
     const int split = blockIdx.z;
     const int total_chunks = (int)((p.K + KC - 1) / KC);
     const int cps = (total_chunks + p.splits - 1) / p.splits;
@@ -364,10 +378,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            const int32_t brow = (int32_t)(col0 + rank * 128);
-            for (int i = 0; i < n_chunks; ++i) {
-                const int s = i % S;
-                ptx::mbar_wait_bounded(&empty[s], (uint32_t)(((i / S) & 1) ^ 1));
+          int ig = 0;  // chunk counter across tiles (stage ring position)
+          for (int64_t nt = blockIdx.y; nt < n_tiles; nt += gridDim.y) {
+            const int32_t brow = (int32_t)(nt * 256 + rank * 128);
+            for (int i = 0; i < n_chunks; ++i, ++ig) {
+                const int s = ig % S;
+                ptx::mbar_wait_bounded(&empty[s], (uint32_t)(((ig / S) & 1) ^ 1));
                 if (rank == 0)
                     ptx::mbar_arrive_expect_tx(&full[s], 2 * (p.products == 3 ? LP::kStage
                                                                              : LP::kStage - LP::kA));
@@ -377,20 +393,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::tma_load_2d_pair(&tBh, &full[s], bh(s), kc, brow);
                 ptx::tma_load_2d_pair(&tBl, &full[s], bl(s), kc, brow);
             }
+          }
         }
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             constexpr uint32_t idesc = idesc_f16(2 * BM, 256);
-            for (int i = 0; i < n_chunks; ++i) {
-                const int s = i % S;
-                const int g = i / chain, slot = g & 1;
+            int ig = 0, gbase = 0;  // chunk / chain-group counters across tiles
+            for (int64_t nt = blockIdx.y; nt < n_tiles; nt += gridDim.y, gbase += n_groups) {
+            for (int i = 0; i < n_chunks; ++i, ++ig) {
+                const int s = ig % S;
+                const int g = gbase + i / chain, slot = g & 1;
                 const bool first = (i % chain) == 0;
                 const bool last = (i % chain) == chain - 1 || i == n_chunks - 1;
                 if (first) {
                     ptx::mbar_wait_bounded(&tempty[slot], (uint32_t)(((g >> 1) & 1) ^ 1));
                     ptx::tc_fence_after();
                 }
-                ptx::mbar_wait_bounded(&full[s], (uint32_t)((i / S) & 1));
+                ptx::mbar_wait_bounded(&full[s], (uint32_t)((ig / S) & 1));
                 ptx::tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(slot * LP::kCols);
 #pragma unroll
@@ -408,16 +427,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::mma_commit_pair(&empty[s], 0x3);
                 if (last) ptx::mma_commit_pair(&tfull[slot], 0x3);
             }
+            }
         }
     } else if (warp >= 4) {
         const int wg = (warp - 4) >> 2;
         constexpr int kCols = 128;  // per warpgroup
         const int erow = ((warp & 3) << 5) + lane;
         const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+        int gbase = 0;
+        for (int64_t nt = blockIdx.y; nt < n_tiles; nt += gridDim.y, gbase += n_groups) {
+        const int64_t col0 = nt * 256;
         float acc[kCols];
 #pragma unroll
         for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
-        for (int g = 0; g < n_groups; ++g) {
+        for (int gl = 0; gl < n_groups; ++gl) {
+            const int g = gbase + gl;
             const int slot = g & 1;
             ptx::mbar_wait_bounded(&tfull[slot], (uint32_t)((g >> 1) & 1));
             ptx::tc_fence_after();
@@ -438,6 +462,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int64_t c_first = col0 + (int64_t)wg * kCols;
         if (r < p.M && c_first < p.N)
             f16p_store_row(p, split, r, c_first, (int)min((int64_t)kCols, p.N - c_first), acc);
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -764,6 +789,11 @@ int gemm_f16pair_impl(int64_t M, int64_t N, int64_t K, float alpha, const void* 
     int rc;
     if (pair) {
         grid.x = (unsigned)((m_tiles + 1) & ~1);
+        // one wave of CTA pairs, each looping over 256-column tiles
+        const int64_t pairs_xz = (int64_t)(grid.x / 2) * split;
+        const int64_t slots = kNumSMs / 2;
+        const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(n_tiles, slots / std::max<int64_t>(1, pairs_xz)));
+        grid.y = (unsigned)gy;
         rc = launch_pair(maps, p, grid, st);
     } else switch (BN) {
         case 32: rc = launch16<32>(maps, p, grid, st); break;
