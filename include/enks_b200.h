@@ -73,7 +73,12 @@ int enks_noise_fill_multi(const uint32_t* head, int n_head, int64_t member0, int
                           int cols, int n_jobs, const uint32_t* t, const uint32_t* channel,
                           const int* rows, const double* const* diag, float* const* out,
                           const int64_t* ld_out, const float* const* base, const int64_t* ld_base,
-                          float* const* out_plus, const int64_t* ld_plus, void* stream);
+                          float* const* out_plus, const int64_t* ld_plus, void* ws,
+                          int64_t ws_bytes, void* stream);
+/* Workspace for the segmented launch (few substreams: each substream cut into chunks drawn by
+ * separate warps, chained in order); 0 = one warp per substream.  ws may be NULL (then never
+ * segmented). */
+int64_t enks_noise_ws_bytes(int64_t n_members, int n_jobs, int max_rows, int cols);
 /* Same, with the head words in DEVICE memory (n_head of them), so a captured CUDA graph can
  * be replayed for another (seed, prefix) by rewriting the words (closed-loop MPC steps use
  * NoiseStreams.child(k), matvar.py:153-154). */
@@ -82,7 +87,7 @@ int enks_noise_fill_multi_dev(const uint32_t* head_dev, int n_head, int64_t memb
                               const uint32_t* channel, const int* rows, const double* const* diag,
                               float* const* out, const int64_t* ld_out, const float* const* base,
                               const int64_t* ld_base, float* const* out_plus,
-                              const int64_t* ld_plus, void* stream);
+                              const int64_t* ld_plus, void* ws, int64_t ws_bytes, void* stream);
 
 /*
  * Member statistics (K4/K5).  Replaces members.mean(axis=0) (enks.py:171, 248),

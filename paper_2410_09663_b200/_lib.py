@@ -40,9 +40,11 @@ _SIGS = {
     "enks_noise_fill": (_c_int, [_u32p, _c_int, ctypes.c_uint32, ctypes.c_uint32, _c_i64, _c_i64,
                                  _c_int, _c_int, _vp, _vp, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp]),
     "enks_noise_fill_multi": (_c_int, [_u32p, _c_int, _c_i64, _c_i64, _c_int, _c_int, _u32p, _u32p,
-                                       _ip, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+                                       _ip, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _vp]),
     "enks_noise_fill_multi_dev": (_c_int, [_vp, _c_int, _c_i64, _c_i64, _c_int, _c_int, _u32p,
-                                           _u32p, _ip, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+                                           _u32p, _ip, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                           _c_i64, _vp]),
+    "enks_noise_ws_bytes": (_c_i64, [_c_i64, _c_int, _c_int, _c_int]),
     "enks_member_sum_ws_bytes": (_c_i64, [_c_int, _c_i64, _c_int]),
     "enks_cnn_noise_fusable": (_c_int, [_c_int, _ip, _c_int, _c_int]),
     "enks_cnn_forward_noise": (_c_int, [_c_int, _ip, _vp, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _vp,

@@ -11,6 +11,8 @@
 // accept, resolve numpy's sequential parse on bitmasks (speculative wedge tests in parallel,
 // tails warp-uniformly) and stage whole rows for float4 stores.  The word consumption is
 // exactly numpy's sequential order.
+#include <climits>
+
 #include "noise_dev.cuh"
 
 namespace enks {
@@ -33,16 +35,218 @@ __global__ void __launch_bounds__(kWarps * 32, 6) noise_kernel(const Args args) 
     run_stream<RB>(args, a, local, lane, &s_row[RB ? warp : 0][0], s_buf[warp], s_ki, s_wi);
 }
 
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_volatile_int(const int* p) { return *(const volatile int*)p; }
+__device__ __forceinline__ long long ld_volatile_ll(const long long* p) {
+    return *(const volatile long long*)p;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Segmented substreams for latency-bound launches (few substreams: small ensembles, or one rank's
+// shard).  A substream's word sequence is cut into chunks of G groups (32 words each); one warp
+// per (substream, chunk), taken in ticket order (chunk-major) so every chunk's predecessor is
+// already running or done.  Phase A counts the normals started inside the chunk (speculating that
+// the parse enters at the chunk's first word), then the warp waits for its predecessor's record
+// (words of this chunk consumed by the previous normal = entry carry, normals before the chunk =
+// prefix), recounts in the rare case the entry differs (~1.5 % of chunks), publishes its own
+// record, and phase B re-parses the chunk emitting normals prefix, prefix + 1, ... -- numpy's
+// order exactly, each chunk's words generated twice.  The last chunk runs on until the
+// substream has all its normals (the chunk count is an estimate of the words needed).
+struct SegRec {
+    int carry;
+    int flag;
+    long long prefix;  // normals started before the next chunk (inclusive of this one)
+};
+
+constexpr int kSegWarps = 4;
+
+__global__ void __launch_bounds__(kSegWarps * 32) noise_seg_kernel(const Args args, int n_jobs,
+                                                                   int n_chunks, int G,
+                                                                   SegRec* recs,
+                                                                   unsigned* ticket) {
+    __shared__ uint64_t s_ki[256];
+    __shared__ double s_wi[256];
+    __shared__ uint64_t s_buf[kSegWarps][kBufWords];
+    load_tables(s_ki, s_wi, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* buf = s_buf[warp];
+    const int64_t nm = args.n_members;
+    const int64_t n_streams = nm * n_jobs;
+    const int64_t n_units = n_streams * n_chunks;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const int cols = args.cols;
+    for (;;) {
+        unsigned t0 = 0;
+        if (lane == 0) t0 = atomicAdd(ticket, 1u);
+        const int64_t t = (int64_t)__shfl_sync(0xffffffffu, t0, 0);
+        if (t >= n_units) break;
+        const int c = (int)(t / n_streams);
+        const int64_t sidx = t - (int64_t)c * n_streams;
+        const int j = (int)(sidx / nm);
+        const int64_t local = sidx - (int64_t)j * nm;
+        const Job a = j == 0 ? args.job[0] : (j == 1 ? args.job[1] : (j == 2 ? args.job[2] : args.job[3]));
+        uint64_t k0, k1;
+        if (args.head_dev) {
+            Head hd;
+            hd.n = args.head.n;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) hd.w[q] = q < hd.n ? __ldg(args.head_dev + q) : 0u;
+            seed_key(hd, (uint32_t)(args.member0 + local), a.t, a.ch, k0, k1);
+        } else {
+            seed_key(args.head, (uint32_t)(args.member0 + local), a.t, a.ch, k0, k1);
+        }
+        const int total = a.rows * cols;
+        const int64_t col0 = local * cols;
+        const bool last = c == n_chunks - 1;
+        const int g_begin = c * G, g_end = last ? INT_MAX : (c + 1) * G;
+        int base_w = -(1 << 30);
+        auto word = [&](int ww) -> uint64_t {
+            if (ww >= base_w && ww < base_w + kBufWords) return buf[ww - base_w];
+            Block4 b = philox(k0, k1, (uint64_t)(ww >> 2) + 1);
+            int s = (int)(ww & 3);
+            return s == 0 ? b.v0 : (s == 1 ? b.v1 : (s == 2 ? b.v2 : b.v3));
+        };
+        // parse groups [g_begin, g_end) entering with `carry`; EMIT: write normals q0, q0 + 1, ...
+        // (< total); returns the count of normals started in the range, carry out in `carry`
+        auto parse = [&](bool emit, int& carry, long long q0) -> long long {
+            long long cnt = 0;
+            base_w = -(1 << 30);
+            for (int g = g_begin; g < g_end; ++g) {
+                const int w = g * 32;
+                if (last && q0 + cnt >= total) break;
+                if (w >= base_w + kBufWords) {
+                    base_w = w;
+                    __syncwarp();
+#pragma unroll
+                    for (int bq = 0; bq < kBufWords / 128; ++bq) {
+                        const Block4 b = philox(k0, k1, (uint64_t)((base_w >> 2) + bq * 32 + lane) + 1);
+                        buf[bq * 128 + 4 * lane + 0] = b.v0;
+                        buf[bq * 128 + 4 * lane + 1] = b.v1;
+                        buf[bq * 128 + 4 * lane + 2] = b.v2;
+                        buf[bq * 128 + 4 * lane + 3] = b.v3;
+                    }
+                    __syncwarp();
+                }
+                const uint64_t raw = buf[w - base_w + lane];
+                double x;
+                unsigned O;
+                int next_carry;
+                resolve_group(raw, w, carry, lane, s_ki, s_wi, word, x, O, next_carry);
+                carry = next_carry;
+                if (emit && ((O >> lane) & 1u)) {
+                    const long long q = q0 + cnt + __popc(O & lt_mask);
+                    if (q < total) {
+                        const int r = (int)(q / cols), jj = (int)(q - (long long)r * cols);
+                        const double v = a.diag ? x * a.diag[r] : x;
+                        const float f = (float)v;
+                        if (a.out) a.out[r * a.ld_out + col0 + jj] = f;
+                        if (a.out_plus)
+                            a.out_plus[r * a.ld_plus + col0 + jj] = a.base[r * a.ld_base + col0 + jj] + f;
+                    }
+                }
+                cnt += __popc(O);
+            }
+            return cnt;
+        };
+        int carry_in = 0;
+        long long prefix = 0;
+        long long cnt = 0;
+        int carry_out = 0;
+        if (!last) {  // phase A (speculative entry carry 0)
+            carry_out = 0;
+            cnt = parse(false, carry_out, 0);
+        }
+        if (c > 0) {  // predecessor's record
+            const SegRec* pr = recs + (int64_t)(c - 1) * n_streams + sidx;
+            if (lane == 0) {
+                while (ld_acquire(&pr->flag) == 0) {
+                }
+            }
+            __syncwarp();
+            carry_in = ld_volatile_int(&pr->carry);
+            prefix = ld_volatile_ll(&pr->prefix) - 0;
+        }
+        if (!last) {
+            if (carry_in != 0) {  // the entry differs from the speculation: recount
+                carry_out = carry_in;
+                cnt = parse(false, carry_out, 0);
+            }
+            SegRec* me = recs + (int64_t)c * n_streams + sidx;
+            if (lane == 0) {
+                me->carry = carry_out;
+                me->prefix = prefix + cnt;
+                __threadfence();
+                st_release(&me->flag, 1);
+            }
+        }
+        // phase B: emit this chunk's normals from index prefix
+        if (prefix < total) {
+            int cb = carry_in;
+            parse(true, cb, prefix);
+        }
+        __syncwarp();
+    }
+}
 }  // namespace
 }  // namespace enks
 
 namespace enks {
 namespace {
+// segmented plan: (n_chunks, G) for n_streams substreams of up to max_normals normals, or
+// n_chunks = 0 when one warp per substream already fills the GPU
+struct SegPlan {
+    int n_chunks = 0, G = 0;
+};
+SegPlan seg_plan(int64_t n_streams, int64_t max_normals) {
+    SegPlan P;
+    if (n_streams <= 0 || n_streams >= 8LL * kNumSMs) return P;
+    const int64_t groups = (max_normals * 104 / 100 + 64 + 31) / 32;  // ~1.5 % rejected starts
+    int64_t chunks = (16LL * kNumSMs + n_streams - 1) / n_streams;
+    if (chunks > groups / 8) chunks = groups / 8;  // >= 8 groups per chunk
+    if (chunks < 2) return P;
+    P.n_chunks = (int)chunks;
+    P.G = (int)((groups + chunks - 1) / chunks);
+    return P;
+}
+
+int64_t seg_ws_bytes(int64_t n_streams, int64_t max_normals) {
+    const SegPlan P = seg_plan(n_streams, max_normals);
+    return P.n_chunks ? (int64_t)P.n_chunks * n_streams * (int64_t)sizeof(SegRec) + 256 : 0;
+}
+
 int launch_noise(const uint32_t* head, int n_head, int64_t member0, int64_t n_members, int cols,
-                 const Job* jobs, int n_jobs, cudaStream_t st, const uint32_t* head_dev = nullptr) {
+                 const Job* jobs, int n_jobs, cudaStream_t st, const uint32_t* head_dev = nullptr,
+                 void* ws = nullptr, int64_t ws_bytes = 0) {
     NoiseLaunch L;
     int rc = make_noise_launch(head, n_head, head_dev, member0, n_members, cols, jobs, n_jobs, L);
     if (rc || n_members <= 0 || cols <= 0) return rc;
+    int max_rows = 0;
+    for (int j = 0; j < n_jobs; ++j) max_rows = max_rows > jobs[j].rows ? max_rows : jobs[j].rows;
+    const int64_t n_streams = n_members * n_jobs;
+    const SegPlan P = seg_plan(n_streams, (int64_t)max_rows * cols);
+    const char* se = getenv("ENKS_NOISE_SEG");
+    if (ws && P.n_chunks && !(se && se[0] == '0') &&
+        ws_bytes >= seg_ws_bytes(n_streams, (int64_t)max_rows * cols)) {
+        // records + ticket, zeroed in stream order (capture-safe)
+        unsigned* ticket = static_cast<unsigned*>(ws);
+        SegRec* recs = reinterpret_cast<SegRec*>(static_cast<char*>(ws) + 256);
+        cudaMemsetAsync(ws, 0, seg_ws_bytes(n_streams, (int64_t)max_rows * cols), st);
+        const int64_t units = n_streams * P.n_chunks;
+        const int64_t want = (units + kSegWarps - 1) / kSegWarps;
+        const int blocks = (int)(want < 16LL * kNumSMs ? want : 16LL * kNumSMs);
+        noise_seg_kernel<<<blocks, kSegWarps * 32, 0, st>>>(L.args, n_jobs, P.n_chunks, P.G, recs,
+                                                            ticket);
+        return check_launch("enks_noise_fill(segmented)");
+    }
     int64_t blocks = (n_members + kWarps - 1) / kWarps;
     if (L.rb)
         noise_kernel<true><<<dim3((unsigned)blocks, (unsigned)n_jobs), kWarps * 32, 0, st>>>(L.args);
@@ -69,7 +273,8 @@ extern "C" int enks_noise_fill_multi(const uint32_t* head, int n_head, int64_t m
                                      const double* const* diag, float* const* out,
                                      const int64_t* ld_out, const float* const* base,
                                      const int64_t* ld_base, float* const* out_plus,
-                                     const int64_t* ld_plus, void* stream) {
+                                     const int64_t* ld_plus, void* ws, int64_t ws_bytes,
+                                     void* stream) {
     ENKS_REQUIRE(n_jobs >= 1 && n_jobs <= enks::kMaxJobs, "enks_noise_fill_multi: 1..%d jobs",
                  enks::kMaxJobs);
     enks::Job jobs[enks::kMaxJobs];
@@ -77,7 +282,11 @@ extern "C" int enks_noise_fill_multi(const uint32_t* head, int n_head, int64_t m
         jobs[q] = enks::Job{t[q], channel[q], rows[q], diag[q], out[q], ld_out[q],
                             base[q], ld_base[q], out_plus[q], ld_plus[q]};
     return enks::launch_noise(head, n_head, member0, n_members, cols, jobs, n_jobs,
-                              enks::as_stream(stream));
+                              enks::as_stream(stream), nullptr, ws, ws_bytes);
+}
+
+extern "C" int64_t enks_noise_ws_bytes(int64_t n_members, int n_jobs, int max_rows, int cols) {
+    return enks::seg_ws_bytes(n_members * n_jobs, (int64_t)max_rows * cols);
 }
 
 extern "C" int enks_noise_fill_multi_dev(const uint32_t* head_dev, int n_head, int64_t member0,
@@ -87,7 +296,7 @@ extern "C" int enks_noise_fill_multi_dev(const uint32_t* head_dev, int n_head, i
                                          float* const* out, const int64_t* ld_out,
                                          const float* const* base, const int64_t* ld_base,
                                          float* const* out_plus, const int64_t* ld_plus,
-                                         void* stream) {
+                                         void* ws, int64_t ws_bytes, void* stream) {
     ENKS_REQUIRE(head_dev, "enks_noise_fill_multi_dev: null head");
     ENKS_REQUIRE(n_jobs >= 1 && n_jobs <= enks::kMaxJobs, "enks_noise_fill_multi_dev: 1..%d jobs",
                  enks::kMaxJobs);
@@ -96,5 +305,5 @@ extern "C" int enks_noise_fill_multi_dev(const uint32_t* head_dev, int n_head, i
         jobs[q] = enks::Job{t[q], channel[q], rows[q], diag[q], out[q], ld_out[q],
                             base[q], ld_base[q], out_plus[q], ld_plus[q]};
     return enks::launch_noise(nullptr, n_head, member0, n_members, cols, jobs, n_jobs,
-                              enks::as_stream(stream), head_dev);
+                              enks::as_stream(stream), head_dev, ws, ws_bytes);
 }

@@ -131,6 +131,87 @@ __device__ __forceinline__ void load_tables(uint64_t* s_ki, double* s_wi, int ti
     }
 }
 
+// One group of 32 consecutive words w .. w+31 (lane = word): the ziggurat fast test of every
+// word as if it started a normal, numpy's sequential parse resolved on bitmasks.  In: `carry`
+// words at the group start already consumed by an earlier normal.  Out: O (words that emit a
+// normal; lane's value in x), next_carry.  `word(ww)` returns any word of the stream (uniform).
+template <typename WordFn>
+__device__ __forceinline__ void resolve_group(uint64_t raw, int w, int carry, int lane,
+                                              const uint64_t* s_ki, const double* s_wi,
+                                              WordFn&& word, double& x, unsigned& O,
+                                              int& next_carry) {
+    const int idx = (int)(raw & 0xff);
+    const uint64_t r = raw >> 8;
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    x = (double)rabs * s_wi[idx];
+    if (r & 1) x = -x;
+    const bool ok = rabs < s_ki[idx];
+    const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+    unsigned S = carry >= 32 ? 0u : (0xffffffffu << carry);  // words that start a normal
+    next_carry = carry >= 32 ? carry - 32 : 0;
+    O = S;  // words that emit a normal
+    if (bad & S) {
+        // speculative wedge test of every failing word with the following word as uniform
+        uint64_t nxt = __shfl_down_sync(0xffffffffu, raw, 1);
+        if (bad >> 31) {
+            const uint64_t n31 = word(w + 32);
+            if (lane == 31) nxt = n31;
+        }
+        bool acc = false;
+        if (!ok && idx != 0) {
+            const double fa = __longlong_as_double((long long)g_fi[idx - 1]);
+            const double fb = __longlong_as_double((long long)g_fi[idx]);
+            const double uu = u64_to_unit(nxt);
+            // numpy: accept iff (fa - fb) uu + fb < exp(-x^2 / 2) in double.  Decide with a
+            // single-precision exp (ex2.approx, ~2^-22 relative) when the margin is wide,
+            // and fall back to the double exp only near the boundary: same decisions.
+            const double lhs = (fa - fb) * uu + fb;
+            const float ef = exp2f(-0.72134752044448170f * (float)(x * x));  // e^{-x^2/2}
+            if (lhs < (double)ef * (1.0 - 4e-6))
+                acc = true;
+            else if (lhs > (double)ef * (1.0 + 4e-6))
+                acc = false;
+            else
+                acc = lhs < exp(-0.5 * x * x);
+        }
+        unsigned accm = __ballot_sync(0xffffffffu, acc);
+        unsigned todo = bad & S;
+        while (todo) {  // warp-uniform walk over the failing starts, in word order
+            const int b = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int idb = __shfl_sync(0xffffffffu, idx, b);
+            int used;  // words consumed after word b
+            if (idb != 0) {
+                used = 1;
+            } else {  // tail: pairs of uniforms until accepted (numpy's loop, uniform)
+                const uint64_t rb_raw = __shfl_sync(0xffffffffu, raw, b);
+                const uint64_t ra = ((rb_raw >> 8) >> 1) & 0x000fffffffffffffULL;
+                int ww = w + b + 1;
+                double val;
+                for (;;) {
+                    const double xx = -NPY_ZIG_NOR_INV_R * log1p(-u64_to_unit(word(ww)));
+                    const double yy = -log1p(-u64_to_unit(word(ww + 1)));
+                    ww += 2;
+                    if (yy + yy > xx * xx) {
+                        val = ((ra >> 8) & 1) ? -(NPY_ZIG_NOR_R + xx) : NPY_ZIG_NOR_R + xx;
+                        break;
+                    }
+                }
+                used = ww - (w + b + 1);
+                if (lane == b) x = val;
+                accm |= 1u << b;
+            }
+            // the consumed words start no normal
+            const int e = b + 1 + used;  // first word after this normal (group-relative)
+            const unsigned span = (e >= 32 ? 0xffffffffu : ((1u << e) - 1u)) & ~((2u << b) - 1u);
+            S &= ~span;
+            todo &= ~span;
+            if (e > 32) next_carry = e - 32;
+        }
+        O = S & (~bad | accm);
+    }
+}
+
 template <bool RB>
 __device__ __forceinline__ void run_stream(const Args& args, const Job& a, int64_t local, int lane,
                                            float* s_row, uint64_t* buf, const uint64_t* s_ki,
@@ -266,76 +347,10 @@ __device__ __forceinline__ void run_stream(const Args& args, const Job& a, int64
             __syncwarp();
         }
         const uint64_t raw = buf[w - base_w + lane];
-        const int idx = (int)(raw & 0xff);
-        const uint64_t r = raw >> 8;
-        const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-        double x = (double)rabs * s_wi[idx];
-        if (r & 1) x = -x;
-        const bool ok = rabs < s_ki[idx];
-        const unsigned bad = __ballot_sync(0xffffffffu, !ok);
-        unsigned S = carry >= 32 ? 0u : (0xffffffffu << carry);  // words that start a normal
-        int next_carry = carry >= 32 ? carry - 32 : 0;
-        unsigned O = S;  // words that emit a normal
-        if (bad & S) {
-            // speculative wedge test of every failing word with the following word as uniform
-            uint64_t nxt = __shfl_down_sync(0xffffffffu, raw, 1);
-            if (bad >> 31) {
-                const uint64_t n31 = word(w + 32);
-                if (lane == 31) nxt = n31;
-            }
-            bool acc = false;
-            if (!ok && idx != 0) {
-                const double fa = __longlong_as_double((long long)g_fi[idx - 1]);
-                const double fb = __longlong_as_double((long long)g_fi[idx]);
-                const double uu = u64_to_unit(nxt);
-                // numpy: accept iff (fa - fb) uu + fb < exp(-x^2 / 2) in double.  Decide with a
-                // single-precision exp (ex2.approx, ~2^-22 relative) when the margin is wide,
-                // and fall back to the double exp only near the boundary: same decisions.
-                const double lhs = (fa - fb) * uu + fb;
-                const float ef = exp2f(-0.72134752044448170f * (float)(x * x));  // e^{-x^2/2}
-                if (lhs < (double)ef * (1.0 - 4e-6))
-                    acc = true;
-                else if (lhs > (double)ef * (1.0 + 4e-6))
-                    acc = false;
-                else
-                    acc = lhs < exp(-0.5 * x * x);
-            }
-            unsigned accm = __ballot_sync(0xffffffffu, acc);
-            unsigned todo = bad & S;
-            while (todo) {  // warp-uniform walk over the failing starts, in word order
-                const int b = __ffs(todo) - 1;
-                todo &= todo - 1;
-                const int idb = __shfl_sync(0xffffffffu, idx, b);
-                int used;  // words consumed after word b
-                if (idb != 0) {
-                    used = 1;
-                } else {  // tail: pairs of uniforms until accepted (numpy's loop, uniform)
-                    const uint64_t rb_raw = __shfl_sync(0xffffffffu, raw, b);
-                    const uint64_t ra = ((rb_raw >> 8) >> 1) & 0x000fffffffffffffULL;
-                    int ww = w + b + 1;
-                    double val;
-                    for (;;) {
-                        const double xx = -NPY_ZIG_NOR_INV_R * log1p(-u64_to_unit(word(ww)));
-                        const double yy = -log1p(-u64_to_unit(word(ww + 1)));
-                        ww += 2;
-                        if (yy + yy > xx * xx) {
-                            val = ((ra >> 8) & 1) ? -(NPY_ZIG_NOR_R + xx) : NPY_ZIG_NOR_R + xx;
-                            break;
-                        }
-                    }
-                    used = ww - (w + b + 1);
-                    if (lane == b) x = val;
-                    accm |= 1u << b;
-                }
-                // the consumed words start no normal
-                const int e = b + 1 + used;  // first word after this normal (group-relative)
-                const unsigned span = (e >= 32 ? 0xffffffffu : ((1u << e) - 1u)) & ~((2u << b) - 1u);
-                S &= ~span;
-                todo &= ~span;
-                if (e > 32) next_carry = e - 32;
-            }
-            O = S & (~bad | accm);
-        }
+        double x;
+        unsigned O;
+        int next_carry;
+        resolve_group(raw, w, carry, lane, s_ki, s_wi, word, x, O, next_carry);
         carry = next_carry;
         const int n_emit = min(__popc(O), total - q);
         const int pos = __popc(O & lt_mask);

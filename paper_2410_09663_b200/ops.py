@@ -163,6 +163,15 @@ class DeviceOps:
             fn, words, n_head = "enks_noise_fill_multi_dev", _p(head.words), head.n
         else:
             fn, n_head = "enks_noise_fill_multi", len(head)
+        # segmented launch workspace (few substreams: chunks drawn by separate warps)
+        wsb = int(self.lib.enks_noise_ws_bytes(int(n_members), n, max(int(j["rows"]) for j in jobs),
+                                               int(cols)))
+        ws = None
+        if wsb:
+            if getattr(self, "_noise_ws", None) is None or self._noise_ws.numel() < wsb:
+                self._retire(getattr(self, "_noise_ws", None))
+                self._noise_ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
+            ws = self._noise_ws
         _lib.call(fn, words, n_head, int(member0), int(n_members), int(cols),
                   n, u32(*[int(j["t"]) for j in jobs]), u32(*[int(j["ch"]) for j in jobs]),
                   (ctypes.c_int * n)(*[int(j["rows"]) for j in jobs]),
@@ -172,7 +181,7 @@ class DeviceOps:
                   i64(*[_ld(v) if v is not None else 0 for v in get("base")]),
                   vp(*[_p(v) for v in get("out_plus")]),
                   i64(*[_ld(v) if v is not None else 0 for v in get("out_plus")]),
-                  self._stream())
+                  _p(ws), int(wsb), self._stream())
 
     def member_sum(self, src, n_members, cols, z0, acc, amax=None, src2=None):
         """Member sums of src (+ src2, formed on the fly) relative to z0 (or member 0)."""

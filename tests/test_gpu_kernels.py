@@ -616,3 +616,40 @@ def test_cnn_forward_noise_matches_separate_launches(dev_ops, pm, cols, N):
         outs[fused] = o
     for k in outs[False]:
         assert torch.equal(outs[False][k], outs[True][k]), k
+
+
+@pytest.mark.parametrize("N,rows,cols,m0", [(3, 128, 128, 0), (20, 64, 64, 7), (64, 40, 32, 1000)])
+def test_noise_segmented_bit_exact(dev_ops, N, rows, cols, m0):
+    """Few substreams -> the segmented launch (chunks drawn by separate warps, chained in order):
+    bit-identical to numpy's draws (C oracle) and to the one-warp-per-substream launch."""
+    import os
+
+    from oracle import noise as onoise
+    from paper_2410_09663_b200.matvar import entropy_head
+
+    assert dev_ops.lib.enks_noise_ws_bytes(N, 3, rows, cols) > 0  # takes the segmented path
+    head = entropy_head(11, (2, 5))
+    diag = dev_ops.to_device(np.linspace(0.5, 2.0, rows), dtype=torch.float64)
+    base = torch.randn(rows, N * cols, device=dev_ops.device)
+
+    def draw():
+        outs = [dev_ops.zeros(rows, N * cols) for _ in range(3)]
+        plus = dev_ops.zeros(rows, N * cols)
+        dev_ops.noise_fill_multi(head, m0, N, cols, [
+            dict(t=4, ch=0, rows=rows, diag=diag, out=outs[0], base=base, out_plus=plus),
+            dict(t=4, ch=1, rows=rows, out=outs[1]), dict(t=4, ch=2, rows=rows, out=outs[2])])
+        torch.cuda.synchronize()
+        return outs, plus
+
+    seg, seg_plus = draw()
+    os.environ["ENKS_NOISE_SEG"] = "0"
+    try:
+        ref, ref_plus = draw()
+    finally:
+        del os.environ["ENKS_NOISE_SEG"]
+    for a, b in zip(seg, ref):
+        assert torch.equal(a, b)
+    assert torch.equal(seg_plus, ref_plus)
+    z = onoise.member_normals(11, (2, 5), 4, 1, m0 + N, (rows, cols), backend="c")[m0:]
+    want = np.ascontiguousarray(z.transpose(1, 0, 2).reshape(rows, -1)).astype(np.float32)
+    assert np.array_equal(seg[1].cpu().numpy(), want)
