@@ -65,28 +65,31 @@ __device__ void panel_solve(float* X, const float* L, int lane) {
     float x[kTS];
 #pragma unroll
     for (int j = 0; j < kTS; ++j) x[j] = X[lane * kLd + j];
+    // right-looking: finish x[k], then update every later x[j] (independent FMAs, ILP)
 #pragma unroll
-    for (int j = 0; j < kTS; ++j) {
-        float v = x[j];
+    for (int k = 0; k < kTS; ++k) {
+        x[k] = x[k] / L[k * kLd + k];
 #pragma unroll
-        for (int k = 0; k < j; ++k) v = fmaf(-x[k], L[j * kLd + k], v);
-        x[j] = v / L[j * kLd + j];
+        for (int j = k + 1; j < kTS; ++j) x[j] = fmaf(-x[k], L[j * kLd + k], x[j]);
     }
 #pragma unroll
     for (int j = 0; j < kTS; ++j) X[lane * kLd + j] = x[j];
 }
 
-// C <- C - A B^T (32x32x32), lane = column of C
+// C <- C - A B^T (32x32x32), lane = column of C; k outer so the 32 row sums are independent
+// FMA chains (ILP 32) instead of one 32-long dependent chain per row
 __device__ void tile_syrk_sub(float* C, const float* A, const float* B, int lane) {
-    float b[kTS];
+    float acc[kTS];
 #pragma unroll
-    for (int k = 0; k < kTS; ++k) b[k] = B[lane * kLd + k];
-    for (int r = 0; r < kTS; ++r) {
-        float acc = 0.f;
+    for (int r = 0; r < kTS; ++r) acc[r] = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < kTS; ++k) {
+        const float bk = B[lane * kLd + k];
 #pragma unroll
-        for (int k = 0; k < kTS; ++k) acc = fmaf(A[r * kLd + k], b[k], acc);
-        C[r * kLd + lane] -= acc;
+        for (int r = 0; r < kTS; ++r) acc[r] = fmaf(A[r * kLd + k], bk, acc[r]);
     }
+#pragma unroll
+    for (int r = 0; r < kTS; ++r) C[r * kLd + lane] -= acc[r];
 }
 
 // in-place inverse of a lower-triangular 32x32 tile (warp; lane = column of the inverse)
@@ -222,15 +225,12 @@ __global__ void __launch_bounds__(kThreads)
             for (int K = J; K < I; ++K) {
                 const float* A = Lt + tix(I, K) * kTile;  // L_IK
                 const float* B = Lt + tix(K, J) * kTile;  // Linv_KJ (K == J: Linv_JJ)
-                float b[kTS];  // column `lane` of B
+                // k outer: the 32 row sums are independent chains (ILP)
+#pragma unroll 4
+                for (int k = 0; k < kTS; ++k) {
+                    const float bk = B[k * kLd + lane];  // column `lane` of B
 #pragma unroll
-                for (int k = 0; k < kTS; ++k) b[k] = B[k * kLd + lane];
-#pragma unroll
-                for (int r = 0; r < kTS; ++r) {
-                    float acc = 0.f;
-#pragma unroll
-                    for (int k = 0; k < kTS; ++k) acc = fmaf(A[r * kLd + k], b[k], acc);
-                    res[r] += acc;
+                    for (int r = 0; r < kTS; ++r) res[r] = fmaf(A[r * kLd + k], bk, res[r]);
                 }
             }
         }
@@ -239,13 +239,15 @@ __global__ void __launch_bounds__(kThreads)
             const int J = warp;
             float* out = Lt + tix(I, J) * kTile;
             const float* D = Lt + tix(I, I) * kTile;  // Linv_II
+            float o[kTS];
 #pragma unroll
-            for (int r = 0; r < kTS; ++r) {
-                float acc = 0.f;
+            for (int r = 0; r < kTS; ++r) o[r] = 0.f;
 #pragma unroll
-                for (int k = 0; k <= r; ++k) acc = fmaf(D[r * kLd + k], res[k], acc);
-                out[r * kLd + lane] = -acc;
-            }
+            for (int k = 0; k < kTS; ++k)
+#pragma unroll
+                for (int r = k; r < kTS; ++r) o[r] = fmaf(D[r * kLd + k], res[k], o[r]);
+#pragma unroll
+            for (int r = 0; r < kTS; ++r) out[r * kLd + lane] = -o[r];
         }
         __syncthreads();
     }
