@@ -371,7 +371,7 @@ def run_ours(args):
     kinds = {"cross": ("tensor", "TFLOP/s"), "forecast": ("tensor", "TFLOP/s"),
              "correction": ("tensor", "TFLOP/s"), "gain": ("tensor", "TFLOP/s"),
              "mean": ("tensor", "TFLOP/s"),
-             "shift": ("tensor", "TFLOP/s"), "noise": ("hbm", "GB/s"), "stats": ("hbm", "GB/s"),
+             "shift": ("tensor", "TFLOP/s"), "noise": ("issue", "Gnormal/s"), "stats": ("hbm", "GB/s"),
              "gain_solve": ("latency", "TFLOP/s")}
     kernels = {}
     for tag, (t, w, cnt) in sorted(fam.items(), key=lambda kv: -kv[1][0]):

@@ -129,8 +129,7 @@ class DeviceOps:
             return
         words = (ctypes.c_uint32 * len(head))(*[int(w) for w in head])
         self.launches += 1
-        nb = 4 * rows * cols * n_members * ((out is not None) + 2 * (out_plus is not None))
-        with self._prof("noise", nb):
+        with self._prof("noise", rows * cols * n_members):  # work = normals drawn
             self._noise_fill(words, head, t, ch, member0, n_members, rows, cols, diag, out, base,
                              out_plus)
 
@@ -152,10 +151,7 @@ class DeviceOps:
         i64 = ctypes.c_int64 * n
         get = lambda k: [j.get(k) for j in jobs]  # noqa: E731
         self.launches += 1
-        nb = sum(4 * j["rows"] * cols * n_members * ((j.get("out") is not None)
-                                                      + 2 * (j.get("out_plus") is not None))
-                 for j in jobs)
-        with self._prof("noise", nb):
+        with self._prof("noise", sum(j["rows"] * cols * n_members for j in jobs)):  # normals
             self._noise_multi(words, head, member0, n_members, cols, n, u32, vp, i64, get, jobs)
 
     def _noise_multi(self, words, head, member0, n_members, cols, n, u32, vp, i64, get, jobs):
