@@ -12,8 +12,9 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:f16p
 python tools/timeline.py --steps 1,25,50 > gpurun_out/timeline.txt 2>&1
 out=gpurun_out/sweep.jsonl; : > $out
 for N in 64 256 1024 4096 16384; do
-  timeout 600 python bench.py --config C5 --members $N --steps 3 --warmup 3 --no-cpu-baseline --graph 2>>gpurun_out/sweep_err.log | tail -1 >> $out
+  timeout 600 python bench.py --config C5 --members $N --steps 3 --warmup 3 --no-cpu-baseline 2>>gpurun_out/sweep_err.log | tail -1 >> $out
 done
 for C in C1 C2; do
-  timeout 600 python bench.py --config $C --steps 5 --warmup 3 --no-cpu-baseline --graph 2>>gpurun_out/sweep_err.log | tail -1 >> $out
+  timeout 600 python bench.py --config $C --steps 5 --warmup 3 --no-cpu-baseline 2>>gpurun_out/sweep_err.log | tail -1 >> $out
 done
+timeout 900 python bench.py --config C4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_c4.log 2>&1
