@@ -254,7 +254,12 @@ def run_ours(args):
 
     # --graph (1 GPU): the horizon is one CUDA graph (all kernels of the eager path, replayed)
     graph = None
-    if args.graph and world == 1:
+    # a captured horizon keeps its own engine; the extra profiled horizon and the e2e path need
+    # room for another one, so very large problems (C4) run eager
+    n, l, m = pr.n, pr.l, pr.m
+    est = 4.4 * ((h + 1) * (n + l) + h * (n + l)) * pr.N * m  # fp16-pair basis + gains, bytes
+    fits = est < 0.3 * torch.cuda.get_device_properties(local).total_memory
+    if args.graph and world == 1 and fits:
         graph = enks.HorizonGraph(pr.x0, pr.vs, h, pr.N, streams)
         graph.y_refs.copy_(yref_dev)
 
@@ -286,6 +291,7 @@ def run_ours(args):
     launches = (ops.launches - launches0) // max(args.steps, 1)
     # one extra eager horizon, outside the timed region, for the per-kernel breakdown (CUDA-event
     # brackets on the launching streams)
+    torch.cuda.empty_cache()
     l0 = ops.launches
     ops.profile = []
     enks.smooth_horizon_device(pr.x0, yref_dev, pr.vs, h, pr.N, streams, comm=comm)
