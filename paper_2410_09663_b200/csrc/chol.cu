@@ -76,20 +76,21 @@ __device__ void panel_solve(float* X, const float* L, int lane) {
     for (int j = 0; j < kTS; ++j) X[lane * kLd + j] = x[j];
 }
 
-// C <- C - A B^T (32x32x32), lane = column of C; k outer so the 32 row sums are independent
-// FMA chains (ILP 32) instead of one 32-long dependent chain per row
-__device__ void tile_syrk_sub(float* C, const float* A, const float* B, int lane) {
-    float acc[kTS];
+// rows [r0, r0 + 8) of C <- C - A B^T (lane = column of C): a quarter-tile task, so the trailing
+// update of a block column spreads over 4x more warps
+__device__ __forceinline__ void quarter_syrk_sub(float* C, const float* A, const float* B,
+                                                 int lane, int r0) {
+    float acc[8];
 #pragma unroll
-    for (int r = 0; r < kTS; ++r) acc[r] = 0.f;
-#pragma unroll 4
+    for (int r = 0; r < 8; ++r) acc[r] = 0.f;
+#pragma unroll 8
     for (int k = 0; k < kTS; ++k) {
         const float bk = B[lane * kLd + k];
 #pragma unroll
-        for (int r = 0; r < kTS; ++r) acc[r] = fmaf(A[r * kLd + k], bk, acc[r]);
+        for (int r = 0; r < 8; ++r) acc[r] = fmaf(A[(r0 + r) * kLd + k], bk, acc[r]);
     }
 #pragma unroll
-    for (int r = 0; r < kTS; ++r) C[r * kLd + lane] -= acc[r];
+    for (int r = 0; r < 8; ++r) C[(r0 + r) * kLd + lane] -= acc[r];
 }
 
 // in-place inverse of a lower-triangular 32x32 tile (warp; lane = column of the inverse)
@@ -97,11 +98,13 @@ __device__ void invert_diag(float* T, int lane) {
     // column `lane` of L^{-1}: forward substitution L y = e_lane
     float y[kTS];
 #pragma unroll
-    for (int i = 0; i < kTS; ++i) {
-        float v = (i == lane) ? 1.f : 0.f;
+    for (int i = 0; i < kTS; ++i) y[i] = (i == lane) ? 1.f : 0.f;
+    // right-looking: finish y[k], then update every later y[i] (independent FMAs)
 #pragma unroll
-        for (int k = 0; k < i; ++k) v = fmaf(-T[i * kLd + k], y[k], v);
-        y[i] = (i < lane) ? 0.f : v / T[i * kLd + i];
+    for (int k = 0; k < kTS; ++k) {
+        y[k] = (k < lane) ? 0.f : y[k] / T[k * kLd + k];
+#pragma unroll
+        for (int i = k + 1; i < kTS; ++i) y[i] = fmaf(-T[i * kLd + k], y[k], y[i]);
     }
     __syncwarp();
 #pragma unroll
@@ -181,15 +184,16 @@ __global__ void __launch_bounds__(kThreads)
             for (int I = K + 1 + warp; I < nb; I += kWarps)
                 panel_solve(Lt + tix(I, K) * kTile, Lt + tix(K, K) * kTile, lane);
             __syncthreads();
-            // trailing update of tiles (I, J), K < J <= I
+            // trailing update of tiles (I, J), K < J <= I, in quarter-tile tasks
             const int m = nb - K - 1;
-            for (int q = warp; q < m * (m + 1) / 2; q += kWarps) {
+            for (int t = warp; t < 2 * m * (m + 1); t += kWarps) {
+                const int q = t >> 2, rq = t & 3;
                 int I = 0;
                 while ((I + 1) * (I + 2) / 2 <= q) ++I;
                 const int J = q - I * (I + 1) / 2;
                 const int gI = K + 1 + I, gJ = K + 1 + J;
-                tile_syrk_sub(Lt + tix(gI, gJ) * kTile, Lt + tix(gI, K) * kTile,
-                              Lt + tix(gJ, K) * kTile, lane);
+                quarter_syrk_sub(Lt + tix(gI, gJ) * kTile, Lt + tix(gI, K) * kTile,
+                                 Lt + tix(gJ, K) * kTile, lane, 8 * rq);
             }
             __syncthreads();
         }
@@ -208,46 +212,52 @@ __global__ void __launch_bounds__(kThreads)
 
     // L^{-1}, tile row by tile row: Linv_II = L_II^{-1};
     // Linv_IJ = -Linv_II * sum_{K=J}^{I-1} L_IK Linv_KJ   (J < I), written over L_IJ.
-    // Row I needs Linv tiles of rows < I (already inverted) and L_IK (K < I, still L).
-    for (int I = 0; I < ((debug & 1) ? 0 : nb); ++I) {
-        if (warp == 0) invert_diag(Lt + tix(I, I) * kTile, lane);
+    // The diagonal inverses are independent: all at once first (one warp each).  Then per tile
+    // row I: phase A forms res_J = sum_K L_IK Linv_KJ in quarter-tile tasks into a staging area
+    // (tiles (I, K) are still L there and are read by other tasks), phase B overwrites
+    // (I, J) with -Linv_II res_J, again in quarter tasks.
+    float* res = Lt + (nb * (nb + 1) / 2) * kTile;  // staging: up to nb - 1 tiles
+    if (!(debug & 1)) {
+        for (int I = warp; I < nb; I += kWarps) invert_diag(Lt + tix(I, I) * kTile, lane);
         __syncthreads();
-        // for each J < I (one warp per J): acc = sum_K L_IK Linv_KJ, then Linv_IJ = -Linv_II acc.
-        // L_IK for K >= J are read before any warp overwrites them?  Warp J writes tile (I, J)
-        // only, and reads (I, K) for K >= J: tiles (I, K > J) are written by other warps, so
-        // stage the products in registers and write after a barrier.
-        float res[kTS];
-        const bool active = warp < I;
-        if (active) {
-            const int J = warp;
+    }
+    for (int I = 1; I < ((debug & 1) ? 0 : nb); ++I) {
+        for (int t = warp; t < 4 * I; t += kWarps) {  // phase A: task (J, row quarter)
+            const int J = t >> 2, r0 = 8 * (t & 3);
+            float acc[8];
 #pragma unroll
-            for (int r = 0; r < kTS; ++r) res[r] = 0.f;
+            for (int r = 0; r < 8; ++r) acc[r] = 0.f;
             for (int K = J; K < I; ++K) {
                 const float* A = Lt + tix(I, K) * kTile;  // L_IK
                 const float* B = Lt + tix(K, J) * kTile;  // Linv_KJ (K == J: Linv_JJ)
-                // k outer: the 32 row sums are independent chains (ILP)
-#pragma unroll 4
+#pragma unroll 8
                 for (int k = 0; k < kTS; ++k) {
                     const float bk = B[k * kLd + lane];  // column `lane` of B
 #pragma unroll
-                    for (int r = 0; r < kTS; ++r) res[r] = fmaf(A[r * kLd + k], bk, res[r]);
+                    for (int r = 0; r < 8; ++r) acc[r] = fmaf(A[(r0 + r) * kLd + k], bk, acc[r]);
                 }
             }
+            float* R = res + J * kTile;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) R[(r0 + r) * kLd + lane] = acc[r];
         }
         __syncthreads();
-        if (active) {
-            const int J = warp;
+        const float* D = Lt + tix(I, I) * kTile;  // Linv_II
+        for (int t = warp; t < 4 * I; t += kWarps) {  // phase B: out rows r0 .. r0 + 7
+            const int J = t >> 2, r0 = 8 * (t & 3);
+            const float* R = res + J * kTile;
+            float o[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) o[r] = 0.f;
+            for (int k = 0; k < r0 + 8; ++k) {  // D lower triangular: k <= r
+                const float rk = R[k * kLd + lane];
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (k <= r0 + r) o[r] = fmaf(D[(r0 + r) * kLd + k], rk, o[r]);
+            }
             float* out = Lt + tix(I, J) * kTile;
-            const float* D = Lt + tix(I, I) * kTile;  // Linv_II
-            float o[kTS];
 #pragma unroll
-            for (int r = 0; r < kTS; ++r) o[r] = 0.f;
-#pragma unroll
-            for (int k = 0; k < kTS; ++k)
-#pragma unroll
-                for (int r = k; r < kTS; ++r) o[r] = fmaf(D[r * kLd + k], res[k], o[r]);
-#pragma unroll
-            for (int r = 0; r < kTS; ++r) out[r * kLd + lane] = -o[r];
+            for (int r = 0; r < 8; ++r) out[(r0 + r) * kLd + lane] = -o[r];
         }
         __syncthreads();
     }
@@ -428,7 +438,8 @@ int copy_block(const float* src, int64_t lds, int R, int C, float alpha, int tra
 
 size_t spd_smem(int p) {
     const int nb = (p + kTS - 1) / kTS;
-    return (size_t)nb * (nb + 1) / 2 * kTile * sizeof(float);
+    // lower tile-triangle + the inverse's staging tiles
+    return ((size_t)nb * (nb + 1) / 2 + (nb > 1 ? nb - 1 : 0)) * kTile * sizeof(float);
 }
 
 int configure_spd(size_t smem) {
