@@ -56,6 +56,15 @@ constexpr int kW3Stride = 12;
 constexpr int kXD = 2 * 4 * 32;                     // [parity][warp][32]
 constexpr int kXV = 2 * 4 * 4;                      // [parity][warp][3 (+pad)]
 
+// layer-2 bias and layer-3 weights in constant memory: the epilogue reads them as uniform-register
+// operands (LDCU) instead of shared-memory loads (the kernel's shared-memory pipe is its limit)
+struct Cnn3Epi {
+    float b2[C2];
+    float w3[C2][kW3Stride];  // [c][ky*3 + kx], padded to 12
+    float b3;
+};
+__constant__ Cnn3Epi c_epi;
+
 // Shared-memory / TMEM layout.  SH = false: the three horizontal taps are stacked in N
 // (N = 96, one accumulator per OUTPUT row, horizontal taps folded in the epilogue with warp
 // shuffles).  SH = true (128-pixel images): the three VERTICAL taps are stacked in N and the
@@ -410,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         const int ew = warp - 12;  // == warp & 3 -> TMEM lane quarter
         const int x = ew * 32 + lane;
         const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-        const float b3 = b3s[0];
+        const float b3 = c_epi.b3;
         // cross-warp tap exchange only inside an image (seg = 32: never; 64: not across 63|64)
         const bool xl = ew > 0 && ((ew * 32) & (a.seg - 1)) != 0;
         const bool xr = ew < 3 && (((ew + 1) * 32) & (a.seg - 1)) != 0;
@@ -431,15 +440,15 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
 #pragma unroll
             for (int c = 0; c < ((a.debug & 4) ? 0 : 32); ++c) {
                 const int g = c & 3;
-                const float h = tanh_fast(s[c] + b2s[c]);
+                const float h = tanh_fast(s[c] + c_epi.b2[c]);
                 const float2 hh = make_float2(h, h);
-                const float4 w0 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride);
-                const float4 w1 = *reinterpret_cast<const float4*>(w3s + c * kW3Stride + 4);
+                const float4 w0 = *reinterpret_cast<const float4*>(&c_epi.w3[c][0]);
+                const float4 w1 = *reinterpret_cast<const float4*>(&c_epi.w3[c][4]);
                 v01[g] = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01[g]);
                 v23[g] = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23[g]);
                 v45[g] = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45[g]);
                 v67[g] = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67[g]);
-                v8[g] = fmaf(w3s[c * kW3Stride + 8], h, v8[g]);
+                v8[g] = fmaf(c_epi.w3[c][8], h, v8[g]);
             }
 #pragma unroll
             for (int g = 1; g < 4; ++g) {
@@ -634,6 +643,25 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     if (warp == 2) ptx::tmem_dealloc(tmem, L::kTmemAlloc);
 }
 
+__global__ void cnn3_epi_pack_kernel(const float* __restrict__ b2, const float* __restrict__ w3,
+                                     const float* __restrict__ b3, Cnn3Epi* __restrict__ out) {
+    for (int e = threadIdx.x; e < C2 * kW3Stride; e += blockDim.x) {
+        const int c = e / kW3Stride, k = e - c * kW3Stride;
+        out->w3[c][k] = k < 9 ? w3[c * 9 + k] : 0.f;
+    }
+    for (int e = threadIdx.x; e < C2; e += blockDim.x) out->b2[e] = b2[e];
+    if (threadIdx.x == 0) out->b3 = b3[0];
+}
+
+Cnn3Epi* epi_scratch() {  // per device (one process drives one GPU, but stay per-device)
+    static Cnn3Epi* buf[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!buf[dev] && cudaMalloc(&buf[dev], sizeof(Cnn3Epi)) != cudaSuccess) buf[dev] = nullptr;
+    return buf[dev];
+}
+
 }  // namespace
 
 bool cnn3_tc_applicable(int n_layers, const int* widths, int rows, int cols) {
@@ -670,6 +698,21 @@ int cnn3_tc_forward_nz(const float* weights, const float* biases, float alpha, c
         a.products = (pe && atoi(pe) == 2) ? 2 : 3;
     }
     const int grid = (int)(n_members < kNumSMs ? n_members : kNumSMs);
+    {   // stream-ordered refresh of the epilogue's constant bank
+        Cnn3Epi* scr = epi_scratch();
+        if (!scr) {
+            set_error("cnn3_tc: constant scratch allocation failed");
+            return ENKS_E_CUDA;
+        }
+        cnn3_epi_pack_kernel<<<1, 256, 0, st>>>(a.b2, a.w3, a.b3, scr);
+        int rc = check_launch("enks_cnn_forward(epi pack)");
+        if (rc) return rc;
+        if (cudaMemcpyToSymbolAsync(c_epi, scr, sizeof(Cnn3Epi), 0, cudaMemcpyDeviceToDevice, st) !=
+            cudaSuccess) {
+            set_error("cnn3_tc: constant upload failed");
+            return ENKS_E_CUDA;
+        }
+    }
     if (cols == W) return launch_cnn3<true>(a, grid, st);
     return launch_cnn3<false>(a, grid, st);
 }
