@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     uint64_t* acc_full = bars + 2 * NA;  // [NACC]
     uint64_t* acc_empty = bars + 2 * NA + NACC;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NA + 2 * NACC);
+    uint64_t* xb_full = bars + 2 * NA + 2 * NACC + 1;  // [4] SH: row's boundary taps written
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = a.rows;
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
             ptx::mbar_init(&acc_full[q], 1);
             ptx::mbar_init(&acc_empty[q], 4);
         }
+        for (int q = 0; q < 4; ++q) ptx::mbar_init(&xb_full[q], 128);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc(tmem_slot, L::kTmemAlloc);
@@ -519,6 +521,79 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&acc_empty[(it * n + j) % NACC]);
                 };
+                // SH: the cross-warp boundary taps of row y are exchanged through 4 smem buffers
+                // with an mbarrier each, and consumed one row later (phase B), so the four
+                // epilogue warps never wait for each other within a row.  4 buffers: a warp
+                // writing row Yg has passed phase B of row Yg - 2, so every warp has finished
+                // phase A of Yg - 2 and hence phase B of Yg - 4 (the buffer's previous row)
+                float* xvA = xd0;        // [4][4 warps][4]: v[ky][0] of lane 31
+                float* xvB = xd0 + 64;   // [4][4 warps][4]: v[ky][2] of lane 0
+                auto taps = [&](const float (&sv)[32], float (&vv)[9]) {
+                    float2 v01[4], v23[4], v45[4], v67[4];
+                    float v8[4];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        v01[g] = v23[g] = v45[g] = v67[g] = make_float2(0.f, 0.f);
+                        v8[g] = 0.f;
+                    }
+#pragma unroll
+                    for (int c = 0; c < ((a.debug & 4) ? 0 : 32); ++c) {
+                        const int g = c & 3;
+                        const float h = tanh_fast(sv[c] + c_epi.b2[c]);
+                        const float2 hh = make_float2(h, h);
+                        const float4 w0 = *reinterpret_cast<const float4*>(&c_epi.w3[c][0]);
+                        const float4 w1 = *reinterpret_cast<const float4*>(&c_epi.w3[c][4]);
+                        v01[g] = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01[g]);
+                        v23[g] = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23[g]);
+                        v45[g] = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45[g]);
+                        v67[g] = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67[g]);
+                        v8[g] = fmaf(c_epi.w3[c][8], h, v8[g]);
+                    }
+#pragma unroll
+                    for (int g = 1; g < 4; ++g) {
+                        v01[0].x += v01[g].x; v01[0].y += v01[g].y;
+                        v23[0].x += v23[g].x; v23[0].y += v23[g].y;
+                        v45[0].x += v45[g].x; v45[0].y += v45[g].y;
+                        v67[0].x += v67[g].x; v67[0].y += v67[g].y;
+                        v8[0] += v8[g];
+                    }
+                    vv[0] = v01[0].x; vv[1] = v01[0].y; vv[2] = v23[0].x; vv[3] = v23[0].y;
+                    vv[4] = v45[0].x; vv[5] = v45[0].y; vv[6] = v67[0].x; vv[7] = v67[0].y;
+                    vv[8] = v8[0];
+                };
+                struct Pend {
+                    float t0, t1, t2;
+                    int y, Yg;
+                    float xr_m, xres0;
+                };
+                Pend pend{0.f, 0.f, 0.f, 0, 0, 0.f, 0.f};
+                auto finish = [&](const Pend& P) {
+                    const int b = P.Yg % 4;
+                    ptx::mbar_wait(&xb_full[b], (uint32_t)((P.Yg / 4) & 1));
+                    float tk[3] = {P.t0, P.t1, P.t2};
+                    if (lane == 0 && xl) {
+#pragma unroll
+                        for (int ky = 0; ky < 3; ++ky) tk[ky] += xvA[(b * 4 + ew - 1) * 4 + ky];
+                    }
+                    if (lane == 31 && xr) {
+#pragma unroll
+                        for (int ky = 0; ky < 3; ++ky) tk[ky] += xvB[(b * 4 + ew + 1) * 4 + ky];
+                    }
+                    const int y = P.y;
+                    acc3[(y + 1) % 3] += tk[0];
+                    acc3[y % 3] += tk[1];
+                    if (y >= 1) {
+                        const int yo = y - 1;
+                        const float o = acc3[yo % 3] + tk[2];
+                        acc3[yo % 3] = 0.f;
+                        if (col_ok) om[(int64_t)yo * a.ldo + x] = P.xr_m + a.alpha * (b3 + o);
+                    }
+                    if (y == n - 1) {
+                        const float o = acc3[y % 3];
+                        acc3[y % 3] = 0.f;
+                        if (col_ok) om[(int64_t)y * a.ldo + x] = P.xres0 + a.alpha * (b3 + o);
+                    }
+                };
                 float xpre = 0.f;
                 wait_acc(0);
                 for (int y = 0; y < n; ++y) {
@@ -545,8 +620,26 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     if (y == n - 1) release(y);
                     const float xr_m = xpre;  // X[y - 1]
                     xpre = col_ok ? xm[(int64_t)y * a.ldx + x] : 0.f;  // X[y]: next row's X[y' - 1]
-                    layer3(y, s, (nproc++) & 1, acc3, xr_m, y == n - 1 ? xpre : 0.f, om, col_ok);
+                    // phase A: layer-3 taps, fold inside the warp, publish the boundary taps
+                    const int Yg = it * n + y, b = Yg % 4;
+                    float vv[9];
+                    taps(s, vv);
+                    float tk[3];
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky) {
+                        const float up = __shfl_up_sync(0xffffffffu, vv[ky * 3 + 0], 1);
+                        const float dn = __shfl_down_sync(0xffffffffu, vv[ky * 3 + 2], 1);
+                        tk[ky] = vv[ky * 3 + 1] + (lane == 0 ? 0.f : up) + (lane == 31 ? 0.f : dn);
+                        if (lane == 31) xvA[(b * 4 + ew) * 4 + ky] = vv[ky * 3 + 0];
+                        if (lane == 0) xvB[(b * 4 + ew) * 4 + ky] = vv[ky * 3 + 2];
+                    }
+                    __syncwarp();
+                    ptx::mbar_arrive(&xb_full[b]);
+                    // phase B of the previous row (its neighbours' taps are out by now)
+                    if (y >= 1) finish(pend);
+                    pend = Pend{tk[0], tk[1], tk[2], y, Yg, xr_m, y == n - 1 ? xpre : 0.f};
                 }
+                finish(pend);
             } else {
                 float xpre = 0.f;
                 for (int y = 0; y < n; ++y) {
