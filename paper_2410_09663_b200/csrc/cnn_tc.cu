@@ -136,6 +136,15 @@ __device__ __forceinline__ float tanh_fast_t(float x) {
 }
 #define tanh_fast tanh_fast_t<false>
 
+// two tanh at once: the non-SFU steps as packed f32x2 instructions (FADD2 / FMUL2 / FFMA2)
+__device__ __forceinline__ float2 tanh2_fast(float2 x) {
+    const float2 e = __fmul2_rn(x, make_float2(2.8853900817779268f, 2.8853900817779268f));
+    const float2 d = __fadd2_rn(make_float2(exp2f_approx(e.x), exp2f_approx(e.y)),
+                                make_float2(1.f, 1.f));
+    return __ffma2_rn(make_float2(-2.f, -2.f), make_float2(rcp_approx(d.x), rcp_approx(d.y)),
+                      make_float2(1.f, 1.f));
+}
+
 struct Cnn3Args {
     const float* w1;  // (C1, 2, 3, 3)
     const float* b1;
@@ -537,17 +546,22 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                         v8[g] = 0.f;
                     }
 #pragma unroll
-                    for (int c = 0; c < ((a.debug & 4) ? 0 : 32); ++c) {
-                        const int g = c & 3;
-                        const float h = tanh_fast(sv[c] + c_epi.b2[c]);
-                        const float2 hh = make_float2(h, h);
-                        const float4 w0 = *reinterpret_cast<const float4*>(&c_epi.w3[c][0]);
-                        const float4 w1 = *reinterpret_cast<const float4*>(&c_epi.w3[c][4]);
-                        v01[g] = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01[g]);
-                        v23[g] = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23[g]);
-                        v45[g] = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45[g]);
-                        v67[g] = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67[g]);
-                        v8[g] = fmaf(c_epi.w3[c][8], h, v8[g]);
+                    for (int c = 0; c < ((a.debug & 4) ? 0 : 32); c += 2) {
+                        const float2 h2 = tanh2_fast(__fadd2_rn(make_float2(sv[c], sv[c + 1]),
+                                                                make_float2(c_epi.b2[c], c_epi.b2[c + 1])));
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int cc = c + u, g = cc & 3;
+                            const float h = u ? h2.y : h2.x;
+                            const float2 hh = make_float2(h, h);
+                            const float4 w0 = *reinterpret_cast<const float4*>(&c_epi.w3[cc][0]);
+                            const float4 w1 = *reinterpret_cast<const float4*>(&c_epi.w3[cc][4]);
+                            v01[g] = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01[g]);
+                            v23[g] = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23[g]);
+                            v45[g] = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45[g]);
+                            v67[g] = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67[g]);
+                            v8[g] = fmaf(c_epi.w3[cc][8], h, v8[g]);
+                        }
                     }
 #pragma unroll
                     for (int g = 1; g < 4; ++g) {
@@ -604,17 +618,25 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     ptx::tmem_ld_wait();
 #pragma unroll
                     for (int c = 0; c < 32; ++c) s[c] = __uint_as_float(v[c]);
+                    auto add_into = [&]() {  // s += v, as packed f32x2 adds
+#pragma unroll
+                        for (int c = 0; c < 32; c += 2) {
+                            const float2 t = __fadd2_rn(make_float2(s[c], s[c + 1]),
+                                                        make_float2(__uint_as_float(v[c]),
+                                                                    __uint_as_float(v[c + 1])));
+                            s[c] = t.x;
+                            s[c + 1] = t.y;
+                        }
+                    };
                     if (y >= 1) {
                         ptx::tmem_ld_32x32b_x32(acc_base(y - 1), v);  // D_{y-1}[dy = 0]
                         ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int c = 0; c < 32; ++c) s[c] += __uint_as_float(v[c]);
+                        add_into();
                     }
                     if (y + 1 < n) {
                         ptx::tmem_ld_32x32b_x32(acc_base(y + 1) + 2 * C2, v);  // D_{y+1}[dy = 2]
                         ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int c = 0; c < 32; ++c) s[c] += __uint_as_float(v[c]);
+                        add_into();
                     }
                     if (y >= 1) release(y - 1);
                     if (y == n - 1) release(y);
