@@ -408,8 +408,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                             acc = __ffma2_rn(make_float2(wv.z, wv.w),
                                              make_float2(in[2 * q + 1], in[2 * q + 1]), acc);
                         }
-                        hv[2 * pr] = tanh_fast(acc.x);
-                        hv[2 * pr + 1] = tanh_fast(acc.y);
+                        const float2 t2 = tanh2_fast(acc);  // packed non-SFU steps
+                        hv[2 * pr] = t2.x;
+                        hv[2 * pr + 1] = t2.y;
                     }
                     float4 h4, l4;
                     h4.x = ptx::tf32_round(hv[0]); l4.x = hv[0] - h4.x;
