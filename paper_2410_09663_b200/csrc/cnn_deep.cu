@@ -350,6 +350,92 @@ __global__ void __launch_bounds__(128) deep_last_kernel(const __half* __restrict
     out[r * ldo + col] = x[r * ldx + col] + alpha * acc;
 }
 
+// Row-streaming variant of the 32 -> 1 layer: one CTA per member image (a thread per column, all
+// W <= 1024 columns, so horizontal neighbours never cross CTAs), each thread walking all rows.  Each activation is read ONCE (the gather form above reads every pixel
+// nine times) and turned into its nine tap contributions v[ky][kx] = sum_ci w[ci][ky][kx] h[ci]
+// (nine independent FMA chains instead of one 288-long chain); horizontal taps are folded with
+// warp shuffles plus a per-row exchange between the strip's four warps, vertical taps through a
+// 3-row register ring (output row r is complete after input row r + 1).
+__global__ void __launch_bounds__(1024) deep_last_rows_kernel(const __half* __restrict__ ah,
+                                                           const __half* __restrict__ al,
+                                                           const float* __restrict__ w,
+                                                           const float* __restrict__ b, float alpha,
+                                                           const float* __restrict__ x, int64_t ldx,
+                                                           float* __restrict__ out, int64_t ldo,
+                                                           int H, int W, int64_t m0) {
+    __shared__ float sw[DC * 12];        // [ci][ky*3+kx], padded to 12
+    __shared__ float xa[2][32][4], xb[2][32][4];  // [parity][warp][ky]: boundary taps
+    for (int e = threadIdx.x; e < DC * 12; e += blockDim.x) {
+        const int ci = e / 12, k = e - ci * 12;
+        sw[e] = k < 9 ? w[ci * 9 + k] : 0.f;
+    }
+    __syncthreads();
+    const int c = threadIdx.x;  // blockDim.x == W
+    const int64_t m = blockIdx.y;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const bool xl = c > 0 && lane == 0, xr = c < W - 1 && lane == 31;  // neighbour across warps
+    const float bias = b[0];
+    const int64_t col = (m0 + m) * W + c;
+    float acc3[3] = {0.f, 0.f, 0.f};
+    for (int rr = 0; rr < H; ++rr) {
+        const int64_t px = ((m * H + rr) * (int64_t)W + c) * DC;
+        const uint4* ph = reinterpret_cast<const uint4*>(ah + px);
+        const uint4* pl = reinterpret_cast<const uint4*>(al + px);
+        float v[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) v[k] = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint4 hv = __ldg(ph + q), lv = __ldg(pl + q);
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float2 h2 = __half22float2(*reinterpret_cast<const __half2*>(&hw[t]));
+                const float2 l2 = __half22float2(*reinterpret_cast<const __half2*>(&lw[t]));
+                const float a0 = h2.x + l2.x, a1 = h2.y + l2.y;
+                const float* w0 = sw + (q * 8 + 2 * t) * 12;
+                const float* w1 = w0 + 12;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) v[k] = fmaf(w1[k], a1, fmaf(w0[k], a0, v[k]));
+            }
+        }
+        // horizontal fold: column c takes v[ky][0] of c - 1 and v[ky][2] of c + 1
+        float tk[3];
+        const int par = rr & 1;
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky) {
+            const float up = __shfl_up_sync(0xffffffffu, v[ky * 3 + 0], 1);
+            const float dn = __shfl_down_sync(0xffffffffu, v[ky * 3 + 2], 1);
+            tk[ky] = v[ky * 3 + 1] + (lane == 0 ? 0.f : up) + (lane == 31 ? 0.f : dn);
+            if (lane == 31) xa[par][wp][ky] = v[ky * 3 + 0];
+            if (lane == 0) xb[par][wp][ky] = v[ky * 3 + 2];
+        }
+        __syncthreads();
+        if (xl) {
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) tk[ky] += xa[par][wp - 1][ky];
+        }
+        if (xr) {
+#pragma unroll
+            for (int ky = 0; ky < 3; ++ky) tk[ky] += xb[par][wp + 1][ky];
+        }
+        // input row rr feeds output rows rr + 1 (ky = 0), rr (ky = 1), rr - 1 (ky = 2)
+        acc3[(rr + 1) % 3] += tk[0];
+        acc3[rr % 3] += tk[1];
+        if (rr >= 1) {
+            const int ro = rr - 1;
+            const float o = acc3[ro % 3] + tk[2];
+            acc3[ro % 3] = 0.f;
+            out[ro * ldo + col] = x[ro * ldx + col] + alpha * (bias + o);
+        }
+        if (rr == H - 1) {
+            const float o = acc3[rr % 3];
+            acc3[rr % 3] = 0.f;
+            out[rr * ldo + col] = x[rr * ldx + col] + alpha * (bias + o);
+        }
+    }
+}
+
 typedef CUresult (*EncodeTiledFnD)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -452,9 +538,17 @@ int cnn_deep_forward(int n_layers, const float* weights, const float* biases, fl
             t1h = th;
             t1l = tl;
         }
-        deep_last_kernel<<<pgrid, DW, 0, st>>>(t0h, t0l, weights + woff[n_layers - 1],
-                                               biases + boff[n_layers - 1], alpha, x, ldx, out, ldo,
-                                               rows, cols, m0);
+        {
+            const char* le = getenv("ENKS_DEEP_LAST");
+            if ((le && le[0] == '0') || cols > 1024 || cols % 32)
+                deep_last_kernel<<<pgrid, DW, 0, st>>>(t0h, t0l, weights + woff[n_layers - 1],
+                                                       biases + boff[n_layers - 1], alpha, x, ldx,
+                                                       out, ldo, rows, cols, m0);
+            else
+                deep_last_rows_kernel<<<dim3(1, (unsigned)cm), (unsigned)cols, 0, st>>>(
+                    t0h, t0l, weights + woff[n_layers - 1], biases + boff[n_layers - 1], alpha, x,
+                    ldx, out, ldo, rows, cols, m0);
+        }
         rc = check_launch("enks_cnn_forward(deep last)");
         if (rc) return rc;
     }
