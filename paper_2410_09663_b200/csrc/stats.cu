@@ -11,6 +11,9 @@
 // chunks in order.  enks_member_center is a flat, float4-vectorised pass.
 #include <cuda_fp16.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace enks {
@@ -52,6 +55,62 @@ __global__ void __launch_bounds__(kSumThreads)
     }
     part[blockIdx.y * rc + e] = (acc0 + acc1) + (acc2 + acc3);
     partmax[blockIdx.y * rc + e] = mx;
+}
+
+// vectorised variant: 4 consecutive columns per thread (cols % 4 == 0, 16-B aligned rows), so a
+// warp reads one 512-B member row per load and keeps 4 members (8 with src2) of loads in flight.
+// Per element the member order and the four interleaved fp64 chains are those of the scalar
+// kernel above (bit-identical partials).
+__global__ void __launch_bounds__(kSumThreads)
+    member_partial_v4_kernel(const float* __restrict__ src, int64_t ld, const float* __restrict__ src2,
+                             int64_t ld2, int rows, int64_t n, int cols,
+                             const float* __restrict__ z0, double* __restrict__ part,
+                             float* __restrict__ partmax, int64_t chunk) {
+    const int64_t rc = (int64_t)rows * cols;
+    const int64_t e = (blockIdx.x * (int64_t)kSumThreads + threadIdx.x) * 4;
+    if (e >= rc) return;
+    const int r = (int)(e / cols), j = (int)(e - (int64_t)r * cols);
+    const float* p = src + r * ld + j;
+    const float* p2 = src2 ? src2 + r * ld2 + j : nullptr;
+    auto val = [&](int64_t i) {
+        float4 v = __ldg(reinterpret_cast<const float4*>(p + i * cols));
+        if (p2) {
+            const float4 w = __ldg(reinterpret_cast<const float4*>(p2 + i * cols));
+            v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+        }
+        return v;
+    };
+    const float4 s = z0 ? __ldg(reinterpret_cast<const float4*>(z0 + e)) : val(0);
+    const int64_t i0 = blockIdx.y * chunk, i1 = min(n, i0 + chunk);
+    double acc[4][4] = {};
+    float mx[4] = {0.f, 0.f, 0.f, 0.f};
+    auto add = [&](int c, const float4& v) {
+        const float d0 = v.x - s.x, d1 = v.y - s.y, d2 = v.z - s.z, d3 = v.w - s.w;
+        acc[c][0] += (double)d0;
+        acc[c][1] += (double)d1;
+        acc[c][2] += (double)d2;
+        acc[c][3] += (double)d3;
+        mx[0] = fmaxf(mx[0], fabsf(d0));
+        mx[1] = fmaxf(mx[1], fabsf(d1));
+        mx[2] = fmaxf(mx[2], fabsf(d2));
+        mx[3] = fmaxf(mx[3], fabsf(d3));
+    };
+    int64_t i = i0;
+    for (; i + 4 <= i1; i += 4) {
+        const float4 v0 = val(i + 0), v1 = val(i + 1), v2 = val(i + 2), v3 = val(i + 3);
+        add(0, v0);
+        add(1, v1);
+        add(2, v2);
+        add(3, v3);
+    }
+    for (; i < i1; ++i) add(0, val(i));
+    double out[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q] = (acc[0][q] + acc[1][q]) + (acc[2][q] + acc[3][q]);
+    double* po = part + blockIdx.y * rc + e;
+    reinterpret_cast<double2*>(po)[0] = make_double2(out[0], out[1]);
+    reinterpret_cast<double2*>(po)[1] = make_double2(out[2], out[3]);
+    *reinterpret_cast<float4*>(partmax + blockIdx.y * rc + e) = make_float4(mx[0], mx[1], mx[2], mx[3]);
 }
 
 __global__ void chunk_reduce_kernel(const double* __restrict__ part, const float* __restrict__ pmax,
@@ -211,22 +270,45 @@ __global__ void __launch_bounds__(256) center_f16pair_t_kernel(
     const bool in = c < K;
     const int j = in ? (int)((uint64_t)c % (uint64_t)cols) : 0;
     float mx = 0.f;
-    for (int r = ty; r < rows; r += 8) {
-        float a = 0.f;
-        if (in) {
-            const float x = src[r * ld + c] + (src2 ? src2[r * ld2 + c] : 0.f);
-            const float s = z0 ? z0[(int64_t)r * cols + j]
-                               : src[r * ld + j] + (src2 ? src2[r * ld2 + j] : 0.f);
-            const float mu = (float)(acc[(int64_t)r * cols + j] * inv_n);
-            if (mean && c < cols) mean[(int64_t)r * cols + j] = s + mu;
-            a = (x - s) - mu;
-            const float v = a * scale[r];
-            const __half hv = __float2half_rn(v);
-            h[r * ldh + c] = hv;
-            l[r * ldh + c] = __float2half_rn(v - __half2float(hv));
+    // rows in batches of kB per warp: all loads of a batch are issued before any use, so each warp
+    // keeps kB (2 kB with src2) 128-B row segments in flight
+    // rows in batches of kB per warp: every load of a batch is issued before any arithmetic (the
+    // x + v and member-0 sums happen after the batch), so each warp keeps up to 4 kB 128-B row
+    // segments in flight instead of waiting on each row
+    constexpr int kB = 4;
+    const float* s1 = z0 ? z0 : src;  // member-0 shift: z0[r, j], or src[r, j] (+ src2[r, j])
+    const int64_t ld_s1 = z0 ? cols : ld;
+    for (int r0 = ty; r0 < rows; r0 += 8 * kB) {
+        float x1[kB], x2[kB], z1[kB], z2[kB];
+        double av[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+            const int r = r0 + 8 * b;
+            const bool ok = in && r < rows;
+            x1[b] = ok ? src[r * ld + c] : 0.f;
+            x2[b] = ok && src2 ? src2[r * ld2 + c] : 0.f;
+            z1[b] = ok ? s1[r * ld_s1 + j] : 0.f;
+            z2[b] = ok && !z0 && src2 ? src2[r * ld2 + j] : 0.f;
+            av[b] = ok ? __ldg(acc + (int64_t)r * cols + j) : 0.0;
         }
-        tile[r][tx] = a;
-        mx = fmaxf(mx, fabsf(a));
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+            const int r = r0 + 8 * b;
+            if (r >= rows) break;
+            float a = 0.f;
+            if (in) {
+                const float x = x1[b] + x2[b], s = z1[b] + z2[b];
+                const float mu = (float)(av[b] * inv_n);
+                if (mean && c < cols) mean[(int64_t)r * cols + j] = s + mu;
+                a = (x - s) - mu;
+                const float v = a * scale[r];
+                const __half hv = __float2half_rn(v);
+                h[r * ldh + c] = hv;
+                l[r * ldh + c] = __float2half_rn(v - __half2float(hv));
+            }
+            tile[r][tx] = a;
+            mx = fmaxf(mx, fabsf(a));
+        }
     }
     red[ty][tx] = mx;
     __syncthreads();
@@ -309,9 +391,19 @@ __global__ void uchain_gain_kernel(const float* __restrict__ g, int64_t ld_g, fl
     gtt[(int64_t)r * ld_gtt + c] = v;
 }
 
-int64_t member_chunks(int rows, int64_t n, int cols) {
+// ENKS_SUM_SCALAR=1: the scalar member-sum kernel (A/B measurements, tools/stats_bench.py)
+bool sum_scalar() {
+    static const bool v = [] {
+        const char* e = getenv("ENKS_SUM_SCALAR");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+// per = columns per thread (4 for the vectorised partial kernel)
+int64_t member_chunks(int rows, int64_t n, int cols, int per) {
     const int64_t rc = (int64_t)rows * cols;
-    const int64_t blocks = (rc + kSumThreads - 1) / kSumThreads;
+    const int64_t blocks = (rc / per + kSumThreads - 1) / kSumThreads;
     // aim for ~8 blocks per SM in flight
     int64_t want = (8LL * kNumSMs + blocks - 1) / blocks;
     if (want > 64) want = 64;
@@ -326,7 +418,9 @@ int64_t member_chunks(int rows, int64_t n, int cols) {
 extern "C" {
 
 int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols) {
-    return enks::member_chunks(rows, n_members, cols) * (int64_t)rows * cols *
+    const int64_t nch = std::max(enks::member_chunks(rows, n_members, cols, 1),
+                                 enks::member_chunks(rows, n_members, cols, 4));
+    return nch * (int64_t)rows * cols *
            (int64_t)(sizeof(double) + sizeof(float));
 }
 
@@ -342,14 +436,28 @@ int enks_member_sum(const float* src, int64_t ld_src, const float* src2, int64_t
         if (amax) cudaMemsetAsync(amax, 0, rc * sizeof(float), st);
         return enks::check_launch("enks_member_sum(memset)");
     }
-    const int64_t nch = enks::member_chunks(rows, n_members, cols);
+    // The vectorised kernel (4 columns per thread) wins with the on-the-fly sum x + v (two
+    // streams: 62 vs 75 us at C3, tools/stats_bench.py); for a single stream the scalar kernel
+    // (more resident warps, 52 vs 63 us) does.
+    auto a16 = [](const void* ptr) { return ((uintptr_t)ptr & 15) == 0; };
+    const bool v4 = !enks::sum_scalar() && src2 && cols % 4 == 0 && ld_src % 4 == 0 && a16(src) &&
+                    ld_src2 % 4 == 0 && a16(src2) && (!z0 || a16(z0)) && rc % 4 == 0;
+    const int64_t nch = enks::member_chunks(rows, n_members, cols, v4 ? 4 : 1);
     const int64_t chunk = (n_members + nch - 1) / nch;
     const int64_t nch_eff = (n_members + chunk - 1) / chunk;
-    dim3 grid((unsigned)((rc + enks::kSumThreads - 1) / enks::kSumThreads), (unsigned)nch_eff);
     double* part = static_cast<double*>(ws);
-    float* pmax = reinterpret_cast<float*>(part + nch * rc);
-    enks::member_partial_kernel<<<grid, enks::kSumThreads, 0, st>>>(
-        src, ld_src, src2, ld_src2, rows, n_members, cols, z0, part, pmax, chunk);
+    const int64_t nch_ws = std::max(enks::member_chunks(rows, n_members, cols, 1),
+                                    enks::member_chunks(rows, n_members, cols, 4));
+    float* pmax = reinterpret_cast<float*>(part + nch_ws * rc);
+    if (v4) {
+        dim3 grid((unsigned)((rc / 4 + enks::kSumThreads - 1) / enks::kSumThreads), (unsigned)nch_eff);
+        enks::member_partial_v4_kernel<<<grid, enks::kSumThreads, 0, st>>>(
+            src, ld_src, src2, ld_src2, rows, n_members, cols, z0, part, pmax, chunk);
+    } else {
+        dim3 grid((unsigned)((rc + enks::kSumThreads - 1) / enks::kSumThreads), (unsigned)nch_eff);
+        enks::member_partial_kernel<<<grid, enks::kSumThreads, 0, st>>>(
+            src, ld_src, src2, ld_src2, rows, n_members, cols, z0, part, pmax, chunk);
+    }
     int rc_ = enks::check_launch("enks_member_sum(partial)");
     if (rc_) return rc_;
     enks::chunk_reduce_kernel<<<(unsigned)((rc + 255) / 256), 256, 0, st>>>(part, pmax, (int)nch_eff,
