@@ -75,13 +75,20 @@ __device__ __forceinline__ void f16p_store_row(const P16& p, int split, int64_t 
     float* orow = p.out + (int64_t)split * p.split_stride + r * p.ldo + c_first;
     if (!p.c0 && !p.bias) {
         if (ncol == NC && (((uintptr_t)orow) & 15) == 0) {
+            // the column scales of a batch are loaded before its stores (out may alias inv_sb as
+            // far as the compiler knows: loads after a store would each wait a full latency)
+            constexpr int kSB = 16;
 #pragma unroll
-            for (int j = 0; j < NC; j += 4)
-                *reinterpret_cast<float4*>(orow + j) =
-                    make_float4(acc[j] * sa * p.inv_sb[c_first + j],
-                                acc[j + 1] * sa * p.inv_sb[c_first + j + 1],
-                                acc[j + 2] * sa * p.inv_sb[c_first + j + 2],
-                                acc[j + 3] * sa * p.inv_sb[c_first + j + 3]);
+            for (int j0 = 0; j0 < NC; j0 += kSB) {
+                float sv[kSB];
+#pragma unroll
+                for (int q = 0; q < kSB; ++q) sv[q] = j0 + q < NC ? p.inv_sb[c_first + j0 + q] : 0.f;
+#pragma unroll
+                for (int j = j0; j < j0 + kSB && j < NC; j += 4)
+                    *reinterpret_cast<float4*>(orow + j) =
+                        make_float4(acc[j] * sa * sv[j - j0], acc[j + 1] * sa * sv[j - j0 + 1],
+                                    acc[j + 2] * sa * sv[j - j0 + 2], acc[j + 3] * sa * sv[j - j0 + 3]);
+            }
             return;
         }
 #pragma unroll
@@ -94,24 +101,45 @@ __device__ __forceinline__ void f16p_store_row(const P16& p, int split, int64_t 
     const bool vec = ncol == NC && (((uintptr_t)orow | (uintptr_t)(crow ? crow : orow)) & 15) == 0 &&
                      (!brow || ((c_first % p.bias_cols) + NC <= p.bias_cols &&
                                 (((uintptr_t)(brow + c_first % p.bias_cols)) & 15) == 0));
-    if (vec) {  // float4 loads / stores: 128 consecutive columns per thread
+    if (vec) {  // float4 loads / stores: NC consecutive columns per thread
         const float* bb = brow ? brow + c_first % p.bias_cols : nullptr;
+        // C0 / bias in batches of kVB float4 loaded before any store of the batch: out and C0
+        // may alias as far as the compiler knows, so loads interleaved with stores would each
+        // wait a full memory latency (the newest-slice shift, 256 columns of C0 per row)
+        constexpr int kVB = 4;
 #pragma unroll
-        for (int j = 0; j < NC; j += 4) {
-            float4 o;
-            o.x = acc[j] * sa * p.inv_sb[c_first + j];
-            o.y = acc[j + 1] * sa * p.inv_sb[c_first + j + 1];
-            o.z = acc[j + 2] * sa * p.inv_sb[c_first + j + 2];
-            o.w = acc[j + 3] * sa * p.inv_sb[c_first + j + 3];
-            if (crow) {
-                const float4 c = __ldg(reinterpret_cast<const float4*>(crow + j));
-                o.x += p.beta * c.x; o.y += p.beta * c.y; o.z += p.beta * c.z; o.w += p.beta * c.w;
+        for (int j0 = 0; j0 < NC; j0 += 4 * kVB) {
+            float4 cv[kVB], bv[kVB], sv[kVB];
+#pragma unroll
+            for (int q = 0; q < kVB; ++q) {
+                const int j = j0 + 4 * q;
+                sv[q] = j < NC ? make_float4(p.inv_sb[c_first + j], p.inv_sb[c_first + j + 1],
+                                             p.inv_sb[c_first + j + 2], p.inv_sb[c_first + j + 3])
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                cv[q] = crow && j < NC ? __ldg(reinterpret_cast<const float4*>(crow + j))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                bv[q] = bb && j < NC ? __ldg(reinterpret_cast<const float4*>(bb + j))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            if (bb) {
-                const float4 b = __ldg(reinterpret_cast<const float4*>(bb + j));
-                o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+#pragma unroll
+            for (int q = 0; q < kVB; ++q) {
+                const int j = j0 + 4 * q;
+                if (j >= NC) break;
+                float4 o;
+                o.x = acc[j] * sa * sv[q].x;
+                o.y = acc[j + 1] * sa * sv[q].y;
+                o.z = acc[j + 2] * sa * sv[q].z;
+                o.w = acc[j + 3] * sa * sv[q].w;
+                if (crow) {
+                    const float4 c = cv[q];
+                    o.x += p.beta * c.x; o.y += p.beta * c.y; o.z += p.beta * c.z; o.w += p.beta * c.w;
+                }
+                if (bb) {
+                    const float4 b = bv[q];
+                    o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+                }
+                *reinterpret_cast<float4*>(orow + j) = o;
             }
-            *reinterpret_cast<float4*>(orow + j) = o;
         }
         return;
     }
