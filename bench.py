@@ -11,17 +11,18 @@ H=50), synthetic inputs, random-init CNN.
   value : horizons/s with inputs resident in HBM, CUDA-event timed (max over ranks); on one
           GPU the horizon is replayed as one CUDA graph (smooth_horizon(graph=True): the same
           kernels as the eager path, without per-launch host cost; --no-graph times eager)
-  e2e   : the same metric through the public API enks.smooth_horizon with host
-          (NumPy) inputs and a host result each step
+  e2e   : the same metric through the public API enks.smooth_horizon (default eager call) with
+          host (NumPy) inputs and the host result each step; e2e_graph: same with graph=True
   kernels : per-kernel-family CUDA-event brackets of one extra eager horizon (untimed)
   roofline : the dominant kernel (the cross-moment contraction P = [A; Yc] Yc^T)
           algorithmic FLOPs / its CUDA-event-measured launch time vs MEASURED_PEAKS.json
-  cpu_baseline : the fp64 oracle port timed on this host on a bounded sample
-          (rank 0, N=1 only), horizon time extrapolated from per-step times
+  cpu_baseline : the UNMODIFIED reference (enksmpc installed in baseline/_ref) timed on this
+          host's physical cores on a bounded sample (rank 0, N=1 only), horizon time from the
+          a + b T per-step model (oracle/refrun.py), plus one single-thread step
 
-N > 1 (torchrun): members sharded over ranks, NCCL allreduce of the covariance
-partials; strong scaling of one horizon.  --impl reference times the CPU
-oracle port (the reference is pure Python and cannot travel to the box).
+N > 1 (torchrun, or --gpus N re-executes itself under torchrun): members sharded over ranks,
+NCCL allreduce of the covariance partials; strong scaling of one horizon.  --impl reference times
+the unmodified reference on the host CPU (rank 0 prints; other ranks exit 0).
 """
 from __future__ import annotations
 
@@ -116,11 +117,19 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def _problem(config: str, members, horizon):
-    from oracle import problems  # builder of synthetic inputs (shapes per SURVEY.md §8d)
+def _modules():
+    from types import SimpleNamespace
 
-    pm = problems.product_modules()
-    return pm, problems.make_cnn_problem(pm, config, n_members=members, horizon=horizon)
+    import paper_2410_09663_b200 as pkg
+
+    return SimpleNamespace(dynamics=pkg.dynamics, virtualsys=pkg.virtualsys, matvar=pkg.matvar)
+
+
+def _problem(config: str, members, horizon):
+    from paper_2410_09663_b200 import configs  # synthetic inputs (shapes per SURVEY.md §8d)
+
+    pm = _modules()
+    return pm, configs.make_cnn_problem(pm, config, n_members=members, horizon=horizon)
 
 
 def _algorithmic(pr):
@@ -136,93 +145,121 @@ def _algorithmic(pr):
     return dict(cnn_tflop=cnn_flops / 1e12, cross_tflop=cross / 1e12, enks_ref_tflop=enks_ref / 1e12)
 
 
-# ---------------------------------------------------------------------- CPU oracle sampling
-def cpu_sample(pr, t_values, threads=None):
-    """Time oracle predict+update steps at trajectory lengths t_values; fit a + b*T.
+# ---------------------------------------------------------------------- reference arm
+def _ref_timer(config, members, horizon):
+    """(modules, problem, kind) of the CPU path timed: the installed unmodified reference
+    (baseline/_ref, kind "reference") or, if it is missing, the fp64 oracle port ("port")."""
+    from oracle import refrun
 
-    Steps are run on synthetic ensembles of the right shape (members = x0 copies
-    plus noise), so a step at T costs exactly what the reference pays there.
-    Returns (horizon_seconds, samples, cores).
-    """
-    import torch
+    rm = refrun.reference_modules()
+    if rm is not None:
+        return rm, refrun.make_problem(rm, config, members, horizon), "reference"
+    from types import SimpleNamespace
 
     from oracle import enks_oracle
 
-    cores = threads or os.cpu_count() or 1
-    torch.set_num_threads(cores)
-    vs, x0, N, H = pr.vs, pr.x0, pr.N, pr.H
-    d = x0.n + 2 * x0.l
-    rng = np.random.default_rng(0)
-    samples = []
-    for T in t_values:
-        ens = enks_oracle.oracle_init(x0.packed, x0.n, x0.l, N, shared_col_cov=vs.shared_col_cov)
-        if T > 1:
-            extra = x0.packed[None, None] + 0.1 * rng.standard_normal((N, T - 1, d, x0.m))
-            ens.members = np.concatenate([ens.members, extra.reshape(N, (T - 1) * d, x0.m)], axis=1)
-            ens.t = T - 1
-            ens.mean = ens.members.mean(axis=0)
-        t0 = time.perf_counter()
-        enks_oracle.oracle_predict(ens, vs, 0)
-        enks_oracle.oracle_update(ens, pr.y_ref, vs, 0)
-        samples.append((T, time.perf_counter() - t0))
-        del ens
-    Ts = np.array([s[0] for s in samples], float)
-    ys = np.array([s[1] for s in samples], float)
-    if len(set(Ts)) >= 2:
-        b, a = np.polyfit(Ts, ys, 1)
-        b = max(b, 0.0)
-        a = max(a, float(ys.min()) - b * Ts[np.argmin(ys)])
-    else:
-        a, b = float(ys.mean()), 0.0
-    horizon = sum(a + b * T for T in range(1, H + 1))
-    return horizon, samples, cores
+    port = SimpleNamespace(enks=SimpleNamespace(
+        init_ensemble=lambda x0, N, shared_col_cov=None: enks_oracle.oracle_init(
+            x0.packed, x0.n, x0.l, N, shared_col_cov=shared_col_cov),
+        predict=lambda e, vs, st: enks_oracle.oracle_predict(e, vs, st.seed, tuple(st.prefix),
+                                                             backend="c"),
+        update=lambda e, y, vs, st: enks_oracle.oracle_update(e, y, vs, st.seed, tuple(st.prefix),
+                                                              backend="c")))
+    pm = _modules()
+    port.matvar = pm.matvar
+    pr = refrun.make_problem(pm, config, members, horizon)
+    return port, pr, "port"
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle port of the reference path, rank 0 only."""
+    """--impl reference: the UNMODIFIED reference smoother (enksmpc from baseline/_ref, fp64,
+    NumPy/SciPy/OpenBLAS + the fp64 torch-CPU CNN) on all physical cores of this host, rank 0
+    only.  Each step times one predict+update at trajectory length T (cycling T_SAMPLES); the
+    horizon time is sum_{T=1..H} (a + b T) fitted over the timed steps (oracle/refrun.py)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    pm, pr = _problem(args.config, args.members, args.horizon)
-    ts = [1, 3, 5, 7]
-    per_step = []
-    all_samples = []
-    for k in range(args.warmup + args.steps):
-        T = ts[k % len(ts)]
-        _, samples, cores = cpu_sample(pr, [T])
-        if k >= args.warmup:
-            all_samples.extend(samples)
-            per_step.append(samples[0][1])
-    Ts = np.array([s[0] for s in all_samples], float)
-    ys = np.array([s[1] for s in all_samples], float)
-    b, a = np.polyfit(Ts, ys, 1) if len(set(Ts)) >= 2 else (0.0, float(ys.mean()))
-    b = max(b, 0.0)
-    horizon = sum(a + b * T for T in range(1, pr.H + 1))
+    from oracle import refrun
+
+    rm, pr, kind = _ref_timer(args.config, args.members, args.horizon)
+    topo = refrun.cpu_topology()
+    cores = topo["physical"]
+    ts = [t for t in T_SAMPLES if t <= pr.H] or [1]
+    samples = []
+    with refrun.threads(cores):
+        for k in range(args.warmup + args.steps):
+            T = ts[k % len(ts)]
+            dt = refrun.time_step(rm, pr, T, seed=k)
+            if k >= args.warmup:
+                samples.append((T, dt))
+    horizon, a, b = refrun.fit_horizon(samples, pr.H)
     value = 1.0 / horizon
     line = {
         "impl": "reference", "metric": "OIC horizon solves/sec", "value": value,
         "unit": "horizons/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": horizon * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": _config(pr, args),
+        "config": _config(pr, args, world=1),
         "member_cnn_steps_per_s": pr.N * pr.H * value,
-        "cpu_baseline": {"value": value, "unit": "horizons/s", "cores": os.cpu_count(),
-                         "kind": "port",
-                         "sample": f"fp64 oracle port (oracle/enks_oracle.py, torch-CPU fp64 CNN) "
-                                   f"predict+update steps at T={[int(t) for t in Ts]} of "
-                                   f"{args.config} (N={pr.N}); horizon = sum_T (a + b T), "
-                                   f"a={a:.3f}s b={b:.3f}s"},
+        "cpu_baseline": {"value": value, "unit": "horizons/s", "cores": cores, "kind": kind,
+                         "topology": topo,
+                         "sample": f"unmodified enksmpc.enks predict+update (baseline/_ref) with the "
+                                   f"fp64 torch-CPU CNN, {cores} threads (BLAS + torch), at "
+                                   f"T={[s[0] for s in samples]} "
+                                   f"({[round(s[1], 2) for s in samples]} s) of {args.config} "
+                                   f"(N={pr.N}); horizon = sum_(T=1..{pr.H}) (a + b T), "
+                                   f"a={a:.3f} s, b={b:.3f} s"
+                                   + ("" if kind == "reference" else " [reference not installed: "
+                                      "fp64 oracle port]")},
+        "fit_validation": _fit_validation(args.config),
         "e2e": {"value": value, "unit": "horizons/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
-def _config(pr, args):
+T_SAMPLES = (1, 4, 8, 12)
+
+
+def _fit_validation(config):
+    """The committed full-horizon reference measurement that validates the a + b T model."""
+    path = os.path.join(ROOT, "profiles", "r02", f"reference_{config.lower()}_full.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return {"source": os.path.relpath(path, ROOT), "measured_horizon_s": d.get("horizon_s"),
+            "fit_from_T_le_12_s": d.get("fit_T_le_12_horizon_s"), "cores": d.get("cores")}
+
+
+def cpu_baseline(config, members, horizon):
+    """Our arm's cpu_baseline: the unmodified reference at T = 1 and 8 on all physical cores
+    (horizon by the a + b T model), plus one single-thread step at T = 1 (~30 s in all)."""
+    from oracle import refrun
+
+    rm, pr, kind = _ref_timer(config, members, horizon)
+    topo = refrun.cpu_topology()
+    cores = topo["physical"]
+    with refrun.threads(cores):
+        samples = [(T, refrun.time_step(rm, pr, T)) for T in (1, 8) if T <= pr.H] or \
+            [(1, refrun.time_step(rm, pr, 1))]
+    with refrun.threads(1):
+        one = refrun.time_step(rm, pr, 1)
+    horizon_s, a, b = refrun.fit_horizon(samples, pr.H)
+    return {"value": 1.0 / horizon_s, "unit": "horizons/s", "cores": cores, "kind": kind,
+            "topology": topo,
+            "sample": f"unmodified enksmpc.enks predict+update at T={[s[0] for s in samples]} "
+                      f"({[round(s[1], 2) for s in samples]} s, {cores} threads) of {config}; "
+                      f"horizon = sum_T (a + b T), a={a:.3f} s, b={b:.3f} s",
+            "single_thread_step_T1_s": one, "step_T1_s": samples[0][1]}
+
+
+def _config(pr, args, world):
     return {"workload": f"{args.config}: OIC horizon solve, {pr.n}x{pr.m} field, "
                         f"CNN {'-'.join(map(str, pr.widths))}, N={pr.N} members, H={pr.H}",
             "n": pr.n, "m": pr.m, "l": pr.l, "members": pr.N, "horizon": pr.H,
-            "cnn_widths": list(pr.widths), "parallelism": f"members sharded x{args.gpus}",
+            "cnn_widths": list(pr.widths),
+            "parallelism": f"members sharded over {world} rank(s)" if world > 1 else "1 GPU",
             "l2": "inputs larger than L2 (append-only basis >> 126 MB at C2/C3)"}
 
 
@@ -311,34 +348,13 @@ def run_ours(args):
         elapsed, kern_s = float(t[0]), float(t[1])
     value = args.steps / elapsed
 
-    # e2e through the public API with host inputs and a host result each step
-    e2e = None
+    # e2e through the public API with host inputs and a host result each step: the default eager
+    # smooth_horizon(...) (the call a reference user makes) is the headline, graph=True beside it
+    e2e = e2e_graph = None
     if not args.no_e2e:
-        ebytes_in = (pr.x0.packed.size + h * pr.y_ref.size) * 8
-        for _ in range(1):
-            enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, h, pr.N, streams, graph=graph is not None)
-        torch.cuda.synchronize()
-        if comm is not None:
-            dist.barrier()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        out = None
-        for _ in range(args.steps):
-            y_host = np.broadcast_to(pr.y_ref, (h,) + pr.y_ref.shape)
-            out, _ = enks.smooth_horizon(pr.x0, y_host, pr.vs, h, pr.N, streams,
-                                         graph=graph is not None)
-        e.record()
-        torch.cuda.synchronize()
-        e2e_s = s.elapsed_time(e) / 1e3
-        if comm is not None:
-            t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t[0])
-        cnn_bytes = sum(np.asarray(w).size for w in pr.model.weights) * 4 + \
-            sum(np.asarray(b).size for b in pr.model.biases) * 4
-        e2e = {"value": args.steps / e2e_s, "unit": "horizons/s",
-               "h2d_bytes_per_step": int(ebytes_in // 2 + cnn_bytes + 3 * pr.n * 8),
-               "d2h_bytes_per_step": int(out.size * 4 + 4)}
+        e2e = _e2e(args, enks, ops, pr, streams, comm, graph=False)
+        if graph is not None:
+            e2e_graph = _e2e(args, enks, ops, pr, streams, comm, graph=True)
 
     peaks, peak_kind = _peaks()
     alg = _algorithmic(pr)
@@ -393,11 +409,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        horizon_s, samples, cores = cpu_sample(pr, [1, 4])
-        cpu = {"value": 1.0 / horizon_s, "unit": "horizons/s", "cores": cores, "kind": "port",
-               "sample": f"fp64 oracle port predict+update at T={[s[0] for s in samples]} "
-                         f"({[round(s[1], 2) for s in samples]} s) of {args.config}, "
-                         f"horizon extrapolated as sum_T (a + b T)"}
+        cpu = cpu_baseline(args.config, args.members, args.horizon)
 
     if rank == 0:
         line = {
@@ -406,9 +418,10 @@ def run_ours(args):
             "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (sine-field x0, random-init CNN, bit-exact numpy noise streams)",
-            "config": _config(pr, args),
+            "config": _config(pr, args, world),
             "member_cnn_steps_per_s": pr.N * h * value,
-            "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,
+            "e2e": e2e, "e2e_graph": e2e_graph,
+            "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,
             "cuda_graph": graph is not None,
             "cpu_baseline": cpu, "clocks": clk,
             "algorithmic": alg,
@@ -419,8 +432,61 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _e2e(args, enks, ops, pr, streams, comm, graph: bool):
+    """horizons/s through enks.smooth_horizon with host NumPy inputs and the host fp64 result,
+    all host<->device copies inside the timed region (bytes counted by DeviceOps)."""
+    import torch
+    import torch.distributed as dist
+
+    h = pr.H
+    enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, h, pr.N, streams, graph=graph)  # warm
+    torch.cuda.synchronize()
+    if comm is not None:
+        dist.barrier()
+    b_in, b_out = ops.h2d_bytes, ops.d2h_bytes
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        y_host = np.broadcast_to(pr.y_ref, (h,) + pr.y_ref.shape)
+        out, _ = enks.smooth_horizon(pr.x0, y_host, pr.vs, h, pr.N, streams, graph=graph)
+    e.record()
+    torch.cuda.synchronize()
+    sec = s.elapsed_time(e) / 1e3
+    if comm is not None:
+        t = torch.tensor([sec], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t[0])
+    return {"value": args.steps / sec, "unit": "horizons/s",
+            "h2d_bytes_per_step": int((ops.h2d_bytes - b_in) // args.steps),
+            "d2h_bytes_per_step": int((ops.d2h_bytes - b_out) // args.steps),
+            "call": f"enks.smooth_horizon(x0, y_refs, vs, h, N, streams{', graph=True' if graph else ''})",
+            "result": f"mean trajectory {tuple(out.shape)} fp64 on the host"}
+
+
+def _relaunch_under_torchrun(args) -> None:
+    """--gpus N > 1 without a torchrun environment: re-exec this command as N ranks (one process
+    per GPU, NCCL), or fail loudly when this node has fewer GPUs -- never a 1-rank line."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has "
+                         f"{have}\n")
+        sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", "--master-port=29517",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = _args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _relaunch_under_torchrun(args)
+    if args.impl == "ours" and int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE="
+                         f"{os.environ.get('WORLD_SIZE')}\n")
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -105,6 +105,14 @@ int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols);
 int enks_member_sum(const float* src, int64_t ld_src, const float* src2, int64_t ld_src2, int rows,
                     int64_t n_members, int cols, const float* z0, double* acc, float* amax, void* ws,
                     void* stream);
+/* Multi-rank member sums without a broadcast of global member 0: each rank sums relative to its
+ * OWN first member s (z0 = NULL), converts to absolute sums with coef = +n_local
+ * (acc += coef * s), the ranks allreduce, and each converts back with coef = -n_total, so the
+ * centring kernels again see sums relative to their local s.  Identical members still give
+ * exactly zero anomalies (n * s is exact in fp64).  src2 as in enks_member_sum (s = src + src2
+ * in fp32).  Replaces the member-0 broadcast of the enks.py:171 / 231 means under sharding. */
+int enks_member_sum_rebase(const float* src, int64_t ld_src, const float* src2, int64_t ld_src2,
+                           int rows, int cols, double* acc, double coef, void* stream);
 int enks_member_center(const float* src, int64_t ld_src, int rows, int64_t n_members, int cols,
                        const float* z0, const double* acc, int64_t n_total, float* mean,
                        float* anom, int64_t ld_anom, void* stream);

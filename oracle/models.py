@@ -47,18 +47,78 @@ def cnn_step(x: np.ndarray, u: np.ndarray, weights, biases, alpha: float) -> np.
     return (xb + alpha * h[:, 0]).reshape(lead + (H, W))
 
 
-class OracleCNN:
-    """fp64 MatrixDynamics for the CNN surrogate, from a CNNDynamics-like spec."""
+def cnn_step_torch(x: np.ndarray, u: np.ndarray, weights, biases, alpha: float,
+                   chunk: int = 64) -> np.ndarray:
+    """The same fp64 stack as ``cnn_step`` through torch-CPU conv2d, in member chunks (bounded
+    memory), for oracle runs at the benchmarked sizes (C2/C3/C5: 10^2..10^4 members of
+    64x64..128x128).  Pinned to ``cnn_step`` at 1e-12 by tests/test_oracle_golden.py."""
+    import torch
+    import torch.nn.functional as F
 
-    def __init__(self, spec):
+    x = np.asarray(x, dtype=float)
+    u = np.asarray(u, dtype=float)
+    lead = np.broadcast_shapes(x.shape[:-2], u.shape[:-2])
+    H, W = x.shape[-2:]
+    xb = np.broadcast_to(x, lead + (H, W)).reshape(-1, H, W)
+    ub = np.broadcast_to(u, lead + (H, W)).reshape(-1, H, W)
+    ws = [torch.from_numpy(np.asarray(w, float)) for w in weights]
+    bs = [torch.from_numpy(np.asarray(b, float)) for b in biases]
+    out = np.empty_like(xb)
+    for i0 in range(0, xb.shape[0], chunk):
+        h = torch.from_numpy(np.stack([xb[i0:i0 + chunk], ub[i0:i0 + chunk]], axis=1))
+        for k, (w, b) in enumerate(zip(ws, bs)):
+            h = F.conv2d(h, w, b, padding=1)
+            if k < len(ws) - 1:
+                h = torch.tanh(h)
+        out[i0:i0 + chunk] = xb[i0:i0 + chunk] + alpha * h[:, 0].numpy()
+    return out.reshape(lead + (H, W))
+
+
+def cnn_init(widths, seed: int = 0):
+    """The CNN surrogate's seeded random init (w ~ N(0,1)/sqrt(9 C_in), bias ~
+    0.01 N(0,1), numpy default_rng(seed), layer by layer), restated so the reference arm builds
+    its model without the product package.  Equal to dynamics.CNNDynamics's init (test)."""
+    rng = np.random.default_rng(seed)
+    weights, biases = [], []
+    for cin, cout in zip(widths[:-1], widths[1:]):
+        weights.append(rng.standard_normal((cout, cin, 3, 3)) / np.sqrt(9.0 * cin))
+        biases.append(0.01 * rng.standard_normal(cout))
+    return weights, biases
+
+
+class CnnSpec:
+    """Minimal CNNDynamics-like spec (weights, biases, alpha, shapes) for OracleCNN."""
+
+    def __init__(self, rows, cols, widths, alpha=0.1, seed=0):
+        self.widths = tuple(widths)
+        self.weights, self.biases = cnn_init(self.widths, seed)
+        self.alpha = float(alpha)
+        self.state_rows = self.input_rows = int(rows)
+        self.state_cols = int(cols)
+
+    def flops_per_member_step(self) -> int:
+        return self.state_rows * self.state_cols * sum(
+            18 * ci * co for ci, co in zip(self.widths[:-1], self.widths[1:]))
+
+
+class OracleCNN:
+    """fp64 MatrixDynamics for the CNN surrogate, from a CNNDynamics-like spec.
+
+    backend "numpy": explicit einsum taps (``cnn_step``); "torch": torch-CPU fp64 conv2d
+    (``cnn_step_torch``), for the large configurations."""
+
+    def __init__(self, spec, backend: str = "numpy"):
         self.weights = [np.asarray(w, float) for w in spec.weights]
         self.biases = [np.asarray(b, float) for b in spec.biases]
         self.alpha = float(spec.alpha)
         self.state_rows = spec.state_rows
         self.state_cols = spec.state_cols
         self.input_rows = spec.input_rows
+        self.backend = backend
 
     def step(self, x, u):
+        if self.backend == "torch":
+            return cnn_step_torch(x, u, self.weights, self.biases, self.alpha)
         return cnn_step(x, u, self.weights, self.biases, self.alpha)
 
 

@@ -75,6 +75,9 @@ def _lib():
         lib.npyo_standard_normal_words.restype = ctypes.c_int64
         lib.npyo_member_noise.argtypes = [u32p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
                                           ctypes.c_int64, ctypes.c_int64, dp]
+        lib.npyo_member_noise_range.argtypes = [u32p, ctypes.c_int, ctypes.c_uint32,
+                                                ctypes.c_uint32, ctypes.c_int64, ctypes.c_int64,
+                                                ctypes.c_int64, dp]
         lib.npyo_philox_block.argtypes = [u64p, u64p, u64p]
         _LIB = lib
     return _LIB
@@ -117,7 +120,20 @@ def member_normals(seed: int, prefix: Sequence[int], t: int, channel: int, n_mem
         raise ValueError(backend)
     head = np.asarray(head_words(seed, prefix), dtype=np.uint32)
     out = np.empty((n_members, rows * cols), dtype=np.float64)
-    _lib().npyo_member_noise(head.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), len(head),
-                             t, channel, n_members, rows * cols,
-                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    hp = head.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+    lib = _lib()
+
+    def run(i0, i1):  # ctypes releases the GIL: member ranges draw in parallel
+        lib.npyo_member_noise_range(hp, len(head), t, channel, i0, i1 - i0, rows * cols,
+                                    out[i0:].ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+
+    workers = min(os.cpu_count() or 1, 32) if n_members * rows * cols >= (1 << 22) else 1
+    if workers == 1:
+        run(0, n_members)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        cuts = np.linspace(0, n_members, workers + 1).astype(int)
+        with ThreadPoolExecutor(workers) as ex:
+            list(ex.map(lambda k: run(cuts[k], cuts[k + 1]), range(workers)))
     return out.reshape(n_members, rows, cols)

@@ -163,19 +163,24 @@ int64_t npyo_standard_normal_words(const uint64_t key[2], int64_t count, double*
     return (int64_t)(s.ctr[0] - 1) * 4 + s.pos;
 }
 
-/* enks.py:142-144 for members [0, n_members): out (n_members, rows*cols),
+/* enks.py:142-144 for members [member0, member0 + n_members): out (n_members, rows*cols),
  * entropy = head words (seed padded to 4 + prefix words) ++ [i, t, ch]. */
-void npyo_member_noise(const uint32_t* head, int n_head, uint32_t t, uint32_t ch, int64_t n_members,
-                       int64_t count, double* out) {
+void npyo_member_noise_range(const uint32_t* head, int n_head, uint32_t t, uint32_t ch,
+                             int64_t member0, int64_t n_members, int64_t count, double* out) {
     uint32_t ent[64];
     if (n_head > 61) return;
     memcpy(ent, head, sizeof(uint32_t) * (size_t)n_head);
     for (int64_t i = 0; i < n_members; ++i) {
-        ent[n_head] = (uint32_t)i;
+        ent[n_head] = (uint32_t)(member0 + i);
         ent[n_head + 1] = t;
         ent[n_head + 2] = ch;
         uint64_t key[2];
         npyo_seedseq_key(ent, n_head + 3, key);
         npyo_standard_normal(key, count, out + i * count);
     }
+}
+
+void npyo_member_noise(const uint32_t* head, int n_head, uint32_t t, uint32_t ch, int64_t n_members,
+                       int64_t count, double* out) {
+    npyo_member_noise_range(head, n_head, t, ch, 0, n_members, count, out);
 }

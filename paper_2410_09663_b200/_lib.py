@@ -53,6 +53,7 @@ _SIGS = {
                                         _vp, _vp]),
     "enks_member_sum": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _c_i64, _c_int, _vp, _vp, _vp,
                                  _vp, _vp]),
+    "enks_member_sum_rebase": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _c_int, _vp, _c_d, _vp]),
     "enks_member_center_f16pair_t": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _c_i64, _c_int,
                                               _vp, _vp, _vp, _c_i64, _vp, _vp, _vp, _c_i64, _vp,
                                               _vp, _vp, _vp, _c_i64, _vp, _vp]),

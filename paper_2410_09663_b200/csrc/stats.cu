@@ -128,6 +128,18 @@ __global__ void chunk_reduce_kernel(const double* __restrict__ part, const float
     if (amax) amax[e] = mx;
 }
 
+// acc[r, j] += coef * s[r, j], s = src[r, j] (+ src2[r, j], summed in fp32 exactly as the member
+// sums form their shift): converts shifted member sums to absolute ones and back (multi-rank)
+__global__ void sum_rebase_kernel(const float* __restrict__ src, int64_t ld,
+                                  const float* __restrict__ src2, int64_t ld2, int rows, int cols,
+                                  double* __restrict__ acc, double coef) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= (int64_t)rows * cols) return;
+    const int r = (int)(e / cols), j = (int)(e - (int64_t)r * cols);
+    const float s = src2 ? src[r * ld + j] + src2[r * ld2 + j] : src[r * ld + j];
+    acc[e] += coef * (double)s;
+}
+
 // basis row of source row r when rows [skip0, skip1) are not stored in the basis (-1: skipped)
 __device__ __forceinline__ int basis_row(int r, int skip0, int skip1) {
     return r < skip0 ? r : (r >= skip1 ? r - (skip1 - skip0) : -1);
@@ -422,6 +434,16 @@ int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols) {
                                  enks::member_chunks(rows, n_members, cols, 4));
     return nch * (int64_t)rows * cols *
            (int64_t)(sizeof(double) + sizeof(float));
+}
+
+int enks_member_sum_rebase(const float* src, int64_t ld_src, const float* src2, int64_t ld_src2,
+                           int rows, int cols, double* acc, double coef, void* stream) {
+    ENKS_REQUIRE(src && acc, "enks_member_sum_rebase: null pointer");
+    const int64_t rc = (int64_t)rows * cols;
+    if (rc <= 0) return ENKS_OK;
+    enks::sum_rebase_kernel<<<(unsigned)((rc + 255) / 256), 256, 0, enks::as_stream(stream)>>>(
+        src, ld_src, src2, ld_src2, rows, cols, acc, coef);
+    return enks::check_launch("enks_member_sum_rebase");
 }
 
 int enks_member_sum(const float* src, int64_t ld_src, const float* src2, int64_t ld_src2, int rows,

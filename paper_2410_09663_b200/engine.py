@@ -58,6 +58,9 @@ class LocalComm:
     def allreduce_(self, t):
         return t
 
+    def allreduce_many(self, ts):
+        return ts
+
     def allreduce_max_(self, t):
         return t
 
@@ -79,6 +82,23 @@ class TorchComm:
     def allreduce_(self, t):
         self.dist.all_reduce(t, group=self.group)
         return t
+
+    def allreduce_many(self, ts):
+        """Sum-allreduce several tensors as ONE collective: one coalesced NCCL group launch
+        (torch's coalescing manager); other backends issue them back to back."""
+        ts = [t for t in ts if t.numel()]
+        if len(ts) == 1:
+            self.dist.all_reduce(ts[0], group=self.group)
+        elif ts and self.dist.get_backend(self.group) == "nccl":
+            from torch.distributed.distributed_c10d import _coalescing_manager
+
+            with _coalescing_manager(group=self.group, device=ts[0].device):
+                for t in ts:
+                    self.dist.all_reduce(t, group=self.group)
+        else:
+            for t in ts:
+                self.dist.all_reduce(t, group=self.group)
+        return ts
 
     def allreduce_max_(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
@@ -253,6 +273,8 @@ class DeviceSmoother:
         self._bound = None
         self.barrier = None
         self.dev_head = None  # ops.DeviceHead: noise entropy words read from device memory
+        self.record = None    # dict: per-update Sigma_y / Sigma_xy / gain (tests, see _record_step)
+        self._last_stale = False  # `last` lags the newest slice (a predict with no update yet)
         self._basis = basis
         self._explicit = False  # explicit members (replace_members): no derived-U chain
         d, q, K = self.d, self.q, self.K
@@ -317,7 +339,9 @@ class DeviceSmoother:
         self.obs_raw = ops.empty(p, K)        # perturbed observations of the newest slice
         self.acc = ops.zeros(max(d, p), m, dtype=torch.float64)
         self.amax = ops.zeros(max(d, p), m)
-        self.z0 = ops.zeros(max(d, p), m) if self.comm.size > 1 else None
+        self.acc_obs = ops.zeros(p, m, dtype=torch.float64)  # observation sums (fused path)
+        self.amax_obs = ops.zeros(p, m)
+        self._obs_sums_t = -1
         self.ybar = ops.zeros(p, m)
         self.innov = ops.zeros(p, m)
         self.sinv = ops.zeros(p, p)
@@ -347,6 +371,8 @@ class DeviceSmoother:
         self.n_upd = 0
         self.slice0_zero = True
         self._obs_t = -1
+        self._obs_sums_t = -1
+        self._last_stale = False
         self.mean[:d].copy_(x0)
         self.last.copy_(x0[:q].repeat(1, self.Nl))
         if self.pair:
@@ -544,56 +570,70 @@ class DeviceSmoother:
         if out_plus is not None:
             ops.gemm(spec.dense, z, out_plus, beta=1.0, C0=base)
 
-    def _center(self, src, mean_out, anom_out, pair_rows=None, f32_rows=0, skip=(0, 0)):
-        """Member mean (rows x m) and anomalies of `src` (rows x K), shift = global member 0.
+    def _local_sums(self, src, acc, amax=None, src2=None) -> None:
+        """This rank's member sums of src (+ src2) relative to its own first member; under
+        sharding converted to absolute sums (+ n_local * s) ready for the allreduce."""
+        self.ops.member_sum(src, self.Nl, self.m, None, acc, amax, src2=src2)
+        if self.comm.size > 1:
+            self.ops.member_sum_rebase(src, self.m, acc, float(self.Nl), src2=src2)
+
+    def _global_sums(self, items) -> None:
+        """ONE collective for every (src, acc, src2) of `items`, then each acc back to sums
+        relative to this rank's first member (-N * s) -- what the centring kernels expect with
+        z0 = NULL.  No broadcast of global member 0 (enks_member_sum_rebase)."""
+        if self.comm.size <= 1:
+            return
+        self.comm.allreduce_many([acc for _, acc, _ in items])
+        for src, acc, src2 in items:
+            self.ops.member_sum_rebase(src, self.m, acc, -float(self.N), src2=src2)
+
+    def _center(self, src, mean_out, anom_out, pair_rows=None, f32_rows=0, skip=(0, 0),
+                obs_sums=False):
+        """Member mean (rows x m) and anomalies of `src` (rows x K) relative to each rank's first
+        member (identical members give exactly zero anomalies at any N and any rank count).
 
         pair_rows=(which, r0): write the anomalies straight into the fp16-pair basis at row r0
-        (plus an fp32 copy of the first f32_rows rows into anom_out)."""
-        ops, comm, rows = self.ops, self.comm, src.shape[0]
+        (plus an fp32 copy of the first f32_rows rows into anom_out).  obs_sums: also form this
+        step's observation sums (slice [x; u] + [v_x; v_u], enks.py:194-200, 231) in the same
+        collective, for the fused observation centring of update()."""
+        ops, rows = self.ops, src.shape[0]
         if rows > self.acc.shape[0]:
             self.acc = ops.zeros(rows, self.m, dtype=torch.float64)
             self.amax = ops.zeros(rows, self.m)
-            if self.z0 is not None:
-                self.z0 = ops.zeros(rows, self.m)
         acc = self.acc[:rows]
-        z0 = None
-        if comm.size > 1:
-            z0 = self.z0[:rows]
-            if comm.rank == 0:
-                z0.copy_(src[:, :self.m])
-            comm.broadcast_(z0, src=0)
+        amax = None if pair_rows is None else self.amax[:rows]
+        self._local_sums(src, acc, amax)
+        items = [(src, acc, None)]
+        if obs_sums:
+            p = self.p
+            self._local_sums(self.slice_raw[:p], self.acc_obs, self.amax_obs, src2=self.v_raw)
+            items.append((self.slice_raw[:p], self.acc_obs, self.v_raw))
+            self._obs_sums_t = self.t + 1
+        self._global_sums(items)
         if pair_rows is None:
-            ops.member_sum(src, self.Nl, self.m, z0, acc)
-            comm.allreduce_(acc)
-            ops.member_center(src, self.Nl, self.m, z0, acc, self.N, mean=mean_out, anom=anom_out)
+            ops.member_center(src, self.Nl, self.m, None, acc, self.N, mean=mean_out,
+                              anom=anom_out)
             return
         which, r0 = pair_rows
-        amax = self.amax[:rows]
-        ops.member_sum(src, self.Nl, self.m, z0, acc, amax)
-        comm.allreduce_(acc)
         h, l, inv = (self.Ah, self.Al, self.a_inv) if which == "A" else (self.Yh, self.Yl,
                                                                         self.y_inv)
         hr = rows - (skip[1] - skip[0])  # basis rows written
-        ops.member_center_f16pair(src, self.Nl, self.m, z0, acc, amax, self.N, mean_out,
+        ops.member_center_f16pair(src, self.Nl, self.m, None, acc, amax, self.N, mean_out,
                                   h[r0:r0 + hr], l[r0:r0 + hr], inv[r0:r0 + hr],
                                   f32=anom_out, rows_f32=f32_rows, skip=skip)
 
     def _center_obs_fused(self, tau) -> None:
         """Centre y = [x; u] + [v_x; v_u] (never materialised) into the basis rows of Yc_tau and
-        the transposed planes of the newest-slice shift; y_bar = member mean (enks.py:231-232)."""
-        ops, comm, p, m = self.ops, self.comm, self.p, self.m
+        the transposed planes of the newest-slice shift; y_bar = member mean (enks.py:231-232).
+        The member sums normally come from predict's collective (obs_sums)."""
+        ops, p, m = self.ops, self.p, self.m
         src, src2 = self.slice_raw[:p], self.v_raw
-        z0 = None
-        if comm.size > 1:
-            z0 = self.z0[:p]
-            if comm.rank == 0:
-                torch.add(src[:, :m], src2[:, :m], out=z0)
-            comm.broadcast_(z0, src=0)
-        acc, amax = self.acc[:p], self.amax[:p]
-        ops.member_sum(src, self.Nl, m, z0, acc, amax, src2=src2)
-        comm.allreduce_(acc)
+        acc, amax = self.acc_obs, self.amax_obs
+        if self._obs_sums_t != tau:
+            self._local_sums(src, acc, amax, src2=src2)
+            self._global_sums([(src, acc, src2)])
         r0 = (tau - 1) * p
-        ops.member_center_f16pair_t(src, src2, self.Nl, m, z0, acc, amax, self.N, self.ybar,
+        ops.member_center_f16pair_t(src, src2, self.Nl, m, None, acc, amax, self.N, self.ybar,
                                     self.Yh[r0:r0 + p], self.Yl[r0:r0 + p], self.y_inv[r0:r0 + p],
                                     self.ycT_h, self.ycT_l, self.ycT_inv)
 
@@ -607,6 +647,14 @@ class DeviceSmoother:
         ops, n, l, d = self.ops, self.n, self.l, self.d
         head = self._head(streams)
         sr, ob = self.slice_raw, self.obs_raw
+        if self.t >= 1 and self.n_upd < self.t:
+            # the previous step had no update (predict twice in a row, as the reference allows):
+            # its observation block and gain column hold no information -- zero them so the
+            # later cross moments / corrections read exact zeros, not stale or uninitialised rows
+            self._zero_obs_block(self.t)
+        if self._last_stale:  # newest members are the un-updated predicted slice [f; u + w]
+            self.last.copy_(sr[:self.q])
+        self._last_stale = True
         if self.fused_noise:
             # W (enks.py:165-168) and this step's observation noise V_X, V_U (enks.py:194-200,
             # drawn at t = tau with the same substream ids update() would use) in one launch on a
@@ -649,7 +697,8 @@ class DeviceSmoother:
             # (derived-U chain: the U rows stay out of the basis; A_new keeps them in fp32)
             self._center(sr, self.mean[tau * d:(tau + 1) * d], self.A_new,
                          pair_rows=("A", tau * self.ds), f32_rows=self.q,
-                         skip=(n, n + l) if self.chain else (0, 0))
+                         skip=(n, n + l) if self.chain else (0, 0),
+                         obs_sums=self.obs_fused and self.fused_noise)
         else:
             self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d])
         self.t = tau
@@ -658,9 +707,15 @@ class DeviceSmoother:
     def update(self, y_ref_dev, streams) -> None:
         """enks.py:212-248 restated on the append-only basis (module docstring)."""
         ops, comm = self.ops, self.comm
+        if self.t < 1:
+            self._update_t0(y_ref_dev, streams)
+            return
+        if self.n_upd >= self.t:
+            # a second update at the same t (the reference allows it: enks.py:212-253 shifts the
+            # members again): the append-only basis holds one observation block per slice, so
+            # re-seed from the explicit members first (slow path, exact)
+            self._reseed_from_members()
         n, l, d, p, tau = self.n, self.l, self.d, self.p, self.t
-        if tau < 1:
-            raise RuntimeError("update before the first predict")
         head = self._head(streams)
         sr, ob = self.slice_raw, self.obs_raw
         # perturbed observations [x + v_x; u + v_u]  (enks.py:194-200)
@@ -701,8 +756,7 @@ class DeviceSmoother:
                 ops.gemm_f16pair(self.Yh[:(tau - 1) * p], self.Yl[:(tau - 1) * p],
                                  self.y_inv[:(tau - 1) * p], yh, yl, yi, PY[:(tau - 1) * p],
                                  tag="cross")
-                comm.allreduce_(PY[:(tau - 1) * p])
-            comm.allreduce_(PA)
+            comm.allreduce_many([PY[:(tau - 1) * p], PA])  # one collective for the rest of P
         else:
             if self.use_tc:
                 ops.tf32_split(yc, self.yc_hi, self.yc_lo)
@@ -711,8 +765,7 @@ class DeviceSmoother:
             else:
                 ops.gemm(self.Abuf[a0:rows_a], yc, PA, trans_b=True, tag="cross")
                 ops.gemm(self.Ybuf[:tau * p], yc, PY, trans_b=True, tag="cross")
-            comm.allreduce_(PA)
-            comm.allreduce_(PY)
+            comm.allreduce_many([PA, PY])
             # Sigma_y^{-1} with the reference's jitter fallback (enks.py:234-244)
             self._spd_async(None, PY[(tau - 1) * p:], scale)
 
@@ -738,6 +791,8 @@ class DeviceSmoother:
                          alpha=-1.0, beta=1.0, C0=PA, tri=tri)
             self._join_side(side)
             ops.gemm(PA, self.sinv, gcol, alpha=scale)
+        if self.record is not None:
+            self._record_step(tau, a0, rows_a, scale)
         # mean_s += G_{tau,s} (y_ref - y_bar)   (enks.py:247-248 on the mean)
         self.n_upd = tau
         ops.sub(y_ref_dev, self.ybar, self.innov)
@@ -774,6 +829,94 @@ class DeviceSmoother:
         else:
             ops.gemm(g_tt, yc, self.last, alpha=-1.0, beta=1.0, C0=a_new[:q],
                      bias=self.mean[r0:r0 + q], bias_cols=self.m)
+        self._last_stale = False
+
+    def _zero_obs_block(self, tau: int) -> None:
+        """Zero the basis rows of Yc_tau and the gain column block of step tau."""
+        p = self.p
+        r0, r1 = (tau - 1) * p, tau * p
+        if self.pair:
+            self.Yh[r0:r1].zero_()
+            self.Yl[r0:r1].zero_()
+            self.y_inv[r0:r1].fill_(1.0)
+        else:
+            self.Ybuf[r0:r1].zero_()
+        self.G[:, r0:r1].zero_()
+
+    def _update_t0(self, y_ref_dev, streams) -> None:
+        """update() before the first predict (enks.py:212-253 at t = 0): the trajectory is slice 0
+        alone.  Observation noise is drawn with t = 0 (enks.py:224); Sigma_y goes through the
+        jittered Cholesky (jitter_events / LinAlgError as the reference); the gain is
+        Sigma_xy Sigma_y^-1 with Sigma_xy = (lam/N) A_0 Yc^T, which is exactly zero for the
+        identical copies of init_ensemble (enks.py:108-110), so only explicit members move.
+        Rare, small path: fp32 SIMT GEMMs, members re-seeded afterwards."""
+        ops, comm = self.ops, self.comm
+        n, l, d, p, q, K = self.n, self.l, self.d, self.p, self.q, self.K
+        head = self._head(streams)
+        self.slice_raw.copy_(self.members_device()[:d])  # slice 0 [x; u; dU] of every member
+        sr, ob = self.slice_raw, self.obs_raw
+        self._noise(self.noise_vx, head, 0, CH_VX, n, base=sr[:n], out_plus=ob[:n])
+        self._noise(self.noise_vu, head, 0, CH_VU, l, base=sr[n:q], out_plus=ob[n:q])
+        self._barrier_row(head, 0)
+        self._obs_t = -1
+        yc = ops.empty(p, K)
+        self._center(ob, self.ybar, yc)
+        scale = self.lam / self.N
+        sy = ops.empty(p, p)
+        ops.gemm(yc, yc, sy, trans_b=True)
+        comm.allreduce_(sy)
+        ops.spd_inverse(sy, scale, self.sinv, self.status, self.jitter)
+        if self.slice0_zero:
+            return
+        a0 = self.deviations()[:d]
+        sxy = ops.empty(d, p)
+        ops.gemm(a0, yc, sxy, trans_b=True)
+        comm.allreduce_(sxy)
+        g = ops.empty(d, p)
+        ops.gemm(sxy, self.sinv, g, alpha=scale)
+        ops.sub(y_ref_dev, self.ybar, self.innov)
+        mean0 = self.mean[:d].clone()
+        ops.gemm(g, self.innov, mean0, beta=1.0, C0=mean0)
+        # members = mean' + A_0 - G Yc
+        new = ops.empty(d, K)
+        ops.gemm(g, yc, new, alpha=-1.0, beta=1.0, C0=a0, bias=mean0, bias_cols=self.m)
+        self._replace_members_dev(new, 0)
+
+    def _reseed_from_members(self) -> None:
+        """Re-seed the representation from the current explicit members (device, exact)."""
+        self._replace_members_dev(self.members_device(), self.t)
+
+    # ------------------------------------------------------------ per-step record (tests)
+    def _expand_rows(self, compact: np.ndarray, a0: int) -> np.ndarray:
+        """Rows of slices a0/ds..t in the basis layout -> full (T d, cols) rows of slices 0..t
+        (zero rows for a skipped slice 0; U rows = prefix sums of dU under the derived-U chain)."""
+        ds, d, n, l, t = self.ds, self.d, self.n, self.l, self.t
+        cols = compact.shape[1]
+        full_c = np.zeros(((t + 1) * ds, cols))
+        full_c[a0:] = compact
+        if not self.chain:
+            return full_c
+        cv = full_c.reshape(t + 1, ds, cols)
+        out = np.zeros((t + 1, d, cols))
+        out[:, :n] = cv[:, :n]
+        out[:, n + l:] = cv[:, n:]
+        out[:, n:n + l] = np.cumsum(cv[:, n:], axis=0)
+        return out.reshape((t + 1) * d, cols)
+
+    def _record_step(self, tau: int, a0: int, rows_a: int, scale: float) -> None:
+        """Append this update's Sigma_y (p x p, symmetrised as enks.py:234), Sigma_xy
+        (T d x p, enks.py:235-236) and gain (T d x p, enks.py:246) as fp64 host arrays to
+        ``self.record`` -- the same keys as the oracle's ``record=`` hook.  Test-only: syncs."""
+        if self.ops.device.type == "cuda":
+            torch.cuda.synchronize(self.ops.device)
+        p = self.p
+        sy = scale * self.PY[(tau - 1) * p:tau * p].double().cpu().numpy()
+        S = scale * self.PA[a0:rows_a].double().cpu().numpy()
+        G = self.G[a0:rows_a, (tau - 1) * p:tau * p].double().cpu().numpy()
+        rec = self.record
+        rec.setdefault("sigma_y", []).append(0.5 * (sy + sy.T))
+        rec.setdefault("sigma_xy", []).append(self._expand_rows(S, a0))
+        rec.setdefault("gain", []).append(self._expand_rows(G, a0))
 
     # ------------------------------------------------------------ readback
     def deviations(self, rows: int | None = None):
@@ -809,21 +952,28 @@ class DeviceSmoother:
 
     def mean_host(self) -> np.ndarray:
         R = (self.t + 1) * self.d
-        return self.mean[:R].double().cpu().numpy()
+        return self.ops.to_host(self.mean[:R])
 
     def jitter_events(self) -> int:
-        return int(self.jitter.item())
+        return int(self.ops.read_scalar(self.jitter))
 
     def check_status(self) -> None:
         fc = getattr(self, "forecast", None)
         if fc is not None and fc.kind == "burgers":
             fc.check_cfl(self.comm)
-        if int(self.status.item()) != 0:
+        if int(self.ops.read_scalar(self.status)) != 0:
             raise np.linalg.LinAlgError("observation covariance not positive definite even "
                                         "after jitter")
 
     def replace_members(self, members_local: np.ndarray, t: int) -> None:
         """Reset the representation to explicit members (local shard, (Nl, (t+1)d, m))."""
+        ops, d = self.ops, self.d
+        R = (int(t) + 1) * d
+        M = np.asarray(members_local, dtype=float).transpose(1, 0, 2).reshape(R, self.K)
+        self._replace_members_dev(ops.to_device(M), t)
+
+    def _replace_members_dev(self, Mdev, t: int) -> None:
+        """replace_members for a device tensor in the member-column layout ((t+1) d x K)."""
         ops, d = self.ops, self.d
         self._obs_t = -1
         self.t = 0
@@ -834,8 +984,6 @@ class DeviceSmoother:
         self._grow(max(t, 1))
         self.t = int(t)
         R = (self.t + 1) * d
-        M = np.asarray(members_local, dtype=float).transpose(1, 0, 2).reshape(R, self.K)
-        Mdev = ops.to_device(M)
         self.G.zero_()
         anom = ops.empty(R, self.K)
         self._center(Mdev, self.mean[:R], anom)
@@ -849,3 +997,4 @@ class DeviceSmoother:
         self.slice0_zero = not x0_spread
         last = Mdev[self.t * d:self.t * d + self.q]
         self.last.copy_(last)
+        self._last_stale = False

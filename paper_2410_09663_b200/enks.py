@@ -233,9 +233,6 @@ def update(ens: TrajectoryEnsemble, y_ref: np.ndarray, vs, streams,
     obs_shape = (vs.obs_rows, eng.m)
     if y_ref.shape != obs_shape:
         raise ValueError(f"y_ref shape {y_ref.shape} != observation {obs_shape}")
-    if eng.t < 1:
-        raise NotImplementedError("update() before the first predict() is not supported on "
-                                  "the device path")
     eng.bind(vs)
     eng.update(_device_yref(eng, y_ref), streams)
     eng.check_status()
@@ -326,8 +323,9 @@ def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
     if graph and not track_cov and n_members >= 2 and torch.cuda.is_available() and \
             _comm().size == 1:  # (collectives are not captured: multi-rank runs stay eager)
         g = _graph_for(x0, vs, h, n_members, streams)
-        g.x0.copy_(torch.from_numpy(np.asarray(x0.packed, dtype=np.float32)), non_blocking=False)
-        g.y_refs.copy_(torch.from_numpy(np.ascontiguousarray(y_refs, dtype=np.float32)))
+        ops = g.eng.ops
+        ops.copy_from_host(g.x0, np.asarray(x0.packed, dtype=np.float32))
+        ops.copy_from_host(g.y_refs, np.ascontiguousarray(y_refs, dtype=np.float32))
         eng = g.replay()
         eng.check_status()
         return eng.mean_host().reshape(h + 1, eng.d, eng.m), None

@@ -71,6 +71,8 @@ class DeviceOps:
         # (enks.HorizonGraph) may still hold their addresses
         self._retired = []
         self.launches = 0  # kernel launches issued through the C-ABI (bench's gpu_launches)
+        self.h2d_bytes = 0  # host<->device bytes moved by the product (bench's e2e accounting)
+        self.d2h_bytes = 0
         self.profile = None  # list -> (tag, start_event, end_event, algorithmic_flops) per tagged op
 
     # -- memory -----------------------------------------------------------
@@ -82,7 +84,24 @@ class DeviceOps:
 
     def to_device(self, arr, dtype=None):
         arr = np.require(arr, requirements=["C", "W"])  # (copies read-only broadcast views)
-        return torch.as_tensor(arr, dtype=dtype or self.dtype).to(self.device)
+        t = torch.as_tensor(arr, dtype=dtype or self.dtype)
+        self.h2d_bytes += t.numel() * t.element_size()
+        return t.to(self.device)
+
+    def copy_from_host(self, dst, arr) -> None:
+        """dst (device) <- host array, converted to dst's dtype on the host first."""
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dst.dtype)
+        self.h2d_bytes += t.numel() * t.element_size()
+        dst.copy_(t)
+
+    def to_host(self, t) -> np.ndarray:
+        """Device tensor -> fp64 NumPy (copied in its own dtype, widened on the host)."""
+        self.d2h_bytes += t.numel() * t.element_size()
+        return t.cpu().double().numpy()
+
+    def read_scalar(self, t):
+        self.d2h_bytes += t.element_size()
+        return t.item()
 
     def _workspace(self, nbytes: int) -> int:
         if nbytes <= 0:
@@ -190,6 +209,13 @@ class DeviceOps:
             _lib.call("enks_member_sum", _p(src), _ld(src), _p(src2),
                       _ld(src2) if src2 is not None else 0, rows, int(n_members), int(cols),
                       _p(z0), _p(acc), _p(amax), ws, self._stream())
+
+    def member_sum_rebase(self, src, cols, acc, coef, src2=None):
+        """acc += coef * (local member 0 of src (+ src2)): shifted <-> absolute member sums."""
+        self.launches += 1
+        _lib.call("enks_member_sum_rebase", _p(src), _ld(src), _p(src2),
+                  _ld(src2) if src2 is not None else 0, int(acc.shape[0]), int(cols), _p(acc),
+                  float(coef), self._stream())
 
     def member_center_f16pair_t(self, src, src2, n_members, cols, z0, acc, amax, n_total, mean, h,
                                 l, inv_scale, th, tl, t_inv):

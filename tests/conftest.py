@@ -11,7 +11,7 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
-    config.addinivalue_line("markers", "reference: needs /root/reference importable (this container only)")
+    config.addinivalue_line("markers", "reference: drives the product with the installed, unmodified reference (baseline/_ref, built by __graft_entry__.build())")
 
 
 @pytest.fixture(scope="session")

@@ -96,6 +96,15 @@ class CpuOps:
         arr = np.require(arr, requirements=["C", "W"])
         return torch.as_tensor(arr, dtype=dtype or self.dtype).clone()
 
+    def copy_from_host(self, dst, arr):
+        dst.copy_(torch.from_numpy(np.ascontiguousarray(arr)).to(dst.dtype))
+
+    def to_host(self, t):
+        return t.double().numpy()
+
+    def read_scalar(self, t):
+        return t.item()
+
     def noise_fill(self, head, t, ch, member0, n_members, rows, cols, diag=None, out=None,
                    base=None, out_plus=None):
         out_z = np.empty((n_members, rows * cols))
@@ -137,6 +146,10 @@ class CpuOps:
         acc.copy_((s - shift[:, None, :]).sum(dim=1))
         if amax is not None:
             amax.copy_((s - shift[:, None, :]).abs().amax(dim=1))
+
+    def member_sum_rebase(self, src, cols, acc, coef, src2=None):
+        s = src[:acc.shape[0], :cols] + (src2[:acc.shape[0], :cols] if src2 is not None else 0)
+        acc.add_(coef * s)
 
     def member_center(self, src, n_members, cols, z0, acc, n_total, mean=None, anom=None):
         s = src.reshape(src.shape[0], n_members, cols)

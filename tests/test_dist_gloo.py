@@ -88,3 +88,47 @@ def test_two_rank_sharding_matches_single_rank(kind, basis, tmp_path):
     assert np.abs(got["mean"] - ref.mean_host()).max() < 1e-10 * scale
     assert np.abs(got["members"] - ref.members_device().numpy()).max() < 1e-10 * scale
     assert int(got["jitter"]) == ref.jitter.item()
+
+
+def _count_worker(rank, world, port, out):
+    sys.path[:0] = [os.path.dirname(HERE), HERE]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2410_09663_b200.engine import TorchComm
+
+    class Counting(TorchComm):
+        calls = []
+
+        def allreduce_(self, t):
+            self.calls.append(("allreduce", t.numel()))
+            return super().allreduce_(t)
+
+        def allreduce_many(self, ts):
+            self.calls.append(("allreduce_many", sum(t.numel() for t in ts)))
+            return super().allreduce_many(ts)
+
+        def broadcast_(self, t, src=0):
+            self.calls.append(("broadcast", t.numel()))
+            return super().broadcast_(t, src)
+
+    comm = Counting()
+    eng = _run("cnn", comm, "f16pair")
+    if rank == 0:
+        np.savez(out, n=len(comm.calls), h=3, fused=int(eng.obs_fused),
+                 kinds=np.array([c[0] for c in comm.calls]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_collectives_per_step(tmp_path):
+    """three collectives per predict+update under member sharding (fused noise and
+    observation path) -- the slice + observation member sums, the Sigma_y block, and the rest of
+    the cross moments -- and no broadcast (each rank centres relative to its own first member)."""
+    out = str(tmp_path / "c.npz")
+    mp.spawn(_count_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    assert int(got["fused"]) == 1
+    assert "broadcast" not in set(got["kinds"].tolist())
+    assert int(got["n"]) == 3 * int(got["h"])

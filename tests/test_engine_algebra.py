@@ -132,3 +132,65 @@ def test_engine_rejects_host_only_constraint(pm):
     eng = DeviceSmoother(CpuOps(), x0.packed, x0.n, x0.l, 8, 1.0 / x0.m)
     with pytest.raises(TypeError, match="LinearConstraint or BoxConstraint"):
         eng.bind(vs)
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_engine_record_equals_oracle_record(pm, pair):
+    """The per-update record hook (Sigma_y, Sigma_xy, gain on the reference's full T d rows,
+    U rows re-expanded from the derived-U chain) equals the oracle's record= output."""
+    _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(5), n=6, l=3, m=4)
+    y = vs.reference_observation()
+    h, N, seed = 4, 16, 9
+    orec = {}
+    enks_oracle.oracle_smooth(x0, y, vs, h, N, seed=seed, backend="c", record=orec)
+    ops = CpuOps()
+    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, N, 1.0 / np.trace(vs.shared_col_cov),
+                         capacity=h, basis="f16pair" if pair else "fp32")
+    eng.record = {}
+    st = pm.matvar.NoiseStreams(seed=seed)
+    yd = ops.to_device(np.broadcast_to(y, (h,) + y.shape).copy())
+    for k in range(h):
+        eng.predict(vs, st)
+        eng.update(yd[k], st)
+    assert eng.chain == pair
+    for key in ("sigma_y", "sigma_xy", "gain"):
+        assert len(eng.record[key]) == h
+        for a, b in zip(eng.record[key], orec[key]):
+            assert a.shape == b.shape, key
+            assert np.abs(a - b).max() < 1e-10 * np.abs(b).max(), key
+
+
+@pytest.mark.parametrize("pair", [False, True])
+@pytest.mark.parametrize("spread", [False, True])
+def test_engine_irregular_update_sequences_equal_oracle(pm, pair, spread):
+    """update() at t = 0 (before any predict) and a second update at the same t, as the
+    reference allows (enks.py:212-253): identical copies (gain exactly zero at t = 0) and
+    explicit members with spread at t = 0 (the slice-0 gain moves them)."""
+    _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(21), n=5, l=3, m=4)
+    y = vs.reference_observation()
+    N, seed = 16, 4
+    o = enks_oracle.oracle_init(x0.packed, x0.n, x0.l, N)
+    ops = CpuOps()
+    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, N, o.lam, capacity=2,
+                         basis="f16pair" if pair else "fp32")
+    if spread:
+        o.members = o.members + 0.3 * np.random.default_rng(1).standard_normal(o.members.shape)
+        o.mean = o.members.mean(axis=0)
+        eng.replace_members(o.members, 0)
+    eng.bind(vs)
+    st = pm.matvar.NoiseStreams(seed=seed)
+    yd = ops.to_device(y)
+    seq = ["u", "p", "u", "u", "p", "u", "p", "p", "u"]
+    for op in seq:
+        if op == "p":
+            enks_oracle.oracle_predict(o, vs, seed, backend="c")
+            eng.predict(vs, st)
+        else:
+            enks_oracle.oracle_update(o, y, vs, seed, backend="c")
+            eng.update(yd, st)
+        members = eng.members_device().numpy().reshape(eng.t + 1, eng.d, N, x0.m)
+        members = members.reshape((eng.t + 1) * eng.d, N, x0.m).transpose(1, 0, 2)
+        assert eng.t == o.t
+        assert np.abs(members - o.members).max() < 1e-10 * np.abs(o.members).max(), op
+        assert np.abs(eng.mean_host() - o.mean).max() < 1e-10 * np.abs(o.mean).max(), op
+    assert eng.jitter.item() == o.jitter_events

@@ -101,3 +101,32 @@ def test_oracle_burgers_horizon_matches_reference_golden(pm, mode):
     ovs = pm.virtualsys.build_virtual_system(OracleBurgers(pr.model), pr.vs.weights)
     out, _, _ = enks_oracle.oracle_smooth(pr.x0, pr.y_ref, ovs, pr.H, pr.N, seed=2, backend="c")
     np.testing.assert_allclose(out, gold["mean"], rtol=1e-12, atol=1e-12)
+
+
+def test_oracle_cnn_torch_backend_matches_einsum(pm):
+    """The torch-CPU fp64 conv backend (used for oracle runs at C2/C3/C5 sizes) equals the
+    explicit-tap restatement, including member chunking."""
+    from oracle.models import cnn_step, cnn_step_torch
+
+    pr = problems.make_cnn_problem(pm, "C1", size=24, widths=(2, 32, 32, 1))
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((70, 24, 24))
+    u = rng.standard_normal((70, 24, 24))
+    ref = cnn_step(x, u, pr.model.weights, pr.model.biases, pr.model.alpha)
+    got = cnn_step_torch(x, u, pr.model.weights, pr.model.biases, pr.model.alpha, chunk=16)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+    gold = _load("cnn_c1_16")
+    pr = problems.make_cnn_problem(pm, "C1", size=16, n_members=24, horizon=3)
+    ovs = pm.virtualsys.build_virtual_system(OracleCNN(pr.model, backend="torch"), pr.vs.weights)
+    out, _, _ = enks_oracle.oracle_smooth(pr.x0, pr.y_ref, ovs, pr.H, pr.N, seed=1, backend="c")
+    np.testing.assert_allclose(out, gold["mean"], rtol=1e-12, atol=1e-12)
+
+
+def test_oracle_cnn_init_equals_product_init(pm):
+    from oracle.models import CnnSpec
+
+    prod = pm.dynamics.CNNDynamics(rows=8, cols=8, widths=(2, 32, 32, 1), alpha=0.1, seed=0)
+    spec = CnnSpec(8, 8, (2, 32, 32, 1))
+    for a, b in zip(prod.weights + prod.biases, spec.weights + spec.biases):
+        assert np.array_equal(a, b)
+    assert spec.flops_per_member_step() == prod.flops_per_member_step()
