@@ -68,6 +68,18 @@ def _peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def _tf32_peak():
+    """Measured cuBLAS TF32 peak (tools/tf32_peak.py, committed under profiles/), or None."""
+    for rnd in ("r02",):
+        path = os.path.join(ROOT, "profiles", rnd, "tf32_peak.json")
+        if os.path.exists(path):
+            with open(path) as f:
+                d = json.load(f)
+            d["source"] = os.path.relpath(path, ROOT)
+            return d
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -393,17 +405,30 @@ def run_ours(args):
     kinds = {"cross": ("tensor", "TFLOP/s"), "forecast": ("tensor", "TFLOP/s"),
              "correction": ("tensor", "TFLOP/s"), "gain": ("tensor", "TFLOP/s"),
              "mean": ("tensor", "TFLOP/s"),
-             "shift": ("tensor", "TFLOP/s"), "noise": ("issue", "Gnormal/s"), "stats": ("hbm", "GB/s"),
+             "shift": ("hbm", "GB/s"), "noise": ("issue", "Gnormal/s"), "stats": ("hbm", "GB/s"),
              "gain_solve": ("latency", "TFLOP/s")}
+    # the newest-slice shift last = C0 + bias - G_tt Yc^T streams C0 (q x K fp32), the transposed
+    # Yc pair planes (K x p, 2 x fp16) and writes last (q x K fp32): HBM-bound, reported in bytes
+    q, K = pr.n + pr.l, pr.N * pr.m
+    shift_bytes = (4 * q * K + 4 * K * (pr.n + pr.l) + 4 * q * K) * h
+    tf32 = _tf32_peak()
+    three_tf32 = {"forecast", "correction", "gain", "mean"}  # 3xTF32 MMAs (cnn_tc.cu, gemm_tc.cu)
     kernels = {}
     for tag, (t, w, cnt) in sorted(fam.items(), key=lambda kv: -kv[1][0]):
         bound, unit = kinds.get(tag, ("?", "?"))
+        if tag == "shift":
+            w = shift_bytes * prof_steps
         rate = w / max(t, 1e-12) / (1e12 if unit == "TFLOP/s" else 1e9)
         pk = peak if bound == "tensor" else (hbm if bound == "hbm" else None)
         kernels[tag] = {"ms_per_horizon": t / prof_steps * 1e3,
                         "share": t / prof_steps / (elapsed / args.steps),
                         "launches": cnt // max(prof_steps, 1), "achieved": rate, "unit": unit,
                         "bound": bound, "peak": pk, "frac": (rate / pk) if pk else None}
+        if tag in three_tf32 and tf32:
+            # algorithmic flops against the 3xTF32 ceiling (three TF32 MMAs per product)
+            kernels[tag]["peak_3xtf32"] = tf32["tf32_tflops_sustained"] / 3.0
+            kernels[tag]["frac_3xtf32"] = rate / kernels[tag]["peak_3xtf32"]
+            kernels[tag]["peak_3xtf32_source"] = tf32["source"]
     if "forecast" in fam:
         kernels["forecast"]["member_steps_per_s"] = pr.N * h * prof_steps / fam["forecast"][0]
 

@@ -457,12 +457,7 @@ int configure_spd(size_t smem) {
 }
 
 int spd_debug() {
-    static int debug = -1;
-    if (debug < 0) {
-        const char* e = getenv("ENKS_SPD_DEBUG");
-        debug = e ? atoi(e) : 0;
-    }
-    return debug;
+    return debug_knob("ENKS_SPD_DEBUG", 0);  // phase switches: debug builds only
 }
 
 // inv = S^{-1} (p <= kMaxP) with the one-CTA kernel: single = 1 -> one attempt, *flag = 1 on a

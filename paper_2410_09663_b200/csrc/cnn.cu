@@ -177,8 +177,9 @@ int enks_cnn_max_width(void) { return enks::kMaxWidth; }
 
 int64_t enks_cnn_ws_bytes(int n_layers, const int* widths, int rows, int cols, int64_t n_members) {
     if (!widths || n_layers < 1 || n_members <= 0) return 0;
-    const char* fe = getenv("ENKS_CNN_FUSED");
-    if (!(fe && fe[0] == '0') && enks::cnn3_tc_applicable(n_layers, widths, rows, cols)) return 0;
+    if (enks::env_knob("ENKS_CNN_FUSED", 1) != 0 &&
+        enks::cnn3_tc_applicable(n_layers, widths, rows, cols))
+        return 0;
     if (!enks::cnn_deep_applicable(n_layers, widths, rows, cols)) return 0;
     const int64_t per = enks::cnn_deep_member_bytes(rows, cols);
     const int64_t cap = (4LL << 30) / per;  // member chunks of <= 4 GiB of activations
@@ -204,10 +205,9 @@ int enks_cnn_forward_ws(int n_layers, const int* widths, const float* weights,
                  "enks_cnn_forward: widths must start at 2 ([X, U]) and end at 1");
     if (n_members <= 0 || rows <= 0 || cols <= 0) return ENKS_OK;
     {
-        const char* e = getenv("ENKS_CNN_TC");
-        const bool allow = !(e && e[0] == '0');
-        const char* fe = getenv("ENKS_CNN_FUSED");
-        const bool fused_ok = !(fe && fe[0] == '0');
+        // tuning: tcgen05 kernels vs the SIMT one (same results to rounding), read once
+        const bool allow = env_knob("ENKS_CNN_TC", 1) != 0;
+        const bool fused_ok = env_knob("ENKS_CNN_FUSED", 1) != 0;
         if (allow && fused_ok && cnn3_tc_applicable(n_layers, widths, rows, cols))
             return cnn3_tc_forward(weights, biases, alpha, x, ldx, u, ldu, out, ldo, rows, cols, n_members,
                                    as_stream(stream));

@@ -494,8 +494,7 @@ int cnn_deep_forward(int n_layers, const float* weights, const float* biases, fl
         }
         configured = true;
     }
-    const char* dbg = getenv("ENKS_CNN_DEBUG");
-    const int debug = dbg ? atoi(dbg) : 0;
+    const int debug = debug_knob("ENKS_CNN_DEBUG", 0);
     // weight / bias offsets per layer
     int woff[16], boff[16];
     {
@@ -539,8 +538,7 @@ int cnn_deep_forward(int n_layers, const float* weights, const float* biases, fl
             t1l = tl;
         }
         {
-            const char* le = getenv("ENKS_DEEP_LAST");
-            if ((le && le[0] == '0') || cols > 1024 || cols % 32)
+            if (env_knob("ENKS_DEEP_LAST", 1) == 0 || cols > 1024 || cols % 32)
                 deep_last_kernel<<<pgrid, DW, 0, st>>>(t0h, t0l, weights + woff[n_layers - 1],
                                                        biases + boff[n_layers - 1], alpha, x, ldx,
                                                        out, ldo, rows, cols, m0);

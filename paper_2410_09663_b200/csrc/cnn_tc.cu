@@ -808,10 +808,8 @@ int cnn3_tc_forward_nz(const float* weights, const float* biases, float alpha, c
     a.n_members = (a.cols_total + W - 1) / W;
     n_members = a.n_members;
     {
-        const char* e = getenv("ENKS_CNN_DEBUG");
-        a.debug = e ? atoi(e) : 0;
-        const char* pe = getenv("ENKS_CNN_PRODUCTS");
-        a.products = (pe && atoi(pe) == 2) ? 2 : 3;
+        a.debug = debug_knob("ENKS_CNN_DEBUG", 0);  // role switches: debug builds only
+        a.products = debug_knob("ENKS_CNN_PRODUCTS", 3) == 2 ? 2 : 3;  // 2 breaks 1e-4
     }
     const int grid = (int)(n_members < kNumSMs ? n_members : kNumSMs);
     {   // stream-ordered refresh of the epilogue's constant bank

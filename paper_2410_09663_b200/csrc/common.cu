@@ -1,6 +1,12 @@
 // Library identity, error reporting and small elementwise kernels.
 #include "common.cuh"
 
+#include <stdlib.h>
+
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
 #include <string.h>
 
 namespace enks {
@@ -12,6 +18,19 @@ void set_error(const char* fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
+}
+
+int env_knob(const char* name, int dflt) {
+    // a handful of names, each looked up once; later calls read the cached value
+    static std::mutex mu;
+    static std::unordered_map<std::string, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(name);
+    if (it != cache.end()) return it->second;
+    const char* e = getenv(name);
+    const int v = (e && *e) ? atoi(e) : dflt;
+    cache.emplace(name, v);
+    return v;
 }
 
 int check_launch(const char* what) {

@@ -18,6 +18,18 @@ int check_launch(const char* what);
 
 constexpr int kNumSMs = 148;  // B200
 
+// Environment knobs.  Tuning knobs (launch shapes, kernel variants that give the same results to
+// rounding) are read ONCE per process, at the first launch that needs them (env_knob caches).
+// Debug knobs that can break the numerical contract (MMA products dropped, roles switched off,
+// descriptor overrides) exist only in builds with -DENKS_DEBUG_KNOBS (tools/ A/B probes): a
+// production library ignores them and uses the defaults.
+int env_knob(const char* name, int dflt);  // atoi(getenv(name)) or dflt, cached per name
+#ifdef ENKS_DEBUG_KNOBS
+inline int debug_knob(const char* name, int dflt) { return env_knob(name, dflt); }
+#else
+inline int debug_knob(const char*, int dflt) { return dflt; }
+#endif
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 }  // namespace enks

@@ -33,6 +33,12 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int KC = 32;               // fp16 elements per chunk row (64 B, SWIZZLE_64B)
+// TMEM accumulation chain length (chunks of KC): the tensor core truncates as it accumulates, so
+// a chain of c chunks carries a one-sided relative bias of about c * (KC / 16) * 3 * 2^-25 on a
+// sum of positive terms (Gram / Sigma_y diagonal): 1.4e-6 at 8 chunks, 2.9e-6 at 16.  Chains are
+// folded in fp32 registers with round-to-nearest adds.  tests/test_gpu_kernels.py pins the bias
+// at K = 131072 (C3's contraction depth).
+constexpr int kF16pChainDefault = 16;
 constexpr int kThreads = 384;
 constexpr int kSmemBudget = 210 * 1024;
 
@@ -694,12 +700,7 @@ int choose_split_pairs(int pairs, int64_t chunks) {
 }
 
 bool use_pair(int64_t N) {
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = getenv("ENKS_F16P_PAIR");
-        mode = e ? atoi(e) : 1;
-    }
-    return mode != 0 && N > 128;
+    return env_knob("ENKS_F16P_PAIR", 1) != 0 && N > 128;
 }
 
 int choose_split16(int tiles, int64_t chunks) {
@@ -797,13 +798,10 @@ int gemm_f16pair_impl(int64_t M, int64_t N, int64_t K, float alpha, const void* 
     p.inv_sa = inv_sa;
     p.inv_sb = inv_sb;
     p.splits = split;
-    // 16 chunks (512 K) per TMEM chain: the kernel test's 1e-6 (fp32-FFMA level) still holds and
-    // the cross moments run ~1 % faster than at 8 (profiles/r01/ab_chain.txt); gemm_tc keeps 8
-    const char* ch = getenv("ENKS_F16P_CHAIN");
-    if (!ch) ch = getenv("ENKS_TC_CHAIN");
-    p.chain = ch ? atoi(ch) : 16;
-    const char* pr = getenv("ENKS_F16P_PRODUCTS");
-    p.products = (pr && atoi(pr) == 2) ? 2 : 3;
+    // chain length: kF16pChainDefault (own knob only: ENKS_TC_CHAIN tunes gemm_tc and no longer
+    // leaks into this kernel)
+    p.chain = env_knob("ENKS_F16P_CHAIN", kF16pChainDefault);
+    p.products = debug_knob("ENKS_F16P_PRODUCTS", 3) == 2 ? 2 : 3;  // 2 breaks 1e-4
     if (p.chain < 1) p.chain = 1;
     const bool direct = split == 1;
     p.out = direct ? C : static_cast<float*>(ws);

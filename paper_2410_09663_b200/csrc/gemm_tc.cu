@@ -530,16 +530,14 @@ int gemm_tc_general(bool bmn, int64_t M, int64_t N, int64_t K, float alpha, cons
                     int bias_cols, float* C, int64_t ldc, int64_t tri_rows, int64_t tri_k,
                     int split, float* ws, cudaStream_t st) {
     if (M == 0 || N == 0) return ENKS_OK;
-    const char* bne = getenv("ENKS_TC_BN");
-    const int bn_cap = bne ? atoi(bne) : 256;
+    const int bn_cap = env_knob("ENKS_TC_BN", 256);
     const int BN = bn_for(N < bn_cap ? N : bn_cap);
     CUtensorMap ma, mh, ml;
     const int kb = (BN == 256 && !bmn) ? kBK256 : BK;
     const bool sw64 = kb == 16;
     const int m_tiles0 = (int)((M + BM - 1) / BM);
     // cluster the row tiles sharing B (multicast) when there are several and no triangular skip
-    const char* ce = getenv("ENKS_TC_CLUSTER");
-    const int want_cl = ce ? atoi(ce) : 1;
+    const int want_cl = env_knob("ENKS_TC_CLUSTER", 1);
     const int cl = (!bmn && tri_rows == 0 && want_cl == 4 && m_tiles0 >= 4) ? 4
                  : ((!bmn && tri_rows == 0 && want_cl >= 2 && m_tiles0 >= 2) ? 2 : 1);
     bool ok = make_map(&ma, A, M, K, lda, kb, BM, sw64);
@@ -562,16 +560,12 @@ int gemm_tc_general(bool bmn, int64_t M, int64_t N, int64_t K, float alpha, cons
     p.tri_rows = tri_rows; p.tri_k = tri_k;
     p.splits = split;
     {
-        const char* e = getenv("ENKS_TC_PRODUCTS");
-        p.products = e ? atoi(e) : 7;
-        const char* m = getenv("ENKS_TC_MN");
-        const int mode = m ? atoi(m) : 0;
+        p.products = debug_knob("ENKS_TC_PRODUCTS", 7);  // product mask: debug builds only
+        const int mode = debug_knob("ENKS_TC_MN", 0);       // descriptor LBO/SBO probe: debug only
         p.mn_lbo = mode == 1 ? 1024 : (mode == 2 ? 4096 : (mode == 3 ? 1024 : 4096));
         p.mn_sbo = mode == 1 ? 4096 : (mode == 2 ? 4096 : (mode == 3 ? 1024 : 1024));
-        const char* dbg = getenv("ENKS_TC_DEBUG");
-        p.debug = dbg ? atoi(dbg) : 0;
-        const char* ch = getenv("ENKS_TC_CHAIN");
-        p.chain = ch ? atoi(ch) : kChainChunksDefault;
+        p.debug = debug_knob("ENKS_TC_DEBUG", 0);
+        p.chain = env_knob("ENKS_TC_CHAIN", kChainChunksDefault);
         if (p.chain < 1) p.chain = 1;
     }
     const bool direct = (split == 1);

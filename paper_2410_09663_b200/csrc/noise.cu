@@ -233,8 +233,7 @@ int launch_noise(const uint32_t* head, int n_head, int64_t member0, int64_t n_me
     for (int j = 0; j < n_jobs; ++j) max_rows = max_rows > jobs[j].rows ? max_rows : jobs[j].rows;
     const int64_t n_streams = n_members * n_jobs;
     const SegPlan P = seg_plan(n_streams, (int64_t)max_rows * cols);
-    const char* se = getenv("ENKS_NOISE_SEG");
-    if (ws && P.n_chunks && !(se && se[0] == '0') &&
+    if (ws && P.n_chunks && env_knob("ENKS_NOISE_SEG", 1) != 0 &&
         ws_bytes >= seg_ws_bytes(n_streams, (int64_t)max_rows * cols)) {
         // records + ticket, zeroed in stream order (capture-safe)
         unsigned* ticket = static_cast<unsigned*>(ws);

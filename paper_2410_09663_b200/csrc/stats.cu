@@ -405,11 +405,7 @@ __global__ void uchain_gain_kernel(const float* __restrict__ g, int64_t ld_g, fl
 
 // ENKS_SUM_SCALAR=1: the scalar member-sum kernel (A/B measurements, tools/stats_bench.py)
 bool sum_scalar() {
-    static const bool v = [] {
-        const char* e = getenv("ENKS_SUM_SCALAR");
-        return e && e[0] == '1';
-    }();
-    return v;
+    return env_knob("ENKS_SUM_SCALAR", 0) == 1;
 }
 
 // per = columns per thread (4 for the vectorised partial kernel)

@@ -51,6 +51,22 @@ from .matvar import entropy_head
 CH_W, CH_VX, CH_VU, CH_EPS = 0, 1, 2, 3
 
 
+def _nvtx(name: str):
+    """NVTX range around an engine method on CUDA (nsys / ncu --nvtx see predict / update)."""
+    def deco(fn):
+        def wrapped(self, *args, **kw):
+            if getattr(self.ops, "device", None) is None or self.ops.device.type != "cuda":
+                return fn(self, *args, **kw)
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(self, *args, **kw)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        wrapped.__name__, wrapped.__doc__ = fn.__name__, fn.__doc__
+        return wrapped
+    return deco
+
+
 class LocalComm:
     rank = 0
     size = 1
@@ -60,6 +76,12 @@ class LocalComm:
 
     def allreduce_many(self, ts):
         return ts
+
+    def reduce_scatter_rows(self, t):
+        return t
+
+    def all_gather_rows(self, t):
+        return t
 
     def allreduce_max_(self, t):
         return t
@@ -99,6 +121,27 @@ class TorchComm:
             for t in ts:
                 self.dist.all_reduce(t, group=self.group)
         return ts
+
+    def reduce_scatter_rows(self, t):
+        """Sum over ranks of t (R x C, R a multiple of the rank count); returns this rank's row
+        block (R / size rows) -- row-sharded results (covariance tracking)."""
+        rows = t.shape[0] // self.size
+        if self.dist.get_backend(self.group) == "nccl":
+            out = t.new_empty(rows, t.shape[1])
+            self.dist.reduce_scatter_tensor(out, t, group=self.group)
+            return out
+        self.dist.all_reduce(t, group=self.group)  # gloo: no reduce_scatter
+        return t[self.rank * rows:(self.rank + 1) * rows].clone()
+
+    def all_gather_rows(self, t):
+        """Concatenate every rank's row block (inverse of reduce_scatter_rows)."""
+        if self.dist.get_backend(self.group) == "nccl":
+            out = t.new_empty(t.shape[0] * self.size, t.shape[1])
+            self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+            return out
+        parts = [torch.empty_like(t) for _ in range(self.size)]
+        self.dist.all_gather(parts, t.contiguous(), group=self.group)
+        return torch.cat(parts)
 
     def allreduce_max_(self, t):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
@@ -284,7 +327,9 @@ class DeviceSmoother:
         self.jitter = ops.zeros(1, dtype=torch.int32)
         self._alloc_obs()
         self._grow(max(1, int(capacity)))
-        x0 = ops.to_device(np.asarray(x0_packed, float))
+        # slice 0 of identical copies is never moved (enks.py:108-110): read back exactly
+        self.x0_exact = np.array(x0_packed, dtype=float)
+        x0 = ops.to_device(self.x0_exact)
         self.mean[:d] = x0
         self.last.copy_(x0[:q].repeat(1, self.Nl))
         self._store_rows("A", 0, ops.zeros(self.ds, K))
@@ -366,6 +411,7 @@ class DeviceSmoother:
         """Start a new horizon from N identical copies of x0 ((d x m), host or device),
         reusing every buffer (closed-loop driver: one smoother per MPC step, enks.py:105-128)."""
         d, q = self.d, self.q
+        self.x0_exact = None if torch.is_tensor(x0) else np.array(x0, dtype=float)
         x0 = x0 if torch.is_tensor(x0) else self.ops.to_device(np.asarray(x0, float))
         self.t = 0
         self.n_upd = 0
@@ -526,6 +572,7 @@ class DeviceSmoother:
             self._side = torch.cuda.Stream(device=self.ops.device)
         return self._side
 
+    @_nvtx("enks.gain_solve")
     def _spd_async(self, side, S, scale) -> None:
         """Sigma_y^{-1} with the reference's jitter fallback (enks.py:234-244), on `side`
         after everything queued so far on the main stream."""
@@ -638,6 +685,7 @@ class DeviceSmoother:
                                     self.ycT_h, self.ycT_l, self.ycT_inv)
 
     # ------------------------------------------------------------ predict
+    @_nvtx("enks.predict")
     def predict(self, vs, streams) -> None:
         """enks.py:156-171: W draw, new slice [f(x,u); u+w; w], append, mean."""
         self.bind(vs)
@@ -704,6 +752,7 @@ class DeviceSmoother:
         self.t = tau
 
     # ------------------------------------------------------------ update
+    @_nvtx("enks.update")
     def update(self, y_ref_dev, streams) -> None:
         """enks.py:212-248 restated on the append-only basis (module docstring)."""
         ops, comm = self.ops, self.comm
@@ -843,6 +892,7 @@ class DeviceSmoother:
             self.Ybuf[r0:r1].zero_()
         self.G[:, r0:r1].zero_()
 
+    @_nvtx("enks.update_t0")
     def _update_t0(self, y_ref_dev, streams) -> None:
         """update() before the first predict (enks.py:212-253 at t = 0): the trajectory is slice 0
         alone.  Observation noise is drawn with t = 0 (enks.py:224); Sigma_y goes through the
@@ -952,7 +1002,10 @@ class DeviceSmoother:
 
     def mean_host(self) -> np.ndarray:
         R = (self.t + 1) * self.d
-        return self.ops.to_host(self.mean[:R])
+        out = self.ops.to_host(self.mean[:R])
+        if self.slice0_zero and self.x0_exact is not None:
+            out[:self.d] = self.x0_exact  # identical copies: slice 0 is x0 itself, in fp64
+        return out
 
     def jitter_events(self) -> int:
         return int(self.ops.read_scalar(self.jitter))
@@ -969,7 +1022,10 @@ class DeviceSmoother:
         """Reset the representation to explicit members (local shard, (Nl, (t+1)d, m))."""
         ops, d = self.ops, self.d
         R = (int(t) + 1) * d
-        M = np.asarray(members_local, dtype=float).transpose(1, 0, 2).reshape(R, self.K)
+        members_local = np.asarray(members_local, dtype=float)
+        M = members_local.transpose(1, 0, 2).reshape(R, self.K)
+        self.slice0_zero = True  # re-derived from the data below
+        self.x0_exact = members_local[0, :d].copy() if len(members_local) else None
         self._replace_members_dev(ops.to_device(M), t)
 
     def _replace_members_dev(self, Mdev, t: int) -> None:
@@ -993,7 +1049,12 @@ class DeviceSmoother:
             self._store_rows("Y", 0, ops.zeros(self.t * self.p, self.K))
         if self.pair:
             self.A_new[:self.q].copy_(anom[self.t * d:self.t * d + self.q])
-        x0_spread = bool(torch.any(anom[:d] != 0).item())
+        spread = torch.any(anom[:d] != 0).to(torch.float32).reshape(1)
+        if self.comm.size > 1:  # every rank must take the same path (slice0_zero picks rows)
+            self.comm.allreduce_max_(spread)
+        x0_spread = bool(spread.item())
+        if x0_spread or not self.slice0_zero:
+            self.x0_exact = None
         self.slice0_zero = not x0_spread
         last = Mdev[self.t * d:self.t * d + self.q]
         self.last.copy_(last)

@@ -15,12 +15,12 @@ Noise is bit-identical to the reference's NoiseStreams substreams.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
 from typing import Optional
 
 import numpy as np
 import torch
 
+from .covariance import SmootherCovariances, track_predict, track_update
 from .engine import CH_EPS, CH_VU, CH_VX, CH_W, DeviceSmoother, LocalComm
 
 __all__ = [
@@ -62,15 +62,6 @@ def _comm():
     return _COMM or LocalComm()
 
 
-@dataclass
-class SmootherCovariances:
-    """lambda-scaled covariance tracking (enks.py:96-102); fp64 host arrays."""
-
-    sigma_traj: np.ndarray
-    sigma_pred: Optional[np.ndarray] = None
-    sigma_cross: Optional[np.ndarray] = None
-
-
 class TrajectoryEnsemble:
     """N trajectory samples with their running mean (enks.py:56-93), device-resident.
 
@@ -103,8 +94,10 @@ class TrajectoryEnsemble:
     def members(self) -> np.ndarray:
         eng = self._eng
         R = (eng.t + 1) * eng.d
-        local = eng.members_device().double().cpu().numpy()
+        local = eng.ops.to_host(eng.members_device())
         local = local.reshape(R, eng.Nl, eng.m).transpose(1, 0, 2)
+        if eng.slice0_zero and eng.x0_exact is not None:
+            local[:, :eng.d] = eng.x0_exact  # identical copies of x0 (enks.py:108-110), exact
         if eng.comm.size > 1:
             import torch.distributed as dist
 
@@ -184,40 +177,13 @@ def init_ensemble(x0, n_members: int, shared_col_cov: np.ndarray | None = None, 
     return TrajectoryEnsemble(_engine=eng)
 
 
-def _cov_product(eng: DeviceSmoother, a, b) -> np.ndarray:
-    """(lam/N) a b^T over all members (K contraction + allreduce), fp64 on host.
-
-    Covariance tracking at scale: for K >= 128 the contraction runs on
-    the tcgen05 fp16-pair kernel (N in 256-column launches), else on the SIMT GEMM."""
-    ops = eng.ops
-    out = ops.empty(a.shape[0], b.shape[0])
-    K = a.shape[1]
-    if hasattr(ops, "gemm_nt_f16pair") and K >= 128 and K % 8 == 0:
-        ops.gemm_nt_f16pair(a, b, out, alpha=eng.lam / eng.N)
-    else:
-        ops.gemm(a, b, out, trans_b=True, alpha=eng.lam / eng.N)
-    eng.comm.allreduce_(out)
-    return out.double().cpu().numpy()
-
-
 def predict(ens: TrajectoryEnsemble, vs, streams, cov: Optional[SmootherCovariances] = None
             ) -> TrajectoryEnsemble:
     """Advance every member one virtual step and append the new slice (enks.py:156-186)."""
     eng = ens._eng
     eng.predict(vs, streams)
     if cov is not None:
-        d = eng.d
-        dev_new = eng.newest_anomalies()
-        dev_traj = eng.deviations()
-        cov.sigma_pred = _cov_product(eng, dev_new, dev_new)
-        cov.sigma_cross = _cov_product(eng, dev_traj, dev_new)
-        old = cov.sigma_traj.shape[0]
-        block = np.zeros((old + d, old + d))
-        block[:old, :old] = cov.sigma_traj
-        block[:old, old:] = cov.sigma_cross[:old]
-        block[old:, :old] = cov.sigma_cross[:old].T
-        block[old:, old:] = cov.sigma_pred
-        cov.sigma_traj = block
+        track_predict(eng, cov)  # device-resident (covariance.py), read lazily as fp64
     return ens
 
 
@@ -237,8 +203,7 @@ def update(ens: TrajectoryEnsemble, y_ref: np.ndarray, vs, streams,
     eng.update(_device_yref(eng, y_ref), streams)
     eng.check_status()
     if cov is not None:
-        dev = eng.deviations()
-        cov.sigma_traj = _cov_product(eng, dev, dev)
+        track_update(eng, cov)
     return ens
 
 
@@ -325,6 +290,7 @@ def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
         g = _graph_for(x0, vs, h, n_members, streams)
         ops = g.eng.ops
         ops.copy_from_host(g.x0, np.asarray(x0.packed, dtype=np.float32))
+        g.eng.x0_exact = np.array(x0.packed, dtype=float)
         ops.copy_from_host(g.y_refs, np.ascontiguousarray(y_refs, dtype=np.float32))
         eng = g.replay()
         eng.check_status()
@@ -335,11 +301,17 @@ def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
     yref_dev = eng.ops.to_device(np.ascontiguousarray(y_refs))
     cov = SmootherCovariances(sigma_traj=np.zeros((eng.d, eng.d))) if track_cov else None
     for step in range(h):
-        predict(ens, vs, streams, cov=cov)
-        if cov is None:
-            eng.update(yref_dev[step], streams)
-        else:
-            update(ens, y_refs[step], vs, streams, cov=cov)
+        # tracking never feeds back into the smoother (test_enks.py:253-265), and every tracked
+        # field is overwritten by the next predict / update (enks.py:173-185, 250-252), so only
+        # the last step's values are observable: track there only
+        last = cov is not None and step == h - 1
+        eng.predict(vs, streams)
+        if last:
+            track_predict(eng, cov)
+        eng.update(yref_dev[step], streams)
+        if last:
+            eng.check_status()
+            track_update(eng, cov)
     eng.check_status()
     return ens.slices(), cov
 

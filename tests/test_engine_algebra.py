@@ -194,3 +194,37 @@ def test_engine_irregular_update_sequences_equal_oracle(pm, pair, spread):
         assert np.abs(members - o.members).max() < 1e-10 * np.abs(o.members).max(), op
         assert np.abs(eng.mean_host() - o.mean).max() < 1e-10 * np.abs(o.mean).max(), op
     assert eng.jitter.item() == o.jitter_events
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_device_covariance_tracking_equals_oracle(pm, pair):
+    """covariance.py's device tracking (SYRK over 256-blocks, lazy block assembly after predict,
+    sigma_pred = last rows of sigma_cross) equals the oracle's track_cov after every call."""
+    from paper_2410_09663_b200.covariance import (SmootherCovariances, track_predict,
+                                                  track_update)
+
+    _, vs, x0 = problems.make_linear_setup(pm, np.random.default_rng(6), n=60, l=40, m=4)
+    y = vs.reference_observation()
+    h, N, seed = 4, 40, 3  # T d up to 5 * 140 = 700 rows: three 256-blocks
+    o = enks_oracle.oracle_init(x0.packed, x0.n, x0.l, N)
+    ocov = enks_oracle.OracleCov(sigma_traj=np.zeros((o.d, o.d)))
+    ops = CpuOps()
+    eng = DeviceSmoother(ops, x0.packed, x0.n, x0.l, N, o.lam, capacity=2,
+                         basis="f16pair" if pair else "fp32")
+    eng.bind(vs)
+    cov = SmootherCovariances(sigma_traj=np.zeros((o.d, o.d)))
+    st = pm.matvar.NoiseStreams(seed=seed)
+    yd = ops.to_device(y)
+    for _ in range(h):
+        enks_oracle.oracle_predict(o, vs, seed, cov=ocov, backend="c")
+        eng.predict(vs, st)
+        track_predict(eng, cov)
+        for k in ("sigma_traj", "sigma_cross", "sigma_pred"):
+            ref = getattr(ocov, k)
+            assert np.abs(getattr(cov, k) - ref).max() < 1e-10 * np.abs(ref).max(), k
+        enks_oracle.oracle_update(o, y, vs, seed, cov=ocov, backend="c")
+        eng.update(yd, st)
+        track_update(eng, cov)
+        ref = ocov.sigma_traj
+        assert cov.sigma_traj.shape == ref.shape
+        assert np.abs(cov.sigma_traj - ref).max() < 1e-10 * np.abs(ref).max()

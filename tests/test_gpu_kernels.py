@@ -416,8 +416,34 @@ def test_gemm_nt_f16pair_blocked_columns(dev_ops, M, N, K):
     dev_ops.gemm_nt_f16pair(dA, dA, Cs)
     refs = A.double() @ A.double().t()
     # Gram diagonals are all-positive sums: the tensor core's truncating TMEM accumulation
-    # within one 256-deep chain biases them by up to ~chain/2 * 2^-24 (see gemm_f16p.cu)
+    # within one chain biases them (gemm_f16p.cu kF16pChainDefault: ~2.9e-6 at 16 chunks)
     assert ((Cs.double().cpu() - refs).abs() / (A.double().abs() @ A.double().abs().t())).max() < 5e-6
+
+
+def test_f16pair_gram_diagonal_bias_at_c3_depth(dev_ops):
+    """Sigma_y-like Gram matrix at C3's contraction depth (K = N m = 131072, p = 256, split-K as
+    in the smoother): the one-sided truncation bias of the TMEM chains on the positive diagonal
+    stays within the chain-length bound c (KC/16) 3 2^-25 x 2 (c = 16 chunks of KC = 32), and the
+    signed error of the off-diagonal entries stays at fp32-sum level."""
+    g = torch.Generator().manual_seed(11)
+    p, K = 256, 131072
+    Y = torch.randn(p, K, generator=g) * torch.logspace(-1, 1, p).unsqueeze(1)
+    f16 = torch.float16
+    yh, yl, yi = dev_ops.empty(p, K, dtype=f16), dev_ops.empty(p, K, dtype=f16), dev_ops.empty(p)
+    dev_ops.f16pair_split(Y.to(dev_ops.device), yh, yl, yi)
+    C = dev_ops.zeros(p, p)
+    dev_ops.gemm_f16pair(yh, yl, yi, yh, yl, yi, C)
+    Yd = Y.double()
+    ref = Yd @ Yd.t()
+    diag_rel = ((C.double().cpu().diagonal() - ref.diagonal()) / ref.diagonal())
+    bound = 2 * 16 * (32 / 16) * 3 * 2.0 ** -25
+    print(f"diag rel bias mean {diag_rel.mean().item():.2e} min {diag_rel.min().item():.2e} "
+          f"bound {bound:.2e}")
+    assert diag_rel.abs().max().item() < bound
+    scale = (Yd.abs() @ Yd.abs().t())
+    off = ((C.double().cpu() - ref).abs() / scale)
+    off.fill_diagonal_(0)
+    assert off.max().item() < 1e-6
 
 
 def test_gemm_f16pair_ex_shift_operands(dev_ops):

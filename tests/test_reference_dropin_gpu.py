@@ -29,8 +29,10 @@ TOL = 1e-4
 # device computes in fp32 (north_star: relative error <= 1e-4), so those become 1e-4 absolute.
 # Bit-identity (np.array_equal), shapes, lambda, jitter counts and the 5 % statistical checks
 # are unchanged.
+# The PSD check's -1e-8 tr(Sigma) floor is below fp32 resolution of a Gram matrix (eigenvalue
+# error ~ eps_fp32 * ||Sigma||), so it becomes -1e-6 tr(Sigma).
 FP32_RELAX = [("< 1e-12", "< 1e-4"), ("rel < 1e-10", "rel < 1e-4"), ("atol=1e-12", "atol=1e-4"),
-              ("atol=1e-9", "atol=1e-4")]
+              ("atol=1e-9", "atol=1e-4"), ("> -1e-8 * np.trace", "> -1e-6 * np.trace")]
 
 
 def _ref_mods():
