@@ -18,7 +18,9 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-TOL = 1e-6
+# fp32 rounding only: the ranks' member sums and K-partial cross moments are summed in another
+# order than one rank's (and each rank picks its own fp16-pair row scales); noise is bit-identical
+TOL = 5e-6
 
 
 def _free_port():
