@@ -308,9 +308,16 @@ def run_ours(args):
     n, l, m = pr.n, pr.l, pr.m
     est = 4.4 * ((h + 1) * (n + l) + h * (n + l)) * pr.N * m  # fp16-pair basis + gains, bytes
     fits = est < 0.3 * torch.cuda.get_device_properties(local).total_memory
-    if args.graph and world == 1 and fits:
-        graph = enks.HorizonGraph(pr.x0, pr.vs, h, pr.N, streams)
-        graph.y_refs.copy_(yref_dev)
+    if args.graph and fits:
+        try:  # multi-rank: the NCCL collectives are captured inside the horizon graph
+            graph = enks.HorizonGraph(pr.x0, pr.vs, h, pr.N, streams)
+            graph.y_refs.copy_(yref_dev)
+        except RuntimeError as exc:  # a backend that cannot be captured: time eager launches
+            if world == 1:
+                raise
+            sys.stderr.write(f"bench.py: horizon graph capture failed ({exc}); eager\n")
+            graph = None
+            torch.cuda.synchronize()
 
     def one_step():
         if graph is not None:

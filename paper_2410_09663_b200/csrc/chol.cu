@@ -71,6 +71,9 @@ __device__ void panel_solve(float* X, const float* L, int lane) {
         x[k] = x[k] / L[k * kLd + k];
 #pragma unroll
         for (int j = k + 1; j < kTS; ++j) x[j] = fmaf(-x[k], L[j * kLd + k], x[j]);
+        // keep the next columns' L loads from being hoisted across k (they would pin ~500
+        // registers of prefetched values and spill x[])
+        asm volatile("" ::: "memory");
     }
 #pragma unroll
     for (int j = 0; j < kTS; ++j) X[lane * kLd + j] = x[j];
@@ -138,11 +141,13 @@ __global__ void __launch_bounds__(kThreads)
     // attempt 0: no jitter; attempt 1: the reference's 1e-9 tr / p + 1e-30 (enks.py:241).  A
     // relative 1e-9 is below fp32 resolution, so when it cannot rescue a rank-deficient Sigma_y
     // (N m < p) the jitter is escalated (1e-7, 1e-6, 1e-5 relative) -- still one jitter event.
-    const double kJit[5] = {0.0, 1e-9, 1e-7, 1e-6, 1e-5};
     int failed = 0;
     float used_jit = 0.f;
     for (int attempt = 0; attempt < (single ? 1 : 5); ++attempt) {
-        const float jitter = attempt == 0 ? 0.f : (float)(kJit[attempt] * trace / (double)p + 1e-30);
+        // relative jitter per attempt: 0, 1e-9 (the reference), then 1e-7, 1e-6, 1e-5 (selects,
+        // not an indexed local array: no stack frame)
+        const double rel = attempt == 1 ? 1e-9 : (attempt == 2 ? 1e-7 : (attempt == 3 ? 1e-6 : 1e-5));
+        const float jitter = attempt == 0 ? 0.f : (float)(rel * trace / (double)p + 1e-30);
         used_jit = jitter;
         // load sym(S) (+ jitter I) tile by tile with coalesced rows: tile (I, J) gets
         // 0.5 scale S[I-block][J-block] row-wise, then += 0.5 scale S[J-block][I-block]^T
@@ -273,192 +278,6 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
     (void)n_tiles;
-}
-
-// ---------------------------------------------------------------------------------------------
-// Blocked symmetric SWEEP (Gauss-Jordan without pivoting, stable for SPD): sweeping every pivot of
-// W leaves -W^{-1} in place, so one pass replaces Cholesky + triangular inverse + L^{-T} L^{-1}
-// (three dependent phases, ~40 barriers at p = 256) with nb block steps of three barriers each.
-// Block step K (32 pivots), D = W_KK the current Schur-complement block:
-//   D^{-1} by an unblocked sweep in one warp's registers (pivot <= 0 or NaN: W is not positive
-//   definite -- exactly where dpotrf fails, up to rounding -> the reference's jitter rule);
-//   P_I = W_IK D^{-1} (I != K);  W_IJ -= P_I W_JK^T (I >= J, I, J != K);
-//   W_IK <- P_I,  W_KK <- -D^{-1}.
-// The lower tile-triangle lives in shared memory (32 x 33 tiles); W_IK for I < K is read as the
-// transpose of stored tile (K, I).  Work per step: (nb - 1) P tiles + (nb - 1) nb / 2 update tiles
-// as quarter-tile tasks over 32 warps.
-constexpr int kSwThreads = 512;
-constexpr int kSwWarps = kSwThreads / 32;
-
-// W_IK element (r, c) (row r of block I, column c of block K) from the lower tile-triangle
-__device__ __forceinline__ float w_blk(const float* Lt, int I, int K, int r, int c) {
-    return I >= K ? Lt[tix(I, K) * kTile + r * kLd + c] : Lt[tix(K, I) * kTile + c * kLd + r];
-}
-
-// -D^{-1} of the symmetric 32 x 32 tile T in place (warp; lane = row); false on a bad pivot
-__device__ bool sweep_diag(float* T, int lane) {
-    float a[kTS];
-#pragma unroll
-    for (int j = 0; j < kTS; ++j) a[j] = T[lane * kLd + j];
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < kTS; ++k) {
-        const float d = __shfl_sync(0xffffffffu, a[k], k);
-        if (!(d > 0.f)) ok = false;
-        const float inv = 1.f / d;
-        const float aik = a[k];
-#pragma unroll
-        for (int j = 0; j < kTS; ++j) {
-            const float akj = __shfl_sync(0xffffffffu, a[j], k);  // row k (lane k's registers)
-            if (lane == k)
-                a[j] = (j == k) ? -inv : akj * inv;
-            else
-                a[j] = (j == k) ? aik * inv : fmaf(-aik * inv, akj, a[j]);
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < kTS; ++j) T[lane * kLd + j] = a[j];
-    return ok;
-}
-
-__global__ void __launch_bounds__(kSwThreads)
-    sweep_inverse_kernel(const float* __restrict__ S, int64_t lds, int p, float scale,
-                         float* __restrict__ out, int* status, int* jitter_events, int single,
-                         float* jit_out) {
-    extern __shared__ float sm[];
-    float* Lt = sm;                                   // lower tile-triangle of W
-    const int nb = (p + kTS - 1) / kTS;
-    float* P = Lt + (nb * (nb + 1) / 2) * kTile;      // staging: P_I, I = 0..nb-1
-    __shared__ int s_fail;
-    __shared__ double s_trace_part[kSwWarps];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n_tiles = nb * (nb + 1) / 2;
-    {   // trace (fp64) for the jitter
-        double t = 0.0;
-        for (int i = tid; i < p; i += kSwThreads) t += (double)(scale * S[(int64_t)i * lds + i]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == 0) s_trace_part[warp] = t;
-    }
-    __syncthreads();
-    double trace = 0.0;
-    for (int w = 0; w < kSwWarps; ++w) trace += s_trace_part[w];
-    const double kJit[5] = {0.0, 1e-9, 1e-7, 1e-6, 1e-5};  // as spd_inverse_kernel
-    int failed = 0;
-    float used_jit = 0.f;
-    for (int attempt = 0; attempt < (single ? 1 : 5); ++attempt) {
-        const float jitter = attempt == 0 ? 0.f : (float)(kJit[attempt] * trace / (double)p + 1e-30);
-        used_jit = jitter;
-        for (int q = warp; q < n_tiles; q += kSwWarps) {  // sym(S) + jitter I, padding = identity
-            int I = 0;
-            while ((I + 1) * (I + 2) / 2 <= q) ++I;
-            const int J = q - I * (I + 1) / 2;
-            float* T = Lt + q * kTile;
-            const float hs = 0.5f * scale;
-            const int cj = J * kTS + lane, ci = I * kTS + lane;
-            for (int r = 0; r < kTS; ++r) {
-                const int ri = I * kTS + r;
-                T[r * kLd + lane] = (ri < p && cj < p) ? hs * S[(int64_t)ri * lds + cj] : 0.f;
-            }
-            __syncwarp();
-            for (int r = 0; r < kTS; ++r) {
-                const int rj = J * kTS + r;
-                const float v = (rj < p && ci < p) ? hs * S[(int64_t)rj * lds + ci] : 0.f;
-                T[lane * kLd + r] += v;
-            }
-            __syncwarp();
-            if (I == J) {
-                const int gi = I * kTS + lane;
-                T[lane * kLd + lane] = gi < p ? T[lane * kLd + lane] + jitter : 1.f;
-            }
-        }
-        if (tid == 0) s_fail = 0;
-        __syncthreads();
-        if (warp == 0 && !sweep_diag(Lt + tix(0, 0) * kTile, lane) && lane == 0) s_fail = 1;
-        __syncthreads();
-        for (int K = 0; K < nb && !s_fail; ++K) {
-            const float* Dn = Lt + tix(K, K) * kTile;  // -D^{-1}
-            // (b) P_I = W_IK D^{-1} = -(W_IK)(-D^{-1}), quarter tasks (I, rows r0..r0+7)
-            for (int t = warp; t < 4 * nb; t += kSwWarps) {
-                const int I = t >> 2, r0 = 8 * (t & 3);
-                if (I == K) continue;
-                float acc[8];
-#pragma unroll
-                for (int r = 0; r < 8; ++r) acc[r] = 0.f;
-#pragma unroll 8
-                for (int k = 0; k < kTS; ++k) {
-                    const float dk = Dn[k * kLd + lane];  // (-D^{-1})[k][lane]
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) acc[r] = fmaf(w_blk(Lt, I, K, r0 + r, k), dk, acc[r]);
-                }
-#pragma unroll
-                for (int r = 0; r < 8; ++r) P[I * kTile + (r0 + r) * kLd + lane] = -acc[r];
-            }
-            __syncthreads();
-            // (c) W_IJ -= P_I W_JK^T for I >= J, I, J != K (quarter tasks)
-            const int nt = n_tiles * 4;
-            for (int t = warp; t < nt; t += kSwWarps) {
-                const int q = t >> 2, r0 = 8 * (t & 3);
-                int I = 0;
-                while ((I + 1) * (I + 2) / 2 <= q) ++I;
-                const int J = q - I * (I + 1) / 2;
-                if (I == K || J == K) continue;
-                const float* PI = P + I * kTile;
-                float acc[8];
-#pragma unroll
-                for (int r = 0; r < 8; ++r) acc[r] = 0.f;
-#pragma unroll 8
-                for (int k = 0; k < kTS; ++k) {
-                    const float wj = w_blk(Lt, J, K, lane, k);  // W_JK[lane][k]
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) acc[r] = fmaf(PI[(r0 + r) * kLd + k], wj, acc[r]);
-                }
-                float* C = Lt + q * kTile;
-#pragma unroll
-                for (int r = 0; r < 8; ++r) C[(r0 + r) * kLd + lane] -= acc[r];
-            }
-            __syncthreads();
-            // (d) W_IK <- P_I (tile orientation), while warp 0 sweeps the next diagonal block
-            //     (updated in (c), untouched by (d))
-            if (warp == 0) {
-                if (K + 1 < nb && !sweep_diag(Lt + tix(K + 1, K + 1) * kTile, lane) && lane == 0)
-                    s_fail = 1;
-            } else {
-                for (int t = warp - 1; t < nb * kTS; t += kSwWarps - 1) {
-                    const int I = t / kTS, r = t - I * kTS;
-                    if (I == K) continue;
-                    const float v = P[I * kTile + r * kLd + lane];
-                    if (I > K)
-                        Lt[tix(I, K) * kTile + r * kLd + lane] = v;
-                    else
-                        Lt[tix(K, I) * kTile + lane * kLd + r] = v;
-                }
-            }
-            __syncthreads();
-        }
-        failed = s_fail;
-        __syncthreads();
-        if (!failed) break;
-        if (attempt == 0 && tid == 0 && !single) atomicAdd(jitter_events, 1);
-    }
-    if (tid == 0 && jit_out) *jit_out = used_jit;
-    if (failed) {
-        if (tid == 0) *status = 1;
-        const float nan = __int_as_float(0x7fc00000);
-        for (int e = tid; e < p * p; e += kSwThreads) out[e] = nan;
-        return;
-    }
-    // W^{-1} = -(swept W), dense p x p (tile rows coalesced; upper tiles mirrored)
-    for (int q = warp; q < nb * nb; q += kSwWarps) {
-        const int I = q / nb, J = q - I * nb;
-        const int c = J * kTS + lane;
-        for (int r = 0; r < kTS; ++r) {
-            const int i = I * kTS + r;
-            if (i >= p || c >= p) continue;
-            out[(int64_t)i * p + c] = -(I >= J ? Lt[tix(I, J) * kTile + r * kLd + lane]
-                                               : Lt[tix(J, I) * kTile + lane * kLd + r]);
-        }
-    }
 }
 
 // inv = L^{-T} L^{-1}: inv[i][j] = sum_{k >= max(i, j)} Linv[k][i] Linv[k][j]; one CTA per
@@ -648,33 +467,9 @@ int spd_debug() {
 
 // inv = S^{-1} (p <= kMaxP) with the one-CTA kernel: single = 1 -> one attempt, *flag = 1 on a
 // bad pivot (no jitter); single = 0 -> the reference's jitter rule with status / jitter_events
-size_t sweep_smem(int p) {
-    const int nb = (p + kTS - 1) / kTS;
-    return ((size_t)nb * (nb + 1) / 2 + nb) * kTile * sizeof(float);
-}
-
 int spd_small(const float* S, int64_t lds, int p, float scale, float* inv, float* linv_ws,
               int* status, int* jitter_events, int single, cudaStream_t st,
               float* jit_out = nullptr) {
-    if (env_knob("ENKS_SPD_SWEEP", 1) != 0 && sweep_smem(p) <= 227 * 1024) {
-        // one-kernel blocked sweep (W^{-1} directly; ENKS_SPD_SWEEP=0: Cholesky + L^{-T} L^{-1})
-        static size_t configured = 0;
-        const size_t smem = sweep_smem(p);
-        if (smem > 48 * 1024 && smem > configured) {
-            cudaError_t e = cudaFuncSetAttribute(sweep_inverse_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem);
-            if (e != cudaSuccess) {
-                set_error("enks_spd_inverse: smem attribute: %s", cudaGetErrorString(e));
-                return ENKS_E_CUDA;
-            }
-            configured = smem;
-        }
-        sweep_inverse_kernel<<<1, kSwThreads, smem, st>>>(S, lds, p, scale, inv, status,
-                                                          jitter_events, single, jit_out);
-        (void)linv_ws;
-        return check_launch("enks_spd_inverse(sweep)");
-    }
     const size_t smem = spd_smem(p);
     int rc = configure_spd(smem);
     if (rc) return rc;

@@ -90,6 +90,46 @@ class LocalComm:
         return t
 
 
+class SimComm:
+    """Rank 0 of a SIMULATED `size`-rank job on one GPU (tools/shard_model.py): it owns N/size
+    members and runs exactly the per-rank kernels; every collective is replaced by `t *= size`
+    (as if each other rank held a copy of this rank's shard), which keeps the smoother numerically
+    sane, and its bytes are logged for the collective-cost model.  Timing only."""
+
+    rank = 0
+
+    def __init__(self, size: int):
+        self.size = int(size)
+        self.log = []  # (kind, bytes)
+
+    def allreduce_(self, t):
+        self.log.append(("allreduce", t.numel() * t.element_size()))
+        t.mul_(self.size)
+        return t
+
+    def allreduce_many(self, ts):
+        self.log.append(("allreduce", sum(t.numel() * t.element_size() for t in ts)))
+        for t in ts:
+            t.mul_(self.size)
+        return ts
+
+    def allreduce_max_(self, t):
+        self.log.append(("allreduce", t.numel() * t.element_size()))
+        return t
+
+    def broadcast_(self, t, src=0):
+        self.log.append(("broadcast", t.numel() * t.element_size()))
+        return t
+
+    def reduce_scatter_rows(self, t):
+        self.log.append(("reduce_scatter", t.numel() * t.element_size()))
+        return t[:t.shape[0] // self.size].mul_(self.size)
+
+    def all_gather_rows(self, t):
+        self.log.append(("all_gather", t.numel() * t.element_size() * self.size))
+        return t.repeat(self.size, 1)
+
+
 class TorchComm:
     """torch.distributed process group (NCCL on B200, gloo on CPU tests)."""
 

@@ -211,12 +211,17 @@ class HorizonGraph:
     """One whole horizon solve (reset + H x (predict, update)) captured as a CUDA graph.
 
     Static device inputs ``x0`` ((d x m)) and ``y_refs`` ((h, p, m)) are copied in before each
-    ``replay``; the result is the engine's ``mean``.  The noise substreams (seed, prefix), the
-    model and the virtual system are baked into the graph.  Every kernel of the eager path runs
-    on replay (same launches, same order, side-stream gain solve included) -- the graph only
-    removes the per-launch host cost, which dominates small problems."""
+    ``replay``; the result is the engine's ``mean``.  The model and the virtual system are baked
+    into the graph; the noise streams' entropy words live in device memory (ops.DeviceHead), so
+    one capture serves every NoiseStreams / child(k) with the same number of entropy words
+    (``set_streams``).  Every kernel of the eager path runs on replay (same launches, same order,
+    side-stream gain solve included) -- the graph only removes the per-launch host cost, which
+    dominates small problems."""
 
     def __init__(self, x0, vs, h: int, n_members: int, streams, comm=None):
+        from .matvar import entropy_head
+        from .ops import DeviceHead
+
         packed = np.asarray(x0.packed, dtype=float)
         lam = 1.0 / float(np.trace(vs.shared_col_cov))
         ops = _ops()
@@ -224,6 +229,10 @@ class HorizonGraph:
         self.eng = DeviceSmoother(ops, packed, x0.n, x0.l, n_members, lam, capacity=h,
                                   comm=comm or _comm())
         self.eng.bind(vs)
+        words = entropy_head(streams.seed, tuple(streams.prefix))
+        self.head = DeviceHead(ops.zeros(max(32, len(words)), dtype=torch.int32), len(words))
+        self.head.set(words)
+        self.eng.dev_head = self.head
         self.x0 = ops.to_device(packed)
         self.y_refs = ops.zeros(h, vs.obs_rows, packed.shape[1])
         self._run()  # warm-up: kernel attributes, workspaces, tensor maps
@@ -238,6 +247,13 @@ class HorizonGraph:
         for step in range(self.h):
             eng.predict(self.vs, self.streams)
             eng.update(self.y_refs[step], self.streams)
+
+    def set_streams(self, streams) -> None:
+        """Noise substreams for the next replays (same entropy word count as the capture)."""
+        from .matvar import entropy_head
+
+        self.head.set(entropy_head(streams.seed, tuple(streams.prefix)))
+        self.streams = streams
 
     def replay(self) -> DeviceSmoother:
         eng = self.eng
@@ -255,14 +271,40 @@ class HorizonGraph:
 _GRAPHS: dict = {}
 
 
-def _graph_for(x0, vs, h, n_members, streams) -> HorizonGraph:
+def _nccl(comm) -> bool:
+    group = getattr(comm, "group", None)
+    try:
+        import torch.distributed as dist
+
+        return getattr(comm, "dist", None) is not None and dist.get_backend(group) == "nccl"
+    except (RuntimeError, ValueError):
+        return False
+
+
+GRAPH_CACHE_FRACTION = 0.25  # of device memory, summed over the cached horizon engines
+
+
+def _graph_for(x0, vs, h, n_members, streams):
+    """Cached HorizonGraph for this (virtual system, shapes, h, N, entropy word count), or None
+    when its engine would not fit the cache budget (the caller then runs eager)."""
+    from .matvar import entropy_head
+
+    n_words = len(entropy_head(streams.seed, tuple(streams.prefix)))
     key = (id(vs), id(vs.model), tuple(np.shape(x0.packed)), x0.n, x0.l, int(h), int(n_members),
-           int(streams.seed), tuple(streams.prefix), id(_COMM))
+           n_words, id(_COMM))
     g = _GRAPHS.get(key)
-    if g is None or g.vs is not vs:
-        if len(_GRAPHS) >= 8:
-            _GRAPHS.pop(next(iter(_GRAPHS)))
-        g = _GRAPHS[key] = HorizonGraph(x0, vs, h, n_members, streams)
+    if g is not None and g.vs is vs:
+        g.set_streams(streams)
+        return g
+    budget = GRAPH_CACHE_FRACTION * torch.cuda.get_device_properties(
+        torch.cuda.current_device()).total_memory
+    d, p, m = x0.n + 2 * x0.l, x0.n + x0.l, np.shape(x0.packed)[1]
+    est = 4.4 * ((h + 1) * p + h * p) * n_members * m + 4 * (h + 1) * d * m  # basis + gains
+    if est > budget:
+        return None
+    while _GRAPHS and sum(v.eng.memory_bytes() for v in _GRAPHS.values()) + est > budget:
+        _GRAPHS.pop(next(iter(_GRAPHS)))
+    g = _GRAPHS[key] = HorizonGraph(x0, vs, h, n_members, streams)
     return g
 
 
@@ -286,8 +328,11 @@ def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
     if y_refs.shape[1:] != (vs.obs_rows, x0.m):
         raise ValueError(f"y_ref shape {y_refs.shape[1:]} != observation {(vs.obs_rows, x0.m)}")
     if graph and not track_cov and n_members >= 2 and torch.cuda.is_available() and \
-            _comm().size == 1:  # (collectives are not captured: multi-rank runs stay eager)
+            (_comm().size == 1 or _nccl(_comm())):  # NCCL collectives are captured too
         g = _graph_for(x0, vs, h, n_members, streams)
+    else:
+        g = None
+    if g is not None:
         ops = g.eng.ops
         ops.copy_from_host(g.x0, np.asarray(x0.packed, dtype=np.float32))
         g.eng.x0_exact = np.array(x0.packed, dtype=float)

@@ -679,3 +679,24 @@ def test_noise_segmented_bit_exact(dev_ops, N, rows, cols, m0):
     z = onoise.member_normals(11, (2, 5), 4, 1, m0 + N, (rows, cols), backend="c")[m0:]
     want = np.ascontiguousarray(z.transpose(1, 0, 2).reshape(rows, -1)).astype(np.float32)
     assert np.array_equal(seg[1].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("rows,N", [(24, 300), (2, 150), (3, 149)])
+def test_cnn_forward_tcgen05_several_images_per_cta(dev_ops, pm, rows, N):
+    """128-pixel images with more images than SMs: each CTA streams several images through the
+    same row pipeline (TMEM ring, A slots, tap ring continue across image boundaries); minimum
+    image height 2 (both edge rows at once)."""
+    from oracle.models import cnn_step_torch
+    from paper_2410_09663_b200.engine import Forecaster
+
+    model = pm.dynamics.CNNDynamics(rows=rows, cols=128, widths=(2, 32, 32, 1), seed=5)
+    model.state_rows = model.input_rows = rows
+    rng = np.random.default_rng(N)
+    x = rng.standard_normal((N, rows, 128))
+    u = rng.standard_normal((N, rows, 128))
+    ref = cnn_step_torch(x, u, model.weights, model.biases, model.alpha)
+    last = dev_ops.to_device(np.concatenate([x, u], axis=1).transpose(1, 0, 2).reshape(2 * rows, -1))
+    out = dev_ops.zeros(rows, N * 128)
+    Forecaster(model, dev_ops, rows, rows)(dev_ops, last, out, rows, N)
+    got = _cpu(out).reshape(rows, N, 128).transpose(1, 0, 2)
+    np.testing.assert_allclose(got, ref, rtol=1e-5, atol=2e-6)

@@ -212,6 +212,15 @@ def test_cuda_graph_horizon_bit_identical_to_eager(pm):
     e1, _ = enks.smooth_horizon(x1, pr.y_ref, pr.vs, pr.H, pr.N, st)
     g3, _ = enks.smooth_horizon(x1, pr.y_ref, pr.vs, pr.H, pr.N, st, graph=True)
     assert np.array_equal(g3, e1)
+    # other noise streams with the same entropy word count replay the SAME capture (device head)
+    n_graphs = len(enks._GRAPHS)
+    for st2 in (pm.matvar.NoiseStreams(seed=4), pm.matvar.NoiseStreams(seed=3, prefix=(7,)),
+                pm.matvar.NoiseStreams(seed=4, prefix=(8,))):
+        e2, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, st2)
+        g4, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, st2, graph=True)
+        assert np.array_equal(g4, e2)
+        assert not np.array_equal(g4, eager)
+    assert len(enks._GRAPHS) == n_graphs + 1  # one extra capture: the prefixed word count
 
 
 def test_smooth_horizon_wide_observation_schur_gain(pm):
