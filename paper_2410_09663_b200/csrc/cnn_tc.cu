@@ -759,374 +759,6 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     if (warp == 2) ptx::tmem_dealloc(tmem, L::kTmemAlloc);
 }
 
-// =============================================================================================
-// 128-pixel images, UNIFORM SIMT warpgroups (default for SH): the 12 CUDA-core warps form three
-// warpgroups that each own every third layer-1 row AND every third layer-2/3 output row, so the
-// layer-1 producer work and the latency-bound epilogue (TMEM loads, bias + tanh, 32 -> 1 taps) are
-// spread evenly over 3 warps per scheduler instead of 2 producer warps + 1 epilogue warp.  Same
-// MMA formulation as cnn3_tc_kernel<true> (vertical taps stacked in N, horizontal taps as row-
-// shifted A operands, 3xTF32).  Per warpgroup g, over the CTA's global row index R = it * n + r:
-//     for R = g, g + 3, ...:  produce layer-1 row R;  epilogue of row R - 3
-// Epilogue of row E: s = D_{E-1}[dy0] + D_E[dy1] + D_{E+1}[dy2] from TMEM (each D read by three
-// warpgroups: acc_empty counts 12 warps; image-edge rows arrive twice), layer-2 bias + tanh, the
-// nine layer-3 taps, horizontal fold (shuffles + a per-warpgroup boundary exchange), then the
-// vertical fold across warpgroups through a shared-memory ring: row E publishes tk0 (-> output
-// E + 1) and tk1 (-> output E) and finishes output E - 1 = T0[E-2] + T1[E-1] + tk2.
-constexpr int kUniRing = 6;  // tap-ring slots (a multiple of 3: a slot always belongs to one WG)
-struct CU {
-    static constexpr int kBTile = NB * 128;
-    static constexpr int kATile = 136 * 128;
-    static constexpr int kOffB = 0;
-    static constexpr int kOffA = kOffB + 3 * 2 * kBTile;
-    static constexpr int kStageF = 2 * 3 * 2 * kInRow;           // floats per WG: [buf][row][ch][W+2]
-    static constexpr int kOffStage = kOffA + NA * 2 * kATile;
-    static constexpr int kOffW1 = kOffStage + 3 * kStageF * 4;
-    static constexpr int kOffB1 = kOffW1 + (C1 / 2) * kW1Stride * 8;
-    static constexpr int kOffT = kOffB1 + C1 * 4;                 // [slot][T0, T1][W]
-    static constexpr int kOffXv = kOffT + kUniRing * 2 * W * 4;   // [WG][parity][A/B][warp][4]
-    static constexpr int kOffBar = kOffXv + 3 * 2 * 2 * 4 * 4 * 4;
-    static constexpr int kSmem = kOffBar + 40 * 8 + 1024;
-    static_assert(kSmem <= 232448, "shared memory budget");
-    static_assert(kOffA % 1024 == 0 && kATile % 1024 == 0, "SW128 tiles need 1 KB alignment");
-};
-
-__global__ void __launch_bounds__(kThreads, 1) cnn3_uni_kernel(const Cnn3Args a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    float* w1s = reinterpret_cast<float*>(sm + CU::kOffW1);
-    float* b1s = reinterpret_cast<float*>(sm + CU::kOffB1);
-    float* Tring = reinterpret_cast<float*>(sm + CU::kOffT);
-    float* xvs = reinterpret_cast<float*>(sm + CU::kOffXv);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + CU::kOffBar);
-    uint64_t* a_full = bars;                   // [NA]
-    uint64_t* a_empty = bars + NA;             // [NA]
-    uint64_t* acc_full = bars + 2 * NA;        // [NACC]
-    uint64_t* acc_empty = bars + 2 * NA + NACC;
-    uint64_t* rowpub = bars + 2 * NA + 2 * NACC;              // [kUniRing]
-    uint64_t* rowfree = rowpub + kUniRing;                    // [kUniRing]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rowfree + kUniRing);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n = a.rows;
-    // ---- stage weights: B[dx][row = dy*C2 + co][ci] = W2[co][ci][dy][dx] (hi / lo tf32)
-    for (int e = threadIdx.x; e < 3 * NB * C1; e += kThreads) {
-        const int dx = e / (NB * C1), rem = e - dx * NB * C1;
-        const int row = rem / C1, ci = rem - row * C1;
-        const int dy = row / C2, co = row - dy * C2;
-        const float v = a.w2[((co * C1 + ci) * 3 + dy) * 3 + dx];
-        const float h = ptx::tf32_round(v);
-        const uint32_t off = sw128(row, ci * 4);
-        *reinterpret_cast<float*>(sm + CU::kOffB + (dx * 2 + 0) * CU::kBTile + off) = h;
-        *reinterpret_cast<float*>(sm + CU::kOffB + (dx * 2 + 1) * CU::kBTile + off) = v - h;
-    }
-    for (int e = threadIdx.x; e < NA * 2 * 8 * 32; e += kThreads) {  // zero pad rows of A slots
-        const int tile = e / (8 * 32), rem = e - tile * 8 * 32;
-        const int pr = rem >> 5, k = rem & 31;
-        const int row = pr == 0 ? 0 : 128 + pr;
-        *reinterpret_cast<float*>(sm + CU::kOffA + tile * CU::kATile + sw128(row, k * 4)) = 0.f;
-    }
-    for (int e = threadIdx.x; e < C1 * 18; e += kThreads) {
-        const int c = e / 18, k = e - c * 18;
-        w1s[((c >> 1) * kW1Stride + k) * 2 + (c & 1)] = a.w1[c * 18 + k];
-    }
-    for (int e = threadIdx.x; e < C1; e += kThreads) b1s[e] = a.b1[e];
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NA; ++s) {
-            ptx::mbar_init(&a_full[s], 128);
-            ptx::mbar_init(&a_empty[s], 1);
-        }
-        for (int q = 0; q < NACC; ++q) {
-            ptx::mbar_init(&acc_full[q], 1);
-            ptx::mbar_init(&acc_empty[q], 12);  // 3 reading rows x 4 warps
-        }
-        for (int s = 0; s < kUniRing; ++s) {
-            ptx::mbar_init(&rowpub[s], 128);
-            ptx::mbar_init(&rowfree[s], 256);   // read by rows E + 1 and E + 2
-        }
-        ptx::fence_barrier_init();
-    }
-    if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
-    ptx::fence_proxy_async_smem();
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const int64_t n_mem = a.n_members > blockIdx.x ? (a.n_members - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int64_t total = n_mem * n;  // this CTA's rows, global index R = it * n + r
-    if (warp == 0) {
-        // ================= MMA issuer (as cnn3_tc_kernel<true>) =================
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_tf32(W, NB);
-            const uint64_t dA0 = ptx::desc_kmajor_sw128(sm + CU::kOffA);
-            const uint64_t dB0 = ptx::desc_kmajor_sw128(sm + CU::kOffB);
-            constexpr uint64_t kAT = CU::kATile >> 4, kBT = CU::kBTile >> 4;
-            const bool do_mma = !(a.debug & 1), p3 = a.products == 3;
-            for (int64_t Rg = 0; Rg < total; ++Rg) {
-                const int slot = (int)(Rg % NA);
-                ptx::mbar_wait(&a_full[slot], (uint32_t)((Rg / NA) & 1));
-                ptx::tc_fence_after();
-                const uint64_t dah0 = dA0 + (uint64_t)(slot * 2) * kAT, dal0 = dah0 + kAT;
-                const int q = (int)(Rg % NACC);
-                ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Rg / NACC) & 1) ^ 1));
-                ptx::tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)(q * NB);
-                if (do_mma) {
-#pragma unroll
-                    for (int dx = 0; dx < 3; ++dx) {
-                        const uint64_t bh0 = dB0 + (uint64_t)(dx * 2) * kBT;
-#pragma unroll
-                        for (int k = 0; k < C1 / 8; ++k) {
-                            const uint64_t adh = dah0 + (uint64_t)(dx * 8 + 2 * k);
-                            const uint64_t adl = dal0 + (uint64_t)(dx * 8 + 2 * k);
-                            const uint64_t bdh = bh0 + (uint64_t)(2 * k), bdl = bdh + kBT;
-                            const uint32_t acc0 = (dx == 0 && k == 0) ? 0u : 1u;
-                            if (p3) ptx::mma_tf32_ss(d, adl, bdh, idesc, acc0);
-                            ptx::mma_tf32_ss(d, adh, bdl, idesc, p3 ? 1u : acc0);
-                            ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
-                        }
-                    }
-                }
-                ptx::mma_commit(&acc_full[q]);
-                ptx::mma_commit(&a_empty[slot]);
-            }
-        }
-    } else if (warp >= 4) {
-        // ================= uniform SIMT warpgroups: thread = pixel = TMEM lane =================
-        const int g = (warp - 4) >> 2;
-        const int ew = warp & 3;
-        const int x = ew * 32 + lane;
-        const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
-        const int bar_id = 1 + g;
-        float* stage = reinterpret_cast<float*>(sm + CU::kOffStage) + g * CU::kStageF;
-        const float b3 = c_epi.b3;
-        auto mem_of = [&](int64_t Rg) { return (int64_t)blockIdx.x + (Rg / n) * gridDim.x; };
-        // input rows r-1..r+1 of row Rg into registers (zero outside the image / columns)
-        auto fetch3 = [&](int64_t Rg, float (&vx)[3], float (&vu)[3]) {
-            const int64_t mem = mem_of(Rg);
-            const int r = (int)(Rg % n);
-            const bool col_ok = mem * W + x < a.cols_total;
-            const float* xm = a.x + mem * W;
-            const float* um = a.u + mem * W;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const int j = r + k - 1;
-                const bool ok = col_ok && j >= 0 && j < n;
-                vx[k] = ok ? xm[(int64_t)j * a.ldx + x] : 0.f;
-                vu[k] = ok ? um[(int64_t)j * a.ldu + x] : 0.f;
-            }
-        };
-        float px[3], pu[3];
-        if (g < total) fetch3(g, px, pu);
-        int buf = 0;
-        for (int64_t R = g; R < total + 3; R += 3) {
-            // ---------------- layer 1 of row R ----------------
-            if (R < total) {
-                float* st = stage + buf * (3 * 2 * kInRow);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    st[(k * 2 + 0) * kInRow + x + 1] = px[k];
-                    st[(k * 2 + 1) * kInRow + x + 1] = pu[k];
-                    if (x == 0) {
-                        st[(k * 2 + 0) * kInRow] = 0.f; st[(k * 2 + 0) * kInRow + kInRow - 1] = 0.f;
-                        st[(k * 2 + 1) * kInRow] = 0.f; st[(k * 2 + 1) * kInRow + kInRow - 1] = 0.f;
-                    }
-                }
-                if (R + 3 < total) fetch3(R + 3, px, pu);  // next row's inputs in flight
-                asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-                float in[18];
-#pragma unroll
-                for (int ci = 0; ci < 2; ++ci)
-#pragma unroll
-                    for (int ky = 0; ky < 3; ++ky) {
-                        const float* src = st + (ky * 2 + ci) * kInRow + x;
-                        in[ci * 9 + ky * 3 + 0] = src[0];
-                        in[ci * 9 + ky * 3 + 1] = src[1];
-                        in[ci * 9 + ky * 3 + 2] = src[2];
-                    }
-                buf ^= 1;
-                const int slot = (int)(R % NA);
-                ptx::mbar_wait(&a_empty[slot], (uint32_t)(((R / NA) & 1) ^ 1));
-                uint8_t* ah_t = sm + CU::kOffA + (slot * 2 + 0) * CU::kATile;
-                uint8_t* al_t = sm + CU::kOffA + (slot * 2 + 1) * CU::kATile;
-#pragma unroll 2
-                for (int c4 = 0; c4 < ((a.debug & 2) ? 0 : C1 / 4); ++c4) {
-                    float hv[4];
-#pragma unroll
-                    for (int pr = 0; pr < 2; ++pr) {
-                        const int cp = c4 * 2 + pr;
-                        const float4* wr = reinterpret_cast<const float4*>(w1s + cp * kW1Stride * 2);
-                        float2 acc = make_float2(b1s[2 * cp], b1s[2 * cp + 1]);
-#pragma unroll
-                        for (int q = 0; q < 9; ++q) {
-                            const float4 wv = wr[q];
-                            acc = __ffma2_rn(make_float2(wv.x, wv.y), make_float2(in[2 * q], in[2 * q]), acc);
-                            acc = __ffma2_rn(make_float2(wv.z, wv.w),
-                                             make_float2(in[2 * q + 1], in[2 * q + 1]), acc);
-                        }
-                        const float2 t2 = tanh2_fast(acc);
-                        hv[2 * pr] = t2.x;
-                        hv[2 * pr + 1] = t2.y;
-                    }
-                    float4 h4, l4;
-                    h4.x = ptx::tf32_round(hv[0]); l4.x = hv[0] - h4.x;
-                    h4.y = ptx::tf32_round(hv[1]); l4.y = hv[1] - h4.y;
-                    h4.z = ptx::tf32_round(hv[2]); l4.z = hv[2] - h4.z;
-                    h4.w = ptx::tf32_round(hv[3]); l4.w = hv[3] - h4.w;
-                    const uint32_t off = sw128(x + 1, c4 * 16);
-                    *reinterpret_cast<float4*>(ah_t + off) = h4;
-                    *reinterpret_cast<float4*>(al_t + off) = l4;
-                }
-                ptx::fence_proxy_async_smem();
-                ptx::mbar_arrive(&a_full[slot]);
-            }
-            // ---------------- epilogue of row E = R - 3 ----------------
-            const int64_t E = R - 3;
-            if (E < 0 || E >= total) continue;
-            const int e = (int)(E % n);  // local row
-            const int64_t mem = mem_of(E);
-            const bool col_ok = mem * W + x < a.cols_total;
-            const float* xm = a.x + mem * W;
-            float* om = a.out + mem * W;
-            // residual inputs of the outputs this row finishes (E - 1, and E itself at the bottom)
-            const float xr_m = (e >= 1 && col_ok) ? xm[(int64_t)(e - 1) * a.ldx + x] : 0.f;
-            const float xr_0 = (e == n - 1 && col_ok) ? xm[(int64_t)e * a.ldx + x] : 0.f;
-            auto acc_addr = [&](int64_t J) {
-                return tmem + lane_base + (uint32_t)((J % NACC) * NB);
-            };
-            auto wait_acc = [&](int64_t J) {
-                ptx::mbar_wait(&acc_full[J % NACC], (uint32_t)((J / NACC) & 1));
-                ptx::tc_fence_after();
-            };
-            float s[32];
-            uint32_t v[32];
-            wait_acc(E);
-            ptx::tmem_ld_32x32b_x32(acc_addr(E) + C2, v);  // D_E[dy = 1]
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) s[c] = __uint_as_float(v[c]);
-            auto add_into = [&]() {
-#pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                    const float2 t = __fadd2_rn(make_float2(s[c], s[c + 1]),
-                                                make_float2(__uint_as_float(v[c]),
-                                                            __uint_as_float(v[c + 1])));
-                    s[c] = t.x;
-                    s[c + 1] = t.y;
-                }
-            };
-            if (e >= 1) {
-                wait_acc(E - 1);
-                ptx::tmem_ld_32x32b_x32(acc_addr(E - 1), v);  // D_{E-1}[dy = 0]
-                ptx::tmem_ld_wait();
-                add_into();
-            }
-            if (e + 1 < n) {
-                wait_acc(E + 1);
-                ptx::tmem_ld_32x32b_x32(acc_addr(E + 1) + 2 * C2, v);  // D_{E+1}[dy = 2]
-                ptx::tmem_ld_wait();
-                add_into();
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {  // this row's reads of D_{E-1}, D_E, D_{E+1} are done
-                ptx::mbar_arrive(&acc_empty[E % NACC]);
-                if (e == 0 || e == n - 1) ptx::mbar_arrive(&acc_empty[E % NACC]);  // edge: 2 readers
-                if (e >= 1) ptx::mbar_arrive(&acc_empty[(E - 1) % NACC]);
-                if (e + 1 < n) ptx::mbar_arrive(&acc_empty[(E + 1) % NACC]);
-            }
-            // layer-2 bias + tanh and the nine layer-3 taps v[ky][kx] = sum_c w3 h
-            float2 v01[4], v23[4], v45[4], v67[4];
-            float v8[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                v01[q] = v23[q] = v45[q] = v67[q] = make_float2(0.f, 0.f);
-                v8[q] = 0.f;
-            }
-#pragma unroll
-            for (int c = 0; c < ((a.debug & 4) ? 0 : 32); c += 2) {
-                const float2 h2 = tanh2_fast(__fadd2_rn(make_float2(s[c], s[c + 1]),
-                                                        make_float2(c_epi.b2[c], c_epi.b2[c + 1])));
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int cc = c + u, q = cc & 3;
-                    const float h = u ? h2.y : h2.x;
-                    const float2 hh = make_float2(h, h);
-                    const float4 w0 = *reinterpret_cast<const float4*>(&c_epi.w3[cc][0]);
-                    const float4 w1 = *reinterpret_cast<const float4*>(&c_epi.w3[cc][4]);
-                    v01[q] = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01[q]);
-                    v23[q] = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23[q]);
-                    v45[q] = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45[q]);
-                    v67[q] = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67[q]);
-                    v8[q] = fmaf(c_epi.w3[cc][8], h, v8[q]);
-                }
-            }
-#pragma unroll
-            for (int q = 1; q < 4; ++q) {
-                v01[0].x += v01[q].x; v01[0].y += v01[q].y;
-                v23[0].x += v23[q].x; v23[0].y += v23[q].y;
-                v45[0].x += v45[q].x; v45[0].y += v45[q].y;
-                v67[0].x += v67[q].x; v67[0].y += v67[q].y;
-                v8[0] += v8[q];
-            }
-            const float vv[9] = {v01[0].x, v01[0].y, v23[0].x, v23[0].y, v45[0].x,
-                                 v45[0].y, v67[0].x, v67[0].y, v8[0]};
-            // horizontal fold: lane x takes v[ky][0] from x - 1 and v[ky][2] from x + 1; the warp
-            // boundaries go through a per-warpgroup exchange, double-buffered by row parity (a
-            // warp may run one row ahead of the group's barrier at the tail)
-            float* xvA = xvs + ((g * 2 + (int)((E / 3) & 1)) * 2 + 0) * 16;  // v[ky][0] of lane 31
-            float* xvB = xvA + 16;                                            // v[ky][2] of lane 0
-            float tk[3];
-#pragma unroll
-            for (int ky = 0; ky < 3; ++ky) {
-                const float up = __shfl_up_sync(0xffffffffu, vv[ky * 3 + 0], 1);
-                const float dn = __shfl_down_sync(0xffffffffu, vv[ky * 3 + 2], 1);
-                tk[ky] = vv[ky * 3 + 1] + (lane == 0 ? 0.f : up) + (lane == 31 ? 0.f : dn);
-                if (lane == 31) xvA[ew * 4 + ky] = vv[ky * 3 + 0];
-                if (lane == 0) xvB[ew * 4 + ky] = vv[ky * 3 + 2];
-            }
-            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-            if (lane == 0 && ew > 0) {
-#pragma unroll
-                for (int ky = 0; ky < 3; ++ky) tk[ky] += xvA[(ew - 1) * 4 + ky];
-            }
-            if (lane == 31 && ew < 3) {
-#pragma unroll
-                for (int ky = 0; ky < 3; ++ky) tk[ky] += xvB[(ew + 1) * 4 + ky];
-            }
-            // vertical fold across warpgroups: publish tk0 (output E + 1) and tk1 (output E)
-            const int slot = (int)(E % kUniRing);
-            if (E >= kUniRing)  // rows E - 6 + 1 and E - 6 + 2 have read this slot
-                ptx::mbar_wait(&rowfree[slot], (uint32_t)(((E / kUniRing) - 1) & 1));
-            float* T0 = Tring + slot * 2 * W;
-            T0[x] = tk[0];
-            T0[W + x] = tk[1];
-            ptx::mbar_arrive(&rowpub[slot]);
-            // finish output row E - 1 = T0[E - 2] + T1[E - 1] + tk2 (same image only)
-            float t0m = 0.f, t1m = 0.f, t0e1 = 0.f;
-            if (E >= 1) {
-                const int s1 = (int)((E - 1) % kUniRing);
-                ptx::mbar_wait(&rowpub[s1], (uint32_t)(((E - 1) / kUniRing) & 1));
-                if (e >= 1) t1m = Tring[s1 * 2 * W + W + x];
-                t0e1 = Tring[s1 * 2 * W + x];  // T0[E - 1] (for output E at the image bottom)
-            }
-            if (E >= 2) {
-                const int s2 = (int)((E - 2) % kUniRing);
-                ptx::mbar_wait(&rowpub[s2], (uint32_t)(((E - 2) / kUniRing) & 1));
-                if (e >= 2) t0m = Tring[s2 * 2 * W + x];
-            }
-            if (E >= 1) ptx::mbar_arrive(&rowfree[(E - 1) % kUniRing]);
-            if (E >= 2) ptx::mbar_arrive(&rowfree[(E - 2) % kUniRing]);
-            if (e >= 1 && col_ok)
-                om[(int64_t)(e - 1) * a.ldo + x] = xr_m + a.alpha * (b3 + (t0m + t1m + tk[2]));
-            if (e == n - 1 && col_ok)
-                om[(int64_t)e * a.ldo + x] = xr_0 + a.alpha * (b3 + ((e >= 1 ? t0e1 : 0.f) + tk[1]));
-        }
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 2) ptx::tmem_dealloc(tmem, 512);
-}
-
 __global__ void cnn3_epi_pack_kernel(const float* __restrict__ b2, const float* __restrict__ w3,
                                      const float* __restrict__ b3, Cnn3Epi* __restrict__ out) {
     for (int e = threadIdx.x; e < C2 * kW3Stride; e += blockDim.x) {
@@ -1207,26 +839,8 @@ int cnn3_tc_forward(const float* weights, const float* biases, float alpha, cons
                               n_members, st, nullptr);
 }
 
-int launch_cnn3_uni(const Cnn3Args& a, int grid, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(cnn3_uni_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, CU::kSmem);
-        if (e != cudaSuccess) {
-            set_error("cnn3_uni: smem attribute: %s", cudaGetErrorString(e));
-            return ENKS_E_CUDA;
-        }
-        configured = true;
-    }
-    cnn3_uni_kernel<<<grid, kThreads, CU::kSmem, st>>>(a);
-    return check_launch("enks_cnn_forward(tcgen05, uniform warpgroups)");
-}
-
 template <bool SH>
 int launch_cnn3(const Cnn3Args& a, int grid, cudaStream_t st) {
-    // 128-pixel images without in-kernel noise: the uniform-warpgroup kernel (ENKS_CNN_UNI=0:
-    // the producer / epilogue-role kernel)
-    if (SH && a.nz.n_jobs == 0 && env_knob("ENKS_CNN_UNI", 1) != 0) return launch_cnn3_uni(a, grid, st);
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(cnn3_tc_kernel<SH>,
