@@ -20,6 +20,8 @@ ap.add_argument("--config", default="C3")
 ap.add_argument("--members", type=int, default=None)
 ap.add_argument("--horizon", type=int, default=None)
 ap.add_argument("--steps", default="1,2,25,26")
+ap.add_argument("--sim-ranks", type=int, default=1,
+                help="rank 0 of a simulated R-rank job (engine.SimComm, N/R members)")
 a = ap.parse_args()
 pm = problems.product_modules()
 pr = problems.make_cnn_problem(pm, a.config, n_members=a.members, horizon=a.horizon)
@@ -53,14 +55,17 @@ ops._prof = _prof
 _lib.call = _call
 streams = pm.matvar.NoiseStreams(seed=0)
 yref = ops.to_device(np.broadcast_to(pr.y_ref, (pr.H,) + pr.y_ref.shape).copy())
+from paper_2410_09663_b200.engine import SimComm  # noqa: E402
+
+comm = SimComm(a.sim_ranks) if a.sim_ranks > 1 else None
 for _ in range(2):
-    enks.smooth_horizon_device(pr.x0, yref, pr.vs, pr.H, pr.N, streams)
+    enks.smooth_horizon_device(pr.x0, yref, pr.vs, pr.H, pr.N, streams, comm=comm)
 torch.cuda.synchronize()
 ops.profile = []
 base = torch.cuda.Event(enable_timing=True)
 end = torch.cuda.Event(enable_timing=True)
 base.record()
-enks.smooth_horizon_device(pr.x0, yref, pr.vs, pr.H, pr.N, streams)
+enks.smooth_horizon_device(pr.x0, yref, pr.vs, pr.H, pr.N, streams, comm=comm)
 end.record()
 torch.cuda.synchronize()
 prof, ops.profile = ops.profile, None
