@@ -862,24 +862,37 @@ class DeviceSmoother:
         tri = (ds, p) if a0 == ds else (0, 0)
         gcol = self.G[a0:rows_a, (tau - 1) * p:tau * p]
         r0 = tau * d
+        # under sharding the correction and gain GEMMs are row-sharded: this rank owns a
+        # contiguous run of slices [s_lo, s_lo + s_cnt) (rows lo..hi of S), and the gain rows are
+        # allgathered afterwards so G stays replicated (mean / shift / readback read all of it)
+        nsl = (rows_a - a0) // ds
+        s_lo, s_cnt = partition(nsl, comm.size, comm.rank) if comm.size > 1 else (0, nsl)
+        lo, hi = s_lo * ds, (s_lo + s_cnt) * ds
+        kk = (tau - 1) * p
+        k0 = min(s_lo * p, kk) if tri[0] else 0  # block-triangular: owned slices skip early K
+        PAo, Go = PA[lo:hi], self.G[a0 + lo:a0 + hi]
         if self.use_tc2:
             if tau > 1:
-                kk = (tau - 1) * p
                 pth = self.pyT_hi[:p * kk].view(p, kk)
                 ptl = self.pyT_lo[:p * kk].view(p, kk)
                 ops.tf32_split(self.PY[:kk], pth, ptl, transpose=True)
-                ops.gemm_tc(self.G[a0:rows_a, :kk], pth, ptl, PA, alpha=-1.0, beta=1.0, C0=PA,
-                            tri=tri, tag="correction")
+                if hi > lo and kk > k0:
+                    ops.gemm_tc(Go[:, k0:kk], pth[:, k0:], ptl[:, k0:], PAo, alpha=-1.0, beta=1.0,
+                                C0=PAo, tri=tri, tag="correction")
             # G_{tau,s} = (lam/N) S_s Sigma_y^{-1}
             self._join_side(side)
             ops.tf32_split(self.sinv, self.sinvT_hi, self.sinvT_lo, transpose=True)
-            ops.gemm_tc(PA, self.sinvT_hi, self.sinvT_lo, gcol, alpha=scale, tag="gain")
+            if hi > lo:
+                ops.gemm_tc(PAo, self.sinvT_hi, self.sinvT_lo, gcol[lo:hi], alpha=scale,
+                            tag="gain")
         else:
-            if tau > 1:
-                ops.gemm(self.G[a0:rows_a, :(tau - 1) * p], self.PY[:(tau - 1) * p], PA,
-                         alpha=-1.0, beta=1.0, C0=PA, tri=tri)
+            if tau > 1 and hi > lo and kk > k0:
+                ops.gemm(Go[:, k0:kk], self.PY[k0:kk], PAo, alpha=-1.0, beta=1.0, C0=PAo, tri=tri)
             self._join_side(side)
-            ops.gemm(PA, self.sinv, gcol, alpha=scale)
+            if hi > lo:
+                ops.gemm(PAo, self.sinv, gcol[lo:hi], alpha=scale)
+        if comm.size > 1:
+            self._allgather_gain_rows(gcol, nsl, ds)
         if self.record is not None:
             self._record_step(tau, a0, rows_a, scale)
         # mean_s += G_{tau,s} (y_ref - y_bar)   (enks.py:247-248 on the mean)
@@ -919,6 +932,23 @@ class DeviceSmoother:
             ops.gemm(g_tt, yc, self.last, alpha=-1.0, beta=1.0, C0=a_new[:q],
                      bias=self.mean[r0:r0 + q], bias_cols=self.m)
         self._last_stale = False
+
+    def _allgather_gain_rows(self, gcol, nsl: int, ds: int) -> None:
+        """Every rank's gain rows (slice-aligned, uneven) into every rank's G column block: one
+        all-gather of equal padded row blocks through a staging buffer."""
+        comm, p = self.comm, self.p
+        per = -(-nsl // comm.size) * ds
+        if getattr(self, "_gstage", None) is None or self._gstage.shape[0] < per:
+            self._gstage = self.ops.empty(max(per, ds), p)
+        st = self._gstage[:per]
+        s_lo, s_cnt = partition(nsl, comm.size, comm.rank)
+        if s_cnt:
+            st[:s_cnt * ds].copy_(gcol[s_lo * ds:(s_lo + s_cnt) * ds])
+        full = comm.all_gather_rows(st)
+        for r in range(comm.size):
+            r_lo, r_cnt = partition(nsl, comm.size, r)
+            if r_cnt and r != comm.rank:
+                gcol[r_lo * ds:(r_lo + r_cnt) * ds].copy_(full[r * per:r * per + r_cnt * ds])
 
     def _zero_obs_block(self, tau: int) -> None:
         """Zero the basis rows of Yc_tau and the gain column block of step tau."""
@@ -996,7 +1026,10 @@ class DeviceSmoother:
     def _record_step(self, tau: int, a0: int, rows_a: int, scale: float) -> None:
         """Append this update's Sigma_y (p x p, symmetrised as enks.py:234), Sigma_xy
         (T d x p, enks.py:235-236) and gain (T d x p, enks.py:246) as fp64 host arrays to
-        ``self.record`` -- the same keys as the oracle's ``record=`` hook.  Test-only: syncs."""
+        ``self.record`` -- the same keys as the oracle's ``record=`` hook.  Test-only: syncs;
+        single rank (under sharding each rank corrects only its own rows of P)."""
+        if self.comm.size > 1:
+            raise RuntimeError("record= is single-rank only")
         if self.ops.device.type == "cuda":
             torch.cuda.synchronize(self.ops.device)
         p = self.p

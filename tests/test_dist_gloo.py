@@ -113,6 +113,10 @@ def _count_worker(rank, world, port, out):
             self.calls.append(("broadcast", t.numel()))
             return super().broadcast_(t, src)
 
+        def all_gather_rows(self, t):
+            self.calls.append(("all_gather", t.numel()))
+            return super().all_gather_rows(t)
+
     comm = Counting()
     eng = _run("cnn", comm, "f16pair")
     if rank == 0:
@@ -123,15 +127,18 @@ def _count_worker(rank, world, port, out):
 
 
 def test_collectives_per_step(tmp_path):
-    """three collectives per predict+update under member sharding (fused noise and
-    observation path) -- the slice + observation member sums, the Sigma_y block, and the rest of
-    the cross moments -- and no broadcast (each rank centres relative to its own first member)."""
+    """four collectives per predict+update under member sharding (fused noise and
+    observation path) -- the slice + observation member sums, the Sigma_y block, the rest of the
+    cross moments (one coalesced group), and the all-gather of the row-sharded gain rows -- and
+    no broadcast (each rank centres relative to its own first member)."""
     out = str(tmp_path / "c.npz")
     mp.spawn(_count_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     got = np.load(out)
+    kinds = got["kinds"].tolist()
     assert int(got["fused"]) == 1
-    assert "broadcast" not in set(got["kinds"].tolist())
-    assert int(got["n"]) == 3 * int(got["h"])
+    assert "broadcast" not in set(kinds)
+    assert int(got["n"]) == 4 * int(got["h"])
+    assert kinds.count("all_gather") == int(got["h"])
 
 
 def _cov_run(comm):
