@@ -208,9 +208,12 @@ struct SegPlan {
 };
 SegPlan seg_plan(int64_t n_streams, int64_t max_normals) {
     SegPlan P;
-    if (n_streams <= 0 || n_streams >= 8LL * kNumSMs) return P;
+    // target resident warps per SM (tuning; ENKS_NOISE_WARPS, read once): below half of it the
+    // substreams are cut into chunks so that the latency-bound per-warp parse has company
+    const int64_t target = env_knob("ENKS_NOISE_WARPS", 16);
+    if (n_streams <= 0 || 2 * n_streams >= target * kNumSMs) return P;
     const int64_t groups = (max_normals * 104 / 100 + 64 + 31) / 32;  // ~1.5 % rejected starts
-    int64_t chunks = (16LL * kNumSMs + n_streams - 1) / n_streams;
+    int64_t chunks = (target * kNumSMs + n_streams - 1) / n_streams;
     if (chunks > groups / 8) chunks = groups / 8;  // >= 8 groups per chunk
     if (chunks < 2) return P;
     P.n_chunks = (int)chunks;

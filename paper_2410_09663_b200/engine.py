@@ -1080,6 +1080,16 @@ class DeviceSmoother:
             out[:self.d] = self.x0_exact  # identical copies: slice 0 is x0 itself, in fp64
         return out
 
+    def clear_flags(self) -> None:
+        """Per-solve device flags back to a fresh engine's: failure status, jitter count and the
+        Burgers CFL maxima (a reused engine must not inherit an earlier solve's failure)."""
+        self.status.zero_()
+        self.jitter.zero_()
+        fc = getattr(self, "forecast", None)
+        if fc is not None and fc.kind == "burgers":
+            fc.vmax.zero_()
+            fc.flags.zero_()
+
     def jitter_events(self) -> int:
         return int(self.ops.read_scalar(self.jitter))
 
