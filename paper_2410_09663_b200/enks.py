@@ -304,35 +304,6 @@ def _graph_for(x0, vs, h, n_members, streams):
     return g
 
 
-_ENGINES: dict = {}
-
-
-def _engine_for(x0, vs, h, n_members):
-    """A cached horizon engine for eager smooth_horizon calls on the same (virtual system,
-    shapes, h, N): its device buffers (the append-only basis, gains, workspaces) are reused and
-    reset to N identical copies of x0 instead of being reallocated and zero-filled every call.
-    None (fresh engine) when it would exceed the cache budget.  The engine never escapes: each
-    call returns host arrays, and the next call's reset starts a new horizon."""
-    if not torch.cuda.is_available():
-        return None
-    key = (id(vs), id(vs.model), tuple(np.shape(x0.packed)), x0.n, x0.l, int(h), int(n_members),
-           id(_COMM))
-    e = _ENGINES.get(key)
-    if e is not None and e[0] is vs:
-        return e[1]
-    budget = GRAPH_CACHE_FRACTION * torch.cuda.get_device_properties(
-        torch.cuda.current_device()).total_memory
-    d, p, m = x0.n + 2 * x0.l, x0.n + x0.l, np.shape(x0.packed)[1]
-    est = 4.4 * ((h + 1) * p + h * p) * n_members * m + 4 * (h + 1) * d * m
-    if est > budget:
-        return None
-    while _ENGINES and sum(v[1].memory_bytes() for v in _ENGINES.values()) + est > budget:
-        _ENGINES.pop(next(iter(_ENGINES)))
-    eng = init_ensemble(x0, n_members, shared_col_cov=vs.shared_col_cov, capacity=h)._eng
-    _ENGINES[key] = (vs, eng)
-    return eng
-
-
 def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
                    track_cov: bool = False, *, graph: bool = False):
     """Forward predict/update sweep over an h-step horizon (enks.py:256-284).
@@ -367,13 +338,8 @@ def smooth_horizon(x0, y_refs: np.ndarray, vs, h: int, n_members: int, streams,
         return eng.mean_host().reshape(h + 1, eng.d, eng.m), None
     if n_members < 2:
         raise ValueError("need at least 2 ensemble members")
-    eng = _engine_for(x0, vs, h, n_members)
-    if eng is None:
-        eng = init_ensemble(x0, n_members, shared_col_cov=vs.shared_col_cov, capacity=h)._eng
-    else:  # the same N identical copies of x0 (enks.py:105-128) in reused device buffers
-        eng.reset(np.asarray(x0.packed, dtype=float))
-        eng.clear_flags()
-    ens = TrajectoryEnsemble(_engine=eng)
+    ens = init_ensemble(x0, n_members, shared_col_cov=vs.shared_col_cov, capacity=h)
+    eng = ens._eng
     eng.bind(vs)
     yref_dev = eng.ops.to_device(np.ascontiguousarray(y_refs))
     cov = SmootherCovariances(sigma_traj=np.zeros((eng.d, eng.d))) if track_cov else None

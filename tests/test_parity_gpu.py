@@ -283,32 +283,3 @@ def test_smooth_horizon_c4_shape_matches_oracle(pm):
     n, l = pr.n, pr.l
     assert _rel(got, ref) < TOL
     assert _rel(got[:, n:n + l], ref[:, n:n + l]) < TOL
-
-
-def test_smooth_horizon_engine_reuse_is_a_fresh_solve(pm):
-    """Eager smooth_horizon reuses a cached engine's device buffers for the same (vs, shapes, h,
-    N): every call must equal a solve on a freshly allocated engine, including after a call whose
-    Cholesky needed jitter (scale = 0) and across different x0."""
-    from oracle import problems
-    from paper_2410_09663_b200 import enks
-
-    pr = problems.make_cnn_problem(pm, "C1", size=32, n_members=48, horizon=3,
-                                   widths=(2, 32, 32, 1))
-    st = pm.matvar.NoiseStreams(seed=8)
-    x1 = pm.virtualsys.AugmentedState(0.5 * pr.x0.x, pr.x0.u, pr.x0.du)
-    enks._ENGINES.clear()
-    fresh_a, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, st)
-    enks._ENGINES.clear()
-    fresh_b, _ = enks.smooth_horizon(x1, pr.y_ref, pr.vs, pr.H, pr.N, st)
-    a1, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, st)  # reuses the engine of b
-    b1, _ = enks.smooth_horizon(x1, pr.y_ref, pr.vs, pr.H, pr.N, st)
-    assert len(enks._ENGINES) == 1
-    assert np.array_equal(a1, fresh_a) and np.array_equal(b1, fresh_b)
-    # a degenerate solve (jittered Cholesky, scale = 0) on a cached engine, then a normal one
-    model, vs0, x0 = _linear_case(pm, 14, scale=0.0)
-    y0 = np.vstack([vs0.weights.x_ref, vs0.weights.u_ref])
-    d1, _ = enks.smooth_horizon(x0, y0, vs0, 2, 8, st)
-    d2, _ = enks.smooth_horizon(x0, y0, vs0, 2, 8, st)
-    assert np.array_equal(d1, d2)
-    a2, _ = enks.smooth_horizon(pr.x0, pr.y_ref, pr.vs, pr.H, pr.N, st)
-    assert np.array_equal(a2, fresh_a)
