@@ -166,9 +166,42 @@ struct Cnn3Args {
     int debug;  // ENKS_CNN_DEBUG: 1 = no MMAs, 2 = no layer-1 math, 4 = no epilogue math
     int products;  // 3 (default): lo*hi + hi*lo + hi*hi; 2 (ENKS_CNN_PRODUCTS=2): hi*lo + hi*hi
     NoiseLaunch nz;  // nz.n_jobs > 0: warps 1-3 draw these noise jobs (member-column layout)
+    int parts;       // 128-pixel images: each image's rows split into `parts` units (small N)
 };
 
-template <bool SH>
+// A unit of work: output rows [o0, o1) of one image, which need layer-2 (h2) rows [e0, e1) and
+// layer-1 rows [l0, l1) (the 3x3 layer-3 and layer-2 taps: a two-row halo of recomputation at an
+// interior cut; image edges keep the zero 'same' padding).  parts == 1: the whole image.
+struct Unit {
+    int mem;
+    int o0, o1, e0, e1, l0, l1;
+};
+// 32-bit arithmetic only: a 64-bit division here compiles to a helper call, and a call inside the
+// MMA issuer's loop corrupts the uniform-register descriptors of the tcgen05.mma that follow
+// (garbage accumulators in the first rows -- measured)
+template <bool SPLIT>
+__device__ __forceinline__ Unit unit_of(const Cnn3Args& a, int u) {
+    Unit U;
+    const int n = a.rows;
+    if constexpr (!SPLIT) {  // whole images: the ranges fold to constants
+        U.mem = u;
+        U.o0 = U.e0 = U.l0 = 0;
+        U.o1 = U.e1 = U.l1 = n;
+        return U;
+    }
+    const int S = a.parts;
+    U.mem = u / S;
+    const int part = u - U.mem * S;
+    U.o0 = part * n / S;
+    U.o1 = (part + 1) * n / S;
+    U.e0 = max(0, U.o0 - 1);
+    U.e1 = min(n, U.o1 + 1);
+    U.l0 = max(0, U.o0 - 2);
+    U.l1 = min(n, U.o1 + 2);
+    return U;
+}
+
+template <bool SH, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) {
     using L = CL<SH>;
     extern __shared__ uint8_t smem_raw[];
@@ -268,19 +301,23 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
             const uint64_t dB0 = ptx::desc_kmajor_sw128(sm + L::kOffB);
             constexpr uint64_t kAT = L::kATile >> 4, kBT = L::kBTile >> 4;
             const bool do_mma = !(a.debug & 1), p3 = a.products == 3;
-            int it = 0;
-            for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
-                for (int r = 0; r < n; ++r) {
-                    const int Rg = it * n + r;
+            int Lbase = 0;  // layer-1 rows of this CTA's earlier units (ring / slot counter)
+            const int n_units = (int)(a.n_members * a.parts);
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const Unit U = unit_of<SPLIT>(a, u);
+                const int Lb = Lbase - U.l0;
+                Lbase += U.l1 - U.l0;
+                for (int r = U.l0; r < U.l1; ++r) {
+                    const int Rg = Lb + r;
                     const int slot = Rg % NA;
                     ptx::mbar_wait(&a_full[slot], (uint32_t)((Rg / NA) & 1));
-                    ptx::tc_fence_after();
+                                        ptx::tc_fence_after();
                     const uint64_t dah0 = dA0 + (uint64_t)(slot * 2) * kAT, dal0 = dah0 + kAT;
                     if constexpr (SH) {
                         // D_r[x][(dy, co)] = sum_dx sum_ci h1[r][x + dx - 1][ci] W2[co][ci][dy][dx]
                         const int q = Rg % NACC;
                         ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Rg / NACC) & 1) ^ 1));
-                        ptx::tc_fence_after();
+                                                ptx::tc_fence_after();
                         const uint32_t d = tmem + (uint32_t)(q * L::kAccCols);
                         if (do_mma) {
 #pragma unroll
@@ -299,16 +336,16 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                             }
                         }
                         ptx::mma_commit(&acc_full[q]);
-                    } else {
+                                            } else {
                         for (int dy = 0; dy < 3; ++dy) {
                             const int y = r - dy + 1;
                             if (y < 0 || y >= n) continue;
-                            const int Yg = it * n + y;
+                            const int Yg = Lb + y;  // (parts == 1 off the SH path)
                             const int q = Yg % NACC;
                             const bool first = (dy == 0) || (r == 0 && dy == 1);
                             if (first) {
                                 ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Yg / NACC) & 1) ^ 1));
-                                ptx::tc_fence_after();
+                                                                ptx::tc_fence_after();
                             }
                             const uint32_t d = tmem + (uint32_t)(q * L::kAccCols);
                             const uint64_t bh0 = dB0 + (uint64_t)(dy * 2) * kBT;
@@ -326,10 +363,10 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                             }
                             // row y complete: after its dy=2 contribution, or the last row's dy=1
                             if (dy == 2 || (r == n - 1 && dy == 1)) ptx::mma_commit(&acc_full[q]);
-                        }
+                                                    }
                     }
                     ptx::mma_commit(&a_empty[slot]);
-                }
+                                    }
             }
         }
     } else if (warp >= 4 && warp < 12) {
@@ -338,8 +375,13 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         const int x = threadIdx.x - 128 - 128 * g;
         const int xs = x & (a.seg - 1);  // pixel within its image
         float* ring = in_ring + g * kRing * 2 * kInRow;
-        int it = 0;
-        for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
+        int Lbase = 0;
+        const int n_units = (int)(a.n_members * a.parts);
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const Unit U = unit_of<SPLIT>(a, u);
+            const int64_t mem = U.mem;
+            const int Lb = Lbase - U.l0;
+            Lbase += U.l1 - U.l0;
             const float* xm = a.x + mem * W;
             const float* um = a.u + mem * W;
             const bool col_ok = mem * W + x < a.cols_total;
@@ -360,13 +402,16 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 }
             };
             float p0x, p0u, p1x, p1u;
-            if (g == 1) {  // row 0 (the first odd output row's upper neighbour)
-                fetch(0, p0x, p0u);
-                put(0, p0x, p0u);
+            if (g == 1) {  // row l0 (the group's first row l0 + 1 reads it)
+                fetch(U.l0, p0x, p0u);
+                put(U.l0, p0x, p0u);
+            } else if (U.l0 > 0) {  // interior cut: row l0 - 1 is data, not padding
+                fetch(U.l0 - 1, p0x, p0u);
+                put(U.l0 - 1, p0x, p0u);
             }
-            fetch(g, p0x, p0u);
-            fetch(g + 1, p1x, p1u);
-            for (int r = g; r < n; r += 2) {
+            fetch(U.l0 + g, p0x, p0u);
+            fetch(U.l0 + g + 1, p1x, p1u);
+            for (int r = U.l0 + g; r < U.l1; r += 2) {
                 put(r, p0x, p0u);
                 if (r + 1 < n) put(r + 1, p1x, p1u);
                 fetch(r + 2, p0x, p0u);
@@ -384,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                         in[ci * 9 + ky * 3 + 1] = ok ? src[1] : 0.f;
                         in[ci * 9 + ky * 3 + 2] = (ok && xs != a.seg - 1) ? src[2] : 0.f;
                     }
-                const int Rg = it * n + r;
+                const int Rg = Lb + r;
                 const int slot = Rg % NA;
                 ptx::mbar_wait(&a_empty[slot], (uint32_t)(((Rg / NA) & 1) ^ 1));
                 if (a.debug & 16) {
@@ -424,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 ptx::fence_proxy_async_smem();
                 ptx::mbar_arrive(&a_full[slot]);
             }
-            asm volatile("bar.sync %0, 128;" ::"r"(1 + 2 * g) : "memory");  // ring reuse across members
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + 2 * g) : "memory");  // ring reuse across units
         }
     } else if (warp >= 12) {
         // ================= epilogue: thread = pixel = TMEM lane =================
@@ -506,8 +551,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 if (col_ok) om[(int64_t)y * a.ldo + x] = xres_0 + a.alpha * (b3 + o);
             }
         };
+        if constexpr (!SPLIT) {  // whole images (the common case): the tuned loop as is
         int it = 0;
-        int nproc = 0;  // rows finished by this thread (exchange-buffer parity)
         for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
             float acc3[3] = {0.f, 0.f, 0.f};  // layer-3 partial sums, ring over output rows
             const float* xm = a.x + mem * W;
@@ -730,6 +775,247 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 }
             }
         }
+        } else {  // split images: units with a halo (small ensembles)
+        int Lbase = 0, Hbase = 0;  // layer-1 / layer-2 rows of this CTA's earlier units
+        const int n_units = (int)(a.n_members * a.parts);
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const Unit U = unit_of<SPLIT>(a, u);
+            const int64_t mem = U.mem;
+            const int Lb = Lbase - U.l0, Hb = Hbase - U.e0;
+            Lbase += U.l1 - U.l0;
+            Hbase += U.e1 - U.e0;
+            const int o0 = U.o0, o1 = U.o1;
+            float acc3[3] = {0.f, 0.f, 0.f};  // layer-3 partial sums, ring over output rows
+            const float* xm = a.x + mem * W;
+            float* om = a.out + mem * W;
+            const bool col_ok = mem * W + x < a.cols_total;
+            if constexpr (SH) {
+                // accumulator D_j (input row j) holds contributions to output rows j + 1 (dy = 0
+                // block), j (dy = 1) and j - 1 (dy = 2): output row y = D_{y-1}[0] + D_y[1] +
+                // D_{y+1}[2], read straight from TMEM (three live accumulators of the ring), so no
+                // running sums are carried in registers; D_{y-1} is released after row y
+                auto acc_base = [&](int j) {
+                    return tmem + lane_base + (uint32_t)(((Lb + j) % NACC) * L::kAccCols);
+                };
+                auto wait_acc = [&](int j) {
+                    const int Jg = Lb + j;
+                    ptx::mbar_wait(&acc_full[Jg % NACC], (uint32_t)((Jg / NACC) & 1));
+                    ptx::tc_fence_after();
+                };
+                auto release = [&](int j) {
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&acc_empty[(Lb + j) % NACC]);
+                };
+                // SH: the cross-warp boundary taps of row y are exchanged through 4 smem buffers
+                // with an mbarrier each, and consumed one row later (phase B), so the four
+                // epilogue warps never wait for each other within a row.  4 buffers: a warp
+                // writing row Yg has passed phase B of row Yg - 2, so every warp has finished
+                // phase A of Yg - 2 and hence phase B of Yg - 4 (the buffer's previous row)
+                float* xvA = xd0;        // [4][4 warps][4]: v[ky][0] of lane 31
+                float* xvB = xd0 + 64;   // [4][4 warps][4]: v[ky][2] of lane 0
+                auto taps = [&](const float (&sv)[32], float (&vv)[9]) {
+                    float2 v01[4], v23[4], v45[4], v67[4];
+                    float v8[4];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        v01[g] = v23[g] = v45[g] = v67[g] = make_float2(0.f, 0.f);
+                        v8[g] = 0.f;
+                    }
+#pragma unroll
+                    for (int c = 0; c < ((a.debug & 4) ? 0 : 32); c += 2) {
+                        const float2 h2 = tanh2_fast(__fadd2_rn(make_float2(sv[c], sv[c + 1]),
+                                                                make_float2(c_epi.b2[c], c_epi.b2[c + 1])));
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int cc = c + u, g = cc & 3;
+                            const float h = u ? h2.y : h2.x;
+                            const float2 hh = make_float2(h, h);
+                            const float4 w0 = *reinterpret_cast<const float4*>(&c_epi.w3[cc][0]);
+                            const float4 w1 = *reinterpret_cast<const float4*>(&c_epi.w3[cc][4]);
+                            v01[g] = __ffma2_rn(make_float2(w0.x, w0.y), hh, v01[g]);
+                            v23[g] = __ffma2_rn(make_float2(w0.z, w0.w), hh, v23[g]);
+                            v45[g] = __ffma2_rn(make_float2(w1.x, w1.y), hh, v45[g]);
+                            v67[g] = __ffma2_rn(make_float2(w1.z, w1.w), hh, v67[g]);
+                            v8[g] = fmaf(c_epi.w3[cc][8], h, v8[g]);
+                        }
+                    }
+#pragma unroll
+                    for (int g = 1; g < 4; ++g) {
+                        v01[0].x += v01[g].x; v01[0].y += v01[g].y;
+                        v23[0].x += v23[g].x; v23[0].y += v23[g].y;
+                        v45[0].x += v45[g].x; v45[0].y += v45[g].y;
+                        v67[0].x += v67[g].x; v67[0].y += v67[g].y;
+                        v8[0] += v8[g];
+                    }
+                    vv[0] = v01[0].x; vv[1] = v01[0].y; vv[2] = v23[0].x; vv[3] = v23[0].y;
+                    vv[4] = v45[0].x; vv[5] = v45[0].y; vv[6] = v67[0].x; vv[7] = v67[0].y;
+                    vv[8] = v8[0];
+                };
+                struct Pend {
+                    float t0, t1, t2;
+                    int y, Yg;
+                    float xr_m, xres0;
+                };
+                Pend pend{0.f, 0.f, 0.f, 0, 0, 0.f, 0.f};
+                auto finish = [&](const Pend& P) {
+                    const int b = P.Yg % 4;
+                    ptx::mbar_wait(&xb_full[b], (uint32_t)((P.Yg / 4) & 1));
+                    float tk[3] = {P.t0, P.t1, P.t2};
+                    if (lane == 0 && xl) {
+#pragma unroll
+                        for (int ky = 0; ky < 3; ++ky) tk[ky] += xvA[(b * 4 + ew - 1) * 4 + ky];
+                    }
+                    if (lane == 31 && xr) {
+#pragma unroll
+                        for (int ky = 0; ky < 3; ++ky) tk[ky] += xvB[(b * 4 + ew + 1) * 4 + ky];
+                    }
+                    const int y = P.y;
+                    acc3[(y + 1) % 3] += tk[0];
+                    acc3[y % 3] += tk[1];
+                    if (y >= 1) {  // output rows outside [o0, o1) are another unit's (halo rows)
+                        const int yo = y - 1;
+                        const float o = acc3[yo % 3] + tk[2];
+                        acc3[yo % 3] = 0.f;
+                        if (col_ok && yo >= o0 && yo < o1)
+                            om[(int64_t)yo * a.ldo + x] = P.xr_m + a.alpha * (b3 + o);
+                    }
+                    if (y == n - 1) {
+                        const float o = acc3[y % 3];
+                        acc3[y % 3] = 0.f;
+                        if (col_ok && y < o1)
+                            om[(int64_t)y * a.ldo + x] = P.xres0 + a.alpha * (b3 + o);
+                    }
+                };
+                float xpre = 0.f;
+                // h2 rows [e0, e1) from D rows [l0, l1): at an interior cut D_{e0 - 1} = D_{l0} is
+                // data (at the image top e0 = l0 = 0 and D_{-1} is padding)
+                wait_acc(U.e0);
+                if (U.e0 - 1 >= U.l0) wait_acc(U.e0 - 1);
+                for (int y = U.e0; y < U.e1; ++y) {
+                    if (y + 1 < U.l1) wait_acc(y + 1);
+                    float s[32];
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(acc_base(y) + C2, v);  // D_y[dy = 1]
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) s[c] = __uint_as_float(v[c]);
+                    auto add_into = [&]() {  // s += v, as packed f32x2 adds
+#pragma unroll
+                        for (int c = 0; c < 32; c += 2) {
+                            const float2 t = __fadd2_rn(make_float2(s[c], s[c + 1]),
+                                                        make_float2(__uint_as_float(v[c]),
+                                                                    __uint_as_float(v[c + 1])));
+                            s[c] = t.x;
+                            s[c + 1] = t.y;
+                        }
+                    };
+                    if (y - 1 >= U.l0) {
+                        ptx::tmem_ld_32x32b_x32(acc_base(y - 1), v);  // D_{y-1}[dy = 0]
+                        ptx::tmem_ld_wait();
+                        add_into();
+                    }
+                    if (y + 1 < U.l1) {
+                        ptx::tmem_ld_32x32b_x32(acc_base(y + 1) + 2 * C2, v);  // D_{y+1}[dy = 2]
+                        ptx::tmem_ld_wait();
+                        add_into();
+                    }
+                    // D_j's last reader is h2 row j + 1 (or the unit's last h2 row)
+                    if (y - 1 >= U.l0) release(y - 1);
+                    if (y == U.e1 - 1) {
+                        release(y);
+                        if (y + 1 < U.l1) release(y + 1);
+                    }
+                    const float xr_m = xpre;  // X[y - 1]
+                    xpre = col_ok ? xm[(int64_t)y * a.ldx + x] : 0.f;  // X[y]: next row's X[y' - 1]
+                    // phase A: layer-3 taps, fold inside the warp, publish the boundary taps
+                    const int Yg = Hb + y, b = Yg % 4;
+                    float vv[9];
+                    taps(s, vv);
+                    float tk[3];
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky) {
+                        const float up = __shfl_up_sync(0xffffffffu, vv[ky * 3 + 0], 1);
+                        const float dn = __shfl_down_sync(0xffffffffu, vv[ky * 3 + 2], 1);
+                        tk[ky] = vv[ky * 3 + 1] + (lane == 0 ? 0.f : up) + (lane == 31 ? 0.f : dn);
+                        if (lane == 31) xvA[(b * 4 + ew) * 4 + ky] = vv[ky * 3 + 0];
+                        if (lane == 0) xvB[(b * 4 + ew) * 4 + ky] = vv[ky * 3 + 2];
+                    }
+                    __syncwarp();
+                    ptx::mbar_arrive(&xb_full[b]);
+                    // phase B of the previous row (its neighbours' taps are out by now)
+                    if (y > U.e0) finish(pend);
+                    pend = Pend{tk[0], tk[1], tk[2], y, Yg, xr_m, y == n - 1 ? xpre : 0.f};
+                }
+                finish(pend);
+            } else {
+                float xpre = 0.f;
+                for (int y = 0; y < n; ++y) {
+                    const int Yg = Lb + y;  // parts == 1 here: Lb = rows of earlier images
+                    const int q = Yg % NACC;
+                    const int par = Yg & 1;
+                    ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / NACC) & 1));
+                    ptx::tc_fence_after();
+                    const uint32_t base = tmem + lane_base + (uint32_t)(q * L::kAccCols);
+                    float s[32];
+                    float t[32];
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(base + 0, v);  // dx = 0 block
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
+                    if (lane == 31) {
+#pragma unroll
+                        for (int c = 0; c < 32; c += 4)
+                            *reinterpret_cast<float4*>(xd0 + (par * 4 + ew) * 32 + c) =
+                                make_float4(t[c], t[c + 1], t[c + 2], t[c + 3]);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) s[c] = __shfl_up_sync(0xffffffffu, t[c], 1);
+                    ptx::tmem_ld_32x32b_x32(base + 32, v);  // dx = 1 block
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) s[c] = (lane == 0 ? 0.f : s[c]) + __uint_as_float(v[c]);
+                    ptx::tmem_ld_32x32b_x32(base + 64, v);  // dx = 2 block
+                    ptx::tmem_ld_wait();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&acc_empty[q]);
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) t[c] = __uint_as_float(v[c]);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int c = 0; c < 32; c += 4)
+                            *reinterpret_cast<float4*>(xd2 + (par * 4 + ew) * 32 + c) =
+                                make_float4(t[c], t[c + 1], t[c + 2], t[c + 3]);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const float dn = __shfl_down_sync(0xffffffffu, t[c], 1);
+                        if (lane != 31) s[c] += dn;
+                    }
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    if (lane == 0 && xl) {
+#pragma unroll
+                        for (int c = 0; c < 32; c += 4) {
+                            const float4 e4 = *reinterpret_cast<const float4*>(xd0 + (par * 4 + ew - 1) * 32 + c);
+                            s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
+                        }
+                    }
+                    if (lane == 31 && xr) {
+#pragma unroll
+                        for (int c = 0; c < 32; c += 4) {
+                            const float4 e4 = *reinterpret_cast<const float4*>(xd2 + (par * 4 + ew + 1) * 32 + c);
+                            s[c] += e4.x; s[c + 1] += e4.y; s[c + 2] += e4.z; s[c + 3] += e4.w;
+                        }
+                    }
+                    const float xr_m = xpre;
+                    xpre = col_ok ? xm[(int64_t)y * a.ldx + x] : 0.f;
+                    layer3(y, s, par, acc3, xr_m, y == n - 1 ? xpre : 0.f, om, col_ok);
+                }
+            }
+        }
+        }
     } else if (warp >= 1 && warp <= 3 && a.nz.n_jobs > 0) {
         // ================= noise workers: one substream per warp at a time =================
         uint64_t* s_ki = reinterpret_cast<uint64_t*>(sm + L::kOffNz);
@@ -807,11 +1093,24 @@ int cnn3_tc_forward_nz(const float* weights, const float* biases, float alpha, c
     a.cols_total = n_members * cols;
     a.n_members = (a.cols_total + W - 1) / W;
     n_members = a.n_members;
+    // 128-pixel images, fewer images than SMs: split every image's rows into `parts` units (a
+    // two-row halo recomputed per cut) so that up to one unit per SM runs -- the per-image row
+    // pipeline, not the SM count, bounds small ensembles.  ENKS_CNN_PARTS (tuning): 0 = auto.
+    a.parts = 1;
+    if (cols == W && !(nz && nz->n_jobs > 0)) {
+        const int want = env_knob("ENKS_CNN_PARTS", 0);
+        int parts = want > 0 ? want : (int)(kNumSMs / (n_members > 0 ? n_members : 1));
+        parts = parts < 1 ? 1 : parts;
+        if (parts > rows / 16) parts = rows / 16 > 0 ? rows / 16 : 1;  // >= 16 output rows each
+        if (parts > 8) parts = 8;
+        a.parts = parts;
+    }
     {
         a.debug = debug_knob("ENKS_CNN_DEBUG", 0);  // role switches: debug builds only
         a.products = debug_knob("ENKS_CNN_PRODUCTS", 3) == 2 ? 2 : 3;  // 2 breaks 1e-4
     }
-    const int grid = (int)(n_members < kNumSMs ? n_members : kNumSMs);
+    const int64_t n_units = n_members * a.parts;
+    const int grid = (int)(n_units < kNumSMs ? n_units : kNumSMs);
     {   // stream-ordered refresh of the epilogue's constant bank
         Cnn3Epi* scr = epi_scratch();
         if (!scr) {
@@ -839,11 +1138,11 @@ int cnn3_tc_forward(const float* weights, const float* biases, float alpha, cons
                               n_members, st, nullptr);
 }
 
-template <bool SH>
-int launch_cnn3(const Cnn3Args& a, int grid, cudaStream_t st) {
+template <bool SH, bool SPLIT>
+int launch_cnn3_v(const Cnn3Args& a, int grid, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(cnn3_tc_kernel<SH>,
+        cudaError_t e = cudaFuncSetAttribute(cnn3_tc_kernel<SH, SPLIT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              CL<SH>::kSmem);
         if (e != cudaSuccess) {
@@ -852,8 +1151,15 @@ int launch_cnn3(const Cnn3Args& a, int grid, cudaStream_t st) {
         }
         configured = true;
     }
-    cnn3_tc_kernel<SH><<<grid, kThreads, CL<SH>::kSmem, st>>>(a);
+    cnn3_tc_kernel<SH, SPLIT><<<grid, kThreads, CL<SH>::kSmem, st>>>(a);
     return check_launch("enks_cnn_forward(tcgen05)");
+}
+
+template <bool SH>
+int launch_cnn3(const Cnn3Args& a, int grid, cudaStream_t st) {
+    // split images (parts > 1) only for 128-pixel rows; whole images keep the simpler instance
+    if (SH && a.parts > 1) return launch_cnn3_v<true, true>(a, grid, st);
+    return launch_cnn3_v<SH, false>(a, grid, st);
 }
 
 }  // namespace enks

@@ -681,11 +681,14 @@ def test_noise_segmented_bit_exact(dev_ops, N, rows, cols, m0):
     assert np.array_equal(seg[1].cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("rows,N", [(24, 300), (2, 150), (3, 149)])
+@pytest.mark.parametrize("rows,N", [(24, 300), (2, 150), (3, 149), (128, 20), (37, 4), (128, 64),
+                                    (50, 9)])
 def test_cnn_forward_tcgen05_several_images_per_cta(dev_ops, pm, rows, N):
     """128-pixel images with more images than SMs: each CTA streams several images through the
     same row pipeline (TMEM ring, A slots, tap ring continue across image boundaries); minimum
-    image height 2 (both edge rows at once)."""
+    image height 2 (both edge rows at once).  Fewer images than SMs: every image's rows are split
+    into units with a two-row halo (7 uneven parts of 128 rows at N = 20, 2 parts at N = 64, ...),
+    several units per CTA when parts x N > 148."""
     from oracle.models import cnn_step_torch
     from paper_2410_09663_b200.engine import Forecaster
 
