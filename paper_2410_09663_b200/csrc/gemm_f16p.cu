@@ -600,14 +600,32 @@ __global__ void f16pair_recon_kernel(const __half* __restrict__ h, const __half*
             (__half2float(h[r * ldi + k]) + __half2float(l[r * ldi + k])) * inv_scale[r];
 }
 
+// split-K partials -> C, summed in split order (deterministic).  One thread per 4 columns of a
+// row (2-D grid: no 64-bit division per element; float4 when N and ldc allow it).
 __global__ void f16p_sum_splits(const float* __restrict__ ws, int split, int64_t M, int64_t N,
                                 float* __restrict__ C, int64_t ldc) {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (e >= M * N) return;
-    const int64_t r = e / N, c = e - r * N;
-    float v = 0.f;
-    for (int z = 0; z < split; ++z) v += ws[(int64_t)z * M * N + e];
-    C[r * ldc + c] = v;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (c >= N) return;
+    const int64_t MN = M * N;
+    const bool vec = c + 4 <= N && (N & 3) == 0 && (ldc & 3) == 0 && (((uintptr_t)C) & 15) == 0;
+    for (int64_t r = blockIdx.y; r < M; r += gridDim.y) {
+        const float* src = ws + r * N + c;
+        float* dst = C + r * ldc + c;
+        if (vec) {
+            float4 v = __ldg(reinterpret_cast<const float4*>(src));
+            for (int z = 1; z < split; ++z) {
+                const float4 w = __ldg(reinterpret_cast<const float4*>(src + (int64_t)z * MN));
+                v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+            }
+            *reinterpret_cast<float4*>(dst) = v;
+            continue;
+        }
+        for (int q = 0; q < 4 && c + q < N; ++q) {
+            float v = src[q];
+            for (int z = 1; z < split; ++z) v += src[(int64_t)z * MN + q];
+            dst[q] = v;
+        }
+    }
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -831,8 +849,8 @@ int gemm_f16pair_impl(int64_t M, int64_t N, int64_t K, float alpha, const void* 
         default: rc = launch16<256>(maps, p, grid, st); break;
     }
     if (rc || direct) return rc;
-    f16p_sum_splits<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(static_cast<float*>(ws), split,
-                                                                     M, N, C, ldc);
+    const dim3 sgrid((unsigned)((N + 4 * 128 - 1) / (4 * 128)), (unsigned)(M < 65535 ? M : 65535));
+    f16p_sum_splits<<<sgrid, 128, 0, st>>>(static_cast<float*>(ws), split, M, N, C, ldc);
     return check_launch("enks_gemm_f16pair(split reduce)");
 }
 }  // namespace

@@ -357,6 +357,7 @@ class DeviceSmoother:
         self.barrier = None
         self.dev_head = None  # ops.DeviceHead: noise entropy words read from device memory
         self.record = None    # dict: per-update Sigma_y / Sigma_xy / gain (tests, see _record_step)
+        self._pending = None  # deferred centring of the newest predicted slice (_finish_slice)
         self._last_stale = False  # `last` lags the newest slice (a predict with no update yet)
         self._basis = basis
         self._explicit = False  # explicit members (replace_members): no derived-U chain
@@ -456,6 +457,7 @@ class DeviceSmoother:
         self.t = 0
         self.n_upd = 0
         self.slice0_zero = True
+        self._pending = None
         self._obs_t = -1
         self._obs_sums_t = -1
         self._last_stale = False
@@ -537,6 +539,7 @@ class DeviceSmoother:
 
     def newest_anomalies(self):
         """fp32 anomalies of the newest predicted slice (d x K)."""
+        self._finish_slice()
         d, ds, t, q = self.d, self.ds, self.t, self.q
         if self.chain:  # [X; U] from the fp32 copy, dU from the basis
             out = self.ops.empty(d, self.K)
@@ -675,7 +678,7 @@ class DeviceSmoother:
             self.ops.member_sum_rebase(src, self.m, acc, -float(self.N), src2=src2)
 
     def _center(self, src, mean_out, anom_out, pair_rows=None, f32_rows=0, skip=(0, 0),
-                obs_sums=False):
+                obs_sums=False, defer=False):
         """Member mean (rows x m) and anomalies of `src` (rows x K) relative to each rank's first
         member (identical members give exactly zero anomalies at any N and any rank count).
 
@@ -697,17 +700,32 @@ class DeviceSmoother:
             items.append((self.slice_raw[:p], self.acc_obs, self.v_raw))
             self._obs_sums_t = self.t + 1
         self._global_sums(items)
-        if pair_rows is None:
-            ops.member_center(src, self.Nl, self.m, None, acc, self.N, mean=mean_out,
-                              anom=anom_out)
-            return
-        which, r0 = pair_rows
-        h, l, inv = (self.Ah, self.Al, self.a_inv) if which == "A" else (self.Yh, self.Yl,
-                                                                        self.y_inv)
-        hr = rows - (skip[1] - skip[0])  # basis rows written
-        ops.member_center_f16pair(src, self.Nl, self.m, None, acc, amax, self.N, mean_out,
-                                  h[r0:r0 + hr], l[r0:r0 + hr], inv[r0:r0 + hr],
-                                  f32=anom_out, rows_f32=f32_rows, skip=skip)
+
+        def centre():
+            if pair_rows is None:
+                ops.member_center(src, self.Nl, self.m, None, acc, self.N, mean=mean_out,
+                                  anom=anom_out)
+                return
+            which, r0 = pair_rows
+            h, l, inv = (self.Ah, self.Al, self.a_inv) if which == "A" else (self.Yh, self.Yl,
+                                                                            self.y_inv)
+            hr = rows - (skip[1] - skip[0])  # basis rows written
+            ops.member_center_f16pair(src, self.Nl, self.m, None, acc, amax, self.N, mean_out,
+                                      h[r0:r0 + hr], l[r0:r0 + hr], inv[r0:r0 + hr],
+                                      f32=anom_out, rows_f32=f32_rows, skip=skip)
+
+        if defer:  # the new slice's centring waits for update(), behind the gain-solve launch
+            self._pending = centre
+        else:
+            centre()
+
+    def _finish_slice(self) -> None:
+        """Run the deferred centring of the newest predicted slice (predict's last stage), if any:
+        update() issues it after launching the side-stream gain solve, so at small ensembles the
+        two overlap; every reader of the slice's basis rows / mean calls this first."""
+        f, self._pending = self._pending, None
+        if f is not None:
+            f()
 
     def _center_obs_fused(self, tau) -> None:
         """Centre y = [x; u] + [v_x; v_u] (never materialised) into the basis rows of Yc_tau and
@@ -735,6 +753,7 @@ class DeviceSmoother:
         ops, n, l, d = self.ops, self.n, self.l, self.d
         head = self._head(streams)
         sr, ob = self.slice_raw, self.obs_raw
+        self._finish_slice()  # (a predict with no update in between)
         if self.t >= 1 and self.n_upd < self.t:
             # the previous step had no update (predict twice in a row, as the reference allows):
             # its observation block and gain column hold no information -- zero them so the
@@ -786,9 +805,10 @@ class DeviceSmoother:
             self._center(sr, self.mean[tau * d:(tau + 1) * d], self.A_new,
                          pair_rows=("A", tau * self.ds), f32_rows=self.q,
                          skip=(n, n + l) if self.chain else (0, 0),
-                         obs_sums=self.obs_fused and self.fused_noise)
+                         obs_sums=self.obs_fused and self.fused_noise, defer=True)
         else:
-            self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d])
+            self._center(sr, self.mean[tau * d:(tau + 1) * d], self.Abuf[tau * d:(tau + 1) * d],
+                         defer=True)
         self.t = tau
 
     # ------------------------------------------------------------ update
@@ -816,6 +836,8 @@ class DeviceSmoother:
             self._barrier_row(head, tau)
         yc = self.Yc_new if self.pair else self.Ybuf[(tau - 1) * p:tau * p]
         fused_obs = self.obs_fused and not redraw
+        if not (fused_obs and self.pair):
+            self._finish_slice()  # the observation centring below reuses the sum buffers
         if fused_obs:
             self._center_obs_fused(tau)
         elif self.pair:
@@ -839,6 +861,7 @@ class DeviceSmoother:
             ops.gemm_f16pair(yh, yl, yi, yh, yl, yi, PY[(tau - 1) * p:], tag="cross")
             comm.allreduce_(PY[(tau - 1) * p:])
             self._spd_async(side, PY[(tau - 1) * p:], scale)
+            self._finish_slice()  # the new slice's centring, next to the gain solve
             ops.gemm_f16pair(self.Ah[a0:rows_a], self.Al[a0:rows_a], self.a_inv[a0:rows_a],
                              yh, yl, yi, PA, tag="cross")
             if tau > 1:
@@ -1044,6 +1067,7 @@ class DeviceSmoother:
     # ------------------------------------------------------------ readback
     def deviations(self, rows: int | None = None):
         """Member deviations M - mean for slices 0..t, (T d x K) on device."""
+        self._finish_slice()
         ops, d, ds, p, t = self.ops, self.d, self.ds, self.p, self.t
         R, Rc = (t + 1) * d, (t + 1) * ds
         out = ops.empty(Rc, self.K)
@@ -1074,6 +1098,7 @@ class DeviceSmoother:
         return dev + mean.repeat(1, self.Nl)
 
     def mean_host(self) -> np.ndarray:
+        self._finish_slice()
         R = (self.t + 1) * self.d
         out = self.ops.to_host(self.mean[:R])
         if self.slice0_zero and self.x0_exact is not None:
@@ -1114,6 +1139,7 @@ class DeviceSmoother:
     def _replace_members_dev(self, Mdev, t: int) -> None:
         """replace_members for a device tensor in the member-column layout ((t+1) d x K)."""
         ops, d = self.ops, self.d
+        self._pending = None  # the explicit members replace any deferred centring
         self._obs_t = -1
         self.t = 0
         if self.chain:  # explicit members need not obey U_s = U_{s-1} + dU_s: full rows
