@@ -11,7 +11,7 @@ Here they stay on the device between calls:
 * D is formed once per tracked call (engine.deviations()), split into fp16-pair planes and
   contracted on the tcgen05 kind::f16 kernel (3 products, fp32-level accuracy);
 * sigma_traj after an update is a SYRK: only the 256-wide block columns on and below the
-  diagonal are computed (half the flops), the upper blocks are mirrored when the host reads it;
+  diagonal are computed (half the flops), the upper triangle is mirrored when the host reads it;
 * sigma_pred is the last d rows of sigma_cross (the same contraction, reference enks.py:176-177);
 * after predict the grown sigma_traj is an unevaluated block assembly [old, cross; cross^T,
   pred] -- evaluated only if read before the next update replaces it;
@@ -50,8 +50,11 @@ class _SymRows:
     def host(self):
         full = self.comm.all_gather_rows(self.local)[:self.R, :self.R]
         a = self.ops.to_host(full)
-        blk = np.arange(self.R) // BLOCK
-        return np.where(blk[:, None] >= blk[None, :], a, a.T)
+        # lower triangle as computed, upper mirrored (the diagonal blocks' upper halves were
+        # computed too, in a different summation order -- mirroring keeps sigma_traj exactly
+        # symmetric like the reference's D @ D.T)
+        i = np.arange(self.R)
+        return np.where(i[:, None] >= i[None, :], a, a.T)
 
 
 class _Assembled:
