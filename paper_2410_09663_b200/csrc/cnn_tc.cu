@@ -32,6 +32,7 @@
 // warps 4-7 / 8-11 = layer-1 producers of the even / odd image rows (thread = pixel; two
 // groups so that two rows of the latency-bound CUDA-core layer are in flight per SM),
 // warps 12-15 = epilogue (thread = pixel = TMEM lane).
+#include <cuda_fp16.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -50,15 +51,56 @@ constexpr int NACC = 5;    // TMEM accumulators (ring over rows; 5 x 96 <= 512 c
 constexpr int kThreads = 512;
 constexpr int kRing = 8;   // input-row ring slots per producer group
 
+// Layer-2 operand format.  fp16 pairs (default): one 128-B SWIZZLE_128B row holds a pixel's (or a
+// weight row's) 32 channels as fp16 hi (bytes 0-63) and lo (bytes 64-127) -- one tile per operand,
+// kind::f16 MMAs (K = 16) at twice the kind::tf32 rate, half the shared-memory stores of the
+// producers.  Three products (lo*hi + hi*lo + hi*hi) give the same ~2^-22 operand precision as
+// 3xTF32 as long as neither half is subnormal, so both operands are pre-scaled by powers of two:
+// the layer-1 activations (|tanh| < 1) by 2^14, W2 so that its largest |entry| lands in
+// [2^14, 2^15); the epilogue folds the inverse scale into the layer-2 bias add (one FFMA in place
+// of the FADD).  Build with -DENKS_CNN_TF32=1 for the previous 3xTF32 operands (separate fp32
+// hi / lo tiles).
+#ifndef ENKS_CNN_TF32
+#define ENKS_CNN_TF32 0
+#endif
+constexpr bool kF16 = !ENKS_CNN_TF32;
+constexpr int kPlanes = kF16 ? 1 : 2;  // tiles per operand (hi and lo share a row in fp16)
+constexpr float kScaleA = 16384.f;    // activation pre-scale (fp16 pairs)
+
+// Layer 3 (32 -> 1) on the tensor core (128-pixel whole images, fp16 pairs): the epilogue writes
+// the layer-2 activations h2 of each row into a shared-memory tile laid out like the layer-1
+// tiles, and the MMA warp contracts it with W3 -- for each horizontal tap kx one MMA group whose
+// A operand starts kx rows down (the zero pad rows give the 'same' padding), N = 16 columns of
+// which the first three are the vertical taps ky:  U_j[x][ky] = sum_kx sum_c h2[j][x+kx-1][c]
+// W3[c][ky][kx].  Output row y = U_{y-1}[0] + U_y[1] + U_{y+1}[2], three TMEM columns.  The
+// epilogue keeps tanh, the fp16 split and that three-term fold; the 288 FMAs per pixel and the
+// cross-warp tap exchange of the CUDA-core layer 3 go away (the epilogue was the kernel's
+// bottleneck: one warp per SM sub-partition, latency-bound).  -DENKS_CNN_L3=0: CUDA-core layer 3.
+#ifndef ENKS_CNN_L3
+#define ENKS_CNN_L3 1
+#endif
+constexpr bool kL3 = ENKS_CNN_L3 && kF16;
+constexpr int NH = 3;       // h2 tiles (layer-3 A operand ring)
+constexpr int NU = 8;       // layer-3 accumulators (16 TMEM columns each, after 4 x 96)
+constexpr int kUCol0 = 4 * NB;
+#ifndef ENKS_CNN_CONV_ISSUER
+#define ENKS_CNN_CONV_ISSUER 1
+#endif
+constexpr bool kConvIssuer = ENKS_CNN_CONV_ISSUER;
+constexpr float kGrid = 1.5f * 67108864.f;  // 1.5 * 2^26: (v + kGrid) - kGrid rounds v to a multiple of 8
+
 constexpr int kInRow = W + 2;
 constexpr int kW1Stride = 20;                        // float2 per channel pair (18 used)
 constexpr int kW3Stride = 12;
 constexpr int kXD = 2 * 4 * 32;                     // [parity][warp][32]
 constexpr int kXV = 2 * 4 * 4;                      // [parity][warp][3 (+pad)]
 
-// layer-2 bias and layer-3 weights in constant memory: the epilogue reads them as uniform-register
-// operands (LDCU) instead of shared-memory loads (the kernel's shared-memory pipe is its limit)
+// layer-1 weights / bias, layer-2 bias and layer-3 weights in constant memory: the producers and
+// the epilogue read them as uniform-register operands (LDCU) instead of shared-memory loads (the
+// kernel's shared-memory pipe is its limit; the layer-1 weights were 85 % of its wavefronts)
 struct Cnn3Epi {
+    alignas(16) float w1[C1 / 2][kW1Stride * 2];  // channel pair cp: (w[2cp][k], w[2cp+1][k]) per k
+    float b1[C1];
     float b2[C2];
     float w3[C2][kW3Stride];  // [c][ky*3 + kx], padded to 12
     float b3;
@@ -81,19 +123,24 @@ struct CL {
     static constexpr int kARows = SH ? 136 : W;            // SH: pixel x at row x + 1
     static constexpr int kATile = kARows * 128;
     static constexpr int kOffB = 0;                        // [tap][hi/lo] B tiles
-    static constexpr int kOffA = kOffB + kNBT * 2 * kBTile;  // [slot][hi/lo] A tiles
-    static constexpr int kOffIn = kOffA + NA * 2 * kATile;   // input rings [2][kRing][2][W + 2]
+    static constexpr int kOffA = kOffB + kNBT * kPlanes * kBTile;  // [slot][plane] A tiles
+    static constexpr int kOffIn = kOffA + NA * kPlanes * kATile;   // rings [2][kRing][2][W + 2]
     static constexpr int kOffW1 = kOffIn + 2 * kRing * 2 * kInRow * 4;
     static constexpr int kOffB1 = kOffW1 + (C1 / 2) * kW1Stride * 8;
     static constexpr int kOffB2 = kOffB1 + C1 * 4;
     static constexpr int kOffW3 = kOffB2 + C2 * 4;
-    static constexpr int kOffB3 = kOffW3 + C2 * kW3Stride * 4;
+    static constexpr int kOffB3 = kOffW3 + C2 * kW3Stride * 4;  // b3, layer-2 inverse scale
     static constexpr int kOffX = kOffB3 + 16;
     static constexpr int kOffBar = kOffX + (2 * kXD + 2 * kXV) * 4;
-    static constexpr int kOffNz = kOffBar + 32 * 8;                       // noise: ki, wi tables
+    static constexpr int kOffNz = kOffBar + 64 * 8;                       // noise: ki, wi tables
     static constexpr int kNzWarp = 2 * kMaxRowCols * 4 + kBufWords * 8;     // row slots + words
     static constexpr int kOffNzW = kOffNz + 256 * 16;                       // [3] per noise warp
-    static constexpr int kSmem = kOffNzW + 3 * kNzWarp + 1024;
+    static constexpr int kEndNz = kOffNzW + 3 * kNzWarp;
+    // layer 3 on the tensor core (SH): W3 B tiles [kx] (16 rows: ky 0..2, then zeros), h2 tiles
+    static constexpr int kOffW3T = (kEndNz + 1023) / 1024 * 1024;
+    static constexpr int kW3Tile = 16 * 128;
+    static constexpr int kOffH2 = kOffW3T + 3 * kW3Tile;
+    static constexpr int kSmem = (SH && kL3 ? kOffH2 + NH * kATile : kEndNz) + 1024;
     static constexpr int kAccCols = NB;                    // TMEM columns per accumulator
     static constexpr uint32_t kTmemAlloc = 512;
     static_assert(kSmem <= 232448, "shared memory budget");
@@ -143,6 +190,42 @@ __device__ __forceinline__ float2 tanh2_fast(float2 x) {
                                 make_float2(1.f, 1.f));
     return __ffma2_rn(make_float2(-2.f, -2.f), make_float2(rcp_approx(d.x), rcp_approx(d.y)),
                       make_float2(1.f, 1.f));
+}
+
+// s * tanh(x) for two values: the scale folds into the last FFMA2
+__device__ __forceinline__ float2 tanh2_fast_s(float2 x, float s) {
+    const float2 e = __fmul2_rn(x, make_float2(2.8853900817779268f, 2.8853900817779268f));
+    const float2 d = __fadd2_rn(make_float2(exp2f_approx(e.x), exp2f_approx(e.y)),
+                                make_float2(1.f, 1.f));
+    return __ffma2_rn(make_float2(-2.f * s, -2.f * s), make_float2(rcp_approx(d.x), rcp_approx(d.y)),
+                      make_float2(s, s));
+}
+
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) {
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// fp16 pair of two values |v| <= 2^14: hi = v rounded to a multiple of 8 (exact in fp16 there),
+// lo = v - hi (|lo| <= 4, rounded to fp16: 2^-10 absolute)
+__device__ __forceinline__ void split_grid(float2 v, uint32_t& hi, uint32_t& lo) {
+    const float2 h = __fadd2_rn(__fadd2_rn(v, make_float2(kGrid, kGrid)), make_float2(-kGrid, -kGrid));
+    hi = h2_bits(__float22half2_rn(h));
+    lo = h2_bits(__float22half2_rn(__ffma2_rn(h, make_float2(-1.f, -1.f), v)));
+}
+
+// one B row entry of W2 (hi / lo) into a tile at (row, ci)
+__device__ __forceinline__ void stage_w2(uint8_t* tile, int row, int ci, float v, float ws) {
+    if constexpr (kF16) {
+        const float vs = v * ws;
+        const __half h = __float2half_rn(vs);
+        *reinterpret_cast<__half*>(tile + sw128(row, ci * 2)) = h;
+        *reinterpret_cast<__half*>(tile + sw128(row, 64 + ci * 2)) =
+            __float2half_rn(vs - __half2float(h));
+    } else {
+        const float h = ptx::tf32_round(v);
+        *reinterpret_cast<float*>(tile + sw128(row, ci * 4)) = h;
+        *reinterpret_cast<float*>(tile + NB * 128 + sw128(row, ci * 4)) = v - h;
+    }
 }
 
 struct Cnn3Args {
@@ -225,25 +308,86 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     uint64_t* acc_empty = bars + 2 * NA + NACC;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NA + 2 * NACC);
     uint64_t* xb_full = bars + 2 * NA + 2 * NACC + 1;  // [4] SH: row's boundary taps written
+    uint64_t* h2_full = bars + 24;   // [NH] layer 3: h2 row written by the epilogue
+    uint64_t* h2_empty = bars + 28;  // [NH] layer 3: its MMAs done
+    uint64_t* u_full = bars + 32;    // [NU] layer-3 accumulator complete
+    uint64_t* u_empty = bars + 40;   // [NU] layer-3 accumulator read
+    // layer 3 on the tensor core (128-pixel images, whole or split into units); the layer-2 ring
+    // then has 4 accumulators (4 x 96 + NU x 16 columns).
+    // (One 32-column accumulator per output row instead -- 54 N = 32 MMAs per row in place of
+    // 18 N = 96 -- ran at half the speed: the MMA cost is per instruction at these shapes.)
+    constexpr bool L3 = SH && kL3;
+    constexpr int kNAcc = L3 ? 4 : NACC;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = a.rows;
 
     // ---- stage weights (all threads) -------------------------------------------------
+    // fp16 pairs: W2 pre-scale ws = 2^(15 - e) for max |W2| = m 2^e (m in [0.5, 1)), from a
+    // block-wide max (the input ring is free scratch until the producers start)
+    // (the same for W3 when layer 3 runs on the tensor core)
+    float ws = 1.f, inv2 = 1.f, ws3 = 1.f, inv3 = 1.f;
+    if constexpr (kF16) {
+        float mx = 0.f, mx3 = 0.f;
+        for (int e = threadIdx.x; e < C2 * C1 * 9; e += kThreads) mx = fmaxf(mx, fabsf(a.w2[e]));
+        for (int e = threadIdx.x; e < C2 * 9; e += kThreads) mx3 = fmaxf(mx3, fabsf(a.w3[e]));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mx3 = fmaxf(mx3, __shfl_xor_sync(0xffffffffu, mx3, o));
+        }
+        if (lane_id() == 0) {
+            in_ring[threadIdx.x >> 5] = mx;
+            in_ring[kThreads / 32 + (threadIdx.x >> 5)] = mx3;
+        }
+        __syncthreads();
+        mx = mx3 = 0.f;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) {
+            mx = fmaxf(mx, in_ring[w]);
+            mx3 = fmaxf(mx3, in_ring[kThreads / 32 + w]);
+        }
+        __syncthreads();
+        if (mx > 0.f && mx < 3.0e38f) {
+            int ex;
+            frexpf(mx, &ex);
+            ws = ldexpf(1.f, 15 - ex);
+            inv2 = ldexpf(1.f, ex - 15 - 14);  // 1 / (ws * kScaleA)
+        }
+        if (mx3 > 0.f && mx3 < 3.0e38f) {
+            int ex;
+            frexpf(mx3, &ex);
+            ws3 = ldexpf(1.f, 15 - ex);
+            inv3 = ldexpf(1.f, ex - 15 - 14);
+        }
+    }
+    if constexpr (SH && kL3) {
+        // W3 B tiles: row ky (< 3) of tile kx holds W3[c][ky][kx] as (hi | lo); rows 3..15 zero
+        for (int e = threadIdx.x; e < 3 * 16 * C2; e += kThreads) {
+            const int kx = e / (16 * C2), rem = e - kx * 16 * C2;
+            const int row = rem / C2, c = rem - row * C2;
+            const float v = row < 3 ? a.w3[(c * 3 + row) * 3 + kx] : 0.f;
+            stage_w2(sm + L::kOffW3T + kx * L::kW3Tile, row, c, v, ws3);
+        }
+        // zero pad rows (0 and 129..135) of the h2 tiles
+        for (int e = threadIdx.x; e < NH * 8 * 32; e += kThreads) {
+            const int tile = e / (8 * 32), rem = e - tile * 8 * 32;
+            const int pr = rem >> 5, k = rem & 31;
+            const int row = pr == 0 ? 0 : 128 + pr;
+            *reinterpret_cast<float*>(sm + L::kOffH2 + tile * L::kATile + sw128(row, k * 4)) = 0.f;
+        }
+    }
     if constexpr (SH) {
         for (int e = threadIdx.x; e < 3 * NB * C1; e += kThreads) {
             // B[dx][row = dy*C2 + co][ci] = W2[co][ci][dy][dx]
             const int dx = e / (NB * C1), rem = e - dx * NB * C1;
             const int row = rem / C1, ci = rem - row * C1;
             const int dy = row / C2, co = row - dy * C2;
-            const float v = a.w2[((co * C1 + ci) * 3 + dy) * 3 + dx];
-            const float h = ptx::tf32_round(v);
-            const uint32_t off = sw128(row, ci * 4);
-            *reinterpret_cast<float*>(sm + L::kOffB + (dx * 2 + 0) * L::kBTile + off) = h;
-            *reinterpret_cast<float*>(sm + L::kOffB + (dx * 2 + 1) * L::kBTile + off) = v - h;
+            stage_w2(sm + L::kOffB + dx * kPlanes * L::kBTile, row, ci,
+                     a.w2[((co * C1 + ci) * 3 + dy) * 3 + dx], ws);
         }
         // zero pad rows (0 and 129..135) of every A slot; never written afterwards
-        for (int e = threadIdx.x; e < NA * 2 * 8 * 32; e += kThreads) {
+        for (int e = threadIdx.x; e < NA * kPlanes * 8 * 32; e += kThreads) {
             const int tile = e / (8 * 32), rem = e - tile * 8 * 32;
             const int pr = rem >> 5, k = rem & 31;
             const int row = pr == 0 ? 0 : 128 + pr;
@@ -255,11 +399,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
             const int dy = e / (NB * C1), rem = e - dy * NB * C1;
             const int row = rem / C1, ci = rem - row * C1;
             const int dx = row / C2, co = row - dx * C2;
-            const float v = a.w2[((co * C1 + ci) * 3 + dy) * 3 + dx];
-            const float h = ptx::tf32_round(v);
-            const uint32_t off = sw128(row, ci * 4);
-            *reinterpret_cast<float*>(sm + L::kOffB + (dy * 2 + 0) * L::kBTile + off) = h;
-            *reinterpret_cast<float*>(sm + L::kOffB + (dy * 2 + 1) * L::kBTile + off) = v - h;
+            stage_w2(sm + L::kOffB + dy * kPlanes * L::kBTile, row, ci,
+                     a.w2[((co * C1 + ci) * 3 + dy) * 3 + dx], ws);
         }
     }
     for (int e = threadIdx.x; e < C1 * 18; e += kThreads) {
@@ -274,6 +415,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     }
     if (threadIdx.x == 0) {
         b3s[0] = a.b3[0];
+        b3s[1] = inv2;
+        b3s[2] = inv3;
         for (int s = 0; s < NA; ++s) {
             ptx::mbar_init(&a_full[s], 128);
             ptx::mbar_init(&a_empty[s], 1);
@@ -283,6 +426,14 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
             ptx::mbar_init(&acc_empty[q], 4);
         }
         for (int q = 0; q < 4; ++q) ptx::mbar_init(&xb_full[q], 128);
+        for (int q = 0; q < NH; ++q) {
+            ptx::mbar_init(&h2_full[q], 128);
+            ptx::mbar_init(&h2_empty[q], 1);
+        }
+        for (int q = 0; q < NU; ++q) {
+            ptx::mbar_init(&u_full[q], 1);
+            ptx::mbar_init(&u_empty[q], 4);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc(tmem_slot, L::kTmemAlloc);
@@ -293,80 +444,144 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     const uint32_t tmem = *tmem_slot;
     if (warp == 0) {
         // ================= MMA issuer =================
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_tf32(W, L::kAccCols);
+        // kConvIssuer: the whole warp runs the loop and an elected lane issues each MMA / commit
+        // (see tc_ptx.cuh); otherwise lane 0 alone
+        if (kConvIssuer || lane == 0) {
+            constexpr uint32_t idesc = kF16 ? ptx::idesc_f16(W, L::kAccCols)
+                                            : ptx::idesc_tf32(W, L::kAccCols);
+            // one K step: 16 fp16 or 8 tf32 channels = 32 B of the 128-B row (+2 in the
+            // descriptor's start field); fp16: the lo half is 64 B (+4) along the same row,
+            // tf32: the lo plane is the next tile
+            constexpr int kSteps = kF16 ? C1 / 16 : C1 / 8;
+            auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc) {
+                if constexpr (kF16 && kConvIssuer) ptx::mma_f16_ss_elect(d, ad, bd, idesc, acc);
+                else if constexpr (kF16) ptx::mma_f16_ss(d, ad, bd, idesc, acc);
+                else if constexpr (kConvIssuer) ptx::mma_tf32_ss_elect(d, ad, bd, idesc, acc);
+                else ptx::mma_tf32_ss(d, ad, bd, idesc, acc);
+            };
+            auto commit = [&](uint64_t* bar) {
+                if constexpr (kConvIssuer) ptx::mma_commit_elect(bar);
+                else ptx::mma_commit(bar);
+            };
             // descriptors are built once: the start-address field (addr >> 4, 14 bits) of a tile
             // at a byte offset o from a base is the base descriptor + (o >> 4)
             const uint64_t dA0 = ptx::desc_kmajor_sw128(sm + L::kOffA);
             const uint64_t dB0 = ptx::desc_kmajor_sw128(sm + L::kOffB);
             constexpr uint64_t kAT = L::kATile >> 4, kBT = L::kBTile >> 4;
             const bool do_mma = !(a.debug & 1), p3 = a.products == 3;
+            // layer 3 of the h2 row with global index Jg (L3): three horizontal taps x 2 K steps
+            // x 3 products into the 16-column accumulator U_Jg
+            const uint64_t dH0 = ptx::desc_kmajor_sw128(sm + L::kOffH2);
+            const uint64_t dW0 = ptx::desc_kmajor_sw128(sm + L::kOffW3T);
+            auto mma3 = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t acc) {
+                constexpr uint32_t idesc3 = ptx::idesc_f16(W, 16);
+                if constexpr (kConvIssuer) ptx::mma_f16_ss_elect(d, ad, bd, idesc3, acc);
+                else ptx::mma_f16_ss(d, ad, bd, idesc3, acc);
+            };
+            auto layer3 = [&](int Jg) {
+                const int hs = Jg % NH, qu = Jg % NU;
+                ptx::mbar_wait(&h2_full[hs], (uint32_t)((Jg / NH) & 1));
+                ptx::mbar_wait(&u_empty[qu], (uint32_t)(((Jg / NU) & 1) ^ 1));
+                ptx::tc_fence_after();
+                const uint32_t du = tmem + (uint32_t)(kUCol0 + qu * 16);
+                if (do_mma) {
+                    const uint64_t dh = dH0 + (uint64_t)hs * kAT;
+#pragma unroll
+                    for (int kx = 0; kx < 3; ++kx) {
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            const uint64_t adh = dh + (uint64_t)(kx * 8 + 2 * k), adl = adh + 4;
+                            const uint64_t bdh = dW0 + (uint64_t)(kx * (L::kW3Tile >> 4) + 2 * k);
+                            const uint64_t bdl = bdh + 4;
+                            mma3(du, adl, bdh, (kx == 0 && k == 0) ? 0u : 1u);
+                            mma3(du, adh, bdl, 1u);
+                            mma3(du, adh, bdh, 1u);
+                        }
+                    }
+                }
+                commit(&u_full[qu]);
+                commit(&h2_empty[hs]);
+            };
+            int l3_next = 0;  // global index of the next h2 row for layer 3
             int Lbase = 0;  // layer-1 rows of this CTA's earlier units (ring / slot counter)
+            int Hbase = 0;  // h2 rows of this CTA's earlier units (layer-3 ring counter)
             const int n_units = (int)(a.n_members * a.parts);
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 const Unit U = unit_of<SPLIT>(a, u);
-                const int Lb = Lbase - U.l0;
+                const int Lb = Lbase - U.l0, Hb = Hbase - U.e0;
                 Lbase += U.l1 - U.l0;
+                Hbase += U.e1 - U.e0;
                 for (int r = U.l0; r < U.l1; ++r) {
                     const int Rg = Lb + r;
                     const int slot = Rg % NA;
                     ptx::mbar_wait(&a_full[slot], (uint32_t)((Rg / NA) & 1));
                                         ptx::tc_fence_after();
-                    const uint64_t dah0 = dA0 + (uint64_t)(slot * 2) * kAT, dal0 = dah0 + kAT;
+                    const uint64_t dah0 = dA0 + (uint64_t)(slot * kPlanes) * kAT;
+                    const uint64_t dal0 = dah0 + (kF16 ? 4 : kAT);
                     if constexpr (SH) {
+                        // layer 3 runs three rows behind: h2 row j needs D_{j+1} (issued at
+                        // iteration j + 1) and the epilogue's pass over it
+                        if constexpr (L3) {
+                            while (l3_next <= Hb + r - 3) layer3(l3_next++);
+                        }
                         // D_r[x][(dy, co)] = sum_dx sum_ci h1[r][x + dx - 1][ci] W2[co][ci][dy][dx]
-                        const int q = Rg % NACC;
-                        ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Rg / NACC) & 1) ^ 1));
+                        const int q = Rg % kNAcc;
+                        ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Rg / kNAcc) & 1) ^ 1));
                                                 ptx::tc_fence_after();
                         const uint32_t d = tmem + (uint32_t)(q * L::kAccCols);
                         if (do_mma) {
 #pragma unroll
                             for (int dx = 0; dx < 3; ++dx) {
-                                const uint64_t bh0 = dB0 + (uint64_t)(dx * 2) * kBT;
+                                const uint64_t bh0 = dB0 + (uint64_t)(dx * kPlanes) * kBT;
 #pragma unroll
-                                for (int k = 0; k < C1 / 8; ++k) {  // A starts dx 128-B rows down
+                                for (int k = 0; k < kSteps; ++k) {  // A starts dx 128-B rows down
                                     const uint64_t adh = dah0 + (uint64_t)(dx * 8 + 2 * k);
                                     const uint64_t adl = dal0 + (uint64_t)(dx * 8 + 2 * k);
-                                    const uint64_t bdh = bh0 + (uint64_t)(2 * k), bdl = bdh + kBT;
+                                    const uint64_t bdh = bh0 + (uint64_t)(2 * k);
+                                    const uint64_t bdl = bdh + (kF16 ? 4 : kBT);
                                     const uint32_t acc0 = (dx == 0 && k == 0) ? 0u : 1u;
-                                    if (p3) ptx::mma_tf32_ss(d, adl, bdh, idesc, acc0);
-                                    ptx::mma_tf32_ss(d, adh, bdl, idesc, p3 ? 1u : acc0);
-                                    ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                                    if (p3) mma(d, adl, bdh, acc0);
+                                    mma(d, adh, bdl, p3 ? 1u : acc0);
+                                    mma(d, adh, bdh, 1u);
                                 }
                             }
                         }
-                        ptx::mma_commit(&acc_full[q]);
+                        commit(&acc_full[q]);
                                             } else {
                         for (int dy = 0; dy < 3; ++dy) {
                             const int y = r - dy + 1;
                             if (y < 0 || y >= n) continue;
                             const int Yg = Lb + y;  // (parts == 1 off the SH path)
-                            const int q = Yg % NACC;
+                            const int q = Yg % kNAcc;
                             const bool first = (dy == 0) || (r == 0 && dy == 1);
                             if (first) {
-                                ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Yg / NACC) & 1) ^ 1));
+                                ptx::mbar_wait(&acc_empty[q], (uint32_t)(((Yg / kNAcc) & 1) ^ 1));
                                                                 ptx::tc_fence_after();
                             }
                             const uint32_t d = tmem + (uint32_t)(q * L::kAccCols);
-                            const uint64_t bh0 = dB0 + (uint64_t)(dy * 2) * kBT;
+                            const uint64_t bh0 = dB0 + (uint64_t)(dy * kPlanes) * kBT;
                             if (do_mma) {
 #pragma unroll
-                                for (int k = 0; k < C1 / 8; ++k) {
+                                for (int k = 0; k < kSteps; ++k) {
                                     const uint64_t adh = dah0 + (uint64_t)(2 * k);
                                     const uint64_t adl = dal0 + (uint64_t)(2 * k);
-                                    const uint64_t bdh = bh0 + (uint64_t)(2 * k), bdl = bdh + kBT;
+                                    const uint64_t bdh = bh0 + (uint64_t)(2 * k);
+                                    const uint64_t bdl = bdh + (kF16 ? 4 : kBT);
                                     const uint32_t acc0 = (first && k == 0) ? 0u : 1u;
-                                    if (p3) ptx::mma_tf32_ss(d, adl, bdh, idesc, acc0);
-                                    ptx::mma_tf32_ss(d, adh, bdl, idesc, p3 ? 1u : acc0);
-                                    ptx::mma_tf32_ss(d, adh, bdh, idesc, 1u);
+                                    if (p3) mma(d, adl, bdh, acc0);
+                                    mma(d, adh, bdl, p3 ? 1u : acc0);
+                                    mma(d, adh, bdh, 1u);
                                 }
                             }
                             // row y complete: after its dy=2 contribution, or the last row's dy=1
-                            if (dy == 2 || (r == n - 1 && dy == 1)) ptx::mma_commit(&acc_full[q]);
+                            if (dy == 2 || (r == n - 1 && dy == 1)) commit(&acc_full[q]);
                                                     }
                     }
-                    ptx::mma_commit(&a_empty[slot]);
+                    commit(&a_empty[slot]);
                                     }
+            }
+            if constexpr (L3) {
+                while (l3_next < Hbase) layer3(l3_next++);  // the last rows
             }
         }
     } else if (warp >= 4 && warp < 12) {
@@ -436,8 +651,38 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     ptx::mbar_arrive(&a_full[slot]);
                     continue;
                 }
-                uint8_t* ah_t = sm + L::kOffA + (slot * 2 + 0) * L::kATile;
-                uint8_t* al_t = sm + L::kOffA + (slot * 2 + 1) * L::kATile;
+                uint8_t* ah_t = sm + L::kOffA + (slot * kPlanes + 0) * L::kATile;
+                uint8_t* al_t = ah_t + (kF16 ? 0 : L::kATile);
+                if constexpr (kF16) {
+                    const int row = SH ? x + 1 : x;
+#pragma unroll
+                    for (int c8 = 0; c8 < ((a.debug & 2) ? 0 : C1 / 8); ++c8) {
+                        uint32_t hw[4], lw[4];
+#pragma unroll
+                        for (int pr = 0; pr < 4; ++pr) {  // channel pair (c, c+1), packed FFMA2
+                            const int cp = c8 * 4 + pr;
+                            const float4* wr = reinterpret_cast<const float4*>(c_epi.w1[cp]);
+                            float2 acc = make_float2(c_epi.b1[2 * cp], c_epi.b1[2 * cp + 1]);
+#pragma unroll
+                            for (int q = 0; q < 9; ++q) {
+                                const float4 wv = wr[q];
+                                acc = __ffma2_rn(make_float2(wv.x, wv.y),
+                                                 make_float2(in[2 * q], in[2 * q]), acc);
+                                acc = __ffma2_rn(make_float2(wv.z, wv.w),
+                                                 make_float2(in[2 * q + 1], in[2 * q + 1]), acc);
+                            }
+                            const float2 t2 = tanh2_fast_s(acc, kScaleA);  // 2^14 tanh
+                            const __half2 h2 = __float22half2_rn(t2);
+                            const float2 hf = __half22float2(h2);
+                            hw[pr] = h2_bits(h2);
+                            lw[pr] = h2_bits(__float22half2_rn(make_float2(t2.x - hf.x, t2.y - hf.y)));
+                        }
+                        *reinterpret_cast<uint4*>(ah_t + sw128(row, c8 * 16)) =
+                            make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                        *reinterpret_cast<uint4*>(ah_t + sw128(row, 64 + c8 * 16)) =
+                            make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                    }
+                } else {
 #pragma unroll 2
                 for (int c4 = 0; c4 < ((a.debug & 2) ? 0 : C1 / 4); ++c4) {
                     float hv[4];
@@ -466,6 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     *reinterpret_cast<float4*>(ah_t + off) = h4;
                     *reinterpret_cast<float4*>(al_t + off) = l4;
                 }
+                }
                 ptx::fence_proxy_async_smem();
                 ptx::mbar_arrive(&a_full[slot]);
             }
@@ -473,6 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
         }
     } else if (warp >= 12) {
         // ================= epilogue: thread = pixel = TMEM lane =================
+        const float inv2 = b3s[1];  // layer-2 accumulator -> pre-activation (operand pre-scales)
         const int ew = warp - 12;  // == warp & 3 -> TMEM lane quarter
         const int x = ew * 32 + lane;
         const uint32_t lane_base = (uint32_t)(ew * 32) << 16;
@@ -497,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
 #pragma unroll
             for (int c = 0; c < ((a.debug & 4) ? 0 : 32); ++c) {
                 const int g = c & 3;
-                const float h = tanh_fast(s[c] + c_epi.b2[c]);
+                const float h = tanh_fast(fmaf(s[c], inv2, c_epi.b2[c]));
                 const float2 hh = make_float2(h, h);
                 const float4 w0 = *reinterpret_cast<const float4*>(&c_epi.w3[c][0]);
                 const float4 w1 = *reinterpret_cast<const float4*>(&c_epi.w3[c][4]);
@@ -551,6 +798,123 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 if (col_ok) om[(int64_t)y * a.ldo + x] = xres_0 + a.alpha * (b3 + o);
             }
         };
+        // layer 3 on the tensor core, one unit (output rows [o0, o1) of an image; h2 rows
+        // [e0, e1) from layer-2 accumulators [l0, l1); Lb / Hb: global ring index of row 0)
+        // pass 1 (h2 row y): layer-2 pre-activation D_{y-1}[0] + D_y[1] + D_{y+1}[2] from TMEM,
+        // h2 = tanh(. inv2 + b2) as a scaled fp16 pair into h2 tile (Hb + y) % NH (pixel x at
+        // row x + 1); the MMA warp contracts it with W3 into U_{Hb + y}.
+        // pass 2 (two rows behind): out[o] = X[o] + alpha (b3 + inv3 (U_{o-1}[0] + U_o[1] +
+        // U_{o+1}[2])).
+        auto l3_unit = [&](const Unit& U, int Lb, int Hb, const float* xm, float* om,
+                           bool col_ok) {
+            const float inv3 = b3s[2];
+            auto acc_base = [&](int j) {
+                return tmem + lane_base + (uint32_t)(((Lb + j) % kNAcc) * L::kAccCols);
+            };
+            auto wait_acc = [&](int j) {
+                const int Jg = Lb + j;
+                ptx::mbar_wait(&acc_full[Jg % kNAcc], (uint32_t)((Jg / kNAcc) & 1));
+                ptx::tc_fence_after();
+            };
+            auto release = [&](int j) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&acc_empty[(Lb + j) % kNAcc]);
+            };
+            auto u_col = [&](int j, int col) {
+                return tmem + lane_base + (uint32_t)(kUCol0 + ((Hb + j) % NU) * 16 + col);
+            };
+            float xnext = col_ok ? xm[(int64_t)U.o0 * a.ldx + x] : 0.f;  // X of the next output row
+            auto out_row = [&](int o) {
+                const int jw = o + 1 < n ? o + 1 : o;  // newest U the row needs
+                const int Jg = Hb + jw;
+                ptx::mbar_wait(&u_full[Jg % NU], (uint32_t)((Jg / NU) & 1));
+                ptx::tc_fence_after();
+                const uint32_t u1 = ptx::tmem_ld_32x32b_x1(u_col(o, 1));
+                const uint32_t u0 = o >= 1 ? ptx::tmem_ld_32x32b_x1(u_col(o - 1, 0)) : 0u;
+                const uint32_t u2 = o + 1 < n ? ptx::tmem_ld_32x32b_x1(u_col(o + 1, 2)) : 0u;
+                ptx::tmem_ld_wait();
+                // U_{o-1} is done after this row; the unit's last row also hands back U_o and
+                // U_{o+1} (an interior cut's halo row)
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (o >= 1) ptx::mbar_arrive(&u_empty[(Hb + o - 1) % NU]);
+                    if (o == U.o1 - 1) {
+                        ptx::mbar_arrive(&u_empty[(Hb + o) % NU]);
+                        if (o + 1 < U.e1) ptx::mbar_arrive(&u_empty[(Hb + o + 1) % NU]);
+                    }
+                }
+                const float v = __uint_as_float(u1) + (o >= 1 ? __uint_as_float(u0) : 0.f) +
+                                (o + 1 < n ? __uint_as_float(u2) : 0.f);
+                const float xr = xnext;
+                if (o + 1 < U.o1) xnext = col_ok ? xm[(int64_t)(o + 1) * a.ldx + x] : 0.f;
+                if (col_ok) om[(int64_t)o * a.ldo + x] = xr + a.alpha * fmaf(v, inv3, b3);
+            };
+            // at an interior cut D_{e0 - 1} = D_{l0} is data (at the image top e0 = l0 = 0)
+            wait_acc(U.e0);
+            if (U.e0 - 1 >= U.l0) wait_acc(U.e0 - 1);
+            for (int y = U.e0; y < U.e1; ++y) {
+                if (y + 1 < U.l1) wait_acc(y + 1);
+                float s[32];
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(acc_base(y) + C2, v);  // D_y[dy = 1]
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) s[c] = __uint_as_float(v[c]);
+                auto add_into = [&]() {  // s += v, as packed f32x2 adds
+#pragma unroll
+                    for (int c = 0; c < 32; c += 2) {
+                        const float2 t = __fadd2_rn(make_float2(s[c], s[c + 1]),
+                                                    make_float2(__uint_as_float(v[c]),
+                                                                __uint_as_float(v[c + 1])));
+                        s[c] = t.x;
+                        s[c + 1] = t.y;
+                    }
+                };
+                if (y - 1 >= U.l0) {
+                    ptx::tmem_ld_32x32b_x32(acc_base(y - 1), v);  // D_{y-1}[dy = 0]
+                    ptx::tmem_ld_wait();
+                    add_into();
+                }
+                if (y + 1 < U.l1) {
+                    ptx::tmem_ld_32x32b_x32(acc_base(y + 1) + 2 * C2, v);  // D_{y+1}[dy = 2]
+                    ptx::tmem_ld_wait();
+                    add_into();
+                }
+                // D_j's last reader is h2 row j + 1 (or the unit's last h2 row)
+                if (y - 1 >= U.l0) release(y - 1);
+                if (y == U.e1 - 1) {
+                    release(y);
+                    if (y + 1 < U.l1) release(y + 1);
+                }
+                const int Yg = Hb + y, hs = Yg % NH;
+                ptx::mbar_wait(&h2_empty[hs], (uint32_t)(((Yg / NH) & 1) ^ 1));
+                uint8_t* ht = sm + L::kOffH2 + hs * L::kATile;
+#pragma unroll
+                for (int c8 = 0; c8 < 4; ++c8) {
+                    uint32_t hw[4], lw[4];
+#pragma unroll
+                    for (int pr = 0; pr < 4; ++pr) {
+                        const int c = c8 * 8 + 2 * pr;
+                        const float2 t2 = tanh2_fast_s(
+                            __ffma2_rn(make_float2(s[c], s[c + 1]), make_float2(inv2, inv2),
+                                       make_float2(c_epi.b2[c], c_epi.b2[c + 1])),
+                            kScaleA);
+                        split_grid(t2, hw[pr], lw[pr]);
+                    }
+                    *reinterpret_cast<uint4*>(ht + sw128(x + 1, c8 * 16)) =
+                        make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                    *reinterpret_cast<uint4*>(ht + sw128(x + 1, 64 + c8 * 16)) =
+                        make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                }
+                // the output row two behind while the stores drain, then publish h2 row y
+                if (y - 2 >= U.o0 && y - 2 < U.o1) out_row(y - 2);
+                ptx::fence_proxy_async_smem();
+                ptx::mbar_arrive(&h2_full[hs]);
+            }
+            for (int o = max(U.o0, U.e1 - 2); o < U.o1; ++o) out_row(o);
+        };
         if constexpr (!SPLIT) {  // whole images (the common case): the tuned loop as is
         int it = 0;
         for (int64_t mem = blockIdx.x; mem < a.n_members; mem += gridDim.x, ++it) {
@@ -558,23 +922,25 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
             const float* xm = a.x + mem * W;
             float* om = a.out + mem * W;
             const bool col_ok = mem * W + x < a.cols_total;
-            if constexpr (SH) {
+            if constexpr (L3) {
+                l3_unit(Unit{(int)mem, 0, n, 0, n, 0, n}, it * n, it * n, xm, om, col_ok);
+            } else if constexpr (SH) {
                 // accumulator D_j (input row j) holds contributions to output rows j + 1 (dy = 0
                 // block), j (dy = 1) and j - 1 (dy = 2): output row y = D_{y-1}[0] + D_y[1] +
                 // D_{y+1}[2], read straight from TMEM (three live accumulators of the ring), so no
                 // running sums are carried in registers; D_{y-1} is released after row y
                 auto acc_base = [&](int j) {
-                    return tmem + lane_base + (uint32_t)(((it * n + j) % NACC) * L::kAccCols);
+                    return tmem + lane_base + (uint32_t)(((it * n + j) % kNAcc) * L::kAccCols);
                 };
                 auto wait_acc = [&](int j) {
                     const int Jg = it * n + j;
-                    ptx::mbar_wait(&acc_full[Jg % NACC], (uint32_t)((Jg / NACC) & 1));
+                    ptx::mbar_wait(&acc_full[Jg % kNAcc], (uint32_t)((Jg / kNAcc) & 1));
                     ptx::tc_fence_after();
                 };
                 auto release = [&](int j) {
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&acc_empty[(it * n + j) % NACC]);
+                    if (lane == 0) ptx::mbar_arrive(&acc_empty[(it * n + j) % kNAcc]);
                 };
                 // SH: the cross-warp boundary taps of row y are exchanged through 4 smem buffers
                 // with an mbarrier each, and consumed one row later (phase B), so the four
@@ -593,7 +959,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     }
 #pragma unroll
                     for (int c = 0; c < ((a.debug & 4) ? 0 : 32); c += 2) {
-                        const float2 h2 = tanh2_fast(__fadd2_rn(make_float2(sv[c], sv[c + 1]),
+                        const float2 h2 = tanh2_fast(__ffma2_rn(make_float2(sv[c], sv[c + 1]),
+                                                                make_float2(inv2, inv2),
                                                                 make_float2(c_epi.b2[c], c_epi.b2[c + 1])));
 #pragma unroll
                         for (int u = 0; u < 2; ++u) {
@@ -712,9 +1079,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 float xpre = 0.f;
                 for (int y = 0; y < n; ++y) {
                     const int Yg = it * n + y;
-                    const int q = Yg % NACC;
+                    const int q = Yg % kNAcc;
                     const int par = Yg & 1;
-                    ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / NACC) & 1));
+                    ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / kNAcc) & 1));
                     ptx::tc_fence_after();
                     const uint32_t base = tmem + lane_base + (uint32_t)(q * L::kAccCols);
                     float s[32];
@@ -789,23 +1156,25 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
             const float* xm = a.x + mem * W;
             float* om = a.out + mem * W;
             const bool col_ok = mem * W + x < a.cols_total;
-            if constexpr (SH) {
+            if constexpr (L3) {
+                l3_unit(U, Lb, Hb, xm, om, col_ok);
+            } else if constexpr (SH) {
                 // accumulator D_j (input row j) holds contributions to output rows j + 1 (dy = 0
                 // block), j (dy = 1) and j - 1 (dy = 2): output row y = D_{y-1}[0] + D_y[1] +
                 // D_{y+1}[2], read straight from TMEM (three live accumulators of the ring), so no
                 // running sums are carried in registers; D_{y-1} is released after row y
                 auto acc_base = [&](int j) {
-                    return tmem + lane_base + (uint32_t)(((Lb + j) % NACC) * L::kAccCols);
+                    return tmem + lane_base + (uint32_t)(((Lb + j) % kNAcc) * L::kAccCols);
                 };
                 auto wait_acc = [&](int j) {
                     const int Jg = Lb + j;
-                    ptx::mbar_wait(&acc_full[Jg % NACC], (uint32_t)((Jg / NACC) & 1));
+                    ptx::mbar_wait(&acc_full[Jg % kNAcc], (uint32_t)((Jg / kNAcc) & 1));
                     ptx::tc_fence_after();
                 };
                 auto release = [&](int j) {
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&acc_empty[(Lb + j) % NACC]);
+                    if (lane == 0) ptx::mbar_arrive(&acc_empty[(Lb + j) % kNAcc]);
                 };
                 // SH: the cross-warp boundary taps of row y are exchanged through 4 smem buffers
                 // with an mbarrier each, and consumed one row later (phase B), so the four
@@ -824,7 +1193,8 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                     }
 #pragma unroll
                     for (int c = 0; c < ((a.debug & 4) ? 0 : 32); c += 2) {
-                        const float2 h2 = tanh2_fast(__fadd2_rn(make_float2(sv[c], sv[c + 1]),
+                        const float2 h2 = tanh2_fast(__ffma2_rn(make_float2(sv[c], sv[c + 1]),
+                                                                make_float2(inv2, inv2),
                                                                 make_float2(c_epi.b2[c], c_epi.b2[c + 1])));
 #pragma unroll
                         for (int u = 0; u < 2; ++u) {
@@ -952,9 +1322,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                 float xpre = 0.f;
                 for (int y = 0; y < n; ++y) {
                     const int Yg = Lb + y;  // parts == 1 here: Lb = rows of earlier images
-                    const int q = Yg % NACC;
+                    const int q = Yg % kNAcc;
                     const int par = Yg & 1;
-                    ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / NACC) & 1));
+                    ptx::mbar_wait(&acc_full[q], (uint32_t)((Yg / kNAcc) & 1));
                     ptx::tc_fence_after();
                     const uint32_t base = tmem + lane_base + (uint32_t)(q * L::kAccCols);
                     float s[32];
@@ -1045,8 +1415,14 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     if (warp == 2) ptx::tmem_dealloc(tmem, L::kTmemAlloc);
 }
 
-__global__ void cnn3_epi_pack_kernel(const float* __restrict__ b2, const float* __restrict__ w3,
+__global__ void cnn3_epi_pack_kernel(const float* __restrict__ w1, const float* __restrict__ b1,
+                                     const float* __restrict__ b2, const float* __restrict__ w3,
                                      const float* __restrict__ b3, Cnn3Epi* __restrict__ out) {
+    for (int e = threadIdx.x; e < C1 * 18; e += blockDim.x) {
+        const int c = e / 18, k = e - c * 18;  // k = ci*9 + ky*3 + kx
+        out->w1[c >> 1][k * 2 + (c & 1)] = w1[c * 18 + k];
+    }
+    for (int e = threadIdx.x; e < C1; e += blockDim.x) out->b1[e] = b1[e];
     for (int e = threadIdx.x; e < C2 * kW3Stride; e += blockDim.x) {
         const int c = e / kW3Stride, k = e - c * kW3Stride;
         out->w3[c][k] = k < 9 ? w3[c * 9 + k] : 0.f;
@@ -1117,7 +1493,7 @@ int cnn3_tc_forward_nz(const float* weights, const float* biases, float alpha, c
             set_error("cnn3_tc: constant scratch allocation failed");
             return ENKS_E_CUDA;
         }
-        cnn3_epi_pack_kernel<<<1, 256, 0, st>>>(a.b2, a.w3, a.b3, scr);
+        cnn3_epi_pack_kernel<<<1, 256, 0, st>>>(a.w1, a.b1, a.b2, a.w3, a.b3, scr);
         int rc = check_launch("enks_cnn_forward(epi pack)");
         if (rc) return rc;
         if (cudaMemcpyToSymbolAsync(c_epi, scr, sizeof(Cnn3Epi), 0, cudaMemcpyDeviceToDevice, st) !=
