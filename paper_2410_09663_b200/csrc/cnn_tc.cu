@@ -319,7 +319,9 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     constexpr bool L3 = SH && kL3;
     constexpr int kNAcc = L3 ? 4 : NACC;
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index and TMEM base through a lane-0 shuffle: provably warp-uniform, so the MMA warp's
+    // descriptor arithmetic can stay in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int n = a.rows;
 
     // ---- stage weights (all threads) -------------------------------------------------
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
     if (warp == 0) {
         // ================= MMA issuer =================
         // kConvIssuer: the whole warp runs the loop and an elected lane issues each MMA / commit
