@@ -64,15 +64,6 @@ __device__ __forceinline__ uint64_t desc_sw64d(const void* smem) {
     return d;
 }
 
-__device__ __forceinline__ void mma_f16d(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-
 __device__ __forceinline__ float tanh_d(float x) {
     x = fminf(fmaxf(x, -15.f), 15.f);
     float t, r;
@@ -130,7 +121,9 @@ __global__ void __launch_bounds__(kDThreads, 1)
     uint64_t* acc_full = bars + 2 * kDStages;
     uint64_t* acc_empty = acc_full + kDAcc;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kDAcc);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index / TMEM base via a lane-0 shuffle (provably warp-uniform: the converged MMA warp
+    // keeps its descriptors in uniform registers)
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int H = a.H, strips_w = a.W / DW;
     const int64_t n_strips = a.n_members * strips_w;
 
@@ -165,7 +158,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -185,7 +178,7 @@ __global__ void __launch_bounds__(kDThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // converged: an elected lane issues
             constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(DN >> 3) << 17) |
                                        ((uint32_t)(DW >> 4) << 24);
             int64_t g = 0;
@@ -208,13 +201,13 @@ __global__ void __launch_bounds__(kDThreads, 1)
                             const uint64_t dal = desc_sw64d(al + dx * 64 + 32 * k);
                             const uint64_t dbh = desc_sw64d(bh + 32 * k);
                             const uint64_t dbl = desc_sw64d(bl + 32 * k);
-                            mma_f16d(d, dal, dbh, idesc, (dx == 0 && k == 0) ? 0u : 1u);
-                            mma_f16d(d, dah, dbl, idesc, 1u);
-                            mma_f16d(d, dah, dbh, idesc, 1u);
+                            ptx::mma_f16_ss_elect(d, dal, dbh, idesc, (dx == 0 && k == 0) ? 0u : 1u);
+                            ptx::mma_f16_ss_elect(d, dah, dbl, idesc, 1u);
+                            ptx::mma_f16_ss_elect(d, dah, dbh, idesc, 1u);
                         }
                     }
-                    ptx::mma_commit(&empty[st]);
-                    ptx::mma_commit(&acc_full[q]);
+                    ptx::mma_commit_elect(&empty[st]);
+                    ptx::mma_commit_elect(&acc_full[q]);
                 }
             }
         }

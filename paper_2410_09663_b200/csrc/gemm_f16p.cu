@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty = bars + 2 * S + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * BM;
     const int64_t col0 = (int64_t)blockIdx.y * BN;
     const int split = blockIdx.z;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // converged: an elected lane issues (uniform-register descriptors)
             constexpr uint32_t idesc = idesc_f16(BM, BN);
             for (int i = 0; i < n_chunks; ++i) {
                 const int s = i % S;
@@ -275,15 +275,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint64_t dah = desc_sw64(ah(s) + 32 * k), dal = desc_sw64(al(s) + 32 * k);
                     const uint64_t dbh = desc_sw64(bh(s) + 32 * k), dbl = desc_sw64(bl(s) + 32 * k);
                     if (p.products == 3) {
-                        mma_f16_ss(d, dal, dbh, idesc, (first && k == 0) ? 0u : 1u);
-                        mma_f16_ss(d, dah, dbl, idesc, 1u);
+                        ptx::mma_f16_ss_elect(d, dal, dbh, idesc, (first && k == 0) ? 0u : 1u);
+                        ptx::mma_f16_ss_elect(d, dah, dbl, idesc, 1u);
                     } else {
-                        mma_f16_ss(d, dah, dbl, idesc, (first && k == 0) ? 0u : 1u);
+                        ptx::mma_f16_ss_elect(d, dah, dbl, idesc, (first && k == 0) ? 0u : 1u);
                     }
-                    mma_f16_ss(d, dah, dbh, idesc, 1u);
+                    ptx::mma_f16_ss_elect(d, dah, dbh, idesc, 1u);
                 }
-                ptx::mma_commit(&empty[s]);
-                if (last) ptx::mma_commit(&tfull[slot]);
+                ptx::mma_commit_elect(&empty[s]);
+                if (last) ptx::mma_commit_elect(&tfull[slot]);
             }
         }
     } else if (warp >= 4) {
@@ -353,6 +353,24 @@ __device__ __forceinline__ void mma_f16_pair(uint32_t d_tmem, uint64_t adesc, ui
         : "memory");
 }
 
+// the same issued by an elected lane of a converged warp (operands in uniform registers)
+__device__ __forceinline__ void mma_f16_pair_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                   uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+#ifndef ENKS_F16P_CONV
+#define ENKS_F16P_CONV 1
+#endif
+constexpr bool kConvPair = ENKS_F16P_CONV;
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     f16p_gemm_pair_kernel(const __grid_constant__ CUtensorMap tAh,
                           const __grid_constant__ CUtensorMap tAl,
@@ -369,7 +387,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
 
     const uint32_t rank = ptx::cluster_ctarank();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index / TMEM base via a lane-0 shuffle: provably warp-uniform, so the converged MMA
+    // warp keeps its descriptors in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * BM;
     // persistent over 256-column tiles (blockIdx.y, + gridDim.y, ...): the next tile's loads and
     // MMAs overlap this tile's epilogue (double-buffered TMEM slots continue across tiles)
@@ -408,7 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::cluster_sync();
     ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -430,8 +450,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {
+        if ((kConvPair || lane == 0) && rank == 0) {
             constexpr uint32_t idesc = idesc_f16(2 * BM, 256);
+            auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+                if constexpr (kConvPair) mma_f16_pair_elect(d, a, b, idesc, acc);
+                else mma_f16_pair(d, a, b, idesc, acc);
+            };
+            auto commit = [&](uint64_t* bar) {
+                if constexpr (kConvPair) ptx::mma_commit_pair_elect(bar, 0x3);
+                else ptx::mma_commit_pair(bar, 0x3);
+            };
             int ig = 0, gbase = 0;  // chunk / chain-group counters across tiles
             for (int64_t nt = blockIdx.y; nt < n_tiles; nt += gridDim.y, gbase += n_groups) {
             for (int i = 0; i < n_chunks; ++i, ++ig) {
@@ -451,15 +479,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const uint64_t dah = desc_sw64(ah(s) + 32 * k), dal = desc_sw64(al(s) + 32 * k);
                     const uint64_t dbh = desc_sw64(bh(s) + 32 * k), dbl = desc_sw64(bl(s) + 32 * k);
                     if (p.products == 3) {
-                        mma_f16_pair(d, dal, dbh, idesc, (first && k == 0) ? 0u : 1u);
-                        mma_f16_pair(d, dah, dbl, idesc, 1u);
+                        mma(d, dal, dbh, (first && k == 0) ? 0u : 1u);
+                        mma(d, dah, dbl, 1u);
                     } else {
-                        mma_f16_pair(d, dah, dbl, idesc, (first && k == 0) ? 0u : 1u);
+                        mma(d, dah, dbl, (first && k == 0) ? 0u : 1u);
                     }
-                    mma_f16_pair(d, dah, dbh, idesc, 1u);
+                    mma(d, dah, dbh, 1u);
                 }
-                ptx::mma_commit_pair(&empty[s], 0x3);
-                if (last) ptx::mma_commit_pair(&tfull[slot], 0x3);
+                commit(&empty[s]);
+                if (last) commit(&tfull[slot]);
             }
             }
         }

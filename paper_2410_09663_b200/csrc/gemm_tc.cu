@@ -115,7 +115,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty = bars + 3 * S + 2;  // [2] slot drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warp index / TMEM base via a lane-0 shuffle: provably warp-uniform, so the converged MMA
+    // warp keeps its descriptors in uniform registers (tc_ptx.cuh, *_elect)
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * BM;
     const int64_t col0 = (int64_t)blockIdx.y * BN;
     // CL > 1: the CTAs of a cluster (consecutive row tiles, same K range) share the B tile:
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (CL > 1) ptx::cluster_sync();  // peers' barriers initialised before any multicast
     ptx::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {  // converged: an elected lane issues
             uint32_t idesc = ptx::idesc_tf32(BM, BN);
             if (BMN) idesc |= 1u << 16;  // B MN-major
             for (int i = 0; i < n_chunks; ++i) {
@@ -225,13 +227,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         bl = desc_mnmajor_sw128(stage_bl(s) + 1024 * k, p.mn_lbo, p.mn_sbo);
                     }
                     uint32_t acc = (first && k == 0) ? 0u : 1u;
-                    if (p.products & 1) { ptx::mma_tf32_ss(d, al, bh, idesc, acc); acc = 1u; }
-                    if (p.products & 2) { ptx::mma_tf32_ss(d, ah, bl, idesc, acc); acc = 1u; }
-                    if (p.products & 4) { ptx::mma_tf32_ss(d, ah, bh, idesc, acc); }
+                    if (p.products & 1) { ptx::mma_tf32_ss_elect(d, al, bh, idesc, acc); acc = 1u; }
+                    if (p.products & 2) { ptx::mma_tf32_ss_elect(d, ah, bl, idesc, acc); acc = 1u; }
+                    if (p.products & 4) { ptx::mma_tf32_ss_elect(d, ah, bh, idesc, acc); }
                 }
-                if (CL > 1) ptx::mma_commit_mc(&empty[s], kMask);
-                else ptx::mma_commit(&empty[s]);
-                if (last) ptx::mma_commit(&tfull[slot]);
+                if (CL > 1) ptx::mma_commit_mc_elect(&empty[s], kMask);
+                else ptx::mma_commit_elect(&empty[s]);
+                if (last) ptx::mma_commit_elect(&tfull[slot]);
             }
         }
     } else if (warp >= 4) {
