@@ -612,7 +612,10 @@ class DeviceSmoother:
         if getattr(self.ops, "device", None) is None or self.ops.device.type != "cuda":
             return None
         if getattr(self, "_side", None) is None:
-            self._side = torch.cuda.Stream(device=self.ops.device)
+            # high priority: the one-CTA gain solve is dispatched ahead of the cross-moment CTAs
+            # queued behind it on the main stream, instead of waiting for an SM to drain
+            prio = int(os.environ.get("ENKS_SIDE_PRIORITY", "-1"))
+            self._side = torch.cuda.Stream(device=self.ops.device, priority=prio)
         return self._side
 
     @_nvtx("enks.gain_solve")
