@@ -46,7 +46,10 @@ constexpr int W = 128;     // image width (== MMA M)
 constexpr int C1 = 32;     // layer-1 width
 constexpr int C2 = 32;     // layer-2 width
 constexpr int NB = 3 * C2; // MMA N: (dx, co)
-constexpr int NA = 3;      // layer-1 row slots
+#ifndef ENKS_CNN_NA
+#define ENKS_CNN_NA 3
+#endif
+constexpr int NA = ENKS_CNN_NA;      // layer-1 row slots
 constexpr int NACC = 5;    // TMEM accumulators (ring over rows; 5 x 96 <= 512 columns)
 constexpr int kThreads = 512;
 constexpr int kRing = 8;   // input-row ring slots per producer group
@@ -132,7 +135,8 @@ struct CL {
     static constexpr int kOffB3 = kOffW3 + C2 * kW3Stride * 4;  // b3, layer-2 inverse scale
     static constexpr int kOffX = kOffB3 + 16;
     static constexpr int kOffBar = kOffX + (2 * kXD + 2 * kXV) * 4;
-    static constexpr int kOffNz = kOffBar + 64 * 8;                       // noise: ki, wi tables
+    static constexpr int kOffNz = kOffBar + 64 * 8;
+    static_assert(2 * NA + 2 * NACC + 1 + 4 + 2 * NH + 2 * NU <= 64, "mbarrier region");                       // noise: ki, wi tables
     static constexpr int kNzWarp = 2 * kMaxRowCols * 4 + kBufWords * 8;     // row slots + words
     static constexpr int kOffNzW = kOffNz + 256 * 16;                       // [3] per noise warp
     static constexpr int kEndNz = kOffNzW + 3 * kNzWarp;
@@ -308,10 +312,10 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
     uint64_t* acc_empty = bars + 2 * NA + NACC;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NA + 2 * NACC);
     uint64_t* xb_full = bars + 2 * NA + 2 * NACC + 1;  // [4] SH: row's boundary taps written
-    uint64_t* h2_full = bars + 24;   // [NH] layer 3: h2 row written by the epilogue
-    uint64_t* h2_empty = bars + 28;  // [NH] layer 3: its MMAs done
-    uint64_t* u_full = bars + 32;    // [NU] layer-3 accumulator complete
-    uint64_t* u_empty = bars + 40;   // [NU] layer-3 accumulator read
+    uint64_t* h2_full = xb_full + 4;     // [NH] layer 3: h2 row written by the epilogue
+    uint64_t* h2_empty = h2_full + NH;   // [NH] layer 3: its MMAs done
+    uint64_t* u_full = h2_empty + NH;    // [NU] layer-3 accumulator complete
+    uint64_t* u_empty = u_full + NU;     // [NU] layer-3 accumulator read
     // layer 3 on the tensor core (128-pixel images, whole or split into units); the layer-2 ring
     // then has 4 accumulators (4 x 96 + NU x 16 columns).
     // (One 32-column accumulator per output row instead -- 54 N = 32 MMAs per row in place of

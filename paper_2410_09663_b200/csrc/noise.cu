@@ -21,7 +21,10 @@ namespace {
 constexpr int kWarps = 4;          // warps (streams) per block
 
 template <bool RB>
-__global__ void __launch_bounds__(kWarps * 32, 6) noise_kernel(const Args args) {
+#ifndef ENKS_NOISE_MINB
+#define ENKS_NOISE_MINB 6  // blocks per SM: 3072 C3 substreams = 768 blocks fit one wave of 6 x 148
+#endif
+__global__ void __launch_bounds__(kWarps * 32, ENKS_NOISE_MINB) noise_kernel(const Args args) {
     const Job a = args.job[blockIdx.y];  // by value: fields live in registers, not re-read
     __shared__ __align__(16) float s_row[RB ? kWarps : 1][RB ? 2 * kMaxRowCols : 1];
     __shared__ uint64_t s_ki[256];

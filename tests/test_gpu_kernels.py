@@ -446,11 +446,13 @@ def test_f16pair_gram_diagonal_bias_at_c3_depth(dev_ops):
     assert off.max().item() < 1e-6
 
 
-def test_gemm_f16pair_ex_shift_operands(dev_ops):
+@pytest.mark.parametrize("p,q,K", [(256, 256, 4096 + 128), (256, 200, 1000), (128, 96, 776)])
+def test_gemm_f16pair_ex_shift_operands(dev_ops, p, q, K):
     """Newest-slice shift: transposed re-split of fp16-pair rows, then the fused-epilogue GEMM
-    C = C0 + bias - G Yc with N = K in 256-column tiles."""
-    g = torch.Generator().manual_seed(5)
-    p, q, K, m = 256, 256, 4096 + 128, 128
+    C = C0 + bias - G Yc with N = K in 256-column tiles (the coalesced transposed epilogue; rows
+    and columns not multiples of the 128 x 256 tile)."""
+    g = torch.Generator().manual_seed(5 + q)
+    m = 128
     Y = torch.randn(p, K, generator=g) * torch.logspace(-2, 2, p).unsqueeze(1)
     G = torch.randn(q, p, generator=g) * 0.01
     C0 = torch.randn(q, K, generator=g)
