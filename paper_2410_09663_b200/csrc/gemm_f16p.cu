@@ -322,12 +322,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 // The leader CTA (rank 0) issues the MMAs; its full[] barriers count both CTAs' TMA bytes;
 // MMA completion is multicast to both CTAs' empty[] / tfull[] barriers; each CTA drains
 // its own TMEM (its 128 rows x 256 columns) and arrives on the leader's tempty[].
-constexpr int kTBufBytes = 8 * 32 * 32 * 4;  // pair kernel: coalesced-epilogue transpose buffers
-#ifndef ENKS_F16P_TB
-#define ENKS_F16P_TB 8
-#endif
-constexpr int kTB = ENKS_F16P_TB;  // rows per load batch of that epilogue
-
 struct LP {
     static constexpr int kA = BM * KC * 2;       // 8 KB per plane (128 rows)
     static constexpr int kB = 128 * KC * 2;      // 8 KB per plane (this CTA's 128 B rows)
@@ -379,7 +373,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tfull = bars + 2 * S;   // both
     uint64_t* tempty = bars + 2 * S + 2;  // leader's are used
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
-    float* tbuf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);  // kTBufBytes
 
     const uint32_t rank = ptx::cluster_ctarank();
     // warp index / TMEM base via a lane-0 shuffle: provably warp-uniform, so the converged MMA
@@ -494,61 +487,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int gbase = 0;
         for (int64_t nt = blockIdx.y; nt < n_tiles; nt += gridDim.y, gbase += n_groups) {
         const int64_t col0 = nt * 256;
-        if ((p.c0 || p.bias) && n_groups == 1) {
-            // fused C0 / bias epilogue of a single-chain tile (the newest-slice shift: q x K
-            // outputs, HBM-bound): per 32-column block straight from TMEM, the warp's 32 rows go
-            // through shared memory (XOR-swizzled: no bank conflicts either way), so every global
-            // access of C0, bias and out is one 128-B row segment per warp instruction instead of
-            // 32 scattered 16-B pieces
-            const int slot = gbase & 1;
-            ptx::mbar_wait_bounded(&tfull[slot], (uint32_t)((gbase >> 1) & 1));
-            ptx::tc_fence_after();
-            const uint32_t base = tmem + lane_base + (uint32_t)(slot * LP::kCols + wg * kCols);
-            float* tb = tbuf + (warp - 4) * 1024;
-            const int64_t r = row0 + erow;
-            const float sa = r < p.M ? p.alpha * p.inv_sa[r] : 0.f;
-            const int64_t rbase = row0 + ((warp & 3) << 5);
-            const int64_t c_first = col0 + (int64_t)wg * kCols;
-            for (int cb = 0; cb < kCols / 32; ++cb) {
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(base + cb * 32, v);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    tb[lane * 32 + (j ^ lane)] = __uint_as_float(v[j]) * sa;
-                __syncwarp();
-                const int64_t c = c_first + cb * 32 + lane;
-                const bool cok = c < p.N;
-                const float sb = cok ? p.inv_sb[c] : 0.f;
-                const float* bcol = p.bias && cok ? p.bias + (int)(c % p.bias_cols) : nullptr;
-                const float* ccol = p.c0 && cok ? p.c0 + c : nullptr;
-                float* ocol = p.out + c;
-#pragma unroll
-                for (int i0 = 0; i0 < 32; i0 += kTB) {
-                    float cv[kTB], bv[kTB];
-#pragma unroll
-                    for (int u = 0; u < kTB; ++u) {  // loads of the batch before its stores
-                        const int64_t rr = rbase + i0 + u;
-                        const bool ok = rr < p.M;
-                        cv[u] = ok && ccol ? __ldg(ccol + rr * p.ldc0) : 0.f;
-                        bv[u] = ok && bcol ? __ldg(bcol + rr * p.ld_bias) : 0.f;
-                    }
-#pragma unroll
-                    for (int u = 0; u < kTB; ++u) {
-                        const int i = i0 + u;
-                        const int64_t rr = rbase + i;
-                        if (rr < p.M && cok)
-                            ocol[rr * p.ldo] = fmaf(tb[i * 32 + (lane ^ i)], sb,
-                                                    fmaf(p.beta, cv[u], bv[u]));
-                    }
-                }
-                __syncwarp();
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(&tempty[slot], 0);
-            continue;
-        }
         float acc[kCols];
 #pragma unroll
         for (int j = 0; j < kCols; ++j) acc[j] = 0.f;
@@ -572,9 +510,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         const int64_t r = row0 + erow;
         const int64_t c_first = col0 + (int64_t)wg * kCols;
-        if (r < p.M && c_first < p.N) {
+        if (r < p.M && c_first < p.N)
             f16p_store_row(p, split, r, c_first, (int)min((int64_t)kCols, p.N - c_first), acc);
-        }
         }
     }
     ptx::tc_fence_before();
@@ -762,8 +699,7 @@ int launch_pair(const CUtensorMap* maps, P16 p, dim3 grid, cudaStream_t st) {
     int stages = kSmemBudget / LP::kStage;
     if (stages > 8) stages = 8;
     p.stages = stages;
-    // + the epilogue's transpose buffers (8 warps x 32 x 32 fp32) behind the barriers
-    const size_t smem = (size_t)stages * LP::kStage + 1024 + 512 + kTBufBytes;
+    const size_t smem = (size_t)stages * LP::kStage + 1024 + 512;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(f16p_gemm_pair_kernel,
