@@ -243,6 +243,13 @@ int enks_f16pair_split(const float* src, int64_t ld, int64_t rows, int64_t K, vo
 int enks_f16pair_recon(const void* h, const void* l, int64_t ldi, const float* inv_scale,
                        int64_t rows, int64_t K, float* out, int64_t ldo, void* stream);
 int64_t enks_gemm_f16pair_ws_bytes(int64_t M, int64_t N, int64_t K);
+
+/* Leave `sms` SMs (0..16) free in the grids of the following enks_gemm_f16pair launches (split-K
+ * and persistent-pair sizing), so a concurrent one-CTA kernel -- the side-stream gain solve of
+ * enks.py:234-246, which overlaps the cross moments of enks.py:148-153 -- gets an SM at once
+ * instead of after the first cross-moment CTA drains.  Host-side state, read at launch (and so
+ * baked into captured graphs); 0 restores full grids.  Returns ENKS_OK. */
+int enks_set_sm_reserve(int sms);
 int enks_gemm_f16pair(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah, const void* Al,
                       int64_t lda, const float* inv_sa, const void* Bh, const void* Bl, int64_t ldb,
                       const float* inv_sb, float* C, int64_t ldc, void* ws, void* stream);

@@ -78,6 +78,7 @@ _SIGS = {
     "enks_f16pair_split": (_c_int, [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_i64, _vp, _vp]),
     "enks_f16pair_recon": (_c_int, [_vp, _vp, _c_i64, _vp, _c_i64, _c_i64, _vp, _c_i64, _vp]),
     "enks_gemm_f16pair_ws_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
+    "enks_set_sm_reserve": (_c_int, [_c_int]),
     "enks_gemm_f16pair": (_c_int, [_c_i64, _c_i64, _c_i64, _c_f, _vp, _vp, _c_i64, _vp, _vp, _vp,
                                    _c_i64, _vp, _vp, _c_i64, _vp, _vp]),
     "enks_gemm_f16pair_ex": (_c_int, [_c_i64, _c_i64, _c_i64, _c_f, _vp, _vp, _c_i64, _vp, _vp, _vp,

@@ -715,10 +715,15 @@ int launch_pair(const CUtensorMap* maps, P16 p, dim3 grid, cudaStream_t st) {
 }
 
 // pairs of CTAs over 74 pair slots
+// SMs left free for a concurrent one-CTA kernel (the side-stream gain solve): set by the host
+// around the cross-moment launches of update() (enks_set_sm_reserve), 0 otherwise
+int g_sm_reserve = 0;
+int usable_sms() { return kNumSMs - g_sm_reserve; }
+
 int choose_split_pairs(int pairs, int64_t chunks) {
     int best = 1;
     double best_eff = 0.0;
-    const int slots = kNumSMs / 2;
+    const int slots = usable_sms() / 2;
     for (int s = 1; s <= 64; ++s) {
         if (chunks / s < 8 && s > 1) break;
         const int units = pairs * s;
@@ -743,8 +748,8 @@ int choose_split16(int tiles, int64_t chunks) {
     for (int s = 1; s <= 64; ++s) {
         if (chunks / s < 8 && s > 1) break;
         const int units = tiles * s;
-        const int waves = (units + kNumSMs - 1) / kNumSMs;
-        const double eff = (double)units / (double)(waves * kNumSMs);
+        const int waves = (units + usable_sms() - 1) / usable_sms();
+        const double eff = (double)units / (double)(waves * usable_sms());
         if (eff > best_eff + 0.03) {
             best_eff = eff;
             best = s;
@@ -854,7 +859,7 @@ int gemm_f16pair_impl(int64_t M, int64_t N, int64_t K, float alpha, const void* 
         grid.x = (unsigned)((m_tiles + 1) & ~1);
         // one wave of CTA pairs, each looping over 256-column tiles
         const int64_t pairs_xz = (int64_t)(grid.x / 2) * split;
-        const int64_t slots = kNumSMs / 2;
+        const int64_t slots = usable_sms() / 2;
         const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(n_tiles, slots / std::max<int64_t>(1, pairs_xz)));
         grid.y = (unsigned)gy;
         rc = launch_pair(maps, p, grid, st);
@@ -873,6 +878,12 @@ int gemm_f16pair_impl(int64_t M, int64_t N, int64_t K, float alpha, const void* 
 }  // namespace enks
 
 extern "C" {
+
+int enks_set_sm_reserve(int sms) {
+    ENKS_REQUIRE(sms >= 0 && sms <= 16, "enks_set_sm_reserve: %d outside [0, 16]", sms);
+    enks::g_sm_reserve = sms;
+    return ENKS_OK;
+}
 
 int64_t enks_gemm_f16pair_ws_bytes(int64_t M, int64_t N, int64_t K) {
     const int split = enks::f16p_split_for(M, N, K, false);

@@ -578,6 +578,9 @@ class DeviceSmoother:
                    and hasattr(ops, "cnn_forward_noise") and ops.cnn_noise_fusable(self.forecast, self.n))
         self.noise_in_forecast = (max(0, min(3, int(os.environ.get("ENKS_NOISE_IN_CNN", "0"))))
                                   if fusable else 0)
+        # SMs the cross-moment grids leave to the concurrent side-stream gain solve (update())
+        self.sm_reserve = (max(0, min(16, int(os.environ.get("ENKS_SM_RESERVE", "2"))))
+                           if hasattr(ops, "set_sm_reserve") else 0)
         if self.fused_noise and getattr(self, "v_raw", None) is None:
             self.v_raw = ops.empty(self.q, self.K)  # raw [v_x; v_u] of the newest step
         # observation never materialised: its centring forms [x; u] + [v_x; v_u] on the fly and
@@ -865,12 +868,19 @@ class DeviceSmoother:
             comm.allreduce_(PY[(tau - 1) * p:])
             self._spd_async(side, PY[(tau - 1) * p:], scale)
             self._finish_slice()  # the new slice's centring, next to the gain solve
+            # the cross-moment grids leave SMs to the side-stream gain solve (one CTA that
+            # otherwise waits for the first cross CTA to drain: exposed at small ensembles)
+            reserve = self.sm_reserve if side is not None else 0
+            if reserve:
+                ops.set_sm_reserve(reserve)
             ops.gemm_f16pair(self.Ah[a0:rows_a], self.Al[a0:rows_a], self.a_inv[a0:rows_a],
                              yh, yl, yi, PA, tag="cross")
             if tau > 1:
                 ops.gemm_f16pair(self.Yh[:(tau - 1) * p], self.Yl[:(tau - 1) * p],
                                  self.y_inv[:(tau - 1) * p], yh, yl, yi, PY[:(tau - 1) * p],
                                  tag="cross")
+            if reserve:
+                ops.set_sm_reserve(0)
             comm.allreduce_many([PY[:(tau - 1) * p], PA])  # one collective for the rest of P
         else:
             if self.use_tc:

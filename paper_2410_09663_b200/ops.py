@@ -359,6 +359,10 @@ class DeviceOps:
         _lib.call("enks_f16pair_recon", _p(h), _p(l), _ld(h), _p(inv_scale), out.shape[0],
                   out.shape[1], _p(out), _ld(out), self._stream())
 
+    def set_sm_reserve(self, sms: int) -> None:
+        """SMs left free in the next cross-moment grids (enks_set_sm_reserve)."""
+        _lib.call("enks_set_sm_reserve", int(sms))
+
     def gemm_f16pair(self, Ah, Al, inv_sa, Bh, Bl, inv_sb, C, *, alpha=1.0, tag=None):
         """C = alpha * diag(inv_sa) (Ah + Al)(Bh + Bl)^T diag(inv_sb), tcgen05 kind::f16."""
         M, K = Ah.shape
