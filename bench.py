@@ -380,8 +380,9 @@ def run_ours(args):
     achieved = (kern_flops / max(kern_s, 1e-12)) / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
     traffic, traffic_note = None, None
-    tpath = os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")
-    if os.path.exists(tpath):
+    tpath = next((q for q in (os.path.join(ROOT, "profiles", r, "roofline_traffic.json")
+                              for r in ("r02", "r01")) if os.path.exists(q)), "")
+    if tpath:
         with open(tpath) as f:
             tj = json.load(f)
         traffic = tj.get("dram_bytes")
