@@ -57,11 +57,11 @@ constexpr int kRing = 8;   // input-row ring slots per producer group
 // Layer-2 operand format.  fp16 pairs (default): one 128-B SWIZZLE_128B row holds a pixel's (or a
 // weight row's) 32 channels as fp16 hi (bytes 0-63) and lo (bytes 64-127) -- one tile per operand,
 // kind::f16 MMAs (K = 16) at twice the kind::tf32 rate, half the shared-memory stores of the
-// producers.  Three products (lo*hi + hi*lo + hi*hi) give the same ~2^-22 operand precision as
-// 3xTF32 as long as neither half is subnormal, so both operands are pre-scaled by powers of two:
-// the layer-1 activations (|tanh| < 1) by 2^14, W2 so that its largest |entry| lands in
-// [2^14, 2^15); the epilogue folds the inverse scale into the layer-2 bias add (one FFMA in place
-// of the FADD).  Build with -DENKS_CNN_TF32=1 for the previous 3xTF32 operands (separate fp32
+// producers.  Three products (lo*hi + hi*lo + hi*hi) keep the operands to ~2^-22 of their range,
+// as 3xTF32 does, so both are pre-scaled by powers of two: the activations (|tanh| < 1) by 2^14
+// and split on a fixed grid (split_grid: |error| <= 2^-10 at scale 2^14, i.e. 6e-8 absolute),
+// W2 / W3 so that their largest |entry| lands in [2^14, 2^15) (exact split); the epilogue folds
+// the inverse scale into the bias add (one FFMA in place of the FADD).  Build with -DENKS_CNN_TF32=1 for the previous 3xTF32 operands (separate fp32
 // hi / lo tiles).
 #ifndef ENKS_CNN_TF32
 #define ENKS_CNN_TF32 0
@@ -677,11 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                                 acc = __ffma2_rn(make_float2(wv.z, wv.w),
                                                  make_float2(in[2 * q + 1], in[2 * q + 1]), acc);
                             }
-                            const float2 t2 = tanh2_fast_s(acc, kScaleA);  // 2^14 tanh
-                            const __half2 h2 = __float22half2_rn(t2);
-                            const float2 hf = __half22float2(h2);
-                            hw[pr] = h2_bits(h2);
-                            lw[pr] = h2_bits(__float22half2_rn(make_float2(t2.x - hf.x, t2.y - hf.y)));
+                            split_grid(tanh2_fast_s(acc, kScaleA), hw[pr], lw[pr]);  // 2^14 tanh
                         }
                         *reinterpret_cast<uint4*>(ah_t + sw128(row, c8 * 16)) =
                             make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -863,11 +859,7 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
             for (int y = U.e0; y < U.e1; ++y) {
                 if (y + 1 < U.l1) wait_acc(y + 1);
                 float s[32];
-                uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(acc_base(y) + C2, v);  // D_y[dy = 1]
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int c = 0; c < 32; ++c) s[c] = __uint_as_float(v[c]);
+                uint32_t v[32], w[32];
                 auto add_into = [&]() {  // s += v, as packed f32x2 adds
 #pragma unroll
                     for (int c = 0; c < 32; c += 2) {
@@ -878,9 +870,15 @@ __global__ void __launch_bounds__(kThreads, 1) cnn3_tc_kernel(const Cnn3Args a) 
                         s[c + 1] = t.y;
                     }
                 };
-                if (y - 1 >= U.l0) {
-                    ptx::tmem_ld_32x32b_x32(acc_base(y - 1), v);  // D_{y-1}[dy = 0]
-                    ptx::tmem_ld_wait();
+                // D_y[dy = 1] and D_{y-1}[dy = 0] in flight together (one TMEM round trip)
+                const bool up = y - 1 >= U.l0;
+                ptx::tmem_ld_32x32b_x32(acc_base(y) + C2, w);
+                if (up) ptx::tmem_ld_32x32b_x32(acc_base(y - 1), v);
+                ptx::tmem_ld_wait_regs(w);
+#pragma unroll
+                for (int c = 0; c < 32; ++c) s[c] = __uint_as_float(w[c]);
+                if (up) {
+                    ptx::tmem_ld_wait_regs(v);
                     add_into();
                 }
                 if (y + 1 < U.l1) {
