@@ -95,7 +95,15 @@ class DeviceOps:
         dst.copy_(t)
 
     def to_host(self, t) -> np.ndarray:
-        """Device tensor -> fp64 NumPy (copied in its own dtype, widened on the host)."""
+        """Device tensor -> fp64 NumPy.  Results up to 64 MB (mean trajectories, P / G blocks) are
+        widened on the device and copied once into pinned memory (torch's cached pinned pool; the
+        array keeps its buffer alive); larger ones (tracked covariances) are copied in their own
+        dtype and widened on the host, without a pinned / fp64 device copy of their size."""
+        if t.is_cuda and t.numel() * 8 <= (64 << 20):
+            h = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
+            h.copy_(t.double())
+            self.d2h_bytes += h.numel() * h.element_size()
+            return h.numpy()
         self.d2h_bytes += t.numel() * t.element_size()
         return t.cpu().double().numpy()
 
