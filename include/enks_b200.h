@@ -161,7 +161,9 @@ int enks_cnn_forward_noise(int n_layers, const int* widths, const float* weights
  * fly as src + src2 ([x; u] + [v_x; v_u]; enks_member_sum takes the same src2): writes the
  * fp16-pair basis rows (h, l, inv_scale, as enks_member_center_f16pair), the member mean, and
  * the transposed pair planes th / tl (K x rows, ld ldt) with one scale per K row (t_inv) --
- * the K-major B operand of the newest-slice shift (enks.py:247).  rows <= 256.
+ * the K-major B operand of the newest-slice shift (enks.py:247).  rows <= 256.  th, tl and
+ * t_inv may all be NULL: no transposed planes (the shift then reads the basis rows MN-major,
+ * enks_gemm_f16pair_ex_mn).
  */
 int enks_member_center_f16pair_t(const float* src, int64_t ld_src, const float* src2,
                                  int64_t ld_src2, int rows, int64_t n_members, int cols,
@@ -240,6 +242,11 @@ int enks_gemm_tc(int64_t M, int64_t N, int64_t K, float alpha, const float* A, i
  */
 int enks_f16pair_split(const float* src, int64_t ld, int64_t rows, int64_t K, void* h, void* l,
                        int64_t ldo, float* inv_scale, void* stream);
+/* enks_f16pair_split of src[r][k] * col_scale[k] (a per-column power of two folded in first:
+ * the per-row scale of the other operand of a reduction over k, e.g. Yc_tau's for G_tt). */
+int enks_f16pair_split_cs(const float* src, int64_t ld, int64_t rows, int64_t K,
+                          const float* col_scale, void* h, void* l, int64_t ldo, float* inv_scale,
+                          void* stream);
 int enks_f16pair_recon(const void* h, const void* l, int64_t ldi, const float* inv_scale,
                        int64_t rows, int64_t K, float* out, int64_t ldo, void* stream);
 int64_t enks_gemm_f16pair_ws_bytes(int64_t M, int64_t N, int64_t K);
@@ -276,6 +283,16 @@ int enks_gemm_f16pair_ex(int64_t M, int64_t N, int64_t K, float alpha, const voi
                          const void* Bl, int64_t ldb, const float* inv_sb, float beta,
                          const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias,
                          int bias_cols, float* C, int64_t ldc, void* stream);
+/* As enks_gemm_f16pair_ex, but B is given MN-major: Bh / Bl are K x N row-major (ldb), i.e. the
+ * fp16-pair rows of the centred observations Yc_tau themselves (enks.py:247, newest-slice shift
+ * last = C0 + bias - G_tt Yc_tau), so no transposed copy is needed.  B carries no per-reduction-row
+ * scale here: fold it into A first (enks_f16pair_split_cs); inv_sn scales output columns (N > 128,
+ * K % 32 == 0, N % 8 == 0; CTA-pair kernel). */
+int enks_gemm_f16pair_ex_mn(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah,
+                            const void* Al, int64_t lda, const float* inv_sa, const void* Bh,
+                            const void* Bl, int64_t ldb, const float* inv_sn, float beta,
+                            const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias,
+                            int bias_cols, float* C, int64_t ldc, void* stream);
 int enks_f16pair_transpose(const void* h, const void* l, int64_t ldi, const float* inv_src,
                            int rows, int64_t cols, void* oh, void* ol, int64_t ldo, float* inv_out,
                            void* stream);

@@ -84,6 +84,11 @@ _SIGS = {
     "enks_gemm_f16pair_ex": (_c_int, [_c_i64, _c_i64, _c_i64, _c_f, _vp, _vp, _c_i64, _vp, _vp, _vp,
                                       _c_i64, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _c_int, _vp,
                                       _c_i64, _vp]),
+    "enks_gemm_f16pair_ex_mn": (_c_int, [_c_i64, _c_i64, _c_i64, _c_f, _vp, _vp, _c_i64, _vp, _vp,
+                                         _vp, _c_i64, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _c_int,
+                                         _vp, _c_i64, _vp]),
+    "enks_f16pair_split_cs": (_c_int, [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _c_i64, _vp,
+                                       _vp]),
     "enks_f16pair_transpose": (_c_int, [_vp, _vp, _c_i64, _vp, _c_int, _c_i64, _vp, _vp, _c_i64,
                                         _vp, _vp]),
     "enks_spd_max_p": (_c_int, []),

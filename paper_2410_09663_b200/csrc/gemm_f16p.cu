@@ -64,6 +64,7 @@ struct P16 {
     int stages;
     int chain;
     int products;  // 3: lh + hl + hh;  2: hl + hh (A's low plane not read)
+    int b_mn;      // pair kernel: B given MN-major ([K][N], N contiguous), no per-column scale
     // fused epilogue terms (split == 1 only): + beta * C0[r, c] + bias[r, c % bias_cols]
     float beta;
     const float* c0;
@@ -88,7 +89,8 @@ __device__ __forceinline__ void f16p_store_row(const P16& p, int split, int64_t 
             for (int j0 = 0; j0 < NC; j0 += kSB) {
                 float sv[kSB];
 #pragma unroll
-                for (int q = 0; q < kSB; ++q) sv[q] = j0 + q < NC ? p.inv_sb[c_first + j0 + q] : 0.f;
+                for (int q = 0; q < kSB; ++q)
+                    sv[q] = j0 + q < NC ? p.inv_sb[c_first + j0 + q] : 0.f;
 #pragma unroll
                 for (int j = j0; j < j0 + kSB && j < NC; j += 4)
                     *reinterpret_cast<float4*>(orow + j) =
@@ -165,6 +167,19 @@ __device__ __forceinline__ uint64_t desc_sw64(const void* smem) {
     uint64_t d = 0;
     d |= (addr >> 4) & 0x3FFFull;
     d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+    return d;
+}
+
+// MN-major SWIZZLE_64B operand (fp16): atoms of 32 MN elements (64 B) x 8 K rows; the TMA boxes
+// are 32 MN x KC K (2 KB) side by side along MN (LBO = 2048 B), 8-row K groups 512 B apart (SBO)
+__device__ __forceinline__ uint64_t desc_mn_sw64(const void* smem) {
+    const uint64_t addr = ptx::smem_u32(smem);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= (uint64_t)(2048 >> 4) << 16;
     d |= (uint64_t)(512 >> 4) << 32;
     d |= (uint64_t)1 << 46;
     d |= (uint64_t)4 << 61;  // SWIZZLE_64B
@@ -359,6 +374,7 @@ __device__ __forceinline__ void mma_f16_pair_elect(uint32_t d_tmem, uint64_t ade
 #endif
 constexpr bool kConvPair = ENKS_F16P_CONV;
 
+template <bool BMN>  // B MN-major (p.b_mn): a separate instance, the K-major one is unchanged
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     f16p_gemm_pair_kernel(const __grid_constant__ CUtensorMap tAh,
                           const __grid_constant__ CUtensorMap tAl,
@@ -432,14 +448,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int kc = (c_lo + i) * KC;
                 ptx::tma_load_2d_pair(&tAh, &full[s], ah(s), kc, (int32_t)row0);
                 if (p.products == 3) ptx::tma_load_2d_pair(&tAl, &full[s], al(s), kc, (int32_t)row0);
-                ptx::tma_load_2d_pair(&tBh, &full[s], bh(s), kc, brow);
-                ptx::tma_load_2d_pair(&tBl, &full[s], bl(s), kc, brow);
+                if constexpr (BMN) {  // this CTA's 128 columns as four 32-column MN-major boxes
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        ptx::tma_load_2d_pair(&tBh, &full[s], bh(s) + q * 2048, brow + 32 * q, kc);
+                        ptx::tma_load_2d_pair(&tBl, &full[s], bl(s) + q * 2048, brow + 32 * q, kc);
+                    }
+                } else {
+                    ptx::tma_load_2d_pair(&tBh, &full[s], bh(s), kc, brow);
+                    ptx::tma_load_2d_pair(&tBl, &full[s], bl(s), kc, brow);
+                }
             }
           }
         }
     } else if (warp == 1) {
         if ((kConvPair || lane == 0) && rank == 0) {
-            constexpr uint32_t idesc = idesc_f16(2 * BM, 256);
+            constexpr uint32_t idesc = idesc_f16(2 * BM, 256) | (BMN ? (1u << 16) : 0u);  // B major
             auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
                 if constexpr (kConvPair) mma_f16_pair_elect(d, a, b, idesc, acc);
                 else mma_f16_pair(d, a, b, idesc, acc);
@@ -465,7 +489,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int k = 0; k < KC / 16; ++k) {
                     const uint64_t dah = desc_sw64(ah(s) + 32 * k), dal = desc_sw64(al(s) + 32 * k);
-                    const uint64_t dbh = desc_sw64(bh(s) + 32 * k), dbl = desc_sw64(bl(s) + 32 * k);
+                    // K-major: the K = 16 step is 32 B along the row; MN-major: 16 K rows (1 KB)
+                    const uint64_t dbh = BMN ? desc_mn_sw64(bh(s) + 1024 * k)
+                                             : desc_sw64(bh(s) + 32 * k);
+                    const uint64_t dbl = BMN ? desc_mn_sw64(bl(s) + 1024 * k)
+                                             : desc_sw64(bl(s) + 32 * k);
                     if (p.products == 3) {
                         mma(d, dal, dbh, (first && k == 0) ? 0u : 1u);
                         mma(d, dah, dbl, 1u);
@@ -521,14 +549,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // one block per row: scale = 2^e with max|x| * scale in [2^13, 2^14); h = fp16(xs), l = fp16(xs - h)
+// col_scale (optional): the row is split as src[r][k] * col_scale[k] (a per-column power of two
+// folded in first, e.g. the other operand's per-row scale of a reduction over k)
 __global__ void __launch_bounds__(256) f16pair_split_kernel(const float* __restrict__ src, int64_t ld,
                                                             int64_t K, __half* __restrict__ h,
                                                             __half* __restrict__ l, int64_t ldo,
-                                                            float* __restrict__ inv_scale) {
+                                                            float* __restrict__ inv_scale,
+                                                            const float* __restrict__ col_scale) {
     const int64_t r = blockIdx.x;
     const float* row = src + r * ld;
+    auto at = [&](int64_t k) { return col_scale ? row[k] * col_scale[k] : row[k]; };
     float mx = 0.f;
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(row[k]));
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) mx = fmaxf(mx, fabsf(at(k)));
     __shared__ float red[8];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -548,7 +580,7 @@ __global__ void __launch_bounds__(256) f16pair_split_kernel(const float* __restr
     __half* hr = h + r * ldo;
     __half* lr = l + r * ldo;
     for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
-        const float v = row[k] * s;
+        const float v = at(k) * s;
         const __half hv = __float2half_rn(v);
         hr[k] = hv;
         lr[k] = __float2half_rn(v - __half2float(hv));
@@ -674,6 +706,19 @@ bool map16(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int64_t ld
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// MN-major B ([K][N] with N contiguous): boxes of 32 N x KC K rows
+bool map16_mn(CUtensorMap* m, const void* base, int64_t krows, int64_t N, int64_t ld) {
+    EncodeTiledFn fn = encode16();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)krows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {32u, (cuuint32_t)KC};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BN>
 int launch16(const CUtensorMap* maps, P16 p, dim3 grid, cudaStream_t st) {
     using L = L16<BN>;
@@ -702,15 +747,21 @@ int launch_pair(const CUtensorMap* maps, P16 p, dim3 grid, cudaStream_t st) {
     const size_t smem = (size_t)stages * LP::kStage + 1024 + 512;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(f16p_gemm_pair_kernel,
+        cudaError_t e = cudaFuncSetAttribute(f16p_gemm_pair_kernel<false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(f16p_gemm_pair_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) {
             set_error("f16p pair gemm: smem attribute: %s", cudaGetErrorString(e));
             return ENKS_E_CUDA;
         }
         configured = true;
     }
-    f16p_gemm_pair_kernel<<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+    if (p.b_mn)
+        f16p_gemm_pair_kernel<true><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+    else
+        f16p_gemm_pair_kernel<false><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
     return check_launch("enks_gemm_f16pair(pair)");
 }
 
@@ -769,8 +820,18 @@ int enks_f16pair_split(const float* src, int64_t ld, int64_t rows, int64_t K, vo
     ENKS_REQUIRE(src && h && l && inv_scale, "enks_f16pair_split: null pointer");
     if (rows <= 0 || K <= 0) return ENKS_OK;
     enks::f16pair_split_kernel<<<(unsigned)rows, 256, 0, enks::as_stream(stream)>>>(
-        src, ld, K, static_cast<__half*>(h), static_cast<__half*>(l), ldo, inv_scale);
+        src, ld, K, static_cast<__half*>(h), static_cast<__half*>(l), ldo, inv_scale, nullptr);
     return enks::check_launch("enks_f16pair_split");
+}
+
+int enks_f16pair_split_cs(const float* src, int64_t ld, int64_t rows, int64_t K,
+                          const float* col_scale, void* h, void* l, int64_t ldo, float* inv_scale,
+                          void* stream) {
+    ENKS_REQUIRE(src && col_scale && h && l && inv_scale, "enks_f16pair_split_cs: null pointer");
+    if (rows <= 0 || K <= 0) return ENKS_OK;
+    enks::f16pair_split_kernel<<<(unsigned)rows, 256, 0, enks::as_stream(stream)>>>(
+        src, ld, K, static_cast<__half*>(h), static_cast<__half*>(l), ldo, inv_scale, col_scale);
+    return enks::check_launch("enks_f16pair_split_cs");
 }
 
 int enks_f16pair_recon(const void* h, const void* l, int64_t ldi, const float* inv_scale,
@@ -811,8 +872,10 @@ int f16p_split_for(int64_t M, int64_t N, int64_t K, bool fused) {
 int gemm_f16pair_impl(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah, const void* Al,
                       int64_t lda, const float* inv_sa, const void* Bh, const void* Bl, int64_t ldb,
                       const float* inv_sb, float* C, int64_t ldc, void* ws, void* stream,
-                      const Epi* epi) {
+                      const Epi* epi, bool b_mn = false) {
     ENKS_REQUIRE(Ah && Al && Bh && Bl && inv_sa && inv_sb && C, "enks_gemm_f16pair: null pointer");
+    ENKS_REQUIRE(!b_mn || (epi && use_pair(N) && (K % KC) == 0 && (N % 8) == 0),
+                 "enks_gemm_f16pair_ex_mn: needs N > 128, K %% 32 == 0, N %% 8 == 0");
     ENKS_REQUIRE(N >= 1 && K >= 1 && (lda % 8) == 0 && (ldb % 8) == 0,
                  "enks_gemm_f16pair: need 16-B aligned fp16 rows (ld %% 8 == 0)");
     ENKS_REQUIRE(N <= 256 || use_pair(N), "enks_gemm_f16pair: N > 256 needs the CTA-pair kernel");
@@ -821,9 +884,10 @@ int gemm_f16pair_impl(int64_t M, int64_t N, int64_t K, float alpha, const void* 
     const int BN = N <= 32 ? 32 : (N <= 64 ? 64 : (N <= 128 ? 128 : 256));
     const bool pair = use_pair(N);
     CUtensorMap maps[4];
-    if (!map16(&maps[0], Ah, M, K, lda, BM) || !map16(&maps[1], Al, M, K, lda, BM) ||
-        !map16(&maps[2], Bh, N, K, ldb, pair ? 128 : BN) ||
-        !map16(&maps[3], Bl, N, K, ldb, pair ? 128 : BN)) {
+    const bool bmaps = b_mn ? (map16_mn(&maps[2], Bh, K, N, ldb) && map16_mn(&maps[3], Bl, K, N, ldb))
+                            : (map16(&maps[2], Bh, N, K, ldb, pair ? 128 : BN) &&
+                               map16(&maps[3], Bl, N, K, ldb, pair ? 128 : BN));
+    if (!map16(&maps[0], Ah, M, K, lda, BM) || !map16(&maps[1], Al, M, K, lda, BM) || !bmaps) {
         set_error("enks_gemm_f16pair: cuTensorMapEncodeTiled failed (alignment?)");
         return ENKS_E_UNSUPPORTED;
     }
@@ -841,6 +905,7 @@ int gemm_f16pair_impl(int64_t M, int64_t N, int64_t K, float alpha, const void* 
     // leaks into this kernel)
     p.chain = env_knob("ENKS_F16P_CHAIN", kF16pChainDefault);
     p.products = debug_knob("ENKS_F16P_PRODUCTS", 3) == 2 ? 2 : 3;  // 2 breaks 1e-4
+    p.b_mn = b_mn ? 1 : 0;
     if (p.chain < 1) p.chain = 1;
     const bool direct = split == 1;
     p.out = direct ? C : static_cast<float*>(ws);
@@ -905,6 +970,16 @@ int enks_gemm_f16pair_ex(int64_t M, int64_t N, int64_t K, float alpha, const voi
     const enks::Epi epi{beta, C0, ldc0, bias, ld_bias, bias_cols};
     return enks::gemm_f16pair_impl(M, N, K, alpha, Ah, Al, lda, inv_sa, Bh, Bl, ldb, inv_sb, C, ldc,
                                    nullptr, stream, &epi);
+}
+
+int enks_gemm_f16pair_ex_mn(int64_t M, int64_t N, int64_t K, float alpha, const void* Ah,
+                            const void* Al, int64_t lda, const float* inv_sa, const void* Bh,
+                            const void* Bl, int64_t ldb, const float* inv_sn, float beta,
+                            const float* C0, int64_t ldc0, const float* bias, int64_t ld_bias,
+                            int bias_cols, float* C, int64_t ldc, void* stream) {
+    const enks::Epi epi{beta, C0, ldc0, bias, ld_bias, bias_cols};
+    return enks::gemm_f16pair_impl(M, N, K, alpha, Ah, Al, lda, inv_sa, Bh, Bl, ldb, inv_sn, C,
+                                   ldc, nullptr, stream, &epi, true);
 }
 
 int enks_f16pair_transpose(const void* h, const void* l, int64_t ldi, const float* inv_src,

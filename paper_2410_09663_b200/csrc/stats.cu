@@ -318,10 +318,13 @@ __global__ void __launch_bounds__(256) center_f16pair_t_kernel(
                 h[r * ldh + c] = hv;
                 l[r * ldh + c] = __float2half_rn(v - __half2float(hv));
             }
-            tile[r][tx] = a;
-            mx = fmaxf(mx, fabsf(a));
+            if (th) {
+                tile[r][tx] = a;
+                mx = fmaxf(mx, fabsf(a));
+            }
         }
     }
+    if (!th) return;  // no transposed planes (the shift reads Yc_tau MN-major)
     red[ty][tx] = mx;
     __syncthreads();
     if (ty == 0) {
@@ -565,10 +568,10 @@ int enks_member_center_f16pair_t(const float* src, int64_t ld_src, const float* 
                                  int64_t n_total, float* mean, void* h, void* l, int64_t ldh,
                                  float* inv_scale, float* scale_ws, void* th, void* tl, int64_t ldt,
                                  float* t_inv, void* stream) {
-    ENKS_REQUIRE(src && acc && amax && h && l && inv_scale && scale_ws && th && tl && t_inv &&
-                     n_total > 0,
+    ENKS_REQUIRE(src && acc && amax && h && l && inv_scale && scale_ws && n_total > 0 &&
+                     (!th) == (!tl) && (!th) == (!t_inv),
                  "enks_member_center_f16pair_t: bad arguments");
-    ENKS_REQUIRE(rows <= enks::kTMaxRows && ldt >= rows && ldt % 2 == 0,
+    ENKS_REQUIRE(rows <= enks::kTMaxRows && (!th || (ldt >= rows && ldt % 2 == 0)),
                  "enks_member_center_f16pair_t: rows > %d or bad ldt", enks::kTMaxRows);
     if (rows <= 0 || cols <= 0 || n_members <= 0) return ENKS_OK;
     cudaStream_t st = enks::as_stream(stream);

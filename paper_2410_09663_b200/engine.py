@@ -403,13 +403,19 @@ class DeviceSmoother:
         # from the basis rows; no fp32 copy of Yc_tau is kept
         self.shift_f16 = (self.pair and p <= 256 and p % 8 == 0 and m % 4 == 0
                           and hasattr(ops, "gemm_f16pair_ex"))
+        # ... reading the Yc_tau basis rows themselves as an MN-major B operand (no transposed
+        # planes: G_tt takes Yc_tau's per-row scale before its split); ENKS_SHIFT_MN=0: transposed
+        self.shift_mn = (self.shift_f16 and hasattr(ops, "gemm_f16pair_ex_mn") and p % 32 == 0
+                         and K % 8 == 0 and K > 128 and os.environ.get("ENKS_SHIFT_MN", "1") != "0")
         if self.pair:
             self.A_new = ops.empty(q, K)   # fp32 anomalies of the newest slice, [x; u] rows
             self.Yc_new = None if self.shift_f16 else ops.empty(p, K)  # fp32 centred obs
         if self.shift_f16:
             f16 = torch.float16
-            self.ycT_h, self.ycT_l, self.ycT_inv = (ops.empty(K, p, dtype=f16),
-                                                    ops.empty(K, p, dtype=f16), ops.empty(K))
+            self.ycT_h = self.ycT_l = self.ycT_inv = None
+            if not self.shift_mn:
+                self.ycT_h, self.ycT_l, self.ycT_inv = (ops.empty(K, p, dtype=f16),
+                                                        ops.empty(K, p, dtype=f16), ops.empty(K))
             self.gtt_h, self.gtt_l, self.gtt_inv = (ops.empty(q, p, dtype=f16),
                                                     ops.empty(q, p, dtype=f16), ops.empty(q))
         # the gain-side products (correction, gain, newest-slice shift) on tcgen05 as well
@@ -951,7 +957,13 @@ class DeviceSmoother:
             g_tt = self.G[tau * ds:tau * ds + q, (tau - 1) * p:tau * p]
         # newest slice [x; u] for the next forecast: mean + A_tau - G_{tau,tau} Yc_tau
         a_new = self.A_new if self.pair else self.Abuf[r0:r0 + d]  # (fp32 basis: ds == d)
-        if self.shift_f16:
+        if self.shift_mn:
+            yb = slice((tau - 1) * p, tau * p)
+            ops.f16pair_split_cs(g_tt, self.y_inv[yb], self.gtt_h, self.gtt_l, self.gtt_inv)
+            ops.gemm_f16pair_ex_mn(self.gtt_h, self.gtt_l, self.gtt_inv, self.Yh[yb], self.Yl[yb],
+                                   self.last, alpha=-1.0, beta=1.0, C0=a_new[:q],
+                                   bias=self.mean[r0:r0 + q], bias_cols=self.m, tag="shift")
+        elif self.shift_f16:
             yb = slice((tau - 1) * p, tau * p)
             ops.f16pair_split(g_tt, self.gtt_h, self.gtt_l, self.gtt_inv)
             if not fused_obs:  # (the fused centring wrote the transposed planes)

@@ -238,7 +238,7 @@ class DeviceOps:
             _lib.call("enks_member_center_f16pair_t", _p(src), _ld(src), _p(src2), _ld(src2), rows,
                       int(n_members), int(cols), _p(z0), _p(acc), _p(amax), int(n_total), _p(mean),
                       _p(h), _p(l), _ld(h), _p(inv_scale), _p(self._scale_ws), _p(th), _p(tl),
-                      _ld(th), _p(t_inv), self._stream())
+                      _ld(th) if th is not None else 0, _p(t_inv), self._stream())
 
     def member_center_f16pair(self, src, n_members, cols, z0, acc, amax, n_total, mean, h, l,
                               inv_scale, f32=None, rows_f32=0, skip=(0, 0)):
@@ -362,6 +362,20 @@ class DeviceOps:
         _lib.call("enks_f16pair_split", _p(src), _ld(src), src.shape[0], src.shape[1], _p(h), _p(l),
                   _ld(h), _p(inv_scale), self._stream())
 
+    def f16pair_split_cs(self, src, col_scale, h, l, inv_scale):
+        """f16pair_split of src * col_scale (per column) -- e.g. G_tt with Yc_tau's row scale."""
+        self.launches += 1
+        _lib.call("enks_f16pair_split_cs", _p(src), _ld(src), src.shape[0], src.shape[1],
+                  _p(col_scale), _p(h), _p(l), _ld(h), _p(inv_scale), self._stream())
+
+    def ones(self, n: int):
+        """A cached device vector of n ones (fp32)."""
+        o = getattr(self, "_ones", None)
+        if o is None or o.numel() < n:
+            self._retire(o)
+            self._ones = o = torch.ones(int(n), device=self.device)
+        return o[:n]
+
     def f16pair_recon(self, h, l, inv_scale, out):
         self.launches += 1
         _lib.call("enks_f16pair_recon", _p(h), _p(l), _ld(h), _p(inv_scale), out.shape[0],
@@ -408,6 +422,22 @@ class DeviceOps:
         with self._prof(tag, 2.0 * M * N * K) if tag else contextlib.nullcontext():
             _lib.call("enks_gemm_f16pair_ex", M, N, K, float(alpha), _p(Ah), _p(Al), _ld(Ah),
                       _p(inv_sa), _p(Bh), _p(Bl), _ld(Bh), _p(inv_sb), float(beta), _p(C0),
+                      _ld(C0) if C0 is not None else 0, _p(bias),
+                      _ld(bias) if bias is not None else 0, int(bias_cols), _p(C), _ld(C),
+                      self._stream())
+
+    def gemm_f16pair_ex_mn(self, Ah, Al, inv_sa, Bh, Bl, C, *, alpha=1.0, beta=0.0, C0=None,
+                           bias=None, bias_cols=0, tag=None):
+        """C = alpha A B + beta C0 + bias[:, c % bias_cols] with B given K x N (MN-major fp16
+        pairs, no per-row scale of B: fold it into A); N > 128."""
+        M, K = Ah.shape
+        N = Bh.shape[1]
+        if M == 0:
+            return
+        self.launches += 1
+        with self._prof(tag, 2.0 * M * N * K) if tag else contextlib.nullcontext():
+            _lib.call("enks_gemm_f16pair_ex_mn", M, N, K, float(alpha), _p(Ah), _p(Al), _ld(Ah),
+                      _p(inv_sa), _p(Bh), _p(Bl), _ld(Bh), _p(self.ones(N)), float(beta), _p(C0),
                       _ld(C0) if C0 is not None else 0, _p(bias),
                       _ld(bias) if bias is not None else 0, int(bias_cols), _p(C), _ld(C),
                       self._stream())

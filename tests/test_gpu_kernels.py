@@ -477,6 +477,30 @@ def test_gemm_f16pair_ex_shift_operands(dev_ops, p, q, K):
     assert ((out.double().cpu() - ref).abs() / scale).max().item() < 1e-6
 
 
+@pytest.mark.parametrize("p,q,K", [(256, 256, 4096 + 128), (256, 200, 1000), (128, 96, 776)])
+def test_gemm_f16pair_ex_mn_shift(dev_ops, p, q, K):
+    """Newest-slice shift with B = the Yc basis rows themselves (MN-major, K x N): G_tt takes Yc's
+    per-row scale before its split (enks_f16pair_split_cs), no transposed planes."""
+    g = torch.Generator().manual_seed(7 + q)
+    m = 128
+    Y = torch.randn(p, K, generator=g) * torch.logspace(-2, 2, p).unsqueeze(1)
+    G = torch.randn(q, p, generator=g) * 0.01
+    C0 = torch.randn(q, K, generator=g)
+    bias = torch.randn(q, m, generator=g)
+    f16 = torch.float16
+    yh, yl = dev_ops.empty(p, K, dtype=f16), dev_ops.empty(p, K, dtype=f16)
+    yi = dev_ops.empty(p)
+    dev_ops.f16pair_split(Y.to(dev_ops.device), yh, yl, yi)
+    gh, gl, gi = dev_ops.empty(q, p, dtype=f16), dev_ops.empty(q, p, dtype=f16), dev_ops.empty(q)
+    dev_ops.f16pair_split_cs(G.to(dev_ops.device), yi, gh, gl, gi)
+    out = dev_ops.zeros(q, K)
+    dev_ops.gemm_f16pair_ex_mn(gh, gl, gi, yh, yl, out, alpha=-1.0, beta=1.0,
+                               C0=C0.to(dev_ops.device), bias=bias.to(dev_ops.device), bias_cols=m)
+    ref = C0.double() + bias.double()[:, [k % m for k in range(K)]] - G.double() @ Y.double()
+    scale = (G.double().abs() @ Y.double().abs()) + C0.double().abs() + bias.double().abs().amax()
+    assert ((out.double().cpu() - ref).abs() / scale).max().item() < 1e-6
+
+
 @pytest.mark.parametrize("p", [289, 300, 512, 576])
 def test_spd_inverse_schur_blocks(dev_ops, p):
     """p > 288: 2 x 2 Schur complement of two one-CTA factorisations."""
