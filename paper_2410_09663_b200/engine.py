@@ -589,8 +589,8 @@ class DeviceSmoother:
                            if hasattr(ops, "set_sm_reserve") else 0)
         if self.fused_noise and getattr(self, "v_raw", None) is None:
             self.v_raw = ops.empty(self.q, self.K)  # raw [v_x; v_u] of the newest step
-        # observation never materialised: its centring forms [x; u] + [v_x; v_u] on the fly and
-        # also writes the transposed Yc_tau planes the newest-slice shift reads
+        # observation never materialised: its centring forms [x; u] + [v_x; v_u] on the fly (and,
+        # without the MN-major shift, writes the transposed Yc_tau planes the shift reads)
         self.obs_fused = (self.fused_noise and self.shift_f16 and self.barrier is None
                           and self.p == self.q and hasattr(ops, "member_center_f16pair_t")
                           and os.environ.get("ENKS_OBS_FUSED", "1") != "0")
@@ -741,7 +741,8 @@ class DeviceSmoother:
 
     def _center_obs_fused(self, tau) -> None:
         """Centre y = [x; u] + [v_x; v_u] (never materialised) into the basis rows of Yc_tau and
-        the transposed planes of the newest-slice shift; y_bar = member mean (enks.py:231-232).
+        (without the MN-major shift) the transposed planes of the newest-slice shift; y_bar = member
+        mean (enks.py:231-232).
         The member sums normally come from predict's collective (obs_sums)."""
         ops, p, m = self.ops, self.p, self.m
         src, src2 = self.slice_raw[:p], self.v_raw
