@@ -203,20 +203,31 @@ __global__ void center_f16pair_kernel(const float* __restrict__ src, int64_t ld,
 }
 
 // vectorised variant: 4 consecutive columns per thread (cols % 4 == 0, 16-B aligned rows)
+// src2 (optional): the centred quantity is src + src2, formed on the fly (the perturbed
+// observation [x; u] + [v_x; v_u]); the member-0 shift is then src + src2 of member 0 as well
 __global__ void center_f16pair_v4_kernel(const float* __restrict__ src, int64_t ld, int rows,
                                          int64_t n, int cols, const float* __restrict__ z0,
                                          const double* __restrict__ acc, double inv_n,
                                          float* __restrict__ mean, __half* __restrict__ h,
                                          __half* __restrict__ l, int64_t ldh,
                                          const float* __restrict__ scale, float* __restrict__ f32,
-                                         int64_t ldf, int rows_f32, int skip0, int skip1) {
+                                         int64_t ldf, int rows_f32, int skip0, int skip1,
+                                         const float* __restrict__ src2, int64_t ld2) {
     const int64_t K = n * cols;
     const int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
     const int64_t r = blockIdx.y;
     if (k >= K) return;
     const int j = (int)((uint32_t)k % (uint32_t)cols);
-    const float4 x = __ldg(reinterpret_cast<const float4*>(src + r * ld + k));
-    const float4 zz = __ldg(reinterpret_cast<const float4*>(z0 ? z0 + r * cols + j : src + r * ld + j));
+    float4 x = __ldg(reinterpret_cast<const float4*>(src + r * ld + k));
+    float4 zz = __ldg(reinterpret_cast<const float4*>(z0 ? z0 + r * cols + j : src + r * ld + j));
+    if (src2) {
+        const float4 x2 = __ldg(reinterpret_cast<const float4*>(src2 + r * ld2 + k));
+        x = make_float4(x.x + x2.x, x.y + x2.y, x.z + x2.z, x.w + x2.w);
+        if (!z0) {
+            const float4 z2 = __ldg(reinterpret_cast<const float4*>(src2 + r * ld2 + j));
+            zz = make_float4(zz.x + z2.x, zz.y + z2.y, zz.z + z2.z, zz.w + z2.w);
+        }
+    }
     const double2 a01 = __ldg(reinterpret_cast<const double2*>(acc + r * cols + j));
     const double2 a23 = __ldg(reinterpret_cast<const double2*>(acc + r * cols + j + 2));
     const float m0 = (float)(a01.x * inv_n), m1 = (float)(a01.y * inv_n);
@@ -553,7 +564,7 @@ int enks_member_center_f16pair(const float* src, int64_t ld_src, int rows, int64
         enks::center_f16pair_v4_kernel<<<dim3((unsigned)((K / 4 + 255) / 256), (unsigned)rows), 256,
                                          0, st>>>(
             src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
-            static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32, skip0, skip1);
+            static_cast<__half*>(l), ldh, scale_ws, f32, ld_f32, rows_f32, skip0, skip1, nullptr, 0);
     else
         enks::center_f16pair_kernel<<<dim3((unsigned)((K + 255) / 256), (unsigned)rows), 256, 0,
                                       st>>>(
@@ -581,6 +592,17 @@ int enks_member_center_f16pair_t(const float* src, int64_t ld_src, const float* 
     int rc = enks::check_launch("enks_member_center_f16pair_t(scale)");
     if (rc) return rc;
     const int64_t K = n_members * cols;
+    auto a16 = [](const void* ptr) { return ((uintptr_t)ptr & 15) == 0; };
+    if (!th && cols % 4 == 0 && ld_src % 4 == 0 && ldh % 4 == 0 && a16(src) &&
+        (!src2 || (a16(src2) && ld_src2 % 4 == 0)) && ((uintptr_t)h & 7) == 0 &&
+        ((uintptr_t)l & 7) == 0 && (!z0 || a16(z0)) && a16(acc) && (!mean || a16(mean))) {
+        // no transposed planes: the vectorised centring with the second source on the fly
+        enks::center_f16pair_v4_kernel<<<dim3((unsigned)((K / 4 + 255) / 256), (unsigned)rows), 256,
+                                         0, st>>>(
+            src, ld_src, rows, n_members, cols, z0, acc, inv_n, mean, static_cast<__half*>(h),
+            static_cast<__half*>(l), ldh, scale_ws, nullptr, 0, 0, rows, rows, src2, ld_src2);
+        return enks::check_launch("enks_member_center_f16pair_t(v4)");
+    }
     enks::center_f16pair_t_kernel<<<(unsigned)((K + 31) / 32), 256, 0, st>>>(
         src, ld_src, src2, ld_src2, rows, n_members, cols, z0, acc, inv_n, mean,
         static_cast<__half*>(h), static_cast<__half*>(l), ldh, scale_ws, static_cast<__half*>(th),
