@@ -71,10 +71,15 @@ struct SegRec {
 
 constexpr int kSegWarps = 4;
 
+// rec_x / rec_o: phase A records each group's emitted values (x per lane) and emit mask, so that
+// phase B of an exactly speculated chunk (entry carry 0: ~98.5 %) replays them -- no second
+// Philox / ziggurat pass (G groups per unit, unit = chunk-major ticket index).  The launch stays
+// latency-bound either way; the saved instructions are issue slots the concurrent forecast gets.
 __global__ void __launch_bounds__(kSegWarps * 32) noise_seg_kernel(const Args args, int n_jobs,
                                                                    int n_chunks, int G,
                                                                    SegRec* recs,
-                                                                   unsigned* ticket) {
+                                                                   unsigned* ticket,
+                                                                   double* rec_x, unsigned* rec_o) {
     __shared__ uint64_t s_ki[256];
     __shared__ double s_wi[256];
     __shared__ uint64_t s_buf[kSegWarps][kBufWords];
@@ -118,9 +123,20 @@ __global__ void __launch_bounds__(kSegWarps * 32) noise_seg_kernel(const Args ar
             int s = (int)(ww & 3);
             return s == 0 ? b.v0 : (s == 1 ? b.v1 : (s == 2 ? b.v2 : b.v3));
         };
+        double* ux = rec_x + t * (int64_t)G * 32;
+        unsigned* uo = rec_o + t * (int64_t)G;
+        auto emit1 = [&](long long q, double x) {
+            const int r = (int)(q / cols), jj = (int)(q - (long long)r * cols);
+            const double v = a.diag ? x * a.diag[r] : x;
+            const float f = (float)v;
+            if (a.out) a.out[r * a.ld_out + col0 + jj] = f;
+            if (a.out_plus)
+                a.out_plus[r * a.ld_plus + col0 + jj] = a.base[r * a.ld_base + col0 + jj] + f;
+        };
         // parse groups [g_begin, g_end) entering with `carry`; EMIT: write normals q0, q0 + 1, ...
-        // (< total); returns the count of normals started in the range, carry out in `carry`
-        auto parse = [&](bool emit, int& carry, long long q0) -> long long {
+        // (< total); RECORD: keep each group's x / emit mask for replay (not the last chunk);
+        // returns the count of normals started in the range, carry out in `carry`
+        auto parse = [&](bool emit, bool record, int& carry, long long q0) -> long long {
             long long cnt = 0;
             base_w = -(1 << 30);
             for (int g = g_begin; g < g_end; ++g) {
@@ -145,28 +161,37 @@ __global__ void __launch_bounds__(kSegWarps * 32) noise_seg_kernel(const Args ar
                 int next_carry;
                 resolve_group(raw, w, carry, lane, s_ki, s_wi, word, x, O, next_carry);
                 carry = next_carry;
+                if (record) {
+                    ux[(g - g_begin) * 32 + lane] = x;
+                    if (lane == 0) uo[g - g_begin] = O;
+                }
                 if (emit && ((O >> lane) & 1u)) {
                     const long long q = q0 + cnt + __popc(O & lt_mask);
-                    if (q < total) {
-                        const int r = (int)(q / cols), jj = (int)(q - (long long)r * cols);
-                        const double v = a.diag ? x * a.diag[r] : x;
-                        const float f = (float)v;
-                        if (a.out) a.out[r * a.ld_out + col0 + jj] = f;
-                        if (a.out_plus)
-                            a.out_plus[r * a.ld_plus + col0 + jj] = a.base[r * a.ld_base + col0 + jj] + f;
-                    }
+                    if (q < total) emit1(q, x);
                 }
                 cnt += __popc(O);
             }
             return cnt;
         };
+        // phase B from the records of phase A (this chunk's groups, entry carry 0)
+        auto replay = [&](long long q0) {
+            long long cnt = 0;
+            for (int g = g_begin; g < g_end; ++g) {
+                const unsigned O = uo[g - g_begin];
+                if ((O >> lane) & 1u) {
+                    const long long q = q0 + cnt + __popc(O & lt_mask);
+                    if (q < total) emit1(q, ux[(g - g_begin) * 32 + lane]);
+                }
+                cnt += __popc(O);
+            }
+        };
         int carry_in = 0;
         long long prefix = 0;
         long long cnt = 0;
         int carry_out = 0;
-        if (!last) {  // phase A (speculative entry carry 0)
+        if (!last) {  // phase A (speculative entry carry 0), recorded
             carry_out = 0;
-            cnt = parse(false, carry_out, 0);
+            cnt = parse(false, true, carry_out, 0);
         }
         if (c > 0) {  // predecessor's record
             const SegRec* pr = recs + (int64_t)(c - 1) * n_streams + sidx;
@@ -181,7 +206,7 @@ __global__ void __launch_bounds__(kSegWarps * 32) noise_seg_kernel(const Args ar
         if (!last) {
             if (carry_in != 0) {  // the entry differs from the speculation: recount
                 carry_out = carry_in;
-                cnt = parse(false, carry_out, 0);
+                cnt = parse(false, false, carry_out, 0);
             }
             SegRec* me = recs + (int64_t)c * n_streams + sidx;
             if (lane == 0) {
@@ -191,10 +216,16 @@ __global__ void __launch_bounds__(kSegWarps * 32) noise_seg_kernel(const Args ar
                 st_release(&me->flag, 1);
             }
         }
-        // phase B: emit this chunk's normals from index prefix
+        // phase B: emit this chunk's normals from index prefix -- replayed from phase A's records
+        // when the speculated entry was right, parsed again otherwise (and for the last chunk)
         if (prefix < total) {
-            int cb = carry_in;
-            parse(true, cb, prefix);
+            __syncwarp();  // phase A's records visible to every lane
+            if (!last && carry_in == 0) {
+                replay(prefix);
+            } else {
+                int cb = carry_in;
+                parse(true, false, cb, prefix);
+            }
         }
         __syncwarp();
     }
@@ -224,9 +255,16 @@ SegPlan seg_plan(int64_t n_streams, int64_t max_normals) {
     return P;
 }
 
+// workspace: [ticket (256 B) | records (zeroed per launch) | replay records x, emit masks]
+int64_t seg_rec_bytes(int64_t n_streams, const SegPlan& P) {
+    return ((int64_t)P.n_chunks * n_streams * (int64_t)sizeof(SegRec) + 256 + 255) / 256 * 256;
+}
 int64_t seg_ws_bytes(int64_t n_streams, int64_t max_normals) {
     const SegPlan P = seg_plan(n_streams, max_normals);
-    return P.n_chunks ? (int64_t)P.n_chunks * n_streams * (int64_t)sizeof(SegRec) + 256 : 0;
+    if (!P.n_chunks) return 0;
+    const int64_t groups = (int64_t)P.n_chunks * n_streams * P.G;
+    return seg_rec_bytes(n_streams, P) + groups * 32 * (int64_t)sizeof(double) +
+           groups * (int64_t)sizeof(unsigned);
 }
 
 int launch_noise(const uint32_t* head, int n_head, int64_t member0, int64_t n_members, int cols,
@@ -241,15 +279,18 @@ int launch_noise(const uint32_t* head, int n_head, int64_t member0, int64_t n_me
     const SegPlan P = seg_plan(n_streams, (int64_t)max_rows * cols);
     if (ws && P.n_chunks && env_knob("ENKS_NOISE_SEG", 1) != 0 &&
         ws_bytes >= seg_ws_bytes(n_streams, (int64_t)max_rows * cols)) {
-        // records + ticket, zeroed in stream order (capture-safe)
+        // records + ticket, zeroed in stream order (capture-safe); the replay records need no reset
         unsigned* ticket = static_cast<unsigned*>(ws);
         SegRec* recs = reinterpret_cast<SegRec*>(static_cast<char*>(ws) + 256);
-        cudaMemsetAsync(ws, 0, seg_ws_bytes(n_streams, (int64_t)max_rows * cols), st);
+        const int64_t rec_bytes = seg_rec_bytes(n_streams, P);
+        cudaMemsetAsync(ws, 0, rec_bytes, st);
         const int64_t units = n_streams * P.n_chunks;
+        double* rec_x = reinterpret_cast<double*>(static_cast<char*>(ws) + rec_bytes);
+        unsigned* rec_o = reinterpret_cast<unsigned*>(rec_x + units * P.G * 32);
         const int64_t want = (units + kSegWarps - 1) / kSegWarps;
         const int blocks = (int)(want < 16LL * kNumSMs ? want : 16LL * kNumSMs);
         noise_seg_kernel<<<blocks, kSegWarps * 32, 0, st>>>(L.args, n_jobs, P.n_chunks, P.G, recs,
-                                                            ticket);
+                                                            ticket, rec_x, rec_o);
         return check_launch("enks_noise_fill(segmented)");
     }
     int64_t blocks = (n_members + kWarps - 1) / kWarps;
