@@ -41,6 +41,10 @@ constexpr int KC = 32;               // fp16 elements per chunk row (64 B, SWIZZ
 constexpr int kF16pChainDefault = 16;
 constexpr int kThreads = 384;
 constexpr int kSmemBudget = 210 * 1024;
+// MN-major (shift) instance: epilogue staging, 32 rows x 32 columns (+1 pad) per epilogue warp
+constexpr int kStgFloats = 32 * 33;
+constexpr int kStgBytes = 8 * kStgFloats * 4;  // 33 KB
+constexpr int kMnStages = 4;                   // K = p <= a few hundred: a short ring suffices
 
 template <int BN>
 struct L16 {
@@ -538,8 +542,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         const int64_t r = row0 + erow;
         const int64_t c_first = col0 + (int64_t)wg * kCols;
-        if (r < p.M && c_first < p.N)
-            f16p_store_row(p, split, r, c_first, (int)min((int64_t)kCols, p.N - c_first), acc);
+        if constexpr (BMN) {
+            // wide row-major output (the newest-slice shift, N = N_members m): stage 32 x 32
+            // blocks through shared memory so every store / C0 / bias access is a 512 B row run
+            // of 4 rows per instruction instead of 32 rows x 16 B
+            const int64_t wr0 = row0 + ((warp & 3) << 5);
+            float* po = p.out + (int64_t)split * p.split_stride;
+            auto al16 = [](const void* q) { return (((uintptr_t)q) & 15) == 0; };
+            const bool staged =
+                wr0 + 32 <= p.M && c_first + kCols <= p.N && al16(po) && p.ldo % 4 == 0 &&
+                (!p.c0 || (al16(p.c0) && p.ldc0 % 4 == 0)) &&
+                (!p.bias || (al16(p.bias) && p.ld_bias % 4 == 0 && p.bias_cols % 4 == 0 &&
+                             (c_first % p.bias_cols) + kCols <= p.bias_cols));
+            if (staged) {
+                float* stg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512) +
+                             (warp - 4) * kStgFloats;
+                const float sa = p.alpha * p.inv_sa[r];
+                const int cc = (lane & 7) * 4, rsub = lane >> 3;
+                const int64_t bcol0 = p.bias ? c_first % p.bias_cols : 0;
+#pragma unroll
+                for (int c0 = 0; c0 < kCols; c0 += 32) {
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = acc[c0 + j] * sa;
+                    __syncwarp();
+                    const int64_t c = c_first + c0 + cc;
+                    const float4 sv = *reinterpret_cast<const float4*>(p.inv_sb + c);
+#pragma unroll
+                    for (int i0 = 0; i0 < 8; i0 += 4) {
+                        float4 cv[4], bv[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int64_t row = wr0 + (i0 + i) * 4 + rsub;
+                            cv[i] = p.c0 ? __ldg(reinterpret_cast<const float4*>(p.c0 + row * p.ldc0 + c))
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                            bv[i] = p.bias ? __ldg(reinterpret_cast<const float4*>(
+                                                 p.bias + row * p.ld_bias + bcol0 + c0 + cc))
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int rr = (i0 + i) * 4 + rsub;
+                            const float* sr = stg + rr * 33 + cc;
+                            float4 o;
+                            o.x = sr[0] * sv.x;
+                            o.y = sr[1] * sv.y;
+                            o.z = sr[2] * sv.z;
+                            o.w = sr[3] * sv.w;
+                            if (p.c0) {
+                                o.x += p.beta * cv[i].x; o.y += p.beta * cv[i].y;
+                                o.z += p.beta * cv[i].z; o.w += p.beta * cv[i].w;
+                            }
+                            if (p.bias) {
+                                o.x += bv[i].x; o.y += bv[i].y; o.z += bv[i].z; o.w += bv[i].w;
+                            }
+                            *reinterpret_cast<float4*>(po + (wr0 + rr) * p.ldo + c) = o;
+                        }
+                    }
+                }
+            } else if (r < p.M && c_first < p.N) {
+                f16p_store_row(p, split, r, c_first, (int)min((int64_t)kCols, p.N - c_first), acc);
+            }
+        } else {
+            if (r < p.M && c_first < p.N)
+                f16p_store_row(p, split, r, c_first, (int)min((int64_t)kCols, p.N - c_first), acc);
+        }
         }
     }
     ptx::tc_fence_before();
@@ -743,15 +810,18 @@ int launch16(const CUtensorMap* maps, P16 p, dim3 grid, cudaStream_t st) {
 int launch_pair(const CUtensorMap* maps, P16 p, dim3 grid, cudaStream_t st) {
     int stages = kSmemBudget / LP::kStage;
     if (stages > 8) stages = 8;
+    if (p.b_mn) stages = kMnStages;
     p.stages = stages;
-    const size_t smem = (size_t)stages * LP::kStage + 1024 + 512;
+    const size_t smem = (size_t)stages * LP::kStage + 1024 + 512 + (p.b_mn ? kStgBytes : 0);
     static bool configured = false;
     if (!configured) {
+        const size_t smem_k = (size_t)std::min(kSmemBudget / LP::kStage, 8) * LP::kStage + 1024 + 512;
+        const size_t smem_mn = (size_t)kMnStages * LP::kStage + 1024 + 512 + kStgBytes;
         cudaError_t e = cudaFuncSetAttribute(f16p_gemm_pair_kernel<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(f16p_gemm_pair_kernel<true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mn);
         if (e != cudaSuccess) {
             set_error("f16p pair gemm: smem attribute: %s", cudaGetErrorString(e));
             return ENKS_E_CUDA;
