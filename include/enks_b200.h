@@ -89,6 +89,15 @@ int enks_noise_fill_multi_dev(const uint32_t* head_dev, int n_head, int64_t memb
                               const int64_t* ld_base, float* const* out_plus,
                               const int64_t* ld_plus, void* ws, int64_t ws_bytes, void* stream);
 
+/* Both member sums of a predict in one pass (enks.py:171 slice mean, enks.py:194-200 + 231
+ * observation mean): acc/amax = sums of src's rows relative to the first member (z0 = NULL
+ * semantics of enks_member_sum), acc2/amax2 = the same for src + src2 over the first rows2 rows
+ * (rows2 <= rows); src's first rows2 rows are read once.  cols % 4 == 0, 16-byte aligned rows.
+ * ws: enks_member_sum2_ws_bytes(rows, rows2, n_members, cols) bytes of device memory. */
+int64_t enks_member_sum2_ws_bytes(int rows, int rows2, int64_t n_members, int cols);
+int enks_member_sum2(const float* src, int64_t ld_src, int rows, const float* src2,
+                     int64_t ld_src2, int rows2, int64_t n_members, int cols, double* acc,
+                     float* amax, double* acc2, float* amax2, void* ws, void* stream);
 /*
  * Member statistics (K4/K5).  Replaces members.mean(axis=0) (enks.py:171, 248),
  * obs.mean(axis=0) (enks.py:231) and the anomaly formation (enks.py:232-233).

@@ -46,6 +46,9 @@ _SIGS = {
                                            _c_i64, _vp]),
     "enks_noise_ws_bytes": (_c_i64, [_c_i64, _c_int, _c_int, _c_int]),
     "enks_member_sum_ws_bytes": (_c_i64, [_c_int, _c_i64, _c_int]),
+    "enks_member_sum2_ws_bytes": (_c_i64, [_c_int, _c_int, _c_i64, _c_int]),
+    "enks_member_sum2": (_c_int, [_vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _c_i64, _c_int, _vp, _vp,
+                                  _vp, _vp, _vp, _vp]),
     "enks_cnn_noise_fusable": (_c_int, [_c_int, _ip, _c_int, _c_int]),
     "enks_cnn_forward_noise": (_c_int, [_c_int, _ip, _vp, _vp, _c_f, _vp, _c_i64, _vp, _c_i64, _vp,
                                         _c_i64, _c_int, _c_int, _c_i64, _u32p, _vp, _c_int, _c_i64,

@@ -113,6 +113,88 @@ __global__ void __launch_bounds__(kSumThreads)
     *reinterpret_cast<float4*>(partmax + blockIdx.y * rc + e) = make_float4(mx[0], mx[1], mx[2], mx[3]);
 }
 
+// Both member sums of one predict in one pass (4 columns per thread): the slice sums of src (all
+// rows) and, for rows < rows2, the observation sums of src + src2 (the perturbed observation
+// x + v formed on the fly) -- src's first rows2 rows are read once instead of twice.  Shifts are
+// each quantity's first member (z0 = NULL semantics); per element the member order and the four
+// interleaved fp64 chains are those of the kernels above.
+__global__ void __launch_bounds__(kSumThreads)
+    member_partial2_v4_kernel(const float* __restrict__ src, int64_t ld, int rows,
+                              const float* __restrict__ src2, int64_t ld2, int rows2, int64_t n,
+                              int cols, double* __restrict__ part, float* __restrict__ partmax,
+                              double* __restrict__ part2, float* __restrict__ partmax2,
+                              int64_t chunk) {
+    const int64_t rc = (int64_t)rows * cols, rc2 = (int64_t)rows2 * cols;
+    const int64_t e = (blockIdx.x * (int64_t)kSumThreads + threadIdx.x) * 4;
+    if (e >= rc) return;
+    const int r = (int)(e / cols), j = (int)(e - (int64_t)r * cols);
+    const bool two = r < rows2;
+    const float* p = src + r * ld + j;
+    const float* p2 = two ? src2 + r * ld2 + j : nullptr;
+    auto ld4 = [](const float* q) { return __ldg(reinterpret_cast<const float4*>(q)); };
+    auto plus = [](float4 a, const float4& b) {
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        return a;
+    };
+    const float4 s = ld4(p);
+    const float4 s2 = two ? plus(s, ld4(p2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t i0 = blockIdx.y * chunk, i1 = min(n, i0 + chunk);
+    double acc[4][4] = {}, acc2[4][4] = {};
+    float mx[4] = {0.f, 0.f, 0.f, 0.f}, mx2[4] = {0.f, 0.f, 0.f, 0.f};
+    auto add = [](double (&a)[4][4], float (&m)[4], int c, const float4& v, const float4& z) {
+        const float d0 = v.x - z.x, d1 = v.y - z.y, d2 = v.z - z.z, d3 = v.w - z.w;
+        a[c][0] += (double)d0;
+        a[c][1] += (double)d1;
+        a[c][2] += (double)d2;
+        a[c][3] += (double)d3;
+        m[0] = fmaxf(m[0], fabsf(d0));
+        m[1] = fmaxf(m[1], fabsf(d1));
+        m[2] = fmaxf(m[2], fabsf(d2));
+        m[3] = fmaxf(m[3], fabsf(d3));
+    };
+    int64_t i = i0;
+    if (two) {
+        for (; i + 4 <= i1; i += 4) {
+            float4 v[4], w[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                v[c] = ld4(p + (i + c) * cols);
+                w[c] = ld4(p2 + (i + c) * cols);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                add(acc, mx, c, v[c], s);
+                add(acc2, mx2, c, plus(v[c], w[c]), s2);
+            }
+        }
+        for (; i < i1; ++i) {
+            const float4 v = ld4(p + i * cols);
+            add(acc, mx, 0, v, s);
+            add(acc2, mx2, 0, plus(v, ld4(p2 + i * cols)), s2);
+        }
+    } else {
+        for (; i + 4 <= i1; i += 4) {
+            float4 v[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = ld4(p + (i + c) * cols);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) add(acc, mx, c, v[c], s);
+        }
+        for (; i < i1; ++i) add(acc, mx, 0, ld4(p + i * cols), s);
+    }
+    auto store = [&](double* pp, float* pm, int64_t n_el, double (&a)[4][4], float (&m)[4]) {
+        double out[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[q] = (a[0][q] + a[1][q]) + (a[2][q] + a[3][q]);
+        double* po = pp + blockIdx.y * n_el + e;
+        reinterpret_cast<double2*>(po)[0] = make_double2(out[0], out[1]);
+        reinterpret_cast<double2*>(po)[1] = make_double2(out[2], out[3]);
+        *reinterpret_cast<float4*>(pm + blockIdx.y * n_el + e) = make_float4(m[0], m[1], m[2], m[3]);
+    };
+    store(part, partmax, rc, acc, mx);
+    if (two) store(part2, partmax2, rc2, acc2, mx2);
+}
+
 __global__ void chunk_reduce_kernel(const double* __restrict__ part, const float* __restrict__ pmax,
                                     int nchunks, int64_t rc, double* __restrict__ acc,
                                     float* __restrict__ amax) {
@@ -470,6 +552,50 @@ int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols) {
                                  enks::member_chunks(rows, n_members, cols, 4));
     return nch * (int64_t)rows * cols *
            (int64_t)(sizeof(double) + sizeof(float));
+}
+
+int64_t enks_member_sum2_ws_bytes(int rows, int rows2, int64_t n_members, int cols) {
+    const int64_t nch = enks::member_chunks(rows, n_members, cols, 4);
+    return nch * ((int64_t)rows + rows2) * cols * (int64_t)(sizeof(double) + sizeof(float));
+}
+
+int enks_member_sum2(const float* src, int64_t ld_src, int rows, const float* src2,
+                     int64_t ld_src2, int rows2, int64_t n_members, int cols, double* acc,
+                     float* amax, double* acc2, float* amax2, void* ws, void* stream) {
+    ENKS_REQUIRE(src && src2 && acc && acc2 && ws, "enks_member_sum2: null pointer");
+    ENKS_REQUIRE(rows2 >= 0 && rows2 <= rows, "enks_member_sum2: rows2 %d outside [0, %d]", rows2,
+                 rows);
+    auto a16 = [](const void* ptr) { return ((uintptr_t)ptr & 15) == 0; };
+    ENKS_REQUIRE(cols % 4 == 0 && ld_src % 4 == 0 && ld_src2 % 4 == 0 && a16(src) && a16(src2),
+                 "enks_member_sum2: needs cols %% 4 == 0 and 16-byte aligned rows");
+    if (rows <= 0 || cols <= 0) return ENKS_OK;
+    const int64_t rc = (int64_t)rows * cols, rc2 = (int64_t)rows2 * cols;
+    cudaStream_t st = enks::as_stream(stream);
+    if (n_members <= 0) {
+        cudaMemsetAsync(acc, 0, rc * sizeof(double), st);
+        if (amax) cudaMemsetAsync(amax, 0, rc * sizeof(float), st);
+        if (rc2) cudaMemsetAsync(acc2, 0, rc2 * sizeof(double), st);
+        if (rc2 && amax2) cudaMemsetAsync(amax2, 0, rc2 * sizeof(float), st);
+        return enks::check_launch("enks_member_sum2(memset)");
+    }
+    const int64_t nch = enks::member_chunks(rows, n_members, cols, 4);
+    const int64_t chunk = (n_members + nch - 1) / nch;
+    const int64_t nch_eff = (n_members + chunk - 1) / chunk;
+    double* part = static_cast<double*>(ws);
+    double* part2 = part + nch * rc;
+    float* pmax = reinterpret_cast<float*>(part2 + nch * rc2);
+    float* pmax2 = pmax + nch * rc;
+    dim3 grid((unsigned)((rc / 4 + enks::kSumThreads - 1) / enks::kSumThreads), (unsigned)nch_eff);
+    enks::member_partial2_v4_kernel<<<grid, enks::kSumThreads, 0, st>>>(
+        src, ld_src, rows, src2, ld_src2, rows2, n_members, cols, part, pmax, part2, pmax2, chunk);
+    int rc_ = enks::check_launch("enks_member_sum2(partial)");
+    if (rc_) return rc_;
+    enks::chunk_reduce_kernel<<<(unsigned)((rc + 255) / 256), 256, 0, st>>>(part, pmax, (int)nch_eff,
+                                                                           rc, acc, amax);
+    if (rc2)
+        enks::chunk_reduce_kernel<<<(unsigned)((rc2 + 255) / 256), 256, 0, st>>>(
+            part2, pmax2, (int)nch_eff, rc2, acc2, amax2);
+    return enks::check_launch("enks_member_sum2(reduce)");
 }
 
 int enks_member_sum_rebase(const float* src, int64_t ld_src, const float* src2, int64_t ld_src2,

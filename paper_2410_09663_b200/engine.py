@@ -360,6 +360,7 @@ class DeviceSmoother:
         self._pending = None  # deferred centring of the newest predicted slice (_finish_slice)
         self._last_stale = False  # `last` lags the newest slice (a predict with no update yet)
         self._basis = basis
+        self.sum2 = False  # set by bind()
         self._explicit = False  # explicit members (replace_members): no derived-U chain
         d, q, K = self.d, self.q, self.K
         self.slice_raw = ops.empty(d, K)      # [X; U; W] of the newest predicted slice
@@ -584,6 +585,8 @@ class DeviceSmoother:
                    and hasattr(ops, "cnn_forward_noise") and ops.cnn_noise_fusable(self.forecast, self.n))
         self.noise_in_forecast = (max(0, min(3, int(os.environ.get("ENKS_NOISE_IN_CNN", "0"))))
                                   if fusable else 0)
+        # predict's slice and observation member sums in one pass (ENKS_SUM2=0: two passes)
+        self.sum2 = hasattr(ops, "member_sum2") and os.environ.get("ENKS_SUM2", "1") != "0"
         # SMs the cross-moment grids leave to the concurrent side-stream gain solve (update())
         self.sm_reserve = (max(0, min(16, int(os.environ.get("ENKS_SM_RESERVE", "2"))))
                            if hasattr(ops, "set_sm_reserve") else 0)
@@ -704,11 +707,22 @@ class DeviceSmoother:
             self.amax = ops.zeros(rows, self.m)
         acc = self.acc[:rows]
         amax = None if pair_rows is None else self.amax[:rows]
-        self._local_sums(src, acc, amax)
+        p = self.p
+        if (obs_sums and self.sum2 and src.data_ptr() == self.slice_raw.data_ptr()
+                and amax is not None and self.m % 4 == 0):
+            # slice and observation sums in one pass over the slice (its [x; u] rows read once)
+            self.ops.member_sum2(src, p, self.v_raw, self.Nl, self.m, acc, amax, self.acc_obs,
+                                 self.amax_obs)
+            if self.comm.size > 1:
+                self.ops.member_sum_rebase(src, self.m, acc, float(self.Nl))
+                self.ops.member_sum_rebase(self.slice_raw[:p], self.m, self.acc_obs,
+                                           float(self.Nl), src2=self.v_raw)
+        else:
+            self._local_sums(src, acc, amax)
+            if obs_sums:
+                self._local_sums(self.slice_raw[:p], self.acc_obs, self.amax_obs, src2=self.v_raw)
         items = [(src, acc, None)]
         if obs_sums:
-            p = self.p
-            self._local_sums(self.slice_raw[:p], self.acc_obs, self.amax_obs, src2=self.v_raw)
             items.append((self.slice_raw[:p], self.acc_obs, self.v_raw))
             self._obs_sums_t = self.t + 1
         self._global_sums(items)

@@ -218,6 +218,17 @@ class DeviceOps:
                       _ld(src2) if src2 is not None else 0, rows, int(n_members), int(cols),
                       _p(z0), _p(acc), _p(amax), ws, self._stream())
 
+    def member_sum2(self, src, rows2, src2, n_members, cols, acc, amax, acc2, amax2):
+        """Slice sums of src and observation sums of src[:rows2] + src2 in one pass."""
+        rows = src.shape[0]
+        nbytes = self.lib.enks_member_sum2_ws_bytes(rows, int(rows2), int(n_members), int(cols))
+        ws = self._workspace_sum(nbytes)
+        self.launches += 3
+        with self._prof("stats", 4 * (rows + rows2) * n_members * cols):
+            _lib.call("enks_member_sum2", _p(src), _ld(src), rows, _p(src2), _ld(src2), int(rows2),
+                      int(n_members), int(cols), _p(acc), _p(amax), _p(acc2), _p(amax2), ws,
+                      self._stream())
+
     def member_sum_rebase(self, src, cols, acc, coef, src2=None):
         """acc += coef * (local member 0 of src (+ src2)): shifted <-> absolute member sums."""
         self.launches += 1

@@ -729,3 +729,28 @@ def test_cnn_forward_tcgen05_several_images_per_cta(dev_ops, pm, rows, N):
     Forecaster(model, dev_ops, rows, rows)(dev_ops, last, out, rows, N)
     got = _cpu(out).reshape(rows, N, 128).transpose(1, 0, 2)
     np.testing.assert_allclose(got, ref, rtol=1e-5, atol=2e-6)
+
+
+@pytest.mark.parametrize("rows,rows2,N,cols", [(384, 256, 1024, 128), (12, 8, 37, 8), (8, 0, 5, 4)])
+def test_member_sum2_matches_two_passes(dev_ops, rows, rows2, N, cols):
+    """One pass for the slice sums of src and the observation sums of src[:rows2] + src2 ==
+    the two enks_member_sum passes (same values to fp64 rounding; amax exact)."""
+    g = torch.Generator().manual_seed(rows + N)
+    src = (torch.randn(rows, N * cols, generator=g) * 3 + 1).to(dev_ops.device)
+    src2 = torch.randn(max(rows2, 1), N * cols, generator=g).to(dev_ops.device)
+    acc1 = torch.zeros(rows, cols, dtype=torch.float64, device=dev_ops.device)
+    amax1 = dev_ops.zeros(rows, cols)
+    acc2 = torch.zeros(max(rows2, 1), cols, dtype=torch.float64, device=dev_ops.device)
+    amax2 = dev_ops.zeros(max(rows2, 1), cols)
+    dev_ops.member_sum2(src, rows2, src2, N, cols, acc1, amax1, acc2, amax2)
+    r1 = torch.zeros_like(acc1)
+    m1 = torch.zeros_like(amax1)
+    dev_ops.member_sum(src, N, cols, None, r1, m1)
+    torch.testing.assert_close(acc1, r1, rtol=1e-12, atol=1e-9)
+    assert torch.equal(amax1, m1)
+    if rows2:
+        r2 = torch.zeros_like(acc2)
+        m2 = torch.zeros_like(amax2)
+        dev_ops.member_sum(src[:rows2], N, cols, None, r2, m2, src2=src2[:rows2])
+        torch.testing.assert_close(acc2, r2, rtol=1e-12, atol=1e-9)
+        assert torch.equal(amax2, m2)
