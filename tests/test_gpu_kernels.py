@@ -477,12 +477,14 @@ def test_gemm_f16pair_ex_shift_operands(dev_ops, p, q, K):
     assert ((out.double().cpu() - ref).abs() / scale).max().item() < 1e-6
 
 
-@pytest.mark.parametrize("p,q,K", [(256, 256, 4096 + 128), (256, 200, 1000), (128, 96, 776)])
-def test_gemm_f16pair_ex_mn_shift(dev_ops, p, q, K):
+@pytest.mark.parametrize("p,q,K,m", [(256, 256, 4096 + 128, 128), (256, 200, 1000, 128),
+                                     (128, 96, 776, 128), (256, 256, 96 * 40, 96)])
+def test_gemm_f16pair_ex_mn_shift(dev_ops, p, q, K, m):
     """Newest-slice shift with B = the Yc basis rows themselves (MN-major, K x N): G_tt takes Yc's
-    per-row scale before its split (enks_f16pair_split_cs), no transposed planes."""
-    g = torch.Generator().manual_seed(7 + q)
-    m = 128
+    per-row scale before its split (enks_f16pair_split_cs), no transposed planes.  The cases cover
+    the shared-memory-staged epilogue (full 32-row x 128-column blocks) and its row-per-thread
+    fallback (ragged rows / columns, bias period m = 96 not a multiple of the 128-column block)."""
+    g = torch.Generator().manual_seed(7 + q + m)
     Y = torch.randn(p, K, generator=g) * torch.logspace(-2, 2, p).unsqueeze(1)
     G = torch.randn(q, p, generator=g) * 0.01
     C0 = torch.randn(q, K, generator=g)
