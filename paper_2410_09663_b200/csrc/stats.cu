@@ -530,12 +530,15 @@ bool sum_scalar() {
     return env_knob("ENKS_SUM_SCALAR", 0) == 1;
 }
 
+// blocks per SM the one-pass member sums aim for (tuning; ENKS_SUM2_BPS, read once)
+int sum2_blocks_per_sm() { return env_knob("ENKS_SUM2_BPS", 8); }
+
 // per = columns per thread (4 for the vectorised partial kernel)
-int64_t member_chunks(int rows, int64_t n, int cols, int per) {
+int64_t member_chunks(int rows, int64_t n, int cols, int per, int per_sm = 8) {
     const int64_t rc = (int64_t)rows * cols;
     const int64_t blocks = (rc / per + kSumThreads - 1) / kSumThreads;
-    // aim for ~8 blocks per SM in flight
-    int64_t want = (8LL * kNumSMs + blocks - 1) / blocks;
+    // aim for ~per_sm blocks per SM in flight
+    int64_t want = ((int64_t)per_sm * kNumSMs + blocks - 1) / blocks;
     if (want > 64) want = 64;
     if (want > n) want = n;
     if (want < 1) want = 1;
@@ -555,7 +558,7 @@ int64_t enks_member_sum_ws_bytes(int rows, int64_t n_members, int cols) {
 }
 
 int64_t enks_member_sum2_ws_bytes(int rows, int rows2, int64_t n_members, int cols) {
-    const int64_t nch = enks::member_chunks(rows, n_members, cols, 4);
+    const int64_t nch = enks::member_chunks(rows, n_members, cols, 4, enks::sum2_blocks_per_sm());
     return nch * ((int64_t)rows + rows2) * cols * (int64_t)(sizeof(double) + sizeof(float));
 }
 
@@ -578,7 +581,7 @@ int enks_member_sum2(const float* src, int64_t ld_src, int rows, const float* sr
         if (rc2 && amax2) cudaMemsetAsync(amax2, 0, rc2 * sizeof(float), st);
         return enks::check_launch("enks_member_sum2(memset)");
     }
-    const int64_t nch = enks::member_chunks(rows, n_members, cols, 4);
+    const int64_t nch = enks::member_chunks(rows, n_members, cols, 4, enks::sum2_blocks_per_sm());
     const int64_t chunk = (n_members + nch - 1) / nch;
     const int64_t nch_eff = (n_members + chunk - 1) / chunk;
     double* part = static_cast<double*>(ws);
